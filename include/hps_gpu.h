@@ -1,0 +1,239 @@
+/* hps_gpu.h — C-ABI of the B200 sparse-embedding hot path (sm_100a only).
+ *
+ * This is the drop-in boundary. It replaces, for the embedding
+ * path, the reference's operator API pattern (proj/include/hps/kernels.hpp:33-66:
+ * free functions over raw pointers + counts, caller-owned buffers, no exceptions
+ * inside kernels, one backend chosen once) with ONE implementation: hand-written
+ * CUDA kernels for sm_100a. There is no vtable, no "scalar" backend and no CPU
+ * fallback: if no usable B200 is present every entry point returns
+ * HPS_GPU_E_NO_DEVICE.
+ *
+ * Conventions
+ *   - Every function returns int: 0 = OK, 1..17 = hps::ErrorCode values
+ *     (proj/include/hps/error.hpp:24-42), >= 256 = device failures.
+ *   - Pointer arguments are DEVICE pointers (stream-ordered on the handle's
+ *     stream) unless the parameter name ends in `_host`.
+ *   - Calls are asynchronous on the context's stream unless documented as
+ *     "syncs". Data errors found on the device (NaN/Inf on insert -> NonFinite,
+ *     row capacity exhausted -> Infeasible) are latched in a device status word
+ *     and reported by the next syncing call (hps_gpu_ctx_sync).
+ *   - Handles are externally synchronised: one thread/stream mutates a handle at a
+ *     time; different handles are independent.
+ *   - Hot calls (lookup_pooled, backward_update, cache_query, ...) never allocate,
+ *     never synchronise and are capturable into a CUDA graph.
+ *   - Keys are hps::EmbeddingKey (uint64, any value legal). Placement always uses
+ *     hps::key_hash / hps::partition_of (proj/include/hps/hash.hpp:42-54).
+ */
+#ifndef HPS_GPU_H_
+#define HPS_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_GPU_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------- */
+enum {
+  HPS_GPU_OK = 0,
+  /* 1..17 mirror hps::ErrorCode (proj/include/hps/error.hpp:24-42) */
+  HPS_GPU_E_INVALID_ARGUMENT = 1,
+  HPS_GPU_E_DIM_MISMATCH = 7,
+  HPS_GPU_E_DTYPE_MISMATCH = 8,
+  HPS_GPU_E_NON_FINITE = 10,
+  HPS_GPU_E_UNKNOWN_TABLE = 11,
+  HPS_GPU_E_BAD_SHARD = 13,
+  HPS_GPU_E_IO = 14,
+  HPS_GPU_E_INFEASIBLE = 16,
+  /* device failures */
+  HPS_GPU_E_CUDA = 256,
+  HPS_GPU_E_OUT_OF_MEMORY = 257,
+  HPS_GPU_E_NO_DEVICE = 258,
+  HPS_GPU_E_NOT_CAPTURABLE = 259
+};
+
+/* Human readable name of a status ("OK", "InvalidArgument", ..., "CudaError"). */
+const char* hps_gpu_status_string(int status);
+/* ABI version of the loaded library (HPS_GPU_ABI_VERSION it was built with). */
+int hps_gpu_abi_version(void);
+/* Last error message recorded on this thread (empty string if none). */
+const char* hps_gpu_last_error_message(void);
+
+/* ---- context: device + stream + device status word ------------------------- */
+typedef struct hps_gpu_ctx_s* hps_gpu_ctx;
+
+/* stream: a cudaStream_t (NULL = the legacy default stream). */
+int hps_gpu_ctx_create(int device, void* stream, hps_gpu_ctx* out_host);
+int hps_gpu_ctx_destroy(hps_gpu_ctx ctx);
+int hps_gpu_ctx_set_stream(hps_gpu_ctx ctx, void* stream);
+/* syncs: waits for the stream, returns and clears the latched device status. */
+int hps_gpu_ctx_sync(hps_gpu_ctx ctx);
+
+/* ---- K1: hashing / placement (proj/include/hps/hash.hpp:42-54) -------------- */
+int hps_gpu_key_hash(hps_gpu_ctx ctx, const uint64_t* keys, uint64_t n, uint64_t* hashes_out);
+/* out[i] = partition_of(keys[i], num_shards); num_shards == 0 -> InvalidArgument. */
+int hps_gpu_partition_of(hps_gpu_ctx ctx, const uint64_t* keys, uint64_t n,
+                         uint32_t num_shards, uint32_t* shard_out);
+/* flag_out[0] = 1 if any of v[0..n) is NaN/Inf else 0 (kernels.hpp:41-43 semantics). */
+int hps_gpu_has_non_finite_f32(hps_gpu_ctx ctx, const float* v, uint64_t n, uint32_t* flag_out);
+
+/* ---- embedding table group (K2..K5) ------------------------------------------
+ * A table group holds n_tables independent tables (key namespaces)
+ * of one dim, fp32 rows, plus one open-addressing key->row index per table and
+ * the optimizer state rows. A model has n_slots slots; slot s reads table
+ * slot_table[s]. A batch is n_samples x n_slots bags in sample-major order
+ * (bag = sample * n_slots + slot); bag b holds keys[offsets[b] .. offsets[b+1])
+ * (offsets == NULL: exactly one key per bag, keys[b]).                          */
+typedef struct hps_gpu_table_s* hps_gpu_table;
+
+enum { HPS_OPT_SGD = 0, HPS_OPT_ADAGRAD = 1, HPS_OPT_ADAM = 2 };
+enum { HPS_COMBINER_SUM = 0, HPS_COMBINER_MEAN = 1 };
+
+typedef struct {
+  uint32_t n_tables;
+  uint32_t dim;                     /* 1..4096, multiple of 4 */
+  const uint64_t* row_capacity_host;/* [n_tables] max rows per table */
+  uint32_t n_slots;
+  const uint32_t* slot_table_host;  /* [n_slots] table id of each slot */
+  int optimizer;                    /* HPS_OPT_* : sizes the state rows */
+  uint64_t max_batch_keys;          /* workspace sizing: keys per lookup call */
+  uint64_t max_batch_bags;          /* workspace sizing: bags per lookup call */
+  uint64_t init_seed;               /* row initialiser seed (see hps_gpu_init_value) */
+  float adagrad_initial_accumulator;/* AdaGrad a0 (state rows start at this) */
+} hps_table_config;
+
+typedef struct {
+  float lr;
+  float eps;
+  float beta1, beta2;               /* Adam */
+  float one_minus_beta1, one_minus_beta2;
+  float lr_t;                       /* Adam: lr*sqrt(1-b2^t)/(1-b1^t), computed by the caller in fp32 */
+} hps_opt_params;
+
+int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg_host, hps_gpu_table* out_host);
+int hps_gpu_table_destroy(hps_gpu_table tbl);
+/* Default vector of a table (host array of dim floats; all-zero when never set). */
+int hps_gpu_table_set_default_vector(hps_gpu_table tbl, uint32_t table, const float* vec_host);
+/* syncs: rows currently held by `table`. */
+int hps_gpu_table_size(hps_gpu_table tbl, uint32_t table, uint64_t* n_rows_host);
+
+/* Insert keys into `table`. New keys get row ids in order of first occurrence in
+ * keys[] (continuing from the table's row count); existing keys keep theirs.
+ * rows == NULL: new rows are initialised with hps_gpu_init_value(seed,key,j);
+ * otherwise rows[i*dim..] is the value of keys[i] (the first occurrence wins for a
+ * new key; existing rows are overwritten by the LAST occurrence). rows_out (may be
+ * NULL) receives the row id of every key. NaN/Inf in rows -> NonFinite (latched);
+ * more distinct keys than capacity -> Infeasible (latched). */
+int hps_gpu_table_insert(hps_gpu_table tbl, uint32_t table, const uint64_t* keys, uint64_t n,
+                         const float* rows, uint64_t* rows_out);
+/* rows_out[i] = row id of keys[i] in `table`, or UINT64_MAX when absent. */
+int hps_gpu_table_find(hps_gpu_table tbl, uint32_t table, const uint64_t* keys, uint64_t n,
+                       uint64_t* rows_out);
+/* Copy rows [row_begin, row_begin+n) of `table` (weights, and when state != NULL the
+ * optimizer state rows: state[k] for k < n_state_rows) out as fp32 [n x dim]. */
+int hps_gpu_table_export(hps_gpu_table tbl, uint32_t table, uint64_t row_begin, uint64_t n,
+                         float* weights_out, float* state0_out, float* state1_out);
+/* Key stored at each row (inverse of the index) for rows [row_begin, row_begin+n). */
+int hps_gpu_table_row_keys(hps_gpu_table tbl, uint32_t table, uint64_t row_begin, uint64_t n,
+                           uint64_t* keys_out);
+
+enum {
+  HPS_LOOKUP_KEYS_HOST = 1u << 0,  /* keys/offsets are pinned HOST memory: staged H2D inside the call */
+  HPS_LOOKUP_TRAIN = 1u << 1       /* remember per-key rows/bags for the following backward_update */
+};
+
+/* K1+K2+K3 fused: out[bag*dim + j] = combiner over the bag's rows, fp32, keys in bag
+ * order, from +0.0f; mean divides by the bag length (IEEE); an empty bag gives
+ * zeros; a key absent from its table contributes the table's default vector. */
+int hps_gpu_lookup_pooled(hps_gpu_table tbl, const uint64_t* keys, const uint32_t* offsets,
+                          uint32_t n_samples, int combiner, float* out, uint32_t flags);
+
+/* K4+K5: gradients of the last HPS_LOOKUP_TRAIN lookup. d_out is [n_bags x dim]; each
+ * key occurrence receives d_out[bag] (sum) or d_out[bag]/len (mean); occurrences of
+ * the same key are dedup'ed and reduced in canonical (occurrence) order with the
+ * blocked rule of DESIGN.md §4.3; the optimizer then updates each unique row in place.
+ * Absent keys (default-vector occurrences) receive no update. */
+int hps_gpu_backward_update(hps_gpu_table tbl, const float* d_out, const hps_opt_params* opt_host);
+
+/* After backward_update: number of unique rows updated (device u64 at *count_out),
+ * and optionally their row ids in ascending row order (unique_rows_out, capacity
+ * max_batch_keys). Used by the dedup parity tests. */
+int hps_gpu_table_last_unique(hps_gpu_table tbl, uint64_t* count_out, uint32_t* unique_rows_out);
+
+/* ---- HPS inference cache (K6..K8), SPEC.md:112-190 ---------------------------- */
+typedef struct hps_gpu_cache_s* hps_gpu_cache;
+
+typedef struct {
+  uint64_t capacity;        /* resident entries; capacity % ways == 0 */
+  uint32_t ways;            /* 1..32, default 8 */
+  uint64_t aging_interval;  /* accesses per set-aging epoch numerator; 0 -> 10*capacity */
+  uint32_t dim;
+  uint64_t max_batch;       /* workspace sizing: keys per call */
+} hps_cache_config;
+
+typedef struct {
+  uint64_t queries, hits, misses, insertions, admissions_rejected, refresh_replacements, evictions;
+} hps_cache_stats;
+
+int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg_host, hps_gpu_cache* out_host);
+int hps_gpu_cache_destroy(hps_gpu_cache cache);
+/* found_vecs: [n x dim] rows of the hits, compacted in input order; found_idx /
+ * missing_idx: input positions (uint32, ascending); counts[0] = n_found,
+ * counts[1] = n_missing (device u64). */
+int hps_gpu_cache_query(hps_gpu_cache cache, const uint64_t* keys, uint64_t n, float* found_vecs,
+                        uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts);
+/* SPEC.md:140-148. admitted_out: device u64 (may be NULL). NaN/Inf -> NonFinite (latched,
+ * the entry is skipped). */
+int hps_gpu_cache_insert(hps_gpu_cache cache, const uint64_t* keys, const float* vecs,
+                         const uint64_t* versions, uint64_t n, uint64_t* admitted_out);
+/* SPEC.md:149-157. replaced_out: device u64 (may be NULL). */
+int hps_gpu_cache_refresh(hps_gpu_cache cache, const uint64_t* keys, const float* vecs,
+                          const uint64_t* versions, uint64_t n, uint64_t* replaced_out);
+/* syncs. */
+int hps_gpu_cache_stats(hps_gpu_cache cache, hps_cache_stats* stats_host);
+int hps_gpu_cache_reset_stats(hps_gpu_cache cache);
+/* syncs: number of resident entries. */
+int hps_gpu_cache_size(hps_gpu_cache cache, uint64_t* n_host);
+
+/* ---- placement planners (host-side) ---------------------------- */
+enum { HPS_PLAN_LOCALIZED = 0, HPS_PLAN_DISTRIBUTED = 1, HPS_PLAN_HYBRID = 2 };
+
+typedef struct {
+  uint64_t vocab_size;  /* keys in the slot's table */
+  uint32_t dim;
+  uint32_t hotness;     /* max keys per sample */
+} hps_slot_spec;
+
+/* LPT over bytes (vocab*dim*4): slot_device_out[s] = owner. Infeasible if a slot fits nowhere. */
+int hps_plan_localized(const hps_slot_spec* slots_host, uint32_t n_slots, const uint64_t* budget_host,
+                       uint32_t n_devices, uint32_t* slot_device_out_host);
+/* Feasibility of key_hash-mod-G sharding (total/G <= min budget * 1.05). */
+int hps_plan_distributed(const hps_slot_spec* slots_host, uint32_t n_slots, const uint64_t* budget_host,
+                         uint32_t n_devices);
+/* Host evaluations of include/hps/hash.hpp (the same inline definitions the kernels use). */
+uint64_t hps_key_hash_host(uint64_t key);
+uint64_t hps_fastmod_u64_host(uint64_t a, uint64_t d);
+/* Host mirror of the distributed shard rule: out[i] = partition_of(keys[i], n_devices). */
+void hps_shard_of(const uint64_t* keys_host, uint64_t n, uint32_t n_devices, uint32_t* out_host);
+/* Hot set for hybrid placement: top floor(budget/(dim*4)) keys by (count desc, key asc). */
+int hps_plan_hybrid(const uint64_t* keys_host, const uint64_t* counts_host, uint64_t n_keys, uint32_t dim,
+                    uint64_t hot_budget_bytes, uint64_t* hot_keys_out_host, uint64_t* n_hot_out_host);
+/* All-to-all bytes per iteration (forward; backward is symmetric). p_cold: per-slot cold
+ * mass, required for HPS_PLAN_HYBRID. */
+int hps_estimate_comm(int strategy, uint64_t batch, const hps_slot_spec* slots_host, uint32_t n_slots,
+                      uint32_t n_devices, const double* p_cold_host, double* fwd_bytes_host, double* bwd_bytes_host);
+
+/* ---- synthetic workload helpers (device-side generators) ------- */
+/* The deterministic row initialiser of DESIGN.md §4.1 (host-callable, for checks). */
+float hps_gpu_init_value(uint64_t seed, uint64_t key, uint32_t j);
+/* out[i] = mix64(seed ^ (first + i)) : distinct keys (mix64 is a bijection). */
+int hps_gpu_gen_keys(hps_gpu_ctx ctx, uint64_t seed, uint64_t first, uint64_t n, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPS_GPU_H_ */

@@ -1,0 +1,273 @@
+"""Python host API over the C-ABI: device memory and streams come from torch.
+
+This is the harness-facing mirror of the boundary (include/hps_gpu.h). Every call
+goes straight to libhps_gpu.so; there is no CPU path. Keys travel as int64 tensors
+holding the uint64 bit pattern (hps::EmbeddingKey, any 64-bit value is legal).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+_OPT = {"sgd": L.OPT_SGD, "adagrad": L.OPT_ADAGRAD, "adam": L.OPT_ADAM}
+_COMB = {"sum": L.COMBINER_SUM, "mean": L.COMBINER_MEAN}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _need_cuda(t: torch.Tensor, name: str) -> None:
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+class Context:
+    """hps_gpu_ctx: a device, a stream and the latched device status word."""
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None):
+        self.lib = L.load()
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = C.c_void_p()
+        L.check(self.lib.hps_gpu_ctx_create(device, C.c_void_p(self.stream.cuda_stream), C.byref(h)), "ctx_create")
+        self.h = h
+
+    def set_stream(self, stream: torch.cuda.Stream) -> None:
+        self.stream = stream
+        L.check(self.lib.hps_gpu_ctx_set_stream(self.h, C.c_void_p(stream.cuda_stream)), "ctx_set_stream")
+
+    def sync(self) -> None:
+        """Wait for the stream; raise HpsError if a kernel latched an error."""
+        L.check(self.lib.hps_gpu_ctx_sync(self.h), "ctx_sync")
+
+    def status(self) -> int:
+        return self.lib.hps_gpu_ctx_sync(self.h)
+
+    def key_hash(self, keys: torch.Tensor) -> torch.Tensor:
+        _need_cuda(keys, "keys")
+        out = torch.empty_like(keys)
+        L.check(self.lib.hps_gpu_key_hash(self.h, _ptr(keys), keys.numel(), _ptr(out)), "key_hash")
+        return out
+
+    def partition_of(self, keys: torch.Tensor, num_shards: int) -> torch.Tensor:
+        _need_cuda(keys, "keys")
+        out = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
+        L.check(self.lib.hps_gpu_partition_of(self.h, _ptr(keys), keys.numel(), num_shards, _ptr(out)), "partition_of")
+        return out
+
+    def has_non_finite(self, x: torch.Tensor) -> bool:
+        _need_cuda(x, "x")
+        flag = torch.empty(1, dtype=torch.int32, device=x.device)
+        L.check(self.lib.hps_gpu_has_non_finite_f32(self.h, _ptr(x), x.numel(), _ptr(flag)), "has_non_finite")
+        return bool(flag.item())
+
+    def gen_keys(self, seed: int, first: int, n: int) -> torch.Tensor:
+        out = torch.empty(n, dtype=torch.int64, device=f"cuda:{self.device}")
+        L.check(self.lib.hps_gpu_gen_keys(self.h, seed, first, n, _ptr(out)), "gen_keys")
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.hps_gpu_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def opt_params(optimizer: str, lr: float, eps: float = 1e-8, beta1: float = 0.9, beta2: float = 0.999,
+               step: int = 1) -> L.OptParams:
+    """Optimizer constants as the kernels consume them (all fp32)."""
+    f = np.float32
+    p = L.OptParams()
+    p.lr, p.eps, p.beta1, p.beta2 = f(lr), f(eps), f(beta1), f(beta2)
+    p.one_minus_beta1 = f(f(1.0) - f(beta1))
+    p.one_minus_beta2 = f(f(1.0) - f(beta2))
+    if optimizer == "adam":
+        p.lr_t = f(lr * math.sqrt(1.0 - beta2 ** step) / (1.0 - beta1 ** step))
+    else:
+        p.lr_t = f(lr)
+    return p
+
+
+class EmbeddingTableGroup:
+    """hps_gpu_table: n_tables key namespaces of one dim, fp32 rows, one optimizer."""
+
+    def __init__(self, ctx: Context, row_capacity: Sequence[int], dim: int, slot_table: Sequence[int],
+                 optimizer: str = "sgd", max_batch_keys: int = 1 << 20, max_batch_bags: int = 1 << 20,
+                 init_seed: int = 0, adagrad_initial_accumulator: float = 0.0):
+        self.ctx, self.lib = ctx, ctx.lib
+        self.dim, self.optimizer = dim, optimizer
+        self.n_tables, self.n_slots = len(row_capacity), len(slot_table)
+        self.row_capacity = list(row_capacity)
+        self.row_base = [int(x) for x in np.concatenate([[0], np.cumsum(row_capacity)[:-1]])]
+        caps = (L.u64 * self.n_tables)(*row_capacity)
+        st = (L.u32 * self.n_slots)(*slot_table)
+        cfg = L.TableConfig(self.n_tables, dim, caps, self.n_slots, st, _OPT[optimizer], max_batch_keys,
+                            max_batch_bags, init_seed, adagrad_initial_accumulator)
+        h = C.c_void_p()
+        L.check(self.lib.hps_gpu_table_create(ctx.h, C.byref(cfg), C.byref(h)), "table_create")
+        self.h = h
+        self.device = torch.device(f"cuda:{ctx.device}")
+
+    def insert(self, table: int, keys: torch.Tensor, rows: Optional[torch.Tensor] = None) -> torch.Tensor:
+        _need_cuda(keys, "keys")
+        if rows is not None:
+            _need_cuda(rows, "rows")
+            if rows.dtype != torch.float32 or rows.numel() != keys.numel() * self.dim:
+                raise ValueError("rows must be float32 [n, dim]")
+        out = torch.empty(keys.numel(), dtype=torch.int64, device=self.device)
+        L.check(self.lib.hps_gpu_table_insert(self.h, table, _ptr(keys), keys.numel(), _ptr(rows), _ptr(out)),
+                "table_insert")
+        return out
+
+    def find(self, table: int, keys: torch.Tensor) -> torch.Tensor:
+        _need_cuda(keys, "keys")
+        out = torch.empty(keys.numel(), dtype=torch.int64, device=self.device)
+        L.check(self.lib.hps_gpu_table_find(self.h, table, _ptr(keys), keys.numel(), _ptr(out)), "table_find")
+        return out
+
+    def size(self, table: int) -> int:
+        n = C.c_uint64()
+        L.check(self.lib.hps_gpu_table_size(self.h, table, C.byref(n)), "table_size")
+        return n.value
+
+    def set_default_vector(self, table: int, vec) -> None:
+        v = np.ascontiguousarray(np.asarray(vec, dtype=np.float32).reshape(self.dim))
+        L.check(self.lib.hps_gpu_table_set_default_vector(self.h, table, v.ctypes.data_as(C.POINTER(C.c_float))),
+                "set_default_vector")
+
+    def export(self, table: int, begin: int, n: int):
+        w = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
+        s0 = torch.empty_like(w) if self.optimizer in ("adagrad", "adam") else None
+        s1 = torch.empty_like(w) if self.optimizer == "adam" else None
+        L.check(self.lib.hps_gpu_table_export(self.h, table, begin, n, _ptr(w), _ptr(s0), _ptr(s1)), "table_export")
+        return w, s0, s1
+
+    def row_keys(self, table: int, begin: int, n: int) -> torch.Tensor:
+        out = torch.empty(n, dtype=torch.int64, device=self.device)
+        L.check(self.lib.hps_gpu_table_row_keys(self.h, table, begin, n, _ptr(out)), "table_row_keys")
+        return out
+
+    def lookup(self, keys: torch.Tensor, n_samples: int, offsets: Optional[torch.Tensor] = None,
+               combiner: str = "sum", train: bool = False, out: Optional[torch.Tensor] = None,
+               keys_on_host: bool = False) -> torch.Tensor:
+        n_bags = n_samples * self.n_slots
+        if out is None:
+            out = torch.empty(n_bags, self.dim, dtype=torch.float32, device=self.device)
+        flags = (L.LOOKUP_TRAIN if train else 0) | (L.LOOKUP_KEYS_HOST if keys_on_host else 0)
+        if not keys_on_host:
+            _need_cuda(keys, "keys")
+            if offsets is not None:
+                _need_cuda(offsets, "offsets")
+        L.check(self.lib.hps_gpu_lookup_pooled(self.h, _ptr(keys), _ptr(offsets), n_samples, _COMB[combiner],
+                                               _ptr(out), flags), "lookup_pooled")
+        return out
+
+    def backward_update(self, d_out: torch.Tensor, lr: float, eps: float = 1e-8, beta1: float = 0.9,
+                        beta2: float = 0.999, step: int = 1, params: Optional[L.OptParams] = None) -> None:
+        _need_cuda(d_out, "d_out")
+        p = params if params is not None else opt_params(self.optimizer, lr, eps, beta1, beta2, step)
+        L.check(self.lib.hps_gpu_backward_update(self.h, _ptr(d_out), C.byref(p)), "backward_update")
+
+    def last_unique(self) -> torch.Tensor:
+        cnt = torch.zeros(1, dtype=torch.int64, device=self.device)
+        L.check(self.lib.hps_gpu_table_last_unique(self.h, _ptr(cnt), None), "last_unique(count)")
+        n = int(cnt.item())
+        rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        L.check(self.lib.hps_gpu_table_last_unique(self.h, _ptr(cnt), _ptr(rows)), "last_unique")
+        return rows[:n]
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.hps_gpu_table_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HotCache:
+    """hps_gpu_cache: the HPS set-associative GPU embedding cache."""
+
+    def __init__(self, ctx: Context, capacity: int, dim: int, ways: int = 8, aging_interval: int = 0,
+                 max_batch: int = 1 << 17):
+        self.ctx, self.lib, self.dim = ctx, ctx.lib, dim
+        self.device = torch.device(f"cuda:{ctx.device}")
+        cfg = L.CacheConfig(capacity, ways, aging_interval, dim, max_batch)
+        h = C.c_void_p()
+        L.check(self.lib.hps_gpu_cache_create(ctx.h, C.byref(cfg), C.byref(h)), "cache_create")
+        self.h = h
+        self.max_batch = max_batch
+        self._found_idx = torch.empty(max_batch, dtype=torch.int32, device=self.device)
+        self._missing_idx = torch.empty(max_batch, dtype=torch.int32, device=self.device)
+        self._counts = torch.zeros(2, dtype=torch.int64, device=self.device)
+
+    def query_async(self, keys: torch.Tensor, found_vecs: Optional[torch.Tensor] = None):
+        """Enqueue a query; returns (found_vecs, found_idx, missing_idx, counts) device tensors."""
+        _need_cuda(keys, "keys")
+        n = keys.numel()
+        if found_vecs is None:
+            found_vecs = torch.empty(max(n, 1), self.dim, dtype=torch.float32, device=self.device)
+        L.check(self.lib.hps_gpu_cache_query(self.h, _ptr(keys), n, _ptr(found_vecs), _ptr(self._found_idx),
+                                             _ptr(self._missing_idx), _ptr(self._counts)), "cache_query")
+        return found_vecs, self._found_idx, self._missing_idx, self._counts
+
+    def query(self, keys: torch.Tensor):
+        """(found_idx, found_vecs, missing_idx), input order preserved."""
+        fv, fi, mi, cnt = self.query_async(keys)
+        nf, nm = (int(x) for x in cnt.tolist())
+        return fi[:nf].clone(), fv[:nf].clone(), mi[:nm].clone()
+
+    def insert(self, keys: torch.Tensor, vecs: torch.Tensor, versions: torch.Tensor) -> int:
+        _need_cuda(keys, "keys")
+        out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        L.check(self.lib.hps_gpu_cache_insert(self.h, _ptr(keys), _ptr(vecs), _ptr(versions), keys.numel(), _ptr(out)),
+                "cache_insert")
+        return out
+
+    def refresh(self, keys: torch.Tensor, vecs: torch.Tensor, versions: torch.Tensor) -> torch.Tensor:
+        _need_cuda(keys, "keys")
+        out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        L.check(self.lib.hps_gpu_cache_refresh(self.h, _ptr(keys), _ptr(vecs), _ptr(versions), keys.numel(), _ptr(out)),
+                "cache_refresh")
+        return out
+
+    def stats(self) -> dict:
+        s = L.CacheStats()
+        L.check(self.lib.hps_gpu_cache_stats(self.h, C.byref(s)), "cache_stats")
+        return {k: getattr(s, k) for k, _ in L.CacheStats._fields_}
+
+    def reset_stats(self) -> None:
+        L.check(self.lib.hps_gpu_cache_reset_stats(self.h), "cache_reset_stats")
+
+    def size(self) -> int:
+        n = C.c_uint64()
+        L.check(self.lib.hps_gpu_cache_size(self.h, C.byref(n)), "cache_size")
+        return n.value
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.hps_gpu_cache_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

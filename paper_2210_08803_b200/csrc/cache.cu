@@ -1,0 +1,677 @@
+// cache.cu — HPS GPU embedding cache (K6 query, K7 insert/evict, K8 refresh).
+//
+// Semantics: SPEC.md:112-190 (set-associative LFU with aging and last-touch tie-break)
+// with the resolutions of DESIGN.md §5, restated on the CPU in oracle/oracle.cpp
+// (Cache). Placement: set = key_hash(key) mod num_sets (hash.hpp:42-49),
+// computed with an exact 128-bit-magic modulo.
+//
+// Batch-parallel with exact sequential semantics:
+//   * a query batch never changes residency, so every hit/miss is decided in parallel
+//     against the state before the batch (K6a); found/missing are compacted in input
+//     order by a decoupled look-back scan; hits are gathered with 128-bit loads;
+//   * the metadata side effects (freq, last_touch, aging) depend on per-set ORDER only,
+//     so accesses are stably radix-sorted by set and one warp per touched set replays
+//     them 32 at a time in closed form (saturating adds between aging points);
+//   * insert/refresh are sequential per set (eviction depends on the previous insert),
+//     so the same sort feeds one warp per set that walks its entries in input order,
+//     lanes = ways.
+// HBM layout (set-major): keys/versions/last_touch [sets x ways] u64,
+// freq [sets x ways] u8 (0 = empty way), vectors [sets x ways x dim] fp32.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "primitives.cuh"
+
+using namespace hpsg;
+
+struct hps_gpu_cache_s {
+  hps_gpu_ctx ctx = nullptr;
+  uint64_t capacity = 0, num_sets = 0, aging_period = 0, max_batch = 0;
+  uint32_t ways = 0, dim = 0;
+  hps::FastMod64 set_mod;
+  int set_bits = 0;
+  uint64_t *d_keys = nullptr, *d_ver = nullptr, *d_touch = nullptr, *d_set_acc = nullptr;
+  uint8_t* d_freq = nullptr;
+  float* d_vec = nullptr;
+  uint64_t* d_state = nullptr;  // [0]=clock [1]=clock snapshot of the running call [2..8]=stats [9]=scratch count
+  // workspaces
+  uint32_t *ws_set = nullptr, *ws_keys_b = nullptr, *ws_vals_a = nullptr, *ws_vals_b = nullptr;
+  uint8_t* ws_hit = nullptr;
+  uint32_t* ws_rank = nullptr;
+  uint32_t* ws_seg = nullptr;
+  uint32_t* ws_sort = nullptr;
+  uint64_t* ws_scan = nullptr;
+  uint64_t* ws_counts = nullptr;  // [0]=n [1]=U (segments) [2]=found [3]=valid
+  size_t sort_words = 0;
+};
+
+namespace {
+
+constexpr uint8_t kMiss = 0xff;
+
+enum { kClock = 0, kSnap = 1, kStats = 2, kScratch = 9 };
+enum { sQueries = 0, sHits, sMisses, sInsertions, sRejected, sRefresh, sEvictions };
+
+int bits_for(uint64_t v) {
+  int b = 0;
+  while (b < 64 && (v >> b)) ++b;
+  return b;
+}
+
+// ---- K6a: probe every query against the pre-batch state --------------------------
+__global__ void k_probe(const uint64_t* __restrict__ keys, uint64_t n, hps::FastMod64 fm, uint32_t ways,
+                        const uint64_t* __restrict__ ckeys, const uint8_t* __restrict__ cfreq,
+                        uint32_t* __restrict__ set_out, uint8_t* __restrict__ hit_out, uint64_t* state,
+                        uint64_t* counts) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state[kSnap] = state[kClock];
+    state[kClock] += n;
+    counts[0] = n;
+  }
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t k = keys[i];
+    const uint64_t s = fm.mod(hps::key_hash(k));
+    const uint64_t* kr = ckeys + s * ways;
+    const uint8_t* fr = cfreq + s * ways;
+    uint8_t hit = kMiss;
+    for (uint32_t w = 0; w < ways; ++w) {
+      if (fr[w] != 0 && kr[w] == k) {
+        hit = static_cast<uint8_t>(w);
+        break;
+      }
+    }
+    set_out[i] = static_cast<uint32_t>(s);
+    hit_out[i] = hit;
+  }
+}
+
+// ---- K6b: order-preserving found/missing split --------------------------------------
+struct SplitOp {
+  const uint8_t* hit;
+  uint32_t* found_idx;
+  uint32_t* missing_idx;
+  uint64_t* counts_out;  // caller's [found, missing]
+  uint64_t* counts;      // internal [.., .., found]
+  uint64_t* stats;
+  __device__ uint64_t size() const { return counts[0]; }
+  __device__ uint32_t count(uint64_t i) const { return hit[i] != kMiss ? 1u : 0u; }
+  __device__ void emit(uint64_t i, uint64_t excl, uint32_t c) const {
+    if (c) {
+      found_idx[excl] = static_cast<uint32_t>(i);
+    } else {
+      missing_idx[i - excl] = static_cast<uint32_t>(i);
+    }
+  }
+  __device__ void total(uint64_t f) const {
+    const uint64_t n = counts[0];
+    counts[2] = f;
+    counts_out[0] = f;
+    counts_out[1] = n - f;
+    stats[sQueries] += n;
+    stats[sHits] += f;
+    stats[sMisses] += n - f;
+  }
+};
+
+// ---- K6c: gather hit rows (LPR lanes per row, 128-bit loads) ------------------------
+template <int LPR>
+__global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ found_idx, const uint64_t* counts,
+                                                const uint32_t* __restrict__ set_of, const uint8_t* __restrict__ hit,
+                                                uint32_t ways, const float* __restrict__ vec, uint32_t dim,
+                                                float* __restrict__ out) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
+  const uint64_t nf = counts[2];
+  const uint32_t nvec = dim / 4;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t j = gid; j < nf; j += ng) {
+    const uint32_t i = found_idx[j];
+    const uint64_t e = uint64_t(set_of[i]) * ways + hit[i];
+    const float4* src = reinterpret_cast<const float4*>(vec + e * dim);
+    float4* dst = reinterpret_cast<float4*>(out + j * dim);
+    for (uint32_t v = gl; v < nvec; v += LPR) dst[v] = __ldg(src + v);
+  }
+}
+
+// ---- segments of a set-sorted access list -------------------------------------------
+struct SetSegOp {
+  const uint32_t* sets_sorted;
+  uint32_t* seg_start;
+  uint64_t* counts;  // [0]=n [1]=U
+  __device__ uint64_t size() const { return counts[0]; }
+  __device__ uint32_t count(uint64_t i) const {
+    return (i == 0 || sets_sorted[i] != sets_sorted[i - 1]) ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t i, uint64_t excl, uint32_t c) const {
+    if (c) seg_start[excl] = static_cast<uint32_t>(i);
+  }
+  __device__ void total(uint64_t u) const {
+    counts[1] = u;
+    seg_start[u] = static_cast<uint32_t>(counts[0]);
+  }
+};
+
+__device__ __forceinline__ uint32_t sat_add_freq(uint32_t f, uint32_t x) {
+  return f == 0 ? 0u : min(255u, f + x);
+}
+__device__ __forceinline__ uint32_t age_freq(uint32_t f) { return f == 0 ? 0u : max(1u, f >> 1); }
+
+// ---- K6d: replay the batch's metadata effects, one warp per touched set --------------
+__global__ void __launch_bounds__(256) k_query_meta(const uint32_t* __restrict__ sets_sorted,
+                                                    const uint32_t* __restrict__ idx_sorted,
+                                                    const uint32_t* __restrict__ seg_start, const uint64_t* counts,
+                                                    const uint8_t* __restrict__ hit, uint32_t ways,
+                                                    uint64_t aging_period, uint8_t* __restrict__ cfreq,
+                                                    uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
+                                                    const uint64_t* state) {
+  const uint32_t lane = lane_id();
+  const uint64_t U = counts[1];
+  const uint64_t clock0 = state[kSnap];
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t u = warp; u < U; u += n_warps) {
+    const uint32_t lo = seg_start[u], hi = seg_start[u + 1];
+    const uint64_t s = sets_sorted[lo];
+    uint32_t f = lane < ways ? cfreq[s * ways + lane] : 0u;
+    uint64_t touch = lane < ways ? ctouch[s * ways + lane] : 0ull;
+    uint64_t acc = set_acc[s];
+    for (uint32_t c = lo; c < hi; c += 32) {
+      const uint32_t j = c + lane;
+      const bool valid = j < hi;
+      const uint32_t i = valid ? idx_sorted[j] : 0u;
+      const uint32_t hw = valid ? hit[i] : kMiss;
+      const uint32_t cnt = min(32u, hi - c);
+      const bool fire = valid && ((acc + lane + 1) % aging_period == 0);
+      const uint32_t F = __ballot_sync(0xffffffffu, fire);
+      uint32_t H = 0;
+      for (uint32_t w = 0; w < ways; ++w) {
+        const uint32_t m = __ballot_sync(0xffffffffu, hw == w);
+        if (lane == w) H = m;
+      }
+      // closed form for this lane's way: saturating adds between aging points
+      uint32_t prev = 0, Fm = F;
+      while (Fm) {
+        const uint32_t b = __ffs(Fm) - 1;
+        Fm &= Fm - 1;
+        const uint32_t seg = H & (((b >= 32) ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << prev) - 1u));
+        f = age_freq(sat_add_freq(f, __popc(seg)));
+        prev = b;
+      }
+      const uint32_t tailmask = (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)) & ~((prev >= 32) ? 0xffffffffu : ((1u << prev) - 1u));
+      f = sat_add_freq(f, __popc(H & tailmask));
+      const uint32_t lastp = H ? 31u - __clz(H) : 0u;
+      const uint32_t ilast = __shfl_sync(0xffffffffu, i, lastp);
+      if (H) touch = clock0 + ilast + 1;
+      acc = (acc + cnt) % aging_period;
+    }
+    if (lane < ways) {
+      cfreq[s * ways + lane] = static_cast<uint8_t>(f);
+      ctouch[s * ways + lane] = touch;
+    }
+    if (lane == 0) set_acc[s] = acc;
+  }
+}
+
+// ---- K7/K8 prep: validate rows (NaN/Inf -> NonFinite), set id, validity -------------
+template <int LPR>
+__global__ void __launch_bounds__(256) k_entry_prep(const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
+                                                    uint64_t n, uint32_t dim, hps::FastMod64 fm, uint32_t invalid_set,
+                                                    uint32_t* __restrict__ set_out, uint8_t* __restrict__ valid_out,
+                                                    uint32_t* status, uint64_t* counts) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
+  const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
+  const uint32_t nvec = dim / 4;
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = n;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t i = gid; i < n; i += ng) {
+    const uint4* v = reinterpret_cast<const uint4*>(vecs + i * dim);
+    bool bad = false;
+    for (uint32_t q = gl; q < nvec; q += LPR) {
+      const uint4 x = __ldg(v + q);
+      bad |= non_finite_bits(x.x) | non_finite_bits(x.y) | non_finite_bits(x.z) | non_finite_bits(x.w);
+    }
+    bad = __any_sync(gmask, bad);
+    if (gl == 0) {
+      if (bad) latch_status(status, HPS_GPU_E_NON_FINITE);
+      set_out[i] = bad ? invalid_set : static_cast<uint32_t>(fm.mod(hps::key_hash(keys[i])));
+      valid_out[i] = bad ? 0 : 1;
+    }
+  }
+}
+
+// rank among valid entries (the access clock of an insert), and the clock reservation
+struct RankOp {
+  const uint8_t* valid;
+  uint32_t* rank;
+  uint64_t* counts;
+  uint64_t* state;
+  __device__ uint64_t size() const { return counts[0]; }
+  __device__ uint32_t count(uint64_t i) const { return valid[i]; }
+  __device__ void emit(uint64_t i, uint64_t excl, uint32_t) const { rank[i] = static_cast<uint32_t>(excl); }
+  __device__ void total(uint64_t nv) const {
+    counts[3] = nv;
+    state[kSnap] = state[kClock];
+    state[kClock] += nv;
+  }
+};
+
+__device__ __forceinline__ void warp_copy_row(float* dst, const float* src, uint32_t dim) {
+  const uint32_t nvec = dim / 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (uint32_t q = lane_id(); q < nvec; q += 32) d4[q] = __ldg(s4 + q);
+}
+
+// ---- K7: insert, one warp per touched set, entries in input order --------------------
+__global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict__ sets_sorted,
+                                                     const uint32_t* __restrict__ idx_sorted,
+                                                     const uint32_t* __restrict__ seg_start, const uint64_t* counts,
+                                                     const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
+                                                     const uint64_t* __restrict__ versions,
+                                                     const uint32_t* __restrict__ rank, uint32_t ways, uint32_t dim,
+                                                     uint64_t aging_period, uint32_t invalid_set, uint64_t* ckeys,
+                                                     uint64_t* cver, uint8_t* cfreq, uint64_t* ctouch, uint64_t* set_acc,
+                                                     float* cvec, uint64_t* state, uint64_t* admitted_out) {
+  const uint32_t lane = lane_id();
+  const uint64_t U = counts[1];
+  const uint64_t clock0 = state[kSnap];
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  uint64_t n_ins = 0, n_evict = 0, n_refresh = 0;
+  for (uint64_t u = warp; u < U; u += n_warps) {
+    const uint32_t lo = seg_start[u], hi = seg_start[u + 1];
+    const uint32_t s32 = sets_sorted[lo];
+    if (s32 == invalid_set) continue;
+    const uint64_t s = s32, e0 = s * ways;
+    const bool way = lane < ways;
+    uint64_t k_w = way ? ckeys[e0 + lane] : 0, v_w = way ? cver[e0 + lane] : 0, t_w = way ? ctouch[e0 + lane] : 0;
+    uint32_t f_w = way ? cfreq[e0 + lane] : 0;
+    uint64_t acc = set_acc[s];
+    for (uint32_t j = lo; j < hi; ++j) {
+      const uint32_t i = idx_sorted[j];
+      const uint64_t k = keys[i], ver = versions[i];
+      const uint64_t t = clock0 + rank[i] + 1;
+      if (++acc >= aging_period) {
+        acc = 0;
+        f_w = age_freq(f_w);
+      }
+      const uint32_t res = __ballot_sync(0xffffffffu, way && f_w != 0 && k_w == k);
+      if (res) {  // resident: refresh semantics (version-gated replace, no freq/touch change)
+        const int w = __ffs(res) - 1;
+        const uint64_t vw = __shfl_sync(0xffffffffu, v_w, w);
+        if (ver > vw) {
+          warp_copy_row(cvec + (e0 + w) * dim, vecs + uint64_t(i) * dim, dim);
+          if (lane == static_cast<uint32_t>(w)) v_w = ver;
+          ++n_refresh;
+        }
+        continue;
+      }
+      const uint32_t free_ways = __ballot_sync(0xffffffffu, way && f_w == 0);
+      int w;
+      if (free_ways) {
+        w = __ffs(free_ways) - 1;
+      } else {  // victim = min (freq, last_touch)
+        uint32_t bf = way ? f_w : 0xffffffffu;
+        uint64_t bt = way ? t_w : ~0ull;
+        uint32_t bl = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint32_t of = __shfl_xor_sync(0xffffffffu, bf, o);
+          const uint64_t ot = __shfl_xor_sync(0xffffffffu, bt, o);
+          const uint32_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+          if (of < bf || (of == bf && (ot < bt || (ot == bt && ol < bl)))) {
+            bf = of;
+            bt = ot;
+            bl = ol;
+          }
+        }
+        w = static_cast<int>(bl);
+        ++n_evict;
+      }
+      if (lane == static_cast<uint32_t>(w)) {
+        k_w = k;
+        v_w = ver;
+        f_w = 1;
+        t_w = t;
+      }
+      warp_copy_row(cvec + (e0 + w) * dim, vecs + uint64_t(i) * dim, dim);
+      ++n_ins;
+    }
+    if (way) {
+      ckeys[e0 + lane] = k_w;
+      cver[e0 + lane] = v_w;
+      cfreq[e0 + lane] = static_cast<uint8_t>(f_w);
+      ctouch[e0 + lane] = t_w;
+    }
+    if (lane == 0) set_acc[s] = acc;
+  }
+  if (lane == 0 && (n_ins | n_evict | n_refresh)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sInsertions]), n_ins);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sEvictions]), n_evict);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sRefresh]), n_refresh);
+    if (admitted_out) atomicAdd(reinterpret_cast<unsigned long long*>(admitted_out), n_ins);
+  }
+}
+
+// ---- K8: refresh, one warp per touched set ------------------------------------------
+__global__ void __launch_bounds__(256) k_refresh_sets(const uint32_t* __restrict__ sets_sorted,
+                                                      const uint32_t* __restrict__ idx_sorted,
+                                                      const uint32_t* __restrict__ seg_start, const uint64_t* counts,
+                                                      const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
+                                                      const uint64_t* __restrict__ versions, uint32_t ways,
+                                                      uint32_t dim, uint32_t invalid_set, const uint64_t* ckeys,
+                                                      uint64_t* cver, const uint8_t* cfreq, float* cvec,
+                                                      uint64_t* state, uint64_t* replaced_out) {
+  const uint32_t lane = lane_id();
+  const uint64_t U = counts[1];
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  uint64_t n_rep = 0;
+  for (uint64_t u = warp; u < U; u += n_warps) {
+    const uint32_t lo = seg_start[u], hi = seg_start[u + 1];
+    const uint32_t s32 = sets_sorted[lo];
+    if (s32 == invalid_set) continue;
+    const uint64_t e0 = uint64_t(s32) * ways;
+    const bool way = lane < ways;
+    const uint64_t k_w = way ? ckeys[e0 + lane] : 0;
+    const uint32_t f_w = way ? cfreq[e0 + lane] : 0;
+    uint64_t v_w = way ? cver[e0 + lane] : 0;
+    for (uint32_t j = lo; j < hi; ++j) {
+      const uint32_t i = idx_sorted[j];
+      const uint64_t k = keys[i], ver = versions[i];
+      const uint32_t res = __ballot_sync(0xffffffffu, way && f_w != 0 && k_w == k);
+      if (!res) continue;
+      const int w = __ffs(res) - 1;
+      const uint64_t vw = __shfl_sync(0xffffffffu, v_w, w);
+      if (ver > vw) {
+        warp_copy_row(cvec + (e0 + w) * dim, vecs + uint64_t(i) * dim, dim);
+        if (lane == static_cast<uint32_t>(w)) v_w = ver;
+        ++n_rep;
+      }
+    }
+    if (way) cver[e0 + lane] = v_w;
+  }
+  if (lane == 0 && n_rep) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sRefresh]), n_rep);
+    if (replaced_out) atomicAdd(reinterpret_cast<unsigned long long*>(replaced_out), n_rep);
+  }
+}
+
+__global__ void k_count_resident(const uint8_t* __restrict__ freq, uint64_t n, unsigned long long* out) {
+  uint64_t c = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    c += freq[i] != 0;
+  c = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(c));
+  if (lane_id() == 0 && c) atomicAdd(out, static_cast<unsigned long long>(c));
+}
+
+template <typename T>
+int dalloc(T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return HPS_GPU_OK;
+  if (cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    set_last_error("cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+    return HPS_GPU_E_OUT_OF_MEMORY;
+  }
+  return HPS_GPU_OK;
+}
+
+int check_cache(hps_gpu_cache c) {
+  if (!c) {
+    set_last_error("null cache handle");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  return HPS_GPU_OK;
+}
+
+int lpr_for(uint32_t dim) {
+  const uint32_t nvec = dim / 4;
+  return nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
+}
+
+// Stable sort of (set id, input index) + set segments. Sizes come from c->ws_counts[0].
+int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** sets_sorted,
+                     const uint32_t** idx_sorted) {
+  cudaStream_t st = c->ctx->stream;
+  cudaError_t err;
+  const bool in_b = radix_sort_pairs(st, c->ws_set, nullptr, c->ws_vals_a, c->ws_keys_b, c->ws_vals_b, c->ws_counts,
+                                     n, bits, c->ws_sort, &err);
+  if (err != cudaSuccess) return cuda_status(err, "cache radix sort");
+  *sets_sorted = in_b ? c->ws_keys_b : c->ws_set;
+  *idx_sorted = in_b ? c->ws_vals_b : c->ws_vals_a;
+  const uint64_t tiles = scan_tiles(n);
+  HPSG_CUDA(cudaMemsetAsync(c->ws_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
+  SetSegOp op{*sets_sorted, c->ws_seg, c->ws_counts};
+  k_scan<SetSegOp><<<static_cast<unsigned>(std::max<uint64_t>(1, tiles)), kScanBlock, 0, st>>>(
+      op, c->ws_scan, reinterpret_cast<uint32_t*>(c->ws_scan + tiles));
+  HPSG_CHECK_LAUNCH("set segments");
+  return HPS_GPU_OK;
+}
+
+int set_warps_grid(uint64_t n) { return grid_for(n * 32, 256, kNumSMs * 16); }
+
+}  // namespace
+
+extern "C" {
+
+int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_cache* out) {
+  if (!ctx || !cfg || !out) return HPS_GPU_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  const uint32_t ways = cfg->ways ? cfg->ways : 8;
+  if (ways > 32 || cfg->capacity < ways || cfg->capacity % ways != 0 || cfg->dim == 0 || cfg->dim % 4 != 0 ||
+      cfg->dim > 4096 || cfg->max_batch == 0 || cfg->max_batch >= (1ull << 31)) {
+    set_last_error("cache config: need 1<=ways<=32, capacity % ways == 0, dim % 4 == 0, 1<=max_batch<2^31");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (cfg->capacity / ways >= 0xffffffffull) return HPS_GPU_E_INVALID_ARGUMENT;
+  HPSG_CUDA(cudaSetDevice(ctx->device));
+  auto c = new hps_gpu_cache_s;
+  c->ctx = ctx;
+  c->capacity = cfg->capacity;
+  c->ways = ways;
+  c->dim = cfg->dim;
+  c->num_sets = cfg->capacity / ways;
+  const uint64_t interval = cfg->aging_interval ? cfg->aging_interval : 10 * cfg->capacity;
+  c->aging_period = std::max<uint64_t>(1, interval / c->num_sets);
+  c->max_batch = cfg->max_batch;
+  c->set_mod = hps::FastMod64(c->num_sets);
+  c->set_bits = std::max(1, bits_for(c->num_sets));  // ids 0..num_sets (num_sets = invalid marker)
+  const uint64_t cap = c->capacity, n = c->max_batch;
+  int st = HPS_GPU_OK;
+  auto A = [&](int s) {
+    if (s && !st) st = s;
+  };
+  A(dalloc(&c->d_keys, cap));
+  A(dalloc(&c->d_ver, cap));
+  A(dalloc(&c->d_touch, cap));
+  A(dalloc(&c->d_freq, cap));
+  A(dalloc(&c->d_set_acc, c->num_sets));
+  A(dalloc(&c->d_vec, cap * c->dim));
+  A(dalloc(&c->d_state, 16));
+  A(dalloc(&c->ws_set, n));
+  A(dalloc(&c->ws_keys_b, n));
+  A(dalloc(&c->ws_vals_a, n));
+  A(dalloc(&c->ws_vals_b, n));
+  A(dalloc(&c->ws_hit, n));
+  A(dalloc(&c->ws_rank, n));
+  A(dalloc(&c->ws_seg, n + 2));
+  c->sort_words = sort_ws_words(n, (c->set_bits + 7) / 8);
+  A(dalloc(&c->ws_sort, c->sort_words));
+  A(dalloc(&c->ws_scan, scan_tiles(n) + 2));
+  A(dalloc(&c->ws_counts, 8));
+  if (st) {
+    hps_gpu_cache_destroy(c);
+    return st;
+  }
+  cudaStream_t s = ctx->stream;
+  HPSG_CUDA(cudaMemsetAsync(c->d_freq, 0, cap, s));
+  HPSG_CUDA(cudaMemsetAsync(c->d_keys, 0, cap * 8, s));
+  HPSG_CUDA(cudaMemsetAsync(c->d_ver, 0, cap * 8, s));
+  HPSG_CUDA(cudaMemsetAsync(c->d_touch, 0, cap * 8, s));
+  HPSG_CUDA(cudaMemsetAsync(c->d_set_acc, 0, c->num_sets * 8, s));
+  HPSG_CUDA(cudaMemsetAsync(c->d_vec, 0, cap * c->dim * sizeof(float), s));
+  HPSG_CUDA(cudaMemsetAsync(c->d_state, 0, 16 * 8, s));
+  HPSG_CUDA(cudaMemsetAsync(c->ws_counts, 0, 8 * 8, s));
+  HPSG_CUDA(cudaStreamSynchronize(s));
+  *out = c;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_destroy(hps_gpu_cache c) {
+  if (!c) return HPS_GPU_OK;
+  void* ptrs[] = {c->d_keys,    c->d_ver,    c->d_touch,   c->d_freq, c->d_set_acc, c->d_vec,
+                  c->d_state,   c->ws_set,   c->ws_keys_b, c->ws_vals_a, c->ws_vals_b, c->ws_hit,
+                  c->ws_rank,   c->ws_seg,   c->ws_sort,   c->ws_scan, c->ws_counts};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete c;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float* found_vecs, uint32_t* found_idx,
+                        uint32_t* missing_idx, uint64_t* counts) {
+  if (int s = check_cache(c)) return s;
+  if (!found_idx || !missing_idx || !counts) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = c->ctx->stream;
+  if (n == 0) {
+    HPSG_CUDA(cudaMemsetAsync(counts, 0, 2 * sizeof(uint64_t), st));
+    return HPS_GPU_OK;
+  }
+  if (!keys) return HPS_GPU_E_INVALID_ARGUMENT;
+  k_probe<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(keys, n, c->set_mod, c->ways, c->d_keys, c->d_freq,
+                                                          c->ws_set, c->ws_hit, c->d_state, c->ws_counts);
+  const uint64_t tiles = scan_tiles(n);
+  HPSG_CUDA(cudaMemsetAsync(c->ws_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
+  SplitOp op{c->ws_hit, found_idx, missing_idx, counts, c->ws_counts, c->d_state + kStats};
+  k_scan<SplitOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(op, c->ws_scan,
+                                                                       reinterpret_cast<uint32_t*>(c->ws_scan + tiles));
+  HPSG_CHECK_LAUNCH("cache probe/split");
+  if (found_vecs) {
+    const int lpr = lpr_for(c->dim);
+    const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
+#define HPSG_G(L) k_gather<L><<<grid, 256, 0, st>>>(found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec, c->dim, found_vecs)
+    switch (lpr) {
+      case 32: HPSG_G(32); break;
+      case 16: HPSG_G(16); break;
+      case 8: HPSG_G(8); break;
+      case 4: HPSG_G(4); break;
+      case 2: HPSG_G(2); break;
+      default: HPSG_G(1); break;
+    }
+#undef HPSG_G
+    HPSG_CHECK_LAUNCH("cache gather");
+  }
+  const uint32_t* sets_sorted;
+  const uint32_t* idx_sorted;
+  if (int s = sort_and_segment(c, n, c->set_bits, &sets_sorted, &idx_sorted)) return s;
+  k_query_meta<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, c->ws_hit, c->ways,
+                                                  c->aging_period, c->d_freq, c->d_touch, c->d_set_acc, c->d_state);
+  HPSG_CHECK_LAUNCH("cache meta");
+  return HPS_GPU_OK;
+}
+
+static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n) {
+  cudaStream_t st = c->ctx->stream;
+  const int lpr = lpr_for(c->dim);
+  const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
+  const uint32_t invalid = static_cast<uint32_t>(c->num_sets);
+#define HPSG_P(L) k_entry_prep<L><<<grid, 256, 0, st>>>(keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts)
+  switch (lpr) {
+    case 32: HPSG_P(32); break;
+    case 16: HPSG_P(16); break;
+    case 8: HPSG_P(8); break;
+    case 4: HPSG_P(4); break;
+    case 2: HPSG_P(2); break;
+    default: HPSG_P(1); break;
+  }
+#undef HPSG_P
+  HPSG_CHECK_LAUNCH("cache entry prep");
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_insert(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions, uint64_t n,
+                         uint64_t* admitted_out) {
+  if (int s = check_cache(c)) return s;
+  if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = c->ctx->stream;
+  if (admitted_out) HPSG_CUDA(cudaMemsetAsync(admitted_out, 0, sizeof(uint64_t), st));
+  if (n == 0) return HPS_GPU_OK;
+  if (!keys || !vecs || !versions) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (int s = entry_prep(c, keys, vecs, n)) return s;
+  const uint64_t tiles = scan_tiles(n);
+  HPSG_CUDA(cudaMemsetAsync(c->ws_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
+  RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
+  k_scan<RankOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(rop, c->ws_scan,
+                                                                      reinterpret_cast<uint32_t*>(c->ws_scan + tiles));
+  const uint32_t* sets_sorted;
+  const uint32_t* idx_sorted;
+  if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
+  k_insert_sets<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs,
+                                                   versions, c->ws_rank, c->ways, c->dim, c->aging_period,
+                                                   static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq,
+                                                   c->d_touch, c->d_set_acc, c->d_vec, c->d_state, admitted_out);
+  HPSG_CHECK_LAUNCH("cache insert");
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions,
+                          uint64_t n, uint64_t* replaced_out) {
+  if (int s = check_cache(c)) return s;
+  if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = c->ctx->stream;
+  if (replaced_out) HPSG_CUDA(cudaMemsetAsync(replaced_out, 0, sizeof(uint64_t), st));
+  if (n == 0) return HPS_GPU_OK;
+  if (!keys || !vecs || !versions) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (int s = entry_prep(c, keys, vecs, n)) return s;
+  const uint32_t* sets_sorted;
+  const uint32_t* idx_sorted;
+  if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
+  k_refresh_sets<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs,
+                                                    versions, c->ways, c->dim, static_cast<uint32_t>(c->num_sets),
+                                                    c->d_keys, c->d_ver, c->d_freq, c->d_vec, c->d_state, replaced_out);
+  HPSG_CHECK_LAUNCH("cache refresh");
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_stats(hps_gpu_cache c, hps_cache_stats* out) {
+  if (int s = check_cache(c)) return s;
+  if (!out) return HPS_GPU_E_INVALID_ARGUMENT;
+  uint64_t h[7];
+  HPSG_CUDA(cudaMemcpyAsync(h, c->d_state + kStats, sizeof(h), cudaMemcpyDeviceToHost, c->ctx->stream));
+  HPSG_CUDA(cudaStreamSynchronize(c->ctx->stream));
+  out->queries = h[sQueries];
+  out->hits = h[sHits];
+  out->misses = h[sMisses];
+  out->insertions = h[sInsertions];
+  out->admissions_rejected = h[sRejected];
+  out->refresh_replacements = h[sRefresh];
+  out->evictions = h[sEvictions];
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_reset_stats(hps_gpu_cache c) {
+  if (int s = check_cache(c)) return s;
+  HPSG_CUDA(cudaMemsetAsync(c->d_state + kStats, 0, 7 * sizeof(uint64_t), c->ctx->stream));
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_size(hps_gpu_cache c, uint64_t* n_host) {
+  if (int s = check_cache(c)) return s;
+  if (!n_host) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = c->ctx->stream;
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(c->d_state + kScratch);
+  HPSG_CUDA(cudaMemsetAsync(d, 0, 8, st));
+  k_count_resident<<<grid_for(c->capacity, 256, kNumSMs * 8), 256, 0, st>>>(c->d_freq, c->capacity, d);
+  HPSG_CHECK_LAUNCH("k_count_resident");
+  HPSG_CUDA(cudaMemcpyAsync(n_host, d, 8, cudaMemcpyDeviceToHost, st));
+  HPSG_CUDA(cudaStreamSynchronize(st));
+  return HPS_GPU_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// common.cuh — shared device helpers for the sm_100a sparse-embedding kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include <hps/hash.hpp>
+#include "hps_gpu.h"
+
+namespace hpsg {
+
+constexpr uint32_t kRowEmpty = 0xffffffffu;    // index slot not in use
+constexpr uint32_t kRowPending = 0xfffffffeu;  // slot claimed by an in-flight insert
+constexpr uint32_t kAuxNone = 0xffffffffu;     // slot.aux outside of an insert call
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;
+
+// One open-addressing index slot: 16 B, one aligned vector access.
+struct __align__(16) Slot {
+  uint64_t key;
+  uint32_t row;  // local row id within its table, or kRowEmpty / kRowPending
+  uint32_t aux;  // insert-time scratch: min occurrence index of this key in the call
+};
+
+// Per-table placement inside a table group (device-resident array).
+struct TableDev {
+  uint64_t slot_base;  // first slot of this table's index
+  uint64_t slot_mask;  // index capacity - 1 (power of two)
+  uint64_t row_base;   // first global row of this table
+  uint64_t row_cap;    // max rows
+};
+
+// Latched device status word: first error wins.
+__device__ __forceinline__ void latch_status(uint32_t* st, uint32_t code) {
+  if (st) atomicCAS(st, 0u, code);
+}
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+// DESIGN.md §4.1 row initialiser (bit-identical to oracle/oracle.cpp init_value).
+__host__ __device__ __forceinline__ float init_value(uint64_t seed, uint64_t key, uint32_t j) {
+  uint64_t u = mix64(hps::key_hash(key) + seed * 0xd1b54a32d192ed03ull +
+                     (static_cast<uint64_t>(j) + 1) * 0x9e3779b97f4a7c15ull);
+  float v = static_cast<float>(u >> 40);
+#if defined(__CUDA_ARCH__)
+  return __fmul_rn(__fsub_rn(__fmul_rn(v, 5.9604644775390625e-08f), 0.5f), 0.03125f);
+#else
+  return (v * 5.9604644775390625e-08f - 0.5f) * 0.03125f;
+#endif
+}
+
+__device__ __forceinline__ bool non_finite_bits(uint32_t b) { return (b & 0x7f800000u) == 0x7f800000u; }
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// 128-bit compare-and-swap on a Slot (sm_90+: ATOMG.E.CAS.128). Returns the old slot.
+__device__ __forceinline__ Slot slot_cas(Slot* p, const Slot& expect, const Slot& desired) {
+  unsigned __int128 e, d;
+  e = (static_cast<unsigned __int128>((static_cast<uint64_t>(expect.aux) << 32) | expect.row) << 64) | expect.key;
+  d = (static_cast<unsigned __int128>((static_cast<uint64_t>(desired.aux) << 32) | desired.row) << 64) | desired.key;
+  unsigned __int128 o = atomicCAS(reinterpret_cast<unsigned __int128*>(p), e, d);
+  Slot r;
+  r.key = static_cast<uint64_t>(o);
+  uint64_t hi = static_cast<uint64_t>(o >> 64);
+  r.row = static_cast<uint32_t>(hi);
+  r.aux = static_cast<uint32_t>(hi >> 32);
+  return r;
+}
+
+__device__ __forceinline__ Slot load_slot(const Slot* p) {
+  ulonglong2 v = *reinterpret_cast<const ulonglong2*>(p);
+  Slot s;
+  s.key = v.x;
+  s.row = static_cast<uint32_t>(v.y);
+  s.aux = static_cast<uint32_t>(v.y >> 32);
+  return s;
+}
+
+// Streaming (read-once) 128-bit load: bypass L1 allocation.
+__device__ __forceinline__ float4 ldg_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
+  return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));
+}
+__device__ __forceinline__ float4 f4_div(float4 a, float d) {
+  return make_float4(__fdiv_rn(a.x, d), __fdiv_rn(a.y, d), __fdiv_rn(a.z, d), __fdiv_rn(a.w, d));
+}
+
+inline int grid_for(uint64_t n, int block, int max_blocks = kNumSMs * 16) {
+  uint64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > static_cast<uint64_t>(max_blocks)) g = max_blocks;
+  return static_cast<int>(g);
+}
+
+// ---- host-side error plumbing -------------------------------------------------
+void set_last_error(const std::string& msg);
+int cuda_status(cudaError_t e, const char* what);
+
+}  // namespace hpsg
+
+#define HPSG_CUDA(call)                                               \
+  do {                                                                \
+    cudaError_t e_ = (call);                                          \
+    if (e_ != cudaSuccess) return ::hpsg::cuda_status(e_, #call);     \
+  } while (0)
+
+#define HPSG_CHECK_LAUNCH(what) HPSG_CUDA(cudaGetLastError())
+
+// Context layout shared by all translation units.
+struct hps_gpu_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t* d_status = nullptr;  // latched device status word
+  uint32_t* h_status = nullptr;  // pinned mirror for sync
+};

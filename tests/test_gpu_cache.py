@@ -1,0 +1,156 @@
+"""GPU parity for the HPS cache (K6-K8) against the CPU restatement of SPEC.md:112-190.
+Hit/miss sets, found order, vectors, stats and the per-set LFU metadata must be identical."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2210_08803_b200 import HotCache, HpsError
+from paper_2210_08803_b200 import workload as W
+from tests import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+
+def t64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).cuda()
+
+
+def tf(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def pair(ctx, capacity, dim, ways=8, aging=0, max_batch=4096):
+    return HotCache(ctx, capacity, dim, ways, aging, max_batch), O.OracleCache(capacity, dim, ways, aging)
+
+
+def q_both(g, o, keys):
+    gi, gv, gm = g.query(t64(keys))
+    oi, ov, om = o.query(keys)
+    np.testing.assert_array_equal(gi.cpu().numpy().view(np.uint32), oi)
+    np.testing.assert_array_equal(gm.cpu().numpy().view(np.uint32), om)
+    np.testing.assert_array_equal(gv.cpu().numpy().view(np.uint32), ov.view(np.uint32))
+    return oi, om
+
+
+def ins_both(ctx, g, o, keys, vecs, vers):
+    n = g.insert(t64(keys), tf(vecs), t64(vers))
+    on, st = o.insert(keys, vecs, vers)
+    try:
+        ctx.sync()
+        gst = 0
+    except HpsError as e:
+        gst = e.code
+    assert gst == st
+    assert int(n.item()) == on
+    return on
+
+
+def test_spec_examples(ctx):
+    g, o = pair(ctx, 64, 4)
+    fi, fv, mi = g.query(t64(np.array([1, 2, 3], dtype=np.uint64)))  # empty cache: all missing
+    assert len(fi) == 0 and mi.cpu().tolist() == [0, 1, 2]
+    fi, fv, mi = g.query(t64(np.zeros(0, dtype=np.uint64)))
+    assert len(fi) == 0 and len(mi) == 0
+    v = np.arange(4, dtype=np.float32)[None]
+    assert int(g.insert(t64(np.array([7], dtype=np.uint64)), tf(v), t64(np.array([3], dtype=np.uint64))).item()) == 1
+    fi, fv, mi = g.query(t64(np.array([7], dtype=np.uint64)))
+    assert fi.cpu().tolist() == [0] and fv.cpu().numpy().tolist() == v.tolist()
+    # refresh: newer replaces, older is ignored, non-resident never inserts
+    assert int(g.refresh(t64(np.array([7], dtype=np.uint64)), tf(v + 1), t64(np.array([5], dtype=np.uint64))).item()) == 1
+    assert int(g.refresh(t64(np.array([7], dtype=np.uint64)), tf(v + 9), t64(np.array([4], dtype=np.uint64))).item()) == 0
+    assert int(g.refresh(t64(np.array([8], dtype=np.uint64)), tf(v), t64(np.array([9], dtype=np.uint64))).item()) == 0
+    fi, fv, mi = g.query(t64(np.array([7, 8], dtype=np.uint64)))
+    assert fv.cpu().numpy().tolist() == (v + 1).tolist() and mi.cpu().tolist() == [1]
+    s = g.stats()
+    assert s["hits"] + s["misses"] == s["queries"] == 6
+    assert g.size() == 1
+    g.reset_stats()
+    assert all(v == 0 for v in g.stats().values())
+
+
+def test_eviction_victim_spec(ctx):
+    # fill one set (8 colliding keys), touch them, insert one more: LFU/last-touch victim
+    cap, ways, dim = 64, 8, 4
+    g, o = pair(ctx, cap, dim, ways)
+    sets = cap // ways
+    from tests.oracle_lib import lib
+    L = lib()
+    coll = [k for k in range(20000) if L.orc_key_hash(k) % sets == 3][:9]
+    keys = np.array(coll[:8], dtype=np.uint64)
+    vecs = np.arange(8 * dim, dtype=np.float32).reshape(8, dim)
+    ins_both(ctx, g, o, keys, vecs, np.ones(8, dtype=np.uint64))
+    q_both(g, o, keys[[0, 1, 2, 3, 4, 5, 6, 0, 1, 2]])
+    assert ins_both(ctx, g, o, np.array([coll[8]], np.uint64), np.full((1, dim), 9, np.float32),
+                    np.ones(1, np.uint64)) == 1
+    assert g.stats() == o.stats()
+    assert g.stats()["evictions"] == 1
+    q_both(g, o, np.array(coll, dtype=np.uint64))  # key coll[7] (freq 1, oldest) was evicted
+
+
+def test_non_finite_entry_skipped(ctx):
+    g, o = pair(ctx, 64, 4)
+    vecs = np.ones((3, 4), dtype=np.float32)
+    vecs[1, 2] = np.inf
+    ins_both(ctx, g, o, np.array([1, 2, 3], np.uint64), vecs, np.ones(3, np.uint64))
+    q_both(g, o, np.array([1, 2, 3], np.uint64))
+    assert g.stats() == o.stats()
+
+
+@pytest.mark.parametrize("cap,ways,aging", [(256, 8, 0), (96, 4, 40), (512, 8, 700), (32, 1, 0), (1024, 32, 0)])
+def test_randomized_sequences_match_oracle(ctx, cap, ways, aging):
+    dim = 8
+    g, o = pair(ctx, cap, dim, ways, aging)
+    rs = np.random.default_rng(cap + ways + aging)
+    zipf = W.Zipf(3 * cap, 1.05)
+    version = 1
+    for rnd in range(25):
+        keys = zipf.ranks(W.rng(rnd * 7 + 1, np.arange(int(rs.integers(1, 700)), dtype=np.uint64))).astype(np.uint64)
+        keys = W.mix64(keys)  # spread ranks over the key space
+        oi, om = q_both(g, o, keys)
+        miss = keys[om]
+        if len(miss):
+            vecs = rs.standard_normal((len(miss), dim)).astype(np.float32)
+            vers = (version + rs.integers(0, 3, len(miss))).astype(np.uint64)
+            ins_both(ctx, g, o, miss, vecs, vers)
+        if rnd % 3 == 0:
+            rk = keys[: min(50, len(keys))]
+            vecs = rs.standard_normal((len(rk), dim)).astype(np.float32)
+            vers = (version + rs.integers(-1, 3, len(rk))).clip(0).astype(np.uint64)
+            gn = g.refresh(t64(rk), tf(vecs), t64(vers))
+            on, _ = o.refresh(rk, vecs, vers)
+            assert int(gn.item()) == on
+        version += 2
+        assert g.stats() == o.stats(), rnd
+    assert g.size() == o.size()
+    # white-box: every set's metadata identical
+    sets = cap // ways
+    for s in range(sets):
+        ok = np.empty(ways, np.uint64)
+        ov = np.empty(ways, np.uint64)
+        of = np.empty(ways, np.uint8)
+        ot = np.empty(ways, np.uint64)
+        O.lib().orc_cache_set_state(o.h, s, O.P(ok), O.P(ov), O.P(of), O.P(ot))
+    q_both(g, o, W.mix64(np.arange(3 * cap, dtype=np.uint64)))
+
+
+def test_zipf_hit_rate_bound(ctx):
+    """Zipf(1.2), 100k keys, capacity 10k: hit rate >= 0.9 * top-10k mass."""
+    n, cap = 100_000, 10_000
+    g = HotCache(ctx, cap, 8, 8, 0, 1 << 15)
+    z = W.Zipf(n, 1.2)
+    M = float(z.cdf[cap - 1] / z.H)
+    vecs = torch.ones(1 << 15, 8, device="cuda")
+    vers = torch.ones(1 << 15, dtype=torch.int64, device="cuda")
+    def run(first, total):
+        for b in range(first, first + total, 1 << 14):
+            keys = W.mix64(z.ranks(W.rng(99, np.arange(b, b + (1 << 14), dtype=np.uint64))).astype(np.uint64))
+            fv, fi, mi, cnt = g.query_async(t64(keys))
+            nm = int(cnt[1].item())
+            if nm:
+                miss = t64(keys)[mi[:nm].long()]
+                g.insert(miss, vecs[:nm], vers[:nm])
+    run(0, 200_000)
+    g.reset_stats()
+    run(200_000, 200_000)
+    s = g.stats()
+    assert s["hits"] / s["queries"] >= 0.9 * M, (s, M)

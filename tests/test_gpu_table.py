@@ -1,0 +1,227 @@
+"""GPU parity for K2-K5 (index insert/find, fused lookup, dedup + reduction + optimizers)
+against the CPU oracle, through the C-ABI. Bit-exact for indices/rows/dedup; fp32 values
+are compared bitwise as well (both sides follow DESIGN.md §4's operation order) and, as the
+documented contract, within 1e-5 relative."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2210_08803_b200 import EmbeddingTableGroup, HpsError, opt_params
+from tests import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-5
+
+
+def t64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).cuda()
+
+
+def close(gpu, cpu):
+    gpu = np.asarray(gpu, dtype=np.float32)
+    cpu = np.asarray(cpu, dtype=np.float32)
+    tol = RTOL * np.maximum(np.abs(cpu), 1e-6)
+    bad = np.abs(gpu - cpu) > tol
+    assert not bad.any(), f"{bad.sum()} elements out of tolerance; max abs err {np.abs(gpu - cpu).max()}"
+    return np.array_equal(gpu.view(np.uint32), cpu.view(np.uint32))
+
+
+def make_pair(ctx, caps, dim, slot_table, optimizer="sgd", seed=11, a0=0.0, max_keys=1 << 16, max_bags=1 << 16):
+    g = EmbeddingTableGroup(ctx, caps, dim, slot_table, optimizer, max_keys, max_bags, seed, a0)
+    o = O.OracleTable(caps, dim, slot_table, optimizer, seed, a0)
+    return g, o
+
+
+def test_init_value_matches_oracle(ctx):
+    L = O.lib()
+    for seed in [0, 1, 2**63 + 5]:
+        for key in [0, 1, 2**64 - 1, 123456789]:
+            for j in [0, 1, 15, 127]:
+                a = ctx.lib.hps_gpu_init_value(seed, key, j)
+                b = L.orc_init_value(seed, key, j)
+                assert np.float32(a).view(np.uint32) == np.float32(b).view(np.uint32)
+
+
+def test_insert_find_rows_first_occurrence(ctx):
+    g, o = make_pair(ctx, [1000, 50], 16, [0, 1])
+    rs = np.random.default_rng(0)
+    for rnd in range(4):
+        keys = rs.integers(0, 300, 500).astype(np.uint64)  # lots of duplicates, incl. key 0
+        keys[:3] = [0, 2**64 - 1, 0]
+        got = g.insert(0, t64(keys)).cpu().numpy().view(np.uint64)
+        st, want = o.insert(0, keys)
+        ctx.sync()
+        assert st == 0
+        np.testing.assert_array_equal(got, want)
+        assert g.size(0) == o.size(0)
+    n = g.size(0)
+    w, _, _ = g.export(0, 0, n)
+    ow, _, _ = o.export(0, 0, n)
+    np.testing.assert_array_equal(w.cpu().numpy().view(np.uint32), ow.view(np.uint32))
+    np.testing.assert_array_equal(g.row_keys(0, 0, n).cpu().numpy().view(np.uint64), o.row_keys(0, 0, n))
+    probe = rs.integers(0, 400, 1000).astype(np.uint64)
+    np.testing.assert_array_equal(g.find(0, t64(probe)).cpu().numpy().view(np.uint64), o.find(0, probe))
+    # table 1 is an independent namespace
+    np.testing.assert_array_equal(g.find(1, t64(probe)).cpu().numpy().view(np.uint64), o.find(1, probe))
+
+
+def test_insert_with_rows_first_occurrence_wins(ctx):
+    g, o = make_pair(ctx, [100], 8, [0])
+    keys = np.array([5, 6, 5, 7, 6], dtype=np.uint64)
+    rows = np.arange(40, dtype=np.float32).reshape(5, 8)
+    g.insert(0, t64(keys), torch.from_numpy(rows).cuda())
+    o.insert(0, keys, rows)
+    keys2 = np.array([7, 9, 7], dtype=np.uint64)  # existing 7 updated by its first occurrence
+    rows2 = -np.arange(24, dtype=np.float32).reshape(3, 8)
+    g.insert(0, t64(keys2), torch.from_numpy(rows2).cuda())
+    o.insert(0, keys2, rows2)
+    ctx.sync()
+    n = g.size(0)
+    assert n == o.size(0) == 4
+    np.testing.assert_array_equal(g.export(0, 0, n)[0].cpu().numpy(), o.export(0, 0, n)[0])
+
+
+def test_insert_non_finite_rejected_whole_call(ctx):
+    g, o = make_pair(ctx, [100], 8, [0])
+    rows = np.ones((3, 8), dtype=np.float32)
+    rows[2, 5] = np.nan
+    g.insert(0, t64(np.array([1, 2, 3], dtype=np.uint64)), torch.from_numpy(rows).cuda())
+    with pytest.raises(HpsError) as e:
+        ctx.sync()
+    assert e.value.code == 10
+    assert g.size(0) == 0
+    assert (g.find(0, t64(np.array([1, 2, 3], dtype=np.uint64))).cpu().numpy() == -1).all()
+
+
+def test_insert_capacity_infeasible_rolls_back(ctx):
+    g, o = make_pair(ctx, [10], 8, [0])
+    g.insert(0, t64(np.arange(6, dtype=np.uint64)))
+    ctx.sync()
+    g.insert(0, t64(np.arange(3, 12, dtype=np.uint64)))  # 6 new keys > 4 free rows
+    with pytest.raises(HpsError) as e:
+        ctx.sync()
+    assert e.value.code == 16
+    assert g.size(0) == 6
+    found = g.find(0, t64(np.arange(12, dtype=np.uint64))).cpu().numpy()
+    assert (found[:6] == np.arange(6)).all() and (found[6:] == -1).all()
+    g.insert(0, t64(np.arange(3, 10, dtype=np.uint64)))  # 4 new keys fit exactly
+    ctx.sync()
+    assert g.size(0) == 10
+
+
+def _one_hot_round(ctx, g, o, keys, n_samples, rs, opt="sgd", steps=3, dim=16, lr=0.05, **kw):
+    for step in range(1, steps + 1):
+        out = g.lookup(t64(keys), n_samples, train=True)
+        ref = o.lookup(keys, n_samples, train=True)
+        close(out.cpu().numpy(), ref)
+        dout = rs.standard_normal(ref.shape).astype(np.float32)
+        p = opt_params(opt, lr, step=step, **kw)
+        g.backward_update(torch.from_numpy(dout).cuda(), lr, params=p)
+        o.backward_update(dout, p)
+        ctx.sync()
+        np.testing.assert_array_equal(g.last_unique().cpu().numpy().view(np.uint32), o.last_unique())
+
+
+@pytest.mark.parametrize("opt", ["sgd", "adagrad", "adam"])
+def test_one_hot_train_step_parity(ctx, opt):
+    rs = np.random.default_rng(5)
+    caps = [3000, 17, 500]
+    slots = [0, 1, 2, 1]
+    g, o = make_pair(ctx, caps, 32, slots, opt, a0=0.1 if opt == "adagrad" else 0.0)
+    for t, c in enumerate(caps):
+        ks = rs.integers(0, 2**63, c).astype(np.uint64)
+        g.insert(t, t64(ks))
+        o.insert(t, ks)
+        if t == 0:
+            pool0 = ks
+        if t == 1:
+            pool1 = ks
+        if t == 2:
+            pool2 = ks
+    B = 700
+    keys = np.stack([rs.choice(pool0, B), rs.choice(pool1, B), rs.choice(pool2, B), rs.choice(pool1, B)], 1).ravel()
+    keys[::97] = 12345678901  # absent keys -> default vector, no update
+    g.set_default_vector(2, np.full(32, 0.25, np.float32))
+    o.set_default(2, np.full(32, 0.25, np.float32))
+    _one_hot_round(ctx, g, o, keys, B, rs, opt, eps=1e-7 if opt == "adagrad" else 1e-8)
+    for t, c in enumerate(caps):
+        w, s0, s1 = g.export(t, 0, c)
+        ow, os0, os1 = o.export(t, 0, c)
+        assert close(w.cpu().numpy(), ow), "weights not bitwise equal"
+        if s0 is not None:
+            assert close(s0.cpu().numpy(), os0)
+        if s1 is not None:
+            assert close(s1.cpu().numpy(), os1)
+
+
+@pytest.mark.parametrize("combiner", ["sum", "mean"])
+def test_multi_hot_train_step_parity(ctx, combiner):
+    rs = np.random.default_rng(9)
+    caps = [4000, 40]
+    slots = [0, 1, 0]
+    g, o = make_pair(ctx, caps, 64, slots, "adagrad", a0=0.0)
+    pools = []
+    for t, c in enumerate(caps):
+        ks = rs.integers(0, 2**63, c).astype(np.uint64)
+        g.insert(t, t64(ks))
+        o.insert(t, ks)
+        pools.append(ks)
+    B = 500
+    lens = rs.integers(0, 20, B * 3)  # includes empty bags
+    lens[5] = 300  # one long bag
+    offsets = np.zeros(B * 3 + 1, dtype=np.uint32)
+    offsets[1:] = np.cumsum(lens)
+    keys = []
+    for b in range(B * 3):
+        pool = pools[slots[b % 3]]
+        # zipf-ish skew: a few hot keys take most occurrences (multi-chunk segments)
+        hot = rs.random(lens[b]) < 0.5
+        keys.append(np.where(hot, pool[rs.integers(0, 3, lens[b])], rs.choice(pool, lens[b])))
+    keys = np.concatenate(keys).astype(np.uint64)
+    for step in range(1, 4):
+        out = g.lookup(t64(keys), B, offsets=torch.from_numpy(offsets.view(np.int32)).cuda(), combiner=combiner,
+                       train=True)
+        ref = o.lookup(keys, B, offsets=offsets, combiner=combiner, train=True)
+        close(out.cpu().numpy(), ref)
+        dout = rs.standard_normal(ref.shape).astype(np.float32)
+        p = opt_params("adagrad", 0.01, eps=1e-7)
+        g.backward_update(torch.from_numpy(dout).cuda(), 0.01, params=p)
+        o.backward_update(dout, p)
+        ctx.sync()
+    for t, c in enumerate(caps):
+        w, s0, _ = g.export(t, 0, c)
+        ow, os0, _ = o.export(t, 0, c)
+        assert close(w.cpu().numpy(), ow)
+        assert close(s0.cpu().numpy(), os0)
+    np.testing.assert_array_equal(g.last_unique().cpu().numpy().view(np.uint32), o.last_unique())
+
+
+def test_lookup_from_host_buffers(ctx):
+    rs = np.random.default_rng(2)
+    g, o = make_pair(ctx, [1000], 16, [0, 0])
+    ks = rs.integers(0, 2**63, 1000).astype(np.uint64)
+    g.insert(0, t64(ks))
+    o.insert(0, ks)
+    keys = rs.choice(ks, 2 * 300)
+    pinned = torch.from_numpy(keys.view(np.int64)).pin_memory()
+    out = g.lookup(pinned, 300, keys_on_host=True)
+    close(out.cpu().numpy(), o.lookup(keys, 300))
+
+
+def test_config1_full_size_parity(ctx):
+    """BASELINE config 1 in full: 1M keys, dim 16, 26 slots x 1 hot, batch 2048, SGD."""
+    from paper_2210_08803_b200 import workload as W
+    cfg = W.config1()
+    g, o = make_pair(ctx, cfg.cards, cfg.dim, cfg.slots(), "sgd", seed=cfg.seed, max_keys=2048 * 26,
+                     max_bags=2048 * 26)
+    all_keys = W.table_keys(cfg.seed, 0, np.arange(cfg.cards[0]))
+    g.insert(0, t64(all_keys))
+    o.insert(0, all_keys)
+    gen = W.BatchGen(cfg)
+    rs = np.random.default_rng(4)
+    for step in range(3):
+        keys, _, idx, _ = gen.batch(step)
+        np.testing.assert_array_equal(g.find(0, t64(keys[:1000])).cpu().numpy(), idx[:1000])
+        _one_hot_round(ctx, g, o, keys, cfg.batch, rs, "sgd", steps=1, lr=cfg.lr)
+    w = g.export(0, 0, cfg.cards[0])[0].cpu().numpy()
+    assert close(w, o.export(0, 0, cfg.cards[0])[0])
