@@ -1,0 +1,344 @@
+"""bench.py — DLRM-shape embedding fwd+bwd+update samples/s on B200 (BASELINE.json metric).
+
+Workload (N=1 default): BASELINE config 2, the MLPerf-DLRM shape — 26 tables at the
+Criteo-1TB cardinalities capped at 40M (187.8M rows, 96.1 GB fp32 at dim 128), one key
+per slot, sum pooling, sparse SGD, 6,912 samples per GPU per step (8 GPUs x 6,912 =
+the config's global batch 55,296). One step = hps_gpu_lookup_pooled (train) +
+hps_gpu_backward_update on synthetic keys; d_out (the dense model's gradient, out of
+scope) is a pre-generated device tensor. Multi-GPU: distributed slot sharding
+(owner = key_hash mod G) through paper_2210_08803_b200.sharded.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg3] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0). `--impl reference` times the CPU implementation of the
+same step (the oracle port, all host threads) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2210_08803_b200 import workload as W  # noqa: E402
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--batch-per-gpu", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pool", type=int, default=4, help="distinct synthetic batches rotated through")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--table-scale", type=float, default=1.0, help="debug only: shrink cardinalities")
+    return ap.parse_args()
+
+
+def get_config(args):
+    if args.config == "cfg1":
+        cfg = W.config1()
+    elif args.config == "cfg2":
+        cfg = W.config2()
+    else:
+        cfg = W.config3()
+    if args.batch_per_gpu:
+        cfg.batch = args.batch_per_gpu
+    if args.table_scale != 1.0:
+        cfg.cards = [max(1, int(c * args.table_scale)) for c in cfg.cards]
+    return cfg
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ---------------------------------------------------------------------------------------
+# algorithmic bytes
+# ---------------------------------------------------------------------------------------
+def algorithmic_bytes(N, U, n_bags, dim, n_state, multi):
+    e, k, P = 4, 8, 16
+    f = 4 if multi else 0
+    fwd = N * (k + P + dim * e) + n_bags * (dim * e + f)
+    bwd = n_bags * (dim * e + f) + N * k + U * (P + 2 * dim * e * (1 + n_state))
+    return fwd, bwd
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 7]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for r in rows for j in range(4) if r[3 + j].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU side: the reference arm and the cpu_baseline leg (oracle port; checker, not product)
+# ---------------------------------------------------------------------------------------
+def cpu_step_runner(cfg, threads):
+    from tests import oracle_lib as O
+    import ctypes as C
+    L = O.lib()
+    L.orc_sparse_create.restype = C.c_void_p
+    L.orc_sparse_create.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32, C.c_int, C.c_uint64, C.c_float]
+    L.orc_sparse_step.restype = C.c_int
+    L.orc_sparse_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_int, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_int]
+    L.orc_sparse_destroy.argtypes = [C.c_void_p]
+    st = np.asarray(cfg.slots(), dtype=np.uint32)
+    opt = {"sgd": 0, "adagrad": 1, "adam": 2}[cfg.optimizer]
+    h = L.orc_sparse_create(len(cfg.cards), cfg.dim, O.P(st), len(st), opt, cfg.seed, 0.0)
+    from paper_2210_08803_b200.api import opt_params
+    p = opt_params(cfg.optimizer, cfg.lr, eps=cfg.eps)
+    o7 = np.array([p.lr, p.eps, p.beta1, p.beta2, p.one_minus_beta1, p.one_minus_beta2, p.lr_t], dtype=np.float32)
+    comb = 1 if cfg.combiner == "mean" else 0
+
+    def step(keys, offs, dout, out):
+        return L.orc_sparse_step(h, O.P(keys), O.P(offs), cfg.batch, comb, O.P(dout), O.P(o7), O.P(out), threads)
+
+    return step, lambda: L.orc_sparse_destroy(h)
+
+
+def run_cpu(cfg, steps, warmup, threads, budget_s=None):
+    """Time the oracle port of one full per-GPU step. Returns (samples/s, sample description)."""
+    gen = W.BatchGen(cfg)
+    batches = [gen.batch(s) for s in range(min(4, steps + warmup))]
+    step, close = cpu_step_runner(cfg, threads)
+    rs = np.random.default_rng(0)
+    n_bags = cfg.batch * cfg.n_slots
+    dout = (rs.standard_normal((n_bags, cfg.dim)) * 0.01).astype(np.float32)
+    out = np.empty((n_bags, cfg.dim), dtype=np.float32)
+    for s in range(warmup):
+        k, o, _, _ = batches[s % len(batches)]
+        step(k, o, dout, out)
+    t0 = time.perf_counter()
+    done = 0
+    for s in range(steps):
+        k, o, _, _ = batches[s % len(batches)]
+        step(k, o, dout, out)
+        done += 1
+        if budget_s and time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    close()
+    return cfg.batch * done / dt, f"{done} full steps of {cfg.batch} samples x {cfg.n_slots} slots (rows materialised on first touch)"
+
+
+def reference_arm(args, cfg, rank, world):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    val, sample = run_cpu(cfg, args.steps, args.warmup, threads)
+    line = {
+        "impl": "reference", "metric": "DLRM-shape embedding fwd+bwd+update samples/s", "value": val,
+        "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * cfg.batch / val, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "tables": len(cfg.cards),
+                   "rows": int(sum(cfg.cards)), "dim": cfg.dim, "combiner": cfg.combiner, "optimizer": cfg.optimizer},
+        "cpu_baseline": {"value": val, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = get_config(args)
+    if args.impl == "reference":
+        return reference_arm(args, cfg, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2210_08803_b200 import Context, opt_params
+    from paper_2210_08803_b200.sharded import build_tables, TrainStep
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ctx = Context(local)
+    t_setup = time.perf_counter()
+    tables = build_tables(ctx, cfg, rank, world)
+    gen = W.BatchGen(cfg)
+    step_fn = TrainStep(ctx, tables, cfg, rank, world)
+    pool = []
+    rs = np.random.default_rng(rank)
+    n_bags = cfg.batch * cfg.n_slots
+    for s in range(args.pool):
+        keys, offs, _, _ = gen.batch(s * world + rank)
+        pool.append(step_fn.stage_batch(keys, offs))
+    douts = [torch.from_numpy((rs.standard_normal((n_bags, cfg.dim)) * 0.01).astype(np.float32)).cuda()
+             for _ in range(min(args.pool, 2))]
+    setup_s = time.perf_counter() - t_setup
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def one(i):
+        b = pool[i % len(pool)]
+        step_fn.run(b, douts[i % len(douts)], step=i + 1)
+
+    for i in range(args.warmup):
+        one(i)
+    ctx.sync()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)  # evict L2 between timed iterations (not inside the step events)
+        starts[i].record(stream)
+        step_fn.run(pool[i % len(pool)], douts[i % len(douts)], step=args.warmup + i + 1)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ctx.sync()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    N, U = step_fn.last_counts()
+    # the dominant kernel alone: one hps_gpu_lookup_pooled launch (k_lookup_*) between events
+    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 0xff)
+        fwd_ev[i][0].record(stream)
+        step_fn.lookup_only(pool[i % len(pool)])
+        fwd_ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    fwd_ms = [a.elapsed_time(b) for a, b in fwd_ev]
+    ms = float(np.mean(step_ms))
+    t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * cfg.batch / (ms_max / 1000.0)
+
+    # algorithmic bytes of the last step's batch on this rank
+    fwd_b, bwd_b = algorithmic_bytes(N, U, n_bags, cfg.dim, {"sgd": 0, "adagrad": 1, "adam": 2}[cfg.optimizer],
+                                     cfg.hot > 1)
+    peak, peak_kind = hbm_peak()
+    fwd_ms_mean = float(np.mean(fwd_ms))
+    fwd_gbs = fwd_b / (fwd_ms_mean / 1000.0) / 1e9
+    step_gbs = (fwd_b + bwd_b) / (ms / 1000.0) / 1e9
+
+    # e2e: the same step through the C-ABI from pinned HOST keys + a D2H read of the step result
+    e2e_steps = args.e2e_steps or args.steps
+    host_batches = []
+    for s in range(min(args.pool, 4)):
+        keys, offs, _, _ = gen.batch(1000 + s * world + rank)
+        host_batches.append(step_fn.stage_host(keys, offs))
+    for i in range(2):
+        step_fn.run_host(host_batches[i % len(host_batches)], douts[0], step=10_000 + i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    h2d = d2h = 0
+    for i in range(e2e_steps):
+        bi, bo = step_fn.run_host(host_batches[i % len(host_batches)], douts[i % len(douts)], step=20_000 + i)
+        h2d, d2h = bi, bo
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    t = torch.tensor([e2e_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = world * cfg.batch / (float(t.item()) / 1000.0)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        cval, sample = run_cpu(cfg, steps=30, warmup=2, threads=threads, budget_s=20.0)
+        cpu = {"value": cval, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "DLRM-shape embedding fwd+bwd+update samples/s",
+            "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * world,
+                       "tables": len(cfg.cards), "rows": int(sum(cfg.cards)), "dim": cfg.dim,
+                       "hot": cfg.hot, "combiner": cfg.combiner, "optimizer": cfg.optimizer,
+                       "parallelism": f"distributed-slot x{world}" if world > 1 else "single",
+                       "l2": "flushed between timed steps (256 MB write)", "graph": step_fn.graph_mode},
+            "roofline": {"bound": "hbm", "kernel": "k_lookup_1hot (fused hash+probe+gather+pool)" if cfg.hot == 1
+                         else "k_lookup_multi (fused hash+probe+gather+pool)",
+                         "achieved": fwd_gbs, "peak": peak, "unit": "GB/s", "frac": fwd_gbs / peak,
+                         "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes": fwd_b,
+                         "kernel_ms": fwd_ms_mean,
+                         "step_achieved": step_gbs, "step_frac": step_gbs / peak, "step_algorithmic_bytes": fwd_b + bwd_b},
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": step_fn.kernels_per_step * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "unique_keys": U, "key_occurrences": N, "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -188,48 +188,48 @@ int lookup_pooled(Table* t, const uint64_t* keys, const uint32_t* offsets, uint3
   return 0;
 }
 
-inline void apply_optimizer(Table* t, uint64_t g_row, const float* g, const OptParams& p) {
-  const uint32_t D = t->dim;
-  float* w = &t->w[g_row * D];
-  if (t->optimizer == 0) {  // SGD: w -= lr*g
+// DESIGN.md §4.4 optimizers, in the exact operation order of the CUDA kernels.
+inline void apply_optimizer(int optimizer, float* w, float* s0, float* s1, uint32_t D, const float* g,
+                            const OptParams& p) {
+  if (optimizer == 0) {  // SGD: w -= lr*g
     for (uint32_t j = 0; j < D; ++j) w[j] = w[j] - p.lr * g[j];
-  } else if (t->optimizer == 1) {  // AdaGrad: a += g^2; w -= lr*g/(sqrt(a)+eps)
-    float* a = &t->s0[g_row * D];
+  } else if (optimizer == 1) {  // AdaGrad: a += g^2; w -= lr*g/(sqrt(a)+eps)
     for (uint32_t j = 0; j < D; ++j) {
-      a[j] = a[j] + g[j] * g[j];
-      w[j] = w[j] - (p.lr * g[j]) / (std::sqrt(a[j]) + p.eps);
+      s0[j] = s0[j] + g[j] * g[j];
+      w[j] = w[j] - (p.lr * g[j]) / (std::sqrt(s0[j]) + p.eps);
     }
   } else {  // Adam (lazy): m,v moments; lr_t carries the bias correction
-    float* m = &t->s0[g_row * D];
-    float* v = &t->s1[g_row * D];
     for (uint32_t j = 0; j < D; ++j) {
-      m[j] = p.beta1 * m[j] + p.one_minus_beta1 * g[j];
-      v[j] = p.beta2 * v[j] + p.one_minus_beta2 * (g[j] * g[j]);
-      w[j] = w[j] - (p.lr_t * m[j]) / (std::sqrt(v[j]) + p.eps);
+      s0[j] = p.beta1 * s0[j] + p.one_minus_beta1 * g[j];
+      s1[j] = p.beta2 * s1[j] + p.one_minus_beta2 * (g[j] * g[j]);
+      w[j] = w[j] - (p.lr_t * s0[j]) / (std::sqrt(s1[j]) + p.eps);
     }
   }
 }
 
 // per-occurrence gradient, dedup by row (stable in occurrence order),
 // blocked reduction (chunks of kChunk summed sequentially, then the chunk partials
-// summed sequentially), then the optimizer on each unique row.
-int backward_update(Table* t, const float* dout, const OptParams& p, int n_threads) {
-  const uint32_t D = t->dim;
-  const uint64_t N = t->occ_row.size();
+// summed sequentially), then the optimizer on each unique row. `row_ptr(row, k)` gives
+// the weight (k=0) and state (k=1,2) row of a global row id.
+template <class RowPtr>
+void reduce_and_update(const std::vector<uint64_t>& occ_row, const std::vector<uint32_t>& occ_bag,
+                       const std::vector<uint32_t>& bag_len, bool mean, const float* dout, uint32_t D, int optimizer,
+                       const OptParams& p, int n_threads, std::vector<uint32_t>* unique_out, RowPtr row_ptr) {
+  const uint64_t N = occ_row.size();
   std::vector<uint64_t> order;
   order.reserve(N);
   for (uint64_t i = 0; i < N; ++i)
-    if (t->occ_row[i] != UINT64_MAX) order.push_back(i);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](uint64_t a, uint64_t b) { return t->occ_row[a] < t->occ_row[b]; });
+    if (occ_row[i] != UINT64_MAX) order.push_back(i);
+  std::stable_sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) { return occ_row[a] < occ_row[b]; });
   std::vector<uint64_t> seg;  // segment starts into `order`
   for (uint64_t i = 0; i < order.size(); ++i)
-    if (i == 0 || t->occ_row[order[i]] != t->occ_row[order[i - 1]]) seg.push_back(i);
+    if (i == 0 || occ_row[order[i]] != occ_row[order[i - 1]]) seg.push_back(i);
   seg.push_back(order.size());
   const uint64_t U = seg.size() - 1;
-  t->last_unique.resize(U);
-  for (uint64_t u = 0; u < U; ++u) t->last_unique[u] = static_cast<uint32_t>(t->occ_row[order[seg[u]]]);
-  const bool mean = t->last_combiner == 1;
+  if (unique_out) {
+    unique_out->resize(U);
+    for (uint64_t u = 0; u < U; ++u) (*unique_out)[u] = static_cast<uint32_t>(occ_row[order[seg[u]]]);
+  }
 #ifdef _OPENMP
 #pragma omp parallel num_threads(n_threads)
 #endif
@@ -241,10 +241,10 @@ int backward_update(Table* t, const float* dout, const OptParams& p, int n_threa
     for (int64_t u = 0; u < static_cast<int64_t>(U); ++u) {
       const uint64_t lo = seg[u], hi = seg[u + 1];
       auto grad_of = [&](uint64_t occ, float* dst) {
-        const uint32_t b = t->occ_bag[occ];
+        const uint32_t b = occ_bag[occ];
         const float* d = dout + static_cast<uint64_t>(b) * D;
         if (mean) {
-          const float fl = static_cast<float>(t->bag_len[b]);
+          const float fl = static_cast<float>(bag_len[b]);
           for (uint32_t j = 0; j < D; ++j) dst[j] = d[j] / fl;
         } else {
           for (uint32_t j = 0; j < D; ++j) dst[j] = d[j];
@@ -263,11 +263,60 @@ int backward_update(Table* t, const float* dout, const OptParams& p, int n_threa
           for (uint32_t j = 0; j < D; ++j) acc[j] = acc[j] + part[j];
         }
       }
-      apply_optimizer(t, t->occ_row[order[lo]], acc.data(), p);
+      const uint64_t r = occ_row[order[lo]];
+      apply_optimizer(optimizer, row_ptr(r, 0), row_ptr(r, 1), row_ptr(r, 2), D, acc.data(), p);
     }
   }
+}
+
+int backward_update(Table* t, const float* dout, const OptParams& p, int n_threads) {
+  const uint32_t D = t->dim;
+  reduce_and_update(t->occ_row, t->occ_bag, t->bag_len, t->last_combiner == 1, dout, D, t->optimizer, p, n_threads,
+                    &t->last_unique, [&](uint64_t r, int k) -> float* {
+                      if (k == 0) return &t->w[r * D];
+                      if (k == 1) return t->s0.empty() ? nullptr : &t->s0[r * D];
+                      return t->s1.empty() ? nullptr : &t->s1[r * D];
+                    });
   return 0;
 }
+
+// ---------------------------------------------------------------------------
+// Sparse (lazily materialised) model of a fully pre-loaded table group, for the CPU
+// baseline at BASELINE scale: every key of every table logically exists with its
+// init_value row (exactly the GPU bench's bulk-loaded state); rows are materialised on
+// first touch instead of allocating 96 GB of host memory.
+// ---------------------------------------------------------------------------
+struct Sparse {
+  uint32_t n_tables = 0, dim = 0, n_slots = 0;
+  int optimizer = 0;
+  uint64_t seed = 0;
+  float a0 = 0.f;
+  std::vector<uint32_t> slot_table;
+  std::vector<std::unordered_map<uint64_t, uint64_t>> index;
+  std::vector<float> w, s0, s1;
+  uint64_t rows = 0;
+  std::vector<uint64_t> occ_row;
+  std::vector<uint32_t> occ_bag, bag_len;
+
+  uint64_t touch(uint32_t table, uint64_t key) {
+    auto it = index[table].find(key);
+    if (it != index[table].end()) return it->second;
+    const uint64_t r = rows++;
+    index[table].emplace(key, r);
+    if (w.size() < rows * dim) {
+      const uint64_t cap = std::max<uint64_t>(rows * dim * 2, 1 << 20);
+      w.resize(cap);
+      if (optimizer >= 1) s0.resize(cap);
+      if (optimizer >= 2) s1.resize(cap);
+    }
+    for (uint32_t j = 0; j < dim; ++j) w[r * dim + j] = init_value(seed, key, j);
+    if (optimizer == 1)
+      for (uint32_t j = 0; j < dim; ++j) s0[r * dim + j] = a0;
+    if (optimizer == 2)
+      for (uint32_t j = 0; j < dim; ++j) s0[r * dim + j] = 0.f, s1[r * dim + j] = 0.f;
+    return r;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // Hot cache model: SPEC.md:112-190 with DESIGN.md §5 resolutions
@@ -540,6 +589,67 @@ void orc_cache_set_state(void* h, uint64_t set, uint64_t* keys, uint64_t* versio
   std::memcpy(versions, &c->version[b], c->ways * 8);
   std::memcpy(freq, &c->freq[b], c->ways);
   std::memcpy(last_touch, &c->last_touch[b], c->ways * 8);
+}
+
+// ---- sparse CPU step (baseline timing; same math as the table model) ----
+void* orc_sparse_create(uint32_t n_tables, uint32_t dim, const uint32_t* slot_table, uint32_t n_slots, int optimizer,
+                        uint64_t seed, float a0) {
+  auto* s = new Sparse;
+  s->n_tables = n_tables;
+  s->dim = dim;
+  s->n_slots = n_slots;
+  s->optimizer = optimizer;
+  s->seed = seed;
+  s->a0 = a0;
+  s->slot_table.assign(slot_table, slot_table + n_slots);
+  s->index.resize(n_tables);
+  return s;
+}
+void orc_sparse_destroy(void* h) { delete static_cast<Sparse*>(h); }
+// One fwd+bwd+update step: keys sample-major, offsets==nullptr => one key per bag.
+int orc_sparse_step(void* h, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples, int combiner,
+                    const float* dout, const float* opt7, float* out, int n_threads) {
+  auto* s = static_cast<Sparse*>(h);
+  const uint32_t D = s->dim, S = s->n_slots;
+  const uint64_t n_bags = static_cast<uint64_t>(n_samples) * S;
+  const uint64_t N = offsets ? offsets[n_bags] : n_bags;
+  s->occ_row.resize(N);
+  s->occ_bag.resize(N);
+  s->bag_len.resize(n_bags);
+  for (uint64_t b = 0; b < n_bags; ++b) {  // index probe (serial: std::unordered_map)
+    const uint32_t table = s->slot_table[b % S];
+    const uint64_t lo = offsets ? offsets[b] : b, hi = offsets ? offsets[b + 1] : b + 1;
+    s->bag_len[b] = static_cast<uint32_t>(hi - lo);
+    for (uint64_t i = lo; i < hi; ++i) {
+      s->occ_row[i] = s->touch(table, keys[i]);
+      s->occ_bag[i] = static_cast<uint32_t>(b);
+    }
+  }
+  const float* W = s->w.data();
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) num_threads(n_threads)
+#endif
+  for (int64_t b = 0; b < static_cast<int64_t>(n_bags); ++b) {
+    const uint64_t lo = offsets ? offsets[b] : b, hi = offsets ? offsets[b + 1] : b + 1;
+    float* o = out + b * D;
+    for (uint32_t j = 0; j < D; ++j) o[j] = 0.0f;
+    for (uint64_t i = lo; i < hi; ++i) {
+      const float* src = W + s->occ_row[i] * D;
+      for (uint32_t j = 0; j < D; ++j) o[j] = o[j] + src[j];
+    }
+    if (combiner == 1 && hi > lo) {
+      const float fl = static_cast<float>(hi - lo);
+      for (uint32_t j = 0; j < D; ++j) o[j] = o[j] / fl;
+    }
+  }
+  OptParams p{opt7[0], opt7[1], opt7[2], opt7[3], opt7[4], opt7[5], opt7[6]};
+  reduce_and_update(s->occ_row, s->occ_bag, s->bag_len, combiner == 1, dout, D, s->optimizer, p, n_threads, nullptr,
+                    [&](uint64_t r, int k) -> float* {
+                      if (k == 0) return &s->w[r * D];
+                      if (k == 1) return s->s0.empty() ? nullptr : &s->s0[r * D];
+                      return s->s1.empty() ? nullptr : &s->s1[r * D];
+                    });
+  return 0;
 }
 
 }  // extern "C"

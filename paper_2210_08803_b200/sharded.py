@@ -1,0 +1,133 @@
+"""Table construction and the training step used by bench.py (1..8 GPUs).
+
+Single GPU: one table group holds every table. Multi-GPU (distributed slot sharding,
+SPEC.md:487-491): rank r owns the keys with partition_of(key, G) == r;
+the exchange lives in paper_2210_08803_b200.exchange.
+"""
+from __future__ import annotations
+
+import math
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import workload as W
+from .api import Context, EmbeddingTableGroup, opt_params
+
+
+def _owned_keys(ctx: Context, cfg: W.Config, t: int, rank: int, world: int, first: int, n: int) -> torch.Tensor:
+    keys = ctx.gen_keys(W.table_seed(cfg.seed, t), first, n)
+    if world > 1:
+        keys = keys[ctx.partition_of(keys, world) == rank]
+    return keys
+
+
+def build_tables(ctx: Context, cfg: W.Config, rank: int = 0, world: int = 1,
+                 chunk: int = 1 << 24) -> EmbeddingTableGroup:
+    """Create the (shard of the) table group and bulk-insert every key of every table,
+    in index order, so that on one GPU row i of table t holds table_key(t, i)."""
+    n_bags = cfg.batch * cfg.n_slots
+    max_keys = n_bags * (2 * cfg.hot - 1 if cfg.hot > 1 else 1)
+    if world > 1:
+        max_keys *= world
+        n_bags_cap = max(n_bags * world, max_keys)
+    else:
+        n_bags_cap = n_bags
+    caps = []
+    for c in cfg.cards:
+        caps.append(c if world == 1 else int(c / world * 1.02 + 64 * math.sqrt(c / world + 1) + 64))
+    g = EmbeddingTableGroup(ctx, caps, cfg.dim, cfg.slots() if world == 1 else list(range(len(cfg.cards))),
+                            cfg.optimizer, max_batch_keys=max_keys, max_batch_bags=n_bags_cap, init_seed=cfg.seed)
+    for t, c in enumerate(cfg.cards):
+        for first in range(0, c, chunk):
+            n = min(chunk, c - first)
+            g.insert(t, _owned_keys(ctx, cfg, t, rank, world, first, n))
+    ctx.sync()
+    return g
+
+
+class TrainStep:
+    """One fwd+bwd+update step over a staged batch. world == 1 runs the fused path
+    (2 C-ABI calls, optionally replayed as one CUDA graph); world > 1 runs the
+    distributed exchange (paper_2210_08803_b200.exchange)."""
+
+    def __init__(self, ctx: Context, table: EmbeddingTableGroup, cfg: W.Config, rank: int = 0, world: int = 1,
+                 use_graph: bool = True):
+        self.ctx, self.table, self.cfg, self.rank, self.world = ctx, table, cfg, rank, world
+        self.n_bags = cfg.batch * cfg.n_slots
+        self.out = torch.empty(self.n_bags, cfg.dim, dtype=torch.float32, device="cuda")
+        self.params = opt_params(cfg.optimizer, cfg.lr, eps=cfg.eps)
+        self.graph_mode = bool(use_graph and world == 1 and cfg.optimizer != "adam")
+        self._graphs = {}
+        bits = max(1, int(sum(table.row_capacity)).bit_length())
+        passes = (bits + 7) // 8
+        self.kernels_per_step = 1 + 1 + passes + 2 + 1
+        self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self.exchange = None
+        if world > 1:
+            from .exchange import DistributedExchange
+            self.exchange = DistributedExchange(ctx, table, cfg, rank, world)
+            self.kernels_per_step = self.exchange.kernels_per_step
+
+    # -- inputs -------------------------------------------------------------------------
+    def stage_batch(self, keys: np.ndarray, offs: Optional[np.ndarray]):
+        k = torch.from_numpy(np.ascontiguousarray(keys).view(np.int64)).cuda()
+        o = None if offs is None else torch.from_numpy(np.ascontiguousarray(offs).view(np.int32)).cuda()
+        return {"keys": k, "offs": o, "n_keys": int(len(keys))}
+
+    def stage_host(self, keys: np.ndarray, offs: Optional[np.ndarray]):
+        k = torch.from_numpy(np.ascontiguousarray(keys).view(np.int64)).pin_memory()
+        o = None if offs is None else torch.from_numpy(np.ascontiguousarray(offs).view(np.int32)).pin_memory()
+        return {"keys": k, "offs": o, "n_keys": int(len(keys))}
+
+    # -- the step --------------------------------------------------------------------------
+    def _eager(self, b, dout, step, keys_on_host=False):
+        if self.cfg.optimizer == "adam":
+            self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
+        self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=True,
+                          out=self.out, keys_on_host=keys_on_host)
+        self.table.backward_update(dout, self.cfg.lr, params=self.params)
+
+    def run(self, b, dout, step: int = 1):
+        self._last_n = b["n_keys"]
+        if self.exchange is not None:
+            return self.exchange.step(b, dout, step, self.out)
+        if not self.graph_mode:
+            return self._eager(b, dout, step)
+        key = (id(b["keys"]), id(dout))
+        g = self._graphs.get(key)
+        if g is None:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self.ctx.set_stream(s)
+                self._eager(b, dout, step)  # warm: lazy module loading outside capture
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self._eager(b, dout, step)
+            torch.cuda.current_stream().wait_stream(s)
+            self.ctx.set_stream(torch.cuda.current_stream())
+            self._graphs[key] = g
+        g.replay()
+
+    def run_host(self, b, dout, step: int = 1):
+        """End-to-end through the C-ABI: keys from pinned host memory (H2D inside the call),
+        and a D2H read of the step's result (the number of rows updated)."""
+        if self.exchange is not None:
+            return self.exchange.step_host(b, dout, step, self.out)
+        self._eager(b, dout, step, keys_on_host=True)
+        self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
+        _ = int(self._cnt.item())
+        h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
+        return h2d, 8
+
+    def last_counts(self):
+        if self.exchange is not None:
+            return self.exchange.last_counts()
+        self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
+        return self._last_n, int(self._cnt.item())
+
+    def lookup_only(self, b):
+        self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=False,
+                          out=self.out)
