@@ -102,11 +102,11 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(Op op, uint64_t* status, ui
   }
   if (tile >= n_tiles) return;
   const uint64_t base = tile * kScanTile + uint64_t(threadIdx.x) * kScanIPT;
-  uint32_t c[kScanIPT];
+  uint64_t c[kScanIPT];  // counts may be packed (several u32 fields summed at once)
   uint64_t sum = 0;
 #pragma unroll
   for (int k = 0; k < kScanIPT; ++k) {
-    c[k] = (base + k < n) ? op.count(base + k) : 0u;
+    c[k] = (base + k < n) ? static_cast<uint64_t>(op.count(base + k)) : 0ull;
     sum += c[k];
   }
   uint64_t agg;

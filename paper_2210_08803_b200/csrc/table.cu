@@ -16,12 +16,12 @@
 
 #include "common.cuh"
 #include "primitives.cuh"
+#include "table_internal.cuh"
 
 using namespace hpsg;
 
 namespace {
 
-constexpr uint32_t kChunk = 32;  // blocked reduction width
 constexpr uint64_t kNoSlot = ~0ull;
 
 // ---------------------------------------------------------------------------------
@@ -216,6 +216,10 @@ __global__ void k_rows_non_finite(const float* __restrict__ v, uint64_t n, uint3
   }
 }
 
+__global__ void k_fill_u64(uint64_t* p, uint64_t n, uint64_t v) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) p[i] = v;
+}
+
 __global__ void k_fill_slots_empty(Slot* slots, uint64_t n) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     *reinterpret_cast<ulonglong2*>(slots + i) = make_ulonglong2(0ull, (uint64_t(kAuxNone) << 32) | kRowEmpty);
@@ -237,19 +241,31 @@ struct LookupArgs {
   uint32_t dim;
   int mean;
   float* out;
-  uint32_t* occ_row;   // train: global row per key occurrence (row_absent for misses)
-  uint32_t* occ_bag;   // train, multi-hot: bag of each occurrence
-  uint32_t* bag_len;   // train, multi-hot mean: bag lengths
-  uint32_t row_absent;
-  uint64_t* d_n;       // train: number of key occurrences (device)
+  // training only: fused dedup insert (table_internal.cuh) + per-occurrence records
+  uint64_t* scr;
+  int scr_bits;
+  uint32_t* occ_scr;   // dedup slot of each occurrence (kNoScr: key absent -> no gradient)
+  uint32_t* occ_rank;  // arrival rank of the occurrence among its key's occurrences
+  uint32_t* occ_bag;   // multi-hot: bag of each occurrence
+  uint32_t* bag_len;   // multi-hot mean: bag lengths
+  uint64_t* d_n;       // number of key occurrences (device)
 };
 
+__device__ __forceinline__ void record_occurrence(const LookupArgs& a, uint64_t i, uint32_t local, uint32_t row) {
+  uint32_t slot = kNoScr, rank = 0;
+  if (local != kRowEmpty) scr_insert(a.scr, a.scr_bits, row, &slot, &rank);
+  a.occ_scr[i] = slot;
+  a.occ_rank[i] = rank;
+}
+
 // One-key-per-bag path. A warp owns 32 consecutive bags: every lane hashes and probes
-// one key (32 independent index loads in flight), then groups of LPR lanes stream the
-// rows with 128-bit loads (VPL float4 per lane) and write the bag outputs coalesced.
-template <int LPR>
+// one key (32 independent index loads in flight) and, when training, registers the
+// occurrence in the dedup table; then groups of LPR lanes stream the rows with 128-bit
+// loads (VPL float4 per lane, 8 rows in flight per group) and write the bags coalesced.
+template <int LPR, int VPL>
 __global__ void __launch_bounds__(256) k_lookup_1hot(LookupArgs a) {
   constexpr int G = 32 / LPR;  // rows handled side by side by one warp
+  constexpr int kBatch = (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) > 0 ? (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) : 1;
   const uint32_t lane = lane_id();
   const uint32_t grp = lane / LPR, gl = lane % LPR;
   const uint32_t nvec = a.dim / 4;
@@ -265,38 +281,49 @@ __global__ void __launch_bounds__(256) k_lookup_1hot(LookupArgs a) {
       const TableDev td = a.tables[table];
       const uint32_t local = probe_find(a.slots, td, key);
       row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
-      if (a.occ_row) a.occ_row[bag] = local == kRowEmpty ? a.row_absent : row;
+      if (a.occ_scr) record_occurrence(a, bag, local, row);
     }
-#pragma unroll 4
-    for (int m = 0; m < LPR; ++m) {
-      const uint32_t src = grp + G * m;
-      const uint32_t r = __shfl_sync(0xffffffffu, row, src);
-      const uint32_t tb = __shfl_sync(0xffffffffu, table, src);
-      const uint64_t b = t0 + src;
-      if (b >= a.n_bags) continue;
-      const float4* p = reinterpret_cast<const float4*>(r == kRowEmpty ? a.defaults + uint64_t(tb) * a.dim
-                                                                       : a.W + uint64_t(r) * a.dim);
-      float4* o = reinterpret_cast<float4*>(a.out + b * a.dim);
-      for (uint32_t v = gl; v < nvec; v += LPR) {
-        // +0.0f + x (and /1.0f for mean) are the identity on every finite x except -0.0.
-        float4 x = ldg_stream(p + v);
-        x = f4_add(make_float4(0.f, 0.f, 0.f, 0.f), x);
-        o[v] = x;
+    for (int m0 = 0; m0 < LPR; m0 += kBatch) {
+      float4 x[kBatch][VPL];
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        const uint32_t src = grp + G * (m0 + j);
+        const uint32_t r = __shfl_sync(0xffffffffu, row, src);
+        const uint32_t tb = __shfl_sync(0xffffffffu, table, src);
+        const float4* p = reinterpret_cast<const float4*>(r == kRowEmpty ? a.defaults + uint64_t(tb) * a.dim
+                                                                         : a.W + uint64_t(r) * a.dim);
+        const bool ok = t0 + src < a.n_bags;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const uint32_t v = gl + k * LPR;
+          x[j][k] = (ok && v < nvec) ? ldg_stream(p + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        const uint64_t b = t0 + grp + G * (m0 + j);
+        if (b >= a.n_bags) continue;
+        float4* o = reinterpret_cast<float4*>(a.out + b * a.dim);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const uint32_t v = gl + k * LPR;
+          // +0.0f + x (and x / 1.0f for mean) is the identity on every finite x except -0.0
+          if (v < nvec) o[v] = f4_add(make_float4(0.f, 0.f, 0.f, 0.f), x[j][k]);
+        }
       }
     }
   }
 }
 
 // Multi-hot path: a group of LPR lanes owns one bag at a time; the group probes LPR
-// keys of the bag in parallel, then accumulates the rows in bag order.
-template <int LPR>
+// keys of the bag in parallel, then accumulates the rows in bag order (4 in flight).
+template <int LPR, int VPL>
 __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id();
   const uint32_t grp = lane / LPR, gl = lane % LPR;
   const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
   const uint32_t nvec = a.dim / 4;
-  constexpr int kMaxVpl = 8;  // dim <= 32*4*8 = 1024 on this path
   const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
   const uint64_t n_groups = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
   if (a.d_n && gid == 0 && gl == 0) *a.d_n = a.offsets[a.n_bags];
@@ -304,29 +331,41 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
     const uint32_t lo = a.offsets[bag], hi = a.offsets[bag + 1];
     const uint32_t table = a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
     const TableDev td = a.tables[table];
-    float4 acc[kMaxVpl];
+    float4 acc[VPL];
 #pragma unroll
-    for (int k = 0; k < kMaxVpl; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (uint32_t c = lo; c < hi; c += LPR) {
       const uint32_t i = c + gl;
       uint32_t row = kRowEmpty;
       if (i < hi) {
         const uint32_t local = probe_find(a.slots, td, a.keys[i]);
         row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
-        if (a.occ_row) {
-          a.occ_row[i] = local == kRowEmpty ? a.row_absent : row;
+        if (a.occ_scr) {
+          record_occurrence(a, i, local, row);
           a.occ_bag[i] = static_cast<uint32_t>(bag);
         }
       }
       const uint32_t cnt = min(uint32_t(LPR), hi - c);
-      for (uint32_t m = 0; m < cnt; ++m) {
-        const uint32_t r = __shfl_sync(gmask, row, grp * LPR + m);
-        const float4* p = reinterpret_cast<const float4*>(r == kRowEmpty ? a.defaults + uint64_t(table) * a.dim
-                                                                         : a.W + uint64_t(r) * a.dim);
+      for (uint32_t m0 = 0; m0 < cnt; m0 += 4) {
+        float4 x[4][VPL];
 #pragma unroll
-        for (int k = 0; k < kMaxVpl; ++k) {
-          const uint32_t v = gl + k * LPR;
-          if (v < nvec) acc[k] = f4_add(acc[k], ldg_stream(p + v));
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t m = m0 + j;
+          const uint32_t r = __shfl_sync(gmask, row, grp * LPR + (m < LPR ? m : 0));
+          const float4* p = reinterpret_cast<const float4*>(r == kRowEmpty ? a.defaults + uint64_t(table) * a.dim
+                                                                           : a.W + uint64_t(r) * a.dim);
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            const uint32_t v = gl + k * LPR;
+            x[j][k] = (m < cnt && v < nvec) ? ldg_stream(p + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (m0 + j < cnt) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) acc[k] = f4_add(acc[k], x[j][k]);
+          }
         }
       }
     }
@@ -335,205 +374,11 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
     float4* o = reinterpret_cast<float4*>(a.out + bag * a.dim);
     const float fl = static_cast<float>(len);
 #pragma unroll
-    for (int k = 0; k < kMaxVpl; ++k) {
+    for (int k = 0; k < VPL; ++k) {
       const uint32_t v = gl + k * LPR;
       if (v < nvec) o[v] = (a.mean && len > 0) ? f4_div(acc[k], fl) : acc[k];
     }
   }
-}
-
-// ---------------------------------------------------------------------------------
-// K4: dedup (segments of the row-sorted occurrence list) + chunk tasks
-// ---------------------------------------------------------------------------------
-struct SegScanOp {  // heads of equal-row runs -> seg_start[u]
-  const uint32_t* rows_sorted;
-  uint32_t* seg_start;
-  uint64_t* counts;  // [0]=N [1]=U
-  __device__ uint64_t size() const { return counts[0]; }
-  __device__ uint32_t count(uint64_t i) const {
-    return (i == 0 || rows_sorted[i] != rows_sorted[i - 1]) ? 1u : 0u;
-  }
-  __device__ void emit(uint64_t i, uint64_t excl, uint32_t c) const {
-    if (c) seg_start[excl] = static_cast<uint32_t>(i);
-  }
-  __device__ void total(uint64_t u) const {
-    counts[1] = u;
-    seg_start[u] = static_cast<uint32_t>(counts[0]);
-  }
-};
-
-struct TaskScanOp {  // ceil(len/kChunk) reduction tasks per segment
-  const uint32_t* seg_start;
-  uint32_t* task_off;
-  uint32_t* task_seg;
-  uint32_t* seg_done;
-  uint64_t* counts;  // [1]=U [2]=T
-  __device__ uint64_t size() const { return counts[1]; }
-  __device__ uint32_t count(uint64_t u) const {
-    const uint32_t len = seg_start[u + 1] - seg_start[u];
-    return (len + kChunk - 1) / kChunk;
-  }
-  __device__ void emit(uint64_t u, uint64_t excl, uint32_t c) const {
-    task_off[u] = static_cast<uint32_t>(excl);
-    seg_done[u] = 0;
-    for (uint32_t k = 0; k < c; ++k) task_seg[excl + k] = static_cast<uint32_t>(u);
-  }
-  __device__ void total(uint64_t t) const {
-    counts[2] = t;
-    task_off[counts[1]] = static_cast<uint32_t>(t);
-  }
-};
-
-struct ReduceArgs {
-  const uint32_t* rows_sorted;
-  const uint32_t* bags_sorted;
-  const uint32_t* seg_start;
-  const uint32_t* task_off;
-  const uint32_t* task_seg;
-  uint32_t* seg_done;
-  const uint64_t* counts;
-  const float* dout;
-  const uint32_t* bag_len;  // mean: length of each bag (nullptr: every bag has length 1)
-  int mean;
-  float* partial;  // [T x dim]
-  float* W;
-  float* S0;
-  float* S1;
-  int optimizer;
-  hps_opt_params opt;
-  uint32_t dim;
-  uint32_t row_absent;
-};
-
-template <int VPL>
-__device__ __forceinline__ void apply_opt(const ReduceArgs& a, uint32_t row, const float4 (&g)[VPL], uint32_t gl,
-                                          uint32_t lpr, uint32_t nvec) {
-  float4* w = reinterpret_cast<float4*>(a.W + uint64_t(row) * a.dim);
-  const float lr = a.opt.lr, eps = a.opt.eps;
-#pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const uint32_t v = gl + k * lpr;
-    if (v >= nvec) break;
-    float4 wv = w[v];
-    float* wf = reinterpret_cast<float*>(&wv);
-    const float* gf = reinterpret_cast<const float*>(&g[k]);
-    if (a.optimizer == HPS_OPT_SGD) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) wf[c] = __fsub_rn(wf[c], __fmul_rn(lr, gf[c]));
-    } else if (a.optimizer == HPS_OPT_ADAGRAD) {
-      float4* s = reinterpret_cast<float4*>(a.S0 + uint64_t(row) * a.dim);
-      float4 sv = s[v];
-      float* sf = reinterpret_cast<float*>(&sv);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        sf[c] = __fadd_rn(sf[c], __fmul_rn(gf[c], gf[c]));
-        wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(lr, gf[c]), __fadd_rn(__fsqrt_rn(sf[c]), eps)));
-      }
-      s[v] = sv;
-    } else {
-      float4* m = reinterpret_cast<float4*>(a.S0 + uint64_t(row) * a.dim);
-      float4* q = reinterpret_cast<float4*>(a.S1 + uint64_t(row) * a.dim);
-      float4 mv = m[v], qv = q[v];
-      float* mf = reinterpret_cast<float*>(&mv);
-      float* qf = reinterpret_cast<float*>(&qv);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        mf[c] = __fadd_rn(__fmul_rn(a.opt.beta1, mf[c]), __fmul_rn(a.opt.one_minus_beta1, gf[c]));
-        qf[c] = __fadd_rn(__fmul_rn(a.opt.beta2, qf[c]), __fmul_rn(a.opt.one_minus_beta2, __fmul_rn(gf[c], gf[c])));
-        wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(a.opt.lr_t, mf[c]), __fadd_rn(__fsqrt_rn(qf[c]), eps)));
-      }
-      m[v] = mv;
-      q[v] = qv;
-    }
-    w[v] = wv;
-  }
-}
-
-// K4+K5 fused: one LPR-lane group per reduction task (a chunk of <= kChunk occurrences
-// of one unique row). Single-chunk segments update their row directly; the last
-// finishing chunk of a multi-chunk segment sums the chunk partials in order and updates.
-template <int LPR, int VPL>
-__global__ void __launch_bounds__(256) k_reduce_update(ReduceArgs a) {
-  constexpr int G = 32 / LPR;
-  const uint32_t lane = lane_id();
-  const uint32_t grp = lane / LPR, gl = lane % LPR;
-  const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
-  const uint32_t nvec = a.dim / 4;
-  const uint64_t T = a.counts[2];
-  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
-  const uint64_t n_groups = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
-  for (uint64_t t = gid; t < T; t += n_groups) {
-    const uint32_t u = a.task_seg[t];
-    const uint32_t toff = a.task_off[u];
-    const uint32_t m = a.task_off[u + 1] - toff;
-    const uint32_t s0 = a.seg_start[u], s1 = a.seg_start[u + 1];
-    const uint32_t row = a.rows_sorted[s0];
-    if (row == a.row_absent) continue;
-    const uint32_t lo = s0 + (static_cast<uint32_t>(t) - toff) * kChunk;
-    const uint32_t hi = min(s1, lo + kChunk);
-    float4 acc[VPL];
-    for (uint32_t c = lo; c < hi; c += LPR) {
-      const uint32_t i = c + gl;
-      const uint32_t my_bag = i < hi ? a.bags_sorted[i] : 0u;
-      float my_len = 1.0f;
-      if (a.mean && i < hi) my_len = static_cast<float>(a.bag_len ? a.bag_len[my_bag] : 1u);
-      const uint32_t cnt = min(uint32_t(LPR), hi - c);
-      for (uint32_t q = 0; q < cnt; ++q) {
-        const uint32_t b = __shfl_sync(gmask, my_bag, grp * LPR + q);
-        const float fl = __shfl_sync(gmask, my_len, grp * LPR + q);
-        const float4* d = reinterpret_cast<const float4*>(a.dout + uint64_t(b) * a.dim);
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          const uint32_t v = gl + k * LPR;
-          if (v < nvec) {
-            float4 x = __ldg(d + v);
-            if (a.mean) x = f4_div(x, fl);
-            acc[k] = (c == lo && q == 0) ? x : f4_add(acc[k], x);
-          }
-        }
-      }
-    }
-    if (m == 1) {
-      apply_opt<VPL>(a, row, acc, gl, LPR, nvec);
-      continue;
-    }
-    float4* part = reinterpret_cast<float4*>(a.partial + uint64_t(t) * a.dim);
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const uint32_t v = gl + k * LPR;
-      if (v < nvec) __stcg(part + v, acc[k]);
-    }
-    __threadfence();
-    __syncwarp(gmask);
-    uint32_t prev = 0;
-    if (gl == 0) prev = atomicAdd(&a.seg_done[u], 1u);
-    prev = __shfl_sync(gmask, prev, grp * LPR);
-    if (prev != m - 1) continue;
-    __threadfence();
-    for (uint32_t j = 0; j < m; ++j) {
-      const float4* pj = reinterpret_cast<const float4*>(a.partial + uint64_t(toff + j) * a.dim);
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const uint32_t v = gl + k * LPR;
-        if (v < nvec) {
-          const float4 x = __ldcg(pj + v);
-          acc[k] = j == 0 ? x : f4_add(acc[k], x);
-        }
-      }
-    }
-    apply_opt<VPL>(a, row, acc, gl, LPR, nvec);
-  }
-}
-
-__global__ void k_unique_rows(const uint32_t* rows_sorted, const uint32_t* seg_start, const uint64_t* counts,
-                              uint32_t row_absent, uint32_t* out, uint64_t* count_out) {
-  const uint64_t U = counts[1];
-  const bool has_absent = U > 0 && rows_sorted[seg_start[U - 1]] == row_absent;
-  const uint64_t n = has_absent ? U - 1 : U;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count_out = n;
-  if (!out) return;
-  for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n; u += uint64_t(gridDim.x) * blockDim.x)
-    out[u] = rows_sorted[seg_start[u]];
 }
 
 int bits_for(uint64_t v) {
@@ -563,45 +408,6 @@ int dalloc(T** p, size_t count) {
 
 }  // namespace
 
-struct hps_gpu_table_s {
-  hps_gpu_ctx ctx = nullptr;
-  uint32_t n_tables = 0, dim = 0, n_slots = 0;
-  int optimizer = 0, n_state = 0;
-  uint64_t seed = 0;
-  float a0 = 0.f;
-  std::vector<uint64_t> row_cap, row_base, slot_cap, slot_base;
-  std::vector<TableDev> h_tables;
-  uint64_t total_rows = 0, total_slots = 0;
-  uint32_t row_absent = 0;
-  int sort_bits = 0;
-  uint64_t max_keys = 0, max_bags = 0;
-  // device state
-  TableDev* d_tables = nullptr;
-  Slot* d_slots = nullptr;
-  float *d_w = nullptr, *d_s0 = nullptr, *d_s1 = nullptr;
-  uint64_t* d_row_keys = nullptr;
-  uint64_t* d_nrows = nullptr;
-  float* d_defaults = nullptr;
-  uint32_t* d_slot_table = nullptr;
-  // per-batch workspaces (sized at create)
-  uint32_t *ws_rows_a = nullptr, *ws_rows_b = nullptr, *ws_bags_a = nullptr, *ws_bags_b = nullptr;
-  uint32_t* ws_occ_bag = nullptr;
-  uint32_t* ws_bag_len = nullptr;
-  uint32_t *ws_seg_start = nullptr, *ws_task_off = nullptr, *ws_task_seg = nullptr, *ws_seg_done = nullptr;
-  float* ws_partial = nullptr;
-  uint64_t* ws_counts = nullptr;  // [0]=N [1]=U [2]=T [3]=insert new-count
-  uint32_t* ws_zero = nullptr;     // sort + scan look-back words, memset per backward
-  size_t ws_zero_words = 0;
-  uint32_t* ws_abort = nullptr;
-  uint64_t* ws_keys_stage = nullptr;
-  uint32_t* ws_offsets_stage = nullptr;
-  // last training lookup
-  bool have_train = false, last_multi = false;
-  int last_combiner = 0;
-  uint64_t last_n_keys_host = 0;  // exact when known on the host, else max_keys
-  bool sorted_in_b = false;
-};
-
 namespace {
 
 int check_tbl(hps_gpu_table t) {
@@ -612,70 +418,40 @@ int check_tbl(hps_gpu_table t) {
   return HPS_GPU_OK;
 }
 
-// Words of the zeroed look-back region: sort workspace + 2 scans (status u64 each) + tickets.
-size_t zero_words(uint64_t max_keys, int passes) {
-  return sort_ws_words(max_keys, passes) + 2 * 2 * scan_tiles(max_keys + 1) + 8;
-}
+// (lanes per row, float4 per lane) for a row of nvec float4: LPR = largest power of two
+// <= min(32, nvec); VPL = ceil(nvec / LPR) (<= 8, so dim <= 1024).
+#define HPSG_DISPATCH_ROW(KERNEL, GRIDF, ...)                                    \
+  do {                                                                           \
+    if (nvec > 128) KERNEL<32, 8><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);       \
+    else if (nvec > 64) KERNEL<32, 4><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec > 32) KERNEL<32, 2><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec == 32) KERNEL<32, 1><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);  \
+    else if (nvec > 16) KERNEL<16, 2><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec == 16) KERNEL<16, 1><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);  \
+    else if (nvec > 8) KERNEL<8, 2><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);      \
+    else if (nvec == 8) KERNEL<8, 1><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);     \
+    else if (nvec > 4) KERNEL<4, 2><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);      \
+    else if (nvec == 4) KERNEL<4, 1><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);     \
+    else if (nvec > 2) KERNEL<2, 2><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);      \
+    else if (nvec == 2) KERNEL<2, 1><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);     \
+    else KERNEL<1, 1><<<GRIDF(1), 256, 0, st>>>(__VA_ARGS__);                    \
+  } while (0)
 
 int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi) {
   const cudaStream_t st = t->ctx->stream;
   const uint32_t nvec = t->dim / 4;
-  const int block = 256;
   if (!multi) {
-    const uint64_t warps = (a.n_bags + 31) / 32;
-    const int grid = grid_for(warps * 32, block, kNumSMs * 64);
-#define HPSG_L1(L) k_lookup_1hot<L><<<grid, block, 0, st>>>(a)
-    if (nvec >= 32) HPSG_L1(32);
-    else if (nvec >= 16) HPSG_L1(16);
-    else if (nvec >= 8) HPSG_L1(8);
-    else if (nvec >= 4) HPSG_L1(4);
-    else if (nvec >= 2) HPSG_L1(2);
-    else HPSG_L1(1);
-#undef HPSG_L1
+    auto grid1 = [&](int) { return grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * 64); };
+    HPSG_DISPATCH_ROW(k_lookup_1hot, grid1, a);
   } else {
-    auto groups_grid = [&](int lpr) {
-      const uint64_t groups_per_block = (block / 32) * (32 / lpr);
-      uint64_t g = (a.n_bags + groups_per_block - 1) / groups_per_block;
+    auto gridm = [&](int lpr) {
+      const uint64_t groups_per_block = 8 * (32 / lpr);
+      const uint64_t g = (a.n_bags + groups_per_block - 1) / groups_per_block;
       return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, kNumSMs * 64)));
     };
-#define HPSG_LM(L) k_lookup_multi<L><<<groups_grid(L), block, 0, st>>>(a)
-    if (nvec >= 32) HPSG_LM(32);
-    else if (nvec >= 16) HPSG_LM(16);
-    else if (nvec >= 8) HPSG_LM(8);
-    else if (nvec >= 4) HPSG_LM(4);
-    else if (nvec >= 2) HPSG_LM(2);
-    else HPSG_LM(1);
-#undef HPSG_LM
+    HPSG_DISPATCH_ROW(k_lookup_multi, gridm, a);
   }
   HPSG_CHECK_LAUNCH("lookup");
-  return HPS_GPU_OK;
-}
-
-template <int LPR, int VPL>
-void launch_reduce_t(const ReduceArgs& a, cudaStream_t st, uint64_t max_tasks) {
-  const uint64_t groups_per_block = 8 * (32 / LPR);
-  const uint64_t g = (max_tasks + groups_per_block - 1) / groups_per_block;
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, kNumSMs * 16)));
-  k_reduce_update<LPR, VPL><<<grid, 256, 0, st>>>(a);
-}
-
-int launch_reduce(hps_gpu_table t, const ReduceArgs& a, uint64_t max_tasks) {
-  const cudaStream_t st = t->ctx->stream;
-  const uint32_t nvec = t->dim / 4;
-  if (nvec > 32 * 8) {
-    set_last_error("dim > 1024 not supported by the reduce kernel");
-    return HPS_GPU_E_INVALID_ARGUMENT;
-  }
-  if (nvec > 128) launch_reduce_t<32, 8>(a, st, max_tasks);
-  else if (nvec > 64) launch_reduce_t<32, 4>(a, st, max_tasks);
-  else if (nvec > 32) launch_reduce_t<32, 2>(a, st, max_tasks);
-  else if (nvec > 16) launch_reduce_t<32, 1>(a, st, max_tasks);
-  else if (nvec > 8) launch_reduce_t<16, 1>(a, st, max_tasks);
-  else if (nvec > 4) launch_reduce_t<8, 1>(a, st, max_tasks);
-  else if (nvec > 2) launch_reduce_t<4, 1>(a, st, max_tasks);
-  else if (nvec > 1) launch_reduce_t<2, 1>(a, st, max_tasks);
-  else launch_reduce_t<1, 1>(a, st, max_tasks);
-  HPSG_CHECK_LAUNCH("reduce");
   return HPS_GPU_OK;
 }
 
@@ -737,9 +513,14 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   }
   t->total_rows = rows;
   t->total_slots = slots;
-  t->row_absent = static_cast<uint32_t>(rows);
-  t->sort_bits = std::max(1, bits_for(rows));
   const uint64_t D = t->dim, N = t->max_keys, B = t->max_bags;
+  t->scr_bits = std::max(10, bits_for(next_pow2(2 * N) - 1));
+  const uint64_t scr_cap = 1ull << t->scr_bits;
+  const uint64_t max_long = N / (kChunk + 1) + 2;
+  t->max_chunks = N / 16 + 2;
+  t->long_ctas = 2 * kNumSMs;
+  t->bitmap_words = (N + 31) / 32 + 1;
+  t->scan_words = scan_tiles(scr_cap) + 3;
   int st = HPS_GPU_OK;
   auto A = [&](int s) {
     if (s && !st) st = s;
@@ -753,20 +534,23 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->d_nrows, t->n_tables));
   A(dalloc(&t->d_defaults, uint64_t(t->n_tables) * D));
   A(dalloc(&t->d_slot_table, t->n_slots));
-  A(dalloc(&t->ws_rows_a, N));
-  A(dalloc(&t->ws_rows_b, N));
-  A(dalloc(&t->ws_bags_a, N));
-  A(dalloc(&t->ws_bags_b, N));
+  A(dalloc(&t->ws_scr, scr_cap));
+  A(dalloc(&t->ws_slot_u, scr_cap));
+  A(dalloc(&t->ws_occ_scr, N));
+  A(dalloc(&t->ws_occ_rank, N));
   A(dalloc(&t->ws_occ_bag, N));
+  A(dalloc(&t->ws_occ_list, N));
   A(dalloc(&t->ws_bag_len, B));
-  A(dalloc(&t->ws_seg_start, N + 2));
-  A(dalloc(&t->ws_task_off, N + 2));
-  A(dalloc(&t->ws_task_seg, N + 1));
-  A(dalloc(&t->ws_seg_done, N + 1));
-  A(dalloc(&t->ws_partial, N * D));
+  A(dalloc(&t->ws_seg_row, N + 1));
+  A(dalloc(&t->ws_seg_len, N + 1));
+  A(dalloc(&t->ws_seg_off, N + 1));
+  A(dalloc(&t->ws_long_seg, max_long));
+  A(dalloc(&t->ws_long_base, max_long));
+  A(dalloc(&t->ws_task_long, t->max_chunks));
+  A(dalloc(&t->ws_partial, t->max_chunks * D));
+  A(dalloc(&t->ws_bitmap, uint64_t(t->long_ctas) * t->bitmap_words));
   A(dalloc(&t->ws_counts, 8));
-  t->ws_zero_words = zero_words(N, (t->sort_bits + 7) / 8);
-  A(dalloc(&t->ws_zero, t->ws_zero_words));
+  A(dalloc(&t->ws_scan, t->scan_words));
   A(dalloc(&t->ws_abort, 4));
   A(dalloc(&t->ws_keys_stage, N));
   A(dalloc(&t->ws_offsets_stage, B + 1));
@@ -781,6 +565,8 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   HPSG_CUDA(cudaMemsetAsync(t->d_nrows, 0, t->n_tables * sizeof(uint64_t), s));
   HPSG_CUDA(cudaMemsetAsync(t->d_defaults, 0, uint64_t(t->n_tables) * D * sizeof(float), s));
   HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, 8 * sizeof(uint64_t), s));
+  HPSG_CUDA(cudaMemsetAsync(t->ws_bitmap, 0, uint64_t(t->long_ctas) * t->bitmap_words * 4, s));
+  k_fill_u64<<<grid_for(scr_cap, 256, kNumSMs * 8), 256, 0, s>>>(t->ws_scr, scr_cap, kScrEmpty);
   k_fill_slots_empty<<<grid_for(slots, 256, kNumSMs * 32), 256, 0, s>>>(t->d_slots, slots);
   HPSG_CHECK_LAUNCH("k_fill_slots_empty");
   HPSG_CUDA(cudaStreamSynchronize(s));  // the host arrays above are caller-owned
@@ -790,11 +576,12 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
 
 int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
-  void* ptrs[] = {t->d_tables,   t->d_slots,      t->d_w,         t->d_s0,         t->d_s1,
-                  t->d_row_keys, t->d_nrows,      t->d_defaults,  t->d_slot_table, t->ws_rows_a,
-                  t->ws_rows_b,  t->ws_bags_a,    t->ws_bags_b,   t->ws_occ_bag,   t->ws_bag_len,
-                  t->ws_seg_start, t->ws_task_off, t->ws_task_seg, t->ws_seg_done, t->ws_partial,
-                  t->ws_counts,  t->ws_zero,      t->ws_abort,    t->ws_keys_stage, t->ws_offsets_stage};
+  void* ptrs[] = {t->d_tables,     t->d_slots,       t->d_w,          t->d_s0,          t->d_s1,
+                  t->d_row_keys,   t->d_nrows,       t->d_defaults,   t->d_slot_table,  t->ws_scr,
+                  t->ws_slot_u,    t->ws_occ_scr,    t->ws_occ_rank,  t->ws_occ_bag,    t->ws_occ_list,
+                  t->ws_bag_len,   t->ws_seg_row,    t->ws_seg_len,   t->ws_seg_off,    t->ws_long_seg,
+                  t->ws_long_base, t->ws_task_long,  t->ws_partial,   t->ws_bitmap,     t->ws_counts,
+                  t->ws_scan,      t->ws_abort,      t->ws_keys_stage, t->ws_offsets_stage};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -941,104 +728,25 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   a.dim = t->dim;
   a.mean = combiner == HPS_COMBINER_MEAN;
   a.out = out;
-  a.row_absent = t->row_absent;
   if (train) {
-    a.occ_row = t->ws_rows_a;
+    if (t->scr_dirty) {  // a previous training lookup was never consumed by a backward
+      const uint64_t cap = 1ull << t->scr_bits;
+      k_fill_u64<<<grid_for(cap, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_scr, cap, kScrEmpty);
+    }
+    a.scr = t->ws_scr;
+    a.scr_bits = t->scr_bits;
+    a.occ_scr = t->ws_occ_scr;
+    a.occ_rank = t->ws_occ_rank;
     a.occ_bag = multi ? t->ws_occ_bag : nullptr;
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
     a.d_n = t->ws_counts;
   }
   if (int s = launch_lookup(t, a, multi)) return s;
   t->have_train = train;
+  t->scr_dirty = train;
   t->last_multi = multi;
   t->last_combiner = combiner;
   t->last_n_keys_host = n_keys_host;
-  return HPS_GPU_OK;
-}
-
-int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_params* opt) {
-  if (int s = check_tbl(t)) return s;
-  if (!opt) return HPS_GPU_E_INVALID_ARGUMENT;
-  if (!t->have_train) {
-    set_last_error("backward_update: no preceding lookup_pooled with HPS_LOOKUP_TRAIN");
-    return HPS_GPU_E_INVALID_ARGUMENT;
-  }
-  if (!d_out) return HPS_GPU_E_INVALID_ARGUMENT;
-  cudaStream_t st = t->ctx->stream;
-  const uint64_t nk = t->last_n_keys_host;
-  const int passes = (t->sort_bits + 7) / 8;
-  uint32_t* z = t->ws_zero;
-  const size_t sort_words = sort_ws_words(nk, passes);
-  const uint64_t tiles = scan_tiles(nk + 1);
-  uint64_t* scan1 = reinterpret_cast<uint64_t*>(z + ((sort_words + 1) & ~size_t(1)));
-  uint64_t* scan2 = scan1 + tiles;
-  uint32_t* tickets = reinterpret_cast<uint32_t*>(scan2 + tiles);
-  const size_t used_words = reinterpret_cast<uint32_t*>(tickets + 4) - z;
-  HPSG_CUDA(cudaMemsetAsync(z, 0, used_words * sizeof(uint32_t), st));
-  // K4a: stable sort of (global row, bag) by row. Identity payload for one-hot bags.
-  cudaError_t err;
-  const uint32_t* bag_in = t->last_multi ? t->ws_occ_bag : nullptr;
-  // sort workspace lives at the head of the zeroed region (already cleared above)
-  {
-    const uint64_t stiles = sort_tiles(nk);
-    uint32_t* hist = z;
-    uint32_t* stick = z + 4 * 256;
-    uint32_t* status = stick + 4;
-    k_radix_hist<<<grid_for(nk, 256, kNumSMs * 2), 256, 0, st>>>(t->ws_rows_a, t->ws_counts, passes, hist);
-    const uint32_t* kin = t->ws_rows_a;
-    const uint32_t* vin = bag_in;
-    bool in_b = false;
-    for (int p = 0; p < passes; ++p) {
-      uint32_t* kout = in_b ? t->ws_rows_a : t->ws_rows_b;
-      uint32_t* vout = in_b ? t->ws_bags_a : t->ws_bags_b;
-      k_radix_pass<<<static_cast<unsigned>(stiles), kSortBlock, 0, st>>>(
-          kin, vin, kout, vout, t->ws_counts, 8 * p, hist + 256 * p, status + size_t(p) * stiles * 256, stick + p);
-      kin = kout;
-      vin = vout;
-      in_b = !in_b;
-    }
-    t->sorted_in_b = in_b;
-    err = cudaGetLastError();
-    if (err != cudaSuccess) return cuda_status(err, "radix sort");
-  }
-  const uint32_t* rows_sorted = t->sorted_in_b ? t->ws_rows_b : t->ws_rows_a;
-  const uint32_t* bags_sorted = t->sorted_in_b ? t->ws_bags_b : t->ws_bags_a;
-  // K4b: segments (unique rows) and chunk tasks.
-  SegScanOp sop{rows_sorted, t->ws_seg_start, t->ws_counts};
-  k_scan<SegScanOp><<<static_cast<unsigned>(scan_tiles(nk)), kScanBlock, 0, st>>>(sop, scan1, tickets);
-  TaskScanOp top{t->ws_seg_start, t->ws_task_off, t->ws_task_seg, t->ws_seg_done, t->ws_counts};
-  k_scan<TaskScanOp><<<static_cast<unsigned>(scan_tiles(nk)), kScanBlock, 0, st>>>(top, scan2, tickets + 1);
-  HPSG_CHECK_LAUNCH("dedup scans");
-  // K4c + K5: blocked reduction fused with the optimizer.
-  ReduceArgs ra{};
-  ra.rows_sorted = rows_sorted;
-  ra.bags_sorted = bags_sorted;
-  ra.seg_start = t->ws_seg_start;
-  ra.task_off = t->ws_task_off;
-  ra.task_seg = t->ws_task_seg;
-  ra.seg_done = t->ws_seg_done;
-  ra.counts = t->ws_counts;
-  ra.dout = d_out;
-  ra.mean = t->last_combiner == HPS_COMBINER_MEAN && t->last_multi;
-  ra.bag_len = ra.mean ? t->ws_bag_len : nullptr;
-  ra.partial = t->ws_partial;
-  ra.W = t->d_w;
-  ra.S0 = t->d_s0;
-  ra.S1 = t->d_s1;
-  ra.optimizer = t->optimizer;
-  ra.opt = *opt;
-  ra.dim = t->dim;
-  ra.row_absent = t->row_absent;
-  return launch_reduce(t, ra, nk);
-}
-
-int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* unique_rows_out) {
-  if (int s = check_tbl(t)) return s;
-  if (!count_out) return HPS_GPU_E_INVALID_ARGUMENT;
-  const uint32_t* rows_sorted = t->sorted_in_b ? t->ws_rows_b : t->ws_rows_a;
-  k_unique_rows<<<grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0, t->ctx->stream>>>(
-      rows_sorted, t->ws_seg_start, t->ws_counts, t->row_absent, unique_rows_out, count_out);
-  HPSG_CHECK_LAUNCH("k_unique_rows");
   return HPS_GPU_OK;
 }
 

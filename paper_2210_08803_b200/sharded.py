@@ -60,9 +60,8 @@ class TrainStep:
         self.params = opt_params(cfg.optimizer, cfg.lr, eps=cfg.eps)
         self.graph_mode = bool(use_graph and world == 1 and cfg.optimizer != "adam")
         self._graphs = {}
-        bits = max(1, int(sum(table.row_capacity)).bit_length())
-        passes = (bits + 7) // 8
-        self.kernels_per_step = 1 + 1 + passes + 2 + 1
+        # lookup + dedup scan + scatter + short reduce + long sort/chunks/combine
+        self.kernels_per_step = 7
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.exchange = None
         if world > 1:

@@ -225,3 +225,50 @@ def test_config1_full_size_parity(ctx):
         _one_hot_round(ctx, g, o, keys, cfg.batch, rs, "sgd", steps=1, lr=cfg.lr)
     w = g.export(0, 0, cfg.cards[0])[0].cpu().numpy()
     assert close(w, o.export(0, 0, cfg.cards[0])[0])
+
+
+@pytest.mark.parametrize("opt", ["sgd", "adam"])
+def test_skewed_segments_all_paths(ctx, opt):
+    """Segment lengths 1, 2, 3..32 (warp bitonic), 33..4096 (CTA smem sort) and > 4096
+    (bitmap walk), in one batch, one key per bag, through every backward kernel."""
+    rs = np.random.default_rng(21)
+    g, o = make_pair(ctx, [100000], 16, [0], opt, max_keys=1 << 17, max_bags=1 << 17)
+    pool = rs.integers(0, 2**63, 100000).astype(np.uint64)
+    g.insert(0, t64(pool))
+    o.insert(0, pool)
+    parts = [np.repeat(pool[0], 20000), np.repeat(pool[1], 4097), np.repeat(pool[2], 4096), np.repeat(pool[3], 33),
+             np.repeat(pool[4:40], 32), np.repeat(pool[40:90], 3), np.repeat(pool[90:300], 2), pool[300:20000]]
+    keys = np.concatenate(parts)
+    keys = keys[rs.permutation(len(keys))]
+    for step in range(1, 3):
+        out = g.lookup(t64(keys), len(keys), train=True)
+        ref = o.lookup(keys, len(keys), train=True)
+        close(out.cpu().numpy(), ref)
+        dout = rs.standard_normal(ref.shape).astype(np.float32)
+        p = opt_params(opt, 0.01, step=step)
+        g.backward_update(torch.from_numpy(dout).cuda(), 0.01, params=p)
+        o.backward_update(dout, p)
+        ctx.sync()
+        np.testing.assert_array_equal(g.last_unique().cpu().numpy().view(np.uint32), o.last_unique())
+    w = g.export(0, 0, 100000)[0].cpu().numpy()
+    assert close(w, o.export(0, 0, 100000)[0])
+
+
+def test_train_lookup_twice_without_backward(ctx):
+    """A training lookup whose gradients are never applied must not leak into the next step."""
+    rs = np.random.default_rng(8)
+    g, o = make_pair(ctx, [500], 16, [0])
+    pool = rs.integers(0, 2**63, 500).astype(np.uint64)
+    g.insert(0, t64(pool))
+    o.insert(0, pool)
+    k1 = rs.choice(pool, 300)
+    g.lookup(t64(k1), 300, train=True)
+    k2 = rs.choice(pool, 400)
+    g.lookup(t64(k2), 400, train=True)
+    o.lookup(k2, 400, train=True)
+    d = rs.standard_normal((400, 16)).astype(np.float32)
+    p = opt_params("sgd", 0.1)
+    g.backward_update(torch.from_numpy(d).cuda(), 0.1, params=p)
+    o.backward_update(d, p)
+    ctx.sync()
+    assert close(g.export(0, 0, 500)[0].cpu().numpy(), o.export(0, 0, 500)[0])
