@@ -151,8 +151,8 @@ inline uint64_t scan_tiles(uint64_t n_max) { return (n_max + kScanTile - 1) / kS
 // Stable LSD radix sort of (u32 key, u32 value) pairs, 8-bit digits.
 // ---------------------------------------------------------------------------------
 constexpr int kSortBlock = 256;
-constexpr int kSortIPT = 16;
-constexpr int kSortTile = kSortBlock * kSortIPT;  // 4096 items
+constexpr int kSortIPT = 8;
+constexpr int kSortTile = kSortBlock * kSortIPT;  // 2048 items
 constexpr int kSortWarps = kSortBlock / 32;
 constexpr uint32_t kSortAgg = 1u << 30;
 constexpr uint32_t kSortInc = 2u << 30;
@@ -246,11 +246,24 @@ static __global__ void __launch_bounds__(kSortBlock) k_radix_pass(const uint32_t
   s_doff[d] = lstart;
   uint32_t prefix = 0;
   if (tile > 0) {
-    for (int64_t p = static_cast<int64_t>(tile) - 1; p >= 0; --p) {
-      uint32_t s;
-      do { s = ld_vol32(&status[p * 256 + d]); } while ((s & ~kSortVal) == 0);
-      prefix += s & kSortVal;
-      if (s & kSortInc) break;
+    // Batched look-back: 16 predecessor words per round are loaded together, so a chain
+    // of tiles that have only published aggregates costs ceil(k/16) L2 round trips.
+    constexpr int kLB = 16;
+    int64_t p = static_cast<int64_t>(tile) - 1;
+    bool done = false;
+    while (!done) {
+      uint32_t sv[kLB];
+#pragma unroll
+      for (int q = 0; q < kLB; ++q) sv[q] = (p - q >= 0) ? ld_vol32(&status[(p - q) * 256 + d]) : kSortInc;
+#pragma unroll
+      for (int q = 0; q < kLB; ++q) {
+        if (done) break;
+        uint32_t s = sv[q];
+        while ((s & ~kSortVal) == 0) s = ld_vol32(&status[(p - q) * 256 + d]);  // not yet published
+        prefix += s & kSortVal;
+        done = (s & kSortInc) != 0;
+      }
+      p -= kLB;
     }
     st_vol32(&status[tile * 256 + d], kSortInc | (prefix + cnt));
   }

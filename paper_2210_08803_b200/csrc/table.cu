@@ -241,21 +241,16 @@ struct LookupArgs {
   uint32_t dim;
   int mean;
   float* out;
-  // training only: fused dedup insert (table_internal.cuh) + per-occurrence records
-  uint64_t* scr;
-  int scr_bits;
-  uint32_t* occ_scr;   // dedup slot of each occurrence (kNoScr: key absent -> no gradient)
-  uint32_t* occ_rank;  // arrival rank of the occurrence among its key's occurrences
+  // training only: per-occurrence records consumed by backward.cu
+  uint32_t* occ_row;   // global row of each occurrence (row_absent: key absent -> no gradient)
+  uint32_t row_absent;
   uint32_t* occ_bag;   // multi-hot: bag of each occurrence
   uint32_t* bag_len;   // multi-hot mean: bag lengths
   uint64_t* d_n;       // number of key occurrences (device)
 };
 
 __device__ __forceinline__ void record_occurrence(const LookupArgs& a, uint64_t i, uint32_t local, uint32_t row) {
-  uint32_t slot = kNoScr, rank = 0;
-  if (local != kRowEmpty) scr_insert(a.scr, a.scr_bits, row, &slot, &rank);
-  a.occ_scr[i] = slot;
-  a.occ_rank[i] = rank;
+  a.occ_row[i] = local == kRowEmpty ? a.row_absent : row;
 }
 
 // One-key-per-bag path. A warp owns 32 consecutive bags: every lane hashes and probes
@@ -281,7 +276,7 @@ __global__ void __launch_bounds__(256) k_lookup_1hot(LookupArgs a) {
       const TableDev td = a.tables[table];
       const uint32_t local = probe_find(a.slots, td, key);
       row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
-      if (a.occ_scr) record_occurrence(a, bag, local, row);
+      if (a.occ_row) record_occurrence(a, bag, local, row);
     }
     for (int m0 = 0; m0 < LPR; m0 += kBatch) {
       float4 x[kBatch][VPL];
@@ -340,7 +335,7 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
       if (i < hi) {
         const uint32_t local = probe_find(a.slots, td, a.keys[i]);
         row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
-        if (a.occ_scr) {
+        if (a.occ_row) {
           record_occurrence(a, i, local, row);
           a.occ_bag[i] = static_cast<uint32_t>(bag);
         }
@@ -514,13 +509,12 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->total_rows = rows;
   t->total_slots = slots;
   const uint64_t D = t->dim, N = t->max_keys, B = t->max_bags;
-  t->scr_bits = std::max(10, bits_for(next_pow2(2 * N) - 1));
-  const uint64_t scr_cap = 1ull << t->scr_bits;
-  const uint64_t max_long = N / (kChunk + 1) + 2;
-  t->max_chunks = N / 16 + 2;
-  t->long_ctas = 2 * kNumSMs;
-  t->bitmap_words = (N + 31) / 32 + 1;
-  t->scan_words = scan_tiles(scr_cap) + 3;
+  t->row_absent = static_cast<uint32_t>(rows);
+  t->sort_bits = std::max(1, bits_for(rows));
+  t->max_long = N / (kItemW + 1) + 2;
+  t->max_chunks = bwd_max_chunks(N);
+  t->max_pieces = bwd_max_pieces(N);
+  t->zero_words = bwd_zero_words(N, (t->sort_bits + 7) / 8);
   int st = HPS_GPU_OK;
   auto A = [&](int s) {
     if (s && !st) st = s;
@@ -534,23 +528,21 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->d_nrows, t->n_tables));
   A(dalloc(&t->d_defaults, uint64_t(t->n_tables) * D));
   A(dalloc(&t->d_slot_table, t->n_slots));
-  A(dalloc(&t->ws_scr, scr_cap));
-  A(dalloc(&t->ws_slot_u, scr_cap));
-  A(dalloc(&t->ws_occ_scr, N));
-  A(dalloc(&t->ws_occ_rank, N));
+  A(dalloc(&t->ws_rows_a, N));
+  A(dalloc(&t->ws_rows_b, N));
+  A(dalloc(&t->ws_bags_a, N));
+  A(dalloc(&t->ws_bags_b, N));
   A(dalloc(&t->ws_occ_bag, N));
-  A(dalloc(&t->ws_occ_list, N));
   A(dalloc(&t->ws_bag_len, B));
-  A(dalloc(&t->ws_seg_row, N + 1));
-  A(dalloc(&t->ws_seg_len, N + 1));
-  A(dalloc(&t->ws_seg_off, N + 1));
-  A(dalloc(&t->ws_long_seg, max_long));
-  A(dalloc(&t->ws_long_base, max_long));
-  A(dalloc(&t->ws_task_long, t->max_chunks));
+  A(dalloc(&t->ws_seg_start, N + 1));
+  A(dalloc(&t->ws_seg_end, N + 1));
+  A(dalloc(&t->ws_occ_seg, N));
+  A(dalloc(&t->ws_long_seg, t->max_long));
+  A(dalloc(&t->ws_long_base, t->max_long));
+  A(dalloc(&t->ws_pieces, 2 * t->max_pieces));
   A(dalloc(&t->ws_partial, t->max_chunks * D));
-  A(dalloc(&t->ws_bitmap, uint64_t(t->long_ctas) * t->bitmap_words));
   A(dalloc(&t->ws_counts, 8));
-  A(dalloc(&t->ws_scan, t->scan_words));
+  A(dalloc(&t->ws_zero, t->zero_words));
   A(dalloc(&t->ws_abort, 4));
   A(dalloc(&t->ws_keys_stage, N));
   A(dalloc(&t->ws_offsets_stage, B + 1));
@@ -565,8 +557,6 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   HPSG_CUDA(cudaMemsetAsync(t->d_nrows, 0, t->n_tables * sizeof(uint64_t), s));
   HPSG_CUDA(cudaMemsetAsync(t->d_defaults, 0, uint64_t(t->n_tables) * D * sizeof(float), s));
   HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, 8 * sizeof(uint64_t), s));
-  HPSG_CUDA(cudaMemsetAsync(t->ws_bitmap, 0, uint64_t(t->long_ctas) * t->bitmap_words * 4, s));
-  k_fill_u64<<<grid_for(scr_cap, 256, kNumSMs * 8), 256, 0, s>>>(t->ws_scr, scr_cap, kScrEmpty);
   k_fill_slots_empty<<<grid_for(slots, 256, kNumSMs * 32), 256, 0, s>>>(t->d_slots, slots);
   HPSG_CHECK_LAUNCH("k_fill_slots_empty");
   HPSG_CUDA(cudaStreamSynchronize(s));  // the host arrays above are caller-owned
@@ -576,12 +566,13 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
 
 int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
-  void* ptrs[] = {t->d_tables,     t->d_slots,       t->d_w,          t->d_s0,          t->d_s1,
-                  t->d_row_keys,   t->d_nrows,       t->d_defaults,   t->d_slot_table,  t->ws_scr,
-                  t->ws_slot_u,    t->ws_occ_scr,    t->ws_occ_rank,  t->ws_occ_bag,    t->ws_occ_list,
-                  t->ws_bag_len,   t->ws_seg_row,    t->ws_seg_len,   t->ws_seg_off,    t->ws_long_seg,
-                  t->ws_long_base, t->ws_task_long,  t->ws_partial,   t->ws_bitmap,     t->ws_counts,
-                  t->ws_scan,      t->ws_abort,      t->ws_keys_stage, t->ws_offsets_stage};
+  void* ptrs[] = {t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
+                  t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
+                  t->ws_rows_b,   t->ws_bags_a,    t->ws_bags_b,    t->ws_occ_bag,    t->ws_bag_len,
+                  t->ws_seg_start, t->ws_seg_end,  t->ws_long_seg,  t->ws_long_base,  t->ws_pieces,
+                  t->ws_occ_seg,
+                  t->ws_partial,  t->ws_counts,    t->ws_zero,      t->ws_abort,      t->ws_keys_stage,
+                  t->ws_offsets_stage};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -729,21 +720,14 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   a.mean = combiner == HPS_COMBINER_MEAN;
   a.out = out;
   if (train) {
-    if (t->scr_dirty) {  // a previous training lookup was never consumed by a backward
-      const uint64_t cap = 1ull << t->scr_bits;
-      k_fill_u64<<<grid_for(cap, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_scr, cap, kScrEmpty);
-    }
-    a.scr = t->ws_scr;
-    a.scr_bits = t->scr_bits;
-    a.occ_scr = t->ws_occ_scr;
-    a.occ_rank = t->ws_occ_rank;
+    a.occ_row = t->ws_rows_a;
+    a.row_absent = t->row_absent;
     a.occ_bag = multi ? t->ws_occ_bag : nullptr;
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
     a.d_n = t->ws_counts;
   }
   if (int s = launch_lookup(t, a, multi)) return s;
   t->have_train = train;
-  t->scr_dirty = train;
   t->last_multi = multi;
   t->last_combiner = combiner;
   t->last_n_keys_host = n_keys_host;
