@@ -208,8 +208,9 @@ inline void apply_optimizer(int optimizer, float* w, float* s0, float* s1, uint3
 }
 
 // per-occurrence gradient, dedup by row (stable in occurrence order),
-// blocked reduction (chunks of kChunk summed sequentially, then the chunk partials
-// summed sequentially), then the optimizer on each unique row. `row_ptr(row, k)` gives
+// kChunk-ary blocked tree reduction (chunks of kChunk summed sequentially; the list of
+// chunk partials reduced the same way until one remains — plain sequential order for
+// <= kChunk occurrences), then the optimizer on each unique row. `row_ptr(row, k)` gives
 // the weight (k=0) and state (k=1,2) row of a global row id.
 template <class RowPtr>
 void reduce_and_update(const std::vector<uint64_t>& occ_row, const std::vector<uint32_t>& occ_bag,
@@ -250,6 +251,8 @@ void reduce_and_update(const std::vector<uint64_t>& occ_row, const std::vector<u
           for (uint32_t j = 0; j < D; ++j) dst[j] = d[j];
         }
       };
+      // Level 1: chunks of kChunk occurrences, each summed sequentially from its first element.
+      std::vector<float> level;  // partials, D floats each
       for (uint64_t c = lo; c < hi; c += kChunk) {
         const uint64_t ce = std::min<uint64_t>(hi, c + kChunk);
         grad_of(order[c], part.data());
@@ -257,12 +260,23 @@ void reduce_and_update(const std::vector<uint64_t>& occ_row, const std::vector<u
           grad_of(order[i], gi.data());
           for (uint32_t j = 0; j < D; ++j) part[j] = part[j] + gi[j];
         }
-        if (c == lo) {
-          acc = part;
-        } else {
-          for (uint32_t j = 0; j < D; ++j) acc[j] = acc[j] + part[j];
-        }
+        level.insert(level.end(), part.begin(), part.end());
       }
+      // Levels 2..: the partial list is reduced the same way (chunks of kChunk, sequential)
+      // until one vector remains — a kChunk-ary blocked tree in canonical order.
+      while (level.size() > D) {
+        const uint64_t m = level.size() / D;
+        std::vector<float> next;
+        for (uint64_t c = 0; c < m; c += kChunk) {
+          const uint64_t ce = std::min<uint64_t>(m, c + kChunk);
+          std::copy(level.begin() + c * D, level.begin() + (c + 1) * D, part.begin());
+          for (uint64_t i = c + 1; i < ce; ++i)
+            for (uint32_t j = 0; j < D; ++j) part[j] = part[j] + level[i * D + j];
+          next.insert(next.end(), part.begin(), part.end());
+        }
+        level.swap(next);
+      }
+      std::copy(level.begin(), level.end(), acc.begin());
       const uint64_t r = occ_row[order[lo]];
       apply_optimizer(optimizer, row_ptr(r, 0), row_ptr(r, 1), row_ptr(r, 2), D, acc.data(), p);
     }

@@ -1,25 +1,24 @@
 // backward.cu — K4 dedup + blocked segmented reduction and K5 fused sparse optimizers.
 //
 // Semantics (oracle/oracle.cpp reduce_and_update): every key
-// occurrence receives d_out[bag] (or d_out[bag]/len for mean); occurrences of one key
-// are taken in canonical (occurrence) order, summed in chunks of 32 from the first
-// element, the chunk partials summed in order; then SGD / AdaGrad / Adam update the row.
+// occurrence receives d_out[bag] (or d_out[bag]/len for mean); the occurrences of one
+// key are taken in canonical (occurrence) order and reduced by a 32-ary blocked tree:
+// chunks of 32 summed sequentially from their first element, the chunk partials reduced
+// the same way until one vector remains (plain sequential order up to 32 occurrences).
+// Then SGD / AdaGrad / Adam update the row in place.
 //
-// Pipeline (sizes device-resident: one memset node + 6 + passes kernels, graph-capturable):
-//   k_radix_hist/k_radix_pass : stable LSD sort of (row, bag) by row — the dedup, and the
-//                               stability keeps each key's occurrences in canonical order
-//   k_scan<SegOp>    : unique-row segments [start, end) + occurrence -> segment
-//   k_list_long      : segments longer than kItemW (or absent keys) are cut into
-//                      chunk-aligned pieces of kItemW occurrences; their occurrences are
-//                      flagged so the short items skip them
-//   k_stream         : persistent blocks take work items — kItemW-wide windows of the
-//                      sorted list (short segments) or long pieces — stage d_out rows in
-//                      shared memory with coalesced 128-bit loads, run the blocked ordered
-//                      sums column-parallel from smem, and apply the optimizer to every
-//                      finished segment in batched warp passes (long pieces emit chunk
-//                      partials instead). Work is balanced by OCCURRENCES, so hot keys
-//                      cannot serialise a warp.
-//   k_long_combine   : one CTA per long segment: chunk partials in order + optimizer
+// Pipeline (sizes device-resident: one memset node + 5 + passes kernels, graph-capturable):
+//   k_radix_hist/k_radix_pass : stable LSD sort of (row, bag) by row — the dedup; stability
+//                               keeps each key's occurrences in canonical order
+//   k_scan<SegOp>   : unique-row segments [start, end) of the sorted list
+//   k_reduce_short  : a warp owns 32 segments — lane l loads segment l's metadata and first
+//                     two bags in one round trip — then its lane groups update the
+//                     segments four at a time (weights/state + gradient rows in flight
+//                     together). Segments longer than 32 are listed (warp-cooperatively)
+//                     as 32-occurrence chunk tasks for:
+//   k_long_chunks   : one warp per chunk -> level-1 partial (L2)
+//   k_long_combine  : one CTA per long segment: higher tree levels (8 warps in parallel per
+//                     level, ping-pong between two scratch regions), then the optimizer
 #include <algorithm>
 #include <cstring>
 
@@ -31,32 +30,22 @@ using namespace hpsg;
 
 namespace {
 
-constexpr uint32_t kSkip = 0x80000000u;  // occ_seg flag: owned by a long piece / absent key
-constexpr uint32_t kSegMask = 0x7fffffffu;
-constexpr int kStreamBlock = 256;
-constexpr uint32_t kMaxTile = 128;
-
 struct BwdArgs {
   const uint64_t* counts;  // [0]=N occurrences [1]=U segments
   const uint32_t* rows;    // sorted global rows
   const uint32_t* bags;    // bag of each sorted occurrence
   uint32_t* seg_start;
   uint32_t* seg_end;
-  uint32_t* occ_seg;
   uint32_t row_absent;
   const uint32_t* bag_len;  // mean combiner: bag lengths (nullptr: sum)
   const float* dout;
   uint32_t dim;
   uint32_t* long_seg;
   uint32_t* long_base;
-  uint32_t* pieces;
-  unsigned long long* long_packed;  // (n_long << 32) | total long chunks
-  unsigned long long* piece_count;
-  unsigned long long* item_ticket;
-  uint64_t n_short_items;
-  uint32_t tile;  // occurrences staged per smem tile
-  float* partial;
-  uint32_t combine_batch;
+  uint32_t* task_long;
+  unsigned long long* long_packed;  // (n_long << 32) | total level-1 chunks
+  float* partial;                   // level-1 partials [max_chunks x dim]
+  float* partial2;                  // higher levels [max_chunks/32 + max_long x dim]
   float* W;
   float* S0;
   float* S1;
@@ -69,60 +58,15 @@ struct SegOp {
   const uint32_t* rows;
   uint32_t* seg_start;
   uint32_t* seg_end;
-  uint32_t* occ_seg;
   uint64_t* counts;
   __device__ uint64_t size() const { return counts[0]; }
   __device__ uint32_t count(uint64_t i) const { return (i == 0 || rows[i] != rows[i - 1]) ? 1u : 0u; }
   __device__ void emit(uint64_t i, uint64_t excl, uint64_t c) const {
-    const uint32_t u = static_cast<uint32_t>(excl + c - 1);
-    if (c) seg_start[u] = static_cast<uint32_t>(i);
-    occ_seg[i] = u;
-    if (i + 1 == counts[0] || rows[i + 1] != rows[i]) seg_end[u] = static_cast<uint32_t>(i + 1);
+    if (c) seg_start[excl] = static_cast<uint32_t>(i);
+    if (i + 1 == counts[0] || rows[i + 1] != rows[i]) seg_end[excl + c - 1] = static_cast<uint32_t>(i + 1);
   }
   __device__ void total(uint64_t u) const { counts[1] = u; }
 };
-
-// ---- long segments -> pieces ----------------------------------------------------------
-// A warp inspects 32 segments (one per lane); long or absent ones are handed out as
-// pieces and their occurrences flagged by the whole warp (coalesced).
-__global__ void __launch_bounds__(256) k_list_long(BwdArgs a) {
-  const uint32_t lane = lane_id();
-  const uint64_t U = a.counts[1];
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
-    const uint64_t u = u0 + lane;
-    uint32_t s = 0, e = 0;
-    bool flag = false;
-    if (u < U) {
-      s = a.seg_start[u];
-      e = a.seg_end[u];
-      const bool absent = a.rows[s] == a.row_absent;
-      const uint32_t len = e - s;
-      flag = absent || len > kItemW;
-      if (!absent && len > kItemW) {
-        const uint32_t m = (len + kChunk - 1) / kChunk;
-        const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
-        const uint32_t j = static_cast<uint32_t>(p >> 32);
-        a.long_seg[j] = static_cast<uint32_t>(u);
-        a.long_base[j] = static_cast<uint32_t>(p);
-        const uint32_t np = (len + kItemW - 1) / kItemW;
-        const uint32_t p0 = static_cast<uint32_t>(atomicAdd(a.piece_count, static_cast<unsigned long long>(np)));
-        for (uint32_t k = 0; k < np; ++k) {
-          a.pieces[2 * (p0 + k)] = j;
-          a.pieces[2 * (p0 + k) + 1] = k;
-        }
-      }
-    }
-    uint32_t todo = __ballot_sync(0xffffffffu, flag);
-    while (todo) {
-      const int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t ss = __shfl_sync(0xffffffffu, s, src), ee = __shfl_sync(0xffffffffu, e, src);
-      for (uint32_t o = ss + lane; o < ee; o += 32) a.occ_seg[o] |= kSkip;
-    }
-  }
-}
 
 // ---- row math --------------------------------------------------------------------------
 template <int VPL>
@@ -184,198 +128,269 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
   }
 }
 
-// ---- the streaming reduction -----------------------------------------------------------
-// CPT: columns (floats) per thread in the ordered-sum phase (dim <= 256 * CPT).
-// VPL: float4 per lane in the optimizer phase (dim <= 128 * VPL).
-template <int CPT, int VPL>
-__global__ void __launch_bounds__(kStreamBlock) k_stream(BwdArgs a) {
-  extern __shared__ float s_tile[];  // [tile][dim] gradient rows, then finished-segment totals
-  __shared__ uint32_t s_row[kMaxTile], s_pos[kMaxTile], s_flag[kMaxTile], s_bag[kMaxTile];
-  __shared__ float s_len[kMaxTile];
-  __shared__ uint32_t s_done[kMaxTile];
-  __shared__ uint32_t s_ndone;
-  __shared__ uint32_t s_mode, s_A, s_B, s_seg_s, s_seg_e, s_cbase;  // item descriptor
-  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint32_t D = a.dim, nvec = D / 4, T = a.tile;
-  const uint64_t N = a.counts[0];
-  const uint64_t n_items = a.n_short_items + *a.piece_count;
-  constexpr uint32_t kLast = 1u, kValid = 2u;
-  while (true) {
-    if (tid == 0) {
-      const uint64_t item = atomicAdd(a.item_ticket, 1ull);
-      uint32_t mode = 0, A = 0, B = 0, ss = 0, se = 0, cb = 0;  // mode 0: nothing, 1: short, 2: long piece, 3: done
-      if (item >= n_items) {
-        mode = 3;
-      } else if (item < a.n_short_items) {
-        const uint64_t lo = item * kItemW;
-        if (lo < N) {
-          const uint64_t hi = std::min<uint64_t>(N, lo + kItemW);
-          const uint32_t U = static_cast<uint32_t>(a.counts[1]);
-          uint32_t s0 = a.occ_seg[lo] & kSegMask;
-          if (a.seg_start[s0] < lo) ++s0;  // that segment belongs to an earlier item
-          uint32_t s1;                     // last segment starting before hi
-          if (hi >= N) {
-            s1 = U - 1;
-          } else {
-            s1 = a.occ_seg[hi] & kSegMask;
-            if (a.seg_start[s1] >= hi) --s1;
-          }
-          if (s0 < U && s0 <= s1) {
-            mode = 1;
-            A = a.seg_start[s0];
-            B = a.seg_end[s1];
-          }
-        }
-      } else {
-        const uint64_t p = item - a.n_short_items;
-        const uint32_t j = a.pieces[2 * p], k = a.pieces[2 * p + 1];
-        const uint32_t u = a.long_seg[j];
-        ss = a.seg_start[u];
-        se = a.seg_end[u];
-        A = ss + k * kItemW;
-        B = min(se, A + kItemW);
-        cb = a.long_base[j];
-        mode = 2;
-      }
-      s_mode = mode;
-      s_A = A;
-      s_B = B;
-      s_seg_s = ss;
-      s_seg_e = se;
-      s_cbase = cb;
-    }
-    __syncthreads();
-    const uint32_t mode = s_mode, A = s_A, B = s_B;
-    if (mode == 3) break;
-    if (mode == 0) {
-      __syncthreads();
-      continue;
-    }
-    float part[CPT], total[CPT];
+// Gradient row of one occurrence: d_out[bag] (/ len for mean).
+template <int VPL>
+__device__ __forceinline__ void load_grad(const BwdArgs& a, uint32_t bag, uint32_t gl, uint32_t lpr, float4 (&x)[VPL]) {
+  const uint32_t nvec = a.dim / 4;
+  const float4* d = reinterpret_cast<const float4*>(a.dout + uint64_t(bag) * a.dim);
 #pragma unroll
-    for (int i = 0; i < CPT; ++i) part[i] = total[i] = 0.f;
-    for (uint32_t t0 = A; t0 < B; t0 += T) {
-      const uint32_t nt = min(T, B - t0);
-      if (tid == 0) s_ndone = 0;
-      // phase 1: per-occurrence metadata
-      if (tid < nt) {
-        const uint32_t o = t0 + tid;
-        uint32_t flag = 0, pos = 0;
-        const uint32_t bag = a.bags[o];
-        s_row[tid] = a.rows[o];
-        if (mode == 2) {
-          pos = o - s_seg_s;
-          flag = kValid | ((o + 1 == s_seg_e) ? kLast : 0u);
-        } else {
-          const uint32_t sg = a.occ_seg[o];
-          if (!(sg & kSkip)) {
-            const uint32_t ss = a.seg_start[sg], se = a.seg_end[sg];
-            pos = o - ss;
-            flag = kValid | ((o + 1 == se) ? kLast : 0u);
-          }
-        }
-        s_bag[tid] = bag;
-        s_pos[tid] = pos;
-        s_flag[tid] = flag;
-        s_len[tid] = (a.bag_len && flag) ? static_cast<float>(a.bag_len[bag]) : 1.0f;
-      }
-      __syncthreads();
-      // phase 2: stage the gradient rows (warp w: rows w, w+8, ...; 128-bit coalesced)
-      for (uint32_t q = w; q < nt; q += kStreamBlock / 32) {
-        if (!s_flag[q]) continue;
-        const float4* src = reinterpret_cast<const float4*>(a.dout + uint64_t(s_bag[q]) * D);
-        float4* dst = reinterpret_cast<float4*>(s_tile + q * D);
-        const float fl = s_len[q];
-        for (uint32_t v = lane; v < nvec; v += 32) {
-          float4 x = __ldg(src + v);
-          if (a.bag_len) x = f4_div(x, fl);
-          dst[v] = x;
-        }
-      }
-      __syncthreads();
-      // phase 3: ordered blocked sums, column-parallel
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const uint32_t c = tid + i * kStreamBlock;
-        if (c >= D) continue;
-        for (uint32_t q = 0; q < nt; ++q) {
-          const uint32_t f = s_flag[q];
-          if (!f) continue;
-          const uint32_t pos = s_pos[q];
-          const float g = s_tile[q * D + c];
-          part[i] = (pos % kChunk == 0) ? g : __fadd_rn(part[i], g);
-          if ((pos % kChunk) == kChunk - 1 || (f & kLast)) {
-            if (mode == 2) {
-              __stcg(a.partial + uint64_t(s_cbase + pos / kChunk) * D + c, part[i]);
-            } else {
-              total[i] = (pos < kChunk) ? part[i] : __fadd_rn(total[i], part[i]);
-              if (f & kLast) s_tile[q * D + c] = total[i];
-            }
-          }
-        }
-      }
-      if (mode == 1 && tid < nt && (s_flag[tid] & kLast)) s_done[atomicAdd(&s_ndone, 1u)] = tid;
-      __syncthreads();
-      // phase 4: optimizer on the segments finished in this tile (4 rows in flight / warp)
-      if (mode == 1) {
-        const uint32_t nd = s_ndone;
-        for (uint32_t d0 = w * 4; d0 < nd; d0 += (kStreamBlock / 32) * 4) {
-          RowState<VPL> rs[4];
-#pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (d0 + r < nd) load_row<VPL>(a, s_row[s_done[d0 + r]], lane, 32, rs[r]);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            if (d0 + r >= nd) continue;
-            const uint32_t q = s_done[d0 + r];
-            float4 g[VPL];
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-              const uint32_t v = lane + 32 * k;
-              g[k] = v < nvec ? reinterpret_cast<const float4*>(s_tile + q * D)[v] : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            update_store<VPL>(a, s_row[q], lane, 32, rs[r], g);
-          }
-        }
-      }
-      __syncthreads();
-    }
+  for (int k = 0; k < VPL; ++k) {
+    const uint32_t v = gl + k * lpr;
+    x[k] = v < nvec ? __ldg(d + v) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
 }
 
 template <int VPL>
+__device__ __forceinline__ void scale_grad(float fl, bool mean, float4 (&x)[VPL]) {
+  if (!mean) return;
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) x[k] = f4_div(x[k], fl);
+}
+
+template <int VPL>
+__device__ __forceinline__ void add_into(float4 (&acc)[VPL], const float4 (&x)[VPL]) {
+#pragma unroll
+  for (int k = 0; k < VPL; ++k) acc[k] = f4_add(acc[k], x[k]);
+}
+
+// ---- short segments (<= 32 occurrences) -------------------------------------------------
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(256) k_reduce_short(BwdArgs a) {
+  constexpr int G = 32 / LPR;  // lane groups (segment streams) per warp
+  constexpr int R = VPL >= 4 ? 1 : 4 / VPL;  // segments in flight per group (register budget)
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
+  const uint64_t U = a.counts[1];
+  const bool mean = a.bag_len != nullptr;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
+    // metadata: lane l <-> segment u0 + l
+    const uint64_t u = u0 + lane;
+    uint32_t start = 0, len = 0, row = 0, b0 = 0, b1 = 0;
+    float f0 = 1.f, f1 = 1.f;
+    bool is_long = false;
+    if (u < U) {
+      start = a.seg_start[u];
+      len = a.seg_end[u] - start;
+      row = a.rows[start];
+      if (row == a.row_absent) {
+        len = 0;
+      } else if (len > kChunk) {
+        is_long = true;
+      } else {
+        b0 = a.bags[start];
+        if (len >= 2) b1 = a.bags[start + 1];
+        if (mean) {
+          f0 = static_cast<float>(a.bag_len[b0]);
+          if (len >= 2) f1 = static_cast<float>(a.bag_len[b1]);
+        }
+      }
+    }
+    // long segments: list their 32-occurrence chunks (the whole warp writes the task map)
+    uint32_t longs = __ballot_sync(0xffffffffu, is_long);
+    uint32_t my_j = 0, my_base = 0;
+    if (is_long) {
+      const uint32_t m = (len + kChunk - 1) / kChunk;
+      const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
+      my_j = static_cast<uint32_t>(p >> 32);
+      my_base = static_cast<uint32_t>(p);
+      a.long_seg[my_j] = static_cast<uint32_t>(u);
+      a.long_base[my_j] = my_base;
+      len = 0;  // not handled below
+    }
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const uint32_t j = __shfl_sync(0xffffffffu, my_j, src);
+      const uint32_t base = __shfl_sync(0xffffffffu, my_base, src);
+      const uint32_t slen = a.seg_end[u0 + src] - a.seg_start[u0 + src];
+      const uint32_t m = (slen + kChunk - 1) / kChunk;
+      for (uint32_t c = lane; c < m; c += 32) a.task_long[base + c] = j;
+    }
+    // short segments: group g handles segments g, g+G, ... of the 32, R at a time
+#pragma unroll 1
+    for (int j0 = 0; j0 < 32; j0 += G * R) {
+      uint32_t s_len[R], s_start[R], s_row[R], s_b1[R];
+      float s_f1[R];
+      RowState<VPL> rs[R];
+      float4 g[R][VPL], x[R][VPL];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t src = j0 + G * r + grp;
+        s_len[r] = __shfl_sync(0xffffffffu, len, src);
+        s_start[r] = __shfl_sync(0xffffffffu, start, src);
+        s_row[r] = __shfl_sync(0xffffffffu, row, src);
+        const uint32_t sb0 = __shfl_sync(0xffffffffu, b0, src);
+        s_b1[r] = __shfl_sync(0xffffffffu, b1, src);
+        const float sf0 = __shfl_sync(0xffffffffu, f0, src);
+        s_f1[r] = __shfl_sync(0xffffffffu, f1, src);
+        if (s_len[r]) {
+          load_row<VPL>(a, s_row[r], gl, LPR, rs[r]);
+          load_grad<VPL>(a, sb0, gl, LPR, g[r]);
+          if (s_len[r] >= 2) load_grad<VPL>(a, s_b1[r], gl, LPR, x[r]);
+          scale_grad<VPL>(sf0, mean, g[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!s_len[r]) continue;
+        if (s_len[r] >= 2) {
+          scale_grad<VPL>(s_f1[r], mean, x[r]);
+          add_into<VPL>(g[r], x[r]);
+        }
+        for (uint32_t q = 2; q < s_len[r]; q += 2) {  // occurrences 3..32: two rows in flight
+          const uint32_t bq = a.bags[s_start[r] + q];
+          const bool two = q + 1 < s_len[r];
+          const uint32_t bq1 = two ? a.bags[s_start[r] + q + 1] : bq;
+          float4 y[VPL], z[VPL];
+          load_grad<VPL>(a, bq, gl, LPR, y);
+          if (two) load_grad<VPL>(a, bq1, gl, LPR, z);
+          scale_grad<VPL>(mean ? static_cast<float>(a.bag_len[bq]) : 1.f, mean, y);
+          add_into<VPL>(g[r], y);
+          if (two) {
+            scale_grad<VPL>(mean ? static_cast<float>(a.bag_len[bq1]) : 1.f, mean, z);
+            add_into<VPL>(g[r], z);
+          }
+        }
+        update_store<VPL>(a, s_row[r], gl, LPR, rs[r], g[r]);
+      }
+    }
+  }
+}
+
+// ---- long segments: level-1 chunk partials -----------------------------------------------
+// One warp per chunk; its bags are loaded in one coalesced access, then the rows stream
+// through G lane groups (G rows per instruction, RB instructions in flight) and are added
+// in order (row q lives in group q % G; the running sum is kept replicated in every group).
+template <int LPR, int VPL>
+__global__ void __launch_bounds__(256) k_long_chunks(BwdArgs a) {
+  constexpr int G = 32 / LPR;
+  constexpr int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = a.dim / 4;
+  const bool mean = a.bag_len != nullptr;
+  const uint64_t T = static_cast<uint32_t>(*a.long_packed);
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t t = warp; t < T; t += n_warps) {
+    const uint32_t j = a.task_long[t];
+    const uint32_t u = a.long_seg[j];
+    const uint32_t c = static_cast<uint32_t>(t) - a.long_base[j];
+    const uint32_t s = a.seg_start[u] + c * kChunk;
+    const uint32_t n = min(kChunk, a.seg_end[u] - s);
+    const uint32_t my_bag = lane < n ? a.bags[s + lane] : 0u;
+    const float my_f = (mean && lane < n) ? static_cast<float>(a.bag_len[my_bag]) : 1.f;
+    float4 acc[VPL];
+    for (uint32_t q0 = 0; q0 < n; q0 += G * RB) {  // n is warp-uniform
+      float4 x[RB][VPL];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        const uint32_t q = q0 + r * G + grp;
+        const uint32_t b = __shfl_sync(0xffffffffu, my_bag, q & 31);
+        const float f = __shfl_sync(0xffffffffu, my_f, q & 31);
+        if (q < n) {
+          load_grad<VPL>(a, b, gl, LPR, x[r]);
+          scale_grad<VPL>(f, mean, x[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+          const uint32_t q = q0 + r * G + h;
+          if (q >= n) break;
+          float4 y[VPL];
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            if (G == 1) {
+              y[k] = x[r][k];
+            } else {
+              const int srcl = h * LPR + gl;
+              y[k].x = __shfl_sync(0xffffffffu, x[r][k].x, srcl);
+              y[k].y = __shfl_sync(0xffffffffu, x[r][k].y, srcl);
+              y[k].z = __shfl_sync(0xffffffffu, x[r][k].z, srcl);
+              y[k].w = __shfl_sync(0xffffffffu, x[r][k].w, srcl);
+            }
+            acc[k] = (q == 0) ? y[k] : f4_add(acc[k], y[k]);
+          }
+        }
+      }
+    }
+    if (grp == 0) {
+      float4* p = reinterpret_cast<float4*>(a.partial + t * a.dim);
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const uint32_t v = gl + k * LPR;
+        if (v < nvec) __stcg(p + v, acc[k]);
+      }
+    }
+  }
+}
+
+// ---- long segments: higher tree levels + optimizer ----------------------------------------
+template <int VPL>
 __global__ void __launch_bounds__(256) k_long_combine(BwdArgs a) {
-  extern __shared__ float4 s_part[];  // combine_batch partials of dim floats
-  const uint32_t tid = threadIdx.x, lane = tid & 31, nvec = a.dim / 4;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nvec = a.dim / 4;
   const uint32_t n_long = static_cast<uint32_t>(*a.long_packed >> 32);
   for (uint32_t j = blockIdx.x; j < n_long; j += gridDim.x) {
     const uint32_t u = a.long_seg[j];
     const uint32_t start = a.seg_start[u];
-    const uint32_t m = (a.seg_end[u] - start + kChunk - 1) / kChunk, base = a.long_base[j];
-    const uint32_t row = a.rows[start];
-    RowState<VPL> rs;
-    if (tid < 32) load_row<VPL>(a, row, lane, 32, rs);
-    float4 acc[VPL];
-    for (uint32_t b0 = 0; b0 < m; b0 += a.combine_batch) {
-      const uint32_t nb = min(a.combine_batch, m - b0);
-      const float4* src = reinterpret_cast<const float4*>(a.partial + uint64_t(base + b0) * a.dim);
-      for (uint32_t e = tid; e < nb * nvec; e += 256) s_part[e] = __ldcg(src + e);
-      __syncthreads();
-      if (tid < 32) {
-        for (uint32_t q = 0; q < nb; ++q) {
+    uint32_t m = (a.seg_end[u] - start + kChunk - 1) / kChunk;
+    const uint32_t base = a.long_base[j];
+    const float* cur = a.partial + uint64_t(base) * a.dim;
+    float* bufs[2] = {a.partial2 + uint64_t(base / kChunk + j) * a.dim, a.partial + uint64_t(base) * a.dim};
+    int nb = 0;
+    while (m > 1) {  // one tree level: groups of 32 partials, 8 warps in parallel
+      const uint32_t mn = (m + kChunk - 1) / kChunk;
+      float* nxt = bufs[nb];
+      for (uint32_t grp = w; grp < mn; grp += 8) {
+        const uint32_t lo = grp * kChunk, n = min(kChunk, m - lo);
+        constexpr int RB = VPL >= 8 ? 1 : 8 / VPL;
+        float4 acc[VPL];
+        for (uint32_t q0 = 0; q0 < n; q0 += RB) {
+          float4 x[RB][VPL];
 #pragma unroll
-          for (int k = 0; k < VPL; ++k) {
-            const uint32_t v = lane + 32 * k;
-            if (v < nvec) {
-              const float4 x = s_part[q * nvec + v];
-              acc[k] = (b0 + q == 0) ? x : f4_add(acc[k], x);
+          for (int r = 0; r < RB; ++r) {
+            const float4* src = reinterpret_cast<const float4*>(cur + uint64_t(lo + q0 + r) * a.dim);
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+              const uint32_t v = lane + 32 * k;
+              x[r][k] = (q0 + r < n && v < nvec) ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
           }
+#pragma unroll
+          for (int r = 0; r < RB; ++r) {
+            if (q0 + r >= n) break;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) acc[k] = (q0 + r == 0) ? x[r][k] : f4_add(acc[k], x[r][k]);
+          }
+        }
+        float4* dst = reinterpret_cast<float4*>(nxt + uint64_t(grp) * a.dim);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const uint32_t v = lane + 32 * k;
+          if (v < nvec) __stcg(dst + v, acc[k]);
         }
       }
+      __threadfence_block();
       __syncthreads();
+      cur = nxt;
+      nb ^= 1;
+      m = mn;
     }
-    if (tid < 32) update_store<VPL>(a, row, lane, 32, rs, acc);
+    if (w == 0) {
+      RowState<VPL> rs;
+      const uint32_t row = a.rows[start];
+      load_row<VPL>(a, row, lane, 32, rs);
+      float4 g[VPL];
+      const float4* src = reinterpret_cast<const float4*>(cur);
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const uint32_t v = lane + 32 * k;
+        g[k] = v < nvec ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      update_store<VPL>(a, row, lane, 32, rs, g);
+    }
+    __syncthreads();
   }
 }
 
@@ -390,16 +405,23 @@ __global__ void k_unique_rows(const uint32_t* rows, const uint32_t* seg_start, c
     out[u] = rows[seg_start[u]];
 }
 
-template <int CPT, int VPL>
-int launch_stream(const BwdArgs& a, cudaStream_t st, size_t smem, int grid) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_stream<CPT, VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-    attr_set = true;
-  }
-  k_stream<CPT, VPL><<<grid, kStreamBlock, smem, st>>>(a);
-  return 0;
-}
+// Lanes per row stream so that a lane holds VPL = ceil(nvec / LPR) float4 of a row.
+#define HPSG_ROW_DISPATCH(KERNEL, GRID)                                          \
+  do {                                                                           \
+    if (nvec > 128) KERNEL<32, 8><<<GRID, 256, 0, st>>>(a);                      \
+    else if (nvec > 64) KERNEL<32, 4><<<GRID, 256, 0, st>>>(a);                  \
+    else if (nvec > 32) KERNEL<32, 2><<<GRID, 256, 0, st>>>(a);                  \
+    else if (nvec == 32) KERNEL<32, 1><<<GRID, 256, 0, st>>>(a);                 \
+    else if (nvec > 16) KERNEL<16, 2><<<GRID, 256, 0, st>>>(a);                  \
+    else if (nvec == 16) KERNEL<16, 1><<<GRID, 256, 0, st>>>(a);                 \
+    else if (nvec > 8) KERNEL<8, 2><<<GRID, 256, 0, st>>>(a);                    \
+    else if (nvec == 8) KERNEL<8, 1><<<GRID, 256, 0, st>>>(a);                   \
+    else if (nvec > 4) KERNEL<4, 2><<<GRID, 256, 0, st>>>(a);                    \
+    else if (nvec == 4) KERNEL<4, 1><<<GRID, 256, 0, st>>>(a);                   \
+    else if (nvec > 2) KERNEL<2, 2><<<GRID, 256, 0, st>>>(a);                    \
+    else if (nvec == 2) KERNEL<2, 1><<<GRID, 256, 0, st>>>(a);                   \
+    else KERNEL<1, 1><<<GRID, 256, 0, st>>>(a);                                  \
+  } while (0)
 
 }  // namespace
 
@@ -422,8 +444,6 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   uint64_t* scan_status = reinterpret_cast<uint64_t*>(z + sort_words);
   uint32_t* scan_ticket = reinterpret_cast<uint32_t*>(scan_status + tiles);
   auto* long_packed = reinterpret_cast<unsigned long long*>(scan_status + tiles + 1);
-  auto* piece_count = reinterpret_cast<unsigned long long*>(scan_status + tiles + 2);
-  auto* item_ticket = reinterpret_cast<unsigned long long*>(scan_status + tiles + 3);
   const size_t used = sort_words + 2 * (tiles + 6);
   HPSG_CUDA(cudaMemsetAsync(z, 0, used * sizeof(uint32_t), st));
 
@@ -452,7 +472,7 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   const uint32_t* rows = t->sorted_in_b ? t->ws_rows_b : t->ws_rows_a;
   const uint32_t* bags = t->sorted_in_b ? t->ws_bags_b : t->ws_bags_a;
   // K4b: unique-row segments.
-  SegOp sop{rows, t->ws_seg_start, t->ws_seg_end, t->ws_occ_seg, t->ws_counts};
+  SegOp sop{rows, t->ws_seg_start, t->ws_seg_end, t->ws_counts};
   k_scan<SegOp><<<static_cast<unsigned>(std::max<uint64_t>(1, tiles)), kScanBlock, 0, st>>>(sop, scan_status,
                                                                                             scan_ticket);
   BwdArgs a{};
@@ -461,43 +481,32 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   a.bags = bags;
   a.seg_start = t->ws_seg_start;
   a.seg_end = t->ws_seg_end;
-  a.occ_seg = t->ws_occ_seg;
   a.row_absent = t->row_absent;
   a.bag_len = (t->last_multi && t->last_combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
   a.dout = d_out;
   a.dim = t->dim;
   a.long_seg = t->ws_long_seg;
   a.long_base = t->ws_long_base;
-  a.pieces = t->ws_pieces;
+  a.task_long = t->ws_task_long;
   a.long_packed = long_packed;
-  a.piece_count = piece_count;
-  a.item_ticket = item_ticket;
-  a.n_short_items = (nk + kItemW - 1) / kItemW;
-  a.tile = static_cast<uint32_t>(std::max<uint64_t>(16, std::min<uint64_t>(kMaxTile, 8192 / t->dim)));
   a.partial = t->ws_partial;
+  a.partial2 = t->ws_partial2;
   a.W = t->d_w;
   a.S0 = t->d_s0;
   a.S1 = t->d_s1;
   a.optimizer = t->optimizer;
   a.opt = *opt;
-  a.combine_batch = static_cast<uint32_t>(std::max<size_t>(1, std::min<size_t>(32, (48 * 1024) / (t->dim * 4))));
-  k_list_long<<<grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 8), 256, 0, st>>>(a);
-  // K4c + K5: streaming reduction fused with the optimizer.
-  const size_t tile_smem = size_t(a.tile) * t->dim * sizeof(float);
-  const uint64_t max_items = a.n_short_items + t->max_pieces;
-  const int sgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(max_items, kNumSMs * 4)));
-  const uint32_t D = t->dim;
-  if (D <= 128) launch_stream<1, 1>(a, st, tile_smem, sgrid);
-  else if (D <= 256) launch_stream<1, 2>(a, st, tile_smem, sgrid);
-  else if (D <= 512) launch_stream<2, 4>(a, st, tile_smem, sgrid);
-  else launch_stream<4, 8>(a, st, tile_smem, sgrid);
-  const size_t smem = a.combine_batch * size_t(t->dim) * sizeof(float);
+  const uint32_t nvec = t->dim / 4;
+  // K4c + K5: reductions fused with the optimizer.
+  const int seg_grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
+  HPSG_ROW_DISPATCH(k_reduce_short, seg_grid);
+  const int chunk_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
+  HPSG_ROW_DISPATCH(k_long_chunks, chunk_grid);
   const int comb_grid = static_cast<int>(std::min<uint64_t>(t->max_long, 2 * kNumSMs));
-  const uint32_t nvec = D / 4;
-  if (nvec > 128) k_long_combine<8><<<comb_grid, 256, smem, st>>>(a);
-  else if (nvec > 64) k_long_combine<4><<<comb_grid, 256, smem, st>>>(a);
-  else if (nvec > 32) k_long_combine<2><<<comb_grid, 256, smem, st>>>(a);
-  else k_long_combine<1><<<comb_grid, 256, smem, st>>>(a);
+  if (nvec > 128) k_long_combine<8><<<comb_grid, 256, 0, st>>>(a);
+  else if (nvec > 64) k_long_combine<4><<<comb_grid, 256, 0, st>>>(a);
+  else if (nvec > 32) k_long_combine<2><<<comb_grid, 256, 0, st>>>(a);
+  else k_long_combine<1><<<comb_grid, 256, 0, st>>>(a);
   HPSG_CHECK_LAUNCH("backward");
   return HPS_GPU_OK;
 }

@@ -511,9 +511,8 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   const uint64_t D = t->dim, N = t->max_keys, B = t->max_bags;
   t->row_absent = static_cast<uint32_t>(rows);
   t->sort_bits = std::max(1, bits_for(rows));
-  t->max_long = N / (kItemW + 1) + 2;
+  t->max_long = bwd_max_long(N);
   t->max_chunks = bwd_max_chunks(N);
-  t->max_pieces = bwd_max_pieces(N);
   t->zero_words = bwd_zero_words(N, (t->sort_bits + 7) / 8);
   int st = HPS_GPU_OK;
   auto A = [&](int s) {
@@ -536,10 +535,10 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->ws_bag_len, B));
   A(dalloc(&t->ws_seg_start, N + 1));
   A(dalloc(&t->ws_seg_end, N + 1));
-  A(dalloc(&t->ws_occ_seg, N));
   A(dalloc(&t->ws_long_seg, t->max_long));
   A(dalloc(&t->ws_long_base, t->max_long));
-  A(dalloc(&t->ws_pieces, 2 * t->max_pieces));
+  A(dalloc(&t->ws_task_long, t->max_chunks));
+  A(dalloc(&t->ws_partial2, (t->max_chunks / kChunk + t->max_long + 2) * D));
   A(dalloc(&t->ws_partial, t->max_chunks * D));
   A(dalloc(&t->ws_counts, 8));
   A(dalloc(&t->ws_zero, t->zero_words));
@@ -569,8 +568,8 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
   void* ptrs[] = {t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
                   t->ws_rows_b,   t->ws_bags_a,    t->ws_bags_b,    t->ws_occ_bag,    t->ws_bag_len,
-                  t->ws_seg_start, t->ws_seg_end,  t->ws_long_seg,  t->ws_long_base,  t->ws_pieces,
-                  t->ws_occ_seg,
+                  t->ws_seg_start, t->ws_seg_end,  t->ws_long_seg,  t->ws_long_base,  t->ws_task_long,
+                  t->ws_partial2,
                   t->ws_partial,  t->ws_counts,    t->ws_zero,      t->ws_abort,      t->ws_keys_stage,
                   t->ws_offsets_stage};
   for (void* p : ptrs)

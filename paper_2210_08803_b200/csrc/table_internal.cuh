@@ -9,8 +9,7 @@
 
 namespace hpsg {
 
-constexpr uint32_t kChunk = 32;   // blocked reduction width
-constexpr uint32_t kItemW = 256;  // occurrences per streaming work item / long piece (multiple of kChunk)
+constexpr uint32_t kChunk = 32;  // blocked reduction width
 
 // Zeroed-per-backward region: [radix sort words][pad][segment-scan status (u64) x tiles]
 // [scan ticket][long packed counter][piece counter][item ticket][spare x2] — one memset.
@@ -18,8 +17,9 @@ inline size_t bwd_sort_words(uint64_t max_keys, int passes) { return (sort_ws_wo
 inline size_t bwd_zero_words(uint64_t max_keys, int passes) {
   return bwd_sort_words(max_keys, passes) + 2 * (scan_tiles(max_keys) + 6);
 }
-inline uint64_t bwd_max_chunks(uint64_t max_keys) { return max_keys / kChunk + max_keys / kItemW + 4; }
-inline uint64_t bwd_max_pieces(uint64_t max_keys) { return 2 * (max_keys / kItemW) + 4; }
+// Level-1 chunks of segments longer than kChunk: sum ceil(len/32) <= N/32 + N/33.
+inline uint64_t bwd_max_chunks(uint64_t max_keys) { return max_keys / kChunk + max_keys / (kChunk + 1) + 4; }
+inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
 
 }  // namespace hpsg
 
@@ -49,11 +49,11 @@ struct hps_gpu_table_s {
   uint32_t* ws_occ_bag = nullptr;   // occurrence -> bag (multi-hot)
   uint32_t* ws_bag_len = nullptr;   // bag lengths (multi-hot mean)
   uint32_t *ws_seg_start = nullptr, *ws_seg_end = nullptr;  // unique-row segments of the sorted list
-  uint32_t* ws_occ_seg = nullptr;   // sorted occurrence -> segment (bit 31: owned by a long piece / absent)
-  uint32_t *ws_long_seg = nullptr, *ws_long_base = nullptr;
-  uint32_t* ws_pieces = nullptr;    // long pieces: (long id, piece index) pairs
-  float* ws_partial = nullptr;      // chunk partials of long segments
-  uint64_t max_chunks = 0, max_long = 0, max_pieces = 0;
+  uint32_t *ws_long_seg = nullptr, *ws_long_base = nullptr;  // long segments: id -> segment, first chunk
+  uint32_t* ws_task_long = nullptr; // level-1 chunk -> long segment id
+  float* ws_partial = nullptr;      // level-1 chunk partials of long segments
+  float* ws_partial2 = nullptr;     // higher tree levels (ping-pong with ws_partial)
+  uint64_t max_chunks = 0, max_long = 0;
   uint64_t* ws_counts = nullptr;    // [0]=N occurrences [1]=U segments
   uint32_t* ws_zero = nullptr;      // look-back words + tickets + long counters, zeroed per backward
   size_t zero_words = 0;
