@@ -69,30 +69,31 @@ struct SegOp {
 };
 
 // ---- row math --------------------------------------------------------------------------
-template <int VPL>
+// Row of weights (+ optimizer state): OPT is HPS_OPT_* at compile time, so the loads are
+// branch-free and the unused state registers do not exist.
+template <int OPT, int VPL>
 struct RowState {
-  float4 w[VPL], s[VPL], q[VPL];
+  float4 w[VPL], s[OPT >= HPS_OPT_ADAGRAD ? VPL : 1], q[OPT == HPS_OPT_ADAM ? VPL : 1];
 };
 
-template <int VPL>
-__device__ __forceinline__ void load_row(const BwdArgs& a, uint32_t row, uint32_t gl, uint32_t lpr, RowState<VPL>& r) {
+template <int OPT, int VPL>
+__device__ __forceinline__ void load_row(const BwdArgs& a, uint32_t row, uint32_t gl, uint32_t lpr,
+                                         RowState<OPT, VPL>& r) {
   const uint32_t nvec = a.dim / 4;
   const uint64_t base = uint64_t(row) * a.dim;
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
-    const uint32_t v = gl + k * lpr;
-    if (v < nvec) {
-      r.w[k] = reinterpret_cast<const float4*>(a.W + base)[v];
-      if (a.optimizer >= HPS_OPT_ADAGRAD) r.s[k] = reinterpret_cast<const float4*>(a.S0 + base)[v];
-      if (a.optimizer == HPS_OPT_ADAM) r.q[k] = reinterpret_cast<const float4*>(a.S1 + base)[v];
-    }
+    const uint32_t v = min(gl + k * lpr, nvec - 1);  // clamped: no branch around the load
+    r.w[k] = reinterpret_cast<const float4*>(a.W + base)[v];
+    if constexpr (OPT >= HPS_OPT_ADAGRAD) r.s[k] = reinterpret_cast<const float4*>(a.S0 + base)[v];
+    if constexpr (OPT == HPS_OPT_ADAM) r.q[k] = reinterpret_cast<const float4*>(a.S1 + base)[v];
   }
 }
 
 // Fused optimizer (operation order identical to the oracle), then store.
-template <int VPL>
+template <int OPT, int VPL>
 __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uint32_t gl, uint32_t lpr,
-                                             RowState<VPL>& r, const float4 (&g)[VPL]) {
+                                             RowState<OPT, VPL>& r, const float4 (&g)[VPL]) {
   const uint32_t nvec = a.dim / 4;
   const uint64_t base = uint64_t(row) * a.dim;
   const float lr = a.opt.lr, eps = a.opt.eps;
@@ -101,19 +102,19 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
     const uint32_t v = gl + k * lpr;
     if (v >= nvec) continue;
     float* wf = reinterpret_cast<float*>(&r.w[k]);
-    float* sf = reinterpret_cast<float*>(&r.s[k]);
-    float* qf = reinterpret_cast<float*>(&r.q[k]);
+    float* sf = reinterpret_cast<float*>(&r.s[OPT >= HPS_OPT_ADAGRAD ? k : 0]);
+    float* qf = reinterpret_cast<float*>(&r.q[OPT == HPS_OPT_ADAM ? k : 0]);
     const float* gf = reinterpret_cast<const float*>(&g[k]);
-    if (a.optimizer == HPS_OPT_SGD) {
+    if constexpr (OPT == HPS_OPT_SGD) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) wf[c] = __fsub_rn(wf[c], __fmul_rn(lr, gf[c]));
-    } else if (a.optimizer == HPS_OPT_ADAGRAD) {
+    } else if constexpr (OPT == HPS_OPT_ADAGRAD) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         sf[c] = __fadd_rn(sf[c], __fmul_rn(gf[c], gf[c]));
         wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(lr, gf[c]), __fadd_rn(__fsqrt_rn(sf[c]), eps)));
       }
-      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[k];
+      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[OPT >= HPS_OPT_ADAGRAD ? k : 0];
     } else {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -121,8 +122,8 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
         qf[c] = __fadd_rn(__fmul_rn(a.opt.beta2, qf[c]), __fmul_rn(a.opt.one_minus_beta2, __fmul_rn(gf[c], gf[c])));
         wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(a.opt.lr_t, sf[c]), __fadd_rn(__fsqrt_rn(qf[c]), eps)));
       }
-      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[k];
-      reinterpret_cast<float4*>(a.S1 + base)[v] = r.q[k];
+      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[OPT >= HPS_OPT_ADAGRAD ? k : 0];
+      reinterpret_cast<float4*>(a.S1 + base)[v] = r.q[OPT == HPS_OPT_ADAM ? k : 0];
     }
     reinterpret_cast<float4*>(a.W + base)[v] = r.w[k];
   }
@@ -134,10 +135,7 @@ __device__ __forceinline__ void load_grad(const BwdArgs& a, uint32_t bag, uint32
   const uint32_t nvec = a.dim / 4;
   const float4* d = reinterpret_cast<const float4*>(a.dout + uint64_t(bag) * a.dim);
 #pragma unroll
-  for (int k = 0; k < VPL; ++k) {
-    const uint32_t v = gl + k * lpr;
-    x[k] = v < nvec ? __ldg(d + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  for (int k = 0; k < VPL; ++k) x[k] = __ldg(d + min(gl + k * lpr, nvec - 1));  // clamped, branch-free
 }
 
 template <int VPL>
@@ -154,8 +152,8 @@ __device__ __forceinline__ void add_into(float4 (&acc)[VPL], const float4 (&x)[V
 }
 
 // ---- short segments (<= 32 occurrences) -------------------------------------------------
-template <int LPR, int VPL>
-__global__ void __launch_bounds__(256) k_reduce_short(BwdArgs a) {
+template <int OPT, int LPR, int VPL>
+__global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_short(BwdArgs a) {
   constexpr int G = 32 / LPR;  // lane groups (segment streams) per warp
   constexpr int R = VPL >= 4 ? 1 : 4 / VPL;  // segments in flight per group (register budget)
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
@@ -212,10 +210,10 @@ __global__ void __launch_bounds__(256) k_reduce_short(BwdArgs a) {
     for (int j0 = 0; j0 < 32; j0 += G * R) {
       uint32_t s_len[R], s_start[R], s_row[R], s_b1[R];
       float s_f1[R];
-      RowState<VPL> rs[R];
+      RowState<OPT, VPL> rs[R];
       float4 g[R][VPL], x[R][VPL];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
+      for (int r = 0; r < R; ++r) {  // every load of the R segments is issued here, unconditionally
         const uint32_t src = j0 + G * r + grp;
         s_len[r] = __shfl_sync(0xffffffffu, len, src);
         s_start[r] = __shfl_sync(0xffffffffu, start, src);
@@ -224,12 +222,10 @@ __global__ void __launch_bounds__(256) k_reduce_short(BwdArgs a) {
         s_b1[r] = __shfl_sync(0xffffffffu, b1, src);
         const float sf0 = __shfl_sync(0xffffffffu, f0, src);
         s_f1[r] = __shfl_sync(0xffffffffu, f1, src);
-        if (s_len[r]) {
-          load_row<VPL>(a, s_row[r], gl, LPR, rs[r]);
-          load_grad<VPL>(a, sb0, gl, LPR, g[r]);
-          if (s_len[r] >= 2) load_grad<VPL>(a, s_b1[r], gl, LPR, x[r]);
-          scale_grad<VPL>(sf0, mean, g[r]);
-        }
+        load_row<OPT, VPL>(a, s_len[r] ? s_row[r] : 0u, gl, LPR, rs[r]);
+        load_grad<VPL>(a, sb0, gl, LPR, g[r]);
+        load_grad<VPL>(a, s_b1[r], gl, LPR, x[r]);
+        scale_grad<VPL>(sf0, mean, g[r]);
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -252,7 +248,7 @@ __global__ void __launch_bounds__(256) k_reduce_short(BwdArgs a) {
             add_into<VPL>(g[r], z);
           }
         }
-        update_store<VPL>(a, s_row[r], gl, LPR, rs[r], g[r]);
+        update_store<OPT, VPL>(a, s_row[r], gl, LPR, rs[r], g[r]);
       }
     }
   }
@@ -327,7 +323,7 @@ __global__ void __launch_bounds__(256) k_long_chunks(BwdArgs a) {
 }
 
 // ---- long segments: higher tree levels + optimizer ----------------------------------------
-template <int VPL>
+template <int OPT, int VPL>
 __global__ void __launch_bounds__(256) k_long_combine(BwdArgs a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nvec = a.dim / 4;
   const uint32_t n_long = static_cast<uint32_t>(*a.long_packed >> 32);
@@ -378,9 +374,9 @@ __global__ void __launch_bounds__(256) k_long_combine(BwdArgs a) {
       m = mn;
     }
     if (w == 0) {
-      RowState<VPL> rs;
+      RowState<OPT, VPL> rs;
       const uint32_t row = a.rows[start];
-      load_row<VPL>(a, row, lane, 32, rs);
+      load_row<OPT, VPL>(a, row, lane, 32, rs);
       float4 g[VPL];
       const float4* src = reinterpret_cast<const float4*>(cur);
 #pragma unroll
@@ -388,7 +384,7 @@ __global__ void __launch_bounds__(256) k_long_combine(BwdArgs a) {
         const uint32_t v = lane + 32 * k;
         g[k] = v < nvec ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      update_store<VPL>(a, row, lane, 32, rs, g);
+      update_store<OPT, VPL>(a, row, lane, 32, rs, g);
     }
     __syncthreads();
   }
@@ -422,6 +418,31 @@ __global__ void k_unique_rows(const uint32_t* rows, const uint32_t* seg_start, c
     else if (nvec == 2) KERNEL<2, 1><<<GRID, 256, 0, st>>>(a);                   \
     else KERNEL<1, 1><<<GRID, 256, 0, st>>>(a);                                  \
   } while (0)
+
+template <int OPT>
+void launch_short(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec) {
+  if (nvec > 128) k_reduce_short<OPT, 32, 8><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 64) k_reduce_short<OPT, 32, 4><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 32) k_reduce_short<OPT, 32, 2><<<grid, 256, 0, st>>>(a);
+  else if (nvec == 32) k_reduce_short<OPT, 32, 1><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 16) k_reduce_short<OPT, 16, 2><<<grid, 256, 0, st>>>(a);
+  else if (nvec == 16) k_reduce_short<OPT, 16, 1><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 8) k_reduce_short<OPT, 8, 2><<<grid, 256, 0, st>>>(a);
+  else if (nvec == 8) k_reduce_short<OPT, 8, 1><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 4) k_reduce_short<OPT, 4, 2><<<grid, 256, 0, st>>>(a);
+  else if (nvec == 4) k_reduce_short<OPT, 4, 1><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 2) k_reduce_short<OPT, 2, 2><<<grid, 256, 0, st>>>(a);
+  else if (nvec == 2) k_reduce_short<OPT, 2, 1><<<grid, 256, 0, st>>>(a);
+  else k_reduce_short<OPT, 1, 1><<<grid, 256, 0, st>>>(a);
+}
+
+template <int OPT>
+void launch_combine(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec) {
+  if (nvec > 128) k_long_combine<OPT, 8><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 64) k_long_combine<OPT, 4><<<grid, 256, 0, st>>>(a);
+  else if (nvec > 32) k_long_combine<OPT, 2><<<grid, 256, 0, st>>>(a);
+  else k_long_combine<OPT, 1><<<grid, 256, 0, st>>>(a);
+}
 
 }  // namespace
 
@@ -499,14 +520,15 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   const uint32_t nvec = t->dim / 4;
   // K4c + K5: reductions fused with the optimizer.
   const int seg_grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
-  HPSG_ROW_DISPATCH(k_reduce_short, seg_grid);
+  if (t->optimizer == HPS_OPT_SGD) launch_short<HPS_OPT_SGD>(a, st, seg_grid, nvec);
+  else if (t->optimizer == HPS_OPT_ADAGRAD) launch_short<HPS_OPT_ADAGRAD>(a, st, seg_grid, nvec);
+  else launch_short<HPS_OPT_ADAM>(a, st, seg_grid, nvec);
   const int chunk_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
   HPSG_ROW_DISPATCH(k_long_chunks, chunk_grid);
   const int comb_grid = static_cast<int>(std::min<uint64_t>(t->max_long, 2 * kNumSMs));
-  if (nvec > 128) k_long_combine<8><<<comb_grid, 256, 0, st>>>(a);
-  else if (nvec > 64) k_long_combine<4><<<comb_grid, 256, 0, st>>>(a);
-  else if (nvec > 32) k_long_combine<2><<<comb_grid, 256, 0, st>>>(a);
-  else k_long_combine<1><<<comb_grid, 256, 0, st>>>(a);
+  if (t->optimizer == HPS_OPT_SGD) launch_combine<HPS_OPT_SGD>(a, st, comb_grid, nvec);
+  else if (t->optimizer == HPS_OPT_ADAGRAD) launch_combine<HPS_OPT_ADAGRAD>(a, st, comb_grid, nvec);
+  else launch_combine<HPS_OPT_ADAM>(a, st, comb_grid, nvec);
   HPSG_CHECK_LAUNCH("backward");
   return HPS_GPU_OK;
 }

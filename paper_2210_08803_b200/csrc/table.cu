@@ -258,7 +258,7 @@ __device__ __forceinline__ void record_occurrence(const LookupArgs& a, uint64_t 
 // occurrence in the dedup table; then groups of LPR lanes stream the rows with 128-bit
 // loads (VPL float4 per lane, 8 rows in flight per group) and write the bags coalesced.
 template <int LPR, int VPL>
-__global__ void __launch_bounds__(256) k_lookup_1hot(LookupArgs a) {
+__global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
   constexpr int G = 32 / LPR;  // rows handled side by side by one warp
   constexpr int kBatch = (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) > 0 ? (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) : 1;
   const uint32_t lane = lane_id();
