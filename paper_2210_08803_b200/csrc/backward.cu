@@ -30,22 +30,12 @@ using namespace hpsg;
 
 namespace {
 
-// Short-segment record written by the segment scan: one 16-byte load gives a reduce warp
-// everything it needs before issuing the row loads.
-//   x = global row, y = start | len << 26 (len 1..32; 0 = long or absent: not short),
-//   z = bag of occurrence 0, w = bag of occurrence 1 (= z when len == 1)
-constexpr uint32_t kLenShift = 26;
-constexpr uint32_t kStartMask = (1u << kLenShift) - 1;
-
 struct BwdArgs {
   const uint64_t* counts;  // [0]=N occurrences [1]=U segments
   const uint32_t* rows;    // sorted global rows
   const uint32_t* bags;    // bag of each sorted occurrence
   uint32_t* seg_start;
   uint32_t* seg_end;
-  const uint4* rec;        // short-segment records (SegOp)
-  uint32_t* long_ids;      // segments longer than kChunk, in discovery order (SegOp)
-  unsigned long long* long_pre;  // count of long_ids
   uint32_t row_absent;
   const uint32_t* bag_len;  // mean combiner: bag lengths (nullptr: sum)
   const float* dout;
@@ -66,68 +56,17 @@ struct BwdArgs {
 // ---- segments of the sorted list ----------------------------------------------------
 struct SegOp {
   const uint32_t* rows;
-  const uint32_t* bags;
   uint32_t* seg_start;
   uint32_t* seg_end;
-  uint4* rec;
-  uint32_t* long_ids;
-  unsigned long long* long_pre;
-  uint32_t row_absent;
   uint64_t* counts;
   __device__ uint64_t size() const { return counts[0]; }
   __device__ uint32_t count(uint64_t i) const { return (i == 0 || rows[i] != rows[i - 1]) ? 1u : 0u; }
   __device__ void emit(uint64_t i, uint64_t excl, uint64_t c) const {
-    const uint64_t n = counts[0];
-    if (c) {
-      seg_start[excl] = static_cast<uint32_t>(i);
-      const uint32_t row = rows[i];
-      uint32_t len = 1;  // probe at most kChunk + 1 elements: enough to classify the segment
-      while (len <= kChunk && i + len < n && rows[i + len] == row) ++len;
-      uint4 r;
-      r.x = row;
-      r.z = bags[i];
-      r.w = len >= 2 ? bags[i + 1] : r.z;
-      if (row == row_absent) {
-        len = 0;
-      } else if (len > kChunk) {
-        len = 0;
-        long_ids[atomicAdd(long_pre, 1ull)] = static_cast<uint32_t>(excl);
-      }
-      r.y = static_cast<uint32_t>(i) | (len << kLenShift);
-      rec[excl] = r;
-    }
-    if (i + 1 == n || rows[i + 1] != rows[i]) seg_end[excl + c - 1] = static_cast<uint32_t>(i + 1);
+    if (c) seg_start[excl] = static_cast<uint32_t>(i);
+    if (i + 1 == counts[0] || rows[i + 1] != rows[i]) seg_end[excl + c - 1] = static_cast<uint32_t>(i + 1);
   }
   __device__ void total(uint64_t u) const { counts[1] = u; }
 };
-
-// Long segments -> level-1 chunk tasks: a warp takes 32 long segments, reserves their
-// chunk ranges with one packed atomic each, then writes the chunk -> segment map together.
-__global__ void __launch_bounds__(256) k_long_prep(BwdArgs a) {
-  const uint32_t lane = lane_id();
-  const uint64_t n_long = *a.long_pre;
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t k0 = warp * 32; k0 < n_long; k0 += n_warps * 32) {
-    const uint64_t k = k0 + lane;
-    uint32_t u = 0, m = 0, j = 0, base = 0;
-    if (k < n_long) {
-      u = a.long_ids[k];
-      m = (a.seg_end[u] - a.seg_start[u] + kChunk - 1) / kChunk;
-      const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
-      j = static_cast<uint32_t>(p >> 32);
-      base = static_cast<uint32_t>(p);
-      a.long_seg[j] = u;
-      a.long_base[j] = base;
-    }
-    for (int src = 0; src < 32; ++src) {
-      const uint32_t sm = __shfl_sync(0xffffffffu, m, src);
-      const uint32_t sj = __shfl_sync(0xffffffffu, j, src);
-      const uint32_t sb = __shfl_sync(0xffffffffu, base, src);
-      for (uint32_t c = lane; c < sm; c += 32) a.task_long[sb + c] = sj;
-    }
-  }
-}
 
 // ---- row math --------------------------------------------------------------------------
 // Row of weights (+ optimizer state): OPT is HPS_OPT_* at compile time, so the loads are
@@ -223,21 +162,48 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
-    // metadata: lane l <-> segment u0 + l, one coalesced 16-byte record each
+    // metadata: lane l <-> segment u0 + l
     const uint64_t u = u0 + lane;
     uint32_t start = 0, len = 0, row = 0, b0 = 0, b1 = 0;
     float f0 = 1.f, f1 = 1.f;
+    bool is_long = false;
     if (u < U) {
-      const uint4 r = a.rec[u];
-      row = r.x;
-      start = r.y & kStartMask;
-      len = r.y >> kLenShift;  // 0: long (k_long_*) or absent key
-      b0 = r.z;
-      b1 = r.w;
-      if (mean && len) {
-        f0 = static_cast<float>(a.bag_len[b0]);
-        f1 = static_cast<float>(a.bag_len[b1]);
+      start = a.seg_start[u];
+      len = a.seg_end[u] - start;
+      row = a.rows[start];
+      if (row == a.row_absent) {
+        len = 0;
+      } else if (len > kChunk) {
+        is_long = true;
+      } else {
+        b0 = a.bags[start];
+        if (len >= 2) b1 = a.bags[start + 1];
+        if (mean) {
+          f0 = static_cast<float>(a.bag_len[b0]);
+          if (len >= 2) f1 = static_cast<float>(a.bag_len[b1]);
+        }
       }
+    }
+    // long segments: list their 32-occurrence chunks (the whole warp writes the task map)
+    uint32_t longs = __ballot_sync(0xffffffffu, is_long);
+    uint32_t my_j = 0, my_base = 0;
+    if (is_long) {
+      const uint32_t m = (len + kChunk - 1) / kChunk;
+      const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
+      my_j = static_cast<uint32_t>(p >> 32);
+      my_base = static_cast<uint32_t>(p);
+      a.long_seg[my_j] = static_cast<uint32_t>(u);
+      a.long_base[my_j] = my_base;
+      len = 0;  // not handled below
+    }
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const uint32_t j = __shfl_sync(0xffffffffu, my_j, src);
+      const uint32_t base = __shfl_sync(0xffffffffu, my_base, src);
+      const uint32_t slen = a.seg_end[u0 + src] - a.seg_start[u0 + src];
+      const uint32_t m = (slen + kChunk - 1) / kChunk;
+      for (uint32_t c = lane; c < m; c += 32) a.task_long[base + c] = j;
     }
     // short segments: group g handles segments g, g+G, ... of the 32, R at a time
 #pragma unroll 1
@@ -268,18 +234,53 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
           scale_grad<VPL>(s_f1[r], mean, x[r]);
           add_into<VPL>(g[r], x[r]);
         }
-        for (uint32_t q = 2; q < s_len[r]; q += 2) {  // occurrences 3..32: two rows in flight
-          const uint32_t bq = a.bags[s_start[r] + q];
-          const bool two = q + 1 < s_len[r];
-          const uint32_t bq1 = two ? a.bags[s_start[r] + q + 1] : bq;
-          float4 y[VPL], z[VPL];
-          load_grad<VPL>(a, bq, gl, LPR, y);
-          if (two) load_grad<VPL>(a, bq1, gl, LPR, z);
-          scale_grad<VPL>(mean ? static_cast<float>(a.bag_len[bq]) : 1.f, mean, y);
-          add_into<VPL>(g[r], y);
-          if (two) {
-            scale_grad<VPL>(mean ? static_cast<float>(a.bag_len[bq1]) : 1.f, mean, z);
-            add_into<VPL>(g[r], z);
+        if constexpr (LPR >= 16) {
+          // occurrences 3..32: the group loads all remaining bags at once (lane gl holds
+          // occurrences 2+gl and 2+gl+LPR), then streams the rows 8 in flight, in order.
+          const uint32_t rest = s_len[r] > 2 ? s_len[r] - 2 : 0;
+          if (rest) {
+            const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (0xffffu << (grp * LPR));
+            const uint32_t p = s_start[r] + 2;
+            const uint32_t bl = gl < rest ? a.bags[p + gl] : 0u;
+            const uint32_t bh = (LPR < 32 && gl + LPR < rest) ? a.bags[p + gl + LPR] : 0u;
+            const float fll = (mean && gl < rest) ? static_cast<float>(a.bag_len[bl]) : 1.f;
+            const float flh = (mean && LPR < 32 && gl + LPR < rest) ? static_cast<float>(a.bag_len[bh]) : 1.f;
+            for (uint32_t q0 = 0; q0 < rest; q0 += 8) {
+              float4 y[8][VPL];
+              float fq[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                const uint32_t q = q0 + k;
+                const int src = static_cast<int>(grp * LPR + (q % LPR));
+                const uint32_t vl = __shfl_sync(gmask, bl, src), vh = __shfl_sync(gmask, bh, src);
+                const float ql = __shfl_sync(gmask, fll, src), qh = __shfl_sync(gmask, flh, src);
+                const bool hi = q >= LPR;
+                fq[k] = hi ? qh : ql;
+                load_grad<VPL>(a, q < rest ? (hi ? vh : vl) : 0u, gl, LPR, y[k]);
+              }
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                if (q0 + k < rest) {
+                  scale_grad<VPL>(fq[k], mean, y[k]);
+                  add_into<VPL>(g[r], y[k]);
+                }
+              }
+            }
+          }
+        } else {
+          for (uint32_t q = 2; q < s_len[r]; q += 2) {  // narrow rows: two rows in flight
+            const uint32_t bq = a.bags[s_start[r] + q];
+            const bool two = q + 1 < s_len[r];
+            const uint32_t bq1 = two ? a.bags[s_start[r] + q + 1] : bq;
+            float4 y[VPL], z[VPL];
+            load_grad<VPL>(a, bq, gl, LPR, y);
+            if (two) load_grad<VPL>(a, bq1, gl, LPR, z);
+            scale_grad<VPL>(mean ? static_cast<float>(a.bag_len[bq]) : 1.f, mean, y);
+            add_into<VPL>(g[r], y);
+            if (two) {
+              scale_grad<VPL>(mean ? static_cast<float>(a.bag_len[bq1]) : 1.f, mean, z);
+              add_into<VPL>(g[r], z);
+            }
           }
         }
         update_store<OPT, VPL>(a, s_row[r], gl, LPR, rs[r], g[r]);
@@ -526,10 +527,8 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   }
   const uint32_t* rows = t->sorted_in_b ? t->ws_rows_b : t->ws_rows_a;
   const uint32_t* bags = t->sorted_in_b ? t->ws_bags_b : t->ws_bags_a;
-  // K4b: unique-row segments (+ short-segment records, long-segment list).
-  auto* long_pre = reinterpret_cast<unsigned long long*>(scan_status + tiles + 2);
-  SegOp sop{rows,        bags,     t->ws_seg_start, t->ws_seg_end, t->ws_rec,
-            t->ws_long_ids, long_pre, t->row_absent, t->ws_counts};
+  // K4b: unique-row segments.
+  SegOp sop{rows, t->ws_seg_start, t->ws_seg_end, t->ws_counts};
   k_scan<SegOp><<<static_cast<unsigned>(std::max<uint64_t>(1, tiles)), kScanBlock, 0, st>>>(sop, scan_status,
                                                                                             scan_ticket);
   BwdArgs a{};
@@ -538,9 +537,6 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   a.bags = bags;
   a.seg_start = t->ws_seg_start;
   a.seg_end = t->ws_seg_end;
-  a.rec = t->ws_rec;
-  a.long_ids = t->ws_long_ids;
-  a.long_pre = long_pre;
   a.row_absent = t->row_absent;
   a.bag_len = (t->last_multi && t->last_combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
   a.dout = d_out;
@@ -559,7 +555,6 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   const uint32_t nvec = t->dim / 4;
   // K4c + K5: reductions fused with the optimizer.
   const int seg_grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
-  k_long_prep<<<grid_for(t->max_long, 256, kNumSMs * 2), 256, 0, st>>>(a);
   if (t->optimizer == HPS_OPT_SGD) launch_short<HPS_OPT_SGD>(a, st, seg_grid, nvec);
   else if (t->optimizer == HPS_OPT_ADAGRAD) launch_short<HPS_OPT_ADAGRAD>(a, st, seg_grid, nvec);
   else launch_short<HPS_OPT_ADAM>(a, st, seg_grid, nvec);

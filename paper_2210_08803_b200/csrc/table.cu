@@ -468,10 +468,9 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   if (cfg->optimizer < HPS_OPT_SGD || cfg->optimizer > HPS_OPT_ADAM) return HPS_GPU_E_INVALID_ARGUMENT;
   for (uint32_t s = 0; s < cfg->n_slots; ++s)
     if (cfg->slot_table_host[s] >= cfg->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
-  // Occurrence positions are packed into 26 bits of the backward's segment records.
-  if (cfg->max_batch_keys == 0 || cfg->max_batch_keys >= (1ull << 26) || cfg->max_batch_bags == 0 ||
+  if (cfg->max_batch_keys == 0 || cfg->max_batch_keys >= (1ull << 31) || cfg->max_batch_bags == 0 ||
       cfg->max_batch_bags >= (1ull << 31)) {
-    set_last_error("table config: max_batch_keys must be in [1, 2^26), max_batch_bags in [1, 2^31)");
+    set_last_error("table config: max_batch_keys / max_batch_bags must be in [1, 2^31)");
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
   HPSG_CUDA(cudaSetDevice(ctx->device));
@@ -536,8 +535,6 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->ws_bag_len, B));
   A(dalloc(&t->ws_seg_start, N + 1));
   A(dalloc(&t->ws_seg_end, N + 1));
-  A(dalloc(&t->ws_rec, N + 1));
-  A(dalloc(&t->ws_long_ids, t->max_long));
   A(dalloc(&t->ws_long_seg, t->max_long));
   A(dalloc(&t->ws_long_base, t->max_long));
   A(dalloc(&t->ws_task_long, t->max_chunks));
@@ -572,7 +569,7 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
                   t->ws_rows_b,   t->ws_bags_a,    t->ws_bags_b,    t->ws_occ_bag,    t->ws_bag_len,
                   t->ws_seg_start, t->ws_seg_end,  t->ws_long_seg,  t->ws_long_base,  t->ws_task_long,
-                  t->ws_partial2, t->ws_rec,       t->ws_long_ids,
+                  t->ws_partial2,
                   t->ws_partial,  t->ws_counts,    t->ws_zero,      t->ws_abort,      t->ws_keys_stage,
                   t->ws_offsets_stage};
   for (void* p : ptrs)

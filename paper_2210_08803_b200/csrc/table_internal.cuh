@@ -49,8 +49,6 @@ struct hps_gpu_table_s {
   uint32_t* ws_occ_bag = nullptr;   // occurrence -> bag (multi-hot)
   uint32_t* ws_bag_len = nullptr;   // bag lengths (multi-hot mean)
   uint32_t *ws_seg_start = nullptr, *ws_seg_end = nullptr;  // unique-row segments of the sorted list
-  uint4* ws_rec = nullptr;          // short-segment records (backward.cu SegOp)
-  uint32_t* ws_long_ids = nullptr;  // segments longer than kChunk (discovery order)
   uint32_t *ws_long_seg = nullptr, *ws_long_base = nullptr;  // long segments: id -> segment, first chunk
   uint32_t* ws_task_long = nullptr; // level-1 chunk -> long segment id
   float* ws_partial = nullptr;      // level-1 chunk partials of long segments
