@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
           scale_grad<VPL>(s_f1[r], mean, x[r]);
           add_into<VPL>(g[r], x[r]);
         }
-        if constexpr (LPR >= 16) {
+        if constexpr (LPR == 32) {  // (narrower groups would diverge across segments of a warp)
           // occurrences 3..32: the group loads all remaining bags at once (lane gl holds
           // occurrences 2+gl and 2+gl+LPR), then streams the rows 8 in flight, in order.
           const uint32_t rest = s_len[r] > 2 ? s_len[r] - 2 : 0;
