@@ -163,6 +163,41 @@ int hps_gpu_backward_update(hps_gpu_table tbl, const float* d_out, const hps_opt
  * max_batch_keys). Used by the dedup parity tests. */
 int hps_gpu_table_last_unique(hps_gpu_table tbl, uint64_t* count_out, uint32_t* unique_rows_out);
 
+/* Owner side of the distributed exchange: rows of keys[i] in table tables[i] (one key per
+ * "bag"; absent keys give the table's default vector). With HPS_LOOKUP_TRAIN the following
+ * backward_update takes d_out = [n x dim] per-key gradients (already combiner-scaled). */
+int hps_gpu_gather_rows(hps_gpu_table tbl, const uint64_t* keys, const uint32_t* tables, uint64_t n,
+                        float* rows_out, uint32_t flags);
+
+/* ---- model-parallel exchange helpers (exchange.cu) ------------------ */
+typedef struct hps_gpu_xplan_s* hps_gpu_xplan;
+
+int hps_gpu_xplan_create(hps_gpu_ctx ctx, uint64_t max_keys, uint32_t n_shards, hps_gpu_xplan* out_host);
+int hps_gpu_xplan_destroy(hps_gpu_xplan plan);
+/* occ_bag_out[i] = bag of occurrence i of a CSR batch. */
+int hps_gpu_occurrence_bags(hps_gpu_ctx ctx, const uint32_t* offsets, uint64_t n_bags, uint32_t* occ_bag_out);
+/* Stable bucketing of n occurrences by owner = partition_of(key, n_shards): send_keys /
+ * send_tables grouped by owner (each group in occurrence order), perm[i] = send position
+ * of occurrence i, counts[g] = occurrences for owner g (u32, device). occ_bag == NULL: one
+ * key per bag. Table of occurrence i = slot_table[bag % n_slots] (slot_table on device). */
+int hps_gpu_xplan_bucketize(hps_gpu_xplan plan, const uint64_t* keys, uint64_t n, const uint32_t* occ_bag,
+                            uint32_t n_slots, const uint32_t* slot_table, uint64_t* send_keys,
+                            uint32_t* send_tables, uint32_t* perm, uint32_t* counts);
+/* out[bag] = combiner over rows[perm[i]] for the bag's occurrences (offsets == NULL: one each). */
+int hps_gpu_pool_rows(hps_gpu_ctx ctx, const float* rows, const uint32_t* perm, const uint32_t* offsets,
+                      uint64_t n_bags, uint32_t dim, int combiner, float* out);
+/* grads_out[perm[i]] = d_out[bag(i)] (/ bag length for mean). */
+int hps_gpu_scatter_grads(hps_gpu_ctx ctx, const float* d_out, const uint32_t* perm, const uint32_t* offsets,
+                          uint64_t n_bags, uint32_t dim, int combiner, float* grads_out);
+/* Localized slot: the bags of slots sel[0..n_sel) for every sample, as CSR (sample-major).
+ * lens_ws: n_samples*n_sel u32; scan_ws: scan_tiles+1 u64 (see exchange.py). */
+int hps_gpu_regroup_bags(hps_gpu_ctx ctx, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,
+                         uint32_t n_slots, const uint32_t* sel, uint32_t n_sel, uint32_t* lens_ws,
+                         uint64_t* out_keys, uint32_t* out_offsets, uint64_t* scan_ws);
+/* direction 0: dst[b*n_slots + sel[j]] = src[b*n_sel + j]; direction 1: the reverse gather. */
+int hps_gpu_place_pooled(hps_gpu_ctx ctx, const float* src, const uint32_t* sel, uint32_t n_sel,
+                         uint32_t n_samples, uint32_t n_slots, uint32_t dim, int direction, float* dst);
+
 /* ---- HPS inference cache (K6..K8), SPEC.md:112-190 ---------------------------- */
 typedef struct hps_gpu_cache_s* hps_gpu_cache;
 

@@ -453,6 +453,34 @@ int orc_lookup_pooled(void* h, const uint64_t* keys, const uint32_t* offsets, ui
   return lookup_pooled(static_cast<Table*>(h), keys, offsets, n_samples, combiner, out, train,
                        n_threads < 1 ? 1 : n_threads);
 }
+// Owner side of the distributed exchange: rows of keys[i] in tables[i]; with `train` the
+// next backward takes one gradient row per key (bag == occurrence, length 1, sum).
+int orc_gather_rows(void* h, const uint64_t* keys, const uint32_t* tables, uint64_t n, float* out, int train) {
+  auto* t = static_cast<Table*>(h);
+  const uint32_t D = t->dim;
+  if (train) {
+    t->occ_row.assign(n, UINT64_MAX);
+    t->occ_bag.resize(n);
+    t->bag_len.assign(n, 1);
+    t->last_combiner = 0;
+    t->last_n_bags = n;
+  }
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t table = tables[i];
+    auto it = t->index[table].find(keys[i]);
+    const float* src;
+    if (it == t->index[table].end()) {
+      src = t->defaults[table].data();
+    } else {
+      const uint64_t g = t->row_base[table] + it->second;
+      src = &t->w[g * D];
+      if (train) t->occ_row[i] = g;
+    }
+    if (train) t->occ_bag[i] = static_cast<uint32_t>(i);
+    for (uint32_t j = 0; j < D; ++j) out[i * D + j] = 0.0f + src[j];
+  }
+  return 0;
+}
 int orc_backward_update(void* h, const float* dout, const float* opt7, int n_threads) {
   OptParams p{opt7[0], opt7[1], opt7[2], opt7[3], opt7[4], opt7[5], opt7[6]};
   return backward_update(static_cast<Table*>(h), dout, p, n_threads < 1 ? 1 : n_threads);

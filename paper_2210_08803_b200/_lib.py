@@ -109,6 +109,15 @@ SIGNATURES = {
     "hps_gpu_lookup_pooled": (i32, [vp, vp, vp, u32, i32, vp, u32]),
     "hps_gpu_backward_update": (i32, [vp, vp, C.POINTER(OptParams)]),
     "hps_gpu_table_last_unique": (i32, [vp, vp, vp]),
+    "hps_gpu_gather_rows": (i32, [vp, vp, vp, u64, vp, u32]),
+    "hps_gpu_xplan_create": (i32, [vp, u64, u32, C.POINTER(vp)]),
+    "hps_gpu_xplan_destroy": (i32, [vp]),
+    "hps_gpu_occurrence_bags": (i32, [vp, vp, u64, vp]),
+    "hps_gpu_xplan_bucketize": (i32, [vp, vp, u64, vp, u32, vp, vp, vp, vp, vp]),
+    "hps_gpu_pool_rows": (i32, [vp, vp, vp, vp, u64, u32, i32, vp]),
+    "hps_gpu_scatter_grads": (i32, [vp, vp, vp, vp, u64, u32, i32, vp]),
+    "hps_gpu_regroup_bags": (i32, [vp, vp, vp, u32, u32, vp, u32, vp, vp, vp, vp]),
+    "hps_gpu_place_pooled": (i32, [vp, vp, vp, u32, u32, u32, u32, i32, vp]),
     "hps_gpu_cache_create": (i32, [vp, C.POINTER(CacheConfig), C.POINTER(vp)]),
     "hps_gpu_cache_destroy": (i32, [vp]),
     "hps_gpu_cache_query": (i32, [vp, vp, u64, vp, vp, vp, vp]),

@@ -234,6 +234,7 @@ struct LookupArgs {
   uint32_t n_bags;
   uint32_t n_slots;
   const uint32_t* slot_table;
+  const uint32_t* key_tables;  // one-key bags only: table of each key (overrides slot_table)
   const TableDev* tables;
   const Slot* slots;
   const float* W;
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
     uint32_t row = kRowEmpty, table = 0;
     if (bag < a.n_bags) {
       const uint64_t key = a.keys[bag];
-      table = a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
+      table = a.key_tables ? a.key_tables[bag] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
       const TableDev td = a.tables[table];
       const uint32_t local = probe_find(a.slots, td, key);
       row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
@@ -730,6 +731,44 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   t->last_multi = multi;
   t->last_combiner = combiner;
   t->last_n_keys_host = n_keys_host;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* tables, uint64_t n, float* rows_out,
+                        uint32_t flags) {
+  if (int s = check_tbl(t)) return s;
+  if (n > t->max_keys || n > t->max_bags) {
+    set_last_error("gather_rows: n exceeds max_batch_keys / max_batch_bags");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  const bool train = (flags & HPS_LOOKUP_TRAIN) != 0;
+  if (n == 0) {
+    t->have_train = false;
+    return HPS_GPU_OK;
+  }
+  if (!keys || !tables || !rows_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  LookupArgs a{};
+  a.keys = keys;
+  a.n_bags = static_cast<uint32_t>(n);
+  a.n_slots = t->n_slots;
+  a.slot_table = t->d_slot_table;
+  a.key_tables = tables;
+  a.tables = t->d_tables;
+  a.slots = t->d_slots;
+  a.W = t->d_w;
+  a.defaults = t->d_defaults;
+  a.dim = t->dim;
+  a.out = rows_out;
+  if (train) {
+    a.occ_row = t->ws_rows_a;
+    a.row_absent = t->row_absent;
+    a.d_n = t->ws_counts;
+  }
+  if (int s = launch_lookup(t, a, false)) return s;
+  t->have_train = train;
+  t->last_multi = false;
+  t->last_combiner = HPS_COMBINER_SUM;
+  t->last_n_keys_host = n;
   return HPS_GPU_OK;
 }
 

@@ -183,3 +183,18 @@ class OracleCache:
             self.L.orc_cache_destroy(self.h)
         except Exception:
             pass
+
+
+lib_sig_extra = {"orc_gather_rows": (i32, [vp, vp, vp, u64, vp, i32])}
+
+
+def gather_rows(table: "OracleTable", keys, tables, train=False):
+    L = lib()
+    for k, (r, a) in lib_sig_extra.items():
+        getattr(L, k).restype = r
+        getattr(L, k).argtypes = a
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    tables = np.ascontiguousarray(tables, dtype=np.uint32)
+    out = np.empty((len(keys), table.dim), dtype=np.float32)
+    L.orc_gather_rows(table.h, P(keys), P(tables), len(keys), P(out), 1 if train else 0)
+    return out

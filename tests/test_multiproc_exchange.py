@@ -1,0 +1,101 @@
+"""World-size-2 gloo test of the distributed-slot exchange orchestration (exchange.py).
+
+Each rank owns the keys with partition_of(key, 2) == rank; the SAME DistributedExchange
+host code that runs over NCCL on B200s runs here over gloo with the CPU engine
+(tests/cpu_engine.py, oracle-backed). Pooled outputs and every updated row must be
+bit-identical to one unsharded oracle table driven with the concatenated global batch.
+"""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _global_batch(rs, pools, slot_table, n_samples, multi):
+    S = len(slot_table)
+    lens = rs.integers(0, 6, n_samples * S) if multi else np.ones(n_samples * S, dtype=np.int64)
+    offs = np.zeros(n_samples * S + 1, dtype=np.int64)
+    offs[1:] = np.cumsum(lens)
+    keys = []
+    for b in range(n_samples * S):
+        pool = pools[slot_table[b % S]]
+        hot = rs.random(lens[b]) < 0.4
+        keys.append(np.where(hot, pool[rs.integers(0, 2, lens[b])], rs.choice(pool, lens[b])))
+    return np.concatenate(keys).astype(np.uint64), offs
+
+
+def _worker(rank, world, port, out_dir, multi, optimizer):
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2210_08803_b200.api import opt_params
+    from paper_2210_08803_b200.exchange import DistributedExchange
+    from tests import oracle_lib as O
+    from tests.cpu_engine import CpuEngine
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rs = np.random.default_rng(123)
+    cards, slot_table, dim = [400, 9, 60], [0, 1, 2, 1], 8
+    combiner = "mean" if multi else "sum"
+    pools = [rs.integers(0, 2**63, c).astype(np.uint64) for c in cards]
+    single = O.OracleTable(cards, dim, slot_table, optimizer, seed=5, a0=0.1)
+    shard = O.OracleTable(cards, dim, slot_table, optimizer, seed=5, a0=0.1)
+    for t, ks in enumerate(pools):
+        single.insert(t, ks)
+        own = np.empty(len(ks), dtype=np.uint32)
+        O.lib().orc_partition_of_n(O.P(ks), len(ks), world, O.P(own))
+        shard.insert(t, ks[own == rank])
+    ex = DistributedExchange(CpuEngine(shard, slot_table, world, dim), combiner, rank, world)
+    B, S = 24, len(slot_table)
+    for step in range(1, 4):
+        keys, offs = _global_batch(rs, pools, slot_table, B * world, multi)
+        ref = single.lookup(keys, B * world, offsets=offs.astype(np.uint32) if multi else None, combiner=combiner,
+                            train=True)
+        lo, hi = offs[rank * B * S], offs[(rank + 1) * B * S]
+        k_local = torch.from_numpy(keys[lo:hi].view(np.int64).copy())
+        o_local = torch.from_numpy((offs[rank * B * S:(rank + 1) * B * S + 1] - lo).astype(np.int32)) if multi else None
+        out = ex.forward(k_local, o_local, B * S).numpy()
+        assert np.array_equal(out.view(np.uint32), ref[rank * B * S:(rank + 1) * B * S].view(np.uint32)), "forward"
+        dout = rs.standard_normal(ref.shape).astype(np.float32)
+        p = opt_params(optimizer, 0.05, step=step, eps=1e-7)
+        ex.backward(torch.from_numpy(dout[rank * B * S:(rank + 1) * B * S].copy()), p)
+        single.backward_update(dout, p)
+    # every key this rank owns: same row values (and optimizer state) as the single table
+    mism = 0
+    for t, ks in enumerate(pools):
+        own = np.empty(len(ks), dtype=np.uint32)
+        O.lib().orc_partition_of_n(O.P(ks), len(ks), world, O.P(own))
+        mine = ks[own == rank]
+        rs_rows, rg_rows = shard.find(t, mine), single.find(t, ks[own == rank])
+        ws, s0s, _ = shard.export(t, 0, shard.size(t))
+        wg, s0g, _ = single.export(t, 0, single.size(t))
+        mism += int((ws[rs_rows.astype(np.int64)].view(np.uint32) != wg[rg_rows.astype(np.int64)].view(np.uint32)).sum())
+        if s0s is not None:
+            mism += int((s0s[rs_rows.astype(np.int64)] != s0g[rg_rows.astype(np.int64)]).sum())
+    with open(os.path.join(out_dir, f"rank{rank}.txt"), "w") as f:
+        f.write(str(mism))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("multi,optimizer", [(False, "sgd"), (True, "adagrad"), (False, "adam")])
+def test_distributed_exchange_world2_bit_exact(multi, optimizer):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d, multi, optimizer), nprocs=2, join=True)
+        for r in range(2):
+            assert open(os.path.join(d, f"rank{r}.txt")).read() == "0"
