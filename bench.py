@@ -334,6 +334,12 @@ def main():
             "cpu_baseline": cpu,
             "unique_keys": U, "key_occurrences": N, "setup_s": setup_s,
         }
+        if world > 1:
+            xb = step_fn.exchange.exchanged_bytes(cfg.dim)
+            line["nvlink"] = {"bytes_per_step_rank0": xb, "achieved_gbs": xb / (ms_max / 1000.0) / 1e9,
+                              "peak_gbs": 770.0, "peak_kind": "measured peer copy (B200_PROFILING.md)",
+                              "frac": xb / (ms_max / 1000.0) / 1e9 / 770.0}
+            line["roofline"]["kernel"] = "distributed forward (bucketize + all-to-all + gather + all-to-all + pool)"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -23,17 +23,20 @@ def _owned_keys(ctx: Context, cfg: W.Config, t: int, rank: int, world: int, firs
     return keys
 
 
+def table_max_keys(cfg: W.Config, world: int) -> int:
+    """Key occurrences one rank may have to hold in a step (an owner can receive every
+    rank's keys in the worst case)."""
+    n_bags = cfg.batch * cfg.n_slots
+    return n_bags * (2 * cfg.hot - 1 if cfg.hot > 1 else 1) * world
+
+
 def build_tables(ctx: Context, cfg: W.Config, rank: int = 0, world: int = 1,
                  chunk: int = 1 << 24) -> EmbeddingTableGroup:
     """Create the (shard of the) table group and bulk-insert every key of every table,
     in index order, so that on one GPU row i of table t holds table_key(t, i)."""
     n_bags = cfg.batch * cfg.n_slots
-    max_keys = n_bags * (2 * cfg.hot - 1 if cfg.hot > 1 else 1)
-    if world > 1:
-        max_keys *= world
-        n_bags_cap = max(n_bags * world, max_keys)
-    else:
-        n_bags_cap = n_bags
+    max_keys = table_max_keys(cfg, world)
+    n_bags_cap = n_bags if world == 1 else max(n_bags * world, max_keys)
     caps = []
     for c in cfg.cards:
         caps.append(c if world == 1 else int(c / world * 1.02 + 64 * math.sqrt(c / world + 1) + 64))
@@ -65,9 +68,13 @@ class TrainStep:
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.exchange = None
         if world > 1:
-            from .exchange import DistributedExchange
-            self.exchange = DistributedExchange(ctx, table, cfg, rank, world)
-            self.kernels_per_step = self.exchange.kernels_per_step
+            from .exchange import DistributedExchange, GpuEngine
+            max_keys = table_max_keys(cfg, 1)
+            self.engine = GpuEngine(ctx, table, cfg.slots(), max_keys, world)
+            self.exchange = DistributedExchange(self.engine, cfg.combiner, rank, world)
+            # bucketize (owner + hist + 1 radix pass + pack + counts) + gather + pool
+            # + scatter + backward (hist + passes + scan + 3 reduce kernels) [+ occ_bags]
+            self.kernels_per_step = 5 + 1 + 1 + 1 + 7 + (1 if cfg.hot > 1 else 0)
 
     # -- inputs -------------------------------------------------------------------------
     def stage_batch(self, keys: np.ndarray, offs: Optional[np.ndarray]):
@@ -88,10 +95,16 @@ class TrainStep:
                           out=self.out, keys_on_host=keys_on_host)
         self.table.backward_update(dout, self.cfg.lr, params=self.params)
 
+    def _exchange_step(self, keys, offs, dout, step):
+        if self.cfg.optimizer == "adam":
+            self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
+        self.out = self.exchange.forward(keys, offs, self.n_bags, train=True)
+        self.exchange.backward(dout, self.params)
+
     def run(self, b, dout, step: int = 1):
         self._last_n = b["n_keys"]
         if self.exchange is not None:
-            return self.exchange.step(b, dout, step, self.out)
+            return self._exchange_step(b["keys"], b["offs"], dout, step)
         if not self.graph_mode:
             return self._eager(b, dout, step)
         key = (id(b["keys"]), id(dout))
@@ -114,7 +127,13 @@ class TrainStep:
         """End-to-end through the C-ABI: keys from pinned host memory (H2D inside the call),
         and a D2H read of the step's result (the number of rows updated)."""
         if self.exchange is not None:
-            return self.exchange.step_host(b, dout, step, self.out)
+            keys = b["keys"].to("cuda", non_blocking=True)
+            offs = None if b["offs"] is None else b["offs"].to("cuda", non_blocking=True)
+            self._exchange_step(keys, offs, dout, step)
+            self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
+            _ = int(self._cnt.item())
+            h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
+            return h2d, 8
         self._eager(b, dout, step, keys_on_host=True)
         self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
         _ = int(self._cnt.item())
@@ -122,11 +141,12 @@ class TrainStep:
         return h2d, 8
 
     def last_counts(self):
-        if self.exchange is not None:
-            return self.exchange.last_counts()
         self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
         return self._last_n, int(self._cnt.item())
 
     def lookup_only(self, b):
+        if self.exchange is not None:
+            self.exchange.forward(b["keys"], b["offs"], self.n_bags, train=False)
+            return
         self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=False,
                           out=self.out)
