@@ -311,6 +311,62 @@ __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
   }
 }
 
+// One-key-per-bag path on the bulk-copy engine (TMA 1-D), used when rows are <= 1 KB and
+// `out` is 16-byte aligned. A warp owns 32 consecutive bags per tile: the lanes hash and
+// probe 32 keys; each lane then issues ONE cp.async.bulk of its row (or the table's
+// default vector) into the warp's shared-memory tile, all completing on one mbarrier; the
+// +0.0f normalisation of the oracle runs in smem; a single bulk store writes the 32 pooled
+// rows (contiguous in `out`) back while the next tile's probes are already in flight.
+// No registers hold row data, so every warp keeps 32 rows (16 KB at dim 128) outstanding.
+constexpr int kTmaWarps = 4;
+
+__global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a) {
+  extern __shared__ __align__(128) float s_rows[];  // [kTmaWarps][32][dim]
+  __shared__ __align__(8) uint64_t s_bar[kTmaWarps];
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  const uint32_t D = a.dim, nvec = D / 4, row_bytes = D * 4;
+  float* tile = s_rows + size_t(w) * 32 * D;
+  if (lane == 0) {
+    mbar_init(&s_bar[w], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  uint32_t phase = 0;
+  const uint64_t warp = uint64_t(blockIdx.x) * kTmaWarps + w;
+  const uint64_t n_warps = uint64_t(gridDim.x) * kTmaWarps;
+  if (a.d_n && warp == 0 && lane == 0) *a.d_n = a.n_bags;
+  for (uint64_t t0 = warp * 32; t0 < a.n_bags; t0 += n_warps * 32) {
+    const uint64_t bag = t0 + lane;
+    const uint32_t nb = static_cast<uint32_t>(min(uint64_t(32), a.n_bags - t0));
+    const float* src = nullptr;
+    if (bag < a.n_bags) {
+      const uint64_t key = a.keys[bag];
+      const uint32_t table = a.key_tables ? a.key_tables[bag] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
+      const TableDev td = a.tables[table];
+      const uint32_t local = probe_find(a.slots, td, key);
+      const uint32_t row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
+      if (a.occ_row) record_occurrence(a, bag, local, row);
+      src = local == kRowEmpty ? a.defaults + uint64_t(table) * D : a.W + uint64_t(row) * D;
+    }
+    if (lane == 0) bulk_wait_read_all();  // the previous tile's store has finished reading smem
+    __syncwarp();
+    if (lane == 0) mbar_arrive_expect_tx(&s_bar[w], nb * row_bytes);
+    __syncwarp();
+    if (bag < a.n_bags) bulk_g2s(tile + lane * D, src, row_bytes, &s_bar[w]);
+    mbar_wait(&s_bar[w], phase);
+    phase ^= 1;
+    float4* t4 = reinterpret_cast<float4*>(tile);
+    for (uint32_t e = lane; e < nb * nvec; e += 32) t4[e] = f4_add(make_float4(0.f, 0.f, 0.f, 0.f), t4[e]);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      bulk_s2g(a.out + t0 * D, tile, nb * row_bytes);
+      bulk_commit();
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
 // Multi-hot path: a group of LPR lanes owns one bag at a time; the group probes LPR
 // keys of the bag in parallel, then accumulates the rows in bag order (4 in flight).
 template <int LPR, int VPL>
@@ -436,7 +492,19 @@ int check_tbl(hps_gpu_table t) {
 int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi) {
   const cudaStream_t st = t->ctx->stream;
   const uint32_t nvec = t->dim / 4;
-  if (!multi) {
+  const bool tma_ok = t->dim <= 256 && (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0 && !t->no_tma;
+  if (!multi && tma_ok) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_lookup_1hot_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaWarps * 32 * 256 * 4);
+      attr = true;
+    }
+    const size_t smem = size_t(kTmaWarps) * 32 * t->dim * sizeof(float);
+    const uint64_t tiles = (uint64_t(a.n_bags) + 31) / 32;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + kTmaWarps - 1) / kTmaWarps,
+                                                                               uint64_t(kNumSMs) * 8)));
+    k_lookup_1hot_tma<<<grid, kTmaWarps * 32, smem, st>>>(a);
+  } else if (!multi) {
     auto grid1 = [&](int) { return grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * 64); };
     HPSG_DISPATCH_ROW(k_lookup_1hot, grid1, a);
   } else {
@@ -486,6 +554,7 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->a0 = cfg->adagrad_initial_accumulator;
   t->max_keys = cfg->max_batch_keys;
   t->max_bags = cfg->max_batch_bags;
+  if (const char* e = std::getenv("HPS_GPU_NO_TMA")) t->no_tma = e[0] == '1';
   uint64_t rows = 0, slots = 0;
   for (uint32_t i = 0; i < t->n_tables; ++i) {
     const uint64_t cap = cfg->row_capacity_host[i];

@@ -62,6 +62,7 @@ struct hps_gpu_table_s {
   uint32_t* ws_offsets_stage = nullptr;
   // last training lookup
   bool have_train = false, last_multi = false, sorted_in_b = false;
+  bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)
   int last_combiner = 0;
   uint64_t last_n_keys_host = 0;  // exact when known on the host, else max_keys
 };
