@@ -46,6 +46,7 @@ struct BwdArgs {
   unsigned long long* long_packed;  // (n_long << 32) | total level-1 chunks
   float* partial;                   // level-1 partials [max_chunks x dim]
   float* partial2;                  // higher levels [max_chunks/32 + max_long x dim]
+  uint32_t tma_rows;                // rows per warp buffer in k_reduce_short_tma
   float* W;
   float* S0;
   float* S1;
@@ -289,6 +290,130 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
   }
 }
 
+// ---- short segments on the bulk-copy engine ----------------------------------------------
+// Same work as k_reduce_short, staged through shared memory by cp.async.bulk: a warp takes
+// 32 segments (lane = segment), packs as many as fit into its smem buffer ("wave": a warp
+// prefix sum over rows needed = weight + state rows + one gradient row per occurrence),
+// every lane issues the bulk copies of its own segment's rows onto the warp's mbarrier,
+// and only then does the warp walk the wave segment by segment (ordered sum from smem,
+// fused optimizer, 128-bit stores). Bytes in flight no longer cost registers.
+constexpr int kRedWarps = 4;
+
+template <int OPT, int VPL>
+__global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) {
+  constexpr uint32_t NS = OPT == HPS_OPT_SGD ? 0 : OPT == HPS_OPT_ADAGRAD ? 1 : 2;  // state rows
+  extern __shared__ __align__(128) float s_buf[];  // [kRedWarps][cap][dim] rows, then [kRedWarps][cap] scales
+  __shared__ __align__(8) uint64_t s_bar[kRedWarps];
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  const uint32_t D = a.dim, nvec = D / 4, row_bytes = D * 4, cap = a.tma_rows;
+  float* buf = s_buf + size_t(w) * cap * D;
+  float* scale = s_buf + size_t(kRedWarps) * cap * D + size_t(w) * cap;
+  const bool mean = a.bag_len != nullptr;
+  if (lane == 0) {
+    mbar_init(&s_bar[w], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  uint32_t phase = 0;
+  const uint64_t U = a.counts[1];
+  const uint64_t warp = uint64_t(blockIdx.x) * kRedWarps + w;
+  const uint64_t n_warps = uint64_t(gridDim.x) * kRedWarps;
+  for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
+    const uint64_t u = u0 + lane;
+    uint32_t start = 0, len = 0, row = 0;
+    bool is_long = false;
+    if (u < U) {
+      start = a.seg_start[u];
+      len = a.seg_end[u] - start;
+      row = a.rows[start];
+      if (row == a.row_absent) {
+        len = 0;
+      } else if (len > kChunk) {
+        is_long = true;
+      }
+    }
+    // long segments -> chunk tasks (warp-cooperative map writes), as in k_reduce_short
+    uint32_t longs = __ballot_sync(0xffffffffu, is_long);
+    uint32_t my_j = 0, my_base = 0;
+    if (is_long) {
+      const uint32_t m = (len + kChunk - 1) / kChunk;
+      const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
+      my_j = static_cast<uint32_t>(p >> 32);
+      my_base = static_cast<uint32_t>(p);
+      a.long_seg[my_j] = static_cast<uint32_t>(u);
+      a.long_base[my_j] = my_base;
+      len = 0;
+    }
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const uint32_t j = __shfl_sync(0xffffffffu, my_j, src);
+      const uint32_t base = __shfl_sync(0xffffffffu, my_base, src);
+      const uint32_t slen = a.seg_end[u0 + src] - a.seg_start[u0 + src];
+      const uint32_t m = (slen + kChunk - 1) / kChunk;
+      for (uint32_t c = lane; c < m; c += 32) a.task_long[base + c] = j;
+    }
+    const uint32_t need = len ? 1 + NS + len : 0;
+    uint32_t first = 0;  // first lane (segment) of the current wave
+    while (first < 32) {
+      const uint32_t r = lane >= first ? need : 0u;
+      const uint32_t incl = warp_incl_scan(r);
+      const bool in_wave = lane >= first && incl <= cap;
+      const uint32_t wave_mask = __ballot_sync(0xffffffffu, in_wave);
+      const uint32_t last = 31 - __clz(wave_mask);  // wave = lanes [first, last]
+      const uint32_t off = incl - r;
+      const uint32_t total_rows = __shfl_sync(0xffffffffu, incl, last);
+      if (lane == 0) mbar_arrive_expect_tx(&s_bar[w], total_rows * row_bytes);
+      __syncwarp();
+      if (in_wave && len) {
+        float* dst = buf + size_t(off) * D;
+        bulk_g2s(dst, a.W + uint64_t(row) * D, row_bytes, &s_bar[w]);
+        if constexpr (NS >= 1) bulk_g2s(dst + D, a.S0 + uint64_t(row) * D, row_bytes, &s_bar[w]);
+        if constexpr (NS >= 2) bulk_g2s(dst + 2 * D, a.S1 + uint64_t(row) * D, row_bytes, &s_bar[w]);
+        for (uint32_t q = 0; q < len; ++q) {
+          const uint32_t bag = a.bags[start + q];
+          bulk_g2s(dst + (1 + NS + q) * D, a.dout + uint64_t(bag) * D, row_bytes, &s_bar[w]);
+          if (mean) scale[off + 1 + NS + q] = static_cast<float>(a.bag_len[bag]);
+        }
+      }
+      mbar_wait(&s_bar[w], phase);
+      phase ^= 1;
+      __syncwarp();  // the scale[] writes of other lanes
+      // walk the wave in segment order
+      for (uint32_t j = first; j <= last; ++j) {
+        const uint32_t jl = __shfl_sync(0xffffffffu, len, j);
+        const uint32_t jo = __shfl_sync(0xffffffffu, off, j);
+        const uint32_t jr = __shfl_sync(0xffffffffu, row, j);
+        if (!jl) continue;
+        const float4* seg = reinterpret_cast<const float4*>(buf + size_t(jo) * D);
+        RowState<OPT, VPL> rs;
+        float4 g[VPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          const uint32_t v = min(lane + 32u * k, nvec - 1);
+          rs.w[k] = seg[v];
+          if constexpr (NS >= 1) rs.s[k] = seg[nvec + v];
+          if constexpr (NS >= 2) rs.q[k] = seg[2 * nvec + v];
+          g[k] = seg[(1 + NS) * nvec + v];
+          if (mean) g[k] = f4_div(g[k], scale[jo + 1 + NS]);
+        }
+        for (uint32_t q = 1; q < jl; ++q) {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) {
+            const uint32_t v = min(lane + 32u * k, nvec - 1);
+            float4 x = seg[(1 + NS + q) * nvec + v];
+            if (mean) x = f4_div(x, scale[jo + 1 + NS + q]);
+            g[k] = f4_add(g[k], x);
+          }
+        }
+        update_store<OPT, VPL>(a, jr, lane, 32, rs, g);
+      }
+      __syncwarp();  // every lane is done reading the buffer before the next wave overwrites it
+      first = last + 1;
+    }
+  }
+}
+
 // ---- long segments: level-1 chunk partials -----------------------------------------------
 // One warp per chunk; its bags are loaded in one coalesced access, then the rows stream
 // through G lane groups (G rows per instruction, RB instructions in flight) and are added
@@ -471,6 +596,22 @@ void launch_short(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec) {
   else k_reduce_short<OPT, 1, 1><<<grid, 256, 0, st>>>(a);
 }
 
+template <int OPT, int VPL>
+void launch_short_tma_v(const BwdArgs& a, cudaStream_t st, int grid, size_t smem) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_reduce_short_tma<OPT, VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_reduce_short_tma<OPT, VPL><<<grid, kRedWarps * 32, smem, st>>>(a);
+}
+
+template <int OPT>
+void launch_short_tma(const BwdArgs& a, cudaStream_t st, int grid, size_t smem, uint32_t nvec) {
+  if (nvec > 32) launch_short_tma_v<OPT, 2>(a, st, grid, smem);
+  else launch_short_tma_v<OPT, 1>(a, st, grid, smem);
+}
+
 template <int OPT>
 void launch_combine(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec) {
   if (nvec > 128) k_long_combine<OPT, 8><<<grid, 256, 0, st>>>(a);
@@ -555,9 +696,21 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   const uint32_t nvec = t->dim / 4;
   // K4c + K5: reductions fused with the optimizer.
   const int seg_grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
-  if (t->optimizer == HPS_OPT_SGD) launch_short<HPS_OPT_SGD>(a, st, seg_grid, nvec);
-  else if (t->optimizer == HPS_OPT_ADAGRAD) launch_short<HPS_OPT_ADAGRAD>(a, st, seg_grid, nvec);
-  else launch_short<HPS_OPT_ADAM>(a, st, seg_grid, nvec);
+  if (t->dim <= 256 && !t->no_tma) {
+    a.tma_rows = static_cast<uint32_t>(std::max<uint64_t>(40, (24 * 1024) / (t->dim * 4)));
+    const size_t smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float);
+    const int grid = static_cast<int>(
+        std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * 4)));
+    if (t->optimizer == HPS_OPT_SGD) launch_short_tma<HPS_OPT_SGD>(a, st, grid, smem, nvec);
+    else if (t->optimizer == HPS_OPT_ADAGRAD) launch_short_tma<HPS_OPT_ADAGRAD>(a, st, grid, smem, nvec);
+    else launch_short_tma<HPS_OPT_ADAM>(a, st, grid, smem, nvec);
+  } else if (t->optimizer == HPS_OPT_SGD) {
+    launch_short<HPS_OPT_SGD>(a, st, seg_grid, nvec);
+  } else if (t->optimizer == HPS_OPT_ADAGRAD) {
+    launch_short<HPS_OPT_ADAGRAD>(a, st, seg_grid, nvec);
+  } else {
+    launch_short<HPS_OPT_ADAM>(a, st, seg_grid, nvec);
+  }
   const int chunk_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
   HPSG_ROW_DISPATCH(k_long_chunks, chunk_grid);
   const int comb_grid = static_cast<int>(std::min<uint64_t>(t->max_long, 2 * kNumSMs));
