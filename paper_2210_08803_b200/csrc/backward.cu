@@ -320,12 +320,14 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) 
   const uint64_t n_warps = uint64_t(gridDim.x) * kRedWarps;
   for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
     const uint64_t u = u0 + lane;
-    uint32_t start = 0, len = 0, row = 0;
+    uint32_t start = 0, len = 0, row = 0, b0 = 0, b1 = 0;
     bool is_long = false;
     if (u < U) {
       start = a.seg_start[u];
       len = a.seg_end[u] - start;
       row = a.rows[start];
+      b0 = a.bags[start];  // loaded with the row: copies of 1-2 occurrence segments issue at once
+      if (len >= 2) b1 = a.bags[start + 1];
       if (row == a.row_absent) {
         len = 0;
       } else if (len > kChunk) {
@@ -370,10 +372,22 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) 
         bulk_g2s(dst, a.W + uint64_t(row) * D, row_bytes, &s_bar[w]);
         if constexpr (NS >= 1) bulk_g2s(dst + D, a.S0 + uint64_t(row) * D, row_bytes, &s_bar[w]);
         if constexpr (NS >= 2) bulk_g2s(dst + 2 * D, a.S1 + uint64_t(row) * D, row_bytes, &s_bar[w]);
-        for (uint32_t q = 0; q < len; ++q) {
-          const uint32_t bag = a.bags[start + q];
-          bulk_g2s(dst + (1 + NS + q) * D, a.dout + uint64_t(bag) * D, row_bytes, &s_bar[w]);
-          if (mean) scale[off + 1 + NS + q] = static_cast<float>(a.bag_len[bag]);
+        bulk_g2s(dst + (1 + NS) * D, a.dout + uint64_t(b0) * D, row_bytes, &s_bar[w]);
+        if (len >= 2) bulk_g2s(dst + (2 + NS) * D, a.dout + uint64_t(b1) * D, row_bytes, &s_bar[w]);
+        if (mean) {
+          scale[off + 1 + NS] = static_cast<float>(a.bag_len[b0]);
+          if (len >= 2) scale[off + 2 + NS] = static_cast<float>(a.bag_len[b1]);
+        }
+        for (uint32_t q0 = 2; q0 < len; q0 += 4) {  // occurrences 3..32: bag ids 4 at a time
+          uint32_t bq[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) bq[k] = q0 + k < len ? a.bags[start + q0 + k] : 0u;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (q0 + k >= len) break;
+            bulk_g2s(dst + (1 + NS + q0 + k) * D, a.dout + uint64_t(bq[k]) * D, row_bytes, &s_bar[w]);
+            if (mean) scale[off + 1 + NS + q0 + k] = static_cast<float>(a.bag_len[bq[k]]);
+          }
         }
       }
       mbar_wait(&s_bar[w], phase);
@@ -696,7 +710,7 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   const uint32_t nvec = t->dim / 4;
   // K4c + K5: reductions fused with the optimizer.
   const int seg_grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
-  if (t->dim <= 256 && !t->no_tma) {
+  if (t->dim >= 128 && t->dim <= 256 && !t->no_tma) {  // narrower rows: the register path wins
     a.tma_rows = static_cast<uint32_t>(std::max<uint64_t>(40, (24 * 1024) / (t->dim * 4)));
     const size_t smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float);
     const int grid = static_cast<int>(
