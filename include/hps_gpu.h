@@ -227,6 +227,18 @@ int hps_gpu_cache_insert(hps_gpu_cache cache, const uint64_t* keys, const float*
 /* SPEC.md:149-157. replaced_out: device u64 (may be NULL). */
 int hps_gpu_cache_refresh(hps_gpu_cache cache, const uint64_t* keys, const float* vecs,
                           const uint64_t* versions, uint64_t n, uint64_t* replaced_out);
+/* insert with the entry count produced on the device (*count <= n_max); versions may be
+ * NULL (= kBulkLoadVersion); skip[i] != 0 (may be NULL) drops entry i without an access. */
+int hps_gpu_cache_insert_count(hps_gpu_cache cache, const uint64_t* keys, const float* vecs,
+                               const uint64_t* versions, uint64_t n_max, const uint64_t* count,
+                               const uint8_t* skip, uint64_t* admitted_out);
+/* Orchestrator read-through after a cache query: out[i] (input order) =
+ * the hit row, else the row of keys[i] in `table` (or its default vector). The misses are
+ * listed (miss_keys, miss_vecs, miss_absent) for hps_gpu_cache_insert_count. counts =
+ * the query's device counts [n_found, n_missing]. */
+int hps_gpu_table_read_through(hps_gpu_table tbl, uint32_t table, const uint64_t* keys, const float* found_vecs,
+                               const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
+                               uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent);
 /* syncs. */
 int hps_gpu_cache_stats(hps_gpu_cache cache, hps_cache_stats* stats_host);
 int hps_gpu_cache_reset_stats(hps_gpu_cache cache);

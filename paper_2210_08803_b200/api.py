@@ -271,3 +271,32 @@ class HotCache:
             self.close()
         except Exception:
             pass
+
+
+class CachedLookup:
+    """Orchestrator read-through for one table: the HPS GPU cache (L1) in
+    front of a GPU-resident backing table. lookup() = cache query -> misses read from the
+    table (default vector when absent) -> misses migrated into the cache (absent keys are
+    never cached) -> rows in input order. Three C-ABI calls, no host round trip."""
+
+    def __init__(self, cache: HotCache, table: EmbeddingTableGroup, table_id: int = 0):
+        self.cache, self.table, self.table_id = cache, table, table_id
+        self.lib, self.dim, self.device = cache.lib, cache.dim, cache.device
+        n = cache.max_batch
+        self.found = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
+        self.out = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
+        self.miss_keys = torch.empty(n, dtype=torch.int64, device=self.device)
+        self.miss_vecs = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
+        self.miss_absent = torch.empty(n, dtype=torch.uint8, device=self.device)
+        self.admitted = torch.zeros(1, dtype=torch.int64, device=self.device)
+
+    def lookup(self, keys: torch.Tensor) -> torch.Tensor:
+        n = keys.numel()
+        fv, fi, mi, cnt = self.cache.query_async(keys, found_vecs=self.found)
+        L.check(self.lib.hps_gpu_table_read_through(self.table.h, self.table_id, _ptr(keys), _ptr(fv), _ptr(fi),
+                                                    _ptr(mi), _ptr(cnt), n, _ptr(self.out), _ptr(self.miss_keys),
+                                                    _ptr(self.miss_vecs), _ptr(self.miss_absent)), "read_through")
+        L.check(self.lib.hps_gpu_cache_insert_count(self.cache.h, _ptr(self.miss_keys), _ptr(self.miss_vecs), None, n,
+                                                    C.c_void_p(cnt.data_ptr() + 8), _ptr(self.miss_absent),
+                                                    _ptr(self.admitted)), "cache_insert_count")
+        return self.out[:n]

@@ -219,11 +219,13 @@ template <int LPR>
 __global__ void __launch_bounds__(256) k_entry_prep(const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
                                                     uint64_t n, uint32_t dim, hps::FastMod64 fm, uint32_t invalid_set,
                                                     uint32_t* __restrict__ set_out, uint8_t* __restrict__ valid_out,
-                                                    uint32_t* status, uint64_t* counts) {
+                                                    uint32_t* status, uint64_t* counts, const uint64_t* d_n,
+                                                    const uint8_t* __restrict__ skip) {
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
   const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
   const uint32_t nvec = dim / 4;
+  if (d_n) n = min(n, *d_n);  // entry count produced on the device (read-through path)
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = n;
   const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
   const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
@@ -237,8 +239,9 @@ __global__ void __launch_bounds__(256) k_entry_prep(const uint64_t* __restrict__
     bad = __any_sync(gmask, bad);
     if (gl == 0) {
       if (bad) latch_status(status, HPS_GPU_E_NON_FINITE);
-      set_out[i] = bad ? invalid_set : static_cast<uint32_t>(fm.mod(hps::key_hash(keys[i])));
-      valid_out[i] = bad ? 0 : 1;
+      const bool skipped = bad || (skip && skip[i]);  // skip: absent from the backing store, never cached
+      set_out[i] = skipped ? invalid_set : static_cast<uint32_t>(fm.mod(hps::key_hash(keys[i])));
+      valid_out[i] = skipped ? 0 : 1;
     }
   }
 }
@@ -293,7 +296,7 @@ __global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict_
     uint64_t acc = set_acc[s];
     for (uint32_t j = lo; j < hi; ++j) {
       const uint32_t i = idx_sorted[j];
-      const uint64_t k = keys[i], ver = versions[i];
+      const uint64_t k = keys[i], ver = versions ? versions[i] : hps::kBulkLoadVersion;
       const uint64_t t = clock0 + rank[i] + 1;
       if (++acc >= aging_period) {
         acc = 0;
@@ -576,12 +579,13 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
   return HPS_GPU_OK;
 }
 
-static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n) {
+static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n,
+                      const uint64_t* d_n = nullptr, const uint8_t* skip = nullptr) {
   cudaStream_t st = c->ctx->stream;
   const int lpr = lpr_for(c->dim);
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
   const uint32_t invalid = static_cast<uint32_t>(c->num_sets);
-#define HPSG_P(L) k_entry_prep<L><<<grid, 256, 0, st>>>(keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts)
+#define HPSG_P(L) k_entry_prep<L><<<grid, 256, 0, st>>>(keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts, d_n, skip)
   switch (lpr) {
     case 32: HPSG_P(32); break;
     case 16: HPSG_P(16); break;
@@ -595,15 +599,15 @@ static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, 
   return HPS_GPU_OK;
 }
 
-int hps_gpu_cache_insert(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions, uint64_t n,
-                         uint64_t* admitted_out) {
+static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions,
+                       uint64_t n, const uint64_t* d_n, uint64_t* admitted_out, const uint8_t* skip = nullptr) {
   if (int s = check_cache(c)) return s;
   if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = c->ctx->stream;
   if (admitted_out) HPSG_CUDA(cudaMemsetAsync(admitted_out, 0, sizeof(uint64_t), st));
   if (n == 0) return HPS_GPU_OK;
-  if (!keys || !vecs || !versions) return HPS_GPU_E_INVALID_ARGUMENT;
-  if (int s = entry_prep(c, keys, vecs, n)) return s;
+  if (!keys || !vecs) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (int s = entry_prep(c, keys, vecs, n, d_n, skip)) return s;
   const uint64_t tiles = scan_tiles(n);
   HPSG_CUDA(cudaMemsetAsync(c->ws_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
   RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
@@ -618,6 +622,18 @@ int hps_gpu_cache_insert(hps_gpu_cache c, const uint64_t* keys, const float* vec
                                                    c->d_touch, c->d_set_acc, c->d_vec, c->d_state, admitted_out);
   HPSG_CHECK_LAUNCH("cache insert");
   return HPS_GPU_OK;
+}
+
+int hps_gpu_cache_insert(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions, uint64_t n,
+                         uint64_t* admitted_out) {
+  if (n && !versions) return HPS_GPU_E_INVALID_ARGUMENT;
+  return insert_impl(c, keys, vecs, versions, n, nullptr, admitted_out);
+}
+
+int hps_gpu_cache_insert_count(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions,
+                               uint64_t n_max, const uint64_t* d_count, const uint8_t* skip, uint64_t* admitted_out) {
+  if (!d_count) return HPS_GPU_E_INVALID_ARGUMENT;
+  return insert_impl(c, keys, vecs, versions, n_max, d_count, admitted_out, skip);
 }
 
 int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions,

@@ -367,6 +367,51 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a
   if (lane == 0) bulk_wait_all();
 }
 
+// Orchestrator read-through (one table): hits come from the cache's
+// compacted rows, misses from this table (or its default vector when absent); the misses
+// are listed in input order for migration into the cache (absent keys flagged: never cached).
+template <int LPR>
+__global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict__ keys,
+                                                      const float* __restrict__ found_vecs,
+                                                      const uint32_t* __restrict__ found_idx,
+                                                      const uint32_t* __restrict__ missing_idx, const uint64_t* counts,
+                                                      const Slot* __restrict__ slots, TableDev td,
+                                                      const float* __restrict__ W, const float* __restrict__ def,
+                                                      uint32_t dim, float* __restrict__ out, uint64_t* miss_keys,
+                                                      float* miss_vecs, uint8_t* miss_absent) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
+  const uint64_t nf = counts[0], nm = counts[1];
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t j = gid; j < nf + nm; j += ng) {
+    const float4* src;
+    float4* dst2 = nullptr;
+    uint32_t i;
+    if (j < nf) {
+      i = found_idx[j];
+      src = reinterpret_cast<const float4*>(found_vecs + j * dim);
+    } else {
+      const uint64_t m = j - nf;
+      i = missing_idx[m];
+      const uint64_t k = keys[i];
+      const uint32_t local = probe_find(slots, td, k);
+      src = reinterpret_cast<const float4*>(local == kRowEmpty ? def : W + (td.row_base + local) * dim);
+      dst2 = reinterpret_cast<float4*>(miss_vecs + m * dim);
+      if (gl == 0) {
+        miss_keys[m] = k;
+        miss_absent[m] = local == kRowEmpty ? 1 : 0;
+      }
+    }
+    float4* dst = reinterpret_cast<float4*>(out + uint64_t(i) * dim);
+    for (uint32_t v = gl; v < nvec; v += LPR) {
+      const float4 x = __ldg(src + v);
+      dst[v] = x;
+      if (dst2) dst2[v] = x;
+    }
+  }
+}
+
 // Multi-hot path: a group of LPR lanes owns one bag at a time; the group probes LPR
 // keys of the bag in parallel, then accumulates the rows in bag order (4 in flight).
 template <int LPR, int VPL>
@@ -800,6 +845,32 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   t->last_multi = multi;
   t->last_combiner = combiner;
   t->last_n_keys_host = n_keys_host;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* keys, const float* found_vecs,
+                               const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
+                               uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent) {
+  if (int s = check_tbl(t)) return s;
+  if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
+  if (n == 0) return HPS_GPU_OK;
+  if (!keys || !found_vecs || !found_idx || !missing_idx || !counts || !out || !miss_keys || !miss_vecs || !miss_absent)
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  const uint32_t nvec = t->dim / 4;
+  const int lpr = nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
+  const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
+  cudaStream_t st = t->ctx->stream;
+  const TableDev td = t->h_tables[table];
+  const float* def = t->d_defaults + uint64_t(table) * t->dim;
+  switch (lpr) {
+    case 32: k_read_through<32><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
+    case 16: k_read_through<16><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
+    case 8: k_read_through<8><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
+    case 4: k_read_through<4><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
+    case 2: k_read_through<2><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
+    default: k_read_through<1><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
+  }
+  HPSG_CHECK_LAUNCH("k_read_through");
   return HPS_GPU_OK;
 }
 

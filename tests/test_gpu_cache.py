@@ -154,3 +154,39 @@ def test_zipf_hit_rate_bound(ctx):
     run(200_000, 200_000)
     s = g.stats()
     assert s["hits"] / s["queries"] >= 0.9 * M, (s, M)
+
+
+def test_read_through_matches_oracle(ctx):
+    """Cache + backing table read-through: outputs in input order, hits/misses, migration
+    of misses (absent keys never cached), bit-exact with the oracle cache + a dict table."""
+    from paper_2210_08803_b200 import EmbeddingTableGroup
+    from paper_2210_08803_b200.api import CachedLookup
+    dim, n_keys, cap = 8, 5000, 512
+    rs = np.random.default_rng(17)
+    keys_all = W.mix64(np.arange(n_keys, dtype=np.uint64))
+    table = EmbeddingTableGroup(ctx, [n_keys], dim, [0], "sgd", 4096, 4096, 3)
+    table.insert(0, t64(keys_all))
+    default = np.full(dim, 0.5, np.float32)
+    table.set_default_vector(0, default)
+    rows = table.export(0, 0, n_keys)[0].cpu().numpy()
+    truth = {int(k): rows[i] for i, k in enumerate(keys_all)}
+    cache = HotCache(ctx, cap, dim, 8, 0, 4096)
+    rt = CachedLookup(cache, table)
+    ocache = O.OracleCache(cap, dim, 8, 0)
+    z = W.Zipf(n_keys + 200, 1.1)
+    for rnd in range(20):
+        ranks = z.ranks(W.rng(rnd, np.arange(int(rs.integers(1, 3000)), dtype=np.uint64)))
+        q = W.mix64(ranks.astype(np.uint64))  # ranks >= n_keys are absent from the table
+        got = rt.lookup(t64(q)).cpu().numpy()
+        fi, fv, mi = ocache.query(q)
+        want = np.empty((len(q), dim), np.float32)
+        want[fi] = fv
+        miss = q[mi]
+        mrows = np.stack([truth.get(int(k), default) for k in miss]) if len(mi) else np.zeros((0, dim), np.float32)
+        want[mi] = mrows
+        present = np.array([int(k) in truth for k in miss], dtype=bool)
+        if present.any():
+            ocache.insert(miss[present], mrows[present], np.zeros(int(present.sum()), np.uint64))
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+        assert cache.stats() == ocache.stats(), rnd
+    assert cache.size() == ocache.size()
