@@ -8,7 +8,10 @@ hps_gpu_backward_update on synthetic keys; d_out (the dense model's gradient, ou
 scope) is a pre-generated device tensor. Multi-GPU: distributed slot sharding
 (owner = key_hash mod G) through paper_2210_08803_b200.sharded.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg3] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg1|cfg3|cfg5] [--impl ours|reference]
+
+cfg5 = one hashed table over a 1e9-key space (power-law keys), dim 128, Adam; rows
+materialise on first touch (insert-on-miss inside the step, HPS_LOOKUP_INSERT).
 
 Prints ONE JSON line (rank 0). `--impl reference` times the CPU implementation of the
 same step (the oracle port, all host threads) on a bounded sample.
@@ -39,7 +42,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg5"])
     ap.add_argument("--batch-per-gpu", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pool", type=int, default=4, help="distinct synthetic batches rotated through")
@@ -55,8 +58,10 @@ def get_config(args):
         cfg = W.config1()
     elif args.config == "cfg2":
         cfg = W.config2()
-    else:
+    elif args.config == "cfg3":
         cfg = W.config3()
+    else:
+        cfg = W.config5()
     if args.batch_per_gpu:
         cfg.batch = args.batch_per_gpu
     if args.table_scale != 1.0:
@@ -203,6 +208,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = get_config(args)
+    if cfg.keyspace:  # every step sees a fresh batch, so new keys keep materialising inside the timed steps
+        args.pool = max(args.pool, args.warmup + args.steps)
     if args.impl == "reference":
         return reference_arm(args, cfg, rank, world)
 
@@ -321,7 +328,8 @@ def main():
                        "tables": len(cfg.cards), "rows": int(sum(cfg.cards)), "dim": cfg.dim,
                        "hot": cfg.hot, "combiner": cfg.combiner, "optimizer": cfg.optimizer,
                        "parallelism": f"distributed-slot x{world}" if world > 1 else "single",
-                       "l2": "flushed between timed steps (256 MB write)", "graph": step_fn.graph_mode},
+                       "l2": "flushed between timed steps (256 MB write)", "graph": step_fn.graph_mode,
+                       "keyspace": cfg.keyspace, "insert_on_miss": step_fn.insert_missing},
             "roofline": {"bound": "hbm", "kernel": "k_lookup_1hot (fused hash+probe+gather+pool)" if cfg.hot == 1
                          else "k_lookup_multi (fused hash+probe+gather+pool)",
                          "achieved": fwd_gbs, "peak": peak, "unit": "GB/s", "frac": fwd_gbs / peak,

@@ -142,7 +142,9 @@ int hps_gpu_table_row_keys(hps_gpu_table tbl, uint32_t table, uint64_t row_begin
 
 enum {
   HPS_LOOKUP_KEYS_HOST = 1u << 0,  /* keys/offsets are pinned HOST memory: staged H2D inside the call */
-  HPS_LOOKUP_TRAIN = 1u << 1       /* remember per-key rows/bags for the following backward_update */
+  HPS_LOOKUP_TRAIN = 1u << 1,      /* remember per-key rows/bags for the following backward_update */
+  HPS_LOOKUP_INSERT = 1u << 2      /* dynamic table: insert absent keys first (single-table groups,
+                                      host-known key count); rows materialise on first touch */
 };
 
 /* K1+K2+K3 fused: out[bag*dim + j] = combiner over the bag's rows, fp32, keys in bag

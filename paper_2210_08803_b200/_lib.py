@@ -29,7 +29,7 @@ E_NO_DEVICE = 258
 
 OPT_SGD, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2
 COMBINER_SUM, COMBINER_MEAN = 0, 1
-LOOKUP_KEYS_HOST, LOOKUP_TRAIN = 1, 2
+LOOKUP_KEYS_HOST, LOOKUP_TRAIN, LOOKUP_INSERT = 1, 2, 4
 PLAN_LOCALIZED, PLAN_DISTRIBUTED, PLAN_HYBRID = 0, 1, 2
 
 

@@ -163,11 +163,12 @@ class EmbeddingTableGroup:
 
     def lookup(self, keys: torch.Tensor, n_samples: int, offsets: Optional[torch.Tensor] = None,
                combiner: str = "sum", train: bool = False, out: Optional[torch.Tensor] = None,
-               keys_on_host: bool = False) -> torch.Tensor:
+               keys_on_host: bool = False, insert_missing: bool = False) -> torch.Tensor:
         n_bags = n_samples * self.n_slots
         if out is None:
             out = torch.empty(n_bags, self.dim, dtype=torch.float32, device=self.device)
-        flags = (L.LOOKUP_TRAIN if train else 0) | (L.LOOKUP_KEYS_HOST if keys_on_host else 0)
+        flags = (L.LOOKUP_TRAIN if train else 0) | (L.LOOKUP_KEYS_HOST if keys_on_host else 0) | \
+            (L.LOOKUP_INSERT if insert_missing else 0)
         if not keys_on_host:
             _need_cuda(keys, "keys")
             if offsets is not None:

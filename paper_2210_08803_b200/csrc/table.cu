@@ -660,6 +660,10 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->ws_abort, 4));
   A(dalloc(&t->ws_keys_stage, N));
   A(dalloc(&t->ws_offsets_stage, B + 1));
+  A(dalloc(&t->ws_ins_slot, N));
+  A(dalloc(&t->ws_ins_pos, N));
+  A(dalloc(&t->ws_ins_flag, N));
+  A(dalloc(&t->ws_ins_scan, scan_tiles(N) + 1));
   if (st) {
     hps_gpu_table_destroy(t);
     return st;
@@ -686,7 +690,7 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
                   t->ws_seg_start, t->ws_seg_end,  t->ws_long_seg,  t->ws_long_base,  t->ws_task_long,
                   t->ws_partial2,
                   t->ws_partial,  t->ws_counts,    t->ws_zero,      t->ws_abort,      t->ws_keys_stage,
-                  t->ws_offsets_stage};
+                  t->ws_offsets_stage, t->ws_ins_slot, t->ws_ins_pos, t->ws_ins_flag, t->ws_ins_scan};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete t;
@@ -730,11 +734,20 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
   uint8_t* ws_flag = nullptr;
   uint64_t* scan_status = nullptr;
   const uint64_t tiles = scan_tiles(n);
-  // Insert is a bulk/setup call, not a hot call: its scratch is stream-ordered.
-  HPSG_CUDA(cudaMallocAsync(&ws_slot, n * sizeof(uint64_t), st));
-  HPSG_CUDA(cudaMallocAsync(&ws_pos, n * sizeof(uint32_t), st));
-  HPSG_CUDA(cudaMallocAsync(&ws_flag, n, st));
-  HPSG_CUDA(cudaMallocAsync(&scan_status, (tiles + 1) * sizeof(uint64_t), st));
+  // Batches up to max_keys (insert-on-miss inside a step) use the preallocated scratch;
+  // larger bulk loads take stream-ordered allocations.
+  const bool own = n > t->max_keys;
+  if (own) {
+    HPSG_CUDA(cudaMallocAsync(&ws_slot, n * sizeof(uint64_t), st));
+    HPSG_CUDA(cudaMallocAsync(&ws_pos, n * sizeof(uint32_t), st));
+    HPSG_CUDA(cudaMallocAsync(&ws_flag, n, st));
+    HPSG_CUDA(cudaMallocAsync(&scan_status, (tiles + 1) * sizeof(uint64_t), st));
+  } else {
+    ws_slot = t->ws_ins_slot;
+    ws_pos = t->ws_ins_pos;
+    ws_flag = t->ws_ins_flag;
+    scan_status = t->ws_ins_scan;
+  }
   HPSG_CUDA(cudaMemsetAsync(scan_status, 0, (tiles + 1) * sizeof(uint64_t), st));
   HPSG_CUDA(cudaMemsetAsync(t->ws_abort, 0, sizeof(uint32_t), st));
   HPSG_CUDA(cudaMemsetAsync(t->ws_counts + 3, 0, sizeof(uint64_t), st));
@@ -751,10 +764,12 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
   k_insert_finish<<<grid, 256, 0, st>>>(t->d_slots, td, table, n, ws_slot, rows_out, t->ws_counts + 3, t->d_nrows,
                                         t->ws_abort);
   HPSG_CHECK_LAUNCH("insert");
-  HPSG_CUDA(cudaFreeAsync(ws_slot, st));
-  HPSG_CUDA(cudaFreeAsync(ws_pos, st));
-  HPSG_CUDA(cudaFreeAsync(ws_flag, st));
-  HPSG_CUDA(cudaFreeAsync(scan_status, st));
+  if (own) {
+    HPSG_CUDA(cudaFreeAsync(ws_slot, st));
+    HPSG_CUDA(cudaFreeAsync(ws_pos, st));
+    HPSG_CUDA(cudaFreeAsync(ws_flag, st));
+    HPSG_CUDA(cudaFreeAsync(scan_status, st));
+  }
   return HPS_GPU_OK;
 }
 
@@ -818,6 +833,15 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
     if (multi) offsets = t->ws_offsets_stage;
   } else if (!multi && n_bags > t->max_keys) {
     return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (flags & HPS_LOOKUP_INSERT) {
+    // Dynamic table (keys materialise on first touch): insert the batch's keys first, in
+    // batch order, so new rows get deterministic ids; then the lookup finds all of them.
+    if (t->n_tables != 1 || (multi && !(flags & HPS_LOOKUP_KEYS_HOST))) {
+      set_last_error("HPS_LOOKUP_INSERT needs a single-table group and a host-known key count");
+      return HPS_GPU_E_INVALID_ARGUMENT;
+    }
+    if (int s = hps_gpu_table_insert(t, 0, keys, n_keys_host, nullptr, nullptr)) return s;
   }
   const bool train = (flags & HPS_LOOKUP_TRAIN) != 0;
   LookupArgs a{};
@@ -887,6 +911,10 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
     return HPS_GPU_OK;
   }
   if (!keys || !tables || !rows_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (flags & HPS_LOOKUP_INSERT) {  // dynamic single-table shard: materialise absent keys first
+    if (t->n_tables != 1) return HPS_GPU_E_INVALID_ARGUMENT;
+    if (int s = hps_gpu_table_insert(t, 0, keys, n, nullptr, nullptr)) return s;
+  }
   LookupArgs a{};
   a.keys = keys;
   a.n_bags = static_cast<uint32_t>(n);

@@ -59,6 +59,11 @@ struct hps_gpu_table_s {
   size_t zero_words = 0;
   uint32_t* ws_abort = nullptr;
   uint64_t* ws_keys_stage = nullptr;
+  // insert scratch for batches up to max_keys (insert-on-miss runs inside the step)
+  uint64_t* ws_ins_slot = nullptr;
+  uint32_t* ws_ins_pos = nullptr;
+  uint8_t* ws_ins_flag = nullptr;
+  uint64_t* ws_ins_scan = nullptr;
   uint32_t* ws_offsets_stage = nullptr;
   // last training lookup
   bool have_train = false, last_multi = false, sorted_in_b = false;

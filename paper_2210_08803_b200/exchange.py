@@ -42,8 +42,10 @@ def _ptr(t):
 class GpuEngine:
     """Device side of the exchange on one rank: a table-group shard + an exchange plan."""
 
-    def __init__(self, ctx, table, slot_table: List[int], max_keys: int, n_shards: int):
+    def __init__(self, ctx, table, slot_table: List[int], max_keys: int, n_shards: int,
+                 insert_missing: bool = False):
         self.ctx, self.table, self.lib = ctx, table, ctx.lib
+        self.insert_flag = L.LOOKUP_INSERT if insert_missing else 0
         self.dim = table.dim
         self.device = table.device
         self.slot_table = torch.tensor(slot_table, dtype=torch.int32, device=self.device)
@@ -76,7 +78,7 @@ class GpuEngine:
         n = keys.numel()
         rows = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
         L.check(self.lib.hps_gpu_gather_rows(self.table.h, _ptr(keys), _ptr(tables), n, _ptr(rows),
-                                             L.LOOKUP_TRAIN if train else 0), "gather_rows")
+                                             (L.LOOKUP_TRAIN if train else 0) | self.insert_flag), "gather_rows")
         return rows
 
     def pool_rows(self, rows, perm, offsets, n_bags: int, combiner: int) -> torch.Tensor:

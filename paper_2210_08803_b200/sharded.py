@@ -39,9 +39,12 @@ def build_tables(ctx: Context, cfg: W.Config, rank: int = 0, world: int = 1,
     n_bags_cap = n_bags if world == 1 else max(n_bags * world, max_keys)
     caps = []
     for c in cfg.cards:
-        caps.append(c if world == 1 else int(c / world * 1.02 + 64 * math.sqrt(c / world + 1) + 64))
+        # a hashed table's card is already the per-GPU row pool
+        caps.append(c if world == 1 or cfg.keyspace else int(c / world * 1.02 + 64 * math.sqrt(c / world + 1) + 64))
     g = EmbeddingTableGroup(ctx, caps, cfg.dim, cfg.slots() if world == 1 else list(range(len(cfg.cards))),
                             cfg.optimizer, max_batch_keys=max_keys, max_batch_bags=n_bags_cap, init_seed=cfg.seed)
+    if cfg.keyspace:  # hashed table: rows materialise on first touch (HPS_LOOKUP_INSERT)
+        return g
     for t, c in enumerate(cfg.cards):
         for first in range(0, c, chunk):
             n = min(chunk, c - first)
@@ -61,6 +64,7 @@ class TrainStep:
         self.n_bags = cfg.batch * cfg.n_slots
         self.out = torch.empty(self.n_bags, cfg.dim, dtype=torch.float32, device="cuda")
         self.params = opt_params(cfg.optimizer, cfg.lr, eps=cfg.eps)
+        self.insert_missing = bool(cfg.keyspace)
         self.graph_mode = bool(use_graph and world == 1 and cfg.optimizer != "adam")
         self._graphs = {}
         # lookup + dedup scan + scatter + short reduce + long sort/chunks/combine
@@ -70,7 +74,7 @@ class TrainStep:
         if world > 1:
             from .exchange import DistributedExchange, GpuEngine
             max_keys = table_max_keys(cfg, 1)
-            self.engine = GpuEngine(ctx, table, cfg.slots(), max_keys, world)
+            self.engine = GpuEngine(ctx, table, cfg.slots(), max_keys, world, insert_missing=self.insert_missing)
             self.exchange = DistributedExchange(self.engine, cfg.combiner, rank, world)
             # bucketize (owner + hist + 1 radix pass + pack + counts) + gather + pool
             # + scatter + backward (hist + passes + scan + 3 reduce kernels) [+ occ_bags]
@@ -92,7 +96,7 @@ class TrainStep:
         if self.cfg.optimizer == "adam":
             self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
         self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=True,
-                          out=self.out, keys_on_host=keys_on_host)
+                          out=self.out, keys_on_host=keys_on_host, insert_missing=self.insert_missing)
         self.table.backward_update(dout, self.cfg.lr, params=self.params)
 
     def _exchange_step(self, keys, offs, dout, step):
@@ -149,4 +153,4 @@ class TrainStep:
             self.exchange.forward(b["keys"], b["offs"], self.n_bags, train=False)
             return
         self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=False,
-                          out=self.out)
+                          out=self.out)  # roofline leg: batches were materialised by the timed steps

@@ -101,6 +101,7 @@ class Config:
     eps: float = 1e-8
     seed: int = 0x5EED0000
     slot_table: List[int] = field(default_factory=list)
+    keyspace: Optional[int] = None  # dynamic (hashed) table: keys drawn from [0, keyspace), rows on first touch
 
     @property
     def n_slots(self) -> int:
@@ -126,6 +127,28 @@ def config3(batch_per_gpu: int = 6912) -> Config:
                   zipf_s=1.1, combiner="mean", optimizer="adagrad", eps=1e-7, seed=0x5EED0003)
 
 
+def config5(batch_per_gpu: int = 6912, capacity: int = 90_000_000) -> Config:
+    """Large hashed table: 26 one-hot slots into ONE table over a 1e9-key space, dim 128,
+    Adam, power-law (Zipf 1.05, continuous inverse) keys. fp32 Adam state for 1e9 rows does
+    not fit 8 x 180 GB (SURVEY hard part 6), so rows materialise on first touch into a
+    `capacity`-row pool per GPU (HPS_LOOKUP_INSERT)."""
+    return Config("cfg5-hashed1e9-d128-adam", [capacity], 128, batch_per_gpu, zipf_s=1.05, optimizer="adam",
+                  lr=0.001, seed=0x5EED0005, slot_table=[0] * 26, keyspace=1_000_000_000)
+
+
+class PowerLaw:
+    """Continuous-inverse Zipf(s) over ranks 1..n for n too large for a CDF table."""
+
+    def __init__(self, n: int, s: float):
+        self.n, self.s = n, s
+        self.a = n ** (1.0 - s) - 1.0
+
+    def ranks(self, r: np.ndarray) -> np.ndarray:
+        u = (r >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+        x = (self.a * u + 1.0) ** (1.0 / (1.0 - self.s))
+        return np.minimum(np.floor(x).astype(np.int64) - 1, self.n - 1)
+
+
 class BatchGen:
     """Deterministic batches: keys (sample-major bags), optional CSR offsets, and table-row indices."""
 
@@ -134,10 +157,14 @@ class BatchGen:
         self.cards = cards if cards is not None else cfg.cards
         self.slot_table = cfg.slots()
         self._zipf = {}
+        # hashed tables draw indices from the logical key space, not from the row pool
+        space = (lambda t: cfg.keyspace) if cfg.keyspace else (lambda t: self.cards[t])
         if cfg.zipf_s is not None:
             for t in set(self.slot_table):
-                self._zipf[t] = Zipf(self.cards[t], cfg.zipf_s)
-        self._perm = {t: affine_perm(cfg.seed + 77 * t, self.cards[t]) for t in set(self.slot_table)}
+                self._zipf[t] = (PowerLaw(space(t), cfg.zipf_s) if cfg.keyspace
+                                 else Zipf(space(t), cfg.zipf_s))
+        self._perm = {t: affine_perm(cfg.seed + 77 * t, space(t)) for t in set(self.slot_table)}
+        self._space = space
 
     def batch(self, step: int, batch: Optional[int] = None, first_sample: int = 0):
         """Returns (keys u64[N], offsets u32[B*S+1] or None, table_idx i64[N], table_of i32[N])."""
@@ -163,7 +190,7 @@ class BatchGen:
         keys = np.empty(N, dtype=np.uint64)
         for t in np.unique(table_of):
             m = table_of == t
-            card = self.cards[t]
+            card = self._space(t)
             if cfg.zipf_s is None:
                 ix = uniform_index(r[m], card)
             else:

@@ -272,3 +272,49 @@ def test_train_lookup_twice_without_backward(ctx):
     o.backward_update(d, p)
     ctx.sync()
     assert close(g.export(0, 0, 500)[0].cpu().numpy(), o.export(0, 0, 500)[0])
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_insert_on_miss_train_parity(ctx, multi):
+    """Config-5 shape at small scale: one hashed table, rows materialise on first touch
+    (HPS_LOOKUP_INSERT), Adam. The oracle inserts the batch (first-occurrence rows) then
+    looks up: same rows, same init, same updates."""
+    from paper_2210_08803_b200 import workload as W
+    cfg = W.config5(batch_per_gpu=128, capacity=40_000)
+    cfg.dim, cfg.keyspace = 64, 2_000_000
+    if multi:
+        cfg.hot = 3
+    gen = W.BatchGen(cfg)
+    g, o = make_pair(ctx, cfg.cards, cfg.dim, cfg.slots(), "adam", max_keys=1 << 15, max_bags=1 << 13)
+    rs = np.random.default_rng(3)
+    for step in range(1, 5):
+        keys, offs, _, _ = gen.batch(step)
+        if multi:
+            kh = torch.from_numpy(keys.view(np.int64)).pin_memory()
+            oh = torch.from_numpy(offs.view(np.int32)).pin_memory()
+            out = g.lookup(kh, cfg.batch, offsets=oh, train=True, keys_on_host=True, insert_missing=True)
+        else:
+            out = g.lookup(t64(keys), cfg.batch, train=True, insert_missing=True)
+        st, _ = o.insert(0, keys)
+        assert st == 0
+        ref = o.lookup(keys, cfg.batch, offsets=offs, train=True)
+        assert close(out.cpu().numpy(), ref)
+        dout = (rs.standard_normal(ref.shape) * 0.1).astype(np.float32)
+        p = opt_params("adam", 0.01, step=step)
+        g.backward_update(torch.from_numpy(dout).cuda(), 0.01, params=p)
+        o.backward_update(dout, p)
+        ctx.sync()
+        assert g.size(0) == o.size(0)
+    n = g.size(0)
+    assert n > cfg.batch  # rows really materialised on first touch
+    np.testing.assert_array_equal(g.row_keys(0, 0, n).cpu().numpy().view(np.uint64), o.row_keys(0, 0, n))
+    w, s0, s1 = g.export(0, 0, n)
+    ow, os0, os1 = o.export(0, 0, n)
+    assert close(w.cpu().numpy(), ow) and close(s0.cpu().numpy(), os0) and close(s1.cpu().numpy(), os1)
+
+
+def test_insert_on_miss_rejects_multi_table(ctx):
+    g, _ = make_pair(ctx, [100, 100], 8, [0, 1])
+    with pytest.raises(HpsError) as e:
+        g.lookup(t64(np.arange(8, dtype=np.uint64)), 4, insert_missing=True)
+    assert e.value.code == 1
