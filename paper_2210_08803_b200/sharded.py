@@ -79,6 +79,8 @@ class TrainStep:
             # bucketize (owner + hist + 1 radix pass + pack + counts) + gather + pool
             # + scatter + backward (hist + passes + scan + 3 reduce kernels) [+ occ_bags]
             self.kernels_per_step = 5 + 1 + 1 + 1 + 7 + (1 if cfg.hot > 1 else 0)
+        if self.insert_missing:  # claim + scan + commit + finish
+            self.kernels_per_step += 4
 
     # -- inputs -------------------------------------------------------------------------
     def stage_batch(self, keys: np.ndarray, offs: Optional[np.ndarray]):

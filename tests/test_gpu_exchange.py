@@ -97,3 +97,5 @@ def test_distributed_step_single_rank_nccl(ctx):
         ctx.sync()
     for t, c in enumerate(cards):
         assert np.array_equal(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])
+    ex.e.close()
+    dist.destroy_process_group()
