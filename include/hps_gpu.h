@@ -196,6 +196,10 @@ int hps_gpu_scatter_grads(hps_gpu_ctx ctx, const float* d_out, const uint32_t* p
 int hps_gpu_regroup_bags(hps_gpu_ctx ctx, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,
                          uint32_t n_slots, const uint32_t* sel, uint32_t n_sel, uint32_t* lens_ws,
                          uint64_t* out_keys, uint32_t* out_offsets, uint64_t* scan_ws);
+/* offsets_out[0..n] = exclusive scan of lens[0..n) (the owner's CSR over received bag
+ * lengths). scan_ws: scan_tiles(n)+1 u64. */
+int hps_gpu_lengths_to_offsets(hps_gpu_ctx ctx, const uint32_t* lens, uint64_t n, uint32_t* offsets_out,
+                               uint64_t* scan_ws);
 /* direction 0: dst[b*n_slots + sel[j]] = src[b*n_sel + j]; direction 1: the reverse gather. */
 int hps_gpu_place_pooled(hps_gpu_ctx ctx, const float* src, const uint32_t* sel, uint32_t n_sel,
                          uint32_t n_samples, uint32_t n_slots, uint32_t dim, int direction, float* dst);

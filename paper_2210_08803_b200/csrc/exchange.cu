@@ -303,6 +303,23 @@ int hps_gpu_regroup_bags(hps_gpu_ctx ctx, const uint64_t* keys, const uint32_t* 
   return HPS_GPU_OK;
 }
 
+int hps_gpu_lengths_to_offsets(hps_gpu_ctx ctx, const uint32_t* lens, uint64_t n, uint32_t* offsets_out,
+                               uint64_t* scan_ws) {
+  if (!ctx || !offsets_out || !scan_ws || (n && !lens)) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = ctx->stream;
+  const uint64_t tiles = scan_tiles(n);
+  if (n == 0) {
+    HPSG_CUDA(cudaMemsetAsync(offsets_out, 0, 4, st));
+    return HPS_GPU_OK;
+  }
+  HPSG_CUDA(cudaMemsetAsync(scan_ws, 0, (tiles + 1) * sizeof(uint64_t), st));
+  OffsetsOp op{lens, offsets_out, n};
+  k_scan<OffsetsOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(
+      op, scan_ws, reinterpret_cast<uint32_t*>(scan_ws + tiles));
+  HPSG_CHECK_LAUNCH("lengths_to_offsets");
+  return HPS_GPU_OK;
+}
+
 int hps_gpu_place_pooled(hps_gpu_ctx ctx, const float* src, const uint32_t* sel, uint32_t n_sel, uint32_t n_samples,
                          uint32_t n_slots, uint32_t dim, int direction, float* dst) {
   if (!ctx || !src || !sel || !dst || dim == 0 || dim % 4) return HPS_GPU_E_INVALID_ARGUMENT;

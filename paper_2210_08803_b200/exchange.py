@@ -146,3 +146,152 @@ class DistributedExchange:
         off_send = sum(c for g, c in enumerate(sc) if g != self.rank)
         off_recv = sum(c for g, c in enumerate(rc) if g != self.rank)
         return off_send * (8 + 4 + dim * 4) + off_recv * dim * 4
+
+
+# ---------------------------------------------------------------------------------------
+# Localized slot placement (config 3)
+# ---------------------------------------------------------------------------------------
+#
+#   requester  regroup its bags by owner of the slot (sample-major CSR)  hps_gpu_regroup_bags
+#   all-to-all keys (+ bag lengths for multi-hot)
+#   owner      offsets over the received lengths                          hps_gpu_lengths_to_offsets
+#              pooled lookup over every rank's samples of its slots       hps_gpu_lookup_pooled
+#   all-to-all pooled [b x S_owned x D] blocks back (batch dimension)
+#   requester  place the blocks into [b x S x D]                          hps_gpu_place_pooled
+#   ... dense model ...
+#   requester  gather d_out per owner                                     hps_gpu_place_pooled(1)
+#   all-to-all gradients
+#   owner      dedup + blocked reduction + optimizer                      hps_gpu_backward_update
+#
+# The owner's bags arrive rank-major (rank 0's samples, then rank 1's, ...), which is the
+# global sample order, so the owner's lookup and backward are the single-GPU kernels on the
+# global batch restricted to its slots: bit-identical to one unsharded table group.
+
+
+class LocalizedGpuEngine:
+    """Device side of localized slot placement on one rank. `table` is the group of the
+    tables this rank owns, with slot_table = the local table of each owned slot, in
+    owned[rank] order (None when the rank owns no slot)."""
+
+    def __init__(self, ctx, table, n_slots: int, owned: List[List[int]], max_samples: int, max_keys: int, dim: int):
+        self.ctx, self.table, self.lib = ctx, table, ctx.lib
+        self.dim, self.n_slots, self.owned = dim, n_slots, owned
+        d = torch.device("cuda", torch.cuda.current_device())
+        self.device = d
+        self.sel = [torch.tensor(s if s else [0], dtype=torch.int32, device=d) for s in owned]
+        n_sel_max = max(len(s) for s in owned)
+        self.lens = [torch.empty(max(1, max_samples * len(s)), dtype=torch.int32, device=d) for s in owned]
+        self.keys = [torch.empty(max(1, max_keys), dtype=torch.int64, device=d) for _ in owned]
+        self.offs = [torch.zeros(max_samples * len(s) + 1, dtype=torch.int32, device=d) for s in owned]
+        world = len(owned)
+        tiles = (max_samples * max(n_sel_max, 1) * world) // 2048 + 2
+        self.scan = torch.empty(tiles + 2, dtype=torch.int64, device=d)
+        self.own_offs = torch.empty(max_samples * world * max(n_sel_max, 1) + 1, dtype=torch.int32, device=d)
+
+    def regroup(self, keys: torch.Tensor, offsets: Optional[torch.Tensor], n_samples: int, g: int):
+        """-> (keys of owner g's slots, their bag lengths, device CSR offsets)."""
+        n_sel = len(self.owned[g])
+        if n_sel == 0:
+            return self.keys[g][:0], self.lens[g][:0], self.offs[g][:1]
+        L.check(self.lib.hps_gpu_regroup_bags(self.ctx.h, _ptr(keys), _ptr(offsets), n_samples, self.n_slots,
+                                              _ptr(self.sel[g]), n_sel, _ptr(self.lens[g]), _ptr(self.keys[g]),
+                                              _ptr(self.offs[g]), _ptr(self.scan)), "regroup_bags")
+        return self.keys[g], self.lens[g][:n_samples * n_sel], self.offs[g][:n_samples * n_sel + 1]
+
+    def offsets_from_lengths(self, lens: torch.Tensor) -> torch.Tensor:
+        n = lens.numel()
+        out = self.own_offs[:n + 1]
+        L.check(self.lib.hps_gpu_lengths_to_offsets(self.ctx.h, _ptr(lens), n, _ptr(out), _ptr(self.scan)),
+                "lengths_to_offsets")
+        return out
+
+    def lookup(self, keys, offsets, n_samples: int, combiner: int, train: bool) -> torch.Tensor:
+        return self.table.lookup(keys, n_samples, offsets=offsets, combiner="mean" if combiner == 1 else "sum",
+                                 train=train)
+
+    def place(self, src: torch.Tensor, g: int, n_samples: int, dst: torch.Tensor, direction: int) -> None:
+        n_sel = len(self.owned[g])
+        if n_sel == 0:
+            return
+        L.check(self.lib.hps_gpu_place_pooled(self.ctx.h, _ptr(src), _ptr(self.sel[g]), n_sel, n_samples,
+                                              self.n_slots, self.dim, direction, _ptr(dst)), "place_pooled")
+
+    def backward(self, grads: torch.Tensor, params: L.OptParams) -> None:
+        L.check(self.lib.hps_gpu_backward_update(self.table.h, _ptr(grads), C.byref(params)), "backward_update")
+
+    def to_host(self, t: torch.Tensor) -> List[int]:
+        return [int(x) for x in t.tolist()]
+
+
+class LocalizedExchange:
+    """Localized-slot forward/backward for one rank (host orchestration). owned[g] = the
+    slots rank g owns (e.g. placement.plan_localized); every rank has n_samples samples."""
+
+    def __init__(self, engine, combiner: str, rank: int, world: int, n_slots: int, owned: List[List[int]],
+                 group=None):
+        self.e, self.rank, self.world, self.group = engine, rank, world, group
+        self.combiner = 1 if combiner == "mean" else 0
+        self.n_slots, self.owned = n_slots, owned
+        self._saved = None
+
+    def _a2a(self, x: torch.Tensor, out_split: List[int], in_split: List[int]) -> torch.Tensor:
+        out = torch.empty((sum(out_split),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(out, x, out_split, in_split, group=self.group)
+        return out
+
+    def forward(self, keys: torch.Tensor, offsets: Optional[torch.Tensor], n_samples: int, train: bool = True):
+        G, b, me = self.world, n_samples, self.rank
+        n_sel = [len(s) for s in self.owned]
+        parts = [self.e.regroup(keys, offsets, b, g) for g in range(G)]
+        dim = self.e.dim
+        if offsets is None:  # one key per bag: sizes are known on every rank
+            sc = [b * n_sel[g] for g in range(G)]
+            rc = [b * n_sel[me]] * G
+            send_keys = torch.cat([p[0][:sc[g]] for g, p in enumerate(parts)])
+            recv_keys = self._a2a(send_keys, rc, sc)
+            own_offs = None
+        else:
+            ends = torch.stack([p[2][-1] for p in parts]).to(torch.int32)
+            in_counts = torch.empty_like(ends)
+            dist.all_to_all_single(in_counts, ends, group=self.group)
+            sc, rc = self.e.to_host(ends), self.e.to_host(in_counts)
+            send_keys = torch.cat([p[0][:sc[g]] for g, p in enumerate(parts)])
+            recv_keys = self._a2a(send_keys, rc, sc)
+            send_lens = torch.cat([p[1] for p in parts])
+            recv_lens = self._a2a(send_lens, [b * n_sel[me]] * G, [b * n_sel[g] for g in range(G)])
+            own_offs = self.e.offsets_from_lengths(recv_lens)
+        if n_sel[me]:
+            pooled = self.e.lookup(recv_keys, own_offs, G * b, self.combiner, train)
+        else:
+            pooled = torch.empty(0, dim, dtype=torch.float32, device=keys.device)
+        back = self._a2a(pooled, [b * n_sel[g] for g in range(G)], [b * n_sel[me]] * G)
+        out = torch.empty(b * self.n_slots, dim, dtype=torch.float32, device=keys.device)
+        base = 0
+        for g in range(G):
+            self.e.place(back[base:base + b * n_sel[g]], g, b, out, 0)
+            base += b * n_sel[g]
+        self._saved = (b, sc, rc, offsets is not None)
+        return out
+
+    def backward(self, dout: torch.Tensor, params: L.OptParams) -> None:
+        G, me = self.world, self.rank
+        b = self._saved[0]
+        n_sel = [len(s) for s in self.owned]
+        send = torch.empty(b * self.n_slots, self.e.dim, dtype=torch.float32, device=dout.device)
+        base = 0
+        for g in range(G):
+            self.e.place(dout, g, b, send[base:base + b * n_sel[g]], 1)
+            base += b * n_sel[g]
+        recv = self._a2a(send, [b * n_sel[me]] * G, [b * n_sel[g] for g in range(G)])
+        if n_sel[me]:
+            self.e.backward(recv, params)
+
+    def exchanged_bytes(self, dim: int) -> int:
+        """Bytes this rank sent off-rank in the last step (keys [+ lengths] + pooled + grads)."""
+        b, sc, rc, multi = self._saved
+        n_sel = [len(s) for s in self.owned]
+        keys_off = sum(c for g, c in enumerate(sc) if g != self.rank) * 8
+        lens_off = sum(b * n_sel[g] for g in range(self.world) if g != self.rank) * 4 if multi else 0
+        pooled_off = b * n_sel[self.rank] * (self.world - 1) * dim * 4
+        grads_off = sum(b * n_sel[g] for g in range(self.world) if g != self.rank) * dim * 4
+        return keys_off + lens_off + pooled_off + grads_off

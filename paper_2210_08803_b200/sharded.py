@@ -7,7 +7,7 @@ the exchange lives in paper_2210_08803_b200.exchange.
 from __future__ import annotations
 
 import math
-from typing import Optional
+from typing import List, Optional
 
 import numpy as np
 import torch
@@ -53,14 +53,51 @@ def build_tables(ctx: Context, cfg: W.Config, rank: int = 0, world: int = 1,
     return g
 
 
+def localized_plan(cfg: W.Config, world: int, budget_bytes: int = 170 * 10**9) -> List[List[int]]:
+    """Owner of every slot under localized placement: LPT over whole tables by bytes
+    (hps_plan_localized), so slots sharing a table share its owner.
+    Returns owned[g] = the slots rank g serves, ascending."""
+    from .placement import SlotSpec, plan_localized
+    n_state = {"sgd": 0, "adagrad": 1, "adam": 2}[cfg.optimizer]
+    # the planner sizes vocab x dim x 4 B; optimizer state scales the effective dim
+    specs = [SlotSpec(c, cfg.dim * (1 + n_state), cfg.hot) for c in cfg.cards]
+    owner_of_table = plan_localized(specs, [budget_bytes] * world)
+    slots = cfg.slots()
+    return [[s for s in range(len(slots)) if owner_of_table[slots[s]] == g] for g in range(world)]
+
+
+def build_tables_localized(ctx: Context, cfg: W.Config, owned: List[List[int]], rank: int, world: int,
+                           chunk: int = 1 << 24) -> Optional[EmbeddingTableGroup]:
+    """The whole tables this rank owns (local table j = my_tables[j]); None if it owns none."""
+    slots = cfg.slots()
+    mine = owned[rank]
+    if not mine:
+        return None
+    my_tables = sorted({slots[s] for s in mine})
+    local_slot_table = [my_tables.index(slots[s]) for s in mine]
+    n_local = table_max_keys(cfg, 1)
+    g = EmbeddingTableGroup(ctx, [cfg.cards[t] for t in my_tables], cfg.dim, local_slot_table, cfg.optimizer,
+                            max_batch_keys=n_local * world, max_batch_bags=cfg.batch * len(mine) * world,
+                            init_seed=cfg.seed)
+    for j, t in enumerate(my_tables):
+        c = cfg.cards[t]
+        for first in range(0, c, chunk):
+            g.insert(j, ctx.gen_keys(W.table_seed(cfg.seed, t), first, min(chunk, c - first)))
+    ctx.sync()
+    return g
+
+
 class TrainStep:
     """One fwd+bwd+update step over a staged batch. world == 1 runs the fused path
     (2 C-ABI calls, optionally replayed as one CUDA graph); world > 1 runs the
-    distributed exchange (paper_2210_08803_b200.exchange)."""
+    distributed or localized exchange (paper_2210_08803_b200.exchange)."""
 
-    def __init__(self, ctx: Context, table: EmbeddingTableGroup, cfg: W.Config, rank: int = 0, world: int = 1,
-                 use_graph: bool = True):
+    def __init__(self, ctx: Context, table: Optional[EmbeddingTableGroup], cfg: W.Config, rank: int = 0,
+                 world: int = 1, use_graph: bool = True, owned: Optional[List[List[int]]] = None):
+        """owned (world > 1): localized placement, owned[g] = slots of rank g (localized_plan);
+        None = distributed placement."""
         self.ctx, self.table, self.cfg, self.rank, self.world = ctx, table, cfg, rank, world
+        self.placement = "single" if world == 1 else ("localized" if owned is not None else "distributed")
         self.n_bags = cfg.batch * cfg.n_slots
         self.out = torch.empty(self.n_bags, cfg.dim, dtype=torch.float32, device="cuda")
         self.params = opt_params(cfg.optimizer, cfg.lr, eps=cfg.eps)
@@ -71,7 +108,15 @@ class TrainStep:
         self.kernels_per_step = 7
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self.exchange = None
-        if world > 1:
+        if world > 1 and owned is not None:
+            from .exchange import LocalizedExchange, LocalizedGpuEngine
+            self.engine = LocalizedGpuEngine(ctx, table, cfg.n_slots, owned, cfg.batch, table_max_keys(cfg, 1), cfg.dim)
+            self.exchange = LocalizedExchange(self.engine, cfg.combiner, rank, world, cfg.n_slots, owned)
+            multi = cfg.hot > 1
+            # regroup (lengths + scan + keys) per owner [+ owner offsets] + lookup + place per owner
+            # + place(1) per owner + backward (hist + passes + scan + 3 reduce kernels)
+            self.kernels_per_step = 3 * world + (1 if multi else 0) + 1 + 2 * world + 7
+        elif world > 1:
             from .exchange import DistributedExchange, GpuEngine
             max_keys = table_max_keys(cfg, 1)
             self.engine = GpuEngine(ctx, table, cfg.slots(), max_keys, world, insert_missing=self.insert_missing)
@@ -104,7 +149,8 @@ class TrainStep:
     def _exchange_step(self, keys, offs, dout, step):
         if self.cfg.optimizer == "adam":
             self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
-        self.out = self.exchange.forward(keys, offs, self.n_bags, train=True)
+        n = self.cfg.batch if self.placement == "localized" else self.n_bags
+        self.out = self.exchange.forward(keys, offs, n, train=True)
         self.exchange.backward(dout, self.params)
 
     def run(self, b, dout, step: int = 1):
@@ -136,8 +182,7 @@ class TrainStep:
             keys = b["keys"].to("cuda", non_blocking=True)
             offs = None if b["offs"] is None else b["offs"].to("cuda", non_blocking=True)
             self._exchange_step(keys, offs, dout, step)
-            self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
-            _ = int(self._cnt.item())
+            _ = self._unique_count()
             h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
             return h2d, 8
         self._eager(b, dout, step, keys_on_host=True)
@@ -146,13 +191,21 @@ class TrainStep:
         h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
         return h2d, 8
 
-    def last_counts(self):
+    def _unique_count(self) -> int:
+        """Rows the last backward updated on this rank (D2H read of the step's result)."""
+        if self.table is None:  # localized rank that owns no slot
+            torch.cuda.current_stream().synchronize()
+            return 0
         self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
-        return self._last_n, int(self._cnt.item())
+        return int(self._cnt.item())
+
+    def last_counts(self):
+        return self._last_n, self._unique_count()
 
     def lookup_only(self, b):
         if self.exchange is not None:
-            self.exchange.forward(b["keys"], b["offs"], self.n_bags, train=False)
+            n = self.cfg.batch if self.placement == "localized" else self.n_bags
+            self.exchange.forward(b["keys"], b["offs"], n, train=False)
             return
         self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=False,
                           out=self.out)  # roofline leg: batches were materialised by the timed steps

@@ -71,3 +71,49 @@ class CpuEngine:
 
     def to_host(self, t):
         return [int(x) for x in t.tolist()]
+
+
+class LocalizedCpuEngine:
+    """Oracle-backed engine for exchange.LocalizedExchange (test infrastructure only)."""
+
+    def __init__(self, oracle_table, n_slots, owned, dim):
+        self.t, self.n_slots, self.owned, self.dim = oracle_table, n_slots, owned, dim
+
+    def regroup(self, keys, offsets, n_samples, g):
+        sel = np.asarray(self.owned[g], dtype=np.int64)
+        k = keys.numpy()
+        S = self.n_slots
+        offs = np.arange(n_samples * S + 1) if offsets is None else offsets.numpy().astype(np.int64)
+        bags = (np.arange(n_samples)[:, None] * S + sel[None, :]).ravel()
+        lens = (offs[bags + 1] - offs[bags]).astype(np.int32)
+        out = np.concatenate([k[offs[b]:offs[b + 1]] for b in bags]) if len(bags) else k[:0]
+        o = np.zeros(len(bags) + 1, dtype=np.int32)
+        o[1:] = np.cumsum(lens)
+        return torch.from_numpy(out.copy()), torch.from_numpy(lens), torch.from_numpy(o)
+
+    def offsets_from_lengths(self, lens):
+        o = np.zeros(lens.numel() + 1, dtype=np.int32)
+        o[1:] = np.cumsum(lens.numpy())
+        return torch.from_numpy(o)
+
+    def lookup(self, keys, offsets, n_samples, combiner, train):
+        k = keys.numpy().view(np.uint64)
+        o = None if offsets is None else offsets.numpy().view(np.uint32)
+        return torch.from_numpy(self.t.lookup(k, n_samples, offsets=o, combiner="mean" if combiner == 1 else "sum",
+                                              train=train))
+
+    def place(self, src, g, n_samples, dst, direction):
+        sel = np.asarray(self.owned[g], dtype=np.int64)
+        if len(sel) == 0:
+            return
+        full = torch.from_numpy((np.arange(n_samples)[:, None] * self.n_slots + sel[None, :]).ravel())
+        if direction == 0:
+            dst[full] = src
+        else:
+            dst.copy_(src[full])
+
+    def backward(self, grads, params):
+        self.t.backward_update(grads.numpy(), params)
+
+    def to_host(self, t):
+        return [int(x) for x in t.tolist()]

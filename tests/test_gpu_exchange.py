@@ -61,15 +61,21 @@ def test_pool_and_scatter(ctx, dim, mean):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
-def test_distributed_step_single_rank_nccl(ctx):
-    """The full exchange path (bucketize -> NCCL all-to-all -> gather -> pool -> grads ->
-    all-to-all -> dedup/reduce/update) on a world of one, bit-exact with the oracle table."""
+@pytest.fixture(scope="module")
+def nccl1(ctx):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     if not dist.is_initialized():
         dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    yield
+    dist.destroy_process_group()
+
+
+def test_distributed_step_single_rank_nccl(ctx, nccl1):
+    """The full exchange path (bucketize -> NCCL all-to-all -> gather -> pool -> grads ->
+    all-to-all -> dedup/reduce/update) on a world of one, bit-exact with the oracle table."""
     rs = np.random.default_rng(3)
     cards, slots, dim = [3000, 12], [0, 1, 0], 32
     g = EmbeddingTableGroup(ctx, cards, dim, list(range(len(cards))), "adagrad", 1 << 16, 1 << 16, 9, 0.1)
@@ -98,4 +104,79 @@ def test_distributed_step_single_rank_nccl(ctx):
     for t, c in enumerate(cards):
         assert np.array_equal(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])
     ex.e.close()
-    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_localized_engine_ops_match_cpu(ctx, multi):
+    """regroup_bags / lengths_to_offsets / place_pooled (both directions) for a 3-owner plan
+    against the numpy engine, bit-exact."""
+    from paper_2210_08803_b200.exchange import LocalizedGpuEngine
+    from tests.cpu_engine import LocalizedCpuEngine
+    rs = np.random.default_rng(7)
+    S, b, dim = 6, 300, 16
+    owned = [[0, 4], [1, 2, 5], [3]]
+    lens = rs.integers(0, 7, b * S) if multi else np.ones(b * S, dtype=np.int64)
+    offs = np.zeros(b * S + 1, dtype=np.int32)
+    offs[1:] = np.cumsum(lens)
+    keys = rs.integers(-2**63, 2**63 - 1, int(offs[-1]), dtype=np.int64)
+    eng = LocalizedGpuEngine(ctx, None, S, owned, b, int(offs[-1]), dim)
+    cpu = LocalizedCpuEngine(None, S, owned, dim)
+    ko, oo = torch.from_numpy(keys), torch.from_numpy(offs) if multi else None
+    kd, od = ko.cuda(), (oo.cuda() if multi else None)
+    full = torch.from_numpy(rs.standard_normal((b * S, dim)).astype(np.float32))
+    out_g = torch.zeros(b * S, dim, device="cuda")
+    out_c = torch.zeros(b * S, dim)
+    for g in range(3):
+        gk, gl, go = eng.regroup(kd, od, b, g)
+        ck, cl, co = cpu.regroup(ko, oo, b, g)
+        n = int(go[-1].item())
+        assert n == int(co[-1])
+        assert np.array_equal(gk[:n].cpu().numpy(), ck.numpy())
+        assert np.array_equal(gl.cpu().numpy(), cl.numpy())
+        assert np.array_equal(go.cpu().numpy(), co.numpy())
+        assert np.array_equal(eng.offsets_from_lengths(gl).cpu().numpy(), co.numpy())
+        blk_g = torch.empty(b * len(owned[g]), dim, device="cuda")
+        blk_c = torch.empty(b * len(owned[g]), dim)
+        eng.place(full.cuda(), g, b, blk_g, 1)
+        cpu.place(full, g, b, blk_c, 1)
+        assert torch.equal(blk_g.cpu(), blk_c)
+        eng.place(blk_g, g, b, out_g, 0)
+        cpu.place(blk_c, g, b, out_c, 0)
+    assert torch.equal(out_g.cpu(), full) and torch.equal(out_c, full)
+
+
+@pytest.mark.parametrize("multi,opt", [(False, "sgd"), (True, "adagrad")])
+def test_localized_step_single_rank_nccl(ctx, nccl1, multi, opt):
+    """Localized exchange over NCCL on a world of one: regroup -> all-to-all -> owner lookup
+    -> all-to-all -> place; backward the reverse. Bit-exact with the oracle table."""
+    from paper_2210_08803_b200.exchange import LocalizedExchange, LocalizedGpuEngine
+    rs = np.random.default_rng(11)
+    cards, slots, dim = [3000, 12, 700], [2, 0, 1, 0], 32
+    S, B = len(slots), 500
+    owned = [[0, 1, 2, 3]]
+    g = EmbeddingTableGroup(ctx, cards, dim, slots, opt, 1 << 16, 1 << 16, 9, 0.1)
+    o = O.OracleTable(cards, dim, slots, opt, 9, 0.1)
+    pools = []
+    for t, c in enumerate(cards):
+        ks = rs.integers(0, 2**63, c).astype(np.uint64)
+        g.insert(t, t64(ks))
+        o.insert(t, ks)
+        pools.append(ks)
+    comb = "mean" if multi else "sum"
+    ex = LocalizedExchange(LocalizedGpuEngine(ctx, g, S, owned, B, 1 << 16, dim), comb, 0, 1, S, owned)
+    for step in range(3):
+        lens = rs.integers(0, 8, B * S) if multi else np.ones(B * S, dtype=np.int64)
+        offs = np.zeros(B * S + 1, dtype=np.uint32)
+        offs[1:] = np.cumsum(lens)
+        keys = np.concatenate([rs.choice(pools[slots[k % S]], lens[k]) for k in range(B * S)]).astype(np.uint64)
+        od = torch.from_numpy(offs.view(np.int32)).cuda() if multi else None
+        out = ex.forward(t64(keys), od, B).cpu().numpy()
+        ref = o.lookup(keys, B, offsets=offs if multi else None, combiner=comb, train=True)
+        assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+        dout = rs.standard_normal(ref.shape).astype(np.float32)
+        p = opt_params(opt, 0.05, eps=1e-7)
+        ex.backward(torch.from_numpy(dout).cuda(), p)
+        o.backward_update(dout, p)
+        ctx.sync()
+    for t, c in enumerate(cards):
+        assert np.array_equal(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])

@@ -99,3 +99,72 @@ def test_distributed_exchange_world2_bit_exact(multi, optimizer):
         mp.spawn(_worker, args=(2, _free_port(), d, multi, optimizer), nprocs=2, join=True)
         for r in range(2):
             assert open(os.path.join(d, f"rank{r}.txt")).read() == "0"
+
+
+def _local_worker(rank, world, port, out_dir, multi, optimizer, owned):
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2210_08803_b200.api import opt_params
+    from paper_2210_08803_b200.exchange import LocalizedExchange
+    from tests import oracle_lib as O
+    from tests.cpu_engine import LocalizedCpuEngine
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rs = np.random.default_rng(321)
+    cards, slot_table, dim = [400, 9, 60], [0, 1, 2, 1], 8
+    combiner = "mean" if multi else "sum"
+    pools = [rs.integers(0, 2**63, c).astype(np.uint64) for c in cards]
+    single = O.OracleTable(cards, dim, slot_table, optimizer, seed=5, a0=0.1)
+    for t, ks in enumerate(pools):
+        single.insert(t, ks)
+    # the owner holds whole tables: local table j = my_tables[j]; local slot table follows owned[rank]
+    mine = owned[rank]
+    my_tables = sorted({slot_table[s] for s in mine})
+    shard = None
+    if mine:
+        shard = O.OracleTable([cards[t] for t in my_tables], dim, [my_tables.index(slot_table[s]) for s in mine],
+                              optimizer, seed=5, a0=0.1)
+        for j, t in enumerate(my_tables):
+            shard.insert(j, pools[t])
+    S = len(slot_table)
+    ex = LocalizedExchange(LocalizedCpuEngine(shard, S, owned, dim), combiner, rank, world, S, owned)
+    B = 24
+    for step in range(1, 4):
+        keys, offs = _global_batch(rs, pools, slot_table, B * world, multi)
+        ref = single.lookup(keys, B * world, offsets=offs.astype(np.uint32) if multi else None, combiner=combiner,
+                            train=True)
+        lo, hi = offs[rank * B * S], offs[(rank + 1) * B * S]
+        k_local = torch.from_numpy(keys[lo:hi].view(np.int64).copy())
+        o_local = torch.from_numpy((offs[rank * B * S:(rank + 1) * B * S + 1] - lo).astype(np.int32)) if multi else None
+        out = ex.forward(k_local, o_local, B).numpy()
+        assert np.array_equal(out.view(np.uint32), ref[rank * B * S:(rank + 1) * B * S].view(np.uint32)), "forward"
+        dout = rs.standard_normal(ref.shape).astype(np.float32)
+        p = opt_params(optimizer, 0.05, step=step, eps=1e-7)
+        ex.backward(torch.from_numpy(dout[rank * B * S:(rank + 1) * B * S].copy()), p)
+        single.backward_update(dout, p)
+    mism = 0
+    for j, t in enumerate(my_tables):
+        a, b = shard.export(j, 0, cards[t]), single.export(t, 0, cards[t])
+        for x, y in zip(a, b):
+            if x is not None:
+                mism += int((x.view(np.uint32) != y.view(np.uint32)).sum())
+    with open(os.path.join(out_dir, f"rank{rank}.txt"), "w") as f:
+        f.write(str(mism))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("multi,optimizer,owned", [
+    (False, "sgd", [[0, 2], [1, 3]]),
+    (True, "adagrad", [[1, 3], [0, 2]]),
+    (True, "adam", [[0, 1, 2, 3], []]),
+])
+def test_localized_exchange_world2_bit_exact(multi, optimizer, owned):
+    """Localized slots (config 3): keys of each slot go to its owner, which pools every
+    rank's samples; pooled blocks and gradients travel back along the batch dimension.
+    Outputs and every owned table's rows + state must equal one unsharded oracle table."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_local_worker, args=(2, _free_port(), d, multi, optimizer, owned), nprocs=2, join=True)
+        for r in range(2):
+            assert open(os.path.join(d, f"rank{r}.txt")).read() == "0"
