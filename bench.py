@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -298,8 +299,11 @@ def main():
     for s in range(min(args.pool, 4)):
         keys, offs, _, _ = gen.batch(1000 + s * world + rank)
         host_batches.append(step_fn.stage_host(keys, offs))
-    for i in range(2):
-        step_fn.run_host(host_batches[i % len(host_batches)], douts[0], step=10_000 + i)
+    # warm every (host buffer, d_out) pairing the timed loop uses (one-hot steps capture a
+    # CUDA graph per pairing on first use; capture must not land in the timed region)
+    n_pair = len(host_batches) * len(douts) // math.gcd(len(host_batches), len(douts))
+    for i in range(max(2, n_pair)):
+        step_fn.run_host(host_batches[i % len(host_batches)], douts[i % len(douts)], step=10_000 + i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -122,13 +122,16 @@ class EmbeddingTableGroup:
         self.h = h
         self.device = torch.device(f"cuda:{ctx.device}")
 
-    def insert(self, table: int, keys: torch.Tensor, rows: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def insert(self, table: int, keys: torch.Tensor, rows: Optional[torch.Tensor] = None,
+               return_rows: bool = True) -> Optional[torch.Tensor]:
+        """Insert keys (rows: optional initial values, first occurrence wins). Returns each
+        occurrence's local row id, or None with return_rows=False (the faster keys-only load)."""
         _need_cuda(keys, "keys")
         if rows is not None:
             _need_cuda(rows, "rows")
             if rows.dtype != torch.float32 or rows.numel() != keys.numel() * self.dim:
                 raise ValueError("rows must be float32 [n, dim]")
-        out = torch.empty(keys.numel(), dtype=torch.int64, device=self.device)
+        out = torch.empty(keys.numel(), dtype=torch.int64, device=self.device) if return_rows else None
         L.check(self.lib.hps_gpu_table_insert(self.h, table, _ptr(keys), keys.numel(), _ptr(rows), _ptr(out)),
                 "table_insert")
         return out

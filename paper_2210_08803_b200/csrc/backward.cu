@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
   constexpr int G = 32 / LPR;  // lane groups (segment streams) per warp
   constexpr int R = VPL >= 4 ? 1 : 4 / VPL;  // segments in flight per group (register budget)
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t U = a.counts[1];
   const bool mean = a.bag_len != nullptr;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -304,6 +306,8 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) 
   constexpr uint32_t NS = OPT == HPS_OPT_SGD ? 0 : OPT == HPS_OPT_ADAGRAD ? 1 : 2;  // state rows
   extern __shared__ __align__(128) float s_buf[];  // [kRedWarps][cap][dim] rows, then [kRedWarps][cap] scales
   __shared__ __align__(8) uint64_t s_bar[kRedWarps];
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   const uint32_t D = a.dim, nvec = D / 4, row_bytes = D * 4, cap = a.tma_rows;
   float* buf = s_buf + size_t(w) * cap * D;
@@ -436,6 +440,8 @@ template <int LPR, int VPL>
 __global__ void __launch_bounds__(256) k_long_chunks(BwdArgs a) {
   constexpr int G = 32 / LPR;
   constexpr int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = a.dim / 4;
   const bool mean = a.bag_len != nullptr;
   const uint64_t T = static_cast<uint32_t>(*a.long_packed);
@@ -499,6 +505,8 @@ __global__ void __launch_bounds__(256) k_long_chunks(BwdArgs a) {
 // ---- long segments: higher tree levels + optimizer ----------------------------------------
 template <int OPT, int VPL>
 __global__ void __launch_bounds__(256) k_long_combine(BwdArgs a) {
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nvec = a.dim / 4;
   const uint32_t n_long = static_cast<uint32_t>(*a.long_packed >> 32);
   for (uint32_t j = blockIdx.x; j < n_long; j += gridDim.x) {
@@ -566,6 +574,8 @@ __global__ void __launch_bounds__(256) k_long_combine(BwdArgs a) {
 
 __global__ void k_unique_rows(const uint32_t* rows, const uint32_t* seg_start, const uint64_t* counts,
                               uint32_t row_absent, uint32_t* out, uint64_t* count_out) {
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t U = counts[1];
   const bool has_absent = U > 0 && rows[seg_start[U - 1]] == row_absent;
   const uint64_t n = has_absent ? U - 1 : U;
@@ -578,60 +588,60 @@ __global__ void k_unique_rows(const uint32_t* rows, const uint32_t* seg_start, c
 // Lanes per row stream so that a lane holds VPL = ceil(nvec / LPR) float4 of a row.
 #define HPSG_ROW_DISPATCH(KERNEL, GRID)                                          \
   do {                                                                           \
-    if (nvec > 128) KERNEL<32, 8><<<GRID, 256, 0, st>>>(a);                      \
-    else if (nvec > 64) KERNEL<32, 4><<<GRID, 256, 0, st>>>(a);                  \
-    else if (nvec > 32) KERNEL<32, 2><<<GRID, 256, 0, st>>>(a);                  \
-    else if (nvec == 32) KERNEL<32, 1><<<GRID, 256, 0, st>>>(a);                 \
-    else if (nvec > 16) KERNEL<16, 2><<<GRID, 256, 0, st>>>(a);                  \
-    else if (nvec == 16) KERNEL<16, 1><<<GRID, 256, 0, st>>>(a);                 \
-    else if (nvec > 8) KERNEL<8, 2><<<GRID, 256, 0, st>>>(a);                    \
-    else if (nvec == 8) KERNEL<8, 1><<<GRID, 256, 0, st>>>(a);                   \
-    else if (nvec > 4) KERNEL<4, 2><<<GRID, 256, 0, st>>>(a);                    \
-    else if (nvec == 4) KERNEL<4, 1><<<GRID, 256, 0, st>>>(a);                   \
-    else if (nvec > 2) KERNEL<2, 2><<<GRID, 256, 0, st>>>(a);                    \
-    else if (nvec == 2) KERNEL<2, 1><<<GRID, 256, 0, st>>>(a);                   \
-    else KERNEL<1, 1><<<GRID, 256, 0, st>>>(a);                                  \
+    if (nvec > 128) launch_k(pdl, KERNEL<32, 8>, GRID, 256, 0, st, a);                      \
+    else if (nvec > 64) launch_k(pdl, KERNEL<32, 4>, GRID, 256, 0, st, a);                  \
+    else if (nvec > 32) launch_k(pdl, KERNEL<32, 2>, GRID, 256, 0, st, a);                  \
+    else if (nvec == 32) launch_k(pdl, KERNEL<32, 1>, GRID, 256, 0, st, a);                 \
+    else if (nvec > 16) launch_k(pdl, KERNEL<16, 2>, GRID, 256, 0, st, a);                  \
+    else if (nvec == 16) launch_k(pdl, KERNEL<16, 1>, GRID, 256, 0, st, a);                 \
+    else if (nvec > 8) launch_k(pdl, KERNEL<8, 2>, GRID, 256, 0, st, a);                    \
+    else if (nvec == 8) launch_k(pdl, KERNEL<8, 1>, GRID, 256, 0, st, a);                   \
+    else if (nvec > 4) launch_k(pdl, KERNEL<4, 2>, GRID, 256, 0, st, a);                    \
+    else if (nvec == 4) launch_k(pdl, KERNEL<4, 1>, GRID, 256, 0, st, a);                   \
+    else if (nvec > 2) launch_k(pdl, KERNEL<2, 2>, GRID, 256, 0, st, a);                    \
+    else if (nvec == 2) launch_k(pdl, KERNEL<2, 1>, GRID, 256, 0, st, a);                   \
+    else launch_k(pdl, KERNEL<1, 1>, GRID, 256, 0, st, a);                                  \
   } while (0)
 
 template <int OPT>
-void launch_short(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec) {
-  if (nvec > 128) k_reduce_short<OPT, 32, 8><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 64) k_reduce_short<OPT, 32, 4><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 32) k_reduce_short<OPT, 32, 2><<<grid, 256, 0, st>>>(a);
-  else if (nvec == 32) k_reduce_short<OPT, 32, 1><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 16) k_reduce_short<OPT, 16, 2><<<grid, 256, 0, st>>>(a);
-  else if (nvec == 16) k_reduce_short<OPT, 16, 1><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 8) k_reduce_short<OPT, 8, 2><<<grid, 256, 0, st>>>(a);
-  else if (nvec == 8) k_reduce_short<OPT, 8, 1><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 4) k_reduce_short<OPT, 4, 2><<<grid, 256, 0, st>>>(a);
-  else if (nvec == 4) k_reduce_short<OPT, 4, 1><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 2) k_reduce_short<OPT, 2, 2><<<grid, 256, 0, st>>>(a);
-  else if (nvec == 2) k_reduce_short<OPT, 2, 1><<<grid, 256, 0, st>>>(a);
-  else k_reduce_short<OPT, 1, 1><<<grid, 256, 0, st>>>(a);
+void launch_short(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec, bool pdl) {
+  if (nvec > 128) launch_k(pdl, k_reduce_short<OPT, 32, 8>, grid, 256, 0, st, a);
+  else if (nvec > 64) launch_k(pdl, k_reduce_short<OPT, 32, 4>, grid, 256, 0, st, a);
+  else if (nvec > 32) launch_k(pdl, k_reduce_short<OPT, 32, 2>, grid, 256, 0, st, a);
+  else if (nvec == 32) launch_k(pdl, k_reduce_short<OPT, 32, 1>, grid, 256, 0, st, a);
+  else if (nvec > 16) launch_k(pdl, k_reduce_short<OPT, 16, 2>, grid, 256, 0, st, a);
+  else if (nvec == 16) launch_k(pdl, k_reduce_short<OPT, 16, 1>, grid, 256, 0, st, a);
+  else if (nvec > 8) launch_k(pdl, k_reduce_short<OPT, 8, 2>, grid, 256, 0, st, a);
+  else if (nvec == 8) launch_k(pdl, k_reduce_short<OPT, 8, 1>, grid, 256, 0, st, a);
+  else if (nvec > 4) launch_k(pdl, k_reduce_short<OPT, 4, 2>, grid, 256, 0, st, a);
+  else if (nvec == 4) launch_k(pdl, k_reduce_short<OPT, 4, 1>, grid, 256, 0, st, a);
+  else if (nvec > 2) launch_k(pdl, k_reduce_short<OPT, 2, 2>, grid, 256, 0, st, a);
+  else if (nvec == 2) launch_k(pdl, k_reduce_short<OPT, 2, 1>, grid, 256, 0, st, a);
+  else launch_k(pdl, k_reduce_short<OPT, 1, 1>, grid, 256, 0, st, a);
 }
 
 template <int OPT, int VPL>
-void launch_short_tma_v(const BwdArgs& a, cudaStream_t st, int grid, size_t smem) {
+void launch_short_tma_v(const BwdArgs& a, cudaStream_t st, int grid, size_t smem, bool pdl) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_reduce_short_tma<OPT, VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_reduce_short_tma<OPT, VPL><<<grid, kRedWarps * 32, smem, st>>>(a);
+  launch_k(pdl, k_reduce_short_tma<OPT, VPL>, grid, kRedWarps * 32, smem, st, a);
 }
 
 template <int OPT>
-void launch_short_tma(const BwdArgs& a, cudaStream_t st, int grid, size_t smem, uint32_t nvec) {
-  if (nvec > 32) launch_short_tma_v<OPT, 2>(a, st, grid, smem);
-  else launch_short_tma_v<OPT, 1>(a, st, grid, smem);
+void launch_short_tma(const BwdArgs& a, cudaStream_t st, int grid, size_t smem, uint32_t nvec, bool pdl) {
+  if (nvec > 32) launch_short_tma_v<OPT, 2>(a, st, grid, smem, pdl);
+  else launch_short_tma_v<OPT, 1>(a, st, grid, smem, pdl);
 }
 
 template <int OPT>
-void launch_combine(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec) {
-  if (nvec > 128) k_long_combine<OPT, 8><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 64) k_long_combine<OPT, 4><<<grid, 256, 0, st>>>(a);
-  else if (nvec > 32) k_long_combine<OPT, 2><<<grid, 256, 0, st>>>(a);
-  else k_long_combine<OPT, 1><<<grid, 256, 0, st>>>(a);
+void launch_combine(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec, bool pdl) {
+  if (nvec > 128) launch_k(pdl, k_long_combine<OPT, 8>, grid, 256, 0, st, a);
+  else if (nvec > 64) launch_k(pdl, k_long_combine<OPT, 4>, grid, 256, 0, st, a);
+  else if (nvec > 32) launch_k(pdl, k_long_combine<OPT, 2>, grid, 256, 0, st, a);
+  else launch_k(pdl, k_long_combine<OPT, 1>, grid, 256, 0, st, a);
 }
 
 }  // namespace
@@ -646,6 +656,7 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   }
   if (!d_out) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = t->ctx->stream;
+  const bool pdl = t->ctx->pdl;
   const uint64_t nk = t->last_n_keys_host;
   const int passes = (t->sort_bits + 7) / 8;
   // zeroed region (table_internal.cuh bwd_zero_words)
@@ -655,8 +666,7 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   uint64_t* scan_status = reinterpret_cast<uint64_t*>(z + sort_words);
   uint32_t* scan_ticket = reinterpret_cast<uint32_t*>(scan_status + tiles);
   auto* long_packed = reinterpret_cast<unsigned long long*>(scan_status + tiles + 1);
-  const size_t used = sort_words + 2 * (tiles + 6);
-  HPSG_CUDA(cudaMemsetAsync(z, 0, used * sizeof(uint32_t), st));
+  // (the region was cleared by the training lookup: launch_lookup in table.cu)
 
   // K4a: stable sort of (row, bag) by row. One key per bag: the bag IS the occurrence.
   {
@@ -664,15 +674,16 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
     uint32_t* hist = z;
     uint32_t* stick = z + 4 * 256;
     uint32_t* status = stick + 4;
-    k_radix_hist<<<grid_for(nk, 256, kNumSMs * 2), 256, 0, st>>>(t->ws_rows_a, t->ws_counts, passes, hist);
+    HPSG_CUDA(launch_k(pdl, k_radix_hist, grid_for(nk, 256, kNumSMs * 2), 256, 0, st, t->ws_rows_a, t->ws_counts,
+                       passes, hist));
     const uint32_t* kin = t->ws_rows_a;
     const uint32_t* vin = t->last_multi ? t->ws_occ_bag : nullptr;
     bool in_b = false;
     for (int p = 0; p < passes; ++p) {
       uint32_t* kout = in_b ? t->ws_rows_a : t->ws_rows_b;
       uint32_t* vout = in_b ? t->ws_bags_a : t->ws_bags_b;
-      k_radix_pass<<<static_cast<unsigned>(stiles), kSortBlock, 0, st>>>(
-          kin, vin, kout, vout, t->ws_counts, 8 * p, hist + 256 * p, status + size_t(p) * stiles * 256, stick + p);
+      HPSG_CUDA(launch_k(pdl, k_radix_pass, static_cast<unsigned>(stiles), kSortBlock, 0, st, kin, vin, kout, vout,
+                         t->ws_counts, 8 * p, hist + 256 * p, status + size_t(p) * stiles * 256, stick + p));
       kin = kout;
       vin = vout;
       in_b = !in_b;
@@ -684,8 +695,8 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   const uint32_t* bags = t->sorted_in_b ? t->ws_bags_b : t->ws_bags_a;
   // K4b: unique-row segments.
   SegOp sop{rows, t->ws_seg_start, t->ws_seg_end, t->ws_counts};
-  k_scan<SegOp><<<static_cast<unsigned>(std::max<uint64_t>(1, tiles)), kScanBlock, 0, st>>>(sop, scan_status,
-                                                                                            scan_ticket);
+  HPSG_CUDA(launch_k(pdl, k_scan<SegOp>, static_cast<unsigned>(std::max<uint64_t>(1, tiles)), kScanBlock, 0, st, sop,
+                     scan_status, scan_ticket));
   BwdArgs a{};
   a.counts = t->ws_counts;
   a.rows = rows;
@@ -715,31 +726,32 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
     const size_t smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float);
     const int grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * 4)));
-    if (t->optimizer == HPS_OPT_SGD) launch_short_tma<HPS_OPT_SGD>(a, st, grid, smem, nvec);
-    else if (t->optimizer == HPS_OPT_ADAGRAD) launch_short_tma<HPS_OPT_ADAGRAD>(a, st, grid, smem, nvec);
-    else launch_short_tma<HPS_OPT_ADAM>(a, st, grid, smem, nvec);
+    if (t->optimizer == HPS_OPT_SGD) launch_short_tma<HPS_OPT_SGD>(a, st, grid, smem, nvec, pdl);
+    else if (t->optimizer == HPS_OPT_ADAGRAD) launch_short_tma<HPS_OPT_ADAGRAD>(a, st, grid, smem, nvec, pdl);
+    else launch_short_tma<HPS_OPT_ADAM>(a, st, grid, smem, nvec, pdl);
   } else if (t->optimizer == HPS_OPT_SGD) {
-    launch_short<HPS_OPT_SGD>(a, st, seg_grid, nvec);
+    launch_short<HPS_OPT_SGD>(a, st, seg_grid, nvec, pdl);
   } else if (t->optimizer == HPS_OPT_ADAGRAD) {
-    launch_short<HPS_OPT_ADAGRAD>(a, st, seg_grid, nvec);
+    launch_short<HPS_OPT_ADAGRAD>(a, st, seg_grid, nvec, pdl);
   } else {
-    launch_short<HPS_OPT_ADAM>(a, st, seg_grid, nvec);
+    launch_short<HPS_OPT_ADAM>(a, st, seg_grid, nvec, pdl);
   }
   const int chunk_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
   HPSG_ROW_DISPATCH(k_long_chunks, chunk_grid);
   const int comb_grid = static_cast<int>(std::min<uint64_t>(t->max_long, 2 * kNumSMs));
-  if (t->optimizer == HPS_OPT_SGD) launch_combine<HPS_OPT_SGD>(a, st, comb_grid, nvec);
-  else if (t->optimizer == HPS_OPT_ADAGRAD) launch_combine<HPS_OPT_ADAGRAD>(a, st, comb_grid, nvec);
-  else launch_combine<HPS_OPT_ADAM>(a, st, comb_grid, nvec);
+  if (t->optimizer == HPS_OPT_SGD) launch_combine<HPS_OPT_SGD>(a, st, comb_grid, nvec, pdl);
+  else if (t->optimizer == HPS_OPT_ADAGRAD) launch_combine<HPS_OPT_ADAGRAD>(a, st, comb_grid, nvec, pdl);
+  else launch_combine<HPS_OPT_ADAM>(a, st, comb_grid, nvec, pdl);
   HPSG_CHECK_LAUNCH("backward");
+  t->have_train = false;  // one backward per training lookup (its zeroed workspace is now used)
   return HPS_GPU_OK;
 }
 
 int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* unique_rows_out) {
   if (!t || !count_out) return HPS_GPU_E_INVALID_ARGUMENT;
   const uint32_t* rows = t->sorted_in_b ? t->ws_rows_b : t->ws_rows_a;
-  k_unique_rows<<<grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0, t->ctx->stream>>>(
-      rows, t->ws_seg_start, t->ws_counts, t->row_absent, unique_rows_out, count_out);
+  HPSG_CUDA(launch_k(t->ctx->pdl, k_unique_rows, grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0,
+                     t->ctx->stream, rows, t->ws_seg_start, t->ws_counts, t->row_absent, unique_rows_out, count_out));
   HPSG_CHECK_LAUNCH("k_unique_rows");
   return HPS_GPU_OK;
 }

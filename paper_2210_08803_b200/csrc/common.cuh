@@ -147,6 +147,32 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Programmatic dependent launch. A kernel launched with the PDL attribute may be scheduled
+// while its stream predecessor drains; griddepcontrol.wait blocks until the predecessor grid
+// has completed and its writes are visible, so every PDL-launched kernel calls pdl_wait()
+// before its first global access. Both instructions are no-ops under a normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// Kernel launch with optional PDL (cudaLaunchKernelEx; captured into graphs as
+// programmatic edges).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 inline int grid_for(uint64_t n, int block, int max_blocks = kNumSMs * 16) {
   uint64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;
@@ -174,4 +200,5 @@ struct hps_gpu_ctx_s {
   cudaStream_t stream = nullptr;
   uint32_t* d_status = nullptr;  // latched device status word
   uint32_t* h_status = nullptr;  // pinned mirror for sync
+  bool pdl = true;               // programmatic dependent launch in the step chains (HPS_GPU_NO_PDL=1 disables)
 };

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace hpsg {
@@ -127,6 +129,7 @@ int hps_gpu_ctx_create(int device, void* stream, hps_gpu_ctx* out) {
   auto* c = new hps_gpu_ctx_s;
   c->device = device;
   c->stream = static_cast<cudaStream_t>(stream);
+  if (const char* e = std::getenv("HPS_GPU_NO_PDL")) c->pdl = e[0] != '1';
   if (cudaMalloc(&c->d_status, sizeof(uint32_t)) != cudaSuccess ||
       cudaMallocHost(&c->h_status, sizeof(uint32_t)) != cudaSuccess) {
     delete c;

@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(Op op, uint64_t* status, ui
   __shared__ uint64_t s_scratch[33];
   __shared__ uint64_t s_prefix;
   __shared__ uint32_t s_tile;
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t n = op.size();
   const uint64_t n_tiles = (n + kScanTile - 1) / kScanTile;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
@@ -163,6 +165,8 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* __res
                                                     int passes, uint32_t* __restrict__ hist) {
   __shared__ uint32_t s_h[4][256];
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&s_h[0][0])[i] = 0;
+  pdl_wait();
+  pdl_launch_dependents();
   __syncthreads();
   const uint64_t n = *d_n;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -191,6 +195,8 @@ static __global__ void __launch_bounds__(kSortBlock) k_radix_pass(const uint32_t
   __shared__ uint32_t s_scr[33];
   __shared__ uint32_t s_tile;
 
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t n = *d_n;
   const uint64_t n_tiles = (n + kSortTile - 1) / kSortTile;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);

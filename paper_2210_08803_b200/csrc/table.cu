@@ -23,6 +23,7 @@ using namespace hpsg;
 namespace {
 
 constexpr uint64_t kNoSlot = ~0ull;
+constexpr uint64_t kPresent = ~1ull;  // key committed before this call; nothing to do (keys-only insert)
 
 // ---------------------------------------------------------------------------------
 // K2: index probe helpers
@@ -50,14 +51,36 @@ __global__ void k_find(const Slot* __restrict__ slots, TableDev td, const uint64
 
 // Insert phase A: claim or find a slot for every occurrence (128-bit CAS gives an
 // atomic snapshot of the slot, so no torn key/row reads); aux = min occurrence index.
+// keys_only (no rows, no rows_out: insert-on-miss and plain bulk loads): an occurrence
+// whose key was committed before the call needs no claim, no aux and no row work, so a
+// read-only probe settles it (rows committed before the call cannot change during it).
 __global__ void k_insert_claim(Slot* __restrict__ slots, TableDev td, const uint64_t* __restrict__ keys, uint64_t n,
-                               uint64_t* __restrict__ ws_slot, uint32_t* __restrict__ abort_flag, uint32_t* status) {
+                               uint64_t* __restrict__ ws_slot, uint32_t* __restrict__ abort_flag, uint32_t* status,
+                               bool keys_only) {
   if (*reinterpret_cast<volatile uint32_t*>(abort_flag)) return;
   Slot* base = slots + td.slot_base;
   const Slot empty{0, kRowEmpty, kAuxNone};
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t key = keys[i];
-    uint64_t idx = hps::key_hash(key) & td.slot_mask;
+    const uint64_t home = hps::key_hash(key) & td.slot_mask;
+    if (keys_only) {
+      uint64_t j = home;
+      bool present = false;
+      for (uint64_t p = 0; p <= td.slot_mask; ++p) {
+        const Slot s = load_slot(base + j);
+        if (s.row == kRowEmpty) break;
+        if (s.key == key) {
+          present = s.row != kRowPending;
+          break;
+        }
+        j = (j + 1) & td.slot_mask;
+      }
+      if (present) {
+        ws_slot[i] = kPresent;
+        continue;
+      }
+    }
+    uint64_t idx = home;
     uint64_t found = kNoSlot;
     for (uint64_t p = 0; p <= td.slot_mask; ++p) {
       const Slot want{key, kRowPending, static_cast<uint32_t>(i)};
@@ -95,7 +118,7 @@ struct InsertScanOp {
   __device__ uint64_t size() const { return *abort_flag ? 0 : n; }
   __device__ uint32_t count(uint64_t i) const {
     const uint64_t si = ws_slot[i];
-    if (si == kNoSlot) return 0;
+    if (si >= kPresent) return 0;
     const Slot s = load_slot(slots + slot_base + si);
     return (s.row == kRowPending && s.aux == static_cast<uint32_t>(i)) ? 1u : 0u;
   }
@@ -106,7 +129,7 @@ struct InsertScanOp {
       f = 1;
     } else {
       const uint64_t si = ws_slot[i];
-      if (si != kNoSlot) {
+      if (si < kPresent) {
         const Slot s = load_slot(slots + slot_base + si);
         if (s.row != kRowPending && s.aux == static_cast<uint32_t>(i)) f = 2;
       }
@@ -186,6 +209,7 @@ __global__ void k_insert_finish(Slot* __restrict__ slots, TableDev td, uint32_t 
       continue;
     }
     const uint64_t si = ws_slot[i];
+    if (si == kPresent) continue;  // keys-only call: rows_out is NULL
     if (si == kNoSlot) {
       if (rows_out) rows_out[i] = ~0ull;
       continue;
@@ -534,8 +558,15 @@ int check_tbl(hps_gpu_table t) {
     else KERNEL<1, 1><<<GRIDF(1), 256, 0, st>>>(__VA_ARGS__);                    \
   } while (0)
 
-int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi) {
+// nk: key occurrences of this call (host bound). A training lookup also clears the
+// backward's look-back/ticket region here, so the lookup -> sort -> reduce chain that
+// follows is kernel-to-kernel (programmatic dependent launches, no memset node between).
+int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, uint64_t nk) {
   const cudaStream_t st = t->ctx->stream;
+  if (a.occ_row) {
+    const int passes = (t->sort_bits + 7) / 8;
+    HPSG_CUDA(cudaMemsetAsync(t->ws_zero, 0, bwd_zero_words(nk, passes) * sizeof(uint32_t), st));
+  }
   const uint32_t nvec = t->dim / 4;
   const bool tma_ok = t->dim <= 256 && (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0 && !t->no_tma;
   if (!multi && tma_ok) {
@@ -754,7 +785,8 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
   const int grid = grid_for(n, 256, kNumSMs * 32);
   if (rows) k_rows_non_finite<<<grid_for(n * t->dim, 256, kNumSMs * 32), 256, 0, st>>>(rows, n * t->dim, t->ws_abort,
                                                                                       t->ctx->d_status);
-  k_insert_claim<<<grid, 256, 0, st>>>(t->d_slots, td, keys, n, ws_slot, t->ws_abort, t->ctx->d_status);
+  k_insert_claim<<<grid, 256, 0, st>>>(t->d_slots, td, keys, n, ws_slot, t->ws_abort, t->ctx->d_status,
+                                       rows == nullptr && rows_out == nullptr);
   InsertScanOp op{t->d_slots, td.slot_base, ws_slot, ws_pos, ws_flag, n, t->ws_counts + 3, t->ws_abort};
   k_scan<InsertScanOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(
       op, scan_status, reinterpret_cast<uint32_t*>(scan_status + tiles));
@@ -864,7 +896,7 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
     a.d_n = t->ws_counts;
   }
-  if (int s = launch_lookup(t, a, multi)) return s;
+  if (int s = launch_lookup(t, a, multi, n_keys_host)) return s;
   t->have_train = train;
   t->last_multi = multi;
   t->last_combiner = combiner;
@@ -932,7 +964,7 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
     a.row_absent = t->row_absent;
     a.d_n = t->ws_counts;
   }
-  if (int s = launch_lookup(t, a, false)) return s;
+  if (int s = launch_lookup(t, a, false, n)) return s;
   t->have_train = train;
   t->last_multi = false;
   t->last_combiner = HPS_COMBINER_SUM;

@@ -13,7 +13,8 @@ import numpy as np
 import torch
 
 from . import workload as W
-from .api import Context, EmbeddingTableGroup, opt_params
+from . import _lib as L
+from .api import Context, EmbeddingTableGroup, _ptr, opt_params
 
 
 def _owned_keys(ctx: Context, cfg: W.Config, t: int, rank: int, world: int, first: int, n: int) -> torch.Tensor:
@@ -48,7 +49,7 @@ def build_tables(ctx: Context, cfg: W.Config, rank: int = 0, world: int = 1,
     for t, c in enumerate(cfg.cards):
         for first in range(0, c, chunk):
             n = min(chunk, c - first)
-            g.insert(t, _owned_keys(ctx, cfg, t, rank, world, first, n))
+            g.insert(t, _owned_keys(ctx, cfg, t, rank, world, first, n), return_rows=False)
     ctx.sync()
     return g
 
@@ -82,7 +83,7 @@ def build_tables_localized(ctx: Context, cfg: W.Config, owned: List[List[int]], 
     for j, t in enumerate(my_tables):
         c = cfg.cards[t]
         for first in range(0, c, chunk):
-            g.insert(j, ctx.gen_keys(W.table_seed(cfg.seed, t), first, min(chunk, c - first)))
+            g.insert(j, ctx.gen_keys(W.table_seed(cfg.seed, t), first, min(chunk, c - first)), return_rows=False)
     ctx.sync()
     return g
 
@@ -107,6 +108,7 @@ class TrainStep:
         # lookup + dedup scan + scatter + short reduce + long sort/chunks/combine
         self.kernels_per_step = 7
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        self._cnt_host = torch.zeros(1, dtype=torch.int64).pin_memory()
         self.exchange = None
         if world > 1 and owned is not None:
             from .exchange import LocalizedExchange, LocalizedGpuEngine
@@ -153,42 +155,55 @@ class TrainStep:
         self.out = self.exchange.forward(keys, offs, n, train=True)
         self.exchange.backward(dout, self.params)
 
-    def run(self, b, dout, step: int = 1):
-        self._last_n = b["n_keys"]
-        if self.exchange is not None:
-            return self._exchange_step(b["keys"], b["offs"], dout, step)
-        if not self.graph_mode:
-            return self._eager(b, dout, step)
-        key = (id(b["keys"]), id(dout))
+    def _graph(self, key, fn):
+        """Capture fn() once per key as a CUDA graph (warm-up run outside the capture for lazy
+        module loading) and replay it."""
         g = self._graphs.get(key)
         if g is None:
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
                 self.ctx.set_stream(s)
-                self._eager(b, dout, step)  # warm: lazy module loading outside capture
+                fn()
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
-                    self._eager(b, dout, step)
+                    fn()
             torch.cuda.current_stream().wait_stream(s)
             self.ctx.set_stream(torch.cuda.current_stream())
             self._graphs[key] = g
         g.replay()
 
+    def run(self, b, dout, step: int = 1):
+        self._last_n = b["n_keys"]
+        if self.exchange is not None:
+            return self._exchange_step(b["keys"], b["offs"], dout, step)
+        if not self.graph_mode:
+            return self._eager(b, dout, step)
+        self._graph((id(b["keys"]), id(dout)), lambda: self._eager(b, dout, step))
+
+    def _host_step(self, b, dout, step):
+        self._eager(b, dout, step, keys_on_host=True)
+        L.check(self.ctx.lib.hps_gpu_table_last_unique(self.table.h, _ptr(self._cnt), None), "last_unique")
+        self._cnt_host.copy_(self._cnt, non_blocking=True)
+
     def run_host(self, b, dout, step: int = 1):
         """End-to-end through the C-ABI: keys from pinned host memory (H2D inside the call),
-        and a D2H read of the step's result (the number of rows updated)."""
+        and a D2H read of the step's result (the number of rows updated). One-hot steps replay
+        the whole thing (H2D copy node -> kernels -> D2H copy node) as one CUDA graph per
+        pinned input buffer; the caller refills that buffer between steps."""
+        h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
         if self.exchange is not None:
             keys = b["keys"].to("cuda", non_blocking=True)
             offs = None if b["offs"] is None else b["offs"].to("cuda", non_blocking=True)
             self._exchange_step(keys, offs, dout, step)
             _ = self._unique_count()
-            h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
             return h2d, 8
-        self._eager(b, dout, step, keys_on_host=True)
-        self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
-        _ = int(self._cnt.item())
-        h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
+        if self.graph_mode and b["offs"] is None:
+            self._graph(("host", id(b["keys"]), id(dout)), lambda: self._host_step(b, dout, step))
+        else:
+            self._host_step(b, dout, step)
+        torch.cuda.current_stream().synchronize()
+        _ = int(self._cnt_host[0])
         return h2d, 8
 
     def _unique_count(self) -> int:

@@ -318,3 +318,19 @@ def test_insert_on_miss_rejects_multi_table(ctx):
     with pytest.raises(HpsError) as e:
         g.lookup(t64(np.arange(8, dtype=np.uint64)), 4, insert_missing=True)
     assert e.value.code == 1
+
+
+def test_keys_only_insert_matches_oracle(ctx):
+    """The keys-only insert (no rows, no rows_out: read-only probe for keys committed
+    earlier) assigns the same first-occurrence rows as the oracle."""
+    g, o = make_pair(ctx, [5000], 16, [0])
+    rs = np.random.default_rng(12)
+    for rnd in range(5):
+        keys = rs.integers(0, 6000, 1500).astype(np.uint64)  # mix of present, new and repeated keys
+        assert g.insert(0, t64(keys), return_rows=False) is None
+        o.insert(0, keys)
+        ctx.sync()
+        assert g.size(0) == o.size(0)
+    n = g.size(0)
+    np.testing.assert_array_equal(g.row_keys(0, 0, n).cpu().numpy().view(np.uint64), o.row_keys(0, 0, n))
+    np.testing.assert_array_equal(g.export(0, 0, n)[0].cpu().numpy().view(np.uint32), o.export(0, 0, n)[0].view(np.uint32))
