@@ -7,18 +7,17 @@
 // the same way until one vector remains (plain sequential order up to 32 occurrences).
 // Then SGD / AdaGrad / Adam update the row in place.
 //
-// Pipeline (sizes device-resident: one memset node + 5 + passes kernels, graph-capturable):
+// Pipeline (sizes device-resident, graph-capturable; the training lookup clears the
+// look-back region, and every kernel below is a programmatic dependent launch):
 //   k_radix_hist/k_radix_pass : stable LSD sort of (row, bag) by row — the dedup; stability
 //                               keeps each key's occurrences in canonical order
 //   k_scan<SegOp>   : unique-row segments [start, end) of the sorted list
-//   k_reduce_short  : a warp owns 32 segments — lane l loads segment l's metadata and first
-//                     two bags in one round trip — then its lane groups update the
-//                     segments four at a time (weights/state + gradient rows in flight
-//                     together). Segments longer than 32 are listed (warp-cooperatively)
-//                     as 32-occurrence chunk tasks for:
-//   k_long_chunks   : one warp per chunk -> level-1 partial (L2)
-//   k_long_combine  : one CTA per long segment: higher tree levels (8 warps in parallel per
-//                     level, ping-pong between two scratch regions), then the optimizer
+//   k_reduce_short  : a warp owns 32 segments: short ones (<= 32 occurrences) are reduced
+//                     and updated (register path, or the bulk-copy path for 128 <= dim <=
+//                     256); long ones are registered as 32-occurrence chunk tasks
+//   k_long          : one warp per chunk -> level-1 partial; the last chunk to finish below
+//                     a tree node sums that node's <= 32 children in order, up to the root,
+//                     whose sum goes through the optimizer (hierarchical last-arriver)
 #include <algorithm>
 #include <cstring>
 
@@ -46,7 +45,10 @@ struct BwdArgs {
   unsigned long long* long_packed;  // (n_long << 32) | total level-1 chunks
   float* partial;                   // level-1 partials [max_chunks x dim]
   float* partial2;                  // higher levels [max_chunks/32 + max_long x dim]
-  uint32_t tma_rows;                // rows per warp buffer in k_reduce_short_tma
+  uint32_t* long_hbase;             // long segment -> first node of its levels >= 2 in partial2
+  uint32_t* node_cnt;               // arrivals per tree node (self-resetting)
+  uint32_t* higher_total;           // allocator of partial2 nodes (zeroed per call)
+  uint32_t tma_rows;                // rows per warp buffer in short_tma
   float* W;
   float* S0;
   float* S1;
@@ -152,18 +154,53 @@ __device__ __forceinline__ void add_into(float4 (&acc)[VPL], const float4 (&x)[V
   for (int k = 0; k < VPL; ++k) acc[k] = f4_add(acc[k], x[k]);
 }
 
-// ---- short segments (<= 32 occurrences) -------------------------------------------------
+// ---- long segments: registration ----------------------------------------------------------
+// Nodes above level 1 of a long segment's 32-ary tree (m level-1 chunks).
+__device__ __forceinline__ uint32_t higher_nodes(uint32_t m) {
+  uint32_t n = 0;
+  while (m > 1) {
+    m = (m + kChunk - 1) / kChunk;
+    n += m;
+  }
+  return n;
+}
+
+// Lanes holding a long segment (> kChunk occurrences) register it: id j, first global
+// chunk id, its higher-level node block; then the warp writes the chunk -> segment map.
+__device__ __forceinline__ void register_longs(const BwdArgs& a, uint64_t u0, uint64_t u, bool is_long, uint32_t len) {
+  uint32_t longs = __ballot_sync(0xffffffffu, is_long);
+  uint32_t my_j = 0, my_base = 0;
+  if (is_long) {
+    const uint32_t m = (len + kChunk - 1) / kChunk;
+    const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
+    my_j = static_cast<uint32_t>(p >> 32);
+    my_base = static_cast<uint32_t>(p);
+    a.long_seg[my_j] = static_cast<uint32_t>(u);
+    a.long_base[my_j] = my_base;
+    a.long_hbase[my_j] = atomicAdd(a.higher_total, higher_nodes(m));
+  }
+  while (longs) {
+    const int src = __ffs(longs) - 1;
+    longs &= longs - 1;
+    const uint32_t j = __shfl_sync(0xffffffffu, my_j, src);
+    const uint32_t base = __shfl_sync(0xffffffffu, my_base, src);
+    const uint32_t slen = a.seg_end[u0 + src] - a.seg_start[u0 + src];
+    const uint32_t m = (slen + kChunk - 1) / kChunk;
+    for (uint32_t c = lane_id(); c < m; c += 32) a.task_long[base + c] = j;
+  }
+}
+
+// ---- short segments (<= 32 occurrences), register path ----------------------------------
+// A warp owns 32 segments — lane l loads segment l's metadata and first two bags in one
+// round trip — then its lane groups update the segments R at a time (weights/state +
+// gradient rows in flight together).
 template <int OPT, int LPR, int VPL>
-__global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_short(BwdArgs a) {
+__device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint64_t n_warps) {
   constexpr int G = 32 / LPR;  // lane groups (segment streams) per warp
   constexpr int R = VPL >= 4 ? 1 : 4 / VPL;  // segments in flight per group (register budget)
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
-  pdl_wait();
-  pdl_launch_dependents();
   const uint64_t U = a.counts[1];
   const bool mean = a.bag_len != nullptr;
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
     // metadata: lane l <-> segment u0 + l
     const uint64_t u = u0 + lane;
@@ -187,27 +224,8 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
         }
       }
     }
-    // long segments: list their 32-occurrence chunks (the whole warp writes the task map)
-    uint32_t longs = __ballot_sync(0xffffffffu, is_long);
-    uint32_t my_j = 0, my_base = 0;
-    if (is_long) {
-      const uint32_t m = (len + kChunk - 1) / kChunk;
-      const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
-      my_j = static_cast<uint32_t>(p >> 32);
-      my_base = static_cast<uint32_t>(p);
-      a.long_seg[my_j] = static_cast<uint32_t>(u);
-      a.long_base[my_j] = my_base;
-      len = 0;  // not handled below
-    }
-    while (longs) {
-      const int src = __ffs(longs) - 1;
-      longs &= longs - 1;
-      const uint32_t j = __shfl_sync(0xffffffffu, my_j, src);
-      const uint32_t base = __shfl_sync(0xffffffffu, my_base, src);
-      const uint32_t slen = a.seg_end[u0 + src] - a.seg_start[u0 + src];
-      const uint32_t m = (slen + kChunk - 1) / kChunk;
-      for (uint32_t c = lane; c < m; c += 32) a.task_long[base + c] = j;
-    }
+    register_longs(a, u0, u, is_long, len);
+    if (is_long) len = 0;  // handled by the long phase
     // short segments: group g handles segments g, g+G, ... of the 32, R at a time
 #pragma unroll 1
     for (int j0 = 0; j0 < 32; j0 += G * R) {
@@ -238,31 +256,27 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
           add_into<VPL>(g[r], x[r]);
         }
         if constexpr (LPR == 32) {  // (narrower groups would diverge across segments of a warp)
-          // occurrences 3..32: the group loads all remaining bags at once (lane gl holds
-          // occurrences 2+gl and 2+gl+LPR), then streams the rows 8 in flight, in order.
+          // occurrences 3..32: the warp loads all remaining bags at once (lane gl holds
+          // occurrence 2+gl), then streams the rows 8 in flight, in order.
           const uint32_t rest = s_len[r] > 2 ? s_len[r] - 2 : 0;
           if (rest) {
-            const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (0xffffu << (grp * LPR));
             const uint32_t p = s_start[r] + 2;
             const uint32_t bl = gl < rest ? a.bags[p + gl] : 0u;
-            const uint32_t bh = (LPR < 32 && gl + LPR < rest) ? a.bags[p + gl + LPR] : 0u;
             const float fll = (mean && gl < rest) ? static_cast<float>(a.bag_len[bl]) : 1.f;
-            const float flh = (mean && LPR < 32 && gl + LPR < rest) ? static_cast<float>(a.bag_len[bh]) : 1.f;
-            for (uint32_t q0 = 0; q0 < rest; q0 += 8) {
-              float4 y[8][VPL];
-              float fq[8];
+            constexpr int KF = VPL >= 8 ? 1 : 8 / VPL;  // rows in flight (register budget)
+            for (uint32_t q0 = 0; q0 < rest; q0 += KF) {
+              float4 y[KF][VPL];
+              float fq[KF];
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
+              for (int k = 0; k < KF; ++k) {
                 const uint32_t q = q0 + k;
-                const int src = static_cast<int>(grp * LPR + (q % LPR));
-                const uint32_t vl = __shfl_sync(gmask, bl, src), vh = __shfl_sync(gmask, bh, src);
-                const float ql = __shfl_sync(gmask, fll, src), qh = __shfl_sync(gmask, flh, src);
-                const bool hi = q >= LPR;
-                fq[k] = hi ? qh : ql;
-                load_grad<VPL>(a, q < rest ? (hi ? vh : vl) : 0u, gl, LPR, y[k]);
+                const int src = static_cast<int>(q % 32);
+                const uint32_t vl = __shfl_sync(0xffffffffu, bl, src);
+                fq[k] = __shfl_sync(0xffffffffu, fll, src);
+                load_grad<VPL>(a, q < rest ? vl : 0u, gl, LPR, y[k]);
               }
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
+              for (int k = 0; k < KF; ++k) {
                 if (q0 + k < rest) {
                   scale_grad<VPL>(fq[k], mean, y[k]);
                   add_into<VPL>(g[r], y[k]);
@@ -293,8 +307,8 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
 }
 
 // ---- short segments on the bulk-copy engine ----------------------------------------------
-// Same work as k_reduce_short, staged through shared memory by cp.async.bulk: a warp takes
-// 32 segments (lane = segment), packs as many as fit into its smem buffer ("wave": a warp
+// Same work as short_reg, staged through shared memory by cp.async.bulk: a warp takes 32
+// segments (lane = segment), packs as many as fit into its smem buffer ("wave": a warp
 // prefix sum over rows needed = weight + state rows + one gradient row per occurrence),
 // every lane issues the bulk copies of its own segment's rows onto the warp's mbarrier,
 // and only then does the warp walk the wave segment by segment (ordered sum from smem,
@@ -302,12 +316,9 @@ __global__ void __launch_bounds__(256, OPT == HPS_OPT_SGD ? 3 : 2) k_reduce_shor
 constexpr int kRedWarps = 4;
 
 template <int OPT, int VPL>
-__global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) {
+__device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint64_t n_warps, float* s_buf,
+                                          uint64_t* s_bar) {
   constexpr uint32_t NS = OPT == HPS_OPT_SGD ? 0 : OPT == HPS_OPT_ADAGRAD ? 1 : 2;  // state rows
-  extern __shared__ __align__(128) float s_buf[];  // [kRedWarps][cap][dim] rows, then [kRedWarps][cap] scales
-  __shared__ __align__(8) uint64_t s_bar[kRedWarps];
-  pdl_wait();
-  pdl_launch_dependents();
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   const uint32_t D = a.dim, nvec = D / 4, row_bytes = D * 4, cap = a.tma_rows;
   float* buf = s_buf + size_t(w) * cap * D;
@@ -320,8 +331,6 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) 
   __syncwarp();
   uint32_t phase = 0;
   const uint64_t U = a.counts[1];
-  const uint64_t warp = uint64_t(blockIdx.x) * kRedWarps + w;
-  const uint64_t n_warps = uint64_t(gridDim.x) * kRedWarps;
   for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
     const uint64_t u = u0 + lane;
     uint32_t start = 0, len = 0, row = 0, b0 = 0, b1 = 0;
@@ -338,27 +347,8 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) 
         is_long = true;
       }
     }
-    // long segments -> chunk tasks (warp-cooperative map writes), as in k_reduce_short
-    uint32_t longs = __ballot_sync(0xffffffffu, is_long);
-    uint32_t my_j = 0, my_base = 0;
-    if (is_long) {
-      const uint32_t m = (len + kChunk - 1) / kChunk;
-      const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
-      my_j = static_cast<uint32_t>(p >> 32);
-      my_base = static_cast<uint32_t>(p);
-      a.long_seg[my_j] = static_cast<uint32_t>(u);
-      a.long_base[my_j] = my_base;
-      len = 0;
-    }
-    while (longs) {
-      const int src = __ffs(longs) - 1;
-      longs &= longs - 1;
-      const uint32_t j = __shfl_sync(0xffffffffu, my_j, src);
-      const uint32_t base = __shfl_sync(0xffffffffu, my_base, src);
-      const uint32_t slen = a.seg_end[u0 + src] - a.seg_start[u0 + src];
-      const uint32_t m = (slen + kChunk - 1) / kChunk;
-      for (uint32_t c = lane; c < m; c += 32) a.task_long[base + c] = j;
-    }
+    register_longs(a, u0, u, is_long, len);
+    if (is_long) len = 0;
     const uint32_t need = len ? 1 + NS + len : 0;
     uint32_t first = 0;  // first lane (segment) of the current wave
     while (first < 32) {
@@ -432,27 +422,99 @@ __global__ void __launch_bounds__(kRedWarps * 32) k_reduce_short_tma(BwdArgs a) 
   }
 }
 
+// ---- long segments: the tree above level 1 ----------------------------------------------
+// Level-1 chunk c of segment j is complete in partial[base_j + c]. The warp counts itself
+// into its parent node; the last of the parent's (<= 32) children sums them in order into
+// the parent, and so on up: the root's sum goes through the optimizer. Counters reset
+// themselves when their node completes, so they are zero at the start of every call.
+template <int OPT, int VW>
+__device__ __forceinline__ void climb(const BwdArgs& a, uint32_t j, uint32_t c, uint32_t m, uint32_t row) {
+  const uint32_t lane = lane_id(), nvec = a.dim / 4;
+  const float* level = a.partial + uint64_t(__ldcg(a.long_base + j)) * a.dim;
+  const uint32_t hb = __ldcg(a.long_hbase + j);
+  uint32_t off = 0, idx = c, lm = m;
+  while (true) {
+    const uint32_t parent = idx / kChunk, nm = (lm + kChunk - 1) / kChunk;
+    const uint32_t nch = min(static_cast<uint32_t>(kChunk), lm - parent * kChunk);
+    // Arrival: __syncwarp orders every lane's partial stores before lane 0's acq_rel atomic
+    // (release, cumulative); the last arriver's acquire + __syncwarp makes the siblings'
+    // partials visible to the whole warp.
+    __syncwarp();
+    uint32_t old = 0;
+    if (lane == 0) {
+      uint32_t* cnt = a.node_cnt + hb + off + parent;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+      if (old == nch - 1) *cnt = 0;  // node complete: reset for the next call
+    }
+    old = __shfl_sync(0xffffffffu, old, 0);
+    __syncwarp();
+    if (old != nch - 1) return;
+    const float4* ch = reinterpret_cast<const float4*>(level) + uint64_t(parent) * kChunk * nvec;
+    float4 g[VW];
+#pragma unroll
+    for (int k = 0; k < VW; ++k) {
+      const uint32_t v = lane + 32u * k;
+      g[k] = v < nvec ? __ldcg(ch + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    constexpr int RB = VW >= 4 ? 1 : 4 / VW;
+    for (uint32_t q0 = 1; q0 < nch; q0 += RB) {
+      float4 x[RB][VW];
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+#pragma unroll
+        for (int k = 0; k < VW; ++k) {
+          const uint32_t v = lane + 32u * k;
+          x[r][k] = (q0 + r < nch && v < nvec) ? __ldcg(ch + uint64_t(q0 + r) * nvec + v)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        if (q0 + r >= nch) break;
+#pragma unroll
+        for (int k = 0; k < VW; ++k) g[k] = f4_add(g[k], x[r][k]);
+      }
+    }
+    if (nm == 1) {  // root: the segment's gradient
+      RowState<OPT, VW> rs;
+      load_row<OPT, VW>(a, row, lane, 32, rs);
+      update_store<OPT, VW>(a, row, lane, 32, rs, g);
+      return;
+    }
+    float4* dst = reinterpret_cast<float4*>(a.partial2 + uint64_t(hb + off + parent) * a.dim);
+#pragma unroll
+    for (int k = 0; k < VW; ++k) {
+      const uint32_t v = lane + 32u * k;
+      if (v < nvec) __stcg(dst + v, g[k]);
+    }
+    level = a.partial2 + uint64_t(hb + off) * a.dim;
+    off += nm;
+    idx = parent;
+    lm = nm;
+  }
+}
+
 // ---- long segments: level-1 chunk partials -----------------------------------------------
-// One warp per chunk; its bags are loaded in one coalesced access, then the rows stream
-// through G lane groups (G rows per instruction, RB instructions in flight) and are added
-// in order (row q lives in group q % G; the running sum is kept replicated in every group).
-template <int LPR, int VPL>
-__global__ void __launch_bounds__(256) k_long_chunks(BwdArgs a) {
+// One warp per 32-occurrence chunk; its bags are loaded in one coalesced access, then the
+// rows stream through G lane groups (G rows per instruction, RB instructions in flight) and
+// are added in order (row q lives in group q % G; the running sum is kept replicated in
+// every group). Runs after the grid barrier: the task lists are complete.
+template <int OPT, int LPR, int VPL>
+__device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint64_t n_warps) {
   constexpr int G = 32 / LPR;
-  constexpr int RB = VPL >= 4 ? 2 : (VPL == 2 ? 4 : 8);
-  pdl_wait();
-  pdl_launch_dependents();
+  // x G rows in flight (occupancy does the rest); full-warp rows of 128 floats keep 8
+  constexpr int RB = VPL >= 4 ? 1 : (VPL == 2 ? 2 : (G == 1 ? 8 : 4));
+  constexpr int VW = LPR == 32 ? VPL : 1;  // warp-wide layout of the same row (LPR < 32 <=> nvec <= 32)
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = a.dim / 4;
   const bool mean = a.bag_len != nullptr;
-  const uint64_t T = static_cast<uint32_t>(*a.long_packed);
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint64_t T = static_cast<uint32_t>(__ldcg(reinterpret_cast<const unsigned long long*>(a.long_packed)));
   for (uint64_t t = warp; t < T; t += n_warps) {
-    const uint32_t j = a.task_long[t];
-    const uint32_t u = a.long_seg[j];
-    const uint32_t c = static_cast<uint32_t>(t) - a.long_base[j];
-    const uint32_t s = a.seg_start[u] + c * kChunk;
-    const uint32_t n = min(kChunk, a.seg_end[u] - s);
+    const uint32_t j = __ldcg(a.task_long + t);
+    const uint32_t u = __ldcg(a.long_seg + j);
+    const uint32_t c = static_cast<uint32_t>(t) - __ldcg(a.long_base + j);
+    const uint32_t s0 = a.seg_start[u], e = a.seg_end[u];
+    const uint32_t s = s0 + c * kChunk;
+    const uint32_t n = min(static_cast<uint32_t>(kChunk), e - s);
     const uint32_t my_bag = lane < n ? a.bags[s + lane] : 0u;
     const float my_f = (mean && lane < n) ? static_cast<float>(a.bag_len[my_bag]) : 1.f;
     float4 acc[VPL];
@@ -499,77 +561,38 @@ __global__ void __launch_bounds__(256) k_long_chunks(BwdArgs a) {
         if (v < nvec) __stcg(p + v, acc[k]);
       }
     }
+    climb<OPT, VW>(a, j, c, (e - s0 + kChunk - 1) / kChunk, a.rows[s0]);
   }
 }
 
-// ---- long segments: higher tree levels + optimizer ----------------------------------------
-template <int OPT, int VPL>
-__global__ void __launch_bounds__(256) k_long_combine(BwdArgs a) {
+// ---- kernels ------------------------------------------------------------------------------
+// Short segments reduced + updated; long segments registered as chunk tasks.
+template <int OPT, int LPR, int VPL, bool TMA>
+__global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : 2)
+    k_reduce_short(BwdArgs a) {
+  extern __shared__ __align__(128) float s_dyn[];  // TMA: [kRedWarps][cap][dim] rows, then scales
+  __shared__ __align__(8) uint64_t s_bar[kRedWarps];
   pdl_wait();
   pdl_launch_dependents();
-  const uint32_t tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nvec = a.dim / 4;
-  const uint32_t n_long = static_cast<uint32_t>(*a.long_packed >> 32);
-  for (uint32_t j = blockIdx.x; j < n_long; j += gridDim.x) {
-    const uint32_t u = a.long_seg[j];
-    const uint32_t start = a.seg_start[u];
-    uint32_t m = (a.seg_end[u] - start + kChunk - 1) / kChunk;
-    const uint32_t base = a.long_base[j];
-    const float* cur = a.partial + uint64_t(base) * a.dim;
-    float* bufs[2] = {a.partial2 + uint64_t(base / kChunk + j) * a.dim, a.partial + uint64_t(base) * a.dim};
-    int nb = 0;
-    while (m > 1) {  // one tree level: groups of 32 partials, 8 warps in parallel
-      const uint32_t mn = (m + kChunk - 1) / kChunk;
-      float* nxt = bufs[nb];
-      for (uint32_t grp = w; grp < mn; grp += 8) {
-        const uint32_t lo = grp * kChunk, n = min(kChunk, m - lo);
-        constexpr int RB = VPL >= 8 ? 1 : 8 / VPL;
-        float4 acc[VPL];
-        for (uint32_t q0 = 0; q0 < n; q0 += RB) {
-          float4 x[RB][VPL];
-#pragma unroll
-          for (int r = 0; r < RB; ++r) {
-            const float4* src = reinterpret_cast<const float4*>(cur + uint64_t(lo + q0 + r) * a.dim);
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-              const uint32_t v = lane + 32 * k;
-              x[r][k] = (q0 + r < n && v < nvec) ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < RB; ++r) {
-            if (q0 + r >= n) break;
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) acc[k] = (q0 + r == 0) ? x[r][k] : f4_add(acc[k], x[r][k]);
-          }
-        }
-        float4* dst = reinterpret_cast<float4*>(nxt + uint64_t(grp) * a.dim);
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          const uint32_t v = lane + 32 * k;
-          if (v < nvec) __stcg(dst + v, acc[k]);
-        }
-      }
-      __threadfence_block();
-      __syncthreads();
-      cur = nxt;
-      nb ^= 1;
-      m = mn;
-    }
-    if (w == 0) {
-      RowState<OPT, VPL> rs;
-      const uint32_t row = a.rows[start];
-      load_row<OPT, VPL>(a, row, lane, 32, rs);
-      float4 g[VPL];
-      const float4* src = reinterpret_cast<const float4*>(cur);
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const uint32_t v = lane + 32 * k;
-        g[k] = v < nvec ? __ldcg(src + v) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      update_store<OPT, VPL>(a, row, lane, 32, rs, g);
-    }
-    __syncthreads();
+  const uint64_t wpb = blockDim.x >> 5;
+  const uint64_t warp = uint64_t(blockIdx.x) * wpb + (threadIdx.x >> 5);
+  const uint64_t n_warps = uint64_t(gridDim.x) * wpb;
+  if constexpr (TMA) {
+    short_tma<OPT, VPL>(a, warp, n_warps, s_dyn, s_bar);
+  } else {
+    short_reg<OPT, LPR, VPL>(a, warp, n_warps);
   }
+}
+
+// Long segments: chunk partials + the last-arriver tree + optimizer, at full occupancy
+// (this part is a latency-bound gather stream).
+template <int OPT, int LPR, int VPL>
+__global__ void __launch_bounds__(256, VPL >= 4 ? 2 : (LPR == 32 ? 3 : 4)) k_long(BwdArgs a) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  long_phase<OPT, LPR, VPL>(a, warp, n_warps);
 }
 
 __global__ void k_unique_rows(const uint32_t* rows, const uint32_t* seg_start, const uint64_t* counts,
@@ -585,63 +608,43 @@ __global__ void k_unique_rows(const uint32_t* rows, const uint32_t* seg_start, c
     out[u] = rows[seg_start[u]];
 }
 
-// Lanes per row stream so that a lane holds VPL = ceil(nvec / LPR) float4 of a row.
-#define HPSG_ROW_DISPATCH(KERNEL, GRID)                                          \
-  do {                                                                           \
-    if (nvec > 128) launch_k(pdl, KERNEL<32, 8>, GRID, 256, 0, st, a);                      \
-    else if (nvec > 64) launch_k(pdl, KERNEL<32, 4>, GRID, 256, 0, st, a);                  \
-    else if (nvec > 32) launch_k(pdl, KERNEL<32, 2>, GRID, 256, 0, st, a);                  \
-    else if (nvec == 32) launch_k(pdl, KERNEL<32, 1>, GRID, 256, 0, st, a);                 \
-    else if (nvec > 16) launch_k(pdl, KERNEL<16, 2>, GRID, 256, 0, st, a);                  \
-    else if (nvec == 16) launch_k(pdl, KERNEL<16, 1>, GRID, 256, 0, st, a);                 \
-    else if (nvec > 8) launch_k(pdl, KERNEL<8, 2>, GRID, 256, 0, st, a);                    \
-    else if (nvec == 8) launch_k(pdl, KERNEL<8, 1>, GRID, 256, 0, st, a);                   \
-    else if (nvec > 4) launch_k(pdl, KERNEL<4, 2>, GRID, 256, 0, st, a);                    \
-    else if (nvec == 4) launch_k(pdl, KERNEL<4, 1>, GRID, 256, 0, st, a);                   \
-    else if (nvec > 2) launch_k(pdl, KERNEL<2, 2>, GRID, 256, 0, st, a);                    \
-    else if (nvec == 2) launch_k(pdl, KERNEL<2, 1>, GRID, 256, 0, st, a);                   \
-    else launch_k(pdl, KERNEL<1, 1>, GRID, 256, 0, st, a);                                  \
-  } while (0)
-
-template <int OPT>
-void launch_short(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec, bool pdl) {
-  if (nvec > 128) launch_k(pdl, k_reduce_short<OPT, 32, 8>, grid, 256, 0, st, a);
-  else if (nvec > 64) launch_k(pdl, k_reduce_short<OPT, 32, 4>, grid, 256, 0, st, a);
-  else if (nvec > 32) launch_k(pdl, k_reduce_short<OPT, 32, 2>, grid, 256, 0, st, a);
-  else if (nvec == 32) launch_k(pdl, k_reduce_short<OPT, 32, 1>, grid, 256, 0, st, a);
-  else if (nvec > 16) launch_k(pdl, k_reduce_short<OPT, 16, 2>, grid, 256, 0, st, a);
-  else if (nvec == 16) launch_k(pdl, k_reduce_short<OPT, 16, 1>, grid, 256, 0, st, a);
-  else if (nvec > 8) launch_k(pdl, k_reduce_short<OPT, 8, 2>, grid, 256, 0, st, a);
-  else if (nvec == 8) launch_k(pdl, k_reduce_short<OPT, 8, 1>, grid, 256, 0, st, a);
-  else if (nvec > 4) launch_k(pdl, k_reduce_short<OPT, 4, 2>, grid, 256, 0, st, a);
-  else if (nvec == 4) launch_k(pdl, k_reduce_short<OPT, 4, 1>, grid, 256, 0, st, a);
-  else if (nvec > 2) launch_k(pdl, k_reduce_short<OPT, 2, 2>, grid, 256, 0, st, a);
-  else if (nvec == 2) launch_k(pdl, k_reduce_short<OPT, 2, 1>, grid, 256, 0, st, a);
-  else launch_k(pdl, k_reduce_short<OPT, 1, 1>, grid, 256, 0, st, a);
-}
-
-template <int OPT, int VPL>
-void launch_short_tma_v(const BwdArgs& a, cudaStream_t st, int grid, size_t smem, bool pdl) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_reduce_short_tma<OPT, VPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
+template <int OPT, int LPR, int VPL, bool TMA>
+int launch_backward_v(const BwdArgs& a, cudaStream_t st, bool pdl, size_t smem, int grid, int long_grid) {
+  auto kern = k_reduce_short<OPT, LPR, VPL, TMA>;
+  constexpr int block = TMA ? kRedWarps * 32 : 256;
+  if (TMA) {
+    static bool attr = false;
+    if (!attr) {
+      HPSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
   }
-  launch_k(pdl, k_reduce_short_tma<OPT, VPL>, grid, kRedWarps * 32, smem, st, a);
+  HPSG_CUDA(launch_k(pdl, kern, grid, block, smem, st, a));
+  HPSG_CUDA(launch_k(pdl, k_long<OPT, LPR, VPL>, long_grid, 256, 0, st, a));
+  return HPS_GPU_OK;
 }
 
+// Lanes per row stream so that a lane holds VPL = ceil(nvec / LPR) float4 of a row.
 template <int OPT>
-void launch_short_tma(const BwdArgs& a, cudaStream_t st, int grid, size_t smem, uint32_t nvec, bool pdl) {
-  if (nvec > 32) launch_short_tma_v<OPT, 2>(a, st, grid, smem, pdl);
-  else launch_short_tma_v<OPT, 1>(a, st, grid, smem, pdl);
-}
-
-template <int OPT>
-void launch_combine(const BwdArgs& a, cudaStream_t st, int grid, uint32_t nvec, bool pdl) {
-  if (nvec > 128) launch_k(pdl, k_long_combine<OPT, 8>, grid, 256, 0, st, a);
-  else if (nvec > 64) launch_k(pdl, k_long_combine<OPT, 4>, grid, 256, 0, st, a);
-  else if (nvec > 32) launch_k(pdl, k_long_combine<OPT, 2>, grid, 256, 0, st, a);
-  else launch_k(pdl, k_long_combine<OPT, 1>, grid, 256, 0, st, a);
+int launch_backward(const BwdArgs& a, cudaStream_t st, bool pdl, bool tma, size_t smem, int g, int lg,
+                    uint32_t nvec) {
+  if (tma) {
+    if (nvec > 32) return launch_backward_v<OPT, 32, 2, true>(a, st, pdl, smem, g, lg);
+    return launch_backward_v<OPT, 32, 1, true>(a, st, pdl, smem, g, lg);
+  }
+  if (nvec > 128) return launch_backward_v<OPT, 32, 8, false>(a, st, pdl, 0, g, lg);
+  if (nvec > 64) return launch_backward_v<OPT, 32, 4, false>(a, st, pdl, 0, g, lg);
+  if (nvec > 32) return launch_backward_v<OPT, 32, 2, false>(a, st, pdl, 0, g, lg);
+  if (nvec == 32) return launch_backward_v<OPT, 32, 1, false>(a, st, pdl, 0, g, lg);
+  if (nvec > 16) return launch_backward_v<OPT, 16, 2, false>(a, st, pdl, 0, g, lg);
+  if (nvec == 16) return launch_backward_v<OPT, 16, 1, false>(a, st, pdl, 0, g, lg);
+  if (nvec > 8) return launch_backward_v<OPT, 8, 2, false>(a, st, pdl, 0, g, lg);
+  if (nvec == 8) return launch_backward_v<OPT, 8, 1, false>(a, st, pdl, 0, g, lg);
+  if (nvec > 4) return launch_backward_v<OPT, 4, 2, false>(a, st, pdl, 0, g, lg);
+  if (nvec == 4) return launch_backward_v<OPT, 4, 1, false>(a, st, pdl, 0, g, lg);
+  if (nvec > 2) return launch_backward_v<OPT, 2, 2, false>(a, st, pdl, 0, g, lg);
+  if (nvec == 2) return launch_backward_v<OPT, 2, 1, false>(a, st, pdl, 0, g, lg);
+  return launch_backward_v<OPT, 1, 1, false>(a, st, pdl, 0, g, lg);
 }
 
 }  // namespace
@@ -718,30 +721,30 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   a.S1 = t->d_s1;
   a.optimizer = t->optimizer;
   a.opt = *opt;
+  a.long_hbase = t->ws_long_hbase;
+  a.node_cnt = t->ws_node_cnt;
+  a.higher_total = reinterpret_cast<uint32_t*>(scan_status + tiles + 3);
   const uint32_t nvec = t->dim / 4;
-  // K4c + K5: reductions fused with the optimizer.
-  const int seg_grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
-  if (t->dim >= 128 && t->dim <= 256 && !t->no_tma) {  // narrower rows: the register path wins
+  // K4c + K5: short segments (reduce fused with the optimizer), then the long segments'
+  // chunk partials + tree + optimizer.
+  const bool tma = t->dim >= 128 && t->dim <= 256 && !t->no_tma;  // narrower rows: the register path wins
+  size_t smem = 0;
+  int grid = 0;
+  if (tma) {
     a.tma_rows = static_cast<uint32_t>(std::max<uint64_t>(40, (24 * 1024) / (t->dim * 4)));
-    const size_t smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float);
-    const int grid = static_cast<int>(
+    smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float);
+    grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * 4)));
-    if (t->optimizer == HPS_OPT_SGD) launch_short_tma<HPS_OPT_SGD>(a, st, grid, smem, nvec, pdl);
-    else if (t->optimizer == HPS_OPT_ADAGRAD) launch_short_tma<HPS_OPT_ADAGRAD>(a, st, grid, smem, nvec, pdl);
-    else launch_short_tma<HPS_OPT_ADAM>(a, st, grid, smem, nvec, pdl);
-  } else if (t->optimizer == HPS_OPT_SGD) {
-    launch_short<HPS_OPT_SGD>(a, st, seg_grid, nvec, pdl);
-  } else if (t->optimizer == HPS_OPT_ADAGRAD) {
-    launch_short<HPS_OPT_ADAGRAD>(a, st, seg_grid, nvec, pdl);
   } else {
-    launch_short<HPS_OPT_ADAM>(a, st, seg_grid, nvec, pdl);
+    grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
   }
-  const int chunk_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
-  HPSG_ROW_DISPATCH(k_long_chunks, chunk_grid);
-  const int comb_grid = static_cast<int>(std::min<uint64_t>(t->max_long, 2 * kNumSMs));
-  if (t->optimizer == HPS_OPT_SGD) launch_combine<HPS_OPT_SGD>(a, st, comb_grid, nvec, pdl);
-  else if (t->optimizer == HPS_OPT_ADAGRAD) launch_combine<HPS_OPT_ADAGRAD>(a, st, comb_grid, nvec, pdl);
-  else launch_combine<HPS_OPT_ADAM>(a, st, comb_grid, nvec, pdl);
+  const int long_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
+  int s = HPS_GPU_OK;
+  if (t->optimizer == HPS_OPT_SGD) s = launch_backward<HPS_OPT_SGD>(a, st, pdl, tma, smem, grid, long_grid, nvec);
+  else if (t->optimizer == HPS_OPT_ADAGRAD)
+    s = launch_backward<HPS_OPT_ADAGRAD>(a, st, pdl, tma, smem, grid, long_grid, nvec);
+  else s = launch_backward<HPS_OPT_ADAM>(a, st, pdl, tma, smem, grid, long_grid, nvec);
+  if (s) return s;
   HPSG_CHECK_LAUNCH("backward");
   t->have_train = false;  // one backward per training lookup (its zeroed workspace is now used)
   return HPS_GPU_OK;

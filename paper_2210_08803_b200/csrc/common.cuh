@@ -157,20 +157,51 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 // Kernel launch with optional PDL (cudaLaunchKernelEx; captured into graphs as
 // programmatic edges).
+// coop: cooperative launch (all CTAs co-resident, so a grid-wide barrier is safe even
+// with other streams' kernels on the device).
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                            cudaStream_t st, Args... args) {
+inline cudaError_t launch_kx(bool pdl, bool coop, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (coop) {
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args... args) {
+  return launch_kx(pdl, false, kernel, grid, block, smem, st, args...);
+}
+
+// One-shot grid barrier over a zeroed counter (cooperative launches only).
+__device__ __forceinline__ void grid_barrier_once(uint32_t* counter) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(counter, 1u);
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      if (v < gridDim.x) __nanosleep(64);
+    } while (v < gridDim.x);
+  }
+  __syncthreads();
 }
 
 inline int grid_for(uint64_t n, int block, int max_blocks = kNumSMs * 16) {

@@ -684,7 +684,9 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->ws_long_seg, t->max_long));
   A(dalloc(&t->ws_long_base, t->max_long));
   A(dalloc(&t->ws_task_long, t->max_chunks));
-  A(dalloc(&t->ws_partial2, (t->max_chunks / kChunk + t->max_long + 2) * D));
+  A(dalloc(&t->ws_partial2, bwd_max_nodes(N) * D));
+  A(dalloc(&t->ws_long_hbase, t->max_long));
+  A(dalloc(&t->ws_node_cnt, bwd_max_nodes(N)));
   A(dalloc(&t->ws_partial, t->max_chunks * D));
   A(dalloc(&t->ws_counts, 8));
   A(dalloc(&t->ws_zero, t->zero_words));
@@ -706,6 +708,7 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   HPSG_CUDA(cudaMemsetAsync(t->d_nrows, 0, t->n_tables * sizeof(uint64_t), s));
   HPSG_CUDA(cudaMemsetAsync(t->d_defaults, 0, uint64_t(t->n_tables) * D * sizeof(float), s));
   HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, 8 * sizeof(uint64_t), s));
+  HPSG_CUDA(cudaMemsetAsync(t->ws_node_cnt, 0, bwd_max_nodes(N) * sizeof(uint32_t), s));
   k_fill_slots_empty<<<grid_for(slots, 256, kNumSMs * 32), 256, 0, s>>>(t->d_slots, slots);
   HPSG_CHECK_LAUNCH("k_fill_slots_empty");
   HPSG_CUDA(cudaStreamSynchronize(s));  // the host arrays above are caller-owned
@@ -719,7 +722,7 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
                   t->ws_rows_b,   t->ws_bags_a,    t->ws_bags_b,    t->ws_occ_bag,    t->ws_bag_len,
                   t->ws_seg_start, t->ws_seg_end,  t->ws_long_seg,  t->ws_long_base,  t->ws_task_long,
-                  t->ws_partial2,
+                  t->ws_partial2, t->ws_long_hbase, t->ws_node_cnt,
                   t->ws_partial,  t->ws_counts,    t->ws_zero,      t->ws_abort,      t->ws_keys_stage,
                   t->ws_offsets_stage, t->ws_ins_slot, t->ws_ins_pos, t->ws_ins_flag, t->ws_ins_scan};
   for (void* p : ptrs)

@@ -20,6 +20,9 @@ inline size_t bwd_zero_words(uint64_t max_keys, int passes) {
 // Level-1 chunks of segments longer than kChunk: sum ceil(len/32) <= N/32 + N/33.
 inline uint64_t bwd_max_chunks(uint64_t max_keys) { return max_keys / kChunk + max_keys / (kChunk + 1) + 4; }
 inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
+// Tree nodes above level 1 over all long segments: sum_j (ceil(m_j/32) + ceil(m_j/1024) + ...)
+// <= total_chunks/31 + (levels <= 5) per segment.
+inline uint64_t bwd_max_nodes(uint64_t max_keys) { return bwd_max_chunks(max_keys) / 31 + 5 * bwd_max_long(max_keys) + 8; }
 
 }  // namespace hpsg
 
@@ -52,7 +55,9 @@ struct hps_gpu_table_s {
   uint32_t *ws_long_seg = nullptr, *ws_long_base = nullptr;  // long segments: id -> segment, first chunk
   uint32_t* ws_task_long = nullptr; // level-1 chunk -> long segment id
   float* ws_partial = nullptr;      // level-1 chunk partials of long segments
-  float* ws_partial2 = nullptr;     // higher tree levels (ping-pong with ws_partial)
+  float* ws_partial2 = nullptr;     // tree nodes above level 1 [max_nodes x dim]
+  uint32_t* ws_long_hbase = nullptr;  // long segment -> its first node in ws_partial2
+  uint32_t* ws_node_cnt = nullptr;    // arrivals per node; zero at rest (reset by the completing warp)
   uint64_t max_chunks = 0, max_long = 0;
   uint64_t* ws_counts = nullptr;    // [0]=N occurrences [1]=U segments
   uint32_t* ws_zero = nullptr;      // look-back words + tickets + long counters, zeroed per backward
