@@ -41,6 +41,11 @@ enum {
   HPS_GPU_OK = 0,
   /* 1..17 mirror hps::ErrorCode (proj/include/hps/error.hpp:24-42) */
   HPS_GPU_E_INVALID_ARGUMENT = 1,
+  HPS_GPU_E_BAD_MAGIC = 2,
+  HPS_GPU_E_BAD_FORMAT_VERSION = 3,
+  HPS_GPU_E_TRUNCATED = 4,
+  HPS_GPU_E_TRAILING_BYTES = 5,
+  HPS_GPU_E_DUPLICATE_KEY = 6,
   HPS_GPU_E_DIM_MISMATCH = 7,
   HPS_GPU_E_DTYPE_MISMATCH = 8,
   HPS_GPU_E_NON_FINITE = 10,
@@ -250,6 +255,39 @@ int hps_gpu_cache_stats(hps_gpu_cache cache, hps_cache_stats* stats_host);
 int hps_gpu_cache_reset_stats(hps_gpu_cache cache);
 /* syncs: number of resident entries. */
 int hps_gpu_cache_size(hps_gpu_cache cache, uint64_t* n_host);
+
+/* ---- UpdateBatch frames -> cache refresh (update.cu) ----
+ * Frame (little-endian): "HPSU" | version u8 = 1 | name_len u16 | name |
+ * seq u64 | count u32 | dim u16 | dtype u8 (0 F32, 1 F16) | count x (key u64, dim scalars).
+ * There is no encode/decode in the reference sources; these follow SPEC.md with the
+ * primitive encodings of proj/include/hps/bytes.hpp:33-133 (ByteWriter / ByteReader). */
+typedef struct {
+  char table[256];          /* NUL-terminated table name */
+  uint32_t name_len;
+  uint64_t seq;
+  uint32_t count;
+  uint32_t dim;
+  int dtype;                /* 0 = F32, 1 = F16 */
+  uint64_t entries_offset;  /* byte offset of entry 0 within the frame */
+  uint64_t entry_bytes;     /* 8 + dim * scalar size */
+} hps_update_header;
+
+/* Host: validate a frame (BadMagic, BadFormatVersion, Truncated, TrailingBytes,
+ * DuplicateKey, InvalidArgument for dim/dtype/name) and fill *header_host. */
+int hps_update_batch_parse(const uint8_t* frame_host, uint64_t n, hps_update_header* header_host);
+/* Host: encode a frame (values: count x dim scalars, float or uint16 F16 bits). With
+ * out_host == NULL only *out_len_host (the frame size) is produced. */
+int hps_update_batch_encode(const char* table_host, uint32_t name_len, uint64_t seq, uint32_t count, uint32_t dim,
+                            int dtype, const uint64_t* keys_host, const void* values_host, uint8_t* out_host,
+                            uint64_t out_cap, uint64_t* out_len_host);
+/* Device: decode the entries (frame bytes from entries_offset, already on the device)
+ * into keys, fp32 rows (F16 widened exactly) and versions (= seq; may be NULL). */
+int hps_gpu_update_decode(hps_gpu_ctx ctx, const uint8_t* entries, const hps_update_header* header_host,
+                          uint64_t* keys_out, float* vecs_out, uint64_t* versions_out);
+/* syncs: parse on the host, move the entry bytes to the device once, decode, then
+ * hps_gpu_cache_refresh with version = seq (replace only resident keys with an older
+ * version). replaced_out (device, may be NULL) receives the replacement count. */
+int hps_gpu_cache_apply_update(hps_gpu_cache cache, const uint8_t* frame_host, uint64_t n, uint64_t* replaced_out);
 
 /* ---- placement planners (host-side) ---------------------------- */
 enum { HPS_PLAN_LOCALIZED = 0, HPS_PLAN_DISTRIBUTED = 1, HPS_PLAN_HYBRID = 2 };

@@ -19,6 +19,7 @@ vp = C.c_void_p
 # hps_gpu.h status codes
 OK = 0
 E_INVALID_ARGUMENT = 1
+E_BAD_MAGIC, E_BAD_FORMAT_VERSION, E_TRUNCATED, E_TRAILING_BYTES, E_DUPLICATE_KEY = 2, 3, 4, 5, 6
 E_DIM_MISMATCH = 7
 E_NON_FINITE = 10
 E_UNKNOWN_TABLE = 11
@@ -82,6 +83,19 @@ class CacheStats(C.Structure):
     ]
 
 
+class UpdateHeader(C.Structure):
+    _fields_ = [
+        ("table", C.c_char * 256),
+        ("name_len", u32),
+        ("seq", u64),
+        ("count", u32),
+        ("dim", u32),
+        ("dtype", i32),
+        ("entries_offset", u64),
+        ("entry_bytes", u64),
+    ]
+
+
 class SlotSpec(C.Structure):
     _fields_ = [("vocab_size", u64), ("dim", u32), ("hotness", u32)]
 
@@ -129,6 +143,10 @@ SIGNATURES = {
     "hps_gpu_cache_stats": (i32, [vp, C.POINTER(CacheStats)]),
     "hps_gpu_cache_reset_stats": (i32, [vp]),
     "hps_gpu_cache_size": (i32, [vp, C.POINTER(u64)]),
+    "hps_update_batch_parse": (i32, [vp, u64, C.POINTER(UpdateHeader)]),
+    "hps_update_batch_encode": (i32, [C.c_char_p, u32, u64, u32, u32, i32, vp, vp, vp, u64, C.POINTER(u64)]),
+    "hps_gpu_update_decode": (i32, [vp, vp, C.POINTER(UpdateHeader), vp, vp, vp]),
+    "hps_gpu_cache_apply_update": (i32, [vp, vp, u64, vp]),
     "hps_plan_localized": (i32, [C.POINTER(SlotSpec), u32, C.POINTER(u64), u32, C.POINTER(u32)]),
     "hps_plan_distributed": (i32, [C.POINTER(SlotSpec), u32, C.POINTER(u64), u32]),
     "hps_shard_of": (None, [C.POINTER(u64), u64, u32, C.POINTER(u32)]),

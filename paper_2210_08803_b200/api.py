@@ -252,6 +252,14 @@ class HotCache:
                 "cache_refresh")
         return out
 
+    def apply_update(self, frame: bytes) -> int:
+        """Refresh from one UpdateBatch frame: resident keys with an older
+        version take the frame's vectors at version = seq. Returns the replacement count."""
+        buf = np.frombuffer(frame, dtype=np.uint8)
+        out = torch.zeros(1, dtype=torch.int64, device=self.device)
+        L.check(self.lib.hps_gpu_cache_apply_update(self.h, buf.ctypes.data, len(buf), _ptr(out)), "cache_apply_update")
+        return int(out.item())
+
     def stats(self) -> dict:
         s = L.CacheStats()
         L.check(self.lib.hps_gpu_cache_stats(self.h, C.byref(s)), "cache_stats")

@@ -655,6 +655,19 @@ int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* ve
   return HPS_GPU_OK;
 }
 
+}  // extern "C"
+
+namespace hpsg {
+int cache_info(hps_gpu_cache c, hps_gpu_ctx* ctx, uint32_t* dim) {
+  if (int s = check_cache(c)) return s;
+  *ctx = c->ctx;
+  *dim = c->dim;
+  return HPS_GPU_OK;
+}
+}  // namespace hpsg
+
+extern "C" {
+
 int hps_gpu_cache_stats(hps_gpu_cache c, hps_cache_stats* out) {
   if (int s = check_cache(c)) return s;
   if (!out) return HPS_GPU_E_INVALID_ARGUMENT;

@@ -190,3 +190,45 @@ def test_read_through_matches_oracle(ctx):
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
         assert cache.stats() == ocache.stats(), rnd
     assert cache.size() == ocache.size()
+
+
+@pytest.mark.parametrize("f16", [False, True])
+def test_apply_update_frame_matches_oracle_refresh(ctx, f16):
+    """UpdateBatch frame -> host validation -> one H2D of the entry bytes -> device decode
+    -> K8 refresh at version = seq, against the oracle cache's
+    refresh of the same (key, vector, version) entries."""
+    from paper_2210_08803_b200 import updates as U
+    rs = np.random.default_rng(41)
+    dim = 32
+    g, o = pair(ctx, 512, dim, ways=4)
+    keys = np.unique(rs.integers(0, 2**63 - 1, 400, dtype=np.int64)).astype(np.uint64)[:300]
+    vers = rs.integers(1, 6, len(keys)).astype(np.uint64)
+    ins_both(ctx, g, o, keys, rs.standard_normal((len(keys), dim)).astype(np.float32), vers)
+    # frame: half resident keys (mixed older/newer versions than seq 4) + non-resident keys
+    fk = np.concatenate([keys[::2], np.arange(10**6, 10**6 + 50, dtype=np.uint64)])
+    rs.shuffle(fk)
+    vals = rs.standard_normal((len(fk), dim)).astype(np.float32)
+    if f16:
+        bits = vals.astype(np.float16).view(np.uint16)
+        frame = U.encode_update_batch("emb", 4, fk, bits)
+        widened = bits.view(np.float16).astype(np.float32)  # exact widening
+    else:
+        frame = U.encode_update_batch("emb", 4, fk, vals)
+        widened = vals
+    replaced = g.apply_update(frame)
+    o_replaced, st = o.refresh(fk, widened, np.full(len(fk), 4, np.uint64))
+    assert st == 0 and replaced == o_replaced and replaced > 0
+    q_both(g, o, np.concatenate([keys, fk]))
+    assert g.stats() == o.stats()
+
+
+def test_apply_update_rejects_malformed_and_dim_mismatch(ctx):
+    from paper_2210_08803_b200 import updates as U
+    g, _ = pair(ctx, 64, 8)
+    frame = U.encode_update_batch("emb", 1, np.array([1, 2], np.uint64), np.ones((2, 8), np.float32))
+    with pytest.raises(HpsError) as e:
+        g.apply_update(frame[:-1])
+    assert e.value.code == 4
+    with pytest.raises(HpsError) as e:
+        g.apply_update(U.encode_update_batch("emb", 1, np.array([1], np.uint64), np.ones((1, 4), np.float32)))
+    assert e.value.code == 7
