@@ -209,6 +209,40 @@ int hps_gpu_lengths_to_offsets(hps_gpu_ctx ctx, const uint32_t* lens, uint64_t n
 int hps_gpu_place_pooled(hps_gpu_ctx ctx, const float* src, const uint32_t* sel, uint32_t n_sel,
                          uint32_t n_samples, uint32_t n_slots, uint32_t dim, int direction, float* dst);
 
+/* ---- hybrid sparse embedding ------------------------
+ * Hot keys (plan_hybrid) are replicated on every rank in a "hot" table group (DP); all
+ * other keys are sharded by partition_of (MP, the distributed exchange above). Per step:
+ *   hps_gpu_hybrid_probe   hot-index probe of every occurrence; records the hot group's
+ *                          training state (like a training lookup, no pooling) and
+ *                          compacts the cold occurrences (keys, bags, cold_pos[i] = index
+ *                          of occurrence i among the cold ones; count on the device)
+ *   cold occurrences -> hps_gpu_xplan_bucketize (occ_bag = cold bags) -> all-to-all ->
+ *                          owner hps_gpu_gather_rows -> all-to-all back
+ *   hps_gpu_hybrid_pool    bag sums in occurrence order from the hot replica or the
+ *                          returned cold rows (cold_rows[perm[cold_pos[i]]])
+ *   hps_gpu_cold_grads     cold gradient rows in send order -> all-to-all -> owner backward
+ *   hps_gpu_backward_reduce  (hot group) per-row gradient sums of this rank's batch
+ *   hps_gpu_sum_partials   rank-ordered sum of every rank's partials (deterministic
+ *                          all-reduce: all-to-all of row slices, sum, all-gather)
+ *   hps_gpu_apply_grads    (hot group) identical optimizer step on every replica        */
+int hps_gpu_hybrid_probe(hps_gpu_table hot, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,
+                         int combiner, uint64_t n_keys_host, uint32_t* cold_pos_out, uint64_t* cold_keys_out,
+                         uint32_t* cold_bags_out, uint64_t* cold_count_out);
+int hps_gpu_hybrid_pool(hps_gpu_table hot, const uint32_t* cold_pos, const uint32_t* perm, const float* cold_rows,
+                        const uint32_t* offsets, uint64_t n_bags, int combiner, float* out);
+/* grads_out[perm[c]] = d_out[bags[c]] (/ bag length from offsets for mean). */
+int hps_gpu_cold_grads(hps_gpu_ctx ctx, const float* d_out, const uint32_t* bags, const uint32_t* perm,
+                       const uint32_t* offsets, uint64_t n, uint32_t dim, int combiner, float* grads_out);
+/* out[r] = sum over p in order of the parts with touched[p][r] (the first starts the sum). */
+int hps_gpu_sum_partials(hps_gpu_ctx ctx, const float* parts, const uint32_t* touched, uint32_t n_parts, uint64_t rows,
+                         uint32_t dim, float* out, uint32_t* touched_out);
+/* Gradient-only backward of the last training lookup/probe: per-row sums (the canonical
+ * blocked tree) into grads_out[global row x dim], touched_out[row] = 1; rows not in the
+ * batch are left as they were. No optimizer step. */
+int hps_gpu_backward_reduce(hps_gpu_table tbl, const float* d_out, float* grads_out, uint32_t* touched_out);
+/* Optimizer step for every global row r with touched[r], gradient grads[r x dim]. */
+int hps_gpu_apply_grads(hps_gpu_table tbl, const float* grads, const uint32_t* touched, const hps_opt_params* opt);
+
 /* ---- HPS inference cache (K6..K8), SPEC.md:112-190 ---------------------------- */
 typedef struct hps_gpu_cache_s* hps_gpu_cache;
 

@@ -191,7 +191,10 @@ int lookup_pooled(Table* t, const uint64_t* keys, const uint32_t* offsets, uint3
 // DESIGN.md §4.4 optimizers, in the exact operation order of the CUDA kernels.
 inline void apply_optimizer(int optimizer, float* w, float* s0, float* s1, uint32_t D, const float* g,
                             const OptParams& p) {
-  if (optimizer == 0) {  // SGD: w -= lr*g
+  if (optimizer == 3) {  // gradient only (hybrid hot rows): w <- g, s0[0] <- 1 (touched)
+    for (uint32_t j = 0; j < D; ++j) w[j] = g[j];
+    if (s0) s0[0] = 1.0f;
+  } else if (optimizer == 0) {  // SGD: w -= lr*g
     for (uint32_t j = 0; j < D; ++j) w[j] = w[j] - p.lr * g[j];
   } else if (optimizer == 1) {  // AdaGrad: a += g^2; w -= lr*g/(sqrt(a)+eps)
     for (uint32_t j = 0; j < D; ++j) {
@@ -481,6 +484,34 @@ int orc_gather_rows(void* h, const uint64_t* keys, const uint32_t* tables, uint6
   }
   return 0;
 }
+// Hybrid embedding (backward.cu kOptGrad / hps_gpu_backward_reduce): the canonical
+// per-row gradient sums of the last training lookup into grads_out [R x dim], and
+// touched_out[r] = 1 for every row with an occurrence. No optimizer step.
+int orc_reduce_only(void* h, const float* dout, float* grads_out, float* touched_out) {
+  Table* t = static_cast<Table*>(h);
+  const uint32_t D = t->dim;
+  reduce_and_update(t->occ_row, t->occ_bag, t->bag_len, t->last_combiner == 1, dout, D, 3, OptParams{}, 1, nullptr,
+                    [&](uint64_t r, int k) -> float* {
+                      if (k == 0) return grads_out + r * D;
+                      if (k == 1) return touched_out + r;
+                      return nullptr;
+                    });
+  return 0;
+}
+// The optimizer on every global row r with touched[r] != 0 and gradient grads[r x dim].
+int orc_apply_grads(void* h, const float* grads, const uint32_t* touched, const float* opt7) {
+  Table* t = static_cast<Table*>(h);
+  const uint32_t D = t->dim;
+  OptParams p{opt7[0], opt7[1], opt7[2], opt7[3], opt7[4], opt7[5], opt7[6]};
+  const uint64_t R = t->row_key.size();
+  for (uint64_t r = 0; r < R; ++r) {
+    if (!touched[r]) continue;
+    apply_optimizer(t->optimizer, &t->w[r * D], t->s0.empty() ? nullptr : &t->s0[r * D],
+                    t->s1.empty() ? nullptr : &t->s1[r * D], D, grads + r * D, p);
+  }
+  return 0;
+}
+
 int orc_backward_update(void* h, const float* dout, const float* opt7, int n_threads) {
   OptParams p{opt7[0], opt7[1], opt7[2], opt7[3], opt7[4], opt7[5], opt7[6]};
   return backward_update(static_cast<Table*>(h), dout, p, n_threads < 1 ? 1 : n_threads);

@@ -133,6 +133,12 @@ SIGNATURES = {
     "hps_gpu_regroup_bags": (i32, [vp, vp, vp, u32, u32, vp, u32, vp, vp, vp, vp]),
     "hps_gpu_place_pooled": (i32, [vp, vp, vp, u32, u32, u32, u32, i32, vp]),
     "hps_gpu_lengths_to_offsets": (i32, [vp, vp, u64, vp, vp]),
+    "hps_gpu_hybrid_probe": (i32, [vp, vp, vp, u32, i32, u64, vp, vp, vp, vp]),
+    "hps_gpu_hybrid_pool": (i32, [vp, vp, vp, vp, vp, u64, i32, vp]),
+    "hps_gpu_cold_grads": (i32, [vp, vp, vp, vp, vp, u64, u32, i32, vp]),
+    "hps_gpu_sum_partials": (i32, [vp, vp, vp, u32, u64, u32, vp, vp]),
+    "hps_gpu_backward_reduce": (i32, [vp, vp, vp, vp]),
+    "hps_gpu_apply_grads": (i32, [vp, vp, vp, C.POINTER(OptParams)]),
     "hps_gpu_cache_create": (i32, [vp, C.POINTER(CacheConfig), C.POINTER(vp)]),
     "hps_gpu_cache_destroy": (i32, [vp]),
     "hps_gpu_cache_query": (i32, [vp, vp, u64, vp, vp, vp, vp]),

@@ -48,6 +48,7 @@ struct BwdArgs {
   uint32_t* long_hbase;             // long segment -> first node of its levels >= 2 in partial2
   uint32_t* node_cnt;               // arrivals per tree node (self-resetting)
   uint32_t* higher_total;           // allocator of partial2 nodes (zeroed per call)
+  uint32_t* touched;                // kOptGrad: row -> 1 when its gradient was written
   uint32_t tma_rows;                // rows per warp buffer in short_tma
   float* W;
   float* S0;
@@ -74,9 +75,16 @@ struct SegOp {
 // ---- row math --------------------------------------------------------------------------
 // Row of weights (+ optimizer state): OPT is HPS_OPT_* at compile time, so the loads are
 // branch-free and the unused state registers do not exist.
+// kOptGrad: no optimizer — the segment's gradient sum is stored into a dense buffer (a.W
+// points at it) and a.touched[row] = 1 (hybrid embedding: replicated hot rows are
+// all-reduced before the update, hps_gpu_backward_reduce).
+constexpr int kOptGrad = 3;
+template <int OPT>
+constexpr int state_rows() { return OPT == HPS_OPT_ADAGRAD ? 1 : OPT == HPS_OPT_ADAM ? 2 : 0; }
+
 template <int OPT, int VPL>
 struct RowState {
-  float4 w[VPL], s[OPT >= HPS_OPT_ADAGRAD ? VPL : 1], q[OPT == HPS_OPT_ADAM ? VPL : 1];
+  float4 w[VPL], s[state_rows<OPT>() >= 1 ? VPL : 1], q[state_rows<OPT>() >= 2 ? VPL : 1];
 };
 
 template <int OPT, int VPL>
@@ -88,8 +96,8 @@ __device__ __forceinline__ void load_row(const BwdArgs& a, uint32_t row, uint32_
   for (int k = 0; k < VPL; ++k) {
     const uint32_t v = min(gl + k * lpr, nvec - 1);  // clamped: no branch around the load
     r.w[k] = reinterpret_cast<const float4*>(a.W + base)[v];
-    if constexpr (OPT >= HPS_OPT_ADAGRAD) r.s[k] = reinterpret_cast<const float4*>(a.S0 + base)[v];
-    if constexpr (OPT == HPS_OPT_ADAM) r.q[k] = reinterpret_cast<const float4*>(a.S1 + base)[v];
+    if constexpr (state_rows<OPT>() >= 1) r.s[k] = reinterpret_cast<const float4*>(a.S0 + base)[v];
+    if constexpr (state_rows<OPT>() >= 2) r.q[k] = reinterpret_cast<const float4*>(a.S1 + base)[v];
   }
 }
 
@@ -105,10 +113,14 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
     const uint32_t v = gl + k * lpr;
     if (v >= nvec) continue;
     float* wf = reinterpret_cast<float*>(&r.w[k]);
-    float* sf = reinterpret_cast<float*>(&r.s[OPT >= HPS_OPT_ADAGRAD ? k : 0]);
-    float* qf = reinterpret_cast<float*>(&r.q[OPT == HPS_OPT_ADAM ? k : 0]);
+    float* sf = reinterpret_cast<float*>(&r.s[state_rows<OPT>() >= 1 ? k : 0]);
+    float* qf = reinterpret_cast<float*>(&r.q[state_rows<OPT>() >= 2 ? k : 0]);
     const float* gf = reinterpret_cast<const float*>(&g[k]);
-    if constexpr (OPT == HPS_OPT_SGD) {
+    if constexpr (OPT == kOptGrad) {
+      reinterpret_cast<float4*>(a.W + base)[v] = g[k];
+      if (v == 0 && a.touched) a.touched[row] = 1u;
+      continue;
+    } else if constexpr (OPT == HPS_OPT_SGD) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) wf[c] = __fsub_rn(wf[c], __fmul_rn(lr, gf[c]));
     } else if constexpr (OPT == HPS_OPT_ADAGRAD) {
@@ -117,7 +129,7 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
         sf[c] = __fadd_rn(sf[c], __fmul_rn(gf[c], gf[c]));
         wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(lr, gf[c]), __fadd_rn(__fsqrt_rn(sf[c]), eps)));
       }
-      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[OPT >= HPS_OPT_ADAGRAD ? k : 0];
+      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[state_rows<OPT>() >= 1 ? k : 0];
     } else {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -125,8 +137,8 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
         qf[c] = __fadd_rn(__fmul_rn(a.opt.beta2, qf[c]), __fmul_rn(a.opt.one_minus_beta2, __fmul_rn(gf[c], gf[c])));
         wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(a.opt.lr_t, sf[c]), __fadd_rn(__fsqrt_rn(qf[c]), eps)));
       }
-      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[OPT >= HPS_OPT_ADAGRAD ? k : 0];
-      reinterpret_cast<float4*>(a.S1 + base)[v] = r.q[OPT == HPS_OPT_ADAM ? k : 0];
+      reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[state_rows<OPT>() >= 1 ? k : 0];
+      reinterpret_cast<float4*>(a.S1 + base)[v] = r.q[state_rows<OPT>() >= 2 ? k : 0];
     }
     reinterpret_cast<float4*>(a.W + base)[v] = r.w[k];
   }
@@ -318,7 +330,7 @@ constexpr int kRedWarps = 4;
 template <int OPT, int VPL>
 __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint64_t n_warps, float* s_buf,
                                           uint64_t* s_bar) {
-  constexpr uint32_t NS = OPT == HPS_OPT_SGD ? 0 : OPT == HPS_OPT_ADAGRAD ? 1 : 2;  // state rows
+  constexpr uint32_t NS = state_rows<OPT>();  // state rows staged with the weight row
   const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
   const uint32_t D = a.dim, nvec = D / 4, row_bytes = D * 4, cap = a.tma_rows;
   float* buf = s_buf + size_t(w) * cap * D;
@@ -651,8 +663,13 @@ int launch_backward(const BwdArgs& a, cudaStream_t st, bool pdl, bool tma, size_
 
 extern "C" {
 
-int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_params* opt) {
-  if (!t || !opt) return HPS_GPU_E_INVALID_ARGUMENT;
+}  // extern "C"
+
+namespace {
+// grads_out != nullptr: gradient-only mode (kOptGrad) — per-row sums into grads_out
+// [total_rows x dim] (rows not in the batch untouched) and touched_out[row] = 1.
+int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt, float* grads_out,
+                  uint32_t* touched_out) {
   if (!t->have_train) {
     set_last_error("backward_update: no preceding lookup_pooled with HPS_LOOKUP_TRAIN");
     return HPS_GPU_E_INVALID_ARGUMENT;
@@ -716,11 +733,13 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   a.long_packed = long_packed;
   a.partial = t->ws_partial;
   a.partial2 = t->ws_partial2;
-  a.W = t->d_w;
-  a.S0 = t->d_s0;
-  a.S1 = t->d_s1;
+  const bool grad_only = grads_out != nullptr;
+  a.W = grad_only ? grads_out : t->d_w;
+  a.S0 = grad_only ? nullptr : t->d_s0;
+  a.S1 = grad_only ? nullptr : t->d_s1;
+  a.touched = touched_out;
   a.optimizer = t->optimizer;
-  a.opt = *opt;
+  if (opt) a.opt = *opt;
   a.long_hbase = t->ws_long_hbase;
   a.node_cnt = t->ws_node_cnt;
   a.higher_total = reinterpret_cast<uint32_t*>(scan_status + tiles + 3);
@@ -740,13 +759,77 @@ int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_p
   }
   const int long_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
   int s = HPS_GPU_OK;
-  if (t->optimizer == HPS_OPT_SGD) s = launch_backward<HPS_OPT_SGD>(a, st, pdl, tma, smem, grid, long_grid, nvec);
+  if (grad_only) s = launch_backward<kOptGrad>(a, st, pdl, tma, smem, grid, long_grid, nvec);
+  else if (t->optimizer == HPS_OPT_SGD) s = launch_backward<HPS_OPT_SGD>(a, st, pdl, tma, smem, grid, long_grid, nvec);
   else if (t->optimizer == HPS_OPT_ADAGRAD)
     s = launch_backward<HPS_OPT_ADAGRAD>(a, st, pdl, tma, smem, grid, long_grid, nvec);
   else s = launch_backward<HPS_OPT_ADAM>(a, st, pdl, tma, smem, grid, long_grid, nvec);
   if (s) return s;
   HPSG_CHECK_LAUNCH("backward");
   t->have_train = false;  // one backward per training lookup (its zeroed workspace is now used)
+  return HPS_GPU_OK;
+}
+
+// Dense apply: warp per row, rows with touched[r] take the optimizer with grads[r].
+template <int OPT, int VPL>
+__global__ void __launch_bounds__(256) k_apply_grads(BwdArgs a, const float* __restrict__ grads,
+                                                     const uint32_t* __restrict__ touched, uint64_t n_rows) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint32_t lane = lane_id(), nvec = a.dim / 4;
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t r = warp; r < n_rows; r += n_warps) {
+    if (!touched[r]) continue;
+    float4 g[VPL];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k)
+      g[k] = reinterpret_cast<const float4*>(grads + r * a.dim)[min(lane + 32u * k, nvec - 1)];
+    RowState<OPT, VPL> rs;
+    load_row<OPT, VPL>(a, static_cast<uint32_t>(r), lane, 32, rs);
+    update_store<OPT, VPL>(a, static_cast<uint32_t>(r), lane, 32, rs, g);
+  }
+}
+
+template <int OPT>
+void launch_apply(const BwdArgs& a, cudaStream_t st, bool pdl, const float* grads, const uint32_t* touched,
+                  uint64_t n_rows, uint32_t nvec) {
+  const int grid = grid_for(n_rows * 32, 256, kNumSMs * 16);
+  if (nvec > 128) launch_k(pdl, k_apply_grads<OPT, 8>, grid, 256, 0, st, a, grads, touched, n_rows);
+  else if (nvec > 64) launch_k(pdl, k_apply_grads<OPT, 4>, grid, 256, 0, st, a, grads, touched, n_rows);
+  else if (nvec > 32) launch_k(pdl, k_apply_grads<OPT, 2>, grid, 256, 0, st, a, grads, touched, n_rows);
+  else launch_k(pdl, k_apply_grads<OPT, 1>, grid, 256, 0, st, a, grads, touched, n_rows);
+}
+}  // namespace
+
+extern "C" {
+
+int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_params* opt) {
+  if (!t || !opt) return HPS_GPU_E_INVALID_ARGUMENT;
+  return backward_impl(t, d_out, opt, nullptr, nullptr);
+}
+
+int hps_gpu_backward_reduce(hps_gpu_table t, const float* d_out, float* grads_out, uint32_t* touched_out) {
+  if (!t || !grads_out || !touched_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  return backward_impl(t, d_out, nullptr, grads_out, touched_out);
+}
+
+int hps_gpu_apply_grads(hps_gpu_table t, const float* grads, const uint32_t* touched, const hps_opt_params* opt) {
+  if (!t || !grads || !touched || !opt) return HPS_GPU_E_INVALID_ARGUMENT;
+  BwdArgs a{};
+  a.dim = t->dim;
+  a.W = t->d_w;
+  a.S0 = t->d_s0;
+  a.S1 = t->d_s1;
+  a.optimizer = t->optimizer;
+  a.opt = *opt;
+  const uint32_t nvec = t->dim / 4;
+  cudaStream_t st = t->ctx->stream;
+  if (t->optimizer == HPS_OPT_SGD) launch_apply<HPS_OPT_SGD>(a, st, t->ctx->pdl, grads, touched, t->total_rows, nvec);
+  else if (t->optimizer == HPS_OPT_ADAGRAD)
+    launch_apply<HPS_OPT_ADAGRAD>(a, st, t->ctx->pdl, grads, touched, t->total_rows, nvec);
+  else launch_apply<HPS_OPT_ADAM>(a, st, t->ctx->pdl, grads, touched, t->total_rows, nvec);
+  HPSG_CHECK_LAUNCH("k_apply_grads");
   return HPS_GPU_OK;
 }
 

@@ -164,6 +164,50 @@ __global__ void __launch_bounds__(256) k_place(const float* __restrict__ src, co
   }
 }
 
+// Hybrid: per-cold-occurrence gradient rows in send order: out[perm[c]] = d_out[bag_c] (/len).
+template <int LPR>
+__global__ void __launch_bounds__(256) k_cold_grads(const float* __restrict__ dout, const uint32_t* __restrict__ bags,
+                                                    const uint32_t* __restrict__ perm,
+                                                    const uint32_t* __restrict__ offsets, uint64_t n, uint32_t dim,
+                                                    int mean, float* __restrict__ out) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t c = gid; c < n; c += ng) {
+    const uint32_t b = bags[c];
+    const float len = (mean && offsets) ? static_cast<float>(offsets[b + 1] - offsets[b]) : 1.f;
+    const float4* src = reinterpret_cast<const float4*>(dout + uint64_t(b) * dim);
+    float4* dst = reinterpret_cast<float4*>(out + uint64_t(perm[c]) * dim);
+    for (uint32_t v = gl; v < nvec; v += LPR) {
+      float4 x = __ldg(src + v);
+      if (mean) x = f4_div(x, len);
+      dst[v] = x;
+    }
+  }
+}
+
+// Hybrid hot-row all-reduce, deterministic: out[r] = sum over parts p in order of the parts
+// that touched r (the first such part starts the sum), touched_out[r] = any.
+__global__ void k_sum_partials(const float* __restrict__ parts, const uint32_t* __restrict__ touched,
+                               uint32_t n_parts, uint64_t rows, uint32_t dim, float* __restrict__ out,
+                               uint32_t* __restrict__ touched_out) {
+  const uint64_t total = rows * dim;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / dim;
+    float acc = 0.f;
+    bool any = false;
+    for (uint32_t p = 0; p < n_parts; ++p) {
+      if (!touched[uint64_t(p) * rows + r]) continue;
+      const float x = parts[uint64_t(p) * total + i];
+      acc = any ? __fadd_rn(acc, x) : x;
+      any = true;
+    }
+    out[i] = acc;
+    if (i % dim == 0) touched_out[r] = any ? 1u : 0u;
+  }
+}
+
 int lpr_of(uint32_t dim) {
   const uint32_t nvec = dim / 4;
   return nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
@@ -330,6 +374,31 @@ int hps_gpu_place_pooled(hps_gpu_ctx ctx, const float* src, const uint32_t* sel,
   const int grid = grid_for(n * lpr, 256, kNumSMs * 32);
   HPSG_LPR_LAUNCH(k_place, lpr, grid, src, sel, n_sel, n_samples, n_slots, dim, direction, dst);
   HPSG_CHECK_LAUNCH("k_place");
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_cold_grads(hps_gpu_ctx ctx, const float* d_out, const uint32_t* bags, const uint32_t* perm,
+                       const uint32_t* offsets, uint64_t n, uint32_t dim, int combiner, float* grads_out) {
+  if (!ctx || dim == 0 || dim % 4) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (n == 0) return HPS_GPU_OK;
+  if (!d_out || !bags || !perm || !grads_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  const int lpr = lpr_of(dim);
+  const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
+  cudaStream_t st = ctx->stream;
+  const int mean = combiner == HPS_COMBINER_MEAN;
+  HPSG_LPR_LAUNCH(k_cold_grads, lpr, grid, d_out, bags, perm, offsets, n, dim, mean, grads_out);
+  HPSG_CHECK_LAUNCH("k_cold_grads");
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_sum_partials(hps_gpu_ctx ctx, const float* parts, const uint32_t* touched, uint32_t n_parts, uint64_t rows,
+                         uint32_t dim, float* out, uint32_t* touched_out) {
+  if (!ctx || dim == 0) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (rows == 0) return HPS_GPU_OK;
+  if (!parts || !touched || !out || !touched_out || n_parts == 0) return HPS_GPU_E_INVALID_ARGUMENT;
+  k_sum_partials<<<grid_for(rows * dim, 256, kNumSMs * 16), 256, 0, ctx->stream>>>(parts, touched, n_parts, rows, dim,
+                                                                                  out, touched_out);
+  HPSG_CHECK_LAUNCH("k_sum_partials");
   return HPS_GPU_OK;
 }
 

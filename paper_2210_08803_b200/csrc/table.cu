@@ -561,6 +561,85 @@ int check_tbl(hps_gpu_table t) {
 // nk: key occurrences of this call (host bound). A training lookup also clears the
 // backward's look-back/ticket region here, so the lookup -> sort -> reduce chain that
 // follows is kernel-to-kernel (programmatic dependent launches, no memset node between).
+// ---------------------------------------------------------------------------------
+// Hybrid sparse embedding:
+// hot keys live in a replicated table group (this table), cold keys on their owner.
+// ---------------------------------------------------------------------------------
+// Probe every occurrence against the hot index and record the training state exactly as
+// a training lookup does (occ_row = hot row or row_absent, occ_bag, bag_len, N), without
+// pooling. Bag-parallel: thread per bag.
+__global__ void k_hybrid_probe(LookupArgs a) {
+  pdl_wait();
+  const uint64_t n_bags = a.n_bags;
+  for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < n_bags;
+       b += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t table = a.slot_table[b % a.n_slots];
+    const TableDev td = a.tables[table];
+    const uint64_t lo = a.offsets ? a.offsets[b] : b, hi = a.offsets ? a.offsets[b + 1] : b + 1;
+    for (uint64_t i = lo; i < hi; ++i) {
+      const uint32_t local = probe_find(a.slots, td, a.keys[i]);
+      record_occurrence(a, i, local, static_cast<uint32_t>(td.row_base + local));
+      if (a.occ_bag) a.occ_bag[i] = static_cast<uint32_t>(b);
+    }
+    if (a.bag_len) a.bag_len[b] = static_cast<uint32_t>(hi - lo);
+    if (b == 0) *a.d_n = a.offsets ? a.offsets[n_bags] : n_bags;
+  }
+}
+
+// Cold occurrences (absent from the hot index), compacted in occurrence order.
+struct ColdOp {
+  const uint32_t* occ_row;
+  uint32_t row_absent;
+  const uint64_t* keys;
+  const uint32_t* occ_bag;  // nullptr: one key per bag
+  uint32_t* cold_pos;
+  uint64_t* cold_keys;
+  uint32_t* cold_bags;
+  uint64_t* d_count;
+  const uint64_t* d_n;
+  __device__ uint64_t size() const { return *d_n; }
+  __device__ uint32_t count(uint64_t i) const { return occ_row[i] == row_absent ? 1u : 0u; }
+  __device__ void emit(uint64_t i, uint64_t excl, uint32_t c) const {
+    cold_pos[i] = static_cast<uint32_t>(excl);
+    if (c) {
+      cold_keys[excl] = keys[i];
+      cold_bags[excl] = occ_bag ? occ_bag[i] : static_cast<uint32_t>(i);
+    }
+  }
+  __device__ void total(uint64_t t) const { *d_count = t; }
+};
+
+// Pool every bag in occurrence order from the hot replica or the rows returned by the
+// cold owners (cold_rows[perm[cold_pos[i]]]): the same sequential sum as any lookup.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_hybrid_pool(const uint32_t* __restrict__ occ_row, uint32_t row_absent,
+                                                     const float* __restrict__ W, const uint32_t* __restrict__ cold_pos,
+                                                     const uint32_t* __restrict__ perm,
+                                                     const float* __restrict__ cold_rows,
+                                                     const uint32_t* __restrict__ offsets, uint64_t n_bags,
+                                                     uint32_t dim, int mean, float* __restrict__ out) {
+  pdl_wait();
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t b = gid; b < n_bags; b += ng) {
+    const uint64_t lo = offsets ? offsets[b] : b, hi = offsets ? offsets[b + 1] : b + 1;
+    for (uint32_t v = gl; v < nvec; v += LPR) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint64_t i = lo; i < hi; ++i) {
+        const uint32_t r = occ_row[i];
+        const float4* src = r != row_absent
+                                ? reinterpret_cast<const float4*>(W + uint64_t(r) * dim)
+                                : reinterpret_cast<const float4*>(cold_rows + uint64_t(perm[cold_pos[i]]) * dim);
+        acc = f4_add(acc, __ldg(src + v));
+      }
+      if (mean && hi > lo) acc = f4_div(acc, static_cast<float>(hi - lo));
+      reinterpret_cast<float4*>(out + b * dim)[v] = acc;
+    }
+  }
+}
+
 int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, uint64_t nk) {
   const cudaStream_t st = t->ctx->stream;
   if (a.occ_row) {
@@ -930,6 +1009,78 @@ int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* 
     default: k_read_through<1><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
   }
   HPSG_CHECK_LAUNCH("k_read_through");
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,
+                         int combiner, uint64_t n_keys_host, uint32_t* cold_pos_out, uint64_t* cold_keys_out,
+                         uint32_t* cold_bags_out, uint64_t* cold_count_out) {
+  if (int s = check_tbl(t)) return s;
+  const uint64_t n_bags = uint64_t(n_samples) * t->n_slots;
+  const bool multi = offsets != nullptr;
+  if (!multi) n_keys_host = n_bags;
+  if (n_bags > t->max_bags || n_keys_host > t->max_keys) {
+    set_last_error("hybrid_probe: batch exceeds max_batch_bags / max_batch_keys");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (!keys || !cold_pos_out || !cold_keys_out || !cold_bags_out || !cold_count_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (combiner != HPS_COMBINER_SUM && combiner != HPS_COMBINER_MEAN) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = t->ctx->stream;
+  const int passes = (t->sort_bits + 7) / 8;
+  HPSG_CUDA(cudaMemsetAsync(t->ws_zero, 0, bwd_zero_words(n_keys_host, passes) * sizeof(uint32_t), st));
+  LookupArgs a{};
+  a.keys = keys;
+  a.offsets = offsets;
+  a.n_bags = static_cast<uint32_t>(n_bags);
+  a.n_slots = t->n_slots;
+  a.slot_table = t->d_slot_table;
+  a.tables = t->d_tables;
+  a.slots = t->d_slots;
+  a.occ_row = t->ws_rows_a;
+  a.row_absent = t->row_absent;
+  a.occ_bag = multi ? t->ws_occ_bag : nullptr;
+  a.bag_len = (multi && combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
+  a.d_n = t->ws_counts;
+  if (n_bags) k_hybrid_probe<<<grid_for(n_bags, 256, kNumSMs * 16), 256, 0, st>>>(a);
+  else HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, sizeof(uint64_t), st));
+  // compaction scan: its look-back words live past the backward's zeroed region
+  const uint64_t tiles = scan_tiles(std::max<uint64_t>(n_keys_host, 1));
+  HPSG_CUDA(cudaMemsetAsync(t->ws_ins_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
+  ColdOp op{t->ws_rows_a, t->row_absent, keys, a.occ_bag, cold_pos_out, cold_keys_out, cold_bags_out, cold_count_out,
+            t->ws_counts};
+  k_scan<ColdOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(op, t->ws_ins_scan,
+                                                                      reinterpret_cast<uint32_t*>(t->ws_ins_scan + tiles));
+  HPSG_CHECK_LAUNCH("hybrid_probe");
+  t->have_train = true;
+  t->last_multi = multi;
+  t->last_combiner = combiner;
+  t->last_n_keys_host = n_keys_host;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_hybrid_pool(hps_gpu_table t, const uint32_t* cold_pos, const uint32_t* perm, const float* cold_rows,
+                        const uint32_t* offsets, uint64_t n_bags, int combiner, float* out) {
+  if (int s = check_tbl(t)) return s;
+  if (n_bags == 0) return HPS_GPU_OK;
+  if (!cold_pos || !out || (!cold_rows && perm)) return HPS_GPU_E_INVALID_ARGUMENT;
+  const uint32_t nvec = t->dim / 4;
+  const int lpr = nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
+  const int grid = grid_for(n_bags * lpr, 256, kNumSMs * 16);
+  cudaStream_t st = t->ctx->stream;
+  const int mean = combiner == HPS_COMBINER_MEAN;
+#define HPSG_HP(L)                                                                                             \
+  k_hybrid_pool<L><<<grid, 256, 0, st>>>(t->ws_rows_a, t->row_absent, t->d_w, cold_pos, perm, cold_rows, offsets, \
+                                         n_bags, t->dim, mean, out)
+  switch (lpr) {
+    case 32: HPSG_HP(32); break;
+    case 16: HPSG_HP(16); break;
+    case 8: HPSG_HP(8); break;
+    case 4: HPSG_HP(4); break;
+    case 2: HPSG_HP(2); break;
+    default: HPSG_HP(1); break;
+  }
+#undef HPSG_HP
+  HPSG_CHECK_LAUNCH("hybrid_pool");
   return HPS_GPU_OK;
 }
 

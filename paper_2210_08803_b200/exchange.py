@@ -295,3 +295,142 @@ class LocalizedExchange:
         pooled_off = b * n_sel[self.rank] * (self.world - 1) * dim * 4
         grads_off = sum(b * n_sel[g] for g in range(self.world) if g != self.rank) * dim * 4
         return keys_off + lens_off + pooled_off + grads_off
+
+
+# ---------------------------------------------------------------------------------------
+# Hybrid sparse embedding
+# ---------------------------------------------------------------------------------------
+#
+# Hot keys (placement.plan_hybrid) are replicated on every rank in a "hot" table group
+# (data parallel); every other key lives on its owner partition_of(key, G) exactly as in
+# the distributed exchange (model parallel). One step on rank r:
+#
+#   hps_gpu_hybrid_probe     hot-index probe of every occurrence (records the hot group's
+#                            training state) + compaction of the cold occurrences
+#   cold occurrences         bucketize -> all-to-all -> owner gather -> all-to-all back
+#   hps_gpu_hybrid_pool      bag sums in occurrence order (hot replica rows | cold rows)
+#   ... dense model ...
+#   hps_gpu_cold_grads       -> all-to-all -> owner dedup/reduce/optimizer
+#   hps_gpu_backward_reduce  per-hot-row gradient sums of rank r's batch (canonical tree)
+#   deterministic all-reduce: all-to-all of row slices, hps_gpu_sum_partials (ranks in
+#                            order), all-gather of the summed slices
+#   hps_gpu_apply_grads      the same optimizer step on every replica
+#
+# Only cold rows and the dense hot-gradient all-reduce travel. Numerics: cold keys are
+# bit-identical to one unsharded table; a hot key's gradient is the rank-ordered sum of
+# each rank's canonical partial (the data-parallel reduction; identical on every rank).
+
+
+class HybridGpuEngine:
+    def __init__(self, ctx, hot_table, cold_engine: GpuEngine, max_keys: int):
+        self.ctx, self.hot, self.cold, self.lib = ctx, hot_table, cold_engine, ctx.lib
+        self.dim = hot_table.dim
+        d = hot_table.device
+        self.device = d
+        self.hot_rows = int(sum(hot_table.row_capacity))
+        self.cold_pos = torch.empty(max(1, max_keys), dtype=torch.int32, device=d)
+        self.cold_keys = torch.empty(max(1, max_keys), dtype=torch.int64, device=d)
+        self.cold_bags = torch.empty(max(1, max_keys), dtype=torch.int32, device=d)
+        self.cold_count = torch.zeros(1, dtype=torch.int64, device=d)
+        self.grads = torch.empty(self.hot_rows, self.dim, dtype=torch.float32, device=d)
+        self.touched = torch.zeros(self.hot_rows, dtype=torch.int32, device=d)
+
+    def probe(self, keys, offsets, n_samples: int, combiner: int):
+        L.check(self.lib.hps_gpu_hybrid_probe(self.hot.h, _ptr(keys), _ptr(offsets), n_samples, combiner, keys.numel(),
+                                              _ptr(self.cold_pos), _ptr(self.cold_keys), _ptr(self.cold_bags),
+                                              _ptr(self.cold_count)), "hybrid_probe")
+        nc = int(self.cold_count.item())
+        return self.cold_keys[:nc], self.cold_bags[:nc], self.cold_pos, nc
+
+    def pool(self, cold_pos, perm, back, offsets, n_bags: int, combiner: int):
+        out = torch.empty(n_bags, self.dim, dtype=torch.float32, device=self.device)
+        L.check(self.lib.hps_gpu_hybrid_pool(self.hot.h, _ptr(cold_pos), _ptr(perm), _ptr(back), _ptr(offsets), n_bags,
+                                             combiner, _ptr(out)), "hybrid_pool")
+        return out
+
+    def cold_grads(self, dout, bags, perm, offsets, n: int, combiner: int):
+        g = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
+        L.check(self.lib.hps_gpu_cold_grads(self.ctx.h, _ptr(dout), _ptr(bags), _ptr(perm), _ptr(offsets), n, self.dim,
+                                            combiner, _ptr(g)), "cold_grads")
+        return g
+
+    def hot_reduce(self, dout):
+        self.touched.zero_()
+        L.check(self.lib.hps_gpu_backward_reduce(self.hot.h, _ptr(dout), _ptr(self.grads), _ptr(self.touched)),
+                "backward_reduce")
+        return self.grads, self.touched
+
+    def sum_partials(self, parts, touched, n_parts: int, rows: int):
+        out = torch.empty(rows, self.dim, dtype=torch.float32, device=self.device)
+        t = torch.empty(rows, dtype=torch.int32, device=self.device)
+        L.check(self.lib.hps_gpu_sum_partials(self.ctx.h, _ptr(parts), _ptr(touched), n_parts, rows, self.dim,
+                                              _ptr(out), _ptr(t)), "sum_partials")
+        return out, t
+
+    def hot_apply(self, grads, touched, params):
+        L.check(self.lib.hps_gpu_apply_grads(self.hot.h, _ptr(grads), _ptr(touched), C.byref(params)), "apply_grads")
+
+    def to_host(self, t: torch.Tensor) -> List[int]:
+        return [int(x) for x in t.tolist()]
+
+
+class HybridExchange:
+    """Hybrid forward/backward for one rank (host orchestration over an engine)."""
+
+    def __init__(self, engine, combiner: str, rank: int, world: int, n_slots: int, group=None):
+        self.e, self.rank, self.world, self.group = engine, rank, world, group
+        self.combiner = 1 if combiner == "mean" else 0
+        self.n_slots = n_slots
+        self._saved = None
+
+    def _a2a(self, x: torch.Tensor, out_split: List[int], in_split: List[int]) -> torch.Tensor:
+        out = torch.empty((sum(out_split),) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        dist.all_to_all_single(out, x, out_split, in_split, group=self.group)
+        return out
+
+    def forward(self, keys: torch.Tensor, offsets: Optional[torch.Tensor], n_samples: int, train: bool = True):
+        n_bags = n_samples * self.n_slots
+        cold_keys, cold_bags, cold_pos, nc = self.e.probe(keys, offsets, n_samples, self.combiner)
+        send_keys, send_tables, perm, counts = self.e.cold.bucketize(cold_keys, cold_bags)
+        in_counts = torch.empty_like(counts)
+        dist.all_to_all_single(in_counts, counts, group=self.group)
+        sc, rc = self.e.to_host(counts), self.e.to_host(in_counts)
+        recv_keys = self._a2a(send_keys, rc, sc)
+        recv_tables = self._a2a(send_tables, rc, sc)
+        rows = self.e.cold.gather_rows(recv_keys, recv_tables, train)
+        back = self._a2a(rows, sc, rc)
+        out = self.e.pool(cold_pos, perm, back, offsets, n_bags, self.combiner)
+        self._saved = (perm, cold_bags, nc, offsets, sc, rc)
+        return out
+
+    def backward(self, dout: torch.Tensor, params: L.OptParams) -> None:
+        perm, cold_bags, nc, offsets, sc, rc = self._saved
+        grads = self.e.cold_grads(dout, cold_bags, perm, offsets, nc, self.combiner)
+        recv = self._a2a(grads, rc, sc)
+        self.e.cold.backward(recv, params)
+        # hot rows: deterministic all-reduce of the per-rank partial sums, then every
+        # replica takes the same optimizer step
+        g, t = self.e.hot_reduce(dout)
+        G, R = self.world, g.shape[0]
+        sl = (R + G - 1) // G
+        if G * sl != R:
+            g = torch.cat([g, torch.zeros(G * sl - R, g.shape[1], dtype=g.dtype, device=g.device)])
+            t = torch.cat([t, torch.zeros(G * sl - R, dtype=t.dtype, device=t.device)])
+        parts = self._a2a(g, [sl] * G, [sl] * G)   # [G x sl x D]: every rank's partial of my slice
+        tparts = self._a2a(t, [sl] * G, [sl] * G)
+        s, ts = self.e.sum_partials(parts, tparts, G, sl)
+        fs = [torch.empty_like(s) for _ in range(G)]
+        ft = [torch.empty_like(ts) for _ in range(G)]
+        dist.all_gather(fs, s, group=self.group)
+        dist.all_gather(ft, ts, group=self.group)
+        self.e.hot_apply(torch.cat(fs)[:R].contiguous(), torch.cat(ft)[:R].contiguous(), params)
+
+    def exchanged_bytes(self, dim: int) -> int:
+        perm, cold_bags, nc, offsets, sc, rc = self._saved
+        off_send = sum(c for g, c in enumerate(sc) if g != self.rank)
+        off_recv = sum(c for g, c in enumerate(rc) if g != self.rank)
+        G = self.world
+        R = self.e.hot_rows
+        sl = (R + G - 1) // G
+        allreduce = 2 * (G - 1) * sl * (dim * 4 + 4)
+        return off_send * (8 + 4 + dim * 4) + off_recv * dim * 4 + allreduce

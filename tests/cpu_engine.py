@@ -117,3 +117,84 @@ class LocalizedCpuEngine:
 
     def to_host(self, t):
         return [int(x) for x in t.tolist()]
+
+
+class HybridCpuEngine:
+    """Oracle-backed engine for exchange.HybridExchange (test infrastructure only).
+    hot: OracleTable replica of the hot keys; cold: a CpuEngine over this rank's shard."""
+
+    def __init__(self, hot_table, cold_engine, slot_table, dim):
+        self.hot, self.cold, self.dim = hot_table, cold_engine, dim
+        self.slot_table = np.asarray(slot_table, np.int64)
+        self.hot_rows = hot_table.caps_total
+        self._hot_occ = None
+
+    def probe(self, keys, offsets, n_samples, combiner):
+        k = keys.numpy().view(np.uint64)
+        S = len(self.slot_table)
+        n_bags = n_samples * S
+        offs = np.arange(n_bags + 1) if offsets is None else offsets.numpy().astype(np.int64)
+        bag = np.repeat(np.arange(n_bags), offs[1:] - offs[:-1])
+        tables = self.slot_table[bag % S]
+        # training state of the hot replica (pooled output unused) + hot rows per occurrence
+        self.hot.lookup(k, n_samples, offsets=None if offsets is None else offsets.numpy().view(np.uint32),
+                        combiner="mean" if combiner == 1 else "sum", train=True)
+        rows = np.full(len(k), np.iinfo(np.uint64).max, dtype=np.uint64)
+        for t in np.unique(tables):
+            m = tables == t
+            rows[m] = self.hot.find(int(t), k[m])
+        cold = rows == np.iinfo(np.uint64).max
+        cold_pos = (np.cumsum(cold) - 1).astype(np.int32)
+        self._hot_occ = (k, tables, cold)
+        return (torch.from_numpy(k[cold].view(np.int64).copy()), torch.from_numpy(bag[cold].astype(np.int32)),
+                torch.from_numpy(cold_pos), int(cold.sum()))
+
+    def pool(self, cold_pos, perm, back, offsets, n_bags, combiner):
+        from tests import oracle_lib as O
+        k, tables, cold = self._hot_occ
+        rows = O.gather_rows(self.hot, k, tables.astype(np.uint32), False)
+        cp = cold_pos.numpy().astype(np.int64)
+        if cold.any():
+            rows[cold] = back.numpy()[perm.numpy().astype(np.int64)[cp[cold]]]
+        offs = None if offsets is None else offsets.numpy()
+        return torch.from_numpy(pool_sequential(rows, np.arange(len(k)), offs, n_bags, combiner == 1))
+
+    def cold_grads(self, dout, bags, perm, offsets, n, combiner):
+        d = dout.numpy()
+        b = bags.numpy().astype(np.int64)
+        g = d[b]
+        if combiner == 1 and offsets is not None:
+            o = offsets.numpy().astype(np.int64)
+            g = g / (o[b + 1] - o[b])[:, None].astype(np.float32)
+        out = np.empty((n, self.dim), dtype=np.float32)
+        out[perm.numpy().astype(np.int64)] = g
+        return torch.from_numpy(out)
+
+    def hot_reduce(self, dout):
+        g, t = self.hot.reduce_only(dout.numpy())
+        return torch.from_numpy(g), torch.from_numpy(t.astype(np.int32))
+
+    def sum_partials(self, parts, touched, n_parts, rows):
+        return sum_partials_np(parts.numpy(), touched.numpy(), n_parts, rows)
+
+    def hot_apply(self, grads, touched, params):
+        self.hot.apply_grads(grads.numpy(), touched.numpy().astype(np.uint32), params)
+
+    def to_host(self, t):
+        return [int(x) for x in t.tolist()]
+
+
+def sum_partials_np(parts, touched, n_parts, rows):
+    """Rank-ordered sum of the parts that touched a row (the first starts the sum)."""
+    p = parts.reshape(n_parts, rows, -1)
+    t = touched.reshape(n_parts, rows) != 0
+    out = np.zeros((rows, p.shape[2]), dtype=np.float32)
+    any_ = np.zeros(rows, dtype=bool)
+    for q in range(n_parts):
+        m = t[q]
+        first = m & ~any_
+        out[first] = p[q][first]
+        later = m & any_
+        out[later] = out[later] + p[q][later]
+        any_ |= m
+    return torch.from_numpy(out), torch.from_numpy(any_.astype(np.int32))

@@ -33,6 +33,8 @@ _SIG = {
     "orc_table_row_keys": (None, [vp, u32, u64, u64, vp]),
     "orc_lookup_pooled": (i32, [vp, vp, vp, u32, i32, vp, i32, i32]),
     "orc_backward_update": (i32, [vp, vp, vp, i32]),
+    "orc_reduce_only": (i32, [vp, vp, vp, vp]),
+    "orc_apply_grads": (i32, [vp, vp, vp, vp]),
     "orc_last_unique": (u64, [vp, vp]),
     "orc_cache_create": (vp, [u64, u32, u64, u32]),
     "orc_cache_destroy": (None, [vp]),
@@ -71,6 +73,7 @@ class OracleTable:
         self.n_slots = len(slot_table)
         self.optimizer = optimizer
         caps = np.asarray(caps, dtype=np.uint64)
+        self.caps_total = int(caps.sum())
         st = np.asarray(slot_table, dtype=np.uint32)
         opt = {"sgd": 0, "adagrad": 1, "adam": 2}[optimizer]
         self.h = self.L.orc_table_create(len(caps), dim, P(caps), len(st), P(st), opt, seed, a0)
@@ -119,6 +122,24 @@ class OracleTable:
         d = np.ascontiguousarray(dout, dtype=np.float32)
         o = np.array([p.lr, p.eps, p.beta1, p.beta2, p.one_minus_beta1, p.one_minus_beta2, p.lr_t], dtype=np.float32)
         return self.L.orc_backward_update(self.h, P(d), P(o), threads)
+
+    def total_rows(self):
+        return int(self.caps_total)
+
+    def reduce_only(self, dout):
+        """Canonical per-row gradient sums of the last training lookup (no optimizer):
+        (grads [R x dim] with zeros for untouched rows, touched [R] uint32)."""
+        d = np.ascontiguousarray(dout, dtype=np.float32)
+        g = np.zeros((self.caps_total, self.dim), dtype=np.float32)
+        t = np.zeros(self.caps_total, dtype=np.float32)
+        self.L.orc_reduce_only(self.h, P(d), P(g), P(t))
+        return g, (t != 0).astype(np.uint32)
+
+    def apply_grads(self, grads, touched, p):
+        g = np.ascontiguousarray(grads, dtype=np.float32)
+        t = np.ascontiguousarray(touched, dtype=np.uint32)
+        o = np.array([p.lr, p.eps, p.beta1, p.beta2, p.one_minus_beta1, p.one_minus_beta2, p.lr_t], dtype=np.float32)
+        return self.L.orc_apply_grads(self.h, P(g), P(t), P(o))
 
     def last_unique(self):
         n = self.L.orc_last_unique(self.h, None)

@@ -180,3 +180,72 @@ def test_localized_step_single_rank_nccl(ctx, nccl1, multi, opt):
         ctx.sync()
     for t, c in enumerate(cards):
         assert np.array_equal(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])
+
+
+def test_sum_partials_matches_numpy(ctx):
+    from paper_2210_08803_b200.exchange import _ptr
+    from paper_2210_08803_b200 import _lib as L
+    from tests.cpu_engine import sum_partials_np
+    rs = np.random.default_rng(5)
+    G, R, D = 3, 500, 16
+    parts = rs.standard_normal((G, R, D)).astype(np.float32)
+    parts[1, 7] = -0.0
+    touched = (rs.random((G, R)) < 0.5).astype(np.int32)
+    out = torch.empty(R, D, device="cuda")
+    t = torch.empty(R, dtype=torch.int32, device="cuda")
+    pg, tg = torch.from_numpy(parts).cuda(), torch.from_numpy(touched).cuda()
+    L.check(ctx.lib.hps_gpu_sum_partials(ctx.h, _ptr(pg), _ptr(tg), G, R, D, _ptr(out), _ptr(t)), "sum_partials")
+    ro, rt = sum_partials_np(parts, touched, G, R)
+    np.testing.assert_array_equal(t.cpu().numpy(), rt.numpy())
+    m = rt.numpy() != 0
+    assert np.array_equal(out.cpu().numpy()[m].view(np.uint32), ro.numpy()[m].view(np.uint32))
+
+
+@pytest.mark.parametrize("multi,opt", [(False, "sgd"), (True, "adam")])
+def test_hybrid_step_single_rank_nccl(ctx, nccl1, multi, opt):
+    """Hybrid exchange on a world of one over NCCL: hot replica + cold shard, every kernel of
+    the path (probe, cold bucketize/gather, pool, cold grads, backward_reduce, sum_partials,
+    apply_grads), against the single-table oracle with the hybrid reduction order."""
+    from paper_2210_08803_b200.exchange import HybridExchange, HybridGpuEngine
+    from tests.test_multiproc_exchange import _hybrid_reference_step
+    rs = np.random.default_rng(13)
+    cards, slots, dim = [3000, 12, 700], [2, 0, 1, 0], 32
+    S, B = len(slots), 400
+    n_hot = [30, 4, 50]
+    comb = "mean" if multi else "sum"
+    ref = O.OracleTable(cards, dim, slots, opt, 9, 0.1)
+    hot = EmbeddingTableGroup(ctx, n_hot, dim, slots, opt, 1 << 16, 1 << 16, 9, 0.1)
+    cold = EmbeddingTableGroup(ctx, cards, dim, list(range(3)), opt, 1 << 16, 1 << 16, 9, 0.1)
+    pools, hot_rows = [], []
+    for t, c in enumerate(cards):
+        ks = rs.integers(0, 2**63, c).astype(np.uint64)
+        ref.insert(t, ks)
+        hot.insert(t, t64(ks[:n_hot[t]]))
+        cold.insert(t, t64(ks[n_hot[t]:]))
+        hot_rows.extend((int(sum(cards[:t])) + ref.find(t, ks[:n_hot[t]]).astype(np.int64)).tolist())
+        pools.append(ks)
+    hot_rows = np.array(hot_rows, dtype=np.int64)
+    eng = HybridGpuEngine(ctx, hot, GpuEngine(ctx, cold, slots, 1 << 16, 1), 1 << 16)
+    ex = HybridExchange(eng, comb, 0, 1, S)
+    for step in range(1, 4):
+        lens = rs.integers(0, 8, B * S) if multi else np.ones(B * S, dtype=np.int64)
+        offs = np.zeros(B * S + 1, dtype=np.int64)
+        offs[1:] = np.cumsum(lens)
+        keys = np.concatenate([np.where(rs.random(lens[k]) < 0.5, pools[slots[k % S]][rs.integers(0, 3, lens[k])],
+                                        rs.choice(pools[slots[k % S]], lens[k])) for k in range(B * S)]).astype(np.uint64)
+        od = torch.from_numpy(offs.astype(np.int32)).cuda() if multi else None
+        ref_out = ref.lookup(keys, B, offsets=offs.astype(np.uint32) if multi else None, combiner=comb)
+        out = ex.forward(t64(keys), od, B).cpu().numpy()
+        assert np.array_equal(out.view(np.uint32), ref_out.view(np.uint32))
+        dout = rs.standard_normal(ref_out.shape).astype(np.float32)
+        p = opt_params(opt, 0.05, step=step)
+        ex.backward(torch.from_numpy(dout).cuda(), p)
+        _hybrid_reference_step(ref, keys, offs, B, 1, S, multi, comb, dout, p, hot_rows)
+        ctx.sync()
+    for t, c in enumerate(cards):
+        rw = ref.export(t, 0, c)[0]
+        hr = ref.find(t, pools[t][:n_hot[t]]).astype(np.int64)
+        assert np.array_equal(hot.export(t, 0, n_hot[t])[0].cpu().numpy(), rw[hr])
+        cr = ref.find(t, pools[t][n_hot[t]:]).astype(np.int64)
+        assert np.array_equal(cold.export(t, 0, c - n_hot[t])[0].cpu().numpy(), rw[cr])
+    eng.cold.close()
