@@ -45,8 +45,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg5"])
     ap.add_argument("--batch-per-gpu", type=int, default=None)
-    ap.add_argument("--placement", default="auto", choices=["auto", "distributed", "localized"],
+    ap.add_argument("--placement", default="auto", choices=["auto", "distributed", "localized", "hybrid"],
                     help="multi-GPU slot placement (auto: localized for cfg3, distributed otherwise)")
+    ap.add_argument("--hot-budget-gb", type=float, default=0.0625, help="hybrid: replicated hot rows per GPU")
+    ap.add_argument("--force-exchange", action="store_true",
+                    help="run the multi-GPU exchange path (NCCL world of one) on a single GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pool", type=int, default=4, help="distinct synthetic batches rotated through")
     ap.add_argument("--no-graph", action="store_true")
@@ -219,19 +222,31 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2210_08803_b200 import Context, opt_params
-    from paper_2210_08803_b200.sharded import build_tables, build_tables_localized, localized_plan, TrainStep
+    from paper_2210_08803_b200.sharded import (build_tables, build_tables_hybrid, build_tables_localized,
+                                               hybrid_hot_set, localized_plan, TrainStep)
 
     torch.cuda.set_device(local)
-    if world > 1:
+    xchg = world > 1 or args.force_exchange
+    if xchg:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29512")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     ctx = Context(local)
     t_setup = time.perf_counter()
     placement = args.placement if args.placement != "auto" else ("localized" if args.config == "cfg3" else "distributed")
-    owned = localized_plan(cfg, world) if world > 1 and placement == "localized" else None
-    tables = build_tables(ctx, cfg, rank, world) if owned is None else build_tables_localized(ctx, cfg, owned, rank,
-                                                                                               world)
+    owned = localized_plan(cfg, world) if xchg and placement == "localized" else None
+    hot = None
+    if xchg and placement == "hybrid":
+        hot, tables = build_tables_hybrid(ctx, cfg, rank, world, hybrid_hot_set(cfg, int(args.hot_budget_gb * 1e9)))
+    elif owned is None:
+        tables = build_tables(ctx, cfg, rank, world)
+    else:
+        tables = build_tables_localized(ctx, cfg, owned, rank, world)
     gen = W.BatchGen(cfg)
-    step_fn = TrainStep(ctx, tables, cfg, rank, world, owned=owned)
+    step_fn = TrainStep(ctx, tables, cfg, rank, world, owned=owned, hybrid_hot=hot, force_exchange=xchg)
     pool = []
     rs = np.random.default_rng(rank)
     n_bags = cfg.batch * cfg.n_slots
@@ -336,7 +351,7 @@ def main():
             "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * world,
                        "tables": len(cfg.cards), "rows": int(sum(cfg.cards)), "dim": cfg.dim,
                        "hot": cfg.hot, "combiner": cfg.combiner, "optimizer": cfg.optimizer,
-                       "parallelism": f"{step_fn.placement}-slot x{world}" if world > 1 else "single",
+                       "parallelism": f"{step_fn.placement}-slot x{world}" if xchg else "single",
                        "l2": "flushed between timed steps (256 MB write)", "graph": step_fn.graph_mode,
                        "keyspace": cfg.keyspace, "insert_on_miss": step_fn.insert_missing},
             "roofline": {"bound": "hbm", "kernel": "k_lookup_1hot (fused hash+probe+gather+pool)" if cfg.hot == 1
@@ -351,17 +366,17 @@ def main():
             "cpu_baseline": cpu,
             "unique_keys": U, "key_occurrences": N, "setup_s": setup_s,
         }
-        if world > 1:
+        if xchg:
             xb = step_fn.exchange.exchanged_bytes(cfg.dim)
             line["nvlink"] = {"bytes_per_step_rank0": xb, "achieved_gbs": xb / (ms_max / 1000.0) / 1e9,
                               "peak_gbs": 770.0, "peak_kind": "measured peer copy (B200_PROFILING.md)",
                               "frac": xb / (ms_max / 1000.0) / 1e9 / 770.0}
             line["roofline"]["kernel"] = (
-                "distributed forward (bucketize + all-to-all + gather + all-to-all + pool)"
-                if step_fn.placement == "distributed" else
-                "localized forward (regroup + all-to-all + owner lookup + all-to-all + place)")
+                {"distributed": "distributed forward (bucketize + all-to-all + gather + all-to-all + pool)",
+                 "localized": "localized forward (regroup + all-to-all + owner lookup + all-to-all + place)",
+                 "hybrid": "hybrid forward (hot probe + cold all-to-all + gather + all-to-all + pool)"}[step_fn.placement])
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if xchg:
         dist.barrier()
         dist.destroy_process_group()
 

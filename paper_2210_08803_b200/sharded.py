@@ -88,17 +88,67 @@ def build_tables_localized(ctx: Context, cfg: W.Config, owned: List[List[int]], 
     return g
 
 
+def hybrid_hot_set(cfg: W.Config, hot_budget_bytes: int, sample_steps: int = 4) -> List[np.ndarray]:
+    """Hot keys per table (SPEC.md:492-496 plan_hybrid): keys ranked by frequency over
+    `sample_steps` synthetic batches (count desc; ties by table then key asc), taken while
+    the replicated rows (weights + optimizer state) fit hot_budget_bytes per device."""
+    gen = W.BatchGen(cfg)
+    n_state = {"sgd": 0, "adagrad": 1, "adam": 2}[cfg.optimizer]
+    row_bytes = cfg.dim * 4 * (1 + n_state)
+    ks, ts = [], []
+    for s in range(sample_steps):
+        k, _, _, tab = gen.batch(10_000 + s)
+        ks.append(k)
+        ts.append(tab.astype(np.int64))
+    k, t = np.concatenate(ks), np.concatenate(ts)
+    pair = np.stack([t.astype(np.uint64), k]).T
+    uniq, counts = np.unique(pair, axis=0, return_counts=True)
+    order = np.lexsort((uniq[:, 1], uniq[:, 0], -counts))  # count desc, then (table, key) asc
+    take = order[: max(0, hot_budget_bytes // row_bytes)]
+    hot = uniq[take]
+    return [np.sort(hot[hot[:, 0] == i, 1]) for i in range(len(cfg.cards))]
+
+
+def build_tables_hybrid(ctx: Context, cfg: W.Config, rank: int, world: int, hot_keys: List[np.ndarray],
+                        chunk: int = 1 << 24):
+    """(hot replica group, cold shard group): the hot keys of every table on every rank;
+    every other key on its owner partition_of(key, G)."""
+    n_bags = cfg.batch * cfg.n_slots
+    max_keys = table_max_keys(cfg, world)
+    hot_caps = [max(1, len(h)) for h in hot_keys]
+    hot = EmbeddingTableGroup(ctx, hot_caps, cfg.dim, cfg.slots(), cfg.optimizer, max_batch_keys=table_max_keys(cfg, 1),
+                              max_batch_bags=n_bags, init_seed=cfg.seed)
+    caps = [int(c / world * 1.02 + 64 * math.sqrt(c / world + 1) + 64) for c in cfg.cards]
+    cold = EmbeddingTableGroup(ctx, caps, cfg.dim, list(range(len(cfg.cards))), cfg.optimizer,
+                               max_batch_keys=max_keys, max_batch_bags=max(n_bags * world, max_keys),
+                               init_seed=cfg.seed)
+    for t, c in enumerate(cfg.cards):
+        hk = torch.from_numpy(hot_keys[t].view(np.int64)).cuda()
+        if hk.numel():
+            hot.insert(t, hk, return_rows=False)
+        for first in range(0, c, chunk):
+            keys = _owned_keys(ctx, cfg, t, rank, world, first, min(chunk, c - first))
+            if hk.numel():
+                keys = keys[~torch.isin(keys, hk)]
+            cold.insert(t, keys, return_rows=False)
+    ctx.sync()
+    return hot, cold
+
+
 class TrainStep:
     """One fwd+bwd+update step over a staged batch. world == 1 runs the fused path
     (2 C-ABI calls, optionally replayed as one CUDA graph); world > 1 runs the
     distributed or localized exchange (paper_2210_08803_b200.exchange)."""
 
     def __init__(self, ctx: Context, table: Optional[EmbeddingTableGroup], cfg: W.Config, rank: int = 0,
-                 world: int = 1, use_graph: bool = True, owned: Optional[List[List[int]]] = None):
+                 world: int = 1, use_graph: bool = True, owned: Optional[List[List[int]]] = None,
+                 hybrid_hot: Optional[EmbeddingTableGroup] = None, force_exchange: bool = False):
         """owned (world > 1): localized placement, owned[g] = slots of rank g (localized_plan);
         None = distributed placement."""
         self.ctx, self.table, self.cfg, self.rank, self.world = ctx, table, cfg, rank, world
-        self.placement = "single" if world == 1 else ("localized" if owned is not None else "distributed")
+        multi = world > 1 or force_exchange  # force_exchange: the exchange path on a world of one
+        self.placement = ("single" if not multi else "localized" if owned is not None
+                          else "hybrid" if hybrid_hot is not None else "distributed")
         self.n_bags = cfg.batch * cfg.n_slots
         self.out = torch.empty(self.n_bags, cfg.dim, dtype=torch.float32, device="cuda")
         self.params = opt_params(cfg.optimizer, cfg.lr, eps=cfg.eps)
@@ -110,7 +160,7 @@ class TrainStep:
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self._cnt_host = torch.zeros(1, dtype=torch.int64).pin_memory()
         self.exchange = None
-        if world > 1 and owned is not None:
+        if multi and owned is not None:
             from .exchange import LocalizedExchange, LocalizedGpuEngine
             self.engine = LocalizedGpuEngine(ctx, table, cfg.n_slots, owned, cfg.batch, table_max_keys(cfg, 1), cfg.dim)
             self.exchange = LocalizedExchange(self.engine, cfg.combiner, rank, world, cfg.n_slots, owned)
@@ -118,7 +168,15 @@ class TrainStep:
             # regroup (lengths + scan + keys) per owner [+ owner offsets] + lookup + place per owner
             # + place(1) per owner + backward (hist + passes + scan + 3 reduce kernels)
             self.kernels_per_step = 3 * world + (1 if multi else 0) + 1 + 2 * world + 7
-        elif world > 1:
+        elif multi and hybrid_hot is not None:
+            from .exchange import GpuEngine, HybridExchange, HybridGpuEngine
+            cold_engine = GpuEngine(ctx, table, cfg.slots(), table_max_keys(cfg, 1), world)
+            self.engine = HybridGpuEngine(ctx, hybrid_hot, cold_engine, table_max_keys(cfg, 1))
+            self.exchange = HybridExchange(self.engine, cfg.combiner, rank, world, cfg.n_slots)
+            # probe + scan + bucketize(5) + gather + pool + cold grads + cold backward(7)
+            # + reduce(7) + sum_partials + apply
+            self.kernels_per_step = 2 + 5 + 1 + 1 + 1 + 7 + 7 + 2
+        elif multi:
             from .exchange import DistributedExchange, GpuEngine
             max_keys = table_max_keys(cfg, 1)
             self.engine = GpuEngine(ctx, table, cfg.slots(), max_keys, world, insert_missing=self.insert_missing)
@@ -151,7 +209,7 @@ class TrainStep:
     def _exchange_step(self, keys, offs, dout, step):
         if self.cfg.optimizer == "adam":
             self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
-        n = self.cfg.batch if self.placement == "localized" else self.n_bags
+        n = self.cfg.batch if self.placement in ("localized", "hybrid") else self.n_bags
         self.out = self.exchange.forward(keys, offs, n, train=True)
         self.exchange.backward(dout, self.params)
 
@@ -219,7 +277,7 @@ class TrainStep:
 
     def lookup_only(self, b):
         if self.exchange is not None:
-            n = self.cfg.batch if self.placement == "localized" else self.n_bags
+            n = self.cfg.batch if self.placement in ("localized", "hybrid") else self.n_bags
             self.exchange.forward(b["keys"], b["offs"], n, train=False)
             return
         self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=False,
