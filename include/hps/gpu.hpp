@@ -152,6 +152,17 @@ class HotCache {
   /// Replacements (resident keys with a newer version); never inserts.
   uint64_t refresh(std::span<const VersionedEntry> entries) { return apply(entries, false); }
 
+  /// Refresh from one encoded UpdateBatch frame: resident keys with an
+  /// older version take the frame's vectors at version = seq. Returns replacements.
+  uint64_t apply_update(std::span<const std::byte> frame) {
+    counts_.resize(2);
+    check(hps_gpu_cache_apply_update(h_, reinterpret_cast<const uint8_t*>(frame.data()), frame.size(), counts_.get()),
+          "hps_gpu_cache_apply_update");
+    uint64_t n = 0;
+    cuda_check(cudaMemcpy(&n, counts_.get(), 8, cudaMemcpyDeviceToHost), "D2H");
+    return n;
+  }
+
   hps_cache_stats stats() {
     hps_cache_stats s{};
     check(hps_gpu_cache_stats(h_, &s), "hps_gpu_cache_stats");

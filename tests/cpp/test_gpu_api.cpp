@@ -41,6 +41,28 @@ int main() {
   auto s = cache.stats();
   REQUIRE(s.queries == 5 && s.hits + s.misses == s.queries && s.hits == 2);
   REQUIRE(cache.size() == 1);
+  // an encoded UpdateBatch frame refreshes resident keys at version = seq
+  {
+    const uint64_t fk[2] = {7, 12345};
+    std::vector<float> fv(8);
+    for (int j = 0; j < 8; ++j) fv[j] = 40.f + j;
+    uint64_t len = 0;
+    REQUIRE(hps_update_batch_encode("ads", 3, /*seq=*/9, 2, 4, 0, fk, fv.data(), nullptr, 0, &len) == 0);
+    REQUIRE(len == 25 + 2 * (8 + 16));
+    std::vector<std::byte> frame(len);
+    REQUIRE(hps_update_batch_encode("ads", 3, 9, 2, 4, 0, fk, fv.data(), reinterpret_cast<uint8_t*>(frame.data()), len,
+                                    &len) == 0);
+    REQUIRE(cache.apply_update(frame) == 1);  // key 7 (version 5 -> 9); 12345 is not resident
+    r = cache.query(k7);
+    REQUIRE(r.found[0].second == vec(40.f));
+    frame[0] = std::byte{0};  // bad magic
+    try {
+      cache.apply_update(frame);
+      REQUIRE(false);
+    } catch (const hps::Error& e) {
+      REQUIRE(e.code() == hps::ErrorCode::BadMagic);
+    }
+  }
   // a dim mismatch is a DimMismatch, like the reference's entry validation
   std::vector<hps::VersionedEntry> bad{{9, vec(0.f, 8), 1}};
   try {
