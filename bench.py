@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--table-scale", type=float, default=1.0, help="debug only: shrink cardinalities")
+    ap.add_argument("--trace", type=int, default=0,
+                    help="debug: after timing, replay N steps with the in-graph kernel timeline on (stderr)")
     return ap.parse_args()
 
 
@@ -205,6 +207,35 @@ def reference_arm(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+TRACE_NAMES = {0: "probe", 1: "pool", 2: "seg_alloc", 3: "place", 4: "long_hist", 5: "long_pass0",
+               6: "long_pass1", 7: "long_pass2", 8: "long_pass3", 9: "long_reg", 10: "reduce_short",
+               11: "reduce_long", 12: "reset_counts"}
+
+
+def print_trace(ctx, n, step):
+    """In-graph kernel timeline (hps_gpu_debug_trace): median start/end of each traced kernel
+    relative to the step's first kernel, over n replays (L2 flushed before each)."""
+    import ctypes
+    lib = ctx.lib
+    buf = (ctypes.c_uint64 * 64)()
+    lib.hps_gpu_debug_trace(1, None)
+    recs = []
+    for i in range(n):
+        step(i)
+        lib.hps_gpu_debug_trace(2, buf)
+        r = {k: (buf[2 * k], buf[2 * k + 1]) for k in TRACE_NAMES if buf[2 * k] != (1 << 64) - 1}
+        if r:
+            t0 = min(v[0] for v in r.values())
+            recs.append({k: ((a - t0) / 1000.0, (b - t0) / 1000.0) for k, (a, b) in r.items()})
+    lib.hps_gpu_debug_trace(0, None)
+    keys = sorted({k for r in recs for k in r}, key=lambda k: float(np.median([r[k][0] for r in recs if k in r])))
+    print(f"# in-graph timeline, us (median of {len(recs)} steps)", file=sys.stderr)
+    for k in keys:
+        st = float(np.median([r[k][0] for r in recs if k in r]))
+        en = float(np.median([r[k][1] for r in recs if k in r]))
+        print(f"#   {TRACE_NAMES[k]:<14s} {st:8.1f} -> {en:8.1f}  ({en - st:6.1f})", file=sys.stderr)
+
+
 # ---------------------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------------------
@@ -293,6 +324,10 @@ def main():
         fwd_ev[i][1].record(stream)
     torch.cuda.synchronize()
     fwd_ms = [a.elapsed_time(b) for a, b in fwd_ev]
+    if args.trace:
+        print_trace(ctx, args.trace, lambda i: (flush.fill_(i & 0xff),
+                                                step_fn.run(pool[i % len(pool)], douts[i % len(douts)],
+                                                            step=args.warmup + args.steps + i + 1)))
     ms = float(np.mean(step_ms))
     t = torch.tensor([ms], device="cuda")
     if world > 1:

@@ -170,6 +170,14 @@ int hps_gpu_backward_update(hps_gpu_table tbl, const float* d_out, const hps_opt
  * max_batch_keys). Used by the dedup parity tests. */
 int hps_gpu_table_last_unique(hps_gpu_table tbl, uint64_t* count_out, uint32_t* unique_rows_out);
 
+/* Tracing (no reference counterpart): in-graph timeline of the training
+ * step's kernels, %globaltimer ns. mode 1 attaches a zeroed trace buffer, 2 copies
+ * 32 x {first CTA start, last warp end} (u64 pairs; start = UINT64_MAX: not run) into
+ * trace_host and re-arms, 0 detaches. Ids: 0 probe, 1 pool, 2 segment alloc, 3 place,
+ * 4 long-sort histogram, 5..8 long-sort passes, 9 long registration, 10 short reduce,
+ * 11 long reduce, 12 counter reset. Synchronises the device; not for hot paths. */
+int hps_gpu_debug_trace(int mode, uint64_t* trace_host);
+
 /* Owner side of the distributed exchange: rows of keys[i] in table tables[i] (one key per
  * "bag"; absent keys give the table's default vector). With HPS_LOOKUP_TRAIN the following
  * backward_update takes d_out = [n x dim] per-key gradients (already combiner-scaled). */

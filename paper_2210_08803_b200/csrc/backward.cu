@@ -7,14 +7,20 @@
 // the same way until one vector remains (plain sequential order up to 32 occurrences).
 // Then SGD / AdaGrad / Adam update the row in place.
 //
-// Pipeline (sizes device-resident, graph-capturable; the training lookup clears the
-// look-back region, and every kernel below is a programmatic dependent launch):
-//   k_radix_hist/k_radix_pass : stable LSD sort of (row, bag) by row — the dedup; stability
-//                               keeps each key's occurrences in canonical order
-//   k_scan<SegOp>   : unique-row segments [start, end) of the sorted list
-//   k_reduce_short  : a warp owns 32 segments: short ones (<= 32 occurrences) are reduced
-//                     and updated (register path, or the bulk-copy path for 128 <= dim <=
-//                     256); long ones are registered as 32-occurrence chunk tasks
+// Dedup without a global sort (sizes device-resident, graph-capturable; every kernel is a
+// programmatic dependent launch). The training lookup counted each occurrence on its
+// row in the aux word of its index slot (kAuxNone + count; the atomic returns the rank). Then:
+//   k_seg_alloc     : the rank-0 occurrence of each row allocates its segment — short rows
+//                     (<= 32 occurrences) a CSR range of the short list, long rows an id —
+//                     and leaves the locator in the slot aux word
+//   k_scan<PlaceOp> : every occurrence drops its bag into its short segment at `rank`, or is
+//                     compacted (canonical order) into the long list as (long id, bag)
+//   long sort       : stable radix sort of the long list by long id (few bits) — each long
+//                     segment contiguous, occurrences in canonical order
+//   k_scan<LongRegOp>: long segment starts, level-1 chunk bases, tree-node blocks; counters reset
+//   k_reduce_short  : a warp owns 32 short segments: sorts each one's bags back into canonical
+//                     order (warp rank), reduces and updates (bulk-copy or register path),
+//                     resets the counters; it also publishes the long chunk -> segment map
 //   k_long          : one warp per chunk -> level-1 partial; the last chunk to finish below
 //                     a tree node sums that node's <= 32 children in order, up to the root,
 //                     whose sum goes through the optimizer (hierarchical last-arriver)
@@ -30,19 +36,31 @@ using namespace hpsg;
 namespace {
 
 struct BwdArgs {
-  const uint64_t* counts;  // [0]=N occurrences [1]=U segments
-  const uint32_t* rows;    // sorted global rows
-  const uint32_t* bags;    // bag of each sorted occurrence
-  uint32_t* seg_start;
-  uint32_t* seg_end;
+  const uint64_t* counts;   // [0] = N occurrences; [1] <- unique rows (short + long segments)
+  const uint32_t* occ_row;  // row of each occurrence (row_absent: no gradient)
+  const uint32_t* occ_rank; // arrival rank of each occurrence within its row
+  const uint32_t* occ_bag;  // multi-hot: bag of each occurrence (nullptr: occurrence i is bag i)
+  const uint32_t* occ_slot; // index slot of each occurrence's key
+  Slot* slots;              // slot aux: kAuxNone + count -> segment locator -> kAuxNone (reset here)
   uint32_t row_absent;
+  unsigned long long* short_alloc;  // (segments << 32) | occurrences
+  uint4* short_rec;                 // {row, first, len, slot}
+  uint32_t* short_bag;
+  uint32_t* n_long;
+  uint32_t* long_row;
+  uint32_t* long_slot;
+  uint32_t* long_len;
+  uint32_t* long_start;     // first position of the segment in the sorted long list
+  uint32_t* lkey;           // long list: segment id (sort input)
+  uint32_t* lval;           // long list: bag (sort input)
+  const uint32_t* lbag;     // long list sorted by segment id: bags in canonical order
+  unsigned long long* long_occ;     // long-list length
+  unsigned long long* long_chunks;  // level-1 chunks over all long segments
   const uint32_t* bag_len;  // mean combiner: bag lengths (nullptr: sum)
   const float* dout;
   uint32_t dim;
-  uint32_t* long_seg;
   uint32_t* long_base;
   uint32_t* task_long;
-  unsigned long long* long_packed;  // (n_long << 32) | total level-1 chunks
   float* partial;                   // level-1 partials [max_chunks x dim]
   float* partial2;                  // higher levels [max_chunks/32 + max_long x dim]
   uint32_t* long_hbase;             // long segment -> first node of its levels >= 2 in partial2
@@ -57,20 +75,175 @@ struct BwdArgs {
   hps_opt_params opt;
 };
 
-// ---- segments of the sorted list ----------------------------------------------------
-struct SegOp {
-  const uint32_t* rows;
-  uint32_t* seg_start;
-  uint32_t* seg_end;
-  uint64_t* counts;
-  __device__ uint64_t size() const { return counts[0]; }
-  __device__ uint32_t count(uint64_t i) const { return (i == 0 || rows[i] != rows[i - 1]) ? 1u : 0u; }
-  __device__ void emit(uint64_t i, uint64_t excl, uint64_t c) const {
-    if (c) seg_start[excl] = static_cast<uint32_t>(i);
-    if (i + 1 == counts[0] || rows[i + 1] != rows[i]) seg_end[excl + c - 1] = static_cast<uint32_t>(i + 1);
+// ---- K4a: segment allocation (the rank-0 occurrence of each row leads) ------------------
+// A CTA takes 512 consecutive occurrences (2 per thread); its short leaders get
+// consecutive CSR ranges from ONE packed atomic (segments << 32 | occurrences) after a
+// block scan, so segment s+1 starts where segment s ends. Long leaders take ids from a
+// warp-aggregated counter (they are few).
+constexpr int kAllocIPT = 2;
+__global__ void __launch_bounds__(256) k_seg_alloc(BwdArgs a) {
+  __shared__ unsigned long long s_scr[33];
+  __shared__ unsigned long long s_base;
+  pdl_wait();
+  pdl_launch_dependents();
+  trace_begin(kTrAlloc);
+  const uint64_t n = a.counts[0];
+  const uint32_t lane = lane_id(), lt = lanemask_lt();
+  constexpr uint64_t kTile = 256 * kAllocIPT;
+  for (uint64_t t0 = uint64_t(blockIdx.x) * kTile; t0 < n; t0 += uint64_t(gridDim.x) * kTile) {
+    uint32_t row[kAllocIPT], len[kAllocIPT], slot[kAllocIPT];
+    unsigned long long mine = 0;  // (short segments << 32) | their occurrences
+#pragma unroll
+    for (int k = 0; k < kAllocIPT; ++k) {
+      const uint64_t i = t0 + uint64_t(threadIdx.x) * kAllocIPT + k;
+      row[k] = a.row_absent;
+      len[k] = 0;
+      slot[k] = 0;
+      if (i < n) {
+        const uint32_t r = a.occ_row[i];
+        if (r != a.row_absent && a.occ_rank[i] == 0u) {
+          row[k] = r;
+          slot[k] = a.occ_slot[i];
+          len[k] = a.slots[slot[k]].aux + 1u;
+        }
+      }
+      if (len[k] && len[k] <= kChunk) mine += (1ull << 32) | len[k];
+    }
+    unsigned long long total;
+    unsigned long long excl = block_excl_scan<256>(mine, s_scr, &total);
+    if (threadIdx.x == 0 && total) s_base = atomicAdd(a.short_alloc, total);
+    __syncthreads();
+    const unsigned long long base = total ? s_base : 0ull;
+    unsigned long long pos = base + excl;
+#pragma unroll
+    for (int k = 0; k < kAllocIPT; ++k) {
+      if (len[k] && len[k] <= kChunk) {
+        const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
+        a.short_rec[seg] = make_uint4(row[k], first, len[k], slot[k]);
+        a.slots[slot[k]].aux = first;
+        pos += (1ull << 32) | len[k];
+      }
+    }
+    // long leaders (rare): one warp-aggregated id reservation per item slot
+#pragma unroll
+    for (int k = 0; k < kAllocIPT; ++k) {
+      const bool lg = len[k] > kChunk;
+      const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
+      if (!lg_mask) continue;
+      uint32_t j0 = 0;
+      if (lane == __ffs(lg_mask) - 1) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
+      j0 = __shfl_sync(0xffffffffu, j0, __ffs(lg_mask) - 1);
+      if (lg) {
+        const uint32_t j = j0 + __popc(lg_mask & lt);
+        a.long_row[j] = row[k];
+        a.long_slot[j] = slot[k];
+        a.long_len[j] = len[k];
+        a.slots[slot[k]].aux = kLongFlag | j;
+      }
+    }
+    __syncthreads();  // s_base / s_scr reuse
   }
-  __device__ void total(uint64_t u) const { counts[1] = u; }
+  trace_end(kTrAlloc);
+}
+
+// ---- K4b: placement (scan over occurrences; the scan compacts the long ones in order) ----
+struct PlaceOp {
+  static constexpr int kTrace = kTrPlace;
+  BwdArgs a;
+  __device__ uint64_t size() const { return a.counts[0]; }
+  __device__ uint32_t count(uint64_t i) const {
+    const uint32_t r = a.occ_row[i];
+    return r == a.row_absent ? 0u : (a.slots[a.occ_slot[i]].aux >> 31);
+  }
+  __device__ void emit(uint64_t i, uint64_t excl, uint64_t c) const {
+    const uint32_t r = a.occ_row[i];
+    if (r == a.row_absent) return;
+    const uint32_t bag = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+    const uint32_t loc = a.slots[a.occ_slot[i]].aux;
+    if (c) {
+      a.lkey[excl] = loc & ~kLongFlag;
+      a.lval[excl] = bag;
+    } else {
+      a.short_bag[loc + a.occ_rank[i]] = bag;
+    }
+  }
+  __device__ void total(uint64_t t) const { *a.long_occ = t; }
 };
+
+// ---- long segments: registration ---------------------------------------------------------
+// Nodes above level 1 of a long segment's 32-ary tree (m level-1 chunks).
+__device__ __forceinline__ uint32_t higher_nodes(uint32_t m) {
+  uint32_t n = 0;
+  while (m > 1) {
+    m = (m + kChunk - 1) / kChunk;
+    n += m;
+  }
+  return n;
+}
+
+// Scan over long segments of (len | chunks << 32): start in the sorted long list, first
+// level-1 chunk, tree-node block; the row's counter goes back to zero.
+struct LongRegOp {
+  static constexpr int kTrace = kTrLongReg;
+  BwdArgs a;
+  __device__ uint64_t size() const { return *a.n_long; }
+  __device__ uint64_t count(uint64_t j) const {
+    const uint64_t len = a.long_len[j];
+    return len | (((len + kChunk - 1) / kChunk) << 32);
+  }
+  __device__ void emit(uint64_t j, uint64_t excl, uint64_t c) const {
+    const uint32_t m = static_cast<uint32_t>(c >> 32);
+    a.long_start[j] = static_cast<uint32_t>(excl);
+    a.long_base[j] = static_cast<uint32_t>(excl >> 32);
+    a.long_hbase[j] = atomicAdd(a.higher_total, higher_nodes(m));
+    a.slots[a.long_slot[j]].aux = kAuxNone;
+  }
+  __device__ void total(uint64_t t) const {
+    *a.long_chunks = t >> 32;
+    const_cast<uint64_t*>(a.counts)[1] = (*a.short_alloc >> 32) + *a.n_long;
+  }
+};
+
+// Chunk -> long segment map (written by the short-reduce kernel's warps before their own
+// work; consumed by k_long).
+__device__ __forceinline__ void publish_long_tasks(const BwdArgs& a, uint64_t warp, uint64_t n_warps) {
+  const uint32_t nl = *a.n_long;
+  for (uint64_t j = warp; j < nl; j += n_warps) {
+    const uint32_t m = (a.long_len[j] + kChunk - 1) / kChunk, base = a.long_base[j];
+    for (uint32_t c = lane_id(); c < m; c += 32) a.task_long[base + c] = static_cast<uint32_t>(j);
+  }
+}
+
+// A warp's 32 short segments [u0, u0+32) occupy one contiguous range of the short list:
+// load it into shared memory and sort every segment's bags ascending (= canonical order;
+// equal bags carry identical gradients, so their relative order is immaterial).
+// Returns the range start; sbag receives the range (<= 32 * kChunk entries).
+__device__ __forceinline__ uint32_t stage_short_bags(const BwdArgs& a, uint64_t S, uint64_t u0, uint32_t first,
+                                                     uint32_t len, uint32_t* sbag) {
+  const uint32_t lane = lane_id();
+  const uint32_t last = static_cast<uint32_t>(min(uint64_t(31), S - 1 - u0));
+  const uint32_t r0 = __shfl_sync(0xffffffffu, first, 0);
+  const uint32_t r1 = __shfl_sync(0xffffffffu, first + len, last);
+  for (uint32_t p = lane; p < r1 - r0; p += 32) sbag[p] = a.short_bag[r0 + p];
+  __syncwarp();
+  uint32_t multi = __ballot_sync(0xffffffffu, len >= 2);
+  while (multi) {
+    const int j = __ffs(multi) - 1;
+    multi &= multi - 1;
+    const uint32_t jl = __shfl_sync(0xffffffffu, len, j);
+    const uint32_t jo = __shfl_sync(0xffffffffu, first, j) - r0;
+    const uint32_t b = lane < jl ? sbag[jo + lane] : 0xffffffffu;
+    uint32_t rank = 0;
+    for (uint32_t q = 0; q < jl; ++q) {
+      const uint32_t x = __shfl_sync(0xffffffffu, b, q);
+      rank += (x < b || (x == b && q < lane)) ? 1u : 0u;
+    }
+    __syncwarp();
+    if (lane < jl) sbag[jo + rank] = b;
+    __syncwarp();
+  }
+  return r0;
+}
 
 // ---- row math --------------------------------------------------------------------------
 // Row of weights (+ optimizer state): OPT is HPS_OPT_* at compile time, so the loads are
@@ -166,82 +339,43 @@ __device__ __forceinline__ void add_into(float4 (&acc)[VPL], const float4 (&x)[V
   for (int k = 0; k < VPL; ++k) acc[k] = f4_add(acc[k], x[k]);
 }
 
-// ---- long segments: registration ----------------------------------------------------------
-// Nodes above level 1 of a long segment's 32-ary tree (m level-1 chunks).
-__device__ __forceinline__ uint32_t higher_nodes(uint32_t m) {
-  uint32_t n = 0;
-  while (m > 1) {
-    m = (m + kChunk - 1) / kChunk;
-    n += m;
-  }
-  return n;
-}
-
-// Lanes holding a long segment (> kChunk occurrences) register it: id j, first global
-// chunk id, its higher-level node block; then the warp writes the chunk -> segment map.
-__device__ __forceinline__ void register_longs(const BwdArgs& a, uint64_t u0, uint64_t u, bool is_long, uint32_t len) {
-  uint32_t longs = __ballot_sync(0xffffffffu, is_long);
-  uint32_t my_j = 0, my_base = 0;
-  if (is_long) {
-    const uint32_t m = (len + kChunk - 1) / kChunk;
-    const unsigned long long p = atomicAdd(a.long_packed, (1ull << 32) | m);
-    my_j = static_cast<uint32_t>(p >> 32);
-    my_base = static_cast<uint32_t>(p);
-    a.long_seg[my_j] = static_cast<uint32_t>(u);
-    a.long_base[my_j] = my_base;
-    a.long_hbase[my_j] = atomicAdd(a.higher_total, higher_nodes(m));
-  }
-  while (longs) {
-    const int src = __ffs(longs) - 1;
-    longs &= longs - 1;
-    const uint32_t j = __shfl_sync(0xffffffffu, my_j, src);
-    const uint32_t base = __shfl_sync(0xffffffffu, my_base, src);
-    const uint32_t slen = a.seg_end[u0 + src] - a.seg_start[u0 + src];
-    const uint32_t m = (slen + kChunk - 1) / kChunk;
-    for (uint32_t c = lane_id(); c < m; c += 32) a.task_long[base + c] = j;
-  }
-}
-
 // ---- short segments (<= 32 occurrences), register path ----------------------------------
-// A warp owns 32 segments — lane l loads segment l's metadata and first two bags in one
-// round trip — then its lane groups update the segments R at a time (weights/state +
-// gradient rows in flight together).
+// A warp owns 32 segments — lane l holds segment l's record and first two bags — then its
+// lane groups update the segments R at a time (weights/state + gradient rows in flight
+// together). The bags come from the warp's sorted shared-memory copy (stage_short_bags).
 template <int OPT, int LPR, int VPL>
-__device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint64_t n_warps) {
+__device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint64_t n_warps, uint32_t* sbag) {
   constexpr int G = 32 / LPR;  // lane groups (segment streams) per warp
   constexpr int R = VPL >= 4 ? 1 : 4 / VPL;  // segments in flight per group (register budget)
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
-  const uint64_t U = a.counts[1];
+  const uint64_t S = *a.short_alloc >> 32;
   const bool mean = a.bag_len != nullptr;
-  for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
-    // metadata: lane l <-> segment u0 + l
+  for (uint64_t u0 = warp * 32; u0 < S; u0 += n_warps * 32) {
     const uint64_t u = u0 + lane;
-    uint32_t start = 0, len = 0, row = 0, b0 = 0, b1 = 0;
+    uint32_t first = 0, len = 0, row = 0, b0 = 0, b1 = 0, slot = 0;
     float f0 = 1.f, f1 = 1.f;
-    bool is_long = false;
-    if (u < U) {
-      start = a.seg_start[u];
-      len = a.seg_end[u] - start;
-      row = a.rows[start];
-      if (row == a.row_absent) {
-        len = 0;
-      } else if (len > kChunk) {
-        is_long = true;
-      } else {
-        b0 = a.bags[start];
-        if (len >= 2) b1 = a.bags[start + 1];
-        if (mean) {
-          f0 = static_cast<float>(a.bag_len[b0]);
-          if (len >= 2) f1 = static_cast<float>(a.bag_len[b1]);
-        }
+    if (u < S) {
+      const uint4 rec = a.short_rec[u];
+      row = rec.x;
+      first = rec.y;
+      len = rec.z;
+      slot = rec.w;
+    }
+    const uint32_t r0 = stage_short_bags(a, S, u0, first, len, sbag);
+    const uint32_t off = first - r0;
+    if (len) {
+      a.slots[slot].aux = kAuxNone;  // placement (previous kernels) is done with the locator
+      b0 = sbag[off];
+      if (len >= 2) b1 = sbag[off + 1];
+      if (mean) {
+        f0 = static_cast<float>(a.bag_len[b0]);
+        if (len >= 2) f1 = static_cast<float>(a.bag_len[b1]);
       }
     }
-    register_longs(a, u0, u, is_long, len);
-    if (is_long) len = 0;  // handled by the long phase
-    // short segments: group g handles segments g, g+G, ... of the 32, R at a time
+    // group g handles segments g, g+G, ... of the 32, R at a time
 #pragma unroll 1
     for (int j0 = 0; j0 < 32; j0 += G * R) {
-      uint32_t s_len[R], s_start[R], s_row[R], s_b1[R];
+      uint32_t s_len[R], s_off[R], s_row[R], s_b1[R];
       float s_f1[R];
       RowState<OPT, VPL> rs[R];
       float4 g[R][VPL], x[R][VPL];
@@ -249,7 +383,7 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
       for (int r = 0; r < R; ++r) {  // every load of the R segments is issued here, unconditionally
         const uint32_t src = j0 + G * r + grp;
         s_len[r] = __shfl_sync(0xffffffffu, len, src);
-        s_start[r] = __shfl_sync(0xffffffffu, start, src);
+        s_off[r] = __shfl_sync(0xffffffffu, off, src);
         s_row[r] = __shfl_sync(0xffffffffu, row, src);
         const uint32_t sb0 = __shfl_sync(0xffffffffu, b0, src);
         s_b1[r] = __shfl_sync(0xffffffffu, b1, src);
@@ -268,12 +402,11 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
           add_into<VPL>(g[r], x[r]);
         }
         if constexpr (LPR == 32) {  // (narrower groups would diverge across segments of a warp)
-          // occurrences 3..32: the warp loads all remaining bags at once (lane gl holds
-          // occurrence 2+gl), then streams the rows 8 in flight, in order.
+          // occurrences 3..32: lane gl holds occurrence 2+gl's bag, then the warp streams the
+          // rows 8 in flight, in order.
           const uint32_t rest = s_len[r] > 2 ? s_len[r] - 2 : 0;
           if (rest) {
-            const uint32_t p = s_start[r] + 2;
-            const uint32_t bl = gl < rest ? a.bags[p + gl] : 0u;
+            const uint32_t bl = gl < rest ? sbag[s_off[r] + 2 + gl] : 0u;
             const float fll = (mean && gl < rest) ? static_cast<float>(a.bag_len[bl]) : 1.f;
             constexpr int KF = VPL >= 8 ? 1 : 8 / VPL;  // rows in flight (register budget)
             for (uint32_t q0 = 0; q0 < rest; q0 += KF) {
@@ -298,9 +431,9 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
           }
         } else {
           for (uint32_t q = 2; q < s_len[r]; q += 2) {  // narrow rows: two rows in flight
-            const uint32_t bq = a.bags[s_start[r] + q];
+            const uint32_t bq = sbag[s_off[r] + q];
             const bool two = q + 1 < s_len[r];
-            const uint32_t bq1 = two ? a.bags[s_start[r] + q + 1] : bq;
+            const uint32_t bq1 = two ? sbag[s_off[r] + q + 1] : bq;
             float4 y[VPL], z[VPL];
             load_grad<VPL>(a, bq, gl, LPR, y);
             if (two) load_grad<VPL>(a, bq1, gl, LPR, z);
@@ -315,6 +448,7 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
         update_store<OPT, VPL>(a, s_row[r], gl, LPR, rs[r], g[r]);
       }
     }
+    __syncwarp();  // sbag is rewritten by the next iteration
   }
 }
 
@@ -326,6 +460,7 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
 // and only then does the warp walk the wave segment by segment (ordered sum from smem,
 // fused optimizer, 128-bit stores). Bytes in flight no longer cost registers.
 constexpr int kRedWarps = 4;
+constexpr int kBagStage = 32 * kChunk;  // sorted bags of a warp's 32 short segments
 
 template <int OPT, int VPL>
 __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint64_t n_warps, float* s_buf,
@@ -335,6 +470,7 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
   const uint32_t D = a.dim, nvec = D / 4, row_bytes = D * 4, cap = a.tma_rows;
   float* buf = s_buf + size_t(w) * cap * D;
   float* scale = s_buf + size_t(kRedWarps) * cap * D + size_t(w) * cap;
+  uint32_t* sbag = reinterpret_cast<uint32_t*>(s_buf + size_t(kRedWarps) * cap * (D + 1)) + size_t(w) * kBagStage;
   const bool mean = a.bag_len != nullptr;
   if (lane == 0) {
     mbar_init(&s_bar[w], 1);
@@ -342,33 +478,28 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
   }
   __syncwarp();
   uint32_t phase = 0;
-  const uint64_t U = a.counts[1];
-  for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
+  const uint64_t S = *a.short_alloc >> 32;
+  for (uint64_t u0 = warp * 32; u0 < S; u0 += n_warps * 32) {
     const uint64_t u = u0 + lane;
-    uint32_t start = 0, len = 0, row = 0, b0 = 0, b1 = 0;
-    bool is_long = false;
-    if (u < U) {
-      start = a.seg_start[u];
-      len = a.seg_end[u] - start;
-      row = a.rows[start];
-      b0 = a.bags[start];  // loaded with the row: copies of 1-2 occurrence segments issue at once
-      if (len >= 2) b1 = a.bags[start + 1];
-      if (row == a.row_absent) {
-        len = 0;
-      } else if (len > kChunk) {
-        is_long = true;
-      }
+    uint32_t first = 0, len = 0, row = 0, slot = 0;
+    if (u < S) {
+      const uint4 rec = a.short_rec[u];
+      row = rec.x;
+      first = rec.y;
+      len = rec.z;
+      slot = rec.w;
     }
-    register_longs(a, u0, u, is_long, len);
-    if (is_long) len = 0;
+    const uint32_t r0 = stage_short_bags(a, S, u0, first, len, sbag);
+    const uint32_t boff = first - r0;
+    if (len) a.slots[slot].aux = kAuxNone;  // placement (previous kernels) is done with the locator
     const uint32_t need = len ? 1 + NS + len : 0;
-    uint32_t first = 0;  // first lane (segment) of the current wave
-    while (first < 32) {
-      const uint32_t r = lane >= first ? need : 0u;
+    uint32_t first_lane = 0;  // first lane (segment) of the current wave
+    while (first_lane < 32) {
+      const uint32_t r = lane >= first_lane ? need : 0u;
       const uint32_t incl = warp_incl_scan(r);
-      const bool in_wave = lane >= first && incl <= cap;
+      const bool in_wave = lane >= first_lane && incl <= cap;
       const uint32_t wave_mask = __ballot_sync(0xffffffffu, in_wave);
-      const uint32_t last = 31 - __clz(wave_mask);  // wave = lanes [first, last]
+      const uint32_t last = 31 - __clz(wave_mask);  // wave = lanes [first_lane, last]
       const uint32_t off = incl - r;
       const uint32_t total_rows = __shfl_sync(0xffffffffu, incl, last);
       if (lane == 0) mbar_arrive_expect_tx(&s_bar[w], total_rows * row_bytes);
@@ -378,29 +509,17 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
         bulk_g2s(dst, a.W + uint64_t(row) * D, row_bytes, &s_bar[w]);
         if constexpr (NS >= 1) bulk_g2s(dst + D, a.S0 + uint64_t(row) * D, row_bytes, &s_bar[w]);
         if constexpr (NS >= 2) bulk_g2s(dst + 2 * D, a.S1 + uint64_t(row) * D, row_bytes, &s_bar[w]);
-        bulk_g2s(dst + (1 + NS) * D, a.dout + uint64_t(b0) * D, row_bytes, &s_bar[w]);
-        if (len >= 2) bulk_g2s(dst + (2 + NS) * D, a.dout + uint64_t(b1) * D, row_bytes, &s_bar[w]);
-        if (mean) {
-          scale[off + 1 + NS] = static_cast<float>(a.bag_len[b0]);
-          if (len >= 2) scale[off + 2 + NS] = static_cast<float>(a.bag_len[b1]);
-        }
-        for (uint32_t q0 = 2; q0 < len; q0 += 4) {  // occurrences 3..32: bag ids 4 at a time
-          uint32_t bq[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) bq[k] = q0 + k < len ? a.bags[start + q0 + k] : 0u;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (q0 + k >= len) break;
-            bulk_g2s(dst + (1 + NS + q0 + k) * D, a.dout + uint64_t(bq[k]) * D, row_bytes, &s_bar[w]);
-            if (mean) scale[off + 1 + NS + q0 + k] = static_cast<float>(a.bag_len[bq[k]]);
-          }
+        for (uint32_t q = 0; q < len; ++q) {
+          const uint32_t bq = sbag[boff + q];
+          bulk_g2s(dst + (1 + NS + q) * D, a.dout + uint64_t(bq) * D, row_bytes, &s_bar[w]);
+          if (mean) scale[off + 1 + NS + q] = static_cast<float>(a.bag_len[bq]);
         }
       }
       mbar_wait(&s_bar[w], phase);
       phase ^= 1;
       __syncwarp();  // the scale[] writes of other lanes
       // walk the wave in segment order
-      for (uint32_t j = first; j <= last; ++j) {
+      for (uint32_t j = first_lane; j <= last; ++j) {
         const uint32_t jl = __shfl_sync(0xffffffffu, len, j);
         const uint32_t jo = __shfl_sync(0xffffffffu, off, j);
         const uint32_t jr = __shfl_sync(0xffffffffu, row, j);
@@ -429,7 +548,7 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
         update_store<OPT, VPL>(a, jr, lane, 32, rs, g);
       }
       __syncwarp();  // every lane is done reading the buffer before the next wave overwrites it
-      first = last + 1;
+      first_lane = last + 1;
     }
   }
 }
@@ -519,15 +638,14 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
   constexpr int VW = LPR == 32 ? VPL : 1;  // warp-wide layout of the same row (LPR < 32 <=> nvec <= 32)
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = a.dim / 4;
   const bool mean = a.bag_len != nullptr;
-  const uint64_t T = static_cast<uint32_t>(__ldcg(reinterpret_cast<const unsigned long long*>(a.long_packed)));
+  const uint64_t T = *a.long_chunks;
   for (uint64_t t = warp; t < T; t += n_warps) {
-    const uint32_t j = __ldcg(a.task_long + t);
-    const uint32_t u = __ldcg(a.long_seg + j);
-    const uint32_t c = static_cast<uint32_t>(t) - __ldcg(a.long_base + j);
-    const uint32_t s0 = a.seg_start[u], e = a.seg_end[u];
+    const uint32_t j = a.task_long[t];
+    const uint32_t c = static_cast<uint32_t>(t) - a.long_base[j];
+    const uint32_t s0 = a.long_start[j], e = s0 + a.long_len[j];
     const uint32_t s = s0 + c * kChunk;
     const uint32_t n = min(static_cast<uint32_t>(kChunk), e - s);
-    const uint32_t my_bag = lane < n ? a.bags[s + lane] : 0u;
+    const uint32_t my_bag = lane < n ? a.lbag[s + lane] : 0u;
     const float my_f = (mean && lane < n) ? static_cast<float>(a.bag_len[my_bag]) : 1.f;
     float4 acc[VPL];
     for (uint32_t q0 = 0; q0 < n; q0 += G * RB) {  // n is warp-uniform
@@ -573,27 +691,30 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
         if (v < nvec) __stcg(p + v, acc[k]);
       }
     }
-    climb<OPT, VW>(a, j, c, (e - s0 + kChunk - 1) / kChunk, a.rows[s0]);
+    climb<OPT, VW>(a, j, c, (e - s0 + kChunk - 1) / kChunk, a.long_row[j]);
   }
 }
 
 // ---- kernels ------------------------------------------------------------------------------
-// Short segments reduced + updated; long segments registered as chunk tasks.
+// Short segments reduced + updated (after publishing the long chunk -> segment map).
 template <int OPT, int LPR, int VPL, bool TMA>
 __global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : 2)
     k_reduce_short(BwdArgs a) {
-  extern __shared__ __align__(128) float s_dyn[];  // TMA: [kRedWarps][cap][dim] rows, then scales
+  extern __shared__ __align__(128) float s_dyn[];  // TMA: [kRedWarps][cap][dim] rows, scales, bags
   __shared__ __align__(8) uint64_t s_bar[kRedWarps];
   pdl_wait();
   pdl_launch_dependents();
   const uint64_t wpb = blockDim.x >> 5;
   const uint64_t warp = uint64_t(blockIdx.x) * wpb + (threadIdx.x >> 5);
   const uint64_t n_warps = uint64_t(gridDim.x) * wpb;
+  trace_begin(kTrReduce);
+  publish_long_tasks(a, warp, n_warps);
   if constexpr (TMA) {
     short_tma<OPT, VPL>(a, warp, n_warps, s_dyn, s_bar);
   } else {
-    short_reg<OPT, LPR, VPL>(a, warp, n_warps);
+    short_reg<OPT, LPR, VPL>(a, warp, n_warps, reinterpret_cast<uint32_t*>(s_dyn) + (threadIdx.x >> 5) * kBagStage);
   }
+  trace_end(kTrReduce);
 }
 
 // Long segments: chunk partials + the last-arriver tree + optimizer, at full occupancy
@@ -604,34 +725,30 @@ __global__ void __launch_bounds__(256, VPL >= 4 ? 2 : (LPR == 32 ? 3 : 4)) k_lon
   pdl_launch_dependents();
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  trace_begin(kTrLong);
   long_phase<OPT, LPR, VPL>(a, warp, n_warps);
+  trace_end(kTrLong);
 }
 
-__global__ void k_unique_rows(const uint32_t* rows, const uint32_t* seg_start, const uint64_t* counts,
-                              uint32_t row_absent, uint32_t* out, uint64_t* count_out) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const uint64_t U = counts[1];
-  const bool has_absent = U > 0 && rows[seg_start[U - 1]] == row_absent;
-  const uint64_t n = has_absent ? U - 1 : U;
-  if (blockIdx.x == 0 && threadIdx.x == 0 && count_out) *count_out = n;
-  if (!out) return;
-  for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < n; u += uint64_t(gridDim.x) * blockDim.x)
-    out[u] = rows[seg_start[u]];
+// Rows updated by the last backward (short + long segments), unsorted; count -> *count_out.
+__global__ void k_unique_rows(const uint4* short_rec, const unsigned long long* short_alloc, const uint32_t* long_row,
+                              const uint32_t* n_long, uint32_t* out, uint64_t* count_out) {
+  const uint64_t S = *short_alloc >> 32, L = *n_long;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count_out = S + L;
+  for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < S + L; u += uint64_t(gridDim.x) * blockDim.x)
+    out[u] = u < S ? short_rec[u].x : long_row[u - S];
 }
 
 template <int OPT, int LPR, int VPL, bool TMA>
 int launch_backward_v(const BwdArgs& a, cudaStream_t st, bool pdl, size_t smem, int grid, int long_grid) {
   auto kern = k_reduce_short<OPT, LPR, VPL, TMA>;
   constexpr int block = TMA ? kRedWarps * 32 : 256;
-  if (TMA) {
-    static bool attr = false;
-    if (!attr) {
-      HPSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr = true;
-    }
+  static bool attr = false;
+  if (!attr) {
+    HPSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
   }
-  HPSG_CUDA(launch_k(pdl, kern, grid, block, smem, st, a));
+  HPSG_CUDA(launch_k(false, kern, grid, block, smem, st, a));  // first kernel after the join
   HPSG_CUDA(launch_k(pdl, k_long<OPT, LPR, VPL>, long_grid, 256, 0, st, a));
   return HPS_GPU_OK;
 }
@@ -644,26 +761,112 @@ int launch_backward(const BwdArgs& a, cudaStream_t st, bool pdl, bool tma, size_
     if (nvec > 32) return launch_backward_v<OPT, 32, 2, true>(a, st, pdl, smem, g, lg);
     return launch_backward_v<OPT, 32, 1, true>(a, st, pdl, smem, g, lg);
   }
-  if (nvec > 128) return launch_backward_v<OPT, 32, 8, false>(a, st, pdl, 0, g, lg);
-  if (nvec > 64) return launch_backward_v<OPT, 32, 4, false>(a, st, pdl, 0, g, lg);
-  if (nvec > 32) return launch_backward_v<OPT, 32, 2, false>(a, st, pdl, 0, g, lg);
-  if (nvec == 32) return launch_backward_v<OPT, 32, 1, false>(a, st, pdl, 0, g, lg);
-  if (nvec > 16) return launch_backward_v<OPT, 16, 2, false>(a, st, pdl, 0, g, lg);
-  if (nvec == 16) return launch_backward_v<OPT, 16, 1, false>(a, st, pdl, 0, g, lg);
-  if (nvec > 8) return launch_backward_v<OPT, 8, 2, false>(a, st, pdl, 0, g, lg);
-  if (nvec == 8) return launch_backward_v<OPT, 8, 1, false>(a, st, pdl, 0, g, lg);
-  if (nvec > 4) return launch_backward_v<OPT, 4, 2, false>(a, st, pdl, 0, g, lg);
-  if (nvec == 4) return launch_backward_v<OPT, 4, 1, false>(a, st, pdl, 0, g, lg);
-  if (nvec > 2) return launch_backward_v<OPT, 2, 2, false>(a, st, pdl, 0, g, lg);
-  if (nvec == 2) return launch_backward_v<OPT, 2, 1, false>(a, st, pdl, 0, g, lg);
-  return launch_backward_v<OPT, 1, 1, false>(a, st, pdl, 0, g, lg);
+  if (nvec > 128) return launch_backward_v<OPT, 32, 8, false>(a, st, pdl, smem, g, lg);
+  if (nvec > 64) return launch_backward_v<OPT, 32, 4, false>(a, st, pdl, smem, g, lg);
+  if (nvec > 32) return launch_backward_v<OPT, 32, 2, false>(a, st, pdl, smem, g, lg);
+  if (nvec == 32) return launch_backward_v<OPT, 32, 1, false>(a, st, pdl, smem, g, lg);
+  if (nvec > 16) return launch_backward_v<OPT, 16, 2, false>(a, st, pdl, smem, g, lg);
+  if (nvec == 16) return launch_backward_v<OPT, 16, 1, false>(a, st, pdl, smem, g, lg);
+  if (nvec > 8) return launch_backward_v<OPT, 8, 2, false>(a, st, pdl, smem, g, lg);
+  if (nvec == 8) return launch_backward_v<OPT, 8, 1, false>(a, st, pdl, smem, g, lg);
+  if (nvec > 4) return launch_backward_v<OPT, 4, 2, false>(a, st, pdl, smem, g, lg);
+  if (nvec == 4) return launch_backward_v<OPT, 4, 1, false>(a, st, pdl, smem, g, lg);
+  if (nvec > 2) return launch_backward_v<OPT, 2, 2, false>(a, st, pdl, smem, g, lg);
+  if (nvec == 2) return launch_backward_v<OPT, 2, 1, false>(a, st, pdl, smem, g, lg);
+  return launch_backward_v<OPT, 1, 1, false>(a, st, pdl, smem, g, lg);
+}
+
+BwdArgs base_args(hps_gpu_table t) {
+  const BwdZero zl = bwd_zero_layout(t->last_n_keys_host);
+  uint32_t* z = t->ws_zero;
+  BwdArgs a{};
+  a.counts = t->ws_counts;
+  a.occ_row = t->ws_rows_a;
+  a.occ_rank = t->ws_rank;
+  a.occ_bag = t->last_multi ? t->ws_occ_bag : nullptr;
+  a.occ_slot = t->ws_occ_slot;
+  a.slots = t->d_slots;
+  a.row_absent = t->row_absent;
+  a.short_alloc = reinterpret_cast<unsigned long long*>(z);
+  a.short_rec = t->ws_short_rec;
+  a.short_bag = t->ws_short_bag;
+  a.n_long = z + 2;
+  a.higher_total = z + 3;
+  a.long_occ = reinterpret_cast<unsigned long long*>(z + 4);
+  a.long_chunks = reinterpret_cast<unsigned long long*>(z + 6);
+  a.long_row = t->ws_long_row;
+  a.long_slot = t->ws_long_slot;
+  a.long_len = t->ws_long_len;
+  a.long_start = t->ws_long_start;
+  a.lkey = t->ws_lkey_a;
+  a.lval = t->ws_lval_a;
+  a.lbag = (bwd_long_passes(t->last_n_keys_host) & 1) ? t->ws_lval_b : t->ws_lval_a;
+  a.bag_len = (t->last_multi && t->last_combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
+  a.dim = t->dim;
+  a.long_base = t->ws_long_base;
+  a.task_long = t->ws_task_long;
+  a.partial = t->ws_partial;
+  a.partial2 = t->ws_partial2;
+  a.long_hbase = t->ws_long_hbase;
+  a.node_cnt = t->ws_node_cnt;
+  (void)zl;
+  return a;
 }
 
 }  // namespace
 
-extern "C" {
-
-}  // extern "C"
+// K4a-K4d on the table's side stream, right after the training probe (table.cu
+// record_and_fork): they need only the occurrence record, so they overlap the pooling.
+int hpsg::launch_dedup(hps_gpu_table t) {
+  cudaStream_t st = t->side;
+  const bool pdl = t->ctx->pdl;
+  const uint64_t nk = t->last_n_keys_host;
+  const BwdZero zl = bwd_zero_layout(nk);
+  uint32_t* z = t->ws_zero;
+  const BwdArgs a = base_args(t);
+  // K4a: segment allocation (first on this stream after the fork: a plain launch)
+  HPSG_CUDA(launch_k(false, k_seg_alloc, grid_for((nk + kAllocIPT - 1) / kAllocIPT, 256, kNumSMs * 8), 256, 0, st, a));
+  // K4b: placement (short segments) + ordered compaction of the long occurrences
+  {
+    const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(nk));
+    uint64_t* status = reinterpret_cast<uint64_t*>(z + zl.place);
+    HPSG_CUDA(launch_k(pdl, k_scan<PlaceOp>, static_cast<unsigned>(tiles), kScanBlock, 0, st, PlaceOp{a}, status,
+                       reinterpret_cast<uint32_t*>(status + tiles)));
+  }
+  // K4c: stable sort of the long list by segment id (canonical order within each segment)
+  {
+    const int passes = bwd_long_passes(nk);
+    const uint64_t stiles = sort_tiles(nk);
+    uint32_t* hist = z + zl.sort;
+    uint32_t* stick = hist + 4 * 256;
+    uint32_t* status = stick + 4;
+    const auto* d_n = reinterpret_cast<const uint64_t*>(a.long_occ);
+    HPSG_CUDA(launch_k(pdl, k_radix_hist, grid_for(nk, 256, kNumSMs * 2), 256, 0, st,
+                       static_cast<const uint32_t*>(t->ws_lkey_a), d_n, passes, hist));
+    const uint32_t* kin = t->ws_lkey_a;
+    const uint32_t* vin = t->ws_lval_a;
+    bool in_b = false;
+    for (int p = 0; p < passes; ++p) {
+      uint32_t* kout = in_b ? t->ws_lkey_a : t->ws_lkey_b;
+      uint32_t* vout = in_b ? t->ws_lval_a : t->ws_lval_b;
+      HPSG_CUDA(launch_k(pdl, k_radix_pass, static_cast<unsigned>(stiles), kSortBlock, 0, st, kin, vin, kout, vout, d_n,
+                         8 * p, static_cast<const uint32_t*>(hist + 256 * p), status + size_t(p) * stiles * 256,
+                         stick + p));
+      kin = kout;
+      vin = vout;
+      in_b = !in_b;
+    }
+  }
+  // K4d: long segment registration
+  {
+    const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(bwd_max_long(nk)));
+    uint64_t* status = reinterpret_cast<uint64_t*>(z + zl.lreg);
+    HPSG_CUDA(launch_k(pdl, k_scan<LongRegOp>, static_cast<unsigned>(tiles), kScanBlock, 0, st, LongRegOp{a}, status,
+                       reinterpret_cast<uint32_t*>(status + tiles)));
+  }
+  HPSG_CHECK_LAUNCH("backward dedup");
+  return HPS_GPU_OK;
+}
 
 namespace {
 // grads_out != nullptr: gradient-only mode (kOptGrad) — per-row sums into grads_out
@@ -678,61 +881,13 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   cudaStream_t st = t->ctx->stream;
   const bool pdl = t->ctx->pdl;
   const uint64_t nk = t->last_n_keys_host;
-  const int passes = (t->sort_bits + 7) / 8;
-  // zeroed region (table_internal.cuh bwd_zero_words)
-  uint32_t* z = t->ws_zero;
-  const size_t sort_words = bwd_sort_words(nk, passes);
-  const uint64_t tiles = scan_tiles(nk);
-  uint64_t* scan_status = reinterpret_cast<uint64_t*>(z + sort_words);
-  uint32_t* scan_ticket = reinterpret_cast<uint32_t*>(scan_status + tiles);
-  auto* long_packed = reinterpret_cast<unsigned long long*>(scan_status + tiles + 1);
-  // (the region was cleared by the training lookup: launch_lookup in table.cu)
-
-  // K4a: stable sort of (row, bag) by row. One key per bag: the bag IS the occurrence.
-  {
-    const uint64_t stiles = sort_tiles(nk);
-    uint32_t* hist = z;
-    uint32_t* stick = z + 4 * 256;
-    uint32_t* status = stick + 4;
-    HPSG_CUDA(launch_k(pdl, k_radix_hist, grid_for(nk, 256, kNumSMs * 2), 256, 0, st, t->ws_rows_a, t->ws_counts,
-                       passes, hist));
-    const uint32_t* kin = t->ws_rows_a;
-    const uint32_t* vin = t->last_multi ? t->ws_occ_bag : nullptr;
-    bool in_b = false;
-    for (int p = 0; p < passes; ++p) {
-      uint32_t* kout = in_b ? t->ws_rows_a : t->ws_rows_b;
-      uint32_t* vout = in_b ? t->ws_bags_a : t->ws_bags_b;
-      HPSG_CUDA(launch_k(pdl, k_radix_pass, static_cast<unsigned>(stiles), kSortBlock, 0, st, kin, vin, kout, vout,
-                         t->ws_counts, 8 * p, hist + 256 * p, status + size_t(p) * stiles * 256, stick + p));
-      kin = kout;
-      vin = vout;
-      in_b = !in_b;
-    }
-    t->sorted_in_b = in_b;
-    HPSG_CHECK_LAUNCH("radix sort");
+  // join the dedup forked by the training lookup
+  if (t->dedup_pending) {
+    HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
+    t->dedup_pending = false;
   }
-  const uint32_t* rows = t->sorted_in_b ? t->ws_rows_b : t->ws_rows_a;
-  const uint32_t* bags = t->sorted_in_b ? t->ws_bags_b : t->ws_bags_a;
-  // K4b: unique-row segments.
-  SegOp sop{rows, t->ws_seg_start, t->ws_seg_end, t->ws_counts};
-  HPSG_CUDA(launch_k(pdl, k_scan<SegOp>, static_cast<unsigned>(std::max<uint64_t>(1, tiles)), kScanBlock, 0, st, sop,
-                     scan_status, scan_ticket));
-  BwdArgs a{};
-  a.counts = t->ws_counts;
-  a.rows = rows;
-  a.bags = bags;
-  a.seg_start = t->ws_seg_start;
-  a.seg_end = t->ws_seg_end;
-  a.row_absent = t->row_absent;
-  a.bag_len = (t->last_multi && t->last_combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
+  BwdArgs a = base_args(t);
   a.dout = d_out;
-  a.dim = t->dim;
-  a.long_seg = t->ws_long_seg;
-  a.long_base = t->ws_long_base;
-  a.task_long = t->ws_task_long;
-  a.long_packed = long_packed;
-  a.partial = t->ws_partial;
-  a.partial2 = t->ws_partial2;
   const bool grad_only = grads_out != nullptr;
   a.W = grad_only ? grads_out : t->d_w;
   a.S0 = grad_only ? nullptr : t->d_s0;
@@ -740,21 +895,20 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   a.touched = touched_out;
   a.optimizer = t->optimizer;
   if (opt) a.opt = *opt;
-  a.long_hbase = t->ws_long_hbase;
-  a.node_cnt = t->ws_node_cnt;
-  a.higher_total = reinterpret_cast<uint32_t*>(scan_status + tiles + 3);
+
   const uint32_t nvec = t->dim / 4;
-  // K4c + K5: short segments (reduce fused with the optimizer), then the long segments'
+  // K4e + K5: short segments (reduce fused with the optimizer), then the long segments'
   // chunk partials + tree + optimizer.
   const bool tma = t->dim >= 128 && t->dim <= 256 && !t->no_tma;  // narrower rows: the register path wins
   size_t smem = 0;
   int grid = 0;
   if (tma) {
-    a.tma_rows = static_cast<uint32_t>(std::max<uint64_t>(40, (24 * 1024) / (t->dim * 4)));
-    smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float);
+    a.tma_rows = static_cast<uint32_t>(std::max<uint64_t>(40, (22 * 1024) / (t->dim * 4)));
+    smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float) + size_t(kRedWarps) * kBagStage * 4;
     grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * 4)));
   } else {
+    smem = size_t(8) * kBagStage * 4;
     grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
   }
   const int long_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
@@ -766,7 +920,9 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   else s = launch_backward<HPS_OPT_ADAM>(a, st, pdl, tma, smem, grid, long_grid, nvec);
   if (s) return s;
   HPSG_CHECK_LAUNCH("backward");
-  t->have_train = false;  // one backward per training lookup (its zeroed workspace is now used)
+  t->have_train = false;    // one backward per training lookup (its zeroed workspace is now used)
+  t->counts_dirty = false;  // the backward resets every counter it found
+  t->have_unique = true;
   return HPS_GPU_OK;
 }
 
@@ -833,12 +989,59 @@ int hps_gpu_apply_grads(hps_gpu_table t, const float* grads, const uint32_t* tou
   return HPS_GPU_OK;
 }
 
+// In-graph kernel timeline of the training step. mode 1: attach a zeroed
+// trace buffer; 2: copy the kTraceSlots x {start_ns, end_ns} records to trace_host
+// (2 * kTraceSlots u64; start = UINT64_MAX when the kernel did not run) and re-arm;
+// 0: detach. Synchronises the device.
+int hps_gpu_debug_trace(int mode, uint64_t* trace_host) {
+  static TraceRec* buf = nullptr;
+  auto arm = [&]() -> cudaError_t {
+    TraceRec init[kTraceSlots];
+    for (auto& r : init) r = TraceRec{~0ull, 0ull};
+    return cudaMemcpy(buf, init, sizeof(init), cudaMemcpyHostToDevice);
+  };
+  if (mode == 1) {
+    if (!buf) HPSG_CUDA(cudaMalloc(&buf, kTraceSlots * sizeof(TraceRec)));
+    HPSG_CUDA(arm());
+    HPSG_CUDA(trace_attach_tu(buf));
+    HPSG_CUDA(hpsg::trace_attach_table(buf));
+    return HPS_GPU_OK;
+  }
+  if (mode == 2) {
+    if (!buf || !trace_host) return HPS_GPU_E_INVALID_ARGUMENT;
+    HPSG_CUDA(cudaDeviceSynchronize());
+    HPSG_CUDA(cudaMemcpy(trace_host, buf, kTraceSlots * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+    HPSG_CUDA(arm());
+    return HPS_GPU_OK;
+  }
+  if (mode == 0) {
+    HPSG_CUDA(trace_attach_tu(nullptr));
+    HPSG_CUDA(hpsg::trace_attach_table(nullptr));
+    return HPS_GPU_OK;
+  }
+  return HPS_GPU_E_INVALID_ARGUMENT;
+}
+
 int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* unique_rows_out) {
   if (!t || !count_out) return HPS_GPU_E_INVALID_ARGUMENT;
-  const uint32_t* rows = t->sorted_in_b ? t->ws_rows_b : t->ws_rows_a;
-  HPSG_CUDA(launch_k(t->ctx->pdl, k_unique_rows, grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0,
-                     t->ctx->stream, rows, t->ws_seg_start, t->ws_counts, t->row_absent, unique_rows_out, count_out));
+  if (!t->have_unique) {
+    set_last_error("last_unique: no backward since the last training lookup");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  cudaStream_t st = t->ctx->stream;
+  const uint64_t nk = t->last_n_keys_host;
+  const BwdArgs a = base_args(t);
+  // unsorted rows into the (now free) long-list buffers, then an ascending radix sort
+  k_unique_rows<<<grid_for(nk, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_short_rec, a.short_alloc, t->ws_long_row,
+                                                               a.n_long, t->ws_lkey_a, count_out);
   HPSG_CHECK_LAUNCH("k_unique_rows");
+  if (!unique_rows_out) return HPS_GPU_OK;
+  cudaError_t err = cudaSuccess;
+  const bool in_b = radix_sort_pairs(st, t->ws_lkey_a, nullptr, t->ws_lval_a, t->ws_lkey_b, t->ws_lval_b, count_out,
+                                     nk, t->sort_bits, t->ws_zero, &err);
+  if (err != cudaSuccess) return cuda_status(err, "last_unique sort");
+  HPSG_CUDA(cudaMemcpyAsync(unique_rows_out, in_b ? t->ws_lkey_b : t->ws_lkey_a, nk * sizeof(uint32_t),
+                            cudaMemcpyDeviceToDevice, st));
   return HPS_GPU_OK;
 }
 

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <type_traits>
 
 #include <hps/hash.hpp>
 #include "hps_gpu.h"
@@ -210,6 +211,47 @@ inline int grid_for(uint64_t n, int block, int max_blocks = kNumSMs * 16) {
   if (g > static_cast<uint64_t>(max_blocks)) g = max_blocks;
   return static_cast<int>(g);
 }
+
+// ---- in-graph kernel timeline (hps_gpu_debug_trace) ----------------
+// When a trace buffer is attached, the step kernels stamp %globaltimer: the first CTA's
+// start (atomicMin) and every warp's exit (atomicMax), per kernel id. The pointer is a
+// per-translation-unit symbol (null = off: one predicated load per CTA).
+struct TraceRec {
+  unsigned long long start, end;
+};
+constexpr int kTraceSlots = 32;
+enum TraceId : int {
+  kTrProbe = 0, kTrPool = 1, kTrAlloc = 2, kTrPlace = 3, kTrHist = 4, kTrPass0 = 5, kTrLongReg = 9,
+  kTrReduce = 10, kTrLong = 11, kTrReset = 12
+};
+static __device__ TraceRec* g_trace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_begin(int id) {
+  if (id >= 0 && threadIdx.x == 0) {
+    TraceRec* t = g_trace;
+    if (t) atomicMin(&t[id].start, gtimer());
+  }
+}
+__device__ __forceinline__ void trace_end(int id) {
+  if (id >= 0 && (threadIdx.x & 31) == 0) {
+    TraceRec* t = g_trace;
+    if (t) atomicMax(&t[id].end, gtimer());
+  }
+}
+inline cudaError_t trace_attach_tu(TraceRec* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+// Op::kTrace when the scan op declares one, else -1 (untraced).
+template <class Op, class = void>
+struct TraceOf {
+  static constexpr int id = -1;
+};
+template <class Op>
+struct TraceOf<Op, std::void_t<decltype(Op::kTrace)>> {
+  static constexpr int id = Op::kTrace;
+};
 
 // ---- host-side error plumbing -------------------------------------------------
 void set_last_error(const std::string& msg);

@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(Op op, uint64_t* status, ui
   __shared__ uint32_t s_tile;
   pdl_wait();
   pdl_launch_dependents();
+  trace_begin(TraceOf<Op>::id);
   const uint64_t n = op.size();
   const uint64_t n_tiles = (n + kScanTile - 1) / kScanTile;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(Op op, uint64_t* status, ui
     run += c[k];
   }
   if (tile == n_tiles - 1 && threadIdx.x == kScanBlock - 1) op.total(s_prefix + agg);
+  trace_end(TraceOf<Op>::id);
 }
 
 inline uint64_t scan_tiles(uint64_t n_max) { return (n_max + kScanTile - 1) / kScanTile; }
@@ -167,6 +169,7 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* __res
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) (&s_h[0][0])[i] = 0;
   pdl_wait();
   pdl_launch_dependents();
+  trace_begin(kTrHist);
   __syncthreads();
   const uint64_t n = *d_n;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -178,6 +181,7 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* __res
     uint32_t v = (&s_h[0][0])[i];
     if (v) atomicAdd(&hist[i], v);
   }
+  trace_end(kTrHist);
 }
 
 // One digit pass. vals_in == nullptr: the value of item i is i (identity payload).
@@ -197,6 +201,7 @@ static __global__ void __launch_bounds__(kSortBlock) k_radix_pass(const uint32_t
 
   pdl_wait();
   pdl_launch_dependents();
+  trace_begin(kTrPass0 + shift / 8);
   const uint64_t n = *d_n;
   const uint64_t n_tiles = (n + kSortTile - 1) / kSortTile;
   if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
@@ -295,6 +300,7 @@ static __global__ void __launch_bounds__(kSortBlock) k_radix_pass(const uint32_t
     keys_out[g] = k;
     vals_out[g] = s_vals[i];
   }
+  trace_end(kTrPass0 + shift / 8);
 }
 
 inline uint64_t sort_tiles(uint64_t n_max) { return (n_max + kSortTile - 1) / kSortTile; }

@@ -268,21 +268,184 @@ struct LookupArgs {
   float* out;
   // training only: per-occurrence records consumed by backward.cu
   uint32_t* occ_row;   // global row of each occurrence (row_absent: key absent -> no gradient)
+  uint32_t* occ_rank;  // arrival rank of the occurrence among its row's occurrences
+  uint32_t* occ_slot;  // index slot of the occurrence's key (its aux word counts the row)
+  Slot* rw_slots;      // the index, writable (aux = kAuxNone at rest)
   uint32_t row_absent;
   uint32_t* occ_bag;   // multi-hot: bag of each occurrence
   uint32_t* bag_len;   // multi-hot mean: bag lengths
   uint64_t* d_n;       // number of key occurrences (device)
 };
 
-__device__ __forceinline__ void record_occurrence(const LookupArgs& a, uint64_t i, uint32_t local, uint32_t row) {
-  a.occ_row[i] = local == kRowEmpty ? a.row_absent : row;
+// K3a (training): probe every occurrence once and record it — row (row_absent when the
+// key is absent), arrival rank on the row's counter, bag (multi-hot) and bag length (mean).
+// The pooling kernels then read the recorded rows, and the backward's dedup
+// (backward.cu launch_dedup) runs on the side stream concurrently with the pooling.
+//
+// The row's counter is the aux word of the key's own index slot (kAuxNone + count, so the
+// arrival rank is old + 1): the probe has just brought that line into L2, so counting adds
+// no DRAM round trip. Counting is aggregated per CTA so that hot rows (tiny Criteo
+// tables, Zipf heads) do not serialise thousands of same-address atomics: a CTA owns 256
+// consecutive bags; each occurrence takes a local rank from a shared-memory hash of the
+// CTA's slots; then ONE global atomicAdd per distinct slot reserves the CTA's block of
+// ranks, and every occurrence adds its block base. (Slots a full hash cannot hold count
+// directly.)
+constexpr int kProbeBags = 256;      // bags per CTA tile (8 warps x 32)
+constexpr int kProbeHash = 4096;     // shared hash entries
+constexpr uint32_t kDirect = 0xffffffffu;
+
+// Probe returning the key's global index slot (kDirect when absent) and local row.
+__device__ __forceinline__ uint32_t probe_slot(const Slot* __restrict__ slots, const TableDev& td, uint64_t key,
+                                               uint32_t* local) {
+  uint64_t idx = hps::key_hash(key) & td.slot_mask;
+  const Slot* base = slots + td.slot_base;
+  for (uint64_t p = 0; p <= td.slot_mask; ++p) {
+    const Slot s = load_slot(base + idx);
+    if (s.row == kRowEmpty) break;
+    if (s.key == key) {
+      *local = s.row;
+      return static_cast<uint32_t>(td.slot_base + idx);
+    }
+    idx = (idx + 1) & td.slot_mask;
+  }
+  *local = kRowEmpty;
+  return kDirect;
 }
 
-// One-key-per-bag path. A warp owns 32 consecutive bags: every lane hashes and probes
-// one key (32 independent index loads in flight) and, when training, registers the
-// occurrence in the dedup table; then groups of LPR lanes stream the rows with 128-bit
-// loads (VPL float4 per lane, 8 rows in flight per group) and write the bags coalesced.
-template <int LPR, int VPL>
+__device__ __forceinline__ uint32_t smem_hash_slot(uint32_t* s_row, uint32_t row) {
+  uint32_t h = (row * 0x9e3779b1u) >> (32 - 12);
+  for (int probe = 0; probe < 64; ++probe) {
+    const uint32_t cur = s_row[h];
+    if (cur == row) return h;
+    if (cur == kDirect) {
+      const uint32_t old = atomicCAS(&s_row[h], kDirect, row);
+      if (old == kDirect || old == row) return h;
+    }
+    h = (h + 1) & (kProbeHash - 1);
+  }
+  return kDirect;
+}
+
+template <bool MULTI>
+__global__ void __launch_bounds__(256) k_probe(LookupArgs a, uint32_t* __restrict__ tmp) {
+  __shared__ uint32_t s_row[kProbeHash];  // global slot index of the entry
+  __shared__ uint32_t s_cnt[kProbeHash];  // local counts, then the CTA's base rank per slot
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  const uint64_t n_bags = a.n_bags;
+  trace_begin(kTrProbe);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_n = MULTI ? a.offsets[n_bags] : n_bags;
+  for (uint64_t t0 = uint64_t(blockIdx.x) * kProbeBags; t0 < n_bags; t0 += uint64_t(gridDim.x) * kProbeBags) {
+    for (int e = threadIdx.x; e < kProbeHash; e += 256) {
+      s_row[e] = kDirect;
+      s_cnt[e] = 0u;
+    }
+    __syncthreads();
+    // phase A: warp w records bags [b0, b0 + nb)
+    const uint64_t b0 = t0 + uint64_t(w) * 32;
+    if (b0 < n_bags) {
+      const uint64_t b = b0 + lane;
+      const uint32_t nb = static_cast<uint32_t>(min(uint64_t(32), n_bags - b0));
+      uint32_t lo = static_cast<uint32_t>(b), hi_all = static_cast<uint32_t>(b0 + nb);
+      if constexpr (MULTI) {
+        lo = a.offsets[b < n_bags ? b : n_bags];
+        hi_all = __shfl_sync(0xffffffffu, a.offsets[b0 + nb], 0);
+        if (b < n_bags && a.bag_len) a.bag_len[b] = a.offsets[b + 1] - lo;
+      }
+      const uint32_t lo0 = __shfl_sync(0xffffffffu, lo, 0);
+      for (uint32_t p0 = lo0; p0 < hi_all; p0 += 32) {
+        const uint32_t p = p0 + lane;
+        uint32_t k = lane;  // bag of occurrence p within the warp's 32 (one-hot: the lane)
+        if constexpr (MULTI) {
+          k = 0;
+#pragma unroll
+          for (uint32_t step = 16; step > 0; step >>= 1) {
+            const uint32_t cand = k + step;
+            const uint32_t lc = __shfl_sync(0xffffffffu, lo, cand & 31);
+            if (cand < nb && lc <= p) k = cand;
+          }
+        }
+        if (p < hi_all) {
+          const uint64_t bag = b0 + k;
+          const uint32_t table = a.key_tables ? a.key_tables[p] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
+          const TableDev td = a.tables[table];
+          uint32_t local;
+          const uint32_t sidx = probe_slot(a.slots, td, a.keys[p], &local);
+          if (local == kRowEmpty) {
+            a.occ_row[p] = a.row_absent;
+          } else {
+            a.occ_row[p] = static_cast<uint32_t>(td.row_base + local);
+            a.occ_slot[p] = sidx;
+            const uint32_t h = smem_hash_slot(s_row, sidx);
+            if (h != kDirect) {
+              a.occ_rank[p] = atomicAdd(&s_cnt[h], 1u);
+            } else {
+              a.occ_rank[p] = atomicAdd(&a.rw_slots[sidx].aux, 1u) + 1u;
+            }
+            tmp[p] = h;
+          }
+          if constexpr (MULTI) a.occ_bag[p] = static_cast<uint32_t>(bag);
+        }
+      }
+    }
+    __syncthreads();
+    // phase B: one global reservation per distinct row of the tile (all of a thread's
+    // atomics issued before any result is consumed)
+    {
+      constexpr int kPer = kProbeHash / 256;
+      uint32_t res[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const uint32_t e = threadIdx.x + 256u * k;
+        const uint32_t r = s_row[e];
+        res[k] = r != kDirect ? atomicAdd(&a.rw_slots[r].aux, s_cnt[e]) + 1u : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) s_cnt[threadIdx.x + 256u * k] = res[k];
+    }
+    __syncthreads();
+    // phase C: ranks += the CTA's base for the row (the tile's occurrences are contiguous)
+    const uint64_t tb_end = min(t0 + kProbeBags, n_bags);
+    const uint32_t plo = MULTI ? a.offsets[t0] : static_cast<uint32_t>(t0);
+    const uint32_t phi = MULTI ? a.offsets[tb_end] : static_cast<uint32_t>(tb_end);
+    for (uint32_t p = plo + threadIdx.x; p < phi; p += 256) {
+      if (a.occ_row[p] == a.row_absent) continue;
+      const uint32_t h = tmp[p];
+      if (h != kDirect) a.occ_rank[p] += s_cnt[h];
+    }
+    __syncthreads();
+  }
+  trace_end(kTrProbe);
+}
+
+// Counters left by a training record that no backward consumed: back to kAuxNone.
+__global__ void k_reset_counts(const uint32_t* __restrict__ occ_row, const uint32_t* __restrict__ occ_slot,
+                               const uint64_t* d_n, uint32_t row_absent, Slot* slots) {
+  trace_begin(kTrReset);
+  const uint64_t n = *d_n;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    if (occ_row[i] != row_absent) slots[occ_slot[i]].aux = kAuxNone;
+  trace_end(kTrReset);
+}
+
+// Row of occurrence i: ROWS — recorded by the training probe (k_probe_*); otherwise hash
+// and probe the key here (inference: one fused pass).
+template <bool ROWS>
+__device__ __forceinline__ uint32_t occurrence_row(const LookupArgs& a, uint64_t i, uint32_t table) {
+  if constexpr (ROWS) {
+    const uint32_t r = a.occ_row[i];
+    return r == a.row_absent ? kRowEmpty : r;
+  } else {
+    const TableDev td = a.tables[table];
+    const uint32_t local = probe_find(a.slots, td, a.keys[i]);
+    return local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
+  }
+}
+
+// One-key-per-bag path. A warp owns 32 consecutive bags: every lane resolves one key's
+// row (32 independent index loads in flight); then groups of LPR lanes stream the rows
+// with 128-bit loads (VPL float4 per lane, 8 rows in flight per group) and write the bags
+// coalesced.
+template <int LPR, int VPL, bool ROWS>
 __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
   constexpr int G = 32 / LPR;  // rows handled side by side by one warp
   constexpr int kBatch = (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) > 0 ? (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) : 1;
@@ -291,17 +454,12 @@ __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
   const uint32_t nvec = a.dim / 4;
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  if (a.d_n && warp == 0 && lane == 0) *a.d_n = a.n_bags;
   for (uint64_t t0 = warp * 32; t0 < a.n_bags; t0 += n_warps * 32) {
     const uint64_t bag = t0 + lane;
     uint32_t row = kRowEmpty, table = 0;
     if (bag < a.n_bags) {
-      const uint64_t key = a.keys[bag];
       table = a.key_tables ? a.key_tables[bag] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
-      const TableDev td = a.tables[table];
-      const uint32_t local = probe_find(a.slots, td, key);
-      row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
-      if (a.occ_row) record_occurrence(a, bag, local, row);
+      row = occurrence_row<ROWS>(a, bag, table);
     }
     for (int m0 = 0; m0 < LPR; m0 += kBatch) {
       float4 x[kBatch][VPL];
@@ -344,6 +502,7 @@ __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
 // No registers hold row data, so every warp keeps 32 rows (16 KB at dim 128) outstanding.
 constexpr int kTmaWarps = 4;
 
+template <bool ROWS>
 __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a) {
   extern __shared__ __align__(128) float s_rows[];  // [kTmaWarps][32][dim]
   __shared__ __align__(8) uint64_t s_bar[kTmaWarps];
@@ -358,19 +517,15 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a
   uint32_t phase = 0;
   const uint64_t warp = uint64_t(blockIdx.x) * kTmaWarps + w;
   const uint64_t n_warps = uint64_t(gridDim.x) * kTmaWarps;
-  if (a.d_n && warp == 0 && lane == 0) *a.d_n = a.n_bags;
+  trace_begin(ROWS ? kTrPool : -1);
   for (uint64_t t0 = warp * 32; t0 < a.n_bags; t0 += n_warps * 32) {
     const uint64_t bag = t0 + lane;
     const uint32_t nb = static_cast<uint32_t>(min(uint64_t(32), a.n_bags - t0));
     const float* src = nullptr;
     if (bag < a.n_bags) {
-      const uint64_t key = a.keys[bag];
       const uint32_t table = a.key_tables ? a.key_tables[bag] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
-      const TableDev td = a.tables[table];
-      const uint32_t local = probe_find(a.slots, td, key);
-      const uint32_t row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
-      if (a.occ_row) record_occurrence(a, bag, local, row);
-      src = local == kRowEmpty ? a.defaults + uint64_t(table) * D : a.W + uint64_t(row) * D;
+      const uint32_t row = occurrence_row<ROWS>(a, bag, table);
+      src = row == kRowEmpty ? a.defaults + uint64_t(table) * D : a.W + uint64_t(row) * D;
     }
     if (lane == 0) bulk_wait_read_all();  // the previous tile's store has finished reading smem
     __syncwarp();
@@ -389,6 +544,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a
     }
   }
   if (lane == 0) bulk_wait_all();
+  trace_end(ROWS ? kTrPool : -1);
 }
 
 // Orchestrator read-through (one table): hits come from the cache's
@@ -436,9 +592,9 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
   }
 }
 
-// Multi-hot path: a group of LPR lanes owns one bag at a time; the group probes LPR
+// Multi-hot path: a group of LPR lanes owns one bag at a time; the group resolves LPR
 // keys of the bag in parallel, then accumulates the rows in bag order (4 in flight).
-template <int LPR, int VPL>
+template <int LPR, int VPL, bool ROWS>
 __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id();
@@ -447,25 +603,16 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
   const uint32_t nvec = a.dim / 4;
   const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
   const uint64_t n_groups = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
-  if (a.d_n && gid == 0 && gl == 0) *a.d_n = a.offsets[a.n_bags];
+  trace_begin(ROWS ? kTrPool : -1);
   for (uint64_t bag = gid; bag < a.n_bags; bag += n_groups) {
     const uint32_t lo = a.offsets[bag], hi = a.offsets[bag + 1];
     const uint32_t table = a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
-    const TableDev td = a.tables[table];
     float4 acc[VPL];
 #pragma unroll
     for (int k = 0; k < VPL; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     for (uint32_t c = lo; c < hi; c += LPR) {
       const uint32_t i = c + gl;
-      uint32_t row = kRowEmpty;
-      if (i < hi) {
-        const uint32_t local = probe_find(a.slots, td, a.keys[i]);
-        row = local == kRowEmpty ? kRowEmpty : static_cast<uint32_t>(td.row_base + local);
-        if (a.occ_row) {
-          record_occurrence(a, i, local, row);
-          a.occ_bag[i] = static_cast<uint32_t>(bag);
-        }
-      }
+      const uint32_t row = i < hi ? occurrence_row<ROWS>(a, i, table) : kRowEmpty;
       const uint32_t cnt = min(uint32_t(LPR), hi - c);
       for (uint32_t m0 = 0; m0 < cnt; m0 += 4) {
         float4 x[4][VPL];
@@ -491,7 +638,6 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
       }
     }
     const uint32_t len = hi - lo;
-    if (a.bag_len && gl == 0) a.bag_len[bag] = len;
     float4* o = reinterpret_cast<float4*>(a.out + bag * a.dim);
     const float fl = static_cast<float>(len);
 #pragma unroll
@@ -500,6 +646,7 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
       if (v < nvec) o[v] = (a.mean && len > 0) ? f4_div(acc[k], fl) : acc[k];
     }
   }
+  trace_end(ROWS ? kTrPool : -1);
 }
 
 int bits_for(uint64_t v) {
@@ -529,6 +676,8 @@ int dalloc(T** p, size_t count) {
 
 }  // namespace
 
+cudaError_t hpsg::trace_attach_table(TraceRec* p) { return trace_attach_tu(p); }
+
 namespace {
 
 int check_tbl(hps_gpu_table t) {
@@ -541,21 +690,21 @@ int check_tbl(hps_gpu_table t) {
 
 // (lanes per row, float4 per lane) for a row of nvec float4: LPR = largest power of two
 // <= min(32, nvec); VPL = ceil(nvec / LPR) (<= 8, so dim <= 1024).
-#define HPSG_DISPATCH_ROW(KERNEL, GRIDF, ...)                                    \
-  do {                                                                           \
-    if (nvec > 128) KERNEL<32, 8><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);       \
-    else if (nvec > 64) KERNEL<32, 4><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);   \
-    else if (nvec > 32) KERNEL<32, 2><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);   \
-    else if (nvec == 32) KERNEL<32, 1><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);  \
-    else if (nvec > 16) KERNEL<16, 2><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);   \
-    else if (nvec == 16) KERNEL<16, 1><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);  \
-    else if (nvec > 8) KERNEL<8, 2><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);      \
-    else if (nvec == 8) KERNEL<8, 1><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);     \
-    else if (nvec > 4) KERNEL<4, 2><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);      \
-    else if (nvec == 4) KERNEL<4, 1><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);     \
-    else if (nvec > 2) KERNEL<2, 2><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);      \
-    else if (nvec == 2) KERNEL<2, 1><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);     \
-    else KERNEL<1, 1><<<GRIDF(1), 256, 0, st>>>(__VA_ARGS__);                    \
+#define HPSG_DISPATCH_ROW(KERNEL, R, GRIDF, ...)                                    \
+  do {                                                                              \
+    if (nvec > 128) KERNEL<32, 8, R><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);       \
+    else if (nvec > 64) KERNEL<32, 4, R><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec > 32) KERNEL<32, 2, R><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec == 32) KERNEL<32, 1, R><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);  \
+    else if (nvec > 16) KERNEL<16, 2, R><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec == 16) KERNEL<16, 1, R><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);  \
+    else if (nvec > 8) KERNEL<8, 2, R><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);      \
+    else if (nvec == 8) KERNEL<8, 1, R><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);     \
+    else if (nvec > 4) KERNEL<4, 2, R><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);      \
+    else if (nvec == 4) KERNEL<4, 1, R><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);     \
+    else if (nvec > 2) KERNEL<2, 2, R><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);      \
+    else if (nvec == 2) KERNEL<2, 1, R><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);     \
+    else KERNEL<1, 1, R><<<GRIDF(1), 256, 0, st>>>(__VA_ARGS__);                    \
   } while (0)
 
 // nk: key occurrences of this call (host bound). A training lookup also clears the
@@ -565,27 +714,6 @@ int check_tbl(hps_gpu_table t) {
 // Hybrid sparse embedding:
 // hot keys live in a replicated table group (this table), cold keys on their owner.
 // ---------------------------------------------------------------------------------
-// Probe every occurrence against the hot index and record the training state exactly as
-// a training lookup does (occ_row = hot row or row_absent, occ_bag, bag_len, N), without
-// pooling. Bag-parallel: thread per bag.
-__global__ void k_hybrid_probe(LookupArgs a) {
-  pdl_wait();
-  const uint64_t n_bags = a.n_bags;
-  for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < n_bags;
-       b += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t table = a.slot_table[b % a.n_slots];
-    const TableDev td = a.tables[table];
-    const uint64_t lo = a.offsets ? a.offsets[b] : b, hi = a.offsets ? a.offsets[b + 1] : b + 1;
-    for (uint64_t i = lo; i < hi; ++i) {
-      const uint32_t local = probe_find(a.slots, td, a.keys[i]);
-      record_occurrence(a, i, local, static_cast<uint32_t>(td.row_base + local));
-      if (a.occ_bag) a.occ_bag[i] = static_cast<uint32_t>(b);
-    }
-    if (a.bag_len) a.bag_len[b] = static_cast<uint32_t>(hi - lo);
-    if (b == 0) *a.d_n = a.offsets ? a.offsets[n_bags] : n_bags;
-  }
-}
-
 // Cold occurrences (absent from the hot index), compacted in occurrence order.
 struct ColdOp {
   const uint32_t* occ_row;
@@ -640,35 +768,88 @@ __global__ void __launch_bounds__(256) k_hybrid_pool(const uint32_t* __restrict_
   }
 }
 
-int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, uint64_t nk) {
-  const cudaStream_t st = t->ctx->stream;
-  if (a.occ_row) {
-    const int passes = (t->sort_bits + 7) / 8;
-    HPSG_CUDA(cudaMemsetAsync(t->ws_zero, 0, bwd_zero_words(nk, passes) * sizeof(uint32_t), st));
+// A training record is about to overwrite ws_rows_a: counters of a previous record that no
+// backward consumed go back to zero first (they are still described by ws_rows_a, once
+// that record's dedup on the side stream is done).
+int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk) {
+  cudaStream_t st = t->ctx->stream;
+  if (t->dedup_pending) {
+    HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
+    t->dedup_pending = false;
   }
+  if (t->counts_dirty) {
+    k_reset_counts<<<grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0, st>>>(
+        t->ws_rows_a, t->ws_occ_slot, t->ws_counts, t->row_absent, t->d_slots);
+    HPSG_CHECK_LAUNCH("k_reset_counts");
+  }
+  HPSG_CUDA(cudaMemsetAsync(t->ws_zero, 0, bwd_zero_layout(nk).total * sizeof(uint32_t), st));
+  a.occ_row = t->ws_rows_a;
+  a.occ_rank = t->ws_rank;
+  a.occ_slot = t->ws_occ_slot;
+  a.rw_slots = t->d_slots;
+  a.row_absent = t->row_absent;
+  a.d_n = t->ws_counts;
+  t->counts_dirty = true;
+  t->have_unique = false;
+  return HPS_GPU_OK;
+}
+
+// Training record: probe + record every occurrence, then fork the backward's dedup onto
+// the table's side stream (it needs only the record) — the pooling that follows on the
+// main stream and the dedup run concurrently; backward_update joins them.
+int record_and_fork(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk) {
+  cudaStream_t st = t->ctx->stream;
+  const int grid = static_cast<int>(
+      std::max<uint64_t>(1, std::min<uint64_t>((a.n_bags + kProbeBags - 1) / kProbeBags, kNumSMs * 16)));
+  if (multi) k_probe<true><<<grid, 256, 0, st>>>(a, t->ws_probe_tmp);
+  else k_probe<false><<<grid, 256, 0, st>>>(a, t->ws_probe_tmp);
+  HPSG_CHECK_LAUNCH("probe");
+  t->last_multi = multi;
+  t->last_combiner = mean ? HPS_COMBINER_MEAN : HPS_COMBINER_SUM;
+  t->last_n_keys_host = nk;
+  HPSG_CUDA(cudaEventRecord(t->ev_fork, st));
+  HPSG_CUDA(cudaStreamWaitEvent(t->side, t->ev_fork, 0));
+  if (int s = launch_dedup(t)) return s;
+  HPSG_CUDA(cudaEventRecord(t->ev_join, t->side));
+  t->dedup_pending = true;
+  return HPS_GPU_OK;
+}
+
+// Pooled lookup. ROWS (training): rows come from the record (record_and_fork ran first);
+// otherwise hash + probe + gather + pool in one pass.
+int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
+  const cudaStream_t st = t->ctx->stream;
   const uint32_t nvec = t->dim / 4;
   const bool tma_ok = t->dim <= 256 && (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0 && !t->no_tma;
   if (!multi && tma_ok) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_lookup_1hot_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaWarps * 32 * 256 * 4);
+      cudaFuncSetAttribute(k_lookup_1hot_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kTmaWarps * 32 * 256 * 4);
+      cudaFuncSetAttribute(k_lookup_1hot_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kTmaWarps * 32 * 256 * 4);
       attr = true;
     }
     const size_t smem = size_t(kTmaWarps) * 32 * t->dim * sizeof(float);
     const uint64_t tiles = (uint64_t(a.n_bags) + 31) / 32;
-    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + kTmaWarps - 1) / kTmaWarps,
-                                                                               uint64_t(kNumSMs) * 8)));
-    k_lookup_1hot_tma<<<grid, kTmaWarps * 32, smem, st>>>(a);
+    // training: a resident grid (2 CTAs per SM) leaves room for the dedup kernels beside it
+    const uint64_t max_grid = rows ? uint64_t(kNumSMs) * 2 : uint64_t(kNumSMs) * 8;
+    const int grid =
+        static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + kTmaWarps - 1) / kTmaWarps, max_grid)));
+    if (rows) k_lookup_1hot_tma<true><<<grid, kTmaWarps * 32, smem, st>>>(a);
+    else k_lookup_1hot_tma<false><<<grid, kTmaWarps * 32, smem, st>>>(a);
   } else if (!multi) {
-    auto grid1 = [&](int) { return grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * 64); };
-    HPSG_DISPATCH_ROW(k_lookup_1hot, grid1, a);
+    auto grid1 = [&](int) { return grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * (rows ? 4 : 64)); };
+    if (rows) HPSG_DISPATCH_ROW(k_lookup_1hot, true, grid1, a);
+    else HPSG_DISPATCH_ROW(k_lookup_1hot, false, grid1, a);
   } else {
     auto gridm = [&](int lpr) {
       const uint64_t groups_per_block = 8 * (32 / lpr);
       const uint64_t g = (a.n_bags + groups_per_block - 1) / groups_per_block;
-      return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, kNumSMs * 64)));
+      return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(g, kNumSMs * (rows ? 4 : 64))));
     };
-    HPSG_DISPATCH_ROW(k_lookup_multi, gridm, a);
+    if (rows) HPSG_DISPATCH_ROW(k_lookup_multi, true, gridm, a);
+    else HPSG_DISPATCH_ROW(k_lookup_multi, false, gridm, a);
   }
   HPSG_CHECK_LAUNCH("lookup");
   return HPS_GPU_OK;
@@ -738,7 +919,8 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->sort_bits = std::max(1, bits_for(rows));
   t->max_long = bwd_max_long(N);
   t->max_chunks = bwd_max_chunks(N);
-  t->zero_words = bwd_zero_words(N, (t->sort_bits + 7) / 8);
+  // (also the scratch of last_unique's row sort)
+  t->zero_words = std::max(bwd_zero_layout(N).total, sort_ws_words(N, (t->sort_bits + 7) / 8));
   int st = HPS_GPU_OK;
   auto A = [&](int s) {
     if (s && !st) st = s;
@@ -753,14 +935,21 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->d_defaults, uint64_t(t->n_tables) * D));
   A(dalloc(&t->d_slot_table, t->n_slots));
   A(dalloc(&t->ws_rows_a, N));
-  A(dalloc(&t->ws_rows_b, N));
-  A(dalloc(&t->ws_bags_a, N));
-  A(dalloc(&t->ws_bags_b, N));
+  A(dalloc(&t->ws_rank, N));
+  A(dalloc(&t->ws_probe_tmp, N));
+  A(dalloc(&t->ws_occ_slot, N));
+  A(dalloc(&t->ws_long_slot, t->max_long));
   A(dalloc(&t->ws_occ_bag, N));
   A(dalloc(&t->ws_bag_len, B));
-  A(dalloc(&t->ws_seg_start, N + 1));
-  A(dalloc(&t->ws_seg_end, N + 1));
-  A(dalloc(&t->ws_long_seg, t->max_long));
+  A(dalloc(&t->ws_short_rec, N));
+  A(dalloc(&t->ws_short_bag, N));
+  A(dalloc(&t->ws_long_row, t->max_long));
+  A(dalloc(&t->ws_long_len, t->max_long));
+  A(dalloc(&t->ws_long_start, t->max_long));
+  A(dalloc(&t->ws_lkey_a, N));
+  A(dalloc(&t->ws_lval_a, N));
+  A(dalloc(&t->ws_lkey_b, N));
+  A(dalloc(&t->ws_lval_b, N));
   A(dalloc(&t->ws_long_base, t->max_long));
   A(dalloc(&t->ws_task_long, t->max_chunks));
   A(dalloc(&t->ws_partial2, bwd_max_nodes(N) * D));
@@ -787,6 +976,9 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   HPSG_CUDA(cudaMemsetAsync(t->d_nrows, 0, t->n_tables * sizeof(uint64_t), s));
   HPSG_CUDA(cudaMemsetAsync(t->d_defaults, 0, uint64_t(t->n_tables) * D * sizeof(float), s));
   HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, 8 * sizeof(uint64_t), s));
+  HPSG_CUDA(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
+  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
+  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
   HPSG_CUDA(cudaMemsetAsync(t->ws_node_cnt, 0, bwd_max_nodes(N) * sizeof(uint32_t), s));
   k_fill_slots_empty<<<grid_for(slots, 256, kNumSMs * 32), 256, 0, s>>>(t->d_slots, slots);
   HPSG_CHECK_LAUNCH("k_fill_slots_empty");
@@ -799,13 +991,18 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
   void* ptrs[] = {t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
-                  t->ws_rows_b,   t->ws_bags_a,    t->ws_bags_b,    t->ws_occ_bag,    t->ws_bag_len,
-                  t->ws_seg_start, t->ws_seg_end,  t->ws_long_seg,  t->ws_long_base,  t->ws_task_long,
+                  t->ws_probe_tmp, t->ws_occ_slot, t->ws_long_slot, t->ws_rank,      t->ws_short_rec, t->ws_short_bag,  t->ws_occ_bag,
+                  t->ws_bag_len,  t->ws_long_row,  t->ws_long_len,  t->ws_long_start, t->ws_lkey_a,
+                  t->ws_lval_a,   t->ws_lkey_b,    t->ws_lval_b,    t->ws_long_base,  t->ws_task_long,
                   t->ws_partial2, t->ws_long_hbase, t->ws_node_cnt,
                   t->ws_partial,  t->ws_counts,    t->ws_zero,      t->ws_abort,      t->ws_keys_stage,
                   t->ws_offsets_stage, t->ws_ins_slot, t->ws_ins_pos, t->ws_ins_flag, t->ws_ins_scan};
+  if (t->side) cudaStreamSynchronize(t->side);
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (t->ev_fork) cudaEventDestroy(t->ev_fork);
+  if (t->ev_join) cudaEventDestroy(t->ev_join);
+  if (t->side) cudaStreamDestroy(t->side);
   delete t;
   return HPS_GPU_OK;
 }
@@ -972,17 +1169,13 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   a.mean = combiner == HPS_COMBINER_MEAN;
   a.out = out;
   if (train) {
-    a.occ_row = t->ws_rows_a;
-    a.row_absent = t->row_absent;
+    if (int s = begin_training_record(t, a, n_keys_host)) return s;
     a.occ_bag = multi ? t->ws_occ_bag : nullptr;
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
-    a.d_n = t->ws_counts;
+    if (int s = record_and_fork(t, a, multi, a.mean, n_keys_host)) return s;
   }
-  if (int s = launch_lookup(t, a, multi, n_keys_host)) return s;
+  if (int s = launch_lookup(t, a, multi, train)) return s;
   t->have_train = train;
-  t->last_multi = multi;
-  t->last_combiner = combiner;
-  t->last_n_keys_host = n_keys_host;
   return HPS_GPU_OK;
 }
 
@@ -1026,9 +1219,8 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
   if (!keys || !cold_pos_out || !cold_keys_out || !cold_bags_out || !cold_count_out) return HPS_GPU_E_INVALID_ARGUMENT;
   if (combiner != HPS_COMBINER_SUM && combiner != HPS_COMBINER_MEAN) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = t->ctx->stream;
-  const int passes = (t->sort_bits + 7) / 8;
-  HPSG_CUDA(cudaMemsetAsync(t->ws_zero, 0, bwd_zero_words(n_keys_host, passes) * sizeof(uint32_t), st));
   LookupArgs a{};
+  if (int s = begin_training_record(t, a, n_keys_host)) return s;
   a.keys = keys;
   a.offsets = offsets;
   a.n_bags = static_cast<uint32_t>(n_bags);
@@ -1036,13 +1228,9 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
   a.slot_table = t->d_slot_table;
   a.tables = t->d_tables;
   a.slots = t->d_slots;
-  a.occ_row = t->ws_rows_a;
-  a.row_absent = t->row_absent;
   a.occ_bag = multi ? t->ws_occ_bag : nullptr;
   a.bag_len = (multi && combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
-  a.d_n = t->ws_counts;
-  if (n_bags) k_hybrid_probe<<<grid_for(n_bags, 256, kNumSMs * 16), 256, 0, st>>>(a);
-  else HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, sizeof(uint64_t), st));
+  if (int s = record_and_fork(t, a, multi, combiner == HPS_COMBINER_MEAN, n_keys_host)) return s;
   // compaction scan: its look-back words live past the backward's zeroed region
   const uint64_t tiles = scan_tiles(std::max<uint64_t>(n_keys_host, 1));
   HPSG_CUDA(cudaMemsetAsync(t->ws_ins_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
@@ -1052,9 +1240,6 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
                                                                       reinterpret_cast<uint32_t*>(t->ws_ins_scan + tiles));
   HPSG_CHECK_LAUNCH("hybrid_probe");
   t->have_train = true;
-  t->last_multi = multi;
-  t->last_combiner = combiner;
-  t->last_n_keys_host = n_keys_host;
   return HPS_GPU_OK;
 }
 
@@ -1114,15 +1299,11 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
   a.dim = t->dim;
   a.out = rows_out;
   if (train) {
-    a.occ_row = t->ws_rows_a;
-    a.row_absent = t->row_absent;
-    a.d_n = t->ws_counts;
+    if (int s = begin_training_record(t, a, n)) return s;
+    if (int s = record_and_fork(t, a, false, false, n)) return s;
   }
-  if (int s = launch_lookup(t, a, false, n)) return s;
+  if (int s = launch_lookup(t, a, false, train)) return s;
   t->have_train = train;
-  t->last_multi = false;
-  t->last_combiner = HPS_COMBINER_SUM;
-  t->last_n_keys_host = n;
   return HPS_GPU_OK;
 }
 

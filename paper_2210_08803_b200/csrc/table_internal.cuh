@@ -11,20 +11,44 @@ namespace hpsg {
 
 constexpr uint32_t kChunk = 32;  // blocked reduction width
 
-// Zeroed-per-backward region: [radix sort words][pad][segment-scan status (u64) x tiles]
-// [scan ticket][long packed counter][piece counter][item ticket][spare x2] — one memset.
-inline size_t bwd_sort_words(uint64_t max_keys, int passes) { return (sort_ws_words(max_keys, passes) + 1) & ~size_t(1); }
-inline size_t bwd_zero_words(uint64_t max_keys, int passes) {
-  return bwd_sort_words(max_keys, passes) + 2 * (scan_tiles(max_keys) + 6);
+// Zeroed-per-training-lookup region (u32 words), DESIGN.md §3 K4:
+//   [0,2)  u64 short-segment allocator: (segments << 32) | occurrences
+//   [2]    long segments   [3] tree nodes allocated above level 1
+//   [4,6)  u64 long occurrences (place-scan total)   [6,8) u64 level-1 chunks of long segments
+//   then   place-scan look-back (u64 x tiles + ticket), long-registration scan look-back,
+//          and the radix-sort words of the long-occurrence sort.
+constexpr uint32_t kLongFlag = 0x80000000u;  // slot aux after allocation: long segment id
+inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
+inline int bwd_long_passes(uint64_t max_keys) {
+  const uint64_t m = bwd_max_long(max_keys);
+  int b = 0;
+  while (b < 32 && (m >> b)) ++b;
+  return b <= 8 ? 1 : (b + 7) / 8;
+}
+struct BwdZero {
+  size_t place, lreg, sort, total;
+};
+inline BwdZero bwd_zero_layout(uint64_t nk) {
+  BwdZero z;
+  z.place = 8;
+  z.lreg = z.place + 2 * (scan_tiles(nk) + 1);
+  z.sort = z.lreg + 2 * (scan_tiles(bwd_max_long(nk)) + 1);
+  z.total = z.sort + ((sort_ws_words(nk, bwd_long_passes(nk)) + 1) & ~size_t(1));
+  return z;
 }
 // Level-1 chunks of segments longer than kChunk: sum ceil(len/32) <= N/32 + N/33.
 inline uint64_t bwd_max_chunks(uint64_t max_keys) { return max_keys / kChunk + max_keys / (kChunk + 1) + 4; }
-inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
 // Tree nodes above level 1 over all long segments: sum_j (ceil(m_j/32) + ceil(m_j/1024) + ...)
 // <= total_chunks/31 + (levels <= 5) per segment.
 inline uint64_t bwd_max_nodes(uint64_t max_keys) { return bwd_max_chunks(max_keys) / 31 + 5 * bwd_max_long(max_keys) + 8; }
 
 }  // namespace hpsg
+
+struct hps_gpu_table_s;
+namespace hpsg {
+int launch_dedup(hps_gpu_table_s* t);  // backward.cu: K4a-K4d on t->side
+cudaError_t trace_attach_table(TraceRec* p);  // table.cu's copy of the trace pointer
+}
 
 struct hps_gpu_table_s {
   hps_gpu_ctx ctx = nullptr;
@@ -35,7 +59,7 @@ struct hps_gpu_table_s {
   std::vector<uint64_t> row_cap, row_base, slot_cap, slot_base;
   std::vector<hpsg::TableDev> h_tables;
   uint64_t total_rows = 0, total_slots = 0;
-  uint32_t row_absent = 0;  // sort key of an absent-key occurrence (= total_rows, sorts last)
+  uint32_t row_absent = 0;  // occurrence row of an absent key (= total_rows): no gradient
   int sort_bits = 0;        // bits of a global row id (incl. row_absent)
   uint64_t max_keys = 0, max_bags = 0;
   // device state
@@ -47,12 +71,19 @@ struct hps_gpu_table_s {
   float* d_defaults = nullptr;
   uint32_t* d_slot_table = nullptr;
   // per-batch workspaces (sized at create, never reallocated)
-  uint32_t *ws_rows_a = nullptr, *ws_rows_b = nullptr;  // occurrence rows / sort ping-pong
-  uint32_t *ws_bags_a = nullptr, *ws_bags_b = nullptr;  // sort payload: bag of the occurrence
+  uint32_t* ws_rows_a = nullptr;  // occurrence -> global row (row_absent: key absent)
+  uint32_t* ws_rank = nullptr;    // occurrence -> arrival rank within its row (forward atomics)
+  uint32_t* ws_probe_tmp = nullptr;  // occurrence -> the probe CTA's shared-hash entry
+  uint32_t* ws_occ_slot = nullptr;   // occurrence -> index slot; the slot's aux word holds the row's
+                                     // count, then its segment locator (kAuxNone at rest)
+  uint32_t* ws_long_slot = nullptr;  // long segment -> index slot
   uint32_t* ws_occ_bag = nullptr;   // occurrence -> bag (multi-hot)
   uint32_t* ws_bag_len = nullptr;   // bag lengths (multi-hot mean)
-  uint32_t *ws_seg_start = nullptr, *ws_seg_end = nullptr;  // unique-row segments of the sorted list
-  uint32_t *ws_long_seg = nullptr, *ws_long_base = nullptr;  // long segments: id -> segment, first chunk
+  uint4* ws_short_rec = nullptr;    // short segments {row, first, len, 0}, CSR over ws_short_bag
+  uint32_t* ws_short_bag = nullptr; // bags of the short segments' occurrences
+  uint32_t *ws_long_row = nullptr, *ws_long_len = nullptr, *ws_long_start = nullptr;
+  uint32_t *ws_lkey_a = nullptr, *ws_lval_a = nullptr, *ws_lkey_b = nullptr, *ws_lval_b = nullptr;
+  uint32_t* ws_long_base = nullptr;  // long segment -> first level-1 chunk
   uint32_t* ws_task_long = nullptr; // level-1 chunk -> long segment id
   float* ws_partial = nullptr;      // level-1 chunk partials of long segments
   float* ws_partial2 = nullptr;     // tree nodes above level 1 [max_nodes x dim]
@@ -60,7 +91,7 @@ struct hps_gpu_table_s {
   uint32_t* ws_node_cnt = nullptr;    // arrivals per node; zero at rest (reset by the completing warp)
   uint64_t max_chunks = 0, max_long = 0;
   uint64_t* ws_counts = nullptr;    // [0]=N occurrences [1]=U segments
-  uint32_t* ws_zero = nullptr;      // look-back words + tickets + long counters, zeroed per backward
+  uint32_t* ws_zero = nullptr;      // bwd_zero_layout(): allocators + look-back words, zeroed per training lookup
   size_t zero_words = 0;
   uint32_t* ws_abort = nullptr;
   uint64_t* ws_keys_stage = nullptr;
@@ -71,7 +102,14 @@ struct hps_gpu_table_s {
   uint64_t* ws_ins_scan = nullptr;
   uint32_t* ws_offsets_stage = nullptr;
   // last training lookup
-  bool have_train = false, last_multi = false, sorted_in_b = false;
+  bool have_train = false, last_multi = false;
+  bool counts_dirty = false;  // slot aux words hold a training record no backward has consumed
+  bool have_unique = false;   // the segment lists describe the last backward (last_unique)
+  // The backward's dedup runs on a side stream, forked after the training probe and joined
+  // by backward_update (table.cu record_and_fork).
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool dedup_pending = false;
   bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)
   int last_combiner = 0;
   uint64_t last_n_keys_host = 0;  // exact when known on the host, else max_keys
