@@ -209,7 +209,7 @@ def reference_arm(args, cfg, rank, world):
 
 TRACE_NAMES = {0: "probe", 1: "pool", 2: "seg_alloc", 3: "place", 4: "long_hist", 5: "long_pass0",
                6: "long_pass1", 7: "long_pass2", 8: "long_pass3", 9: "long_reg", 10: "reduce_short",
-               11: "reduce_long", 12: "reset_counts"}
+               11: "reduce_long", 12: "reset_counts", 13: "count"}
 
 
 def print_trace(ctx, n, step):
@@ -223,7 +223,9 @@ def print_trace(ctx, n, step):
     for i in range(n):
         step(i)
         lib.hps_gpu_debug_trace(2, buf)
-        r = {k: (buf[2 * k], buf[2 * k + 1]) for k in TRACE_NAMES if buf[2 * k] != (1 << 64) - 1}
+        r = {k: (buf[2 * k], buf[2 * k + 1]) for k in TRACE_NAMES if buf[2 * k] != (1 << 64) - 1 or buf[2 * k + 1]}
+        s0 = min((v[0] for v in r.values() if v[0] != (1 << 64) - 1), default=0)
+        r = {k: (v[0] if v[0] != (1 << 64) - 1 else v[1], v[1]) for k, v in r.items()}  # end-only markers
         if r:
             t0 = min(v[0] for v in r.values())
             recs.append({k: ((a - t0) / 1000.0, (b - t0) / 1000.0) for k, (a, b) in r.items()})

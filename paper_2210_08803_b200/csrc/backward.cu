@@ -7,23 +7,28 @@
 // the same way until one vector remains (plain sequential order up to 32 occurrences).
 // Then SGD / AdaGrad / Adam update the row in place.
 //
-// Dedup without a global sort (sizes device-resident, graph-capturable; every kernel is a
-// programmatic dependent launch). The training lookup counted each occurrence on its
-// row in the aux word of its index slot (kAuxNone + count; the atomic returns the rank). Then:
+// Dedup without a global sort (sizes device-resident, graph-capturable). The training
+// lookup's probe records each occurrence's row; then, on the table's side stream and
+// concurrently with the pooling (table.cu record / fork_dedup):
+//   k_count         : per-row occurrence counts in an L2-resident batch table (CTA-level
+//                     shared-memory aggregation first, so hot rows take one atomic per
+//                     CTA); each occurrence gets an arrival rank within its row
 //   k_seg_alloc     : the rank-0 occurrence of each row allocates its segment — short rows
 //                     (<= 32 occurrences) a CSR range of the short list, long rows an id —
-//                     and leaves the locator in the slot aux word
+//                     and leaves the locator in the batch table
 //   k_scan<PlaceOp> : every occurrence drops its bag into its short segment at `rank`, or is
 //                     compacted (canonical order) into the long list as (long id, bag)
 //   long sort       : stable radix sort of the long list by long id (few bits) — each long
 //                     segment contiguous, occurrences in canonical order
-//   k_scan<LongRegOp>: long segment starts, level-1 chunk bases, tree-node blocks; counters reset
+//   k_scan<LongRegOp>, k_long_tasks: long segment starts, level-1 chunk bases, tree-node
+//                     blocks, the chunk -> segment map
+// and at backward_update, the short and long reductions run side by side (disjoint rows):
 //   k_reduce_short  : a warp owns 32 short segments: sorts each one's bags back into canonical
-//                     order (warp rank), reduces and updates (bulk-copy or register path),
-//                     resets the counters; it also publishes the long chunk -> segment map
-//   k_long          : one warp per chunk -> level-1 partial; the last chunk to finish below
+//                     order (warp rank), reduces and updates (bulk-copy or register path)
+//   k_long (side)   : one warp per chunk -> level-1 partial; the last chunk to finish below
 //                     a tree node sums that node's <= 32 children in order, up to the root,
 //                     whose sum goes through the optimizer (hierarchical last-arriver)
+// Every batch-table entry is reset to empty by the kernel that consumes it last.
 #include <algorithm>
 #include <cstring>
 
@@ -38,17 +43,18 @@ namespace {
 struct BwdArgs {
   const uint64_t* counts;   // [0] = N occurrences; [1] <- unique rows (short + long segments)
   const uint32_t* occ_row;  // row of each occurrence (row_absent: no gradient)
-  const uint32_t* occ_rank; // arrival rank of each occurrence within its row
+  uint32_t* occ_rank;       // arrival rank of each occurrence within its row
   const uint32_t* occ_bag;  // multi-hot: bag of each occurrence (nullptr: occurrence i is bag i)
-  const uint32_t* occ_slot; // index slot of each occurrence's key
-  Slot* slots;              // slot aux: kAuxNone + count -> segment locator -> kAuxNone (reset here)
+  uint32_t* occ_ent;        // batch-table entry of each occurrence's row
+  uint2* bt;                // batch table {row, UINT32_MAX + count -> segment locator}
+  uint64_t bt_mask;
   uint32_t row_absent;
   unsigned long long* short_alloc;  // (segments << 32) | occurrences
-  uint4* short_rec;                 // {row, first, len, slot}
+  uint4* short_rec;                 // {row, first, len, batch-table entry}
   uint32_t* short_bag;
   uint32_t* n_long;
   uint32_t* long_row;
-  uint32_t* long_slot;
+  uint32_t* long_ent;
   uint32_t* long_len;
   uint32_t* long_start;     // first position of the segment in the sorted long list
   uint32_t* lkey;           // long list: segment id (sort input)
@@ -75,100 +81,210 @@ struct BwdArgs {
   hps_opt_params opt;
 };
 
-// ---- K4a: segment allocation (the rank-0 occurrence of each row leads) ------------------
-// A CTA takes 512 consecutive occurrences (2 per thread); its short leaders get
-// consecutive CSR ranges from ONE packed atomic (segments << 32 | occurrences) after a
-// block scan, so segment s+1 starts where segment s ends. Long leaders take ids from a
-// warp-aggregated counter (they are few).
-constexpr int kAllocIPT = 2;
-__global__ void __launch_bounds__(256) k_seg_alloc(BwdArgs a) {
-  __shared__ unsigned long long s_scr[33];
-  __shared__ unsigned long long s_base;
-  pdl_wait();
-  pdl_launch_dependents();
-  trace_begin(kTrAlloc);
-  const uint64_t n = a.counts[0];
-  const uint32_t lane = lane_id(), lt = lanemask_lt();
-  constexpr uint64_t kTile = 256 * kAllocIPT;
-  for (uint64_t t0 = uint64_t(blockIdx.x) * kTile; t0 < n; t0 += uint64_t(gridDim.x) * kTile) {
-    uint32_t row[kAllocIPT], len[kAllocIPT], slot[kAllocIPT];
-    unsigned long long mine = 0;  // (short segments << 32) | their occurrences
-#pragma unroll
-    for (int k = 0; k < kAllocIPT; ++k) {
-      const uint64_t i = t0 + uint64_t(threadIdx.x) * kAllocIPT + k;
-      row[k] = a.row_absent;
-      len[k] = 0;
-      slot[k] = 0;
-      if (i < n) {
-        const uint32_t r = a.occ_row[i];
-        if (r != a.row_absent && a.occ_rank[i] == 0u) {
-          row[k] = r;
-          slot[k] = a.occ_slot[i];
-          len[k] = a.slots[slot[k]].aux + 1u;
-        }
-      }
-      if (len[k] && len[k] <= kChunk) mine += (1ull << 32) | len[k];
-    }
-    unsigned long long total;
-    unsigned long long excl = block_excl_scan<256>(mine, s_scr, &total);
-    if (threadIdx.x == 0 && total) s_base = atomicAdd(a.short_alloc, total);
-    __syncthreads();
-    const unsigned long long base = total ? s_base : 0ull;
-    unsigned long long pos = base + excl;
-#pragma unroll
-    for (int k = 0; k < kAllocIPT; ++k) {
-      if (len[k] && len[k] <= kChunk) {
-        const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
-        a.short_rec[seg] = make_uint4(row[k], first, len[k], slot[k]);
-        a.slots[slot[k]].aux = first;
-        pos += (1ull << 32) | len[k];
-      }
-    }
-    // long leaders (rare): one warp-aggregated id reservation per item slot
-#pragma unroll
-    for (int k = 0; k < kAllocIPT; ++k) {
-      const bool lg = len[k] > kChunk;
-      const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
-      if (!lg_mask) continue;
-      uint32_t j0 = 0;
-      if (lane == __ffs(lg_mask) - 1) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
-      j0 = __shfl_sync(0xffffffffu, j0, __ffs(lg_mask) - 1);
-      if (lg) {
-        const uint32_t j = j0 + __popc(lg_mask & lt);
-        a.long_row[j] = row[k];
-        a.long_slot[j] = slot[k];
-        a.long_len[j] = len[k];
-        a.slots[slot[k]].aux = kLongFlag | j;
-      }
-    }
-    __syncthreads();  // s_base / s_scr reuse
+// ---- batch table ----------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t bt_home(uint32_t row, uint64_t mask) {
+  return static_cast<uint32_t>(((uint64_t(row) * 0x9E3779B97F4A7C15ull) >> 32) & mask);
+}
+// Entry of `row` (inserted if absent); one CAS in the common case.
+__device__ __forceinline__ uint32_t bt_insert(uint2* bt, uint64_t mask, uint32_t row) {
+  uint32_t h = bt_home(row, mask);
+  while (true) {
+    const uint32_t old = atomicCAS(&bt[h].x, kBtEmpty, row);
+    if (old == kBtEmpty || old == row) return h;
+    h = static_cast<uint32_t>((h + 1) & mask);
   }
-  trace_end(kTrAlloc);
 }
 
-// ---- K4b: placement (scan over occurrences; the scan compacts the long ones in order) ----
-struct PlaceOp {
-  static constexpr int kTrace = kTrPlace;
-  BwdArgs a;
-  __device__ uint64_t size() const { return a.counts[0]; }
-  __device__ uint32_t count(uint64_t i) const {
-    const uint32_t r = a.occ_row[i];
-    return r == a.row_absent ? 0u : (a.slots[a.occ_slot[i]].aux >> 31);
+// ---- K4a-c fused: counts, allocation, placement in ONE persistent cooperative kernel ------
+// One CTA per SM (64 KB shared hash + 512 threads: it sits beside the pooling kernel it
+// overlaps); CTA c owns the contiguous occurrence chunk [c*n/G, (c+1)*n/G). Three grid
+// barriers separate the phases that need every CTA's results:
+//   P1 counts: shared-hash aggregation over the chunk, then ONE batch-table reservation
+//      (CAS + add) per distinct row per CTA -> each occurrence's rank and table entry
+//   P2 allocation: the rank-0 occurrence of each row (now final counts) takes a short
+//      CSR range (one packed atomic per CTA, handed out in occurrence order) or a long id
+//   P3 placement: short occurrences drop their bag at first + rank; long occurrences are
+//      compacted in canonical order (per-CTA counts -> prefix over CTAs -> block scans)
+// Batch-table words written by other CTAs are read through L2 (__ldcg) after a barrier.
+constexpr int kDedupBlock = 512;
+constexpr int kDedupHash = 8192;
+constexpr uint32_t kNoEnt = 0xffffffffu;
+constexpr uint32_t kDirectEnt = 0x80000000u;  // occ_ent flag inside P1: counted directly
+
+__device__ __forceinline__ uint32_t smem_hash_slot(uint32_t* s_key, uint32_t row) {
+  uint32_t h = (row * 0x9e3779b1u) >> 19;  // 13 bits
+  for (int probe = 0; probe < 128; ++probe) {
+    const uint32_t cur = s_key[h];
+    if (cur == row) return h;
+    if (cur == kBtEmpty) {
+      const uint32_t old = atomicCAS(&s_key[h], kBtEmpty, row);
+      if (old == kBtEmpty || old == row) return h;
+    }
+    h = (h + 1) & (kDedupHash - 1);
   }
-  __device__ void emit(uint64_t i, uint64_t excl, uint64_t c) const {
-    const uint32_t r = a.occ_row[i];
-    if (r == a.row_absent) return;
-    const uint32_t bag = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
-    const uint32_t loc = a.slots[a.occ_slot[i]].aux;
-    if (c) {
-      a.lkey[excl] = loc & ~kLongFlag;
-      a.lval[excl] = bag;
-    } else {
-      a.short_bag[loc + a.occ_rank[i]] = bag;
+  return kNoEnt;
+}
+
+__global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* coop) {
+  extern __shared__ uint32_t s_dd[];
+  uint32_t* s_key = s_dd;               // row, then its batch-table entry
+  uint32_t* s_val = s_dd + kDedupHash;  // chunk count, then the CTA's base rank
+  __shared__ unsigned long long s_scr[33];
+  __shared__ unsigned long long s_base;
+  __shared__ uint32_t s_scr32[33];
+  trace_begin(kTrCount);
+  const uint64_t n = a.counts[0];
+  const uint64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t lane = lane_id(), lt = lanemask_lt();
+  // ---- P1: counts and ranks
+  for (int e = threadIdx.x; e < kDedupHash; e += kDedupBlock) {
+    s_key[e] = kBtEmpty;
+    s_val[e] = 0u;
+  }
+  __syncthreads();
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
+    const uint32_t row = a.occ_row[i];
+    if (row == a.row_absent) continue;
+    const uint32_t h = smem_hash_slot(s_key, row);
+    if (h != kNoEnt) {
+      a.occ_rank[i] = atomicAdd(&s_val[h], 1u);
+      a.occ_ent[i] = h;
+    } else {  // shared hash full: count directly
+      const uint32_t e = bt_insert(a.bt, a.bt_mask, row);
+      a.occ_rank[i] = atomicAdd(&a.bt[e].y, 1u) + 1u;
+      a.occ_ent[i] = kDirectEnt | e;
     }
   }
-  __device__ void total(uint64_t t) const { *a.long_occ = t; }
-};
+  __syncthreads();
+  {  // one reservation per distinct row: every home-slot CAS in flight at once, the (rare,
+     // sparse table) collisions resolved after, then every add in flight at once
+    constexpr int kPer = kDedupHash / kDedupBlock;
+    uint32_t key[kPer], ent[kPer], res[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      key[q] = s_key[threadIdx.x + kDedupBlock * q];
+      ent[q] = key[q] != kBtEmpty ? bt_home(key[q], a.bt_mask) : kNoEnt;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+      res[q] = ent[q] != kNoEnt ? atomicCAS(&a.bt[ent[q]].x, kBtEmpty, key[q]) : kBtEmpty;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+      if (ent[q] != kNoEnt && res[q] != kBtEmpty && res[q] != key[q]) ent[q] = bt_insert(a.bt, a.bt_mask, key[q]);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q)
+      res[q] = ent[q] != kNoEnt ? atomicAdd(&a.bt[ent[q]].y, s_val[threadIdx.x + kDedupBlock * q]) + 1u : 0u;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {  // entry e is owned by this thread: no hazard with other threads
+      s_key[threadIdx.x + kDedupBlock * q] = ent[q];
+      s_val[threadIdx.x + kDedupBlock * q] = res[q];
+    }
+  }
+  __syncthreads();
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
+    if (a.occ_row[i] == a.row_absent) continue;
+    const uint32_t h = a.occ_ent[i];
+    if (h & kDirectEnt) {
+      a.occ_ent[i] = h & ~kDirectEnt;
+    } else {
+      a.occ_rank[i] += s_val[h];
+      a.occ_ent[i] = s_key[h];
+    }
+  }
+  trace_end(kTrCount);
+  grid_barrier_once(coop + 0);
+  // ---- P2: allocation
+  trace_begin(kTrAlloc);
+  unsigned long long mine = 0;
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
+    if (a.occ_row[i] == a.row_absent || a.occ_rank[i] != 0u) continue;
+    const uint32_t len = __ldcg(&a.bt[a.occ_ent[i]].y) + 1u;
+    if (len <= kChunk) mine += (1ull << 32) | len;
+  }
+  unsigned long long total;
+  (void)block_excl_scan<kDedupBlock>(mine, s_scr, &total);
+  if (threadIdx.x == 0) s_base = total ? atomicAdd(a.short_alloc, total) : 0ull;
+  __syncthreads();
+  unsigned long long run = s_base;
+  for (uint64_t t0 = c0; t0 < c1; t0 += kDedupBlock) {  // tiles in order, one item per thread
+    const uint64_t i = t0 + threadIdx.x;
+    uint32_t row = 0, len = 0, ent = 0;
+    if (i < c1) {
+      const uint32_t r = a.occ_row[i];
+      if (r != a.row_absent && a.occ_rank[i] == 0u) {
+        row = r;
+        ent = a.occ_ent[i];
+        len = __ldcg(&a.bt[ent].y) + 1u;
+      }
+    }
+    const bool sh = len && len <= kChunk, lg = len > kChunk;
+    unsigned long long ttotal;
+    const unsigned long long pos = run + block_excl_scan<kDedupBlock>(sh ? (1ull << 32) | len : 0ull, s_scr, &ttotal);
+    run += ttotal;
+    if (sh) {
+      const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
+      a.short_rec[seg] = make_uint4(row, first, len, ent);
+      a.bt[ent].y = first;
+    }
+    const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
+    if (lg_mask) {
+      const int src = __ffs(lg_mask) - 1;
+      uint32_t j0 = 0;
+      if (static_cast<int>(lane) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
+      j0 = __shfl_sync(0xffffffffu, j0, src);
+      if (lg) {
+        const uint32_t j = j0 + __popc(lg_mask & lt);
+        a.long_row[j] = row;
+        a.long_ent[j] = ent;
+        a.long_len[j] = len;
+        a.bt[ent].y = kLongFlag | j;
+      }
+    }
+  }
+  trace_end(kTrAlloc);
+  grid_barrier_once(coop + 1);
+  // ---- P3: placement
+  trace_begin(kTrPlace);
+  uint32_t my_long = 0;
+  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
+    const uint32_t r = a.occ_row[i];
+    if (r == a.row_absent) continue;
+    const uint32_t loc = __ldcg(&a.bt[a.occ_ent[i]].y);
+    if (loc & kLongFlag) {
+      ++my_long;
+    } else {
+      a.short_bag[loc + a.occ_rank[i]] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+    }
+  }
+  uint32_t cta_long;
+  (void)block_excl_scan<kDedupBlock>(my_long, s_scr32, &cta_long);
+  if (threadIdx.x == 0) st_vol32(coop + 4 + blockIdx.x, cta_long);
+  grid_barrier_once(coop + 2);
+  uint32_t before = 0;
+  for (uint32_t c = threadIdx.x; c < blockIdx.x; c += kDedupBlock) before += ld_vol32(coop + 4 + c);
+  uint32_t lbase;
+  (void)block_excl_scan<kDedupBlock>(before, s_scr32, &lbase);
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *a.long_occ = lbase + cta_long;
+  if (cta_long) {
+    for (uint64_t t0 = c0; t0 < c1; t0 += kDedupBlock) {  // canonical order: tiles in order
+      const uint64_t i = t0 + threadIdx.x;
+      uint32_t loc = 0;
+      bool lg = false;
+      if (i < c1 && a.occ_row[i] != a.row_absent) {
+        loc = __ldcg(&a.bt[a.occ_ent[i]].y);
+        lg = (loc & kLongFlag) != 0;
+      }
+      uint32_t ttotal;
+      const uint32_t excl = block_excl_scan<kDedupBlock>(lg ? 1u : 0u, s_scr32, &ttotal);
+      if (lg) {
+        a.lkey[lbase + excl] = loc & ~kLongFlag;
+        a.lval[lbase + excl] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+      }
+      lbase += ttotal;
+    }
+  }
+  trace_end(kTrPlace);
+}
 
 // ---- long segments: registration ---------------------------------------------------------
 // Nodes above level 1 of a long segment's 32-ary tree (m level-1 chunks).
@@ -196,7 +312,7 @@ struct LongRegOp {
     a.long_start[j] = static_cast<uint32_t>(excl);
     a.long_base[j] = static_cast<uint32_t>(excl >> 32);
     a.long_hbase[j] = atomicAdd(a.higher_total, higher_nodes(m));
-    a.slots[a.long_slot[j]].aux = kAuxNone;
+    a.bt[a.long_ent[j]] = make_uint2(kBtEmpty, 0xffffffffu);
   }
   __device__ void total(uint64_t t) const {
     *a.long_chunks = t >> 32;
@@ -204,9 +320,12 @@ struct LongRegOp {
   }
 };
 
-// Chunk -> long segment map (written by the short-reduce kernel's warps before their own
-// work; consumed by k_long).
-__device__ __forceinline__ void publish_long_tasks(const BwdArgs& a, uint64_t warp, uint64_t n_warps) {
+// Chunk -> long segment map (warp per long segment; consumed by k_long).
+__global__ void __launch_bounds__(256) k_long_tasks(BwdArgs a) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t nl = *a.n_long;
   for (uint64_t j = warp; j < nl; j += n_warps) {
     const uint32_t m = (a.long_len[j] + kChunk - 1) / kChunk, base = a.long_base[j];
@@ -364,7 +483,7 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
     const uint32_t r0 = stage_short_bags(a, S, u0, first, len, sbag);
     const uint32_t off = first - r0;
     if (len) {
-      a.slots[slot].aux = kAuxNone;  // placement (previous kernels) is done with the locator
+      a.bt[slot] = make_uint2(kBtEmpty, 0xffffffffu);  // placement (previous kernels) is done with it
       b0 = sbag[off];
       if (len >= 2) b1 = sbag[off + 1];
       if (mean) {
@@ -491,7 +610,7 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
     }
     const uint32_t r0 = stage_short_bags(a, S, u0, first, len, sbag);
     const uint32_t boff = first - r0;
-    if (len) a.slots[slot].aux = kAuxNone;  // placement (previous kernels) is done with the locator
+    if (len) a.bt[slot] = make_uint2(kBtEmpty, 0xffffffffu);  // placement (previous kernels) is done with it
     const uint32_t need = len ? 1 + NS + len : 0;
     uint32_t first_lane = 0;  // first lane (segment) of the current wave
     while (first_lane < 32) {
@@ -696,7 +815,7 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
 }
 
 // ---- kernels ------------------------------------------------------------------------------
-// Short segments reduced + updated (after publishing the long chunk -> segment map).
+// Short segments reduced + updated.
 template <int OPT, int LPR, int VPL, bool TMA>
 __global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : 2)
     k_reduce_short(BwdArgs a) {
@@ -708,7 +827,6 @@ __global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : 2)
   const uint64_t warp = uint64_t(blockIdx.x) * wpb + (threadIdx.x >> 5);
   const uint64_t n_warps = uint64_t(gridDim.x) * wpb;
   trace_begin(kTrReduce);
-  publish_long_tasks(a, warp, n_warps);
   if constexpr (TMA) {
     short_tma<OPT, VPL>(a, warp, n_warps, s_dyn, s_bar);
   } else {
@@ -730,6 +848,14 @@ __global__ void __launch_bounds__(256, VPL >= 4 ? 2 : (LPR == 32 ? 3 : 4)) k_lon
   trace_end(kTrLong);
 }
 
+__global__ void k_bt_used(const uint2* bt, uint64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    c += (bt[i].x != kBtEmpty || bt[i].y != 0xffffffffu) ? 1ull : 0ull;
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
 // Rows updated by the last backward (short + long segments), unsorted; count -> *count_out.
 __global__ void k_unique_rows(const uint4* short_rec, const unsigned long long* short_alloc, const uint32_t* long_row,
                               const uint32_t* n_long, uint32_t* out, uint64_t* count_out) {
@@ -739,41 +865,44 @@ __global__ void k_unique_rows(const uint4* short_rec, const unsigned long long* 
     out[u] = u < S ? short_rec[u].x : long_row[u - S];
 }
 
+// Short segments on `st` (main), long segments on `side` — disjoint rows, run side by side.
 template <int OPT, int LPR, int VPL, bool TMA>
-int launch_backward_v(const BwdArgs& a, cudaStream_t st, bool pdl, size_t smem, int grid, int long_grid) {
+int launch_backward_v(const BwdArgs& a, cudaStream_t st, cudaStream_t side, size_t smem, int grid, int long_grid) {
   auto kern = k_reduce_short<OPT, LPR, VPL, TMA>;
   constexpr int block = TMA ? kRedWarps * 32 : 256;
   static bool attr = false;
   if (!attr) {
     HPSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HPSG_CUDA(prefer_max_smem(kern));
+    HPSG_CUDA(prefer_max_smem(k_long<OPT, LPR, VPL>));
     attr = true;
   }
-  HPSG_CUDA(launch_k(false, kern, grid, block, smem, st, a));  // first kernel after the join
-  HPSG_CUDA(launch_k(pdl, k_long<OPT, LPR, VPL>, long_grid, 256, 0, st, a));
+  HPSG_CUDA(launch_k(false, k_long<OPT, LPR, VPL>, long_grid, 256, 0, side, a));  // first after a join
+  HPSG_CUDA(launch_k(false, kern, grid, block, smem, st, a));
   return HPS_GPU_OK;
 }
 
 // Lanes per row stream so that a lane holds VPL = ceil(nvec / LPR) float4 of a row.
 template <int OPT>
-int launch_backward(const BwdArgs& a, cudaStream_t st, bool pdl, bool tma, size_t smem, int g, int lg,
+int launch_backward(const BwdArgs& a, cudaStream_t st, cudaStream_t side, bool tma, size_t smem, int g, int lg,
                     uint32_t nvec) {
   if (tma) {
-    if (nvec > 32) return launch_backward_v<OPT, 32, 2, true>(a, st, pdl, smem, g, lg);
-    return launch_backward_v<OPT, 32, 1, true>(a, st, pdl, smem, g, lg);
+    if (nvec > 32) return launch_backward_v<OPT, 32, 2, true>(a, st, side, smem, g, lg);
+    return launch_backward_v<OPT, 32, 1, true>(a, st, side, smem, g, lg);
   }
-  if (nvec > 128) return launch_backward_v<OPT, 32, 8, false>(a, st, pdl, smem, g, lg);
-  if (nvec > 64) return launch_backward_v<OPT, 32, 4, false>(a, st, pdl, smem, g, lg);
-  if (nvec > 32) return launch_backward_v<OPT, 32, 2, false>(a, st, pdl, smem, g, lg);
-  if (nvec == 32) return launch_backward_v<OPT, 32, 1, false>(a, st, pdl, smem, g, lg);
-  if (nvec > 16) return launch_backward_v<OPT, 16, 2, false>(a, st, pdl, smem, g, lg);
-  if (nvec == 16) return launch_backward_v<OPT, 16, 1, false>(a, st, pdl, smem, g, lg);
-  if (nvec > 8) return launch_backward_v<OPT, 8, 2, false>(a, st, pdl, smem, g, lg);
-  if (nvec == 8) return launch_backward_v<OPT, 8, 1, false>(a, st, pdl, smem, g, lg);
-  if (nvec > 4) return launch_backward_v<OPT, 4, 2, false>(a, st, pdl, smem, g, lg);
-  if (nvec == 4) return launch_backward_v<OPT, 4, 1, false>(a, st, pdl, smem, g, lg);
-  if (nvec > 2) return launch_backward_v<OPT, 2, 2, false>(a, st, pdl, smem, g, lg);
-  if (nvec == 2) return launch_backward_v<OPT, 2, 1, false>(a, st, pdl, smem, g, lg);
-  return launch_backward_v<OPT, 1, 1, false>(a, st, pdl, smem, g, lg);
+  if (nvec > 128) return launch_backward_v<OPT, 32, 8, false>(a, st, side, smem, g, lg);
+  if (nvec > 64) return launch_backward_v<OPT, 32, 4, false>(a, st, side, smem, g, lg);
+  if (nvec > 32) return launch_backward_v<OPT, 32, 2, false>(a, st, side, smem, g, lg);
+  if (nvec == 32) return launch_backward_v<OPT, 32, 1, false>(a, st, side, smem, g, lg);
+  if (nvec > 16) return launch_backward_v<OPT, 16, 2, false>(a, st, side, smem, g, lg);
+  if (nvec == 16) return launch_backward_v<OPT, 16, 1, false>(a, st, side, smem, g, lg);
+  if (nvec > 8) return launch_backward_v<OPT, 8, 2, false>(a, st, side, smem, g, lg);
+  if (nvec == 8) return launch_backward_v<OPT, 8, 1, false>(a, st, side, smem, g, lg);
+  if (nvec > 4) return launch_backward_v<OPT, 4, 2, false>(a, st, side, smem, g, lg);
+  if (nvec == 4) return launch_backward_v<OPT, 4, 1, false>(a, st, side, smem, g, lg);
+  if (nvec > 2) return launch_backward_v<OPT, 2, 2, false>(a, st, side, smem, g, lg);
+  if (nvec == 2) return launch_backward_v<OPT, 2, 1, false>(a, st, side, smem, g, lg);
+  return launch_backward_v<OPT, 1, 1, false>(a, st, side, smem, g, lg);
 }
 
 BwdArgs base_args(hps_gpu_table t) {
@@ -784,8 +913,9 @@ BwdArgs base_args(hps_gpu_table t) {
   a.occ_row = t->ws_rows_a;
   a.occ_rank = t->ws_rank;
   a.occ_bag = t->last_multi ? t->ws_occ_bag : nullptr;
-  a.occ_slot = t->ws_occ_slot;
-  a.slots = t->d_slots;
+  a.occ_ent = t->ws_occ_ent;
+  a.bt = t->ws_bt;
+  a.bt_mask = t->bt_mask;
   a.row_absent = t->row_absent;
   a.short_alloc = reinterpret_cast<unsigned long long*>(z);
   a.short_rec = t->ws_short_rec;
@@ -795,7 +925,7 @@ BwdArgs base_args(hps_gpu_table t) {
   a.long_occ = reinterpret_cast<unsigned long long*>(z + 4);
   a.long_chunks = reinterpret_cast<unsigned long long*>(z + 6);
   a.long_row = t->ws_long_row;
-  a.long_slot = t->ws_long_slot;
+  a.long_ent = t->ws_long_ent;
   a.long_len = t->ws_long_len;
   a.long_start = t->ws_long_start;
   a.lkey = t->ws_lkey_a;
@@ -816,23 +946,34 @@ BwdArgs base_args(hps_gpu_table t) {
 }  // namespace
 
 // K4a-K4d on the table's side stream, right after the training probe (table.cu
-// record_and_fork): they need only the occurrence record, so they overlap the pooling.
-int hpsg::launch_dedup(hps_gpu_table t) {
-  cudaStream_t st = t->side;
+// fork_dedup): they need only the occurrence record, so they overlap the pooling.
+int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
   const bool pdl = t->ctx->pdl;
   const uint64_t nk = t->last_n_keys_host;
   const BwdZero zl = bwd_zero_layout(nk);
   uint32_t* z = t->ws_zero;
   const BwdArgs a = base_args(t);
-  // K4a: segment allocation (first on this stream after the fork: a plain launch)
-  HPSG_CUDA(launch_k(false, k_seg_alloc, grid_for((nk + kAllocIPT - 1) / kAllocIPT, 256, kNumSMs * 8), 256, 0, st, a));
-  // K4b: placement (short segments) + ordered compaction of the long occurrences
+  // K4a-c: counts, allocation, placement (first on this stream after the fork: a plain launch)
   {
-    const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(nk));
-    uint64_t* status = reinterpret_cast<uint64_t*>(z + zl.place);
-    HPSG_CUDA(launch_k(pdl, k_scan<PlaceOp>, static_cast<unsigned>(tiles), kScanBlock, 0, st, PlaceOp{a}, status,
-                       reinterpret_cast<uint32_t*>(status + tiles)));
+    static bool attr = false;
+    if (!attr) {
+      HPSG_CUDA(cudaFuncSetAttribute(k_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4));
+      HPSG_CUDA(prefer_max_smem(k_dedup));
+      HPSG_CUDA(prefer_max_smem(k_radix_hist));
+      HPSG_CUDA(prefer_max_smem(k_radix_pass));
+      HPSG_CUDA(prefer_max_smem(k_scan<LongRegOp>));
+      HPSG_CUDA(prefer_max_smem(k_long_tasks));
+      attr = true;
+    }
+    const int g = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kNumSMs, (nk + 511) / 512)));
+    // A plain launch (a cooperative one would not start beside the pooling): co-residency of
+    // the grid barriers holds by construction — at most one CTA per SM, and every kernel it
+    // can share the SMs with (the pooling) runs to completion without waiting on it.
+    HPSG_CUDA(launch_k(false, k_dedup, g, kDedupBlock, size_t(2) * kDedupHash * 4, st, a, z + zl.coop));
   }
+  // the short segments are complete: the short reduce may start (backward_update joins here);
+  // the long segments' sort and registration continue on this stream
+  if (st == t->side) HPSG_CUDA(cudaEventRecord(t->ev_join, st));
   // K4c: stable sort of the long list by segment id (canonical order within each segment)
   {
     const int passes = bwd_long_passes(nk);
@@ -864,6 +1005,7 @@ int hpsg::launch_dedup(hps_gpu_table t) {
     HPSG_CUDA(launch_k(pdl, k_scan<LongRegOp>, static_cast<unsigned>(tiles), kScanBlock, 0, st, LongRegOp{a}, status,
                        reinterpret_cast<uint32_t*>(status + tiles)));
   }
+  HPSG_CUDA(launch_k(pdl, k_long_tasks, grid_for(bwd_max_long(nk) * 32, 256, kNumSMs * 8), 256, 0, st, a));
   HPSG_CHECK_LAUNCH("backward dedup");
   return HPS_GPU_OK;
 }
@@ -881,7 +1023,14 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   cudaStream_t st = t->ctx->stream;
   const bool pdl = t->ctx->pdl;
   const uint64_t nk = t->last_n_keys_host;
-  // join the dedup forked by the training lookup
+  // join the dedup forked by the training lookup; the long reduce runs on the side stream
+  // (after this point of the main stream: the pooling has read the rows, d_out is ready)
+  if (t->dedup_deferred) {
+    if (int s = launch_dedup(t, st)) return s;
+    t->dedup_deferred = false;
+  }
+  HPSG_CUDA(cudaEventRecord(t->ev_bwd, st));
+  HPSG_CUDA(cudaStreamWaitEvent(t->side, t->ev_bwd, 0));
   if (t->dedup_pending) {
     HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
     t->dedup_pending = false;
@@ -903,7 +1052,7 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   size_t smem = 0;
   int grid = 0;
   if (tma) {
-    a.tma_rows = static_cast<uint32_t>(std::max<uint64_t>(40, (22 * 1024) / (t->dim * 4)));
+    a.tma_rows = 40;  // 2 CTAs/SM with room for the long-segment chain's kernels beside them
     smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float) + size_t(kRedWarps) * kBagStage * 4;
     grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * 4)));
@@ -913,13 +1062,15 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   }
   const int long_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
   int s = HPS_GPU_OK;
-  if (grad_only) s = launch_backward<kOptGrad>(a, st, pdl, tma, smem, grid, long_grid, nvec);
-  else if (t->optimizer == HPS_OPT_SGD) s = launch_backward<HPS_OPT_SGD>(a, st, pdl, tma, smem, grid, long_grid, nvec);
+  if (grad_only) s = launch_backward<kOptGrad>(a, st, t->side, tma, smem, grid, long_grid, nvec);
+  else if (t->optimizer == HPS_OPT_SGD) s = launch_backward<HPS_OPT_SGD>(a, st, t->side, tma, smem, grid, long_grid, nvec);
   else if (t->optimizer == HPS_OPT_ADAGRAD)
-    s = launch_backward<HPS_OPT_ADAGRAD>(a, st, pdl, tma, smem, grid, long_grid, nvec);
-  else s = launch_backward<HPS_OPT_ADAM>(a, st, pdl, tma, smem, grid, long_grid, nvec);
+    s = launch_backward<HPS_OPT_ADAGRAD>(a, st, t->side, tma, smem, grid, long_grid, nvec);
+  else s = launch_backward<HPS_OPT_ADAM>(a, st, t->side, tma, smem, grid, long_grid, nvec);
   if (s) return s;
   HPSG_CHECK_LAUNCH("backward");
+  HPSG_CUDA(cudaEventRecord(t->ev_join2, t->side));
+  HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join2, 0));
   t->have_train = false;    // one backward per training lookup (its zeroed workspace is now used)
   t->counts_dirty = false;  // the backward resets every counter it found
   t->have_unique = true;
@@ -1020,6 +1171,24 @@ int hps_gpu_debug_trace(int mode, uint64_t* trace_host) {
     return HPS_GPU_OK;
   }
   return HPS_GPU_E_INVALID_ARGUMENT;
+}
+
+// Invariant check (tests): batch-table entries in use. Zero whenever no training record is
+// pending (every backward and every counter reset empties what it used). Synchronises.
+int hps_gpu_debug_batch_table_used(hps_gpu_table t, uint64_t* used_host) {
+  if (!t || !used_host) return HPS_GPU_E_INVALID_ARGUMENT;
+  unsigned long long* d = nullptr;
+  HPSG_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  HPSG_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), t->ctx->stream));
+  k_bt_used<<<grid_for(t->bt_mask + 1, 256, kNumSMs * 8), 256, 0, t->ctx->stream>>>(t->ws_bt, t->bt_mask + 1, d);
+  HPSG_CHECK_LAUNCH("k_bt_used");
+  HPSG_CUDA(cudaStreamSynchronize(t->ctx->stream));
+  HPSG_CUDA(cudaStreamSynchronize(t->side));
+  unsigned long long v = 0;
+  HPSG_CUDA(cudaMemcpy(&v, d, sizeof(v), cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  *used_host = v;
+  return HPS_GPU_OK;
 }
 
 int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* unique_rows_out) {

@@ -190,6 +190,14 @@ inline cudaError_t launch_k(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 
   return launch_kx(pdl, false, kernel, grid, block, smem, st, args...);
 }
 
+// Kernels that run side by side (pooling beside the dedup, short beside long reduce) need
+// the same L1/shared split: an SM carved out for one cannot take the other's CTAs until
+// it drains. Every step kernel asks for the maximum shared carveout (once per kernel).
+template <typename... KArgs>
+inline cudaError_t prefer_max_smem(void (*kernel)(KArgs...)) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+}
+
 // One-shot grid barrier over a zeroed counter (cooperative launches only).
 __device__ __forceinline__ void grid_barrier_once(uint32_t* counter) {
   __syncthreads();
@@ -222,7 +230,7 @@ struct TraceRec {
 constexpr int kTraceSlots = 32;
 enum TraceId : int {
   kTrProbe = 0, kTrPool = 1, kTrAlloc = 2, kTrPlace = 3, kTrHist = 4, kTrPass0 = 5, kTrLongReg = 9,
-  kTrReduce = 10, kTrLong = 11, kTrReset = 12
+  kTrReduce = 10, kTrLong = 11, kTrReset = 12, kTrCount = 13
 };
 static __device__ TraceRec* g_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -268,162 +268,73 @@ struct LookupArgs {
   float* out;
   // training only: per-occurrence records consumed by backward.cu
   uint32_t* occ_row;   // global row of each occurrence (row_absent: key absent -> no gradient)
-  uint32_t* occ_rank;  // arrival rank of the occurrence among its row's occurrences
-  uint32_t* occ_slot;  // index slot of the occurrence's key (its aux word counts the row)
-  Slot* rw_slots;      // the index, writable (aux = kAuxNone at rest)
+
   uint32_t row_absent;
   uint32_t* occ_bag;   // multi-hot: bag of each occurrence
   uint32_t* bag_len;   // multi-hot mean: bag lengths
   uint64_t* d_n;       // number of key occurrences (device)
 };
 
-// K3a (training): probe every occurrence once and record it — row (row_absent when the
-// key is absent), arrival rank on the row's counter, bag (multi-hot) and bag length (mean).
-// The pooling kernels then read the recorded rows, and the backward's dedup
-// (backward.cu launch_dedup) runs on the side stream concurrently with the pooling.
-//
-// The row's counter is the aux word of the key's own index slot (kAuxNone + count, so the
-// arrival rank is old + 1): the probe has just brought that line into L2, so counting adds
-// no DRAM round trip. Counting is aggregated per CTA so that hot rows (tiny Criteo
-// tables, Zipf heads) do not serialise thousands of same-address atomics: a CTA owns 256
-// consecutive bags; each occurrence takes a local rank from a shared-memory hash of the
-// CTA's slots; then ONE global atomicAdd per distinct slot reserves the CTA's block of
-// ranks, and every occurrence adds its block base. (Slots a full hash cannot hold count
-// directly.)
-constexpr int kProbeBags = 256;      // bags per CTA tile (8 warps x 32)
-constexpr int kProbeHash = 4096;     // shared hash entries
-constexpr uint32_t kDirect = 0xffffffffu;
-
-// Probe returning the key's global index slot (kDirect when absent) and local row.
-__device__ __forceinline__ uint32_t probe_slot(const Slot* __restrict__ slots, const TableDev& td, uint64_t key,
-                                               uint32_t* local) {
-  uint64_t idx = hps::key_hash(key) & td.slot_mask;
-  const Slot* base = slots + td.slot_base;
-  for (uint64_t p = 0; p <= td.slot_mask; ++p) {
-    const Slot s = load_slot(base + idx);
-    if (s.row == kRowEmpty) break;
-    if (s.key == key) {
-      *local = s.row;
-      return static_cast<uint32_t>(td.slot_base + idx);
-    }
-    idx = (idx + 1) & td.slot_mask;
-  }
-  *local = kRowEmpty;
-  return kDirect;
-}
-
-__device__ __forceinline__ uint32_t smem_hash_slot(uint32_t* s_row, uint32_t row) {
-  uint32_t h = (row * 0x9e3779b1u) >> (32 - 12);
-  for (int probe = 0; probe < 64; ++probe) {
-    const uint32_t cur = s_row[h];
-    if (cur == row) return h;
-    if (cur == kDirect) {
-      const uint32_t old = atomicCAS(&s_row[h], kDirect, row);
-      if (old == kDirect || old == row) return h;
-    }
-    h = (h + 1) & (kProbeHash - 1);
-  }
-  return kDirect;
-}
-
+// K3a (training): probe every occurrence once and record its row (row_absent when the
+// key is absent), bag (multi-hot) and the bag lengths (mean). The pooling kernels then
+// read the recorded rows, while the backward's dedup (backward.cu launch_dedup) runs on
+// the side stream from the same record, concurrently with the pooling.
 template <bool MULTI>
-__global__ void __launch_bounds__(256) k_probe(LookupArgs a, uint32_t* __restrict__ tmp) {
-  __shared__ uint32_t s_row[kProbeHash];  // global slot index of the entry
-  __shared__ uint32_t s_cnt[kProbeHash];  // local counts, then the CTA's base rank per slot
-  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+__global__ void __launch_bounds__(256) k_probe(LookupArgs a) {
+  const uint32_t lane = lane_id();
   const uint64_t n_bags = a.n_bags;
   trace_begin(kTrProbe);
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_n = MULTI ? a.offsets[n_bags] : n_bags;
-  for (uint64_t t0 = uint64_t(blockIdx.x) * kProbeBags; t0 < n_bags; t0 += uint64_t(gridDim.x) * kProbeBags) {
-    for (int e = threadIdx.x; e < kProbeHash; e += 256) {
-      s_row[e] = kDirect;
-      s_cnt[e] = 0u;
+  if constexpr (!MULTI) {
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_bags; i += uint64_t(gridDim.x) * blockDim.x) {
+      const uint32_t table = a.key_tables ? a.key_tables[i] : a.slot_table[static_cast<uint32_t>(i) % a.n_slots];
+      const TableDev td = a.tables[table];
+      const uint32_t local = probe_find(a.slots, td, a.keys[i]);
+      a.occ_row[i] = local == kRowEmpty ? a.row_absent : static_cast<uint32_t>(td.row_base + local);
     }
-    __syncthreads();
-    // phase A: warp w records bags [b0, b0 + nb)
-    const uint64_t b0 = t0 + uint64_t(w) * 32;
-    if (b0 < n_bags) {
+  } else {
+    // a warp owns 32 consecutive bags (lane = bag: its offsets), then walks the bags'
+    // occurrences 32 at a time, coalesced; each lane finds its occurrence's bag by a
+    // binary search over the warp's offsets (shuffles)
+    const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+    const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    for (uint64_t b0 = warp * 32; b0 < n_bags; b0 += n_warps * 32) {
       const uint64_t b = b0 + lane;
       const uint32_t nb = static_cast<uint32_t>(min(uint64_t(32), n_bags - b0));
-      uint32_t lo = static_cast<uint32_t>(b), hi_all = static_cast<uint32_t>(b0 + nb);
-      if constexpr (MULTI) {
-        lo = a.offsets[b < n_bags ? b : n_bags];
-        hi_all = __shfl_sync(0xffffffffu, a.offsets[b0 + nb], 0);
-        if (b < n_bags && a.bag_len) a.bag_len[b] = a.offsets[b + 1] - lo;
-      }
+      const uint32_t lo = a.offsets[b < n_bags ? b : n_bags];
+      const uint32_t hi_all = __shfl_sync(0xffffffffu, a.offsets[b0 + nb], 0);
+      if (b < n_bags && a.bag_len) a.bag_len[b] = a.offsets[b + 1] - lo;
       const uint32_t lo0 = __shfl_sync(0xffffffffu, lo, 0);
       for (uint32_t p0 = lo0; p0 < hi_all; p0 += 32) {
         const uint32_t p = p0 + lane;
-        uint32_t k = lane;  // bag of occurrence p within the warp's 32 (one-hot: the lane)
-        if constexpr (MULTI) {
-          k = 0;
+        uint32_t k = 0;
 #pragma unroll
-          for (uint32_t step = 16; step > 0; step >>= 1) {
-            const uint32_t cand = k + step;
-            const uint32_t lc = __shfl_sync(0xffffffffu, lo, cand & 31);
-            if (cand < nb && lc <= p) k = cand;
-          }
+        for (uint32_t step = 16; step > 0; step >>= 1) {
+          const uint32_t cand = k + step;
+          const uint32_t lc = __shfl_sync(0xffffffffu, lo, cand & 31);
+          if (cand < nb && lc <= p) k = cand;
         }
         if (p < hi_all) {
           const uint64_t bag = b0 + k;
-          const uint32_t table = a.key_tables ? a.key_tables[p] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
+          const uint32_t table = a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
           const TableDev td = a.tables[table];
-          uint32_t local;
-          const uint32_t sidx = probe_slot(a.slots, td, a.keys[p], &local);
-          if (local == kRowEmpty) {
-            a.occ_row[p] = a.row_absent;
-          } else {
-            a.occ_row[p] = static_cast<uint32_t>(td.row_base + local);
-            a.occ_slot[p] = sidx;
-            const uint32_t h = smem_hash_slot(s_row, sidx);
-            if (h != kDirect) {
-              a.occ_rank[p] = atomicAdd(&s_cnt[h], 1u);
-            } else {
-              a.occ_rank[p] = atomicAdd(&a.rw_slots[sidx].aux, 1u) + 1u;
-            }
-            tmp[p] = h;
-          }
-          if constexpr (MULTI) a.occ_bag[p] = static_cast<uint32_t>(bag);
+          const uint32_t local = probe_find(a.slots, td, a.keys[p]);
+          a.occ_row[p] = local == kRowEmpty ? a.row_absent : static_cast<uint32_t>(td.row_base + local);
+          a.occ_bag[p] = static_cast<uint32_t>(bag);
         }
       }
     }
-    __syncthreads();
-    // phase B: one global reservation per distinct row of the tile (all of a thread's
-    // atomics issued before any result is consumed)
-    {
-      constexpr int kPer = kProbeHash / 256;
-      uint32_t res[kPer];
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const uint32_t e = threadIdx.x + 256u * k;
-        const uint32_t r = s_row[e];
-        res[k] = r != kDirect ? atomicAdd(&a.rw_slots[r].aux, s_cnt[e]) + 1u : 0u;
-      }
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) s_cnt[threadIdx.x + 256u * k] = res[k];
-    }
-    __syncthreads();
-    // phase C: ranks += the CTA's base for the row (the tile's occurrences are contiguous)
-    const uint64_t tb_end = min(t0 + kProbeBags, n_bags);
-    const uint32_t plo = MULTI ? a.offsets[t0] : static_cast<uint32_t>(t0);
-    const uint32_t phi = MULTI ? a.offsets[tb_end] : static_cast<uint32_t>(tb_end);
-    for (uint32_t p = plo + threadIdx.x; p < phi; p += 256) {
-      if (a.occ_row[p] == a.row_absent) continue;
-      const uint32_t h = tmp[p];
-      if (h != kDirect) a.occ_rank[p] += s_cnt[h];
-    }
-    __syncthreads();
   }
   trace_end(kTrProbe);
 }
 
-// Counters left by a training record that no backward consumed: back to kAuxNone.
-__global__ void k_reset_counts(const uint32_t* __restrict__ occ_row, const uint32_t* __restrict__ occ_slot,
-                               const uint64_t* d_n, uint32_t row_absent, Slot* slots) {
+// Batch-table entries left by a training record that no backward consumed: back to empty.
+__global__ void k_reset_counts(const uint32_t* __restrict__ occ_row, const uint32_t* __restrict__ occ_ent,
+                               const uint64_t* d_n, uint32_t row_absent, uint2* bt) {
   trace_begin(kTrReset);
   const uint64_t n = *d_n;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    if (occ_row[i] != row_absent) slots[occ_slot[i]].aux = kAuxNone;
+    if (occ_row[i] != row_absent) bt[occ_ent[i]] = make_uint2(kBtEmpty, 0xffffffffu);
   trace_end(kTrReset);
 }
 
@@ -773,20 +684,18 @@ __global__ void __launch_bounds__(256) k_hybrid_pool(const uint32_t* __restrict_
 // that record's dedup on the side stream is done).
 int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk) {
   cudaStream_t st = t->ctx->stream;
-  if (t->dedup_pending) {
-    HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
+  if (t->dedup_pending) {  // the whole previous dedup, long-segment part included
+    HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_done, 0));
     t->dedup_pending = false;
   }
   if (t->counts_dirty) {
     k_reset_counts<<<grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0, st>>>(
-        t->ws_rows_a, t->ws_occ_slot, t->ws_counts, t->row_absent, t->d_slots);
+        t->ws_rows_a, t->ws_occ_ent, t->ws_counts, t->row_absent, t->ws_bt);
     HPSG_CHECK_LAUNCH("k_reset_counts");
   }
   HPSG_CUDA(cudaMemsetAsync(t->ws_zero, 0, bwd_zero_layout(nk).total * sizeof(uint32_t), st));
   a.occ_row = t->ws_rows_a;
-  a.occ_rank = t->ws_rank;
-  a.occ_slot = t->ws_occ_slot;
-  a.rw_slots = t->d_slots;
+
   a.row_absent = t->row_absent;
   a.d_n = t->ws_counts;
   t->counts_dirty = true;
@@ -794,28 +703,36 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk) {
   return HPS_GPU_OK;
 }
 
-// Training record: probe + record every occurrence, then fork the backward's dedup onto
-// the table's side stream (it needs only the record) — the pooling that follows on the
-// main stream and the dedup run concurrently; backward_update joins them.
-int record_and_fork(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk) {
+// Training record: probe + record every occurrence (main stream). fork_dedup then puts the
+// backward's dedup on the table's side stream (it needs only the record), after the
+// pooling was launched on the main stream: the two run concurrently; backward_update joins.
+int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk) {
   cudaStream_t st = t->ctx->stream;
-  const int grid = static_cast<int>(
-      std::max<uint64_t>(1, std::min<uint64_t>((a.n_bags + kProbeBags - 1) / kProbeBags, kNumSMs * 16)));
-  if (multi) k_probe<true><<<grid, 256, 0, st>>>(a, t->ws_probe_tmp);
-  else k_probe<false><<<grid, 256, 0, st>>>(a, t->ws_probe_tmp);
+  if (multi) k_probe<true><<<grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * 16), 256, 0, st>>>(a);
+  else k_probe<false><<<grid_for(a.n_bags, 256, kNumSMs * 16), 256, 0, st>>>(a);
   HPSG_CHECK_LAUNCH("probe");
   t->last_multi = multi;
   t->last_combiner = mean ? HPS_COMBINER_MEAN : HPS_COMBINER_SUM;
   t->last_n_keys_host = nk;
-  HPSG_CUDA(cudaEventRecord(t->ev_fork, st));
+  // the fork point: right after the record (the pooling launched next does not gate the dedup)
+  if (!t->no_fork) HPSG_CUDA(cudaEventRecord(t->ev_fork, st));
+  return HPS_GPU_OK;
+}
+
+int fork_dedup(hps_gpu_table t) {
+  cudaStream_t st = t->ctx->stream;
+  if (t->no_fork) {  // A/B measurement: dedup deferred to backward_update, all on the main stream
+    t->dedup_deferred = true;
+    return HPS_GPU_OK;
+  }
   HPSG_CUDA(cudaStreamWaitEvent(t->side, t->ev_fork, 0));
-  if (int s = launch_dedup(t)) return s;
-  HPSG_CUDA(cudaEventRecord(t->ev_join, t->side));
+  if (int s = launch_dedup(t, t->side)) return s;  // records ev_join after the short placement
+  HPSG_CUDA(cudaEventRecord(t->ev_done, t->side));
   t->dedup_pending = true;
   return HPS_GPU_OK;
 }
 
-// Pooled lookup. ROWS (training): rows come from the record (record_and_fork ran first);
+// Pooled lookup. ROWS (training): rows come from the record (record() ran first);
 // otherwise hash + probe + gather + pool in one pass.
 int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
   const cudaStream_t st = t->ctx->stream;
@@ -828,6 +745,8 @@ int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
                            kTmaWarps * 32 * 256 * 4);
       cudaFuncSetAttribute(k_lookup_1hot_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kTmaWarps * 32 * 256 * 4);
+      prefer_max_smem(k_lookup_1hot_tma<true>);
+      prefer_max_smem(k_lookup_1hot_tma<false>);
       attr = true;
     }
     const size_t smem = size_t(kTmaWarps) * 32 * t->dim * sizeof(float);
@@ -891,6 +810,7 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->max_keys = cfg->max_batch_keys;
   t->max_bags = cfg->max_batch_bags;
   if (const char* e = std::getenv("HPS_GPU_NO_TMA")) t->no_tma = e[0] == '1';
+  if (const char* e = std::getenv("HPS_GPU_NO_FORK")) t->no_fork = e[0] == '1';
   uint64_t rows = 0, slots = 0;
   for (uint32_t i = 0; i < t->n_tables; ++i) {
     const uint64_t cap = cfg->row_capacity_host[i];
@@ -936,9 +856,10 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->d_slot_table, t->n_slots));
   A(dalloc(&t->ws_rows_a, N));
   A(dalloc(&t->ws_rank, N));
-  A(dalloc(&t->ws_probe_tmp, N));
-  A(dalloc(&t->ws_occ_slot, N));
-  A(dalloc(&t->ws_long_slot, t->max_long));
+  t->bt_mask = next_pow2(4 * N) - 1;  // load <= 1/4: a home-slot CAS almost always settles an insert
+  A(dalloc(&t->ws_bt, t->bt_mask + 1));
+  A(dalloc(&t->ws_occ_ent, N));
+  A(dalloc(&t->ws_long_ent, t->max_long));
   A(dalloc(&t->ws_occ_bag, N));
   A(dalloc(&t->ws_bag_len, B));
   A(dalloc(&t->ws_short_rec, N));
@@ -976,7 +897,16 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   HPSG_CUDA(cudaMemsetAsync(t->d_nrows, 0, t->n_tables * sizeof(uint64_t), s));
   HPSG_CUDA(cudaMemsetAsync(t->d_defaults, 0, uint64_t(t->n_tables) * D * sizeof(float), s));
   HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, 8 * sizeof(uint64_t), s));
-  HPSG_CUDA(cudaStreamCreateWithFlags(&t->side, cudaStreamNonBlocking));
+  HPSG_CUDA(cudaMemsetAsync(t->ws_bt, 0xff, (t->bt_mask + 1) * sizeof(uint2), s));  // {kBtEmpty, UINT32_MAX}
+  {  // the dedup / long-segment side stream gets the higher priority: its short, latency-bound
+     // kernels are dispatched ahead of the bandwidth-bound main-stream CTAs they overlap
+    int lo = 0, hi = 0;
+    HPSG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    HPSG_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, hi));
+  }
+  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_bwd, cudaEventDisableTiming));
+  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_done, cudaEventDisableTiming));
+  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_join2, cudaEventDisableTiming));
   HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
   HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
   HPSG_CUDA(cudaMemsetAsync(t->ws_node_cnt, 0, bwd_max_nodes(N) * sizeof(uint32_t), s));
@@ -991,7 +921,7 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
   void* ptrs[] = {t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
-                  t->ws_probe_tmp, t->ws_occ_slot, t->ws_long_slot, t->ws_rank,      t->ws_short_rec, t->ws_short_bag,  t->ws_occ_bag,
+                  t->ws_bt,       t->ws_occ_ent,   t->ws_long_ent,  t->ws_rank,      t->ws_short_rec, t->ws_short_bag,  t->ws_occ_bag,
                   t->ws_bag_len,  t->ws_long_row,  t->ws_long_len,  t->ws_long_start, t->ws_lkey_a,
                   t->ws_lval_a,   t->ws_lkey_b,    t->ws_lval_b,    t->ws_long_base,  t->ws_task_long,
                   t->ws_partial2, t->ws_long_hbase, t->ws_node_cnt,
@@ -1002,6 +932,9 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
     if (p) cudaFree(p);
   if (t->ev_fork) cudaEventDestroy(t->ev_fork);
   if (t->ev_join) cudaEventDestroy(t->ev_join);
+  if (t->ev_bwd) cudaEventDestroy(t->ev_bwd);
+  if (t->ev_done) cudaEventDestroy(t->ev_done);
+  if (t->ev_join2) cudaEventDestroy(t->ev_join2);
   if (t->side) cudaStreamDestroy(t->side);
   delete t;
   return HPS_GPU_OK;
@@ -1172,9 +1105,11 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
     if (int s = begin_training_record(t, a, n_keys_host)) return s;
     a.occ_bag = multi ? t->ws_occ_bag : nullptr;
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
-    if (int s = record_and_fork(t, a, multi, a.mean, n_keys_host)) return s;
+    if (int s = record(t, a, multi, a.mean, n_keys_host)) return s;
   }
   if (int s = launch_lookup(t, a, multi, train)) return s;
+  if (train)
+    if (int s = fork_dedup(t)) return s;
   t->have_train = train;
   return HPS_GPU_OK;
 }
@@ -1230,7 +1165,8 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
   a.slots = t->d_slots;
   a.occ_bag = multi ? t->ws_occ_bag : nullptr;
   a.bag_len = (multi && combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
-  if (int s = record_and_fork(t, a, multi, combiner == HPS_COMBINER_MEAN, n_keys_host)) return s;
+  if (int s = record(t, a, multi, combiner == HPS_COMBINER_MEAN, n_keys_host)) return s;
+  if (int s = fork_dedup(t)) return s;
   // compaction scan: its look-back words live past the backward's zeroed region
   const uint64_t tiles = scan_tiles(std::max<uint64_t>(n_keys_host, 1));
   HPSG_CUDA(cudaMemsetAsync(t->ws_ins_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
@@ -1300,9 +1236,11 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
   a.out = rows_out;
   if (train) {
     if (int s = begin_training_record(t, a, n)) return s;
-    if (int s = record_and_fork(t, a, false, false, n)) return s;
+    if (int s = record(t, a, false, false, n)) return s;
   }
   if (int s = launch_lookup(t, a, false, train)) return s;
+  if (train)
+    if (int s = fork_dedup(t)) return s;
   t->have_train = train;
   return HPS_GPU_OK;
 }

@@ -17,7 +17,8 @@ constexpr uint32_t kChunk = 32;  // blocked reduction width
 //   [4,6)  u64 long occurrences (place-scan total)   [6,8) u64 level-1 chunks of long segments
 //   then   place-scan look-back (u64 x tiles + ticket), long-registration scan look-back,
 //          and the radix-sort words of the long-occurrence sort.
-constexpr uint32_t kLongFlag = 0x80000000u;  // slot aux after allocation: long segment id
+constexpr uint32_t kLongFlag = 0x80000000u;  // batch-table value after allocation: long segment id
+constexpr uint32_t kBtEmpty = 0xffffffffu;   // batch-table key of a free entry
 inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
 inline int bwd_long_passes(uint64_t max_keys) {
   const uint64_t m = bwd_max_long(max_keys);
@@ -26,14 +27,15 @@ inline int bwd_long_passes(uint64_t max_keys) {
   return b <= 8 ? 1 : (b + 7) / 8;
 }
 struct BwdZero {
-  size_t place, lreg, sort, total;
+  size_t place, lreg, sort, coop, total;
 };
 inline BwdZero bwd_zero_layout(uint64_t nk) {
   BwdZero z;
   z.place = 8;
   z.lreg = z.place + 2 * (scan_tiles(nk) + 1);
   z.sort = z.lreg + 2 * (scan_tiles(bwd_max_long(nk)) + 1);
-  z.total = z.sort + ((sort_ws_words(nk, bwd_long_passes(nk)) + 1) & ~size_t(1));
+  z.coop = z.sort + ((sort_ws_words(nk, bwd_long_passes(nk)) + 1) & ~size_t(1));  // 3 barriers + per-CTA counts
+  z.total = z.coop + 4 + 160;
   return z;
 }
 // Level-1 chunks of segments longer than kChunk: sum ceil(len/32) <= N/32 + N/33.
@@ -46,7 +48,7 @@ inline uint64_t bwd_max_nodes(uint64_t max_keys) { return bwd_max_chunks(max_key
 
 struct hps_gpu_table_s;
 namespace hpsg {
-int launch_dedup(hps_gpu_table_s* t);  // backward.cu: K4a-K4d on t->side
+int launch_dedup(hps_gpu_table_s* t, cudaStream_t st);  // backward.cu: K4a-K4d (on t->side)
 cudaError_t trace_attach_table(TraceRec* p);  // table.cu's copy of the trace pointer
 }
 
@@ -73,10 +75,13 @@ struct hps_gpu_table_s {
   // per-batch workspaces (sized at create, never reallocated)
   uint32_t* ws_rows_a = nullptr;  // occurrence -> global row (row_absent: key absent)
   uint32_t* ws_rank = nullptr;    // occurrence -> arrival rank within its row (forward atomics)
-  uint32_t* ws_probe_tmp = nullptr;  // occurrence -> the probe CTA's shared-hash entry
-  uint32_t* ws_occ_slot = nullptr;   // occurrence -> index slot; the slot's aux word holds the row's
-                                     // count, then its segment locator (kAuxNone at rest)
-  uint32_t* ws_long_slot = nullptr;  // long segment -> index slot
+  // Batch table: open addressing {row, value} over next_pow2(4 N) entries (L2-resident),
+  // value = UINT32_MAX + occurrences of the row in the batch, then its segment locator;
+  // every entry the backward touches is reset to {kBtEmpty, UINT32_MAX}.
+  uint2* ws_bt = nullptr;
+  uint64_t bt_mask = 0;
+  uint32_t* ws_occ_ent = nullptr;   // occurrence -> batch-table entry of its row
+  uint32_t* ws_long_ent = nullptr;  // long segment -> batch-table entry
   uint32_t* ws_occ_bag = nullptr;   // occurrence -> bag (multi-hot)
   uint32_t* ws_bag_len = nullptr;   // bag lengths (multi-hot mean)
   uint4* ws_short_rec = nullptr;    // short segments {row, first, len, 0}, CSR over ws_short_bag
@@ -109,7 +114,11 @@ struct hps_gpu_table_s {
   // by backward_update (table.cu record_and_fork).
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_bwd = nullptr, ev_join2 = nullptr;  // backward: long reduce on the side stream
+  cudaEvent_t ev_done = nullptr;  // the whole dedup (long-segment part included) is done
   bool dedup_pending = false;
+  bool no_fork = false;         // HPS_GPU_NO_FORK=1: everything on the main stream (A/B measurement)
+  bool dedup_deferred = false;  // no_fork: the dedup runs at backward_update
   bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)
   int last_combiner = 0;
   uint64_t last_n_keys_host = 0;  // exact when known on the host, else max_keys

@@ -334,3 +334,48 @@ def test_keys_only_insert_matches_oracle(ctx):
     n = g.size(0)
     np.testing.assert_array_equal(g.row_keys(0, 0, n).cpu().numpy().view(np.uint64), o.row_keys(0, 0, n))
     np.testing.assert_array_equal(g.export(0, 0, n)[0].cpu().numpy().view(np.uint32), o.export(0, 0, n)[0].view(np.uint32))
+
+
+def _bt_used(ctx, g):
+    import ctypes
+    v = ctypes.c_uint64(0)
+    assert ctx.lib.hps_gpu_debug_batch_table_used(g.h, ctypes.byref(v)) == 0
+    return v.value
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_batch_table_self_cleaning(ctx, multi):
+    """The per-batch dedup table returns to empty after every backward, after a training
+    lookup whose backward never came (reset by the next record), over many steps with
+    skewed keys (long segments, hot rows shared by every counting CTA)."""
+    rs = np.random.default_rng(21)
+    caps = [3, 50, 20000]
+    g, o = make_pair(ctx, caps, 32, [0, 1, 2, 2], optimizer="adagrad")
+    pools = []
+    for t, c in enumerate(caps):
+        ks = rs.integers(0, 2**63, c).astype(np.uint64)
+        g.insert(t, t64(ks))
+        o.insert(t, ks)
+        pools.append(ks)
+    B = 3000
+    for step in range(6):
+        if multi:
+            lens = rs.integers(0, 6, B * 4).astype(np.uint32)
+            offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+            keys = np.concatenate([rs.choice(pools[[0, 1, 2, 2][b % 4]], l) for b, l in enumerate(lens)]).astype(np.uint64)
+            ot = torch.from_numpy(offs.view(np.int32)).cuda()
+        else:
+            keys = np.stack([rs.choice(pools[s], B) for s in [0, 1, 2, 2]], 1).ravel()
+            offs, ot = None, None
+        out = g.lookup(t64(keys), B, offsets=ot, train=True)
+        ref = o.lookup(keys, B, offsets=offs, train=True)
+        assert np.array_equal(out.cpu().numpy(), ref)
+        if step == 2:
+            continue  # no backward: the next record must clean up
+        d = rs.standard_normal(ref.shape).astype(np.float32)
+        p = opt_params("adagrad", 0.05)
+        g.backward_update(torch.from_numpy(d).cuda(), 0.05, params=p)
+        o.backward_update(d, p)
+        assert _bt_used(ctx, g) == 0
+    for t, c in enumerate(caps):
+        assert close(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])
