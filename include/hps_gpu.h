@@ -175,7 +175,7 @@ int hps_gpu_table_last_unique(hps_gpu_table tbl, uint64_t* count_out, uint32_t* 
  * 32 x {first CTA start, last warp end} (u64 pairs; start = UINT64_MAX: not run) into
  * trace_host and re-arms, 0 detaches. Ids: 0 probe, 1 pool, 2 segment alloc, 3 place,
  * 4 long-sort histogram, 5..8 long-sort passes, 9 long registration, 10 short reduce,
- * 11 long reduce, 12 counter reset, 13 counts. Synchronises the device; not for hot paths. */
+ * 11 long reduce, 12 counter reset, 13 counts (14, 15: end of its local / global phase). Synchronises the device; not for hot paths. */
 int hps_gpu_debug_trace(int mode, uint64_t* trace_host);
 
 /* Invariant check for tests: entries of the table's per-batch dedup table still in use

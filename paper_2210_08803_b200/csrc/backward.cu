@@ -30,7 +30,9 @@
 //                     whose sum goes through the optimizer (hierarchical last-arriver)
 // Every batch-table entry is reset to empty by the kernel that consumes it last.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "primitives.cuh"
@@ -85,14 +87,34 @@ struct BwdArgs {
 __device__ __forceinline__ uint32_t bt_home(uint32_t row, uint64_t mask) {
   return static_cast<uint32_t>(((uint64_t(row) * 0x9E3779B97F4A7C15ull) >> 32) & mask);
 }
-// Entry of `row` (inserted if absent); one CAS in the common case.
-__device__ __forceinline__ uint32_t bt_insert(uint2* bt, uint64_t mask, uint32_t row) {
-  uint32_t h = bt_home(row, mask);
+// Entry of `row` (inserted if absent), probing from `h`: each round reads a window of 4
+// keys at once and CASes only the first free one, so a collision chain costs a quarter of
+// the dependent round trips of slot-by-slot probing.
+__device__ __forceinline__ uint32_t bt_insert_from(uint2* bt, uint64_t mask, uint32_t row, uint32_t h) {
   while (true) {
-    const uint32_t old = atomicCAS(&bt[h].x, kBtEmpty, row);
-    if (old == kBtEmpty || old == row) return h;
-    h = static_cast<uint32_t>((h + 1) & mask);
+    uint32_t k[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) k[s] = __ldcg(&bt[(h + s) & mask].x);
+    int free_s = -1;
+#pragma unroll
+    for (int s = 3; s >= 0; --s) {
+      if (k[s] == row) return static_cast<uint32_t>((h + s) & mask);
+      if (k[s] == kBtEmpty) free_s = s;
+    }
+    if (free_s < 0) {
+      h = static_cast<uint32_t>((h + 4) & mask);
+      continue;
+    }
+    // a key equal to `row` cannot sit after the first free slot of the window (entries are
+    // never removed while a batch is being counted), so the free slot is where it belongs
+    const uint32_t slot = static_cast<uint32_t>((h + free_s) & mask);
+    const uint32_t old = atomicCAS(&bt[slot].x, kBtEmpty, row);
+    if (old == kBtEmpty || old == row) return slot;
+    h = slot;  // raced: re-read from this slot
   }
+}
+__device__ __forceinline__ uint32_t bt_insert(uint2* bt, uint64_t mask, uint32_t row) {
+  return bt_insert_from(bt, mask, row, bt_home(row, mask));
 }
 
 // ---- K4a-c fused: counts, allocation, placement in ONE persistent cooperative kernel ------
@@ -125,36 +147,55 @@ __device__ __forceinline__ uint32_t smem_hash_slot(uint32_t* s_key, uint32_t row
   return kNoEnt;
 }
 
+// Every pass walks the chunk in batches of kDedupIPT items per thread whose loads are all
+// issued before any is consumed (these phases are latency-bound, not bandwidth-bound).
+constexpr int kDedupIPT = 8;
+
 __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* coop) {
   extern __shared__ uint32_t s_dd[];
   uint32_t* s_key = s_dd;               // row, then its batch-table entry
   uint32_t* s_val = s_dd + kDedupHash;  // chunk count, then the CTA's base rank
   __shared__ unsigned long long s_scr[33];
-  __shared__ unsigned long long s_base;
+  __shared__ unsigned long long s_cursor;
   __shared__ uint32_t s_scr32[33];
   trace_begin(kTrCount);
   const uint64_t n = a.counts[0];
   const uint64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
   const uint32_t lane = lane_id(), lt = lanemask_lt();
+  constexpr uint64_t kBatch = uint64_t(kDedupBlock) * kDedupIPT;
   // ---- P1: counts and ranks
   for (int e = threadIdx.x; e < kDedupHash; e += kDedupBlock) {
     s_key[e] = kBtEmpty;
     s_val[e] = 0u;
   }
   __syncthreads();
-  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
-    const uint32_t row = a.occ_row[i];
-    if (row == a.row_absent) continue;
-    const uint32_t h = smem_hash_slot(s_key, row);
-    if (h != kNoEnt) {
-      a.occ_rank[i] = atomicAdd(&s_val[h], 1u);
-      a.occ_ent[i] = h;
-    } else {  // shared hash full: count directly
-      const uint32_t e = bt_insert(a.bt, a.bt_mask, row);
-      a.occ_rank[i] = atomicAdd(&a.bt[e].y, 1u) + 1u;
-      a.occ_ent[i] = kDirectEnt | e;
+  for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
+    uint32_t row[kDedupIPT];
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      row[k] = i < c1 ? a.occ_row[i] : a.row_absent;
+    }
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k)  // the rows' batch-table home lines into L2 now: the
+      if (row[k] != a.row_absent)        // reservations below then hit L2
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(&a.bt[bt_home(row[k], a.bt_mask)]));
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      if (row[k] == a.row_absent) continue;
+      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      const uint32_t h = smem_hash_slot(s_key, row[k]);
+      if (h != kNoEnt) {
+        a.occ_rank[i] = atomicAdd(&s_val[h], 1u);
+        a.occ_ent[i] = h;
+      } else {  // shared hash full: count directly
+        const uint32_t e = bt_insert(a.bt, a.bt_mask, row[k]);
+        a.occ_rank[i] = atomicAdd(&a.bt[e].y, 1u) + 1u;
+        a.occ_ent[i] = kDirectEnt | e;
+      }
     }
   }
+  trace_end(kTrCountLocal);
   __syncthreads();
   {  // one reservation per distinct row: every home-slot CAS in flight at once, the (rare,
      // sparse table) collisions resolved after, then every add in flight at once
@@ -170,74 +211,103 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
       res[q] = ent[q] != kNoEnt ? atomicCAS(&a.bt[ent[q]].x, kBtEmpty, key[q]) : kBtEmpty;
 #pragma unroll
     for (int q = 0; q < kPer; ++q)
-      if (ent[q] != kNoEnt && res[q] != kBtEmpty && res[q] != key[q]) ent[q] = bt_insert(a.bt, a.bt_mask, key[q]);
+      if (ent[q] != kNoEnt && res[q] != kBtEmpty && res[q] != key[q])
+        ent[q] = bt_insert_from(a.bt, a.bt_mask, key[q], static_cast<uint32_t>((ent[q] + 1) & a.bt_mask));
 #pragma unroll
     for (int q = 0; q < kPer; ++q)
       res[q] = ent[q] != kNoEnt ? atomicAdd(&a.bt[ent[q]].y, s_val[threadIdx.x + kDedupBlock * q]) + 1u : 0u;
+
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {  // entry e is owned by this thread: no hazard with other threads
       s_key[threadIdx.x + kDedupBlock * q] = ent[q];
       s_val[threadIdx.x + kDedupBlock * q] = res[q];
     }
   }
+  trace_end(kTrCountGlobal);
   __syncthreads();
-  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
-    if (a.occ_row[i] == a.row_absent) continue;
-    const uint32_t h = a.occ_ent[i];
-    if (h & kDirectEnt) {
-      a.occ_ent[i] = h & ~kDirectEnt;
-    } else {
-      a.occ_rank[i] += s_val[h];
-      a.occ_ent[i] = s_key[h];
+  for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
+    uint32_t h[kDedupIPT];
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      h[k] = (i < c1 && a.occ_row[i] != a.row_absent) ? a.occ_ent[i] : kNoEnt;
+    }
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      if (h[k] == kNoEnt) continue;
+      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      if (h[k] & kDirectEnt) {
+        a.occ_ent[i] = h[k] & ~kDirectEnt;
+      } else {
+        a.occ_rank[i] += s_val[h[k]];
+        a.occ_ent[i] = s_key[h[k]];
+      }
     }
   }
   trace_end(kTrCount);
   grid_barrier_once(coop + 0);
-  // ---- P2: allocation
+  // ---- P2: allocation. Short leaders: the CTA reserves its CSR range with one packed
+  // atomic, then hands it out in item order (block scans), so segment s+1 starts where
+  // segment s ends. Long leaders: ids from a warp-aggregated counter.
   trace_begin(kTrAlloc);
   unsigned long long mine = 0;
-  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
-    if (a.occ_row[i] == a.row_absent || a.occ_rank[i] != 0u) continue;
-    const uint32_t len = __ldcg(&a.bt[a.occ_ent[i]].y) + 1u;
-    if (len <= kChunk) mine += (1ull << 32) | len;
+  for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
+    uint32_t ent[kDedupIPT], len[kDedupIPT];
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      ent[k] = (i < c1 && a.occ_row[i] != a.row_absent && a.occ_rank[i] == 0u) ? a.occ_ent[i] : kNoEnt;
+    }
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) len[k] = ent[k] != kNoEnt ? __ldcg(&a.bt[ent[k]].y) + 1u : 0u;
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k)
+      if (len[k] && len[k] <= kChunk) mine += (1ull << 32) | len[k];
   }
   unsigned long long total;
   (void)block_excl_scan<kDedupBlock>(mine, s_scr, &total);
-  if (threadIdx.x == 0) s_base = total ? atomicAdd(a.short_alloc, total) : 0ull;
+  if (threadIdx.x == 0) s_cursor = total ? atomicAdd(a.short_alloc, total) : 0ull;
   __syncthreads();
-  unsigned long long run = s_base;
-  for (uint64_t t0 = c0; t0 < c1; t0 += kDedupBlock) {  // tiles in order, one item per thread
-    const uint64_t i = t0 + threadIdx.x;
-    uint32_t row = 0, len = 0, ent = 0;
-    if (i < c1) {
-      const uint32_t r = a.occ_row[i];
-      if (r != a.row_absent && a.occ_rank[i] == 0u) {
-        row = r;
-        ent = a.occ_ent[i];
-        len = __ldcg(&a.bt[ent].y) + 1u;
-      }
+  unsigned long long run = s_cursor;
+  for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {  // each thread's items contiguous; block scan
+    uint32_t ent[kDedupIPT], len[kDedupIPT];
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      const uint64_t i = b0 + uint64_t(threadIdx.x) * kDedupIPT + k;
+      ent[k] = (i < c1 && a.occ_row[i] != a.row_absent && a.occ_rank[i] == 0u) ? a.occ_ent[i] : kNoEnt;
     }
-    const bool sh = len && len <= kChunk, lg = len > kChunk;
+    unsigned long long tmine = 0;
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      len[k] = ent[k] != kNoEnt ? __ldcg(&a.bt[ent[k]].y) + 1u : 0u;
+      if (len[k] && len[k] <= kChunk) tmine += (1ull << 32) | len[k];
+    }
     unsigned long long ttotal;
-    const unsigned long long pos = run + block_excl_scan<kDedupBlock>(sh ? (1ull << 32) | len : 0ull, s_scr, &ttotal);
+    unsigned long long pos = run + block_excl_scan<kDedupBlock>(tmine, s_scr, &ttotal);
     run += ttotal;
-    if (sh) {
-      const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
-      a.short_rec[seg] = make_uint4(row, first, len, ent);
-      a.bt[ent].y = first;
-    }
-    const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
-    if (lg_mask) {
-      const int src = __ffs(lg_mask) - 1;
-      uint32_t j0 = 0;
-      if (static_cast<int>(lane) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
-      j0 = __shfl_sync(0xffffffffu, j0, src);
-      if (lg) {
-        const uint32_t j = j0 + __popc(lg_mask & lt);
-        a.long_row[j] = row;
-        a.long_ent[j] = ent;
-        a.long_len[j] = len;
-        a.bt[ent].y = kLongFlag | j;
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      const uint64_t i = b0 + uint64_t(threadIdx.x) * kDedupIPT + k;
+      const bool sh = len[k] && len[k] <= kChunk, lg = len[k] > kChunk;
+      if (sh) {
+        const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
+        a.short_rec[seg] = make_uint4(a.occ_row[i], first, len[k], ent[k]);
+        a.bt[ent[k]].y = first;
+        pos += (1ull << 32) | len[k];
+      }
+      const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
+      if (lg_mask) {
+        const int src = __ffs(lg_mask) - 1;
+        uint32_t j0 = 0;
+        if (static_cast<int>(lane) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
+        j0 = __shfl_sync(0xffffffffu, j0, src);
+        if (lg) {
+          const uint32_t j = j0 + __popc(lg_mask & lt);
+          a.long_row[j] = a.occ_row[i];
+          a.long_ent[j] = ent[k];
+          a.long_len[j] = len[k];
+          a.bt[ent[k]].y = kLongFlag | j;
+        }
       }
     }
   }
@@ -246,14 +316,24 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
   // ---- P3: placement
   trace_begin(kTrPlace);
   uint32_t my_long = 0;
-  for (uint64_t i = c0 + threadIdx.x; i < c1; i += kDedupBlock) {
-    const uint32_t r = a.occ_row[i];
-    if (r == a.row_absent) continue;
-    const uint32_t loc = __ldcg(&a.bt[a.occ_ent[i]].y);
-    if (loc & kLongFlag) {
-      ++my_long;
-    } else {
-      a.short_bag[loc + a.occ_rank[i]] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+  for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
+    uint32_t ent[kDedupIPT], loc[kDedupIPT];
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      ent[k] = (i < c1 && a.occ_row[i] != a.row_absent) ? a.occ_ent[i] : kNoEnt;
+    }
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) loc[k] = ent[k] != kNoEnt ? __ldcg(&a.bt[ent[k]].y) : 0u;
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      if (ent[k] == kNoEnt) continue;
+      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      if (loc[k] & kLongFlag) {
+        ++my_long;
+      } else {
+        a.short_bag[loc[k] + a.occ_rank[i]] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+      }
     }
   }
   uint32_t cta_long;
@@ -265,20 +345,27 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
   uint32_t lbase;
   (void)block_excl_scan<kDedupBlock>(before, s_scr32, &lbase);
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *a.long_occ = lbase + cta_long;
-  if (cta_long) {
-    for (uint64_t t0 = c0; t0 < c1; t0 += kDedupBlock) {  // canonical order: tiles in order
-      const uint64_t i = t0 + threadIdx.x;
-      uint32_t loc = 0;
-      bool lg = false;
-      if (i < c1 && a.occ_row[i] != a.row_absent) {
-        loc = __ldcg(&a.bt[a.occ_ent[i]].y);
-        lg = (loc & kLongFlag) != 0;
+  if (cta_long) {  // canonical order: batches in order, each thread's kDedupIPT items contiguous
+    for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
+      uint32_t loc[kDedupIPT];
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k) {
+        const uint64_t i = b0 + uint64_t(threadIdx.x) * kDedupIPT + k;
+        const uint32_t e = (i < c1 && a.occ_row[i] != a.row_absent) ? a.occ_ent[i] : kNoEnt;
+        loc[k] = e != kNoEnt ? __ldcg(&a.bt[e].y) : 0u;
       }
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k) cnt += (loc[k] & kLongFlag) ? 1u : 0u;
       uint32_t ttotal;
-      const uint32_t excl = block_excl_scan<kDedupBlock>(lg ? 1u : 0u, s_scr32, &ttotal);
-      if (lg) {
-        a.lkey[lbase + excl] = loc & ~kLongFlag;
-        a.lval[lbase + excl] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+      uint32_t pos = lbase + block_excl_scan<kDedupBlock>(cnt, s_scr32, &ttotal);
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k) {
+        if (!(loc[k] & kLongFlag)) continue;
+        const uint64_t i = b0 + uint64_t(threadIdx.x) * kDedupIPT + k;
+        a.lkey[pos] = loc[k] & ~kLongFlag;
+        a.lval[pos] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+        ++pos;
       }
       lbase += ttotal;
     }
@@ -1053,6 +1140,7 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   int grid = 0;
   if (tma) {
     a.tma_rows = 40;  // 2 CTAs/SM with room for the long-segment chain's kernels beside them
+    if (const char* e = std::getenv("HPS_GPU_TMA_ROWS")) a.tma_rows = std::max(36, std::atoi(e));  // A/B knob
     smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float) + size_t(kRedWarps) * kBagStage * 4;
     grid = static_cast<int>(
         std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * 4)));
@@ -1146,13 +1234,13 @@ int hps_gpu_apply_grads(hps_gpu_table t, const float* grads, const uint32_t* tou
 // 0: detach. Synchronises the device.
 int hps_gpu_debug_trace(int mode, uint64_t* trace_host) {
   static TraceRec* buf = nullptr;
+  constexpr size_t kRecs = size_t(kTraceSlots) * kTraceSMs;
   auto arm = [&]() -> cudaError_t {
-    TraceRec init[kTraceSlots];
-    for (auto& r : init) r = TraceRec{~0ull, 0ull};
-    return cudaMemcpy(buf, init, sizeof(init), cudaMemcpyHostToDevice);
+    std::vector<TraceRec> init(kRecs, TraceRec{~0ull, 0ull});
+    return cudaMemcpy(buf, init.data(), kRecs * sizeof(TraceRec), cudaMemcpyHostToDevice);
   };
   if (mode == 1) {
-    if (!buf) HPSG_CUDA(cudaMalloc(&buf, kTraceSlots * sizeof(TraceRec)));
+    if (!buf) HPSG_CUDA(cudaMalloc(&buf, kRecs * sizeof(TraceRec)));
     HPSG_CUDA(arm());
     HPSG_CUDA(trace_attach_tu(buf));
     HPSG_CUDA(hpsg::trace_attach_table(buf));
@@ -1161,7 +1249,17 @@ int hps_gpu_debug_trace(int mode, uint64_t* trace_host) {
   if (mode == 2) {
     if (!buf || !trace_host) return HPS_GPU_E_INVALID_ARGUMENT;
     HPSG_CUDA(cudaDeviceSynchronize());
-    HPSG_CUDA(cudaMemcpy(trace_host, buf, kTraceSlots * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+    std::vector<TraceRec> per_sm(kRecs);
+    HPSG_CUDA(cudaMemcpy(per_sm.data(), buf, kRecs * sizeof(TraceRec), cudaMemcpyDeviceToHost));
+    for (int id = 0; id < kTraceSlots; ++id) {
+      TraceRec r{~0ull, 0ull};
+      for (int m = 0; m < kTraceSMs; ++m) {
+        r.start = std::min(r.start, per_sm[size_t(id) * kTraceSMs + m].start);
+        r.end = std::max(r.end, per_sm[size_t(id) * kTraceSMs + m].end);
+      }
+      trace_host[2 * id] = r.start;
+      trace_host[2 * id + 1] = r.end;
+    }
     HPSG_CUDA(arm());
     return HPS_GPU_OK;
   }

@@ -135,6 +135,21 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
                "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// Same, with an L2 eviction-priority hint (createpolicy): rows read once per step stream
+// through L2 as evict_first so they do not displace the step's small hot working sets.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_s2g(void* gdst, const void* smem_src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
                "r"(bytes)
@@ -230,7 +245,7 @@ struct TraceRec {
 constexpr int kTraceSlots = 32;
 enum TraceId : int {
   kTrProbe = 0, kTrPool = 1, kTrAlloc = 2, kTrPlace = 3, kTrHist = 4, kTrPass0 = 5, kTrLongReg = 9,
-  kTrReduce = 10, kTrLong = 11, kTrReset = 12, kTrCount = 13
+  kTrReduce = 10, kTrLong = 11, kTrReset = 12, kTrCount = 13, kTrCountLocal = 14, kTrCountGlobal = 15
 };
 static __device__ TraceRec* g_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -238,16 +253,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// Records are per (id, SM) so the stamps of thousands of warps never pile onto one L2
+// address (that serialisation would distort the kernels being traced); the host reduces.
+constexpr int kTraceSMs = 160;
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 __device__ __forceinline__ void trace_begin(int id) {
   if (id >= 0 && threadIdx.x == 0) {
     TraceRec* t = g_trace;
-    if (t) atomicMin(&t[id].start, gtimer());
+    if (t) atomicMin(&t[id * kTraceSMs + (sm_id() % kTraceSMs)].start, gtimer());
   }
 }
 __device__ __forceinline__ void trace_end(int id) {
   if (id >= 0 && (threadIdx.x & 31) == 0) {
     TraceRec* t = g_trace;
-    if (t) atomicMax(&t[id].end, gtimer());
+    if (t) atomicMax(&t[id * kTraceSMs + (sm_id() % kTraceSMs)].end, gtimer());
   }
 }
 inline cudaError_t trace_attach_tu(TraceRec* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }

@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a
   const uint64_t warp = uint64_t(blockIdx.x) * kTmaWarps + w;
   const uint64_t n_warps = uint64_t(gridDim.x) * kTmaWarps;
   trace_begin(ROWS ? kTrPool : -1);
+  const uint64_t policy = l2_policy_evict_first();  // training: keep the dedup's lines in L2
   for (uint64_t t0 = warp * 32; t0 < a.n_bags; t0 += n_warps * 32) {
     const uint64_t bag = t0 + lane;
     const uint32_t nb = static_cast<uint32_t>(min(uint64_t(32), a.n_bags - t0));
@@ -442,7 +443,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a
     __syncwarp();
     if (lane == 0) mbar_arrive_expect_tx(&s_bar[w], nb * row_bytes);
     __syncwarp();
-    if (bag < a.n_bags) bulk_g2s(tile + lane * D, src, row_bytes, &s_bar[w]);
+    if (bag < a.n_bags) {
+      if (ROWS) bulk_g2s_hint(tile + lane * D, src, row_bytes, &s_bar[w], policy);
+      else bulk_g2s(tile + lane * D, src, row_bytes, &s_bar[w]);
+    }
     mbar_wait(&s_bar[w], phase);
     phase ^= 1;
     float4* t4 = reinterpret_cast<float4*>(tile);
@@ -856,7 +860,8 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->d_slot_table, t->n_slots));
   A(dalloc(&t->ws_rows_a, N));
   A(dalloc(&t->ws_rank, N));
-  t->bt_mask = next_pow2(4 * N) - 1;  // load <= 1/4: a home-slot CAS almost always settles an insert
+  // load <= 1/8 (<= 2^25 entries): a home-slot CAS almost always settles an insert
+  t->bt_mask = std::min<uint64_t>(next_pow2(8 * N), 1ull << 25) - 1;
   A(dalloc(&t->ws_bt, t->bt_mask + 1));
   A(dalloc(&t->ws_occ_ent, N));
   A(dalloc(&t->ws_long_ent, t->max_long));

@@ -75,7 +75,7 @@ struct hps_gpu_table_s {
   // per-batch workspaces (sized at create, never reallocated)
   uint32_t* ws_rows_a = nullptr;  // occurrence -> global row (row_absent: key absent)
   uint32_t* ws_rank = nullptr;    // occurrence -> arrival rank within its row (forward atomics)
-  // Batch table: open addressing {row, value} over next_pow2(4 N) entries (L2-resident),
+  // Batch table: open addressing {row, value} over next_pow2(8 N) entries (L2-resident),
   // value = UINT32_MAX + occurrences of the row in the batch, then its segment locator;
   // every entry the backward touches is reset to {kBtEmpty, UINT32_MAX}.
   uint2* ws_bt = nullptr;

@@ -24,6 +24,13 @@ def _owned_keys(ctx: Context, cfg: W.Config, t: int, rank: int, world: int, firs
     return keys
 
 
+def long_sort_passes(max_keys: int) -> int:
+    """Radix passes of the long-segment list sort (table_internal.cuh bwd_long_passes)."""
+    m = max_keys // 33 + 2
+    b = m.bit_length()
+    return 1 if b <= 8 else (b + 7) // 8
+
+
 def table_max_keys(cfg: W.Config, world: int) -> int:
     """Key occurrences one rank may have to hold in a step (an owner can receive every
     rank's keys in the worst case)."""
@@ -155,8 +162,10 @@ class TrainStep:
         self.insert_missing = bool(cfg.keyspace)
         self.graph_mode = bool(use_graph and world == 1 and cfg.optimizer != "adam")
         self._graphs = {}
-        # lookup + dedup scan + scatter + short reduce + long sort/chunks/combine
-        self.kernels_per_step = 7
+        # training record + dedup (backward.cu launch_dedup): probe, dedup, long-list histogram,
+        # its radix passes, long registration, long tasks; backward: short + long reduce
+        rec = 5 + long_sort_passes(table_max_keys(cfg, 1))
+        self.kernels_per_step = rec + 1 + 2  # + pooling
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self._cnt_host = torch.zeros(1, dtype=torch.int64).pin_memory()
         self.exchange = None
@@ -165,25 +174,25 @@ class TrainStep:
             self.engine = LocalizedGpuEngine(ctx, table, cfg.n_slots, owned, cfg.batch, table_max_keys(cfg, 1), cfg.dim)
             self.exchange = LocalizedExchange(self.engine, cfg.combiner, rank, world, cfg.n_slots, owned)
             multi = cfg.hot > 1
-            # regroup (lengths + scan + keys) per owner [+ owner offsets] + lookup + place per owner
-            # + place(1) per owner + backward (hist + passes + scan + 3 reduce kernels)
-            self.kernels_per_step = 3 * world + (1 if multi else 0) + 1 + 2 * world + 7
+            # regroup (lengths + scan + keys) per owner [+ owner offsets] + training lookup
+            # (record + dedup + pooling) + place per owner + place(1) per owner + backward (2)
+            self.kernels_per_step = 3 * world + (1 if multi else 0) + rec + 1 + 2 * world + 2
         elif multi and hybrid_hot is not None:
             from .exchange import GpuEngine, HybridExchange, HybridGpuEngine
             cold_engine = GpuEngine(ctx, table, cfg.slots(), table_max_keys(cfg, 1), world)
             self.engine = HybridGpuEngine(ctx, hybrid_hot, cold_engine, table_max_keys(cfg, 1))
             self.exchange = HybridExchange(self.engine, cfg.combiner, rank, world, cfg.n_slots)
-            # probe + scan + bucketize(5) + gather + pool + cold grads + cold backward(7)
-            # + reduce(7) + sum_partials + apply
-            self.kernels_per_step = 2 + 5 + 1 + 1 + 1 + 7 + 7 + 2
+            # hot record + dedup + cold scan + bucketize(5) + cold gather (record + dedup + pooling)
+            # + pool + cold grads + cold backward(2) + hot reduce(2) + sum_partials + apply
+            self.kernels_per_step = rec + 1 + 5 + rec + 1 + 1 + 1 + 2 + 2 + 2
         elif multi:
             from .exchange import DistributedExchange, GpuEngine
             max_keys = table_max_keys(cfg, 1)
             self.engine = GpuEngine(ctx, table, cfg.slots(), max_keys, world, insert_missing=self.insert_missing)
             self.exchange = DistributedExchange(self.engine, cfg.combiner, rank, world)
-            # bucketize (owner + hist + 1 radix pass + pack + counts) + gather + pool
-            # + scatter + backward (hist + passes + scan + 3 reduce kernels) [+ occ_bags]
-            self.kernels_per_step = 5 + 1 + 1 + 1 + 7 + (1 if cfg.hot > 1 else 0)
+            # bucketize (owner + hist + 1 radix pass + pack + counts) + owner gather (record +
+            # dedup + pooling) + pool + scatter + backward (2) [+ occ_bags]
+            self.kernels_per_step = 5 + rec + 1 + 1 + 1 + 2 + (1 if cfg.hot > 1 else 0)
         if self.insert_missing:  # claim + scan + commit + finish
             self.kernels_per_step += 4
 

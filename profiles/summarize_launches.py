@@ -20,8 +20,12 @@ def load(path):
     return out
 
 
+SETUP = ("k_insert", "k_fill_slots", "k_gen_keys", "k_scan<InsertScanOp>", "k_rows_non_finite")
+
+
 def main(path, last=None):
-    data = load(path)
+    """Per-kernel share of the step: table setup (bulk inserts, key generation) excluded."""
+    data = [d for d in load(path) if not d[0].startswith(SETUP)]
     if last:
         data = data[-last:]
     agg = collections.OrderedDict()
