@@ -46,6 +46,7 @@ struct BwdArgs {
   const uint64_t* counts;   // [0] = N occurrences; [1] <- unique rows (short + long segments)
   const uint32_t* occ_row;  // row of each occurrence (row_absent: no gradient)
   uint32_t* occ_rank;       // arrival rank of each occurrence within its row
+  uint32_t* lead;           // k_dedup: per-CTA compact list of its leaders (rank-0 occurrences)
   const uint32_t* occ_bag;  // multi-hot: bag of each occurrence (nullptr: occurrence i is bag i)
   uint32_t* occ_ent;        // batch-table entry of each occurrence's row
   uint2* bt;                // batch table {row, UINT32_MAX + count -> segment locator}
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
   __shared__ unsigned long long s_scr[33];
   __shared__ unsigned long long s_cursor;
   __shared__ uint32_t s_scr32[33];
+  __shared__ uint32_t s_nlead;
   trace_begin(kTrCount);
   const uint64_t n = a.counts[0];
   const uint64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
@@ -224,23 +226,36 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
     }
   }
   trace_end(kTrCountGlobal);
+  if (threadIdx.x == 0) s_nlead = 0;
   __syncthreads();
+  // final ranks and entries; the rank-0 occurrences (leaders) go to the CTA's leader list
   for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
-    uint32_t h[kDedupIPT];
+    uint32_t h[kDedupIPT], r[kDedupIPT];
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
       const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
       h[k] = (i < c1 && a.occ_row[i] != a.row_absent) ? a.occ_ent[i] : kNoEnt;
+      r[k] = h[k] != kNoEnt ? a.occ_rank[i] : 1u;
     }
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      if (h[k] == kNoEnt) continue;
       const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
-      if (h[k] & kDirectEnt) {
-        a.occ_ent[i] = h[k] & ~kDirectEnt;
-      } else {
-        a.occ_rank[i] += s_val[h[k]];
-        a.occ_ent[i] = s_key[h[k]];
+      if (h[k] != kNoEnt) {
+        if (h[k] & kDirectEnt) {
+          a.occ_ent[i] = h[k] & ~kDirectEnt;
+        } else {
+          r[k] += s_val[h[k]];
+          a.occ_rank[i] = r[k];
+          a.occ_ent[i] = s_key[h[k]];
+        }
+      }
+      const bool is_lead = h[k] != kNoEnt && r[k] == 0u;
+      const uint32_t m = __ballot_sync(0xffffffffu, is_lead);
+      if (m) {
+        uint32_t base = 0;
+        if (lane == static_cast<uint32_t>(__ffs(m) - 1)) base = atomicAdd(&s_nlead, static_cast<uint32_t>(__popc(m)));
+        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+        if (is_lead) a.lead[c0 + base + __popc(m & lt)] = static_cast<uint32_t>(i);
       }
     }
   }
@@ -250,16 +265,17 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
   // atomic, then hands it out in item order (block scans), so segment s+1 starts where
   // segment s ends. Long leaders: ids from a warp-aggregated counter.
   trace_begin(kTrAlloc);
+  __syncthreads();
+  const uint32_t nlead = s_nlead;  // (the CTA's own list: written before the grid barrier)
+  const uint32_t* lead = a.lead + c0;
   unsigned long long mine = 0;
-  for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
-    uint32_t ent[kDedupIPT], len[kDedupIPT];
+  for (uint32_t b0 = 0; b0 < nlead; b0 += kBatch) {
+    uint32_t len[kDedupIPT];
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
-      ent[k] = (i < c1 && a.occ_row[i] != a.row_absent && a.occ_rank[i] == 0u) ? a.occ_ent[i] : kNoEnt;
+      const uint32_t q = b0 + k * kDedupBlock + threadIdx.x;
+      len[k] = q < nlead ? __ldcg(&a.bt[a.occ_ent[lead[q]]].y) + 1u : 0u;
     }
-#pragma unroll
-    for (int k = 0; k < kDedupIPT; ++k) len[k] = ent[k] != kNoEnt ? __ldcg(&a.bt[ent[k]].y) + 1u : 0u;
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k)
       if (len[k] && len[k] <= kChunk) mine += (1ull << 32) | len[k];
@@ -269,12 +285,13 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
   if (threadIdx.x == 0) s_cursor = total ? atomicAdd(a.short_alloc, total) : 0ull;
   __syncthreads();
   unsigned long long run = s_cursor;
-  for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {  // each thread's items contiguous; block scan
-    uint32_t ent[kDedupIPT], len[kDedupIPT];
+  for (uint32_t b0 = 0; b0 < nlead; b0 += kBatch) {  // each thread's leaders contiguous; block scan
+    uint32_t ent[kDedupIPT], len[kDedupIPT], occ[kDedupIPT];
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      const uint64_t i = b0 + uint64_t(threadIdx.x) * kDedupIPT + k;
-      ent[k] = (i < c1 && a.occ_row[i] != a.row_absent && a.occ_rank[i] == 0u) ? a.occ_ent[i] : kNoEnt;
+      const uint32_t q = b0 + threadIdx.x * kDedupIPT + k;
+      occ[k] = q < nlead ? lead[q] : 0u;
+      ent[k] = q < nlead ? a.occ_ent[occ[k]] : kNoEnt;
     }
     unsigned long long tmine = 0;
 #pragma unroll
@@ -287,11 +304,10 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
     run += ttotal;
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      const uint64_t i = b0 + uint64_t(threadIdx.x) * kDedupIPT + k;
       const bool sh = len[k] && len[k] <= kChunk, lg = len[k] > kChunk;
       if (sh) {
         const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
-        a.short_rec[seg] = make_uint4(a.occ_row[i], first, len[k], ent[k]);
+        a.short_rec[seg] = make_uint4(a.occ_row[occ[k]], first, len[k], ent[k]);
         a.bt[ent[k]].y = first;
         pos += (1ull << 32) | len[k];
       }
@@ -303,7 +319,7 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
         j0 = __shfl_sync(0xffffffffu, j0, src);
         if (lg) {
           const uint32_t j = j0 + __popc(lg_mask & lt);
-          a.long_row[j] = a.occ_row[i];
+          a.long_row[j] = a.occ_row[occ[k]];
           a.long_ent[j] = ent[k];
           a.long_len[j] = len[k];
           a.bt[ent[k]].y = kLongFlag | j;
@@ -999,6 +1015,7 @@ BwdArgs base_args(hps_gpu_table t) {
   a.counts = t->ws_counts;
   a.occ_row = t->ws_rows_a;
   a.occ_rank = t->ws_rank;
+  a.lead = t->ws_lead;
   a.occ_bag = t->last_multi ? t->ws_occ_bag : nullptr;
   a.occ_ent = t->ws_occ_ent;
   a.bt = t->ws_bt;

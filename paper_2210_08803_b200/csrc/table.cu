@@ -864,6 +864,7 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->bt_mask = std::min<uint64_t>(next_pow2(8 * N), 1ull << 25) - 1;
   A(dalloc(&t->ws_bt, t->bt_mask + 1));
   A(dalloc(&t->ws_occ_ent, N));
+  A(dalloc(&t->ws_lead, N));
   A(dalloc(&t->ws_long_ent, t->max_long));
   A(dalloc(&t->ws_occ_bag, N));
   A(dalloc(&t->ws_bag_len, B));
@@ -926,7 +927,7 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
   void* ptrs[] = {t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
-                  t->ws_bt,       t->ws_occ_ent,   t->ws_long_ent,  t->ws_rank,      t->ws_short_rec, t->ws_short_bag,  t->ws_occ_bag,
+                  t->ws_bt,       t->ws_occ_ent,   t->ws_lead,   t->ws_long_ent,  t->ws_rank,      t->ws_short_rec, t->ws_short_bag,  t->ws_occ_bag,
                   t->ws_bag_len,  t->ws_long_row,  t->ws_long_len,  t->ws_long_start, t->ws_lkey_a,
                   t->ws_lval_a,   t->ws_lkey_b,    t->ws_lval_b,    t->ws_long_base,  t->ws_task_long,
                   t->ws_partial2, t->ws_long_hbase, t->ws_node_cnt,

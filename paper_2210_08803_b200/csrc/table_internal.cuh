@@ -81,6 +81,7 @@ struct hps_gpu_table_s {
   uint2* ws_bt = nullptr;
   uint64_t bt_mask = 0;
   uint32_t* ws_occ_ent = nullptr;   // occurrence -> batch-table entry of its row
+  uint32_t* ws_lead = nullptr;      // k_dedup: leaders (rank-0 occurrences), per-CTA lists
   uint32_t* ws_long_ent = nullptr;  // long segment -> batch-table entry
   uint32_t* ws_occ_bag = nullptr;   // occurrence -> bag (multi-hot)
   uint32_t* ws_bag_len = nullptr;   // bag lengths (multi-hot mean)
