@@ -35,6 +35,17 @@ sys.path.insert(0, ROOT)
 from paper_2210_08803_b200 import workload as W  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "round1", "ncu_traffic.json")
+
+
+def ncu_traffic(workload):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu capture, or None."""
+    try:
+        with open(TRAFFIC_PATH) as f:
+            d = json.load(f)[workload]
+        return int(d["dram_read"]) + int(d["dram_write"])
+    except Exception:
+        return None
 FALLBACK_HBM = 6650.0
 
 
@@ -394,7 +405,9 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "k_lookup_1hot (fused hash+probe+gather+pool)" if cfg.hot == 1
                          else "k_lookup_multi (fused hash+probe+gather+pool)",
                          "achieved": fwd_gbs, "peak": peak, "unit": "GB/s", "frac": fwd_gbs / peak,
-                         "peak_kind": peak_kind, "traffic": None, "algorithmic_bytes": fwd_b,
+                         "peak_kind": peak_kind, "traffic": ncu_traffic(cfg.name) if world == 1 else None,
+                         "traffic_source": "ncu --set full dram__bytes_read+write per launch (profiles/round1/ncu_traffic.json)",
+                         "algorithmic_bytes": fwd_b,
                          "kernel_ms": fwd_ms_mean,
                          "step_achieved": step_gbs, "step_frac": step_gbs / peak, "step_algorithmic_bytes": fwd_b + bwd_b},
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

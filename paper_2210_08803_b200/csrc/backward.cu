@@ -1159,8 +1159,10 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
     a.tma_rows = 40;  // 2 CTAs/SM with room for the long-segment chain's kernels beside them
     if (const char* e = std::getenv("HPS_GPU_TMA_ROWS")) a.tma_rows = std::max(36, std::atoi(e));  // A/B knob
     smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float) + size_t(kRedWarps) * kBagStage * 4;
+    int waves = 2;  // CTAs per SM of the grid (2 resident per SM): 2 = a single resident wave
+    if (const char* e = std::getenv("HPS_GPU_RED_WAVES")) waves = std::max(1, std::atoi(e));  // A/B knob
     grid = static_cast<int>(
-        std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * 4)));
+        std::max<uint64_t>(1, std::min<uint64_t>((nk + 32 * kRedWarps - 1) / (32 * kRedWarps), kNumSMs * waves)));
   } else {
     smem = size_t(8) * kBagStage * 4;
     grid = grid_for((nk + 31) / 32 * 32, 256, kNumSMs * 16);
