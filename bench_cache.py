@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--max-batch", type=int, default=131072)
     ap.add_argument("--warmup-mult", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "f16"], help="cache row storage (binary16 halves the bytes)")
     args = ap.parse_args()
 
     import torch
@@ -51,7 +52,7 @@ def main():
     for first in range(0, args.keys, chunk):
         table.insert(0, ctx.gen_keys(tseed, first, min(chunk, args.keys - first)))
     ctx.sync()
-    cache = HotCache(ctx, args.capacity, args.dim, 8, 0, args.max_batch)
+    cache = HotCache(ctx, args.capacity, args.dim, 8, 0, args.max_batch, dtype=args.dtype)
     rt = CachedLookup(cache, table)
     setup_s = time.perf_counter() - t0
 
@@ -103,7 +104,7 @@ def main():
             lat.append(e0.elapsed_time(e1) * 1000.0)
         s = cache.stats()
         lat = np.array(lat)
-        line = {"config": "cfg4-hps-cache", "batch": b, "p50_us": float(np.median(lat)),
+        line = {"config": "cfg4-hps-cache", "dtype": args.dtype, "batch": b, "p50_us": float(np.median(lat)),
                 "p95_us": float(np.percentile(lat, 95)), "keys_per_s": b / (np.median(lat) / 1e6),
                 "hit_rate": s["hits"] / max(1, s["queries"])}
         results.append(line)
@@ -125,7 +126,7 @@ def main():
         dt = time.perf_counter() - t2
         cpu = {"keys_per_s": len(q) / dt, "cores": 1, "kind": "port",
                "sample": "200k cold keys, 4096-key batches, query + insert of misses, 1M-row cache"}
-    summary = {"config": "cfg4-hps-cache", "summary": True, "keys": args.keys, "capacity": args.capacity,
+    summary = {"config": "cfg4-hps-cache", "dtype": args.dtype, "summary": True, "keys": args.keys, "capacity": args.capacity,
                "dim": args.dim, "zipf": args.zipf, "ideal_static_hit_rate": ideal,
                "hit_rate_at_max_batch": results[-1]["hit_rate"], "p50_us_batch1": results[0]["p50_us"],
                "p50_us_max_batch": results[-1]["p50_us"], "keys_per_s_max_batch": results[-1]["keys_per_s"],

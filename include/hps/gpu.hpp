@@ -80,13 +80,61 @@ class Context {
 };
 
 namespace detail {
-inline std::vector<float> rows_of(std::span<const VersionedEntry> entries, uint16_t dim) {
+// binary16 <-> fp32 on the host for F16 tables: the device stores binary16; rows travel as
+// fp32. Widening is exact, and so is narrowing a widened binary16 value.
+inline float f16_bits_to_float(uint16_t h) {
+  const uint32_t sign = static_cast<uint32_t>(h & 0x8000u) << 16, e = (h >> 10) & 0x1fu, m = h & 0x3ffu;
+  uint32_t b;
+  if (e == 31) {
+    b = sign | 0x7f800000u | (m << 13);
+  } else if (e) {
+    b = sign | ((e + 112u) << 23) | (m << 13);
+  } else if (!m) {
+    b = sign;
+  } else {
+    int k = 0;
+    uint32_t mm = m;
+    while (!(mm & 0x400u)) mm <<= 1, ++k;
+    b = sign | (static_cast<uint32_t>(113 - k) << 23) | ((mm & 0x3ffu) << 13);
+  }
+  float f;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+inline uint16_t float_to_f16_bits(float f) {  // round to nearest even; |f| beyond range -> inf
+  uint32_t b;
+  std::memcpy(&b, &f, 4);
+  const uint32_t sign = (b >> 16) & 0x8000u, a = b & 0x7fffffffu;
+  if (a >= 0x7f800000u) return static_cast<uint16_t>(sign | 0x7c00u | (a > 0x7f800000u ? 0x200u : 0u));
+  const int e = static_cast<int>(a >> 23) - 112;
+  if (e >= 31) return static_cast<uint16_t>(sign | 0x7c00u);
+  if (e <= 0) {
+    if (e < -10) return static_cast<uint16_t>(sign);
+    const uint32_t m = (a & 0x7fffffu) | 0x800000u, sh = static_cast<uint32_t>(14 - e);
+    uint32_t q = m >> sh;
+    const uint32_t r = m & ((1u << sh) - 1u), half = 1u << (sh - 1u);
+    if (r > half || (r == half && (q & 1u))) ++q;
+    return static_cast<uint16_t>(sign | q);
+  }
+  uint32_t q = (static_cast<uint32_t>(e) << 10) | ((a >> 13) & 0x3ffu);
+  const uint32_t r = a & 0x1fffu;
+  if (r > 0x1000u || (r == 0x1000u && (q & 1u))) ++q;
+  return static_cast<uint16_t>(sign | q);
+}
+
+// fp32 rows of the entries; their vectors must have the table's dtype (F16 rows widen).
+inline std::vector<float> rows_of(std::span<const VersionedEntry> entries, uint16_t dim, Dtype dtype = Dtype::F32) {
   std::vector<float> rows(entries.size() * dim);
   for (size_t i = 0; i < entries.size(); ++i) {
     const EmbeddingVector& v = entries[i].vector;
-    if (v.dtype() != Dtype::F32) raise(ErrorCode::DtypeMismatch, "the B200 path stores F32 rows");
+    if (v.dtype() != dtype) raise(ErrorCode::DtypeMismatch, "entry dtype does not match the table");
     if (v.dim() != dim) raise(ErrorCode::DimMismatch, "entry dim does not match the table");
-    std::memcpy(rows.data() + i * dim, v.bytes().data(), dim * sizeof(float));
+    if (dtype == Dtype::F32) {
+      std::memcpy(rows.data() + i * dim, v.bytes().data(), dim * sizeof(float));
+    } else {
+      const auto bits = v.f16_bits();
+      for (uint16_t j = 0; j < dim; ++j) rows[i * dim + j] = f16_bits_to_float(bits[j]);
+    }
   }
   return rows;
 }
@@ -104,8 +152,9 @@ class HotCache {
            uint64_t max_batch = 1 << 17)
       : ctx_(ctx), meta_(std::move(meta)), max_batch_(max_batch) {
     meta_.validate();
-    if (meta_.dtype != Dtype::F32) raise(ErrorCode::DtypeMismatch, "the B200 cache stores F32 rows");
-    const hps_cache_config cfg{capacity, ways, aging_interval, meta_.dim, max_batch};
+    // F16 tables: rows held as binary16 on the device (hps_cache_config.dtype)
+    const hps_cache_config cfg{capacity, ways, aging_interval, meta_.dim, max_batch,
+                               meta_.dtype == Dtype::F16 ? uint32_t(HPS_DTYPE_F16) : uint32_t(HPS_DTYPE_F32)};
     check(hps_gpu_cache_create(ctx.handle(), &cfg, &h_), "hps_gpu_cache_create");
   }
   ~HotCache() { hps_gpu_cache_destroy(h_); }
@@ -137,6 +186,12 @@ class HotCache {
       }
       if (c[1]) cuda_check(cudaMemcpy(mi.data(), midx_.get(), c[1] * 4, cudaMemcpyDeviceToHost), "D2H");
       for (uint64_t j = 0; j < c[0]; ++j) {
+        if (meta_.dtype == Dtype::F16) {  // exact: the device holds binary16
+          std::vector<uint16_t> bits(meta_.dim);
+          for (uint16_t q = 0; q < meta_.dim; ++q) bits[q] = detail::float_to_f16_bits(fv[j * meta_.dim + q]);
+          r.found.emplace_back(keys[b + fi[j]], EmbeddingVector::f16(bits));
+          continue;
+        }
         std::vector<std::byte> bytes(meta_.dim * sizeof(float));
         std::memcpy(bytes.data(), fv.data() + j * meta_.dim, bytes.size());
         r.found.emplace_back(keys[b + fi[j]],
@@ -181,7 +236,7 @@ class HotCache {
     for (size_t b = 0; b < entries.size(); b += max_batch_) {
       const size_t n = std::min<size_t>(max_batch_, entries.size() - b);
       auto part = entries.subspan(b, n);
-      std::vector<float> rows = detail::rows_of(part, meta_.dim);
+      std::vector<float> rows = detail::rows_of(part, meta_.dim, meta_.dtype);
       std::vector<uint64_t> k(n), v(n);
       for (size_t i = 0; i < n; ++i) k[i] = part[i].key, v[i] = part[i].version;
       keys_.resize(n);

@@ -48,6 +48,7 @@ enum {
   HPS_GPU_E_DUPLICATE_KEY = 6,
   HPS_GPU_E_DIM_MISMATCH = 7,
   HPS_GPU_E_DTYPE_MISMATCH = 8,
+  HPS_GPU_E_F16_RANGE = 9,
   HPS_GPU_E_NON_FINITE = 10,
   HPS_GPU_E_UNKNOWN_TABLE = 11,
   HPS_GPU_E_BAD_SHARD = 13,
@@ -258,12 +259,19 @@ int hps_gpu_apply_grads(hps_gpu_table tbl, const float* grads, const uint32_t* t
 /* ---- HPS inference cache (K6..K8), SPEC.md:112-190 ---------------------------- */
 typedef struct hps_gpu_cache_s* hps_gpu_cache;
 
+/* Storage dtype of cached rows (hps::Dtype, proj/include/hps/types.hpp:36-40). */
+enum { HPS_DTYPE_F32 = 0, HPS_DTYPE_F16 = 1 };
+
 typedef struct {
   uint64_t capacity;        /* resident entries; capacity % ways == 0 */
   uint32_t ways;            /* 1..32, default 8 */
   uint64_t aging_interval;  /* accesses per set-aging epoch numerator; 0 -> 10*capacity */
   uint32_t dim;
   uint64_t max_batch;       /* workspace sizing: keys per call */
+  uint32_t dtype;           /* HPS_DTYPE_F32 (0, default) or HPS_DTYPE_F16: rows held as IEEE binary16
+                               (round-to-nearest-even on insert/refresh, exact widening on query;
+                               an entry with a value beyond binary16 range is rejected: F16Range,
+                               latched like NonFinite, the entry skipped) — SPEC.md:78-86 */
 } hps_cache_config;
 
 typedef struct {

@@ -336,6 +336,57 @@ struct Sparse {
 };
 
 // ---------------------------------------------------------------------------
+// binary16 storage (restates kernels_scalar.cpp:25-57 f32_bits_to_f16_bits
+// and its inverse — pinned against the compiled reference in tests/test_golden_cpu.py):
+// IEEE round-to-nearest-even, overflow to infinity, NaN kept quiet with its top payload.
+// ---------------------------------------------------------------------------
+uint16_t f32_to_f16_bits(uint32_t b) {
+  const uint32_t sign = (b >> 16) & 0x8000u, a = b & 0x7fffffffu;
+  if (a > 0x7f800000u) return static_cast<uint16_t>(sign | 0x7e00u | ((a >> 13) & 0x3ffu));
+  if (a == 0x7f800000u) return static_cast<uint16_t>(sign | 0x7c00u);
+  const int exp = static_cast<int>(a >> 23) - 112;  // binary16 exponent field (bias 15 vs 127)
+  if (exp >= 31) return static_cast<uint16_t>(sign | 0x7c00u);
+  if (exp <= 0) {  // binary16 subnormal (or zero): quantum 2^-24
+    if (exp < -10) return static_cast<uint16_t>(sign);
+    const uint32_t m = (a & 0x7fffffu) | 0x800000u, shift = static_cast<uint32_t>(14 - exp);
+    uint32_t q = m >> shift;
+    const uint32_t r = m & ((1u << shift) - 1u), half = 1u << (shift - 1u);
+    if (r > half || (r == half && (q & 1u))) ++q;
+    return static_cast<uint16_t>(sign | q);
+  }
+  uint32_t q = (static_cast<uint32_t>(exp) << 10) | ((a >> 13) & 0x3ffu);
+  const uint32_t r = a & 0x1fffu;
+  if (r > 0x1000u || (r == 0x1000u && (q & 1u))) ++q;  // a carry may reach 0x7c00 (infinity)
+  return static_cast<uint16_t>(sign | q);
+}
+uint32_t f16_to_f32_bits(uint16_t h) {
+  const uint32_t sign = static_cast<uint32_t>(h & 0x8000u) << 16, e = (h >> 10) & 0x1fu, m = h & 0x3ffu;
+  if (e == 31) return sign | 0x7f800000u | (m << 13);
+  if (e) return sign | ((e + 112u) << 23) | (m << 13);
+  if (!m) return sign;
+  int k = 0;  // subnormal: normalise
+  uint32_t mm = m;
+  while (!(mm & 0x400u)) {
+    mm <<= 1;
+    ++k;
+  }
+  return sign | (static_cast<uint32_t>(113 - k) << 23) | ((mm & 0x3ffu) << 13);
+}
+float f16_round_trip(float x) {
+  uint32_t b;
+  std::memcpy(&b, &x, 4);
+  const uint32_t w = f16_to_f32_bits(f32_to_f16_bits(b));
+  float y;
+  std::memcpy(&y, &w, 4);
+  return y;
+}
+bool f16_overflows(float x) {  // finite x whose binary16 rounding is infinite
+  uint32_t b;
+  std::memcpy(&b, &x, 4);
+  return ((f32_to_f16_bits(b) & 0x7fffu) == 0x7c00u) && (b & 0x7fffffffu) < 0x7f800000u;
+}
+
+// ---------------------------------------------------------------------------
 // Hot cache model: SPEC.md:112-190 with DESIGN.md §5 resolutions
 // ---------------------------------------------------------------------------
 struct Cache {
@@ -344,8 +395,21 @@ struct Cache {
   uint64_t clock = 0;
   std::vector<uint64_t> key, version, last_touch, set_acc;
   std::vector<uint8_t> freq;  // 0 == empty way
-  std::vector<float> vec;
+  std::vector<float> vec;  // binary16 storage: values held as their exact fp32 widening
+  bool f16 = false;
   uint64_t st[7] = {0, 0, 0, 0, 0, 0, 0};  // queries hits misses insertions rejected refresh evictions
+  // Validate an entry (NaN/Inf -> NonFinite 10; binary16 out of range -> F16Range 9).
+  int check(const float* v) const {
+    bool bad = false, range = false;
+    for (uint32_t j = 0; j < dim; ++j) {
+      bad |= non_finite(v[j]);
+      if (f16) range |= f16_overflows(v[j]);
+    }
+    return bad ? 10 : range ? 9 : 0;
+  }
+  void store(uint64_t e, const float* v) {
+    for (uint32_t j = 0; j < dim; ++j) vec[e * dim + j] = f16 ? f16_round_trip(v[j]) : v[j];
+  }
 
   uint64_t set_of(uint64_t k) const { return key_hash(k) % num_sets; }
   // One access to set s (counted before the access is applied; the
@@ -540,6 +604,21 @@ void* orc_cache_create(uint64_t capacity, uint32_t ways, uint64_t aging_interval
   return c;
 }
 void orc_cache_destroy(void* h) { delete static_cast<Cache*>(h); }
+void orc_cache_set_dtype(void* h, int dtype) { static_cast<Cache*>(h)->f16 = dtype == 1; }
+// binary16 conversions (the restatement above), element-wise
+void orc_f32_to_f16(const float* src, uint16_t* dst, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t b;
+    std::memcpy(&b, src + i, 4);
+    dst[i] = f32_to_f16_bits(b);
+  }
+}
+void orc_f16_to_f32(const uint16_t* src, float* dst, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint32_t b = f16_to_f32_bits(src[i]);
+    std::memcpy(dst + i, &b, 4);
+  }
+}
 // SPEC.md:131-139
 void orc_cache_query(void* h, const uint64_t* keys, uint64_t n, float* found_vecs, uint32_t* found_idx,
                      uint32_t* missing_idx, uint64_t* counts) {
@@ -574,10 +653,8 @@ uint64_t orc_cache_insert(void* h, const uint64_t* keys, const float* vecs, cons
   uint64_t admitted = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const float* v = vecs + i * c->dim;
-    bool bad = false;
-    for (uint32_t j = 0; j < c->dim; ++j) bad |= non_finite(v[j]);
-    if (bad) {
-      if (status) *status = 10;
+    if (const int e = c->check(v)) {
+      if (status && !*status) *status = e;
       continue;
     }
     const uint64_t s = c->set_of(keys[i]);
@@ -587,7 +664,7 @@ uint64_t orc_cache_insert(void* h, const uint64_t* keys, const float* vecs, cons
     if (w >= 0) {  // resident: refresh semantics
       const uint64_t e = s * c->ways + w;
       if (versions[i] > c->version[e]) {
-        std::memcpy(&c->vec[e * c->dim], v, c->dim * 4);
+        c->store(e, v);
         c->version[e] = versions[i];
         c->st[5]++;
       }
@@ -613,7 +690,7 @@ uint64_t orc_cache_insert(void* h, const uint64_t* keys, const float* vecs, cons
     c->version[e] = versions[i];
     c->freq[e] = 1;
     c->last_touch[e] = t;
-    std::memcpy(&c->vec[e * c->dim], v, c->dim * 4);
+    c->store(e, v);
     c->st[3]++;
     ++admitted;
   }
@@ -626,10 +703,8 @@ uint64_t orc_cache_refresh(void* h, const uint64_t* keys, const float* vecs, con
   uint64_t replaced = 0;
   for (uint64_t i = 0; i < n; ++i) {
     const float* v = vecs + i * c->dim;
-    bool bad = false;
-    for (uint32_t j = 0; j < c->dim; ++j) bad |= non_finite(v[j]);
-    if (bad) {
-      if (status) *status = 10;
+    if (const int e = c->check(v)) {
+      if (status && !*status) *status = e;
       continue;
     }
     const uint64_t s = c->set_of(keys[i]);
@@ -637,7 +712,7 @@ uint64_t orc_cache_refresh(void* h, const uint64_t* keys, const float* vecs, con
     if (w < 0) continue;
     const uint64_t e = s * c->ways + w;
     if (versions[i] > c->version[e]) {
-      std::memcpy(&c->vec[e * c->dim], v, c->dim * 4);
+      c->store(e, v);
       c->version[e] = versions[i];
       c->st[5]++;
       ++replaced;

@@ -68,6 +68,7 @@ class CacheConfig(C.Structure):
         ("aging_interval", u64),
         ("dim", u32),
         ("max_batch", u64),
+        ("dtype", u32),  # HPS_DTYPE_F32 = 0, HPS_DTYPE_F16 = 1
     ]
 
 

@@ -210,10 +210,14 @@ class HotCache:
     """hps_gpu_cache: the HPS set-associative GPU embedding cache."""
 
     def __init__(self, ctx: Context, capacity: int, dim: int, ways: int = 8, aging_interval: int = 0,
-                 max_batch: int = 1 << 17):
-        self.ctx, self.lib, self.dim = ctx, ctx.lib, dim
+                 max_batch: int = 1 << 17, dtype: str = "f32"):
+        """dtype: storage of the cached rows, "f32" or "f16" (binary16, round-to-nearest-even
+        on insert/refresh, exact widening on query; out-of-range rows rejected: F16Range)."""
+        if dtype not in ("f32", "f16"):
+            raise HpsError(1, "dtype must be 'f32' or 'f16'")
+        self.ctx, self.lib, self.dim, self.dtype = ctx, ctx.lib, dim, dtype
         self.device = torch.device(f"cuda:{ctx.device}")
-        cfg = L.CacheConfig(capacity, ways, aging_interval, dim, max_batch)
+        cfg = L.CacheConfig(capacity, ways, aging_interval, dim, max_batch, 1 if dtype == "f16" else 0)
         h = C.c_void_p()
         L.check(self.lib.hps_gpu_cache_create(ctx.h, C.byref(cfg), C.byref(h)), "cache_create")
         self.h = h

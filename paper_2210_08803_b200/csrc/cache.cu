@@ -16,9 +16,11 @@
 //     so the same sort feeds one warp per set that walks its entries in input order,
 //     lanes = ways.
 // HBM layout (set-major): keys/versions/last_touch [sets x ways] u64,
-// freq [sets x ways] u8 (0 = empty way), vectors [sets x ways x dim] fp32.
+// freq [sets x ways] u8 (0 = empty way), vectors [sets x ways x dim] fp32 or binary16.
 #include <algorithm>
 #include <vector>
+
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 #include "primitives.cuh"
@@ -33,7 +35,8 @@ struct hps_gpu_cache_s {
   int set_bits = 0;
   uint64_t *d_keys = nullptr, *d_ver = nullptr, *d_touch = nullptr, *d_set_acc = nullptr;
   uint8_t* d_freq = nullptr;
-  float* d_vec = nullptr;
+  void* d_vec = nullptr;  // [capacity x dim] fp32, or binary16 when f16
+  bool f16 = false;
   uint64_t* d_state = nullptr;  // [0]=clock [1]=clock snapshot of the running call [2..8]=stats [9]=scratch count
   // workspaces
   uint32_t *ws_set = nullptr, *ws_keys_b = nullptr, *ws_vals_a = nullptr, *ws_vals_b = nullptr;
@@ -115,10 +118,23 @@ struct SplitOp {
 };
 
 // ---- K6c: gather hit rows (LPR lanes per row, 128-bit loads) ------------------------
-template <int LPR>
+// Four cached scalars of entry e, widened to fp32 (binary16 -> fp32 is exact).
+template <bool F16>
+__device__ __forceinline__ float4 load_cached4(const void* cvec, uint64_t e, uint32_t dim, uint32_t q) {
+  if constexpr (F16) {
+    const uint2 h = __ldg(reinterpret_cast<const uint2*>(static_cast<const __half*>(cvec) + e * dim) + q);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&h.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&h.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  } else {
+    return __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(cvec) + e * dim) + q);
+  }
+}
+
+template <int LPR, bool F16>
 __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ found_idx, const uint64_t* counts,
                                                 const uint32_t* __restrict__ set_of, const uint8_t* __restrict__ hit,
-                                                uint32_t ways, const float* __restrict__ vec, uint32_t dim,
+                                                uint32_t ways, const void* __restrict__ vec, uint32_t dim,
                                                 float* __restrict__ out) {
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
@@ -129,9 +145,8 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ fou
   for (uint64_t j = gid; j < nf; j += ng) {
     const uint32_t i = found_idx[j];
     const uint64_t e = uint64_t(set_of[i]) * ways + hit[i];
-    const float4* src = reinterpret_cast<const float4*>(vec + e * dim);
     float4* dst = reinterpret_cast<float4*>(out + j * dim);
-    for (uint32_t v = gl; v < nvec; v += LPR) dst[v] = __ldg(src + v);
+    for (uint32_t v = gl; v < nvec; v += LPR) dst[v] = load_cached4<F16>(vec, e, dim, v);
   }
 }
 
@@ -214,13 +229,16 @@ __global__ void __launch_bounds__(256) k_query_meta(const uint32_t* __restrict__
   }
 }
 
-// ---- K7/K8 prep: validate rows (NaN/Inf -> NonFinite), set id, validity -------------
+// ---- K7/K8 prep: validate rows (NaN/Inf -> NonFinite; binary16 storage: out of range ->
+// F16Range), set id, validity ----------------------------------------------------------
+__device__ __forceinline__ bool f16_overflows(uint32_t bits) { return (bits & 0x7fffffffu) >= 0x477ff000u; }
+
 template <int LPR>
 __global__ void __launch_bounds__(256) k_entry_prep(const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
                                                     uint64_t n, uint32_t dim, hps::FastMod64 fm, uint32_t invalid_set,
                                                     uint32_t* __restrict__ set_out, uint8_t* __restrict__ valid_out,
                                                     uint32_t* status, uint64_t* counts, const uint64_t* d_n,
-                                                    const uint8_t* __restrict__ skip) {
+                                                    const uint8_t* __restrict__ skip, int f16) {
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
   const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
@@ -231,15 +249,19 @@ __global__ void __launch_bounds__(256) k_entry_prep(const uint64_t* __restrict__
   const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
   for (uint64_t i = gid; i < n; i += ng) {
     const uint4* v = reinterpret_cast<const uint4*>(vecs + i * dim);
-    bool bad = false;
+    bool bad = false, range = false;
     for (uint32_t q = gl; q < nvec; q += LPR) {
       const uint4 x = __ldg(v + q);
       bad |= non_finite_bits(x.x) | non_finite_bits(x.y) | non_finite_bits(x.z) | non_finite_bits(x.w);
+      // binary16 storage: |x| >= 65520 rounds to infinity (the largest finite is 65504)
+      if (f16) range |= f16_overflows(x.x) | f16_overflows(x.y) | f16_overflows(x.z) | f16_overflows(x.w);
     }
     bad = __any_sync(gmask, bad);
+    range = __any_sync(gmask, range) && !bad;
     if (gl == 0) {
       if (bad) latch_status(status, HPS_GPU_E_NON_FINITE);
-      const bool skipped = bad || (skip && skip[i]);  // skip: absent from the backing store, never cached
+      if (range) latch_status(status, HPS_GPU_E_F16_RANGE);
+      const bool skipped = bad || range || (skip && skip[i]);  // skip: absent from the backing store
       set_out[i] = skipped ? invalid_set : static_cast<uint32_t>(fm.mod(hps::key_hash(keys[i])));
       valid_out[i] = skipped ? 0 : 1;
     }
@@ -262,14 +284,27 @@ struct RankOp {
   }
 };
 
-__device__ __forceinline__ void warp_copy_row(float* dst, const float* src, uint32_t dim) {
+// One fp32 row into cached entry e (warp-wide); binary16 storage rounds to nearest even
+// (cvt.rn.f16x2.f32, the reference's f32_to_f16: kernels_scalar.cpp:25-57).
+template <bool F16>
+__device__ __forceinline__ void warp_store_row(void* cvec, uint64_t e, const float* src, uint32_t dim) {
   const uint32_t nvec = dim / 4;
   const float4* s4 = reinterpret_cast<const float4*>(src);
-  float4* d4 = reinterpret_cast<float4*>(dst);
-  for (uint32_t q = lane_id(); q < nvec; q += 32) d4[q] = __ldg(s4 + q);
+  if constexpr (F16) {
+    uint2* d = reinterpret_cast<uint2*>(static_cast<__half*>(cvec) + e * dim);
+    for (uint32_t q = lane_id(); q < nvec; q += 32) {
+      const float4 x = __ldg(s4 + q);
+      const __half2 lo = __floats2half2_rn(x.x, x.y), hi = __floats2half2_rn(x.z, x.w);
+      d[q] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
+  } else {
+    float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(cvec) + e * dim);
+    for (uint32_t q = lane_id(); q < nvec; q += 32) d4[q] = __ldg(s4 + q);
+  }
 }
 
 // ---- K7: insert, one warp per touched set, entries in input order --------------------
+template <bool F16>
 __global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict__ sets_sorted,
                                                      const uint32_t* __restrict__ idx_sorted,
                                                      const uint32_t* __restrict__ seg_start, const uint64_t* counts,
@@ -278,7 +313,7 @@ __global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict_
                                                      const uint32_t* __restrict__ rank, uint32_t ways, uint32_t dim,
                                                      uint64_t aging_period, uint32_t invalid_set, uint64_t* ckeys,
                                                      uint64_t* cver, uint8_t* cfreq, uint64_t* ctouch, uint64_t* set_acc,
-                                                     float* cvec, uint64_t* state, uint64_t* admitted_out) {
+                                                     void* cvec, uint64_t* state, uint64_t* admitted_out) {
   const uint32_t lane = lane_id();
   const uint64_t U = counts[1];
   const uint64_t clock0 = state[kSnap];
@@ -307,7 +342,7 @@ __global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict_
         const int w = __ffs(res) - 1;
         const uint64_t vw = __shfl_sync(0xffffffffu, v_w, w);
         if (ver > vw) {
-          warp_copy_row(cvec + (e0 + w) * dim, vecs + uint64_t(i) * dim, dim);
+          warp_store_row<F16>(cvec, e0 + w, vecs + uint64_t(i) * dim, dim);
           if (lane == static_cast<uint32_t>(w)) v_w = ver;
           ++n_refresh;
         }
@@ -341,7 +376,7 @@ __global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict_
         f_w = 1;
         t_w = t;
       }
-      warp_copy_row(cvec + (e0 + w) * dim, vecs + uint64_t(i) * dim, dim);
+      warp_store_row<F16>(cvec, e0 + w, vecs + uint64_t(i) * dim, dim);
       ++n_ins;
     }
     if (way) {
@@ -361,13 +396,14 @@ __global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict_
 }
 
 // ---- K8: refresh, one warp per touched set ------------------------------------------
+template <bool F16>
 __global__ void __launch_bounds__(256) k_refresh_sets(const uint32_t* __restrict__ sets_sorted,
                                                       const uint32_t* __restrict__ idx_sorted,
                                                       const uint32_t* __restrict__ seg_start, const uint64_t* counts,
                                                       const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
                                                       const uint64_t* __restrict__ versions, uint32_t ways,
                                                       uint32_t dim, uint32_t invalid_set, const uint64_t* ckeys,
-                                                      uint64_t* cver, const uint8_t* cfreq, float* cvec,
+                                                      uint64_t* cver, const uint8_t* cfreq, void* cvec,
                                                       uint64_t* state, uint64_t* replaced_out) {
   const uint32_t lane = lane_id();
   const uint64_t U = counts[1];
@@ -391,7 +427,7 @@ __global__ void __launch_bounds__(256) k_refresh_sets(const uint32_t* __restrict
       const int w = __ffs(res) - 1;
       const uint64_t vw = __shfl_sync(0xffffffffu, v_w, w);
       if (ver > vw) {
-        warp_copy_row(cvec + (e0 + w) * dim, vecs + uint64_t(i) * dim, dim);
+        warp_store_row<F16>(cvec, e0 + w, vecs + uint64_t(i) * dim, dim);
         if (lane == static_cast<uint32_t>(w)) v_w = ver;
         ++n_rep;
       }
@@ -472,12 +508,17 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
   if (cfg->capacity / ways >= 0xffffffffull) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (cfg->dtype != HPS_DTYPE_F32 && cfg->dtype != HPS_DTYPE_F16) {
+    set_last_error("cache config: dtype must be HPS_DTYPE_F32 or HPS_DTYPE_F16");
+    return HPS_GPU_E_DTYPE_MISMATCH;
+  }
   HPSG_CUDA(cudaSetDevice(ctx->device));
   auto c = new hps_gpu_cache_s;
   c->ctx = ctx;
   c->capacity = cfg->capacity;
   c->ways = ways;
   c->dim = cfg->dim;
+  c->f16 = cfg->dtype == HPS_DTYPE_F16;
   c->num_sets = cfg->capacity / ways;
   const uint64_t interval = cfg->aging_interval ? cfg->aging_interval : 10 * cfg->capacity;
   c->aging_period = std::max<uint64_t>(1, interval / c->num_sets);
@@ -494,7 +535,7 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   A(dalloc(&c->d_touch, cap));
   A(dalloc(&c->d_freq, cap));
   A(dalloc(&c->d_set_acc, c->num_sets));
-  A(dalloc(&c->d_vec, cap * c->dim));
+  A(dalloc(reinterpret_cast<uint8_t**>(&c->d_vec), cap * c->dim * (c->f16 ? 2 : 4)));
   A(dalloc(&c->d_state, 16));
   A(dalloc(&c->ws_set, n));
   A(dalloc(&c->ws_keys_b, n));
@@ -517,7 +558,7 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   HPSG_CUDA(cudaMemsetAsync(c->d_ver, 0, cap * 8, s));
   HPSG_CUDA(cudaMemsetAsync(c->d_touch, 0, cap * 8, s));
   HPSG_CUDA(cudaMemsetAsync(c->d_set_acc, 0, c->num_sets * 8, s));
-  HPSG_CUDA(cudaMemsetAsync(c->d_vec, 0, cap * c->dim * sizeof(float), s));
+  HPSG_CUDA(cudaMemsetAsync(c->d_vec, 0, cap * c->dim * (c->f16 ? 2 : 4), s));
   HPSG_CUDA(cudaMemsetAsync(c->d_state, 0, 16 * 8, s));
   HPSG_CUDA(cudaMemsetAsync(c->ws_counts, 0, 8 * 8, s));
   HPSG_CUDA(cudaStreamSynchronize(s));
@@ -558,7 +599,11 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
   if (found_vecs) {
     const int lpr = lpr_for(c->dim);
     const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
-#define HPSG_G(L) k_gather<L><<<grid, 256, 0, st>>>(found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec, c->dim, found_vecs)
+#define HPSG_G(L)                                                                                                   \
+  (c->f16 ? k_gather<L, true><<<grid, 256, 0, st>>>(found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec, \
+                                                     c->dim, found_vecs)                                              \
+          : k_gather<L, false><<<grid, 256, 0, st>>>(found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec,\
+                                                      c->dim, found_vecs))
     switch (lpr) {
       case 32: HPSG_G(32); break;
       case 16: HPSG_G(16); break;
@@ -585,7 +630,7 @@ static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, 
   const int lpr = lpr_for(c->dim);
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
   const uint32_t invalid = static_cast<uint32_t>(c->num_sets);
-#define HPSG_P(L) k_entry_prep<L><<<grid, 256, 0, st>>>(keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts, d_n, skip)
+#define HPSG_P(L) k_entry_prep<L><<<grid, 256, 0, st>>>(keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts, d_n, skip, c->f16 ? 1 : 0)
   switch (lpr) {
     case 32: HPSG_P(32); break;
     case 16: HPSG_P(16); break;
@@ -616,10 +661,10 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
-  k_insert_sets<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs,
-                                                   versions, c->ws_rank, c->ways, c->dim, c->aging_period,
-                                                   static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq,
-                                                   c->d_touch, c->d_set_acc, c->d_vec, c->d_state, admitted_out);
+  (c->f16 ? k_insert_sets<true> : k_insert_sets<false>)<<<set_warps_grid(n), 256, 0, st>>>(
+      sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ws_rank, c->ways, c->dim,
+      c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch, c->d_set_acc,
+      c->d_vec, c->d_state, admitted_out);
   HPSG_CHECK_LAUNCH("cache insert");
   return HPS_GPU_OK;
 }
@@ -648,9 +693,9 @@ int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* ve
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
-  k_refresh_sets<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs,
-                                                    versions, c->ways, c->dim, static_cast<uint32_t>(c->num_sets),
-                                                    c->d_keys, c->d_ver, c->d_freq, c->d_vec, c->d_state, replaced_out);
+  (c->f16 ? k_refresh_sets<true> : k_refresh_sets<false>)<<<set_warps_grid(n), 256, 0, st>>>(
+      sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ways, c->dim,
+      static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_vec, c->d_state, replaced_out);
   HPSG_CHECK_LAUNCH("cache refresh");
   return HPS_GPU_OK;
 }

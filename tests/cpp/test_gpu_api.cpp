@@ -71,6 +71,23 @@ int main() {
   } catch (const hps::Error& e) {
     REQUIRE(e.code() == hps::ErrorCode::DimMismatch);
   }
+  // ---- F16 table: rows held as binary16 on the device ----
+  {
+    hps::gpu::HotCache c16(ctx, hps::TableMeta::make("h", 4, hps::Dtype::F16), 64);
+    const std::vector<uint16_t> bits{0x3c00, 0xbc00, 0x3555, 0x7bff};  // 1, -1, ~1/3, 65504
+    std::vector<hps::VersionedEntry> e{{5, hps::EmbeddingVector::f16(bits), 1}};
+    REQUIRE(c16.insert(e) == 1);
+    std::vector<hps::EmbeddingKey> k5{5};
+    auto r16 = c16.query(k5);
+    REQUIRE(r16.found.size() == 1 && r16.found[0].second == hps::EmbeddingVector::f16(bits));
+    std::vector<hps::VersionedEntry> wrong{{6, vec(1.f), 1}};  // an F32 vector for an F16 table
+    try {
+      c16.insert(wrong);
+      REQUIRE(false);
+    } catch (const hps::Error& ex) {
+      REQUIRE(ex.code() == hps::ErrorCode::DtypeMismatch);
+    }
+  }
   // ---- embedding table ----
   std::vector<hps::TableMeta> metas{hps::TableMeta::make("a", 4), hps::TableMeta::make("b", 4)};
   hps::gpu::EmbeddingTable tbl(ctx, metas, {100, 10}, {0, 1});

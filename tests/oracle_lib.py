@@ -38,6 +38,9 @@ _SIG = {
     "orc_last_unique": (u64, [vp, vp]),
     "orc_cache_create": (vp, [u64, u32, u64, u32]),
     "orc_cache_destroy": (None, [vp]),
+    "orc_cache_set_dtype": (None, [vp, i32]),
+    "orc_f32_to_f16": (None, [vp, vp, u64]),
+    "orc_f16_to_f32": (None, [vp, vp, u64]),
     "orc_cache_query": (None, [vp, vp, u64, vp, vp, vp, vp]),
     "orc_cache_insert": (u64, [vp, vp, vp, vp, u64, vp]),
     "orc_cache_refresh": (u64, [vp, vp, vp, vp, u64, vp]),
@@ -155,10 +158,12 @@ class OracleTable:
 
 
 class OracleCache:
-    def __init__(self, capacity, dim, ways=8, aging_interval=0):
+    def __init__(self, capacity, dim, ways=8, aging_interval=0, dtype="f32"):
         self.L = lib()
         self.dim, self.ways = dim, ways
         self.h = self.L.orc_cache_create(capacity, ways, aging_interval, dim)
+        if dtype == "f16":
+            self.L.orc_cache_set_dtype(self.h, 1)
 
     def query(self, keys):
         keys = np.ascontiguousarray(keys, dtype=np.uint64)

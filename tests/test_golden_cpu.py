@@ -118,3 +118,30 @@ def test_partition_balance_spec_examples():
     seq = np.arange(1_000_000, dtype=np.uint64)
     L.orc_partition_of_n(O.P(seq), len(seq), 8, O.P(out))
     assert (np.bincount(out, minlength=8) == 125_000).all()
+
+
+def test_oracle_f16_matches_reference():
+    """The oracle's binary16 restatement (the F16 cache storage checker) against the
+    reference's own f32_to_f16 / f16_to_f32 (kernels_scalar.cpp:25-57, golden vectors),
+    and against IEEE binary16 (numpy) exhaustively for widening and on random narrowing."""
+    L = O.lib()
+    src = np.array(G["f16"]["f32_bits"], dtype=np.uint32).view(np.float32)
+    out = np.empty(len(src), dtype=np.uint16)
+    L.orc_f32_to_f16(O.P(src), O.P(out), len(src))
+    np.testing.assert_array_equal(out, np.array(G["f16"]["f16_bits"], dtype=np.uint16))
+    back = np.empty(len(src), dtype=np.float32)
+    L.orc_f16_to_f32(O.P(out), O.P(back), len(out))
+    np.testing.assert_array_equal(back.view(np.uint32), np.array(G["f16"]["roundtrip_f32_bits"], dtype=np.uint32))
+    allh = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    wide = np.empty(65536, dtype=np.float32)
+    L.orc_f16_to_f32(O.P(allh), O.P(wide), 65536)
+    ref = allh.view(np.float16).astype(np.float32)
+    fin = np.isfinite(ref)
+    np.testing.assert_array_equal(wide[fin].view(np.uint32), ref[fin].view(np.uint32))
+    rs = np.random.default_rng(5)
+    x = rs.integers(0, 2**32, 200_000, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    x = x[np.isfinite(x)]
+    nar = np.empty(len(x), dtype=np.uint16)
+    L.orc_f32_to_f16(O.P(x), O.P(nar), len(x))
+    with np.errstate(over="ignore"):
+        np.testing.assert_array_equal(nar, x.astype(np.float16).view(np.uint16))

@@ -232,3 +232,55 @@ def test_apply_update_rejects_malformed_and_dim_mismatch(ctx):
     with pytest.raises(HpsError) as e:
         g.apply_update(U.encode_update_batch("emb", 1, np.array([1], np.uint64), np.ones((1, 4), np.float32)))
     assert e.value.code == 7
+
+
+def pair16(ctx, capacity, dim, ways=8, aging=0, max_batch=4096):
+    return (HotCache(ctx, capacity, dim, ways, aging, max_batch, dtype="f16"),
+            O.OracleCache(capacity, dim, ways, aging, dtype="f16"))
+
+
+@pytest.mark.parametrize("cap,ways,aging", [(256, 8, 0), (96, 4, 40), (1024, 32, 0)])
+def test_f16_storage_sequences_match_oracle(ctx, cap, ways, aging):
+    """binary16 cache rows: the same randomized
+    query/insert/refresh sequences; found vectors are the exact widening of the RNE-rounded
+    inserted values, bit-identical to the oracle (whose binary16 is pinned to the reference)."""
+    dim = 12
+    g, o = pair16(ctx, cap, dim, ways, aging)
+    rs = np.random.default_rng(cap * 3 + ways)
+    zipf = W.Zipf(3 * cap, 1.05)
+    version = 1
+    for rnd in range(15):
+        keys = W.mix64(zipf.ranks(W.rng(rnd * 5 + 3, np.arange(int(rs.integers(1, 500)), dtype=np.uint64))).astype(np.uint64))
+        oi, om = q_both(g, o, keys)
+        miss = keys[om]
+        if len(miss):
+            # wide dynamic range: subnormal binary16, ties, values near the 65504 limit
+            vecs = (rs.standard_normal((len(miss), dim)) * np.exp2(rs.integers(-26, 15, (len(miss), dim)))).astype(np.float32)
+            vers = (version + rs.integers(0, 3, len(miss))).astype(np.uint64)
+            ins_both(ctx, g, o, miss, vecs, vers)
+        if rnd % 3 == 0:
+            rk = keys[: min(40, len(keys))]
+            vecs = rs.standard_normal((len(rk), dim)).astype(np.float32)
+            vers = (version + rs.integers(-1, 3, len(rk))).clip(0).astype(np.uint64)
+            gn = g.refresh(t64(rk), tf(vecs), t64(vers))
+            on, _ = o.refresh(rk, vecs, vers)
+            assert int(gn.item()) == on
+        version += 2
+        assert g.stats() == o.stats(), rnd
+    q_both(g, o, W.mix64(np.arange(3 * cap, dtype=np.uint64)))
+
+
+def test_f16_storage_range_and_spec_examples(ctx):
+    """{0, 1, -1} exact; 1/3 within 2^-11; 1e6 is a saturation error
+    (F16Range, the entry skipped — rejected, not clamped). 65504 is the largest accepted."""
+    g, o = pair16(ctx, 64, 4)
+    vecs = np.array([[0.0, 1.0, -1.0, 1.0 / 3.0], [1e6, 0, 0, 0], [65504.0, -65519.0, 0, 0]], dtype=np.float32)
+    ins_both(ctx, g, o, np.array([1, 2, 3], np.uint64), vecs, np.ones(3, np.uint64))
+    fi, fv, mi = g.query(t64(np.array([1, 2, 3], np.uint64)))
+    assert fi.cpu().tolist() == [0, 2] and mi.cpu().tolist() == [1]
+    row = fv.cpu().numpy()[0]
+    assert row[:3].tolist() == [0.0, 1.0, -1.0] and abs(row[3] - 1.0 / 3.0) <= 2.0 ** -11
+    assert fv.cpu().numpy()[1][:2].tolist() == [65504.0, -65504.0]
+    oi, ov, om = o.query(np.array([1, 2, 3], np.uint64))
+    np.testing.assert_array_equal(fv.cpu().numpy().view(np.uint32), ov.view(np.uint32))
+    assert g.stats() == o.stats()
