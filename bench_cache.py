@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--warmup-mult", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f16"], help="cache row storage (binary16 halves the bytes)")
+    ap.add_argument("--phases", action="store_true", help="debug: per-call times (query / read-through / insert) at the max batch")
     args = ap.parse_args()
 
     import torch
@@ -87,6 +88,32 @@ def main():
         rt.lookup(zipf_keys(args.max_batch))
     ctx.sync()
     warm_s = time.perf_counter() - t1
+
+    if args.phases:  # per-call device times at the max batch (events between the three C-ABI calls)
+        import ctypes as C
+        from paper_2210_08803_b200 import _lib as LL
+        ph = {"query": [], "read_through": [], "insert": []}
+        for _ in range(10):
+            kb = zipf_keys(args.max_batch)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            nq = kb.numel()
+            ev[0].record()
+            fv, fi, mi, cnt = cache.query_async(kb, found_vecs=rt.found)
+            ev[1].record()
+            LL.check(rt.lib.hps_gpu_table_read_through(rt.table.h, rt.table_id, kb.data_ptr(), fv.data_ptr(),
+                                                       fi.data_ptr(), mi.data_ptr(), cnt.data_ptr(), nq,
+                                                       rt.out.data_ptr(), rt.miss_keys.data_ptr(),
+                                                       rt.miss_vecs.data_ptr(), rt.miss_absent.data_ptr()), "rt")
+            ev[2].record()
+            LL.check(rt.lib.hps_gpu_cache_insert_count(cache.h, rt.miss_keys.data_ptr(), rt.miss_vecs.data_ptr(), None,
+                                                       nq, C.c_void_p(cnt.data_ptr() + 8), rt.miss_absent.data_ptr(),
+                                                       rt.admitted.data_ptr()), "ins")
+            ev[3].record()
+            ev[3].synchronize()
+            for k, (a, b2) in zip(ph, [(0, 1), (1, 2), (2, 3)]):
+                ph[k].append(ev[a].elapsed_time(ev[b2]) * 1000.0)
+        print("# phases at batch", args.max_batch, {k: round(float(np.median(v)), 1) for k, v in ph.items()},
+              file=sys.stderr, flush=True)
 
     results = []
     b = 1

@@ -18,6 +18,8 @@
 // HBM layout (set-major): keys/versions/last_touch [sets x ways] u64,
 // freq [sets x ways] u8 (0 = empty way), vectors [sets x ways x dim] fp32 or binary16.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include <cuda_fp16.h>
@@ -173,7 +175,53 @@ __device__ __forceinline__ uint32_t sat_add_freq(uint32_t f, uint32_t x) {
 }
 __device__ __forceinline__ uint32_t age_freq(uint32_t f) { return f == 0 ? 0u : max(1u, f >> 1); }
 
-// ---- K6d: replay the batch's metadata effects, one warp per touched set --------------
+// ---- K6d: replay the batch's metadata effects per touched set ---------------------------
+// Warp-cooperative replay of set s's accesses [lo, hi) (32 at a time, closed form per way:
+// saturating adds between aging points).
+__device__ __forceinline__ void meta_set_warp(const uint32_t* __restrict__ idx_sorted, const uint8_t* __restrict__ hit,
+                                              uint32_t ways, uint64_t aging_period, uint8_t* __restrict__ cfreq,
+                                              uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
+                                              uint64_t clock0, uint64_t s, uint32_t lo, uint32_t hi) {
+  const uint32_t lane = lane_id();
+  uint32_t f = lane < ways ? cfreq[s * ways + lane] : 0u;
+  uint64_t touch = lane < ways ? ctouch[s * ways + lane] : 0ull;
+  uint64_t acc = set_acc[s];
+  for (uint32_t c = lo; c < hi; c += 32) {
+    const uint32_t j = c + lane;
+    const bool valid = j < hi;
+    const uint32_t i = valid ? idx_sorted[j] : 0u;
+    const uint32_t hw = valid ? hit[i] : kMiss;
+    const uint32_t cnt = min(32u, hi - c);
+    const bool fire = valid && ((acc + lane + 1) % aging_period == 0);
+    const uint32_t F = __ballot_sync(0xffffffffu, fire);
+    uint32_t H = 0;
+    for (uint32_t w = 0; w < ways; ++w) {
+      const uint32_t m = __ballot_sync(0xffffffffu, hw == w);
+      if (lane == w) H = m;
+    }
+    uint32_t prev = 0, Fm = F;
+    while (Fm) {
+      const uint32_t b = __ffs(Fm) - 1;
+      Fm &= Fm - 1;
+      const uint32_t seg = H & (((b >= 32) ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << prev) - 1u));
+      f = age_freq(sat_add_freq(f, __popc(seg)));
+      prev = b;
+    }
+    const uint32_t tailmask = (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)) & ~((prev >= 32) ? 0xffffffffu : ((1u << prev) - 1u));
+    f = sat_add_freq(f, __popc(H & tailmask));
+    const uint32_t lastp = H ? 31u - __clz(H) : 0u;
+    const uint32_t ilast = __shfl_sync(0xffffffffu, i, lastp);
+    if (H) touch = clock0 + ilast + 1;
+    acc = (acc + cnt) % aging_period;
+  }
+  if (lane < ways) {
+    cfreq[s * ways + lane] = static_cast<uint8_t>(f);
+    ctouch[s * ways + lane] = touch;
+  }
+  if (lane == 0) set_acc[s] = acc;
+}
+
+// Any number of ways: one warp per touched set.
 __global__ void __launch_bounds__(256) k_query_meta(const uint32_t* __restrict__ sets_sorted,
                                                     const uint32_t* __restrict__ idx_sorted,
                                                     const uint32_t* __restrict__ seg_start, const uint64_t* counts,
@@ -181,51 +229,214 @@ __global__ void __launch_bounds__(256) k_query_meta(const uint32_t* __restrict__
                                                     uint64_t aging_period, uint8_t* __restrict__ cfreq,
                                                     uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
                                                     const uint64_t* state) {
+  const uint64_t U = counts[1];
+  const uint64_t clock0 = state[kSnap];
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t u = warp; u < U; u += n_warps)
+    meta_set_warp(idx_sorted, hit, ways, aging_period, cfreq, ctouch, set_acc, clock0, sets_sorted[seg_start[u]],
+                  seg_start[u], seg_start[u + 1]);
+}
+
+// ways <= 8: a lane replays one set (most sets see one or two accesses per batch), 32 sets
+// per warp with every metadata load in flight together; a set with more than
+// kLaneMetaMax accesses is replayed by the whole warp afterwards (closed form), and one
+// with more than kHugeMeta by k_query_meta_huge.
+constexpr uint32_t kLaneMetaMax = 8;
+constexpr uint32_t kHugeMeta = 256;
+constexpr uint32_t kHugeStage = 8192;
+__global__ void __launch_bounds__(256) k_query_meta_lanes(const uint32_t* __restrict__ sets_sorted,
+                                                          const uint32_t* __restrict__ idx_sorted,
+                                                          const uint32_t* __restrict__ seg_start, const uint64_t* counts,
+                                                          const uint8_t* __restrict__ hit, uint32_t ways,
+                                                          uint64_t aging_period, uint8_t* __restrict__ cfreq,
+                                                          uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
+                                                          const uint64_t* state, uint32_t* huge_list,
+                                                          unsigned long long* n_huge) {
   const uint32_t lane = lane_id();
   const uint64_t U = counts[1];
   const uint64_t clock0 = state[kSnap];
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t u = warp; u < U; u += n_warps) {
+  for (uint64_t u0 = warp * 32; u0 < U; u0 += n_warps * 32) {
+    const uint64_t u = u0 + lane;
+    const bool have = u < U;
+    uint32_t lo = 0, hi = 0;
+    uint64_t s = 0;
+    if (have) {
+      lo = seg_start[u];
+      hi = seg_start[u + 1];
+      s = sets_sorted[lo];
+    }
+    const bool mine = have && hi - lo <= kLaneMetaMax;
+    if (mine) {
+      uint32_t f[8];
+      uint64_t t[8];
+#pragma unroll
+      for (uint32_t w = 0; w < 8; ++w) {
+        f[w] = w < ways ? cfreq[s * ways + w] : 0u;
+        t[w] = w < ways ? ctouch[s * ways + w] : 0ull;
+      }
+      uint64_t acc = set_acc[s];
+      uint32_t ii[kLaneMetaMax], hw[kLaneMetaMax];
+#pragma unroll
+      for (uint32_t q = 0; q < kLaneMetaMax; ++q) ii[q] = lo + q < hi ? idx_sorted[lo + q] : 0u;
+#pragma unroll
+      for (uint32_t q = 0; q < kLaneMetaMax; ++q) hw[q] = lo + q < hi ? hit[ii[q]] : kMiss;
+#pragma unroll
+      for (uint32_t q = 0; q < kLaneMetaMax; ++q) {
+        if (lo + q >= hi) break;
+        if (++acc >= aging_period) {  // the access that completes an aging period ages first
+          acc = 0;
+#pragma unroll
+          for (uint32_t w = 0; w < 8; ++w) f[w] = age_freq(f[w]);
+        }
+#pragma unroll
+        for (uint32_t w = 0; w < 8; ++w) {
+          if (hw[q] == w) {
+            f[w] = sat_add_freq(f[w], 1u);
+            t[w] = clock0 + ii[q] + 1;
+          }
+        }
+      }
+#pragma unroll
+      for (uint32_t w = 0; w < 8; ++w) {
+        if (w < ways) {
+          cfreq[s * ways + w] = static_cast<uint8_t>(f[w]);
+          ctouch[s * ways + w] = t[w];
+        }
+      }
+      set_acc[s] = acc;
+    }
+    const bool huge = have && hi - lo > kHugeMeta;  // k_query_meta_huge replays these
+    const uint32_t hm = __ballot_sync(0xffffffffu, huge);
+    if (hm) {
+      unsigned long long b = 0;
+      if (lane == static_cast<uint32_t>(__ffs(hm) - 1)) b = atomicAdd(n_huge, static_cast<unsigned long long>(__popc(hm)));
+      b = __shfl_sync(0xffffffffu, b, __ffs(hm) - 1);
+      if (huge) huge_list[b + __popc(hm & lanemask_lt())] = static_cast<uint32_t>(u);
+    }
+    uint32_t longs = __ballot_sync(0xffffffffu, have && !mine && !huge);
+    while (longs) {
+      const int src = __ffs(longs) - 1;
+      longs &= longs - 1;
+      const uint32_t slo = __shfl_sync(0xffffffffu, lo, src), shi = __shfl_sync(0xffffffffu, hi, src);
+      const uint64_t ss = __shfl_sync(0xffffffffu, s, src);
+      meta_set_warp(idx_sorted, hit, ways, aging_period, cfreq, ctouch, set_acc, clock0, ss, slo, shi);
+    }
+  }
+}
+
+// Sets with more than kHugeMeta accesses in the batch (Zipf-head keys: thousands): one CTA
+// per set gathers the accesses' hit ways and indices into shared memory with all its
+// threads (kHugeStage at a time). Aging fires every P accesses, so (P >= 32) the whole CTA
+// counts each way's hits per aging segment and its last hit (shared atomics) and the
+// sequential part is one step per segment: f = sat(f + hits); f = age(f); ...
+// (identical to the per-access semantics). Small P: the 32-access closed form, from smem.
+constexpr uint32_t kHugeSegs = kHugeStage / 32 + 2;
+__global__ void __launch_bounds__(256) k_query_meta_huge(const uint32_t* __restrict__ sets_sorted,
+                                                         const uint32_t* __restrict__ idx_sorted,
+                                                         const uint32_t* __restrict__ seg_start,
+                                                         const uint32_t* __restrict__ huge_list, const uint64_t* n_huge,
+                                                         const uint8_t* __restrict__ hit, uint32_t ways,
+                                                         uint64_t aging_period, uint8_t* __restrict__ cfreq,
+                                                         uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
+                                                         const uint64_t* state) {
+  __shared__ uint32_t s_idx[kHugeStage];
+  __shared__ uint8_t s_hw[kHugeStage];
+  __shared__ uint16_t s_cnt[kHugeSegs][8];  // hits per (aging segment, way)
+  __shared__ uint32_t s_last[8];            // last hit position per way (+1; 0 = none)
+  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+  const uint64_t clock0 = state[kSnap];
+  const uint64_t nh = *n_huge;
+  for (uint64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    const uint32_t u = huge_list[h];
     const uint32_t lo = seg_start[u], hi = seg_start[u + 1];
     const uint64_t s = sets_sorted[lo];
-    uint32_t f = lane < ways ? cfreq[s * ways + lane] : 0u;
-    uint64_t touch = lane < ways ? ctouch[s * ways + lane] : 0ull;
-    uint64_t acc = set_acc[s];
-    for (uint32_t c = lo; c < hi; c += 32) {
-      const uint32_t j = c + lane;
-      const bool valid = j < hi;
-      const uint32_t i = valid ? idx_sorted[j] : 0u;
-      const uint32_t hw = valid ? hit[i] : kMiss;
-      const uint32_t cnt = min(32u, hi - c);
-      const bool fire = valid && ((acc + lane + 1) % aging_period == 0);
-      const uint32_t F = __ballot_sync(0xffffffffu, fire);
-      uint32_t H = 0;
-      for (uint32_t w = 0; w < ways; ++w) {
-        const uint32_t m = __ballot_sync(0xffffffffu, hw == w);
-        if (lane == w) H = m;
-      }
-      // closed form for this lane's way: saturating adds between aging points
-      uint32_t prev = 0, Fm = F;
-      while (Fm) {
-        const uint32_t b = __ffs(Fm) - 1;
-        Fm &= Fm - 1;
-        const uint32_t seg = H & (((b >= 32) ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << prev) - 1u));
-        f = age_freq(sat_add_freq(f, __popc(seg)));
-        prev = b;
-      }
-      const uint32_t tailmask = (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)) & ~((prev >= 32) ? 0xffffffffu : ((1u << prev) - 1u));
-      f = sat_add_freq(f, __popc(H & tailmask));
-      const uint32_t lastp = H ? 31u - __clz(H) : 0u;
-      const uint32_t ilast = __shfl_sync(0xffffffffu, i, lastp);
-      if (H) touch = clock0 + ilast + 1;
-      acc = (acc + cnt) % aging_period;
+    uint32_t f = 0, acc32 = 0;
+    uint64_t touch = 0;
+    if (w == 0) {
+      f = lane < ways ? cfreq[s * ways + lane] : 0u;
+      touch = lane < ways ? ctouch[s * ways + lane] : 0ull;
+      acc32 = static_cast<uint32_t>(set_acc[s]);  // < aging_period < 2^32
     }
-    if (lane < ways) {
-      cfreq[s * ways + lane] = static_cast<uint8_t>(f);
-      ctouch[s * ways + lane] = touch;
+    const uint32_t P = static_cast<uint32_t>(aging_period);
+    for (uint32_t b0 = lo; b0 < hi; b0 += kHugeStage) {
+      const uint32_t nb = min(kHugeStage, hi - b0);
+      __syncthreads();  // the previous stage is consumed
+      const uint32_t P_acc = __shfl_sync(0xffffffffu, acc32, 0);  // (warp 0's; broadcast below)
+      if (w == 0 && lane == 0) s_last[0] = P_acc;
+      __syncthreads();
+      const uint32_t acc_in = s_last[0];
+      __syncthreads();
+      const bool seg_mode = P >= 32 && ways <= 8;
+      if (seg_mode) {
+        for (uint32_t e = threadIdx.x; e < kHugeSegs * 8; e += blockDim.x) (&s_cnt[0][0])[e] = 0;
+        if (threadIdx.x < 8) s_last[threadIdx.x] = 0;
+        __syncthreads();
+      }
+      // first aging point of this stage: access q0 = P - 1 - acc_in (acc_in < P)
+      const uint32_t q0 = P - 1 - acc_in;
+      for (uint32_t q = threadIdx.x; q < nb; q += blockDim.x) {
+        const uint32_t i = idx_sorted[b0 + q];
+        const uint32_t hw = hit[i];
+        s_idx[q] = i;
+        s_hw[q] = static_cast<uint8_t>(hw);
+        if (seg_mode && hw < ways) {
+          const uint32_t k = q < q0 ? 0u : 1u + (q - q0) / P;  // segment k >= 1 starts at an aging point
+          atomicAdd(reinterpret_cast<unsigned int*>(&s_cnt[0][0]) + ((k * 8 + hw) >> 1), 1u << (16 * ((k * 8 + hw) & 1)));
+          atomicMax(&s_last[hw], q + 1);
+        }
+      }
+      __syncthreads();
+      if (seg_mode) {
+        if (w == 0) {
+          const uint32_t n_seg = nb <= q0 ? 1u : 2u + (nb - 1 - q0) / P;
+          if (lane < ways) {
+            f = sat_add_freq(f, s_cnt[0][lane]);
+            for (uint32_t k = 1; k < n_seg; ++k) f = sat_add_freq(age_freq(f), s_cnt[k][lane]);
+            if (s_last[lane]) touch = clock0 + s_idx[s_last[lane] - 1] + 1;
+          }
+          acc32 = (acc32 + nb) % P;
+        }
+        continue;
+      }
+      if (w == 0) {
+        for (uint32_t c = 0; c < nb; c += 32) {
+          const uint32_t q = c + lane;
+          const bool valid = q < nb;
+          const uint32_t hw = valid ? s_hw[q] : kMiss;
+          const uint32_t cnt = min(32u, nb - c);
+          const bool fire = valid && (acc32 + lane + 1) % P == 0;
+          const uint32_t F = __ballot_sync(0xffffffffu, fire);
+          uint32_t H = 0;
+          for (uint32_t ww = 0; ww < ways; ++ww) {
+            const uint32_t m = __ballot_sync(0xffffffffu, hw == ww);
+            if (lane == ww) H = m;
+          }
+          uint32_t prev = 0, Fm = F;
+          while (Fm) {
+            const uint32_t b = __ffs(Fm) - 1;
+            Fm &= Fm - 1;
+            const uint32_t seg = H & (((b >= 32) ? 0xffffffffu : ((1u << b) - 1u)) & ~((1u << prev) - 1u));
+            f = age_freq(sat_add_freq(f, __popc(seg)));
+            prev = b;
+          }
+          const uint32_t tailmask =
+              (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u)) & ~((prev >= 32) ? 0xffffffffu : ((1u << prev) - 1u));
+          f = sat_add_freq(f, __popc(H & tailmask));
+          if (H) touch = clock0 + s_idx[c + 31u - __clz(H)] + 1;
+          acc32 = (acc32 + cnt) % P;
+        }
+      }
     }
-    if (lane == 0) set_acc[s] = acc;
+    if (w == 0) {
+      if (lane < ways) {
+        cfreq[s * ways + lane] = static_cast<uint8_t>(f);
+        ctouch[s * ways + lane] = touch;
+      }
+      if (lane == 0) set_acc[s] = acc32;
+    }
   }
 }
 
@@ -577,6 +788,35 @@ int hps_gpu_cache_destroy(hps_gpu_cache c) {
   return HPS_GPU_OK;
 }
 
+// HPS_GPU_CACHE_PHASES=1 (debug): per-stage device times of each query, to stderr.
+struct QueryPhases {
+  bool on = false;
+  cudaEvent_t ev[6] = {};
+  int k = 0;
+  explicit QueryPhases(cudaStream_t st) : st_(st) {
+    const char* e = std::getenv("HPS_GPU_CACHE_PHASES");
+    on = e && e[0] == '1';
+    if (on)
+      for (auto& x : ev) cudaEventCreate(&x);
+  }
+  void mark() {
+    if (on && k < 6) cudaEventRecord(ev[k++], st_);
+  }
+  ~QueryPhases() {
+    if (!on) return;
+    cudaEventSynchronize(ev[k - 1]);
+    std::fprintf(stderr, "# cache query phases (us):");
+    for (int i = 1; i < k; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      std::fprintf(stderr, " %.1f", ms * 1000.f);
+    }
+    std::fprintf(stderr, "  [probe+split | gather | sort+segment | meta]\n");
+    for (auto& x : ev) cudaEventDestroy(x);
+  }
+  cudaStream_t st_;
+};
+
 int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float* found_vecs, uint32_t* found_idx,
                         uint32_t* missing_idx, uint64_t* counts) {
   if (int s = check_cache(c)) return s;
@@ -588,6 +828,8 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
     return HPS_GPU_OK;
   }
   if (!keys) return HPS_GPU_E_INVALID_ARGUMENT;
+  QueryPhases ph(st);
+  ph.mark();
   k_probe<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(keys, n, c->set_mod, c->ways, c->d_keys, c->d_freq,
                                                           c->ws_set, c->ws_hit, c->d_state, c->ws_counts);
   const uint64_t tiles = scan_tiles(n);
@@ -596,6 +838,7 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
   k_scan<SplitOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(op, c->ws_scan,
                                                                        reinterpret_cast<uint32_t*>(c->ws_scan + tiles));
   HPSG_CHECK_LAUNCH("cache probe/split");
+  ph.mark();
   if (found_vecs) {
     const int lpr = lpr_for(c->dim);
     const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
@@ -615,12 +858,26 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
 #undef HPSG_G
     HPSG_CHECK_LAUNCH("cache gather");
   }
+  ph.mark();
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, c->set_bits, &sets_sorted, &idx_sorted)) return s;
-  k_query_meta<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, c->ws_hit, c->ways,
-                                                  c->aging_period, c->d_freq, c->d_touch, c->d_set_acc, c->d_state);
+  ph.mark();
+  if (c->ways <= 8) {
+    auto* n_huge = reinterpret_cast<unsigned long long*>(c->ws_counts + 4);
+    HPSG_CUDA(cudaMemsetAsync(n_huge, 0, sizeof(unsigned long long), st));
+    k_query_meta_lanes<<<grid_for((n + 31) / 32 * 32, 256, kNumSMs * 16), 256, 0, st>>>(
+        sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, c->ws_hit, c->ways, c->aging_period, c->d_freq, c->d_touch,
+        c->d_set_acc, c->d_state, c->ws_rank, n_huge);
+    k_query_meta_huge<<<kNumSMs, 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_rank,
+                                               reinterpret_cast<const uint64_t*>(n_huge), c->ws_hit, c->ways,
+                                               c->aging_period, c->d_freq, c->d_touch, c->d_set_acc, c->d_state);
+  } else
+    k_query_meta<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, c->ws_hit,
+                                                    c->ways, c->aging_period, c->d_freq, c->d_touch, c->d_set_acc,
+                                                    c->d_state);
   HPSG_CHECK_LAUNCH("cache meta");
+  ph.mark();
   return HPS_GPU_OK;
 }
 
