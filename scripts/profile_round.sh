@@ -19,6 +19,10 @@ bash scripts/launches.sh ${TAG} cfg2 cfg3
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_probe|k_lookup_1hot_tma|k_dedup|k_reduce_short|k_long<" \
   -s 15 -c 5 -o gpurun_out/full_cfg2_${TAG} python bench.py --steps 3 --warmup 3 --pool 1 --no-cpu-baseline --e2e-steps 1 --no-graph > gpurun_out/ncu_full_${TAG}.log 2>&1
 # the roofline kernel: the fused inference lookup (bench's lookup_only leg)
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_lookup_1hot_tma" \
-  -s 6 -c 1 -o gpurun_out/full_fwd_cfg2_${TAG} python bench.py --steps 3 --warmup 3 --pool 1 --no-cpu-baseline --e2e-steps 1 --no-graph > gpurun_out/ncu_fwd_${TAG}.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"tma<\(bool\)0>" \
+  -c 1 -o gpurun_out/full_fwd_cfg2_${TAG} python bench.py --steps 3 --warmup 3 --pool 1 --no-cpu-baseline --e2e-steps 1 --no-graph > gpurun_out/ncu_fwd_${TAG}.log 2>&1
 ls gpurun_out | grep ${TAG}
+# config 4 (HPS cache) sweeps, f32 and f16 rows
+timeout 900 python bench_cache.py --reps 30 > gpurun_out/bench_cfg4_${TAG}.jsonl 2> gpurun_out/bench_cfg4_${TAG}.err
+timeout 900 python bench_cache.py --reps 30 --no-cpu --dtype f16 > gpurun_out/bench_cfg4_f16_${TAG}.jsonl 2>&1
+tail -1 gpurun_out/bench_cfg4_${TAG}.jsonl | cut -c1-300
