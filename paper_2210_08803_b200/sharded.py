@@ -168,6 +168,9 @@ class TrainStep:
         self.kernels_per_step = rec + 1 + 2  # + pooling
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self._cnt_host = torch.zeros(1, dtype=torch.int64).pin_memory()
+        # pipelined e2e (run_host_async): one pinned result slot + event per step in flight
+        self._cnt_slots = [torch.zeros(1, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self._slot_ev = [torch.cuda.Event() for _ in range(2)]
         self.exchange = None
         if multi and owned is not None:
             from .exchange import LocalizedExchange, LocalizedGpuEngine
@@ -248,10 +251,49 @@ class TrainStep:
             return self._eager(b, dout, step)
         self._graph((id(b["keys"]), id(dout)), lambda: self._eager(b, dout, step))
 
-    def _host_step(self, b, dout, step):
+    def _host_step(self, b, dout, step, out=None):
         self._eager(b, dout, step, keys_on_host=True)
         L.check(self.ctx.lib.hps_gpu_table_last_unique(self.table.h, _ptr(self._cnt), None), "last_unique")
-        self._cnt_host.copy_(self._cnt, non_blocking=True)
+        (self._cnt_host if out is None else out).copy_(self._cnt, non_blocking=True)
+
+    def run_host_async(self, b, dout, step: int, slot: int):
+        """End-to-end step from pinned HOST keys, pipelined one step deep: the keys go H2D on a
+        copy stream into device staging slot `slot` (while the previous step computes), the
+        step (kernels + the D2H of its result into pinned slot `slot`) follows on the main
+        stream; read_host_result(slot) waits for it. Every step moves its inputs H2D and its
+        result D2H inside the timed region; the copies overlap the previous step's kernels."""
+        h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
+        if self.exchange is not None or not self.graph_mode or b["offs"] is not None:
+            self.run_host(b, dout, step)
+            self._cnt_slots[slot].copy_(self._cnt_host)
+            self._slot_ev[slot].record()
+            return h2d, 8
+        if not hasattr(self, "_copy_stream"):
+            self._copy_stream = torch.cuda.Stream()
+            n = self.n_bags
+            self._dev_keys = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(2)]
+            self._copy_ev = [torch.cuda.Event() for _ in range(2)]
+        main = torch.cuda.current_stream()
+        with torch.cuda.stream(self._copy_stream):
+            self._copy_stream.wait_event(self._slot_ev[slot])  # the slot's previous step is done with it
+            self._dev_keys[slot].copy_(b["keys"], non_blocking=True)
+            self._copy_ev[slot].record()
+        main.wait_event(self._copy_ev[slot])
+        dk = {"keys": self._dev_keys[slot], "offs": None, "n_keys": b["n_keys"]}
+        out = self._cnt_slots[slot]
+
+        def dev_step():
+            self._eager(dk, dout, step)
+            L.check(self.ctx.lib.hps_gpu_table_last_unique(self.table.h, _ptr(self._cnt), None), "last_unique")
+            out.copy_(self._cnt, non_blocking=True)
+
+        self._graph(("dev", slot, id(dout)), dev_step)
+        self._slot_ev[slot].record()
+        return h2d, 8
+
+    def read_host_result(self, slot: int) -> int:
+        self._slot_ev[slot].synchronize()
+        return int(self._cnt_slots[slot][0])
 
     def run_host(self, b, dout, step: int = 1):
         """End-to-end through the C-ABI: keys from pinned host memory (H2D inside the call),
