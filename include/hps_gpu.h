@@ -97,6 +97,8 @@ typedef struct hps_gpu_table_s* hps_gpu_table;
 
 enum { HPS_OPT_SGD = 0, HPS_OPT_ADAGRAD = 1, HPS_OPT_ADAM = 2 };
 enum { HPS_COMBINER_SUM = 0, HPS_COMBINER_MEAN = 1 };
+/* Storage dtype of table / cached rows (hps::Dtype, proj/include/hps/types.hpp:36-40). */
+enum { HPS_DTYPE_F32 = 0, HPS_DTYPE_F16 = 1 };
 
 typedef struct {
   uint32_t n_tables;
@@ -109,6 +111,11 @@ typedef struct {
   uint64_t max_batch_bags;          /* workspace sizing: bags per lookup call */
   uint64_t init_seed;               /* row initialiser seed (see hps_gpu_init_value) */
   float adagrad_initial_accumulator;/* AdaGrad a0 (state rows start at this) */
+  uint32_t dtype;                   /* HPS_DTYPE_F32 (0, default) or HPS_DTYPE_F16: binary16 rows, an
+                                       inference table (insert/find/export/lookup/read-through;
+                                       training calls on it -> DtypeMismatch). Insert rounds to
+                                       nearest even; a row beyond binary16 range -> F16Range
+                                       (latched, the call refused) — SPEC.md:78-86 */
 } hps_table_config;
 
 typedef struct {
@@ -258,9 +265,6 @@ int hps_gpu_apply_grads(hps_gpu_table tbl, const float* grads, const uint32_t* t
 
 /* ---- HPS inference cache (K6..K8), SPEC.md:112-190 ---------------------------- */
 typedef struct hps_gpu_cache_s* hps_gpu_cache;
-
-/* Storage dtype of cached rows (hps::Dtype, proj/include/hps/types.hpp:36-40). */
-enum { HPS_DTYPE_F32 = 0, HPS_DTYPE_F16 = 1 };
 
 typedef struct {
   uint64_t capacity;        /* resident entries; capacity % ways == 0 */

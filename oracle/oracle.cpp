@@ -91,9 +91,12 @@ struct Table {
   int last_combiner = 0;
   uint64_t last_n_bags = 0;
   std::vector<uint32_t> last_unique;
+  bool f16 = false;  // binary16 rows (inference table): stored as their exact fp32 widening
 
   int n_state() const { return optimizer == 0 ? 0 : optimizer == 1 ? 1 : 2; }
 };
+float f16_round_trip(float x);
+bool f16_overflows(float x);
 
 // DESIGN.md §4.1 insert: new keys get rows in order of first occurrence, continuing
 // from the table's row count; with `rows`, every distinct key of the call (new or
@@ -107,6 +110,9 @@ int table_insert(Table* t, uint32_t table, const uint64_t* keys, uint64_t n, con
   if (rows) {
     for (uint64_t i = 0; i < n * D; ++i)
       if (non_finite(rows[i])) return 10;
+    if (t->f16)  // binary16 table: a value whose rounding overflows refuses the call (F16Range)
+      for (uint64_t i = 0; i < n * D; ++i)
+        if (f16_overflows(rows[i])) return 9;
   }
   uint64_t new_cnt = 0;
   {
@@ -138,6 +144,8 @@ int table_insert(Table* t, uint32_t table, const uint64_t* keys, uint64_t n, con
     }
     if (rows && written.emplace(keys[i], 1).second)
       std::memcpy(&t->w[g * D], &rows[i * D], D * sizeof(float));
+    if (t->f16 && (fresh || rows))  // rows are held rounded to binary16
+      for (uint32_t j = 0; j < D; ++j) t->w[g * D + j] = f16_round_trip(t->w[g * D + j]);
     if (rows_out) rows_out[i] = local;
   }
   return 0;
@@ -487,6 +495,7 @@ void* orc_table_create(uint32_t n_tables, uint32_t dim, const uint64_t* caps, ui
   return t;
 }
 void orc_table_destroy(void* h) { delete static_cast<Table*>(h); }
+void orc_table_set_dtype(void* h, int dtype) { static_cast<Table*>(h)->f16 = dtype == 1; }
 void orc_table_set_default(void* h, uint32_t table, const float* v) {
   auto* t = static_cast<Table*>(h);
   std::memcpy(t->defaults[table].data(), v, t->dim * sizeof(float));

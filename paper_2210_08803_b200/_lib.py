@@ -46,6 +46,7 @@ class TableConfig(C.Structure):
         ("max_batch_bags", u64),
         ("init_seed", u64),
         ("adagrad_initial_accumulator", f32),
+        ("dtype", u32),  # HPS_DTYPE_F32 = 0, HPS_DTYPE_F16 = 1 (inference table)
     ]
 
 

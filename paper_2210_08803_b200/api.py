@@ -107,8 +107,13 @@ class EmbeddingTableGroup:
 
     def __init__(self, ctx: Context, row_capacity: Sequence[int], dim: int, slot_table: Sequence[int],
                  optimizer: str = "sgd", max_batch_keys: int = 1 << 20, max_batch_bags: int = 1 << 20,
-                 init_seed: int = 0, adagrad_initial_accumulator: float = 0.0):
+                 init_seed: int = 0, adagrad_initial_accumulator: float = 0.0, dtype: str = "f32"):
+        """dtype "f16": binary16 rows, an inference table (lookups without training, find,
+        export, read-through); insert rounds to nearest even, out-of-range rows -> F16Range."""
+        if dtype not in ("f32", "f16"):
+            raise HpsError(1, "dtype must be 'f32' or 'f16'")
         self.ctx, self.lib = ctx, ctx.lib
+        self.dtype = dtype
         self.dim, self.optimizer = dim, optimizer
         self.n_tables, self.n_slots = len(row_capacity), len(slot_table)
         self.row_capacity = list(row_capacity)
@@ -116,7 +121,7 @@ class EmbeddingTableGroup:
         caps = (L.u64 * self.n_tables)(*row_capacity)
         st = (L.u32 * self.n_slots)(*slot_table)
         cfg = L.TableConfig(self.n_tables, dim, caps, self.n_slots, st, _OPT[optimizer], max_batch_keys,
-                            max_batch_bags, init_seed, adagrad_initial_accumulator)
+                            max_batch_bags, init_seed, adagrad_initial_accumulator, 1 if dtype == "f16" else 0)
         h = C.c_void_p()
         L.check(self.lib.hps_gpu_table_create(ctx.h, C.byref(cfg), C.byref(h)), "table_create")
         self.h = h

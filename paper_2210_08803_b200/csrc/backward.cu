@@ -1230,6 +1230,7 @@ int hps_gpu_backward_reduce(hps_gpu_table t, const float* d_out, float* grads_ou
 
 int hps_gpu_apply_grads(hps_gpu_table t, const float* grads, const uint32_t* touched, const hps_opt_params* opt) {
   if (!t || !grads || !touched || !opt) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (t->f16) return HPS_GPU_E_DTYPE_MISMATCH;  // an F16 table is an inference table
   BwdArgs a{};
   a.dim = t->dim;
   a.W = t->d_w;

@@ -1,6 +1,7 @@
 // common.cuh — shared device helpers for the sm_100a sparse-embedding kernels.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -97,6 +98,16 @@ __device__ __forceinline__ float4 ldg_stream(const float4* p) {
                : "l"(p));
   return v;
 }
+
+// Four binary16 values [4v, 4v+4) of a row, widened to fp32 (exact).
+__device__ __forceinline__ float4 ldg_half4(const uint16_t* p, uint32_t v) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p) + v);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+// fp32 -> binary16 bits, round to nearest even (cvt.rn.f16.f32; kernels_scalar.cpp:25-57).
+__device__ __forceinline__ uint16_t f32_to_half_bits(float x) { return __half_as_ushort(__float2half_rn(x)); }
 
 __device__ __forceinline__ float4 f4_add(float4 a, float4 b) {
   return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z), __fadd_rn(a.w, b.w));

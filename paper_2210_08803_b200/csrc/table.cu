@@ -146,7 +146,7 @@ __global__ void k_insert_commit(Slot* __restrict__ slots, TableDev td, uint32_t 
                                 const uint64_t* __restrict__ d_new, const uint64_t* __restrict__ d_nrows,
                                 float* __restrict__ W, float* __restrict__ S0, float* __restrict__ S1, int n_state,
                                 float a0, uint32_t dim, uint64_t seed, uint64_t* __restrict__ row_keys,
-                                uint32_t* abort_flag, uint32_t* status) {
+                                uint32_t* abort_flag, uint32_t* status, uint16_t* __restrict__ Wh) {
   if (*reinterpret_cast<volatile uint32_t*>(abort_flag)) return;
   const uint64_t nrows = d_nrows[table];
   if (nrows + *d_new > td.row_cap) {
@@ -184,9 +184,10 @@ __global__ void k_insert_commit(Slot* __restrict__ slots, TableDev td, uint32_t 
       const uint64_t kr = __shfl_sync(0xffffffffu, key, src);
       const uint8_t fr = static_cast<uint8_t>(__shfl_sync(0xffffffffu, static_cast<uint32_t>(f), src));
       const uint64_t ir = w0 + src;
-      float* wr = W + gr * dim;
       for (uint32_t j = lane; j < dim; j += 32) {
-        wr[j] = rows ? rows[ir * dim + j] : init_value(seed, kr, j);
+        const float val = rows ? rows[ir * dim + j] : init_value(seed, kr, j);
+        if (Wh) Wh[gr * dim + j] = f32_to_half_bits(val);  // F16 table: round to nearest even
+        else W[gr * dim + j] = val;
         if (fr & 1) {
           if (n_state >= 1) S0[gr * dim + j] = (n_state == 1) ? a0 : 0.0f;
           if (n_state >= 2) S1[gr * dim + j] = 0.0f;
@@ -230,14 +231,29 @@ __global__ void k_insert_finish(Slot* __restrict__ slots, TableDev td, uint32_t 
   if (!ab && blockIdx.x == 0 && threadIdx.x == 0) d_nrows[table] += *d_new;
 }
 
-__global__ void k_rows_non_finite(const float* __restrict__ v, uint64_t n, uint32_t* abort_flag, uint32_t* status) {
-  bool bad = false;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    bad |= non_finite_bits(__float_as_uint(v[i]));
+// Ingest validation (the whole call is refused before any claim): NaN/Inf -> NonFinite; for
+// an F16 table, a value whose binary16 rounding overflows (|x| >= 65520) -> F16Range.
+__global__ void k_rows_non_finite(const float* __restrict__ v, uint64_t n, uint32_t* abort_flag, uint32_t* status,
+                                  int f16) {
+  bool bad = false, range = false;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = __float_as_uint(v[i]);
+    bad |= non_finite_bits(b);
+    range |= f16 && (b & 0x7fffffffu) >= 0x477ff000u && !non_finite_bits(b);
+  }
   if (__any_sync(0xffffffffu, bad) && lane_id() == 0) {
     latch_status(status, HPS_GPU_E_NON_FINITE);
     atomicMax(abort_flag, 1u);
   }
+  if (__any_sync(0xffffffffu, range) && lane_id() == 0) {
+    latch_status(status, HPS_GPU_E_F16_RANGE);
+    atomicMax(abort_flag, 1u);
+  }
+}
+
+__global__ void k_widen_half(const uint16_t* __restrict__ src, uint64_t n, float* __restrict__ dst) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] = __half2float(__ushort_as_half(src[i]));
 }
 
 __global__ void k_fill_u64(uint64_t* p, uint64_t n, uint64_t v) {
@@ -262,6 +278,7 @@ struct LookupArgs {
   const TableDev* tables;
   const Slot* slots;
   const float* W;
+  const uint16_t* Wh;  // F16 table: binary16 rows (W unused)
   const float* defaults;
   uint32_t dim;
   int mean;
@@ -356,7 +373,7 @@ __device__ __forceinline__ uint32_t occurrence_row(const LookupArgs& a, uint64_t
 // row (32 independent index loads in flight); then groups of LPR lanes stream the rows
 // with 128-bit loads (VPL float4 per lane, 8 rows in flight per group) and write the bags
 // coalesced.
-template <int LPR, int VPL, bool ROWS>
+template <int LPR, int VPL, bool ROWS, bool F16 = false>
 __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
   constexpr int G = 32 / LPR;  // rows handled side by side by one warp
   constexpr int kBatch = (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) > 0 ? (LPR < 8 ? LPR : 8) / (VPL > 4 ? 4 : VPL) : 1;
@@ -380,12 +397,13 @@ __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
         const uint32_t r = __shfl_sync(0xffffffffu, row, src);
         const uint32_t tb = __shfl_sync(0xffffffffu, table, src);
         const float4* p = reinterpret_cast<const float4*>(r == kRowEmpty ? a.defaults + uint64_t(tb) * a.dim
-                                                                         : a.W + uint64_t(r) * a.dim);
+                                                                         : (F16 ? a.defaults : a.W + uint64_t(r) * a.dim));
+        const uint16_t* ph = (F16 && r != kRowEmpty) ? a.Wh + uint64_t(r) * a.dim : nullptr;
         const bool ok = t0 + src < a.n_bags;
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
           const uint32_t v = gl + k * LPR;
-          x[j][k] = (ok && v < nvec) ? ldg_stream(p + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+          x[j][k] = (ok && v < nvec) ? (F16 && ph ? ldg_half4(ph, v) : ldg_stream(p + v)) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
 #pragma unroll
@@ -473,7 +491,8 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
                                                       const Slot* __restrict__ slots, TableDev td,
                                                       const float* __restrict__ W, const float* __restrict__ def,
                                                       uint32_t dim, float* __restrict__ out, uint64_t* miss_keys,
-                                                      float* miss_vecs, uint8_t* miss_absent) {
+                                                      float* miss_vecs, uint8_t* miss_absent,
+                                                      const uint16_t* __restrict__ Wh) {
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
   const uint64_t nf = counts[0], nm = counts[1];
@@ -481,6 +500,7 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
   const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
   for (uint64_t j = gid; j < nf + nm; j += ng) {
     const float4* src;
+    const uint16_t* srch = nullptr;  // F16 table row (widened on the fly)
     float4* dst2 = nullptr;
     uint32_t i;
     if (j < nf) {
@@ -491,7 +511,8 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
       i = missing_idx[m];
       const uint64_t k = keys[i];
       const uint32_t local = probe_find(slots, td, k);
-      src = reinterpret_cast<const float4*>(local == kRowEmpty ? def : W + (td.row_base + local) * dim);
+      src = reinterpret_cast<const float4*>(local == kRowEmpty || Wh ? def : W + (td.row_base + local) * dim);
+      if (Wh && local != kRowEmpty) srch = Wh + (td.row_base + local) * dim;
       dst2 = reinterpret_cast<float4*>(miss_vecs + m * dim);
       if (gl == 0) {
         miss_keys[m] = k;
@@ -500,7 +521,7 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
     }
     float4* dst = reinterpret_cast<float4*>(out + uint64_t(i) * dim);
     for (uint32_t v = gl; v < nvec; v += LPR) {
-      const float4 x = __ldg(src + v);
+      const float4 x = srch ? ldg_half4(srch, v) : __ldg(src + v);
       dst[v] = x;
       if (dst2) dst2[v] = x;
     }
@@ -509,7 +530,7 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
 
 // Multi-hot path: a group of LPR lanes owns one bag at a time; the group resolves LPR
 // keys of the bag in parallel, then accumulates the rows in bag order (4 in flight).
-template <int LPR, int VPL, bool ROWS>
+template <int LPR, int VPL, bool ROWS, bool F16 = false>
 __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id();
@@ -535,12 +556,14 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
         for (int j = 0; j < 4; ++j) {
           const uint32_t m = m0 + j;
           const uint32_t r = __shfl_sync(gmask, row, grp * LPR + (m < LPR ? m : 0));
-          const float4* p = reinterpret_cast<const float4*>(r == kRowEmpty ? a.defaults + uint64_t(table) * a.dim
-                                                                           : a.W + uint64_t(r) * a.dim);
+          const float4* p = reinterpret_cast<const float4*>(
+              r == kRowEmpty ? a.defaults + uint64_t(table) * a.dim : (F16 ? a.defaults : a.W + uint64_t(r) * a.dim));
+          const uint16_t* ph = (F16 && r != kRowEmpty) ? a.Wh + uint64_t(r) * a.dim : nullptr;
 #pragma unroll
           for (int k = 0; k < VPL; ++k) {
             const uint32_t v = gl + k * LPR;
-            x[j][k] = (m < cnt && v < nvec) ? ldg_stream(p + v) : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[j][k] = (m < cnt && v < nvec) ? (F16 && ph ? ldg_half4(ph, v) : ldg_stream(p + v))
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
 #pragma unroll
@@ -738,9 +761,38 @@ int fork_dedup(hps_gpu_table t) {
 
 // Pooled lookup. ROWS (training): rows come from the record (record() ran first);
 // otherwise hash + probe + gather + pool in one pass.
+#define HPSG_DISPATCH_ROW16(KERNEL, GRIDF, ...)                                          \
+  do {                                                                                    \
+    if (nvec > 128) KERNEL<32, 8, false, true><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec > 64) KERNEL<32, 4, false, true><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);\
+    else if (nvec > 32) KERNEL<32, 2, false, true><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);\
+    else if (nvec == 32) KERNEL<32, 1, false, true><<<GRIDF(32), 256, 0, st>>>(__VA_ARGS__);\
+    else if (nvec > 16) KERNEL<16, 2, false, true><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);\
+    else if (nvec == 16) KERNEL<16, 1, false, true><<<GRIDF(16), 256, 0, st>>>(__VA_ARGS__);\
+    else if (nvec > 8) KERNEL<8, 2, false, true><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec == 8) KERNEL<8, 1, false, true><<<GRIDF(8), 256, 0, st>>>(__VA_ARGS__);  \
+    else if (nvec > 4) KERNEL<4, 2, false, true><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec == 4) KERNEL<4, 1, false, true><<<GRIDF(4), 256, 0, st>>>(__VA_ARGS__);  \
+    else if (nvec > 2) KERNEL<2, 2, false, true><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);   \
+    else if (nvec == 2) KERNEL<2, 1, false, true><<<GRIDF(2), 256, 0, st>>>(__VA_ARGS__);  \
+    else KERNEL<1, 1, false, true><<<GRIDF(1), 256, 0, st>>>(__VA_ARGS__);                 \
+  } while (0)
+
 int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
   const cudaStream_t st = t->ctx->stream;
   const uint32_t nvec = t->dim / 4;
+  if (t->f16) {  // inference table: binary16 rows widened in the register paths
+    auto grid1 = [&](int) { return grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * 64); };
+    auto gridm = [&](int lpr) {
+      const uint64_t groups_per_block = 8 * (32 / lpr);
+      return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((a.n_bags + groups_per_block - 1) / groups_per_block,
+                                                                       kNumSMs * 64)));
+    };
+    if (multi) HPSG_DISPATCH_ROW16(k_lookup_multi, gridm, a);
+    else HPSG_DISPATCH_ROW16(k_lookup_1hot, grid1, a);
+    HPSG_CHECK_LAUNCH("lookup f16");
+    return HPS_GPU_OK;
+  }
   const bool tma_ok = t->dim <= 256 && (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0 && !t->no_tma;
   if (!multi && tma_ok) {
     static bool attr = false;
@@ -809,6 +861,13 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->n_slots = cfg->n_slots;
   t->optimizer = cfg->optimizer;
   t->n_state = cfg->optimizer == HPS_OPT_SGD ? 0 : cfg->optimizer == HPS_OPT_ADAGRAD ? 1 : 2;
+  if (cfg->dtype != HPS_DTYPE_F32 && cfg->dtype != HPS_DTYPE_F16) {
+    delete t;
+    set_last_error("table config: dtype must be HPS_DTYPE_F32 or HPS_DTYPE_F16");
+    return HPS_GPU_E_DTYPE_MISMATCH;
+  }
+  t->f16 = cfg->dtype == HPS_DTYPE_F16;
+  if (t->f16) t->n_state = 0;  // an inference table holds no optimizer state
   t->seed = cfg->init_seed;
   t->a0 = cfg->adagrad_initial_accumulator;
   t->max_keys = cfg->max_batch_keys;
@@ -851,7 +910,8 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   };
   A(dalloc(&t->d_tables, t->n_tables));
   A(dalloc(&t->d_slots, slots));
-  A(dalloc(&t->d_w, rows * D));
+  if (t->f16) A(dalloc(&t->d_wh, rows * D));
+  else A(dalloc(&t->d_w, rows * D));
   if (t->n_state >= 1) A(dalloc(&t->d_s0, rows * D));
   if (t->n_state >= 2) A(dalloc(&t->d_s1, rows * D));
   A(dalloc(&t->d_row_keys, rows));
@@ -925,7 +985,7 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
 
 int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
-  void* ptrs[] = {t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
+  void* ptrs[] = {t->d_wh,        t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
                   t->ws_bt,       t->ws_occ_ent,   t->ws_lead,   t->ws_long_ent,  t->ws_rank,      t->ws_short_rec, t->ws_short_bag,  t->ws_occ_bag,
                   t->ws_bag_len,  t->ws_long_row,  t->ws_long_len,  t->ws_long_start, t->ws_lkey_a,
@@ -1002,7 +1062,7 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
   HPSG_CUDA(cudaMemsetAsync(t->ws_counts + 3, 0, sizeof(uint64_t), st));
   const int grid = grid_for(n, 256, kNumSMs * 32);
   if (rows) k_rows_non_finite<<<grid_for(n * t->dim, 256, kNumSMs * 32), 256, 0, st>>>(rows, n * t->dim, t->ws_abort,
-                                                                                      t->ctx->d_status);
+                                                                                      t->ctx->d_status, t->f16 ? 1 : 0);
   k_insert_claim<<<grid, 256, 0, st>>>(t->d_slots, td, keys, n, ws_slot, t->ws_abort, t->ctx->d_status,
                                        rows == nullptr && rows_out == nullptr);
   InsertScanOp op{t->d_slots, td.slot_base, ws_slot, ws_pos, ws_flag, n, t->ws_counts + 3, t->ws_abort};
@@ -1010,7 +1070,7 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
       op, scan_status, reinterpret_cast<uint32_t*>(scan_status + tiles));
   k_insert_commit<<<grid, 256, 0, st>>>(t->d_slots, td, table, keys, n, rows, ws_slot, ws_pos, ws_flag,
                                         t->ws_counts + 3, t->d_nrows, t->d_w, t->d_s0, t->d_s1, t->n_state, t->a0,
-                                        t->dim, t->seed, t->d_row_keys, t->ws_abort, t->ctx->d_status);
+                                        t->dim, t->seed, t->d_row_keys, t->ws_abort, t->ctx->d_status, t->d_wh);
   k_insert_finish<<<grid, 256, 0, st>>>(t->d_slots, td, table, n, ws_slot, rows_out, t->ws_counts + 3, t->d_nrows,
                                         t->ws_abort);
   HPSG_CHECK_LAUNCH("insert");
@@ -1040,7 +1100,12 @@ int hps_gpu_table_export(hps_gpu_table t, uint32_t table, uint64_t row_begin, ui
   if (row_begin + n > t->row_cap[table]) return HPS_GPU_E_INVALID_ARGUMENT;
   const uint64_t off = (t->row_base[table] + row_begin) * t->dim, bytes = n * t->dim * sizeof(float);
   cudaStream_t st = t->ctx->stream;
-  if (w) HPSG_CUDA(cudaMemcpyAsync(w, t->d_w + off, bytes, cudaMemcpyDeviceToDevice, st));
+  if (w && t->f16) {  // binary16 rows widened exactly
+    k_widen_half<<<grid_for(n * t->dim, 256, kNumSMs * 16), 256, 0, st>>>(t->d_wh + off, n * t->dim, w);
+    HPSG_CHECK_LAUNCH("k_widen_half");
+  } else if (w) {
+    HPSG_CUDA(cudaMemcpyAsync(w, t->d_w + off, bytes, cudaMemcpyDeviceToDevice, st));
+  }
   if (s0 && t->n_state >= 1) HPSG_CUDA(cudaMemcpyAsync(s0, t->d_s0 + off, bytes, cudaMemcpyDeviceToDevice, st));
   if (s1 && t->n_state >= 2) HPSG_CUDA(cudaMemcpyAsync(s1, t->d_s1 + off, bytes, cudaMemcpyDeviceToDevice, st));
   return HPS_GPU_OK;
@@ -1094,6 +1159,10 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
     if (int s = hps_gpu_table_insert(t, 0, keys, n_keys_host, nullptr, nullptr)) return s;
   }
   const bool train = (flags & HPS_LOOKUP_TRAIN) != 0;
+  if (train && t->f16) {
+    set_last_error("lookup: an F16 table is an inference table (no training lookups)");
+    return HPS_GPU_E_DTYPE_MISMATCH;
+  }
   LookupArgs a{};
   a.keys = keys;
   a.offsets = offsets;
@@ -1103,6 +1172,7 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   a.tables = t->d_tables;
   a.slots = t->d_slots;
   a.W = t->d_w;
+  a.Wh = t->d_wh;
   a.defaults = t->d_defaults;
   a.dim = t->dim;
   a.mean = combiner == HPS_COMBINER_MEAN;
@@ -1135,12 +1205,12 @@ int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* 
   const TableDev td = t->h_tables[table];
   const float* def = t->d_defaults + uint64_t(table) * t->dim;
   switch (lpr) {
-    case 32: k_read_through<32><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
-    case 16: k_read_through<16><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
-    case 8: k_read_through<8><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
-    case 4: k_read_through<4><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
-    case 2: k_read_through<2><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
-    default: k_read_through<1><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent); break;
+    case 32: k_read_through<32><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 16: k_read_through<16><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 8: k_read_through<8><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 4: k_read_through<4><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 2: k_read_through<2><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    default: k_read_through<1><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
   }
   HPSG_CHECK_LAUNCH("k_read_through");
   return HPS_GPU_OK;
@@ -1150,6 +1220,7 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
                          int combiner, uint64_t n_keys_host, uint32_t* cold_pos_out, uint64_t* cold_keys_out,
                          uint32_t* cold_bags_out, uint64_t* cold_count_out) {
   if (int s = check_tbl(t)) return s;
+  if (t->f16) return HPS_GPU_E_DTYPE_MISMATCH;  // hybrid hot tables train
   const uint64_t n_bags = uint64_t(n_samples) * t->n_slots;
   const bool multi = offsets != nullptr;
   if (!multi) n_keys_host = n_bags;
@@ -1188,6 +1259,7 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
 int hps_gpu_hybrid_pool(hps_gpu_table t, const uint32_t* cold_pos, const uint32_t* perm, const float* cold_rows,
                         const uint32_t* offsets, uint64_t n_bags, int combiner, float* out) {
   if (int s = check_tbl(t)) return s;
+  if (t->f16) return HPS_GPU_E_DTYPE_MISMATCH;
   if (n_bags == 0) return HPS_GPU_OK;
   if (!cold_pos || !out || (!cold_rows && perm)) return HPS_GPU_E_INVALID_ARGUMENT;
   const uint32_t nvec = t->dim / 4;
@@ -1219,6 +1291,10 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
   const bool train = (flags & HPS_LOOKUP_TRAIN) != 0;
+  if (train && t->f16) {
+    set_last_error("gather_rows: an F16 table is an inference table (no training lookups)");
+    return HPS_GPU_E_DTYPE_MISMATCH;
+  }
   if (n == 0) {
     t->have_train = false;
     return HPS_GPU_OK;
@@ -1237,6 +1313,7 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
   a.tables = t->d_tables;
   a.slots = t->d_slots;
   a.W = t->d_w;
+  a.Wh = t->d_wh;
   a.defaults = t->d_defaults;
   a.dim = t->dim;
   a.out = rows_out;

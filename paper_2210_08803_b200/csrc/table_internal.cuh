@@ -67,7 +67,9 @@ struct hps_gpu_table_s {
   // device state
   hpsg::TableDev* d_tables = nullptr;
   hpsg::Slot* d_slots = nullptr;
-  float *d_w = nullptr, *d_s0 = nullptr, *d_s1 = nullptr;
+  float *d_w = nullptr, *d_s0 = nullptr, *d_s1 = nullptr;  // (d_w unused by F16 tables)
+  bool f16 = false;              // HPS_DTYPE_F16: rows in d_wh as binary16 (inference table)
+  uint16_t* d_wh = nullptr;
   uint64_t* d_row_keys = nullptr;
   uint64_t* d_nrows = nullptr;
   float* d_defaults = nullptr;

@@ -39,6 +39,7 @@ _SIG = {
     "orc_cache_create": (vp, [u64, u32, u64, u32]),
     "orc_cache_destroy": (None, [vp]),
     "orc_cache_set_dtype": (None, [vp, i32]),
+    "orc_table_set_dtype": (None, [vp, i32]),
     "orc_f32_to_f16": (None, [vp, vp, u64]),
     "orc_f16_to_f32": (None, [vp, vp, u64]),
     "orc_cache_query": (None, [vp, vp, u64, vp, vp, vp, vp]),
@@ -70,7 +71,7 @@ def P(a):
 
 
 class OracleTable:
-    def __init__(self, caps, dim, slot_table, optimizer="sgd", seed=0, a0=0.0):
+    def __init__(self, caps, dim, slot_table, optimizer="sgd", seed=0, a0=0.0, dtype="f32"):
         self.L = lib()
         self.dim = dim
         self.n_slots = len(slot_table)
@@ -80,6 +81,8 @@ class OracleTable:
         st = np.asarray(slot_table, dtype=np.uint32)
         opt = {"sgd": 0, "adagrad": 1, "adam": 2}[optimizer]
         self.h = self.L.orc_table_create(len(caps), dim, P(caps), len(st), P(st), opt, seed, a0)
+        if dtype == "f16":
+            self.L.orc_table_set_dtype(self.h, 1)
 
     def insert(self, table, keys, rows=None):
         keys = np.ascontiguousarray(keys, dtype=np.uint64)

@@ -379,3 +379,57 @@ def test_batch_table_self_cleaning(ctx, multi):
         assert _bt_used(ctx, g) == 0
     for t, c in enumerate(caps):
         assert close(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])
+
+
+@pytest.mark.parametrize("multi", [False, True])
+def test_f16_inference_table_matches_oracle(ctx, multi):
+    """binary16 table rows: bulk load (init values and given rows,
+    rounded to nearest even), pooled inference lookups (sum / mean, absent keys -> default
+    vector), export (exact widening) — bit-identical to the oracle; training calls on the
+    inference table are DtypeMismatch; a row beyond binary16 range is F16Range."""
+    rs = np.random.default_rng(31)
+    caps, dim, slots = [3000, 500], 24, [0, 1, 1]
+    g = EmbeddingTableGroup(ctx, caps, dim, slots, "sgd", 1 << 15, 1 << 15, 5, dtype="f16")
+    o = O.OracleTable(caps, dim, slots, "sgd", 5, dtype="f16")
+    pools = []
+    for t, c in enumerate(caps):
+        ks = rs.integers(0, 2**63, c).astype(np.uint64)
+        if t == 0:
+            g.insert(t, t64(ks))
+            o.insert(t, ks)
+        else:  # given rows: a wide dynamic range (binary16 subnormals, ties, near 65504)
+            rows = (rs.standard_normal((c, dim)) * np.exp2(rs.integers(-26, 15, (c, dim)))).astype(np.float32)
+            g.insert(t, t64(ks), torch.from_numpy(rows).cuda())
+            o.insert(t, ks, rows)
+        pools.append(ks)
+    dvec = rs.standard_normal(dim).astype(np.float32)
+    g.set_default_vector(1, dvec)
+    o.set_default(1, dvec)
+    B = 700
+    if multi:
+        lens = rs.integers(0, 5, B * len(slots)).astype(np.uint32)
+        offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+        keys = np.concatenate([np.where(rs.random(l) < 0.1, rs.integers(0, 2**63, l).astype(np.uint64),
+                                        rs.choice(pools[slots[b % len(slots)]], l)) for b, l in enumerate(lens)]).astype(np.uint64)
+        ot = torch.from_numpy(offs.view(np.int32)).cuda()
+        for comb in ("sum", "mean"):
+            out = g.lookup(t64(keys), B, offsets=ot, combiner=comb)
+            ref = o.lookup(keys, B, offsets=offs, combiner=comb)
+            assert np.array_equal(out.cpu().numpy(), ref), comb
+    else:
+        keys = np.stack([rs.choice(pools[s], B) for s in slots], 1).ravel()
+        keys[::17] = rs.integers(0, 2**63, len(keys[::17])).astype(np.uint64)  # absent keys
+        out = g.lookup(t64(keys), B)
+        ref = o.lookup(keys, B)
+        assert np.array_equal(out.cpu().numpy(), ref)
+    for t, c in enumerate(caps):
+        assert np.array_equal(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])
+    with pytest.raises(HpsError) as e:
+        g.lookup(t64(pools[0][:3].repeat(3)), 3, train=True)
+    assert e.value.code == 8  # DtypeMismatch
+    bad = np.zeros((2, dim), np.float32)
+    bad[1, 3] = 1e6
+    with pytest.raises(HpsError) as e:
+        g.insert(0, t64(rs.integers(0, 2**63, 2).astype(np.uint64)), torch.from_numpy(bad).cuda())
+        ctx.sync()
+    assert e.value.code == 9  # F16Range
