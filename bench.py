@@ -290,7 +290,8 @@ def main():
     else:
         tables = build_tables_localized(ctx, cfg, owned, rank, world)
     gen = W.BatchGen(cfg)
-    step_fn = TrainStep(ctx, tables, cfg, rank, world, owned=owned, hybrid_hot=hot, force_exchange=xchg)
+    step_fn = TrainStep(ctx, tables, cfg, rank, world, use_graph=not args.no_graph, owned=owned, hybrid_hot=hot,
+                        force_exchange=xchg)
     pool = []
     rs = np.random.default_rng(rank)
     n_bags = cfg.batch * cfg.n_slots

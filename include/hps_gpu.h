@@ -124,6 +124,8 @@ typedef struct {
   float beta1, beta2;               /* Adam */
   float one_minus_beta1, one_minus_beta2;
   float lr_t;                       /* Adam: lr*sqrt(1-b2^t)/(1-b1^t), computed by the caller in fp32 */
+  const float* lr_t_device;         /* optional (NULL: use lr_t): device fp32 read by the kernels at
+                                       run time, so one captured CUDA graph serves every Adam step */
 } hps_opt_params;
 
 int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg_host, hps_gpu_table* out_host);

@@ -59,6 +59,7 @@ class OptParams(C.Structure):
         ("one_minus_beta1", f32),
         ("one_minus_beta2", f32),
         ("lr_t", f32),
+        ("lr_t_device", C.c_void_p),
     ]
 
 

@@ -503,6 +503,7 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
   const uint32_t nvec = a.dim / 4;
   const uint64_t base = uint64_t(row) * a.dim;
   const float lr = a.opt.lr, eps = a.opt.eps;
+  const float lr_t = (OPT == HPS_OPT_ADAM && a.opt.lr_t_device) ? __ldg(a.opt.lr_t_device) : a.opt.lr_t;
 #pragma unroll
   for (int k = 0; k < VPL; ++k) {
     const uint32_t v = gl + k * lpr;
@@ -530,7 +531,7 @@ __device__ __forceinline__ void update_store(const BwdArgs& a, uint32_t row, uin
       for (int c = 0; c < 4; ++c) {
         sf[c] = __fadd_rn(__fmul_rn(a.opt.beta1, sf[c]), __fmul_rn(a.opt.one_minus_beta1, gf[c]));
         qf[c] = __fadd_rn(__fmul_rn(a.opt.beta2, qf[c]), __fmul_rn(a.opt.one_minus_beta2, __fmul_rn(gf[c], gf[c])));
-        wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(a.opt.lr_t, sf[c]), __fadd_rn(__fsqrt_rn(qf[c]), eps)));
+        wf[c] = __fsub_rn(wf[c], __fdiv_rn(__fmul_rn(lr_t, sf[c]), __fadd_rn(__fsqrt_rn(qf[c]), eps)));
       }
       reinterpret_cast<float4*>(a.S0 + base)[v] = r.s[state_rows<OPT>() >= 1 ? k : 0];
       reinterpret_cast<float4*>(a.S1 + base)[v] = r.q[state_rows<OPT>() >= 2 ? k : 0];

@@ -160,7 +160,12 @@ class TrainStep:
         self.out = torch.empty(self.n_bags, cfg.dim, dtype=torch.float32, device="cuda")
         self.params = opt_params(cfg.optimizer, cfg.lr, eps=cfg.eps)
         self.insert_missing = bool(cfg.keyspace)
-        self.graph_mode = bool(use_graph and world == 1 and cfg.optimizer != "adam")
+        self.graph_mode = bool(use_graph and world == 1)
+        # Adam in a graph: the bias-corrected lr_t of each step (host fp32, as the oracle) is
+        # copied into a device scalar the kernels read (hps_opt_params.lr_t_device)
+        self._lr_dev = torch.zeros(1, dtype=torch.float32, device="cuda")
+        self._lr_ring = torch.zeros(64, dtype=torch.float32).pin_memory()
+        self._lr_ev = [None] * 64
         self._graphs = {}
         # training record + dedup (backward.cu launch_dedup): probe, dedup, long-list histogram,
         # its radix passes, long registration, long tasks; backward: short + long reduce
@@ -211,9 +216,24 @@ class TrainStep:
         return {"keys": k, "offs": o, "n_keys": int(len(keys))}
 
     # -- the step --------------------------------------------------------------------------
+    def _prep_step(self, step: int) -> None:
+        """Adam: this step's lr_t into the device scalar (a pinned ring slot -> async copy,
+        stream-ordered before the step's kernels)."""
+        if self.cfg.optimizer != "adam":
+            return
+        k = step % self._lr_ring.numel()
+        if self._lr_ev[k] is not None:
+            self._lr_ev[k].synchronize()  # the copy that last read this pinned slot has run
+        self._lr_ring[k] = float(opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step).lr_t)
+        self._lr_dev.copy_(self._lr_ring[k:k + 1], non_blocking=True)
+        self._lr_ev[k] = torch.cuda.Event()
+        self._lr_ev[k].record()
+
     def _eager(self, b, dout, step, keys_on_host=False):
         if self.cfg.optimizer == "adam":
             self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
+            if self.graph_mode:
+                self.params.lr_t_device = self._lr_dev.data_ptr()
         self.table.lookup(b["keys"], self.cfg.batch, offsets=b["offs"], combiner=self.cfg.combiner, train=True,
                           out=self.out, keys_on_host=keys_on_host, insert_missing=self.insert_missing)
         self.table.backward_update(dout, self.cfg.lr, params=self.params)
@@ -234,21 +254,33 @@ class TrainStep:
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
                 self.ctx.set_stream(s)
-                fn()
+                fn()  # this call's step (capture below records without executing)
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=s):
                     fn()
             torch.cuda.current_stream().wait_stream(s)
             self.ctx.set_stream(torch.cuda.current_stream())
             self._graphs[key] = g
+            return
         g.replay()
 
     def run(self, b, dout, step: int = 1):
         self._last_n = b["n_keys"]
+        if self.exchange is None:
+            self._prep_step(step)
         if self.exchange is not None:
             return self._exchange_step(b["keys"], b["offs"], dout, step)
         if not self.graph_mode:
             return self._eager(b, dout, step)
+        if self.insert_missing and b["offs"] is None:
+            # a dynamic table streams fresh batches: one graph over a device staging buffer
+            # (a D2D copy of the keys precedes each replay) instead of one capture per batch
+            if not hasattr(self, "_stage_keys"):
+                self._stage_keys = torch.empty(self.n_bags, dtype=torch.int64, device="cuda")
+            self._stage_keys[:b["keys"].numel()].copy_(b["keys"], non_blocking=True)
+            sb = {"keys": self._stage_keys[:b["keys"].numel()], "offs": None, "n_keys": b["n_keys"]}
+            self._graph(("stage", sb["keys"].numel(), id(dout)), lambda: self._eager(sb, dout, step))
+            return
         self._graph((id(b["keys"]), id(dout)), lambda: self._eager(b, dout, step))
 
     def _host_step(self, b, dout, step, out=None):
@@ -268,6 +300,7 @@ class TrainStep:
             self._cnt_slots[slot].copy_(self._cnt_host)
             self._slot_ev[slot].record()
             return h2d, 8
+        self._prep_step(step)
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream()
             n = self.n_bags
@@ -301,6 +334,8 @@ class TrainStep:
         the whole thing (H2D copy node -> kernels -> D2H copy node) as one CUDA graph per
         pinned input buffer; the caller refills that buffer between steps."""
         h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
+        if self.exchange is None:
+            self._prep_step(step)
         if self.exchange is not None:
             keys = b["keys"].to("cuda", non_blocking=True)
             offs = None if b["offs"] is None else b["offs"].to("cuda", non_blocking=True)
