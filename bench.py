@@ -200,6 +200,19 @@ def run_cpu(cfg, steps, warmup, threads, budget_s=None):
     return cfg.batch * done / dt, f"{done} full steps of {cfg.batch} samples x {cfg.n_slots} slots (rows materialised on first touch)"
 
 
+def host_info():
+    """The CPU the baseline ran on: nproc, affinity, model name."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)), "model": model}
+
+
 def reference_arm(args, cfg, rank, world):
     if rank != 0:
         return
@@ -212,7 +225,8 @@ def reference_arm(args, cfg, rank, world):
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "tables": len(cfg.cards),
                    "rows": int(sum(cfg.cards)), "dim": cfg.dim, "combiner": cfg.combiner, "optimizer": cfg.optimizer},
-        "cpu_baseline": {"value": val, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -399,7 +413,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         cval, sample = run_cpu(cfg, steps=30, warmup=2, threads=threads, budget_s=20.0)
-        cpu = {"value": cval, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample}
+        cpu = {"value": cval, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample,
+               "host": host_info()}
 
     if rank == 0:
         line = {

@@ -439,15 +439,9 @@ __global__ void __launch_bounds__(256) k_long_tasks(BwdArgs a) {
 // A warp's 32 short segments [u0, u0+32) occupy one contiguous range of the short list:
 // load it into shared memory and sort every segment's bags ascending (= canonical order;
 // equal bags carry identical gradients, so their relative order is immaterial).
-// Returns the range start; sbag receives the range (<= 32 * kChunk entries).
-__device__ __forceinline__ uint32_t stage_short_bags(const BwdArgs& a, uint64_t S, uint64_t u0, uint32_t first,
-                                                     uint32_t len, uint32_t* sbag) {
+// Sort every segment's bags (already in sbag, range start r0) ascending in place.
+__device__ __forceinline__ void sort_short_bags(uint32_t first, uint32_t len, uint32_t r0, uint32_t* sbag) {
   const uint32_t lane = lane_id();
-  const uint32_t last = static_cast<uint32_t>(min(uint64_t(31), S - 1 - u0));
-  const uint32_t r0 = __shfl_sync(0xffffffffu, first, 0);
-  const uint32_t r1 = __shfl_sync(0xffffffffu, first + len, last);
-  for (uint32_t p = lane; p < r1 - r0; p += 32) sbag[p] = a.short_bag[r0 + p];
-  __syncwarp();
   uint32_t multi = __ballot_sync(0xffffffffu, len >= 2);
   while (multi) {
     const int j = __ffs(multi) - 1;
@@ -464,6 +458,34 @@ __device__ __forceinline__ uint32_t stage_short_bags(const BwdArgs& a, uint64_t 
     if (lane < jl) sbag[jo + rank] = b;
     __syncwarp();
   }
+}
+
+// Asynchronous copy (cp.async, 4 B per element) of the bag range of the 32 segments at u0
+// (records rec in the lanes) into sbag; lands by cp_async_wait_all().
+__device__ __forceinline__ void prefetch_short_bags(const BwdArgs& a, uint64_t S, uint64_t u0, uint32_t first,
+                                                    uint32_t len, uint32_t* sbag) {
+  const uint32_t lane = lane_id();
+  const uint32_t last = static_cast<uint32_t>(min(uint64_t(31), S - 1 - u0));
+  const uint32_t r0 = __shfl_sync(0xffffffffu, first, 0);
+  const uint32_t r1 = __shfl_sync(0xffffffffu, first + len, last);
+  for (uint32_t p = lane; p < r1 - r0; p += 32)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(sbag + p)), "l"(a.short_bag + r0 + p)
+                 : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Returns the range start; sbag receives the range (<= 32 * kChunk entries).
+__device__ __forceinline__ uint32_t stage_short_bags(const BwdArgs& a, uint64_t S, uint64_t u0, uint32_t first,
+                                                     uint32_t len, uint32_t* sbag) {
+  const uint32_t lane = lane_id();
+  const uint32_t last = static_cast<uint32_t>(min(uint64_t(31), S - 1 - u0));
+  const uint32_t r0 = __shfl_sync(0xffffffffu, first, 0);
+  const uint32_t r1 = __shfl_sync(0xffffffffu, first + len, last);
+  for (uint32_t p = lane; p < r1 - r0; p += 32) sbag[p] = a.short_bag[r0 + p];
+  __syncwarp();
+  sort_short_bags(first, len, r0, sbag);
   return r0;
 }
 
@@ -693,7 +715,9 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
   const uint32_t D = a.dim, nvec = D / 4, row_bytes = D * 4, cap = a.tma_rows;
   float* buf = s_buf + size_t(w) * cap * D;
   float* scale = s_buf + size_t(kRedWarps) * cap * D + size_t(w) * cap;
-  uint32_t* sbag = reinterpret_cast<uint32_t*>(s_buf + size_t(kRedWarps) * cap * (D + 1)) + size_t(w) * kBagStage;
+  // two bag stages per warp: the next 32 segments' bags land (cp.async) while this wave's
+  // rows are in flight
+  uint32_t* sbag2 = reinterpret_cast<uint32_t*>(s_buf + size_t(kRedWarps) * cap * (D + 1)) + size_t(w) * 2 * kBagStage;
   const bool mean = a.bag_len != nullptr;
   if (lane == 0) {
     mbar_init(&s_bar[w], 1);
@@ -702,18 +726,23 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
   __syncwarp();
   uint32_t phase = 0;
   const uint64_t S = *a.short_alloc >> 32;
-  for (uint64_t u0 = warp * 32; u0 < S; u0 += n_warps * 32) {
-    const uint64_t u = u0 + lane;
-    uint32_t first = 0, len = 0, row = 0, slot = 0;
-    if (u < S) {
-      const uint4 rec = a.short_rec[u];
-      row = rec.x;
-      first = rec.y;
-      len = rec.z;
-      slot = rec.w;
-    }
-    const uint32_t r0 = stage_short_bags(a, S, u0, first, len, sbag);
+  const uint64_t stride = n_warps * 32;
+  uint4 rec = make_uint4(0, 0, 0, 0);
+  if (warp * 32 + lane < S) rec = a.short_rec[warp * 32 + lane];
+  if (warp * 32 < S) prefetch_short_bags(a, S, warp * 32, rec.y, rec.z, sbag2);
+  uint32_t stage = 0;
+  for (uint64_t u0 = warp * 32; u0 < S; u0 += stride, stage ^= 1) {
+    const uint32_t row = rec.x, first = rec.y, len = rec.z, slot = rec.w;
+    const uint64_t un = u0 + stride;  // the next 32 segments: records now, bags after the first wave's issue
+    uint4 nrec = make_uint4(0, 0, 0, 0);
+    if (un + lane < S) nrec = a.short_rec[un + lane];
+    uint32_t* sbag = sbag2 + stage * kBagStage;
+    cp_async_wait_all();
+    __syncwarp();
+    const uint32_t r0 = __shfl_sync(0xffffffffu, first, 0);
+    sort_short_bags(first, len, r0, sbag);
     const uint32_t boff = first - r0;
+    bool next_issued = false;
     if (len) a.bt[slot] = make_uint2(kBtEmpty, 0xffffffffu);  // placement (previous kernels) is done with it
     const uint32_t need = len ? 1 + NS + len : 0;
     uint32_t first_lane = 0;  // first lane (segment) of the current wave
@@ -737,6 +766,10 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
           bulk_g2s(dst + (1 + NS + q) * D, a.dout + uint64_t(bq) * D, row_bytes, &s_bar[w]);
           if (mean) scale[off + 1 + NS + q] = static_cast<float>(a.bag_len[bq]);
         }
+      }
+      if (!next_issued) {  // the other stage was last read by the previous iteration (done)
+        next_issued = true;
+        if (un < S) prefetch_short_bags(a, S, un, nrec.y, nrec.z, sbag2 + (stage ^ 1) * kBagStage);
       }
       mbar_wait(&s_bar[w], phase);
       phase ^= 1;
@@ -773,6 +806,7 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
       __syncwarp();  // every lane is done reading the buffer before the next wave overwrites it
       first_lane = last + 1;
     }
+    rec = nrec;
   }
 }
 
@@ -1157,9 +1191,9 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   size_t smem = 0;
   int grid = 0;
   if (tma) {
-    a.tma_rows = 40;  // 2 CTAs/SM with room for the long-segment chain's kernels beside them
+    a.tma_rows = 38;  // 2 CTAs/SM (rows + two bag stages per warp) with room for the long chain beside them
     if (const char* e = std::getenv("HPS_GPU_TMA_ROWS")) a.tma_rows = std::max(36, std::atoi(e));  // A/B knob
-    smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float) + size_t(kRedWarps) * kBagStage * 4;
+    smem = size_t(kRedWarps) * a.tma_rows * (t->dim + 1) * sizeof(float) + size_t(kRedWarps) * 2 * kBagStage * 4;
     int waves = 2;  // CTAs per SM of the grid (2 resident per SM): 2 = a single resident wave
     if (const char* e = std::getenv("HPS_GPU_RED_WAVES")) waves = std::max(1, std::atoi(e));  // A/B knob
     grid = static_cast<int>(
