@@ -86,7 +86,9 @@ struct BwdArgs {
 
 // ---- batch table ----------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t bt_home(uint32_t row, uint64_t mask) {
-  return static_cast<uint32_t>(((uint64_t(row) * 0x9E3779B97F4A7C15ull) >> 32) & mask);
+  // Fibonacci hashing: the TOP log2(size) bits of the 64-bit product (the middle bits of it
+  // cluster dense row ids: 4x the home collisions of a uniform hash on config 1)
+  return static_cast<uint32_t>((uint64_t(row) * 0x9E3779B97F4A7C15ull) >> (64 - __popcll(mask)));
 }
 // Entry of `row` (inserted if absent), probing from `h`: each round reads a window of 4
 // keys at once and CASes only the first free one, so a collision chain costs a quarter of
@@ -211,10 +213,12 @@ __global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* c
 #pragma unroll
     for (int q = 0; q < kPer; ++q)
       res[q] = ent[q] != kNoEnt ? atomicCAS(&a.bt[ent[q]].x, kBtEmpty, key[q]) : kBtEmpty;
+    trace_end_after(kTrCountCas, res[0] ^ res[kPer - 1]);
 #pragma unroll
     for (int q = 0; q < kPer; ++q)
       if (ent[q] != kNoEnt && res[q] != kBtEmpty && res[q] != key[q])
         ent[q] = bt_insert_from(a.bt, a.bt_mask, key[q], static_cast<uint32_t>((ent[q] + 1) & a.bt_mask));
+    trace_end_after(kTrCountProbe, ent[0] ^ ent[kPer - 1]);
 #pragma unroll
     for (int q = 0; q < kPer; ++q)
       res[q] = ent[q] != kNoEnt ? atomicAdd(&a.bt[ent[q]].y, s_val[threadIdx.x + kDedupBlock * q]) + 1u : 0u;

@@ -256,7 +256,8 @@ struct TraceRec {
 constexpr int kTraceSlots = 32;
 enum TraceId : int {
   kTrProbe = 0, kTrPool = 1, kTrAlloc = 2, kTrPlace = 3, kTrHist = 4, kTrPass0 = 5, kTrLongReg = 9,
-  kTrReduce = 10, kTrLong = 11, kTrReset = 12, kTrCount = 13, kTrCountLocal = 14, kTrCountGlobal = 15
+  kTrReduce = 10, kTrLong = 11, kTrReset = 12, kTrCount = 13, kTrCountLocal = 14, kTrCountGlobal = 15,
+  kTrCountCas = 16, kTrCountProbe = 17
 };
 static __device__ TraceRec* g_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -283,6 +284,10 @@ __device__ __forceinline__ void trace_end(int id) {
     TraceRec* t = g_trace;
     if (t) atomicMax(&t[id * kTraceSMs + (sm_id() % kTraceSMs)].end, gtimer());
   }
+}
+// trace_end once `dep` has landed (the timer is read under a branch on it)
+__device__ __forceinline__ void trace_end_after(int id, uint32_t dep) {
+  trace_end(dep == 0x9e3779b9u ? -1 : id);
 }
 inline cudaError_t trace_attach_tu(TraceRec* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
 // Op::kTrace when the scan op declares one, else -1 (untraced).

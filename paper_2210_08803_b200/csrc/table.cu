@@ -921,7 +921,9 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->ws_rows_a, N));
   A(dalloc(&t->ws_rank, N));
   // load <= 1/8 (<= 2^25 entries): a home-slot CAS almost always settles an insert
-  t->bt_mask = std::min<uint64_t>(next_pow2(8 * N), 1ull << 25) - 1;
+  uint64_t bt_mult = 8;
+  if (const char* e = std::getenv("HPS_GPU_BT_MULT")) bt_mult = std::max(2, std::atoi(e));  // A/B knob
+  t->bt_mask = std::min<uint64_t>(next_pow2(bt_mult * N), 1ull << 25) - 1;
   A(dalloc(&t->ws_bt, t->bt_mask + 1));
   A(dalloc(&t->ws_occ_ent, N));
   A(dalloc(&t->ws_lead, N));
