@@ -13,7 +13,7 @@ for c in cfg3 cfg5 cfg1; do
   timeout 400 python bench.py --config $c --no-cpu-baseline > gpurun_out/bench_${c}_${TAG}.json 2>&1; tail -1 gpurun_out/bench_${c}_${TAG}.json | cut -c1-200
 done
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_${TAG}.json 2>&1; tail -1 gpurun_out/bench_ref_${TAG}.json | cut -c1-200
-bash scripts/trace.sh ${TAG} cfg2 cfg3 cfg5 > /dev/null 2>&1
+bash scripts/trace.sh ${TAG} cfg2 cfg3 cfg5 cfg1 > /dev/null 2>&1
 bash scripts/launches.sh ${TAG} cfg2 cfg3
 # step kernels (eager steps: probe, pooling, dedup, ..., short reduce, long reduce)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_probe|k_lookup_1hot_tma|k_dedup|k_reduce_short|k_long<" \
