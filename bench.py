@@ -252,6 +252,7 @@ def print_trace(ctx, n, step):
         r = {k: (buf[2 * k], buf[2 * k + 1]) for k in TRACE_NAMES if buf[2 * k] != (1 << 64) - 1 or buf[2 * k + 1]}
         s0 = min((v[0] for v in r.values() if v[0] != (1 << 64) - 1), default=0)
         r = {k: (v[0] if v[0] != (1 << 64) - 1 else v[1], v[1]) for k, v in r.items()}  # end-only markers
+        r = {k: (v[0], v[1] if v[1] else v[0]) for k, v in r.items()}  # began but no warp did work (empty list)
         if r:
             t0 = min(v[0] for v in r.values())
             recs.append({k: ((a - t0) / 1000.0, (b - t0) / 1000.0) for k, (a, b) in r.items()})

@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--warmup-mult", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--dtype", default="f32", choices=["f32", "f16"], help="cache row storage (binary16 halves the bytes)")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graphs (default: one graph per batch size)")
     ap.add_argument("--phases", action="store_true", help="debug: per-call times (query / read-through / insert) at the max batch")
     args = ap.parse_args()
 
@@ -120,18 +121,24 @@ def main():
     while b <= args.max_batch:
         reps = args.reps if b <= 8192 else max(10, args.reps // 4)
         batches = [zipf_keys(b) for _ in range(reps)]
+        if not args.eager:  # capture this size's graph outside the timed calls
+            rt.lookup_graphed(zipf_keys(b))
+            ctx.sync()
         cache.reset_stats()
         lat = []
         for kb in batches:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            rt.lookup(kb)
+            if args.eager:
+                rt.lookup(kb)
+            else:
+                rt.lookup_graphed(kb)
             e1.record()
             e1.synchronize()
             lat.append(e0.elapsed_time(e1) * 1000.0)
         s = cache.stats()
         lat = np.array(lat)
-        line = {"config": "cfg4-hps-cache", "dtype": args.dtype, "batch": b, "p50_us": float(np.median(lat)),
+        line = {"config": "cfg4-hps-cache", "dtype": args.dtype, "graph": not args.eager, "batch": b, "p50_us": float(np.median(lat)),
                 "p95_us": float(np.percentile(lat, 95)), "keys_per_s": b / (np.median(lat) / 1e6),
                 "hit_rate": s["hits"] / max(1, s["queries"])}
         results.append(line)

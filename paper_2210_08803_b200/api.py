@@ -321,3 +321,33 @@ class CachedLookup:
                                                     C.c_void_p(cnt.data_ptr() + 8), _ptr(self.miss_absent),
                                                     _ptr(self.admitted)), "cache_insert_count")
         return self.out[:n]
+
+    def lookup_graphed(self, keys: torch.Tensor) -> torch.Tensor:
+        """lookup() with the three calls replayed as one CUDA graph per batch size (the keys
+        are copied into a device staging buffer first): small batches are launch-bound, and a
+        replay enqueues the ~20 kernels of a read-through as one launch. Same results and
+        cache state as lookup(); the first call of a size runs eagerly and captures."""
+        n = keys.numel()
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+            self._stage = torch.empty(self.cache.max_batch, dtype=torch.int64, device=self.device)
+        self._stage[:n].copy_(keys, non_blocking=True)
+        g = self._graphs.get(n)
+        if g is not None:
+            g.replay()
+            return self.out[:n]
+        ctx, cur = self.cache.ctx, torch.cuda.current_stream()
+        s = torch.cuda.Stream()
+        s.wait_stream(cur)
+        with torch.cuda.stream(s):
+            ctx.set_stream(s)
+            try:
+                self.lookup(self._stage[:n])  # this call's lookup (the capture below does not execute)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    self.lookup(self._stage[:n])
+            finally:
+                cur.wait_stream(s)
+                ctx.set_stream(cur)
+        self._graphs[n] = g
+        return self.out[:n]

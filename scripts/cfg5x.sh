@@ -1,2 +1,13 @@
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -2
-for m in 8 16; do echo "== mult $m"; HPS_GPU_BT_MULT=$m bash scripts/trace.sh v12f cfg1 cfg2 2>&1 | grep "count\|reduce_short\|=="; for c in cfg1 cfg2; do tail -1 gpurun_out/trace_${c}_v12f.json | cut -c100-180; done; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_cache1.csv python bench_cache.py --keys 1000000 --capacity 100000 --reps 3 --max-batch 1 --warmup-mult 0.001 --no-cpu --eager > /dev/null 2>&1
+python - <<'PY'
+import csv,collections
+rows=list(csv.reader(open('gpurun_out/launches_cache1.csv')))
+hdr=None;seq=[]
+for r in rows:
+    if 'Kernel Name' in r: hdr=r;continue
+    if hdr and len(r)==len(hdr):
+        try: seq.append((r[hdr.index('Kernel Name')][:70], float(r[hdr.index('Metric Value')].replace(',',''))/1000))
+        except: pass
+# last ~40 launches = the last lookups
+for k,v in seq[-45:]: print(f"{v:8.2f} {k}")
+PY

@@ -156,9 +156,12 @@ def test_zipf_hit_rate_bound(ctx):
     assert s["hits"] / s["queries"] >= 0.9 * M, (s, M)
 
 
-def test_read_through_matches_oracle(ctx):
+@pytest.mark.parametrize("graphed", [False, True])
+def test_read_through_matches_oracle(ctx, graphed):
     """Cache + backing table read-through: outputs in input order, hits/misses, migration
-    of misses (absent keys never cached), bit-exact with the oracle cache + a dict table."""
+    of misses (absent keys never cached), bit-exact with the oracle cache + a dict table.
+    graphed: lookup_graphed (one CUDA graph per batch size; sizes repeat so most rounds
+    are replays)."""
     from paper_2210_08803_b200 import EmbeddingTableGroup
     from paper_2210_08803_b200.api import CachedLookup
     dim, n_keys, cap = 8, 5000, 512
@@ -175,9 +178,10 @@ def test_read_through_matches_oracle(ctx):
     ocache = O.OracleCache(cap, dim, 8, 0)
     z = W.Zipf(n_keys + 200, 1.1)
     for rnd in range(20):
-        ranks = z.ranks(W.rng(rnd, np.arange(int(rs.integers(1, 3000)), dtype=np.uint64)))
+        m = int(rs.integers(1, 3000)) if not graphed else [1, 37, 2048][rnd % 3]
+        ranks = z.ranks(W.rng(rnd, np.arange(m, dtype=np.uint64)))
         q = W.mix64(ranks.astype(np.uint64))  # ranks >= n_keys are absent from the table
-        got = rt.lookup(t64(q)).cpu().numpy()
+        got = (rt.lookup_graphed(t64(q)) if graphed else rt.lookup(t64(q))).cpu().numpy()
         fi, fv, mi = ocache.query(q)
         want = np.empty((len(q), dim), np.float32)
         want[fi] = fv
