@@ -23,6 +23,8 @@
 #include <vector>
 
 #include <cuda_fp16.h>
+#include <cub/block/block_radix_sort.cuh>
+#include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
 #include "primitives.cuh"
@@ -49,6 +51,7 @@ struct hps_gpu_cache_s {
   uint64_t* ws_scan = nullptr;
   uint64_t* ws_counts = nullptr;  // [0]=n [1]=U (segments) [2]=found [3]=valid
   size_t sort_words = 0;
+  bool no_small_sort = false;  // HPS_GPU_NO_SMALL_SORT=1: small batches take the multi-kernel sort too (tests)
 };
 
 namespace {
@@ -684,10 +687,74 @@ int lpr_for(uint32_t dim) {
   return nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
 }
 
+// Small batches (n_max <= kSmallSort): the stable (set id, input index) sort and the set
+// segments in ONE single-CTA kernel (block radix sort in shared memory + a block scan over
+// the segment heads) instead of histogram + onesweep passes + a segment scan: a batch of
+// a few keys is bound by launches, not bytes. Same outputs as the multi-kernel path.
+constexpr int kSmallSortThreads = 512;
+constexpr int kSmallSortIPT = 4;
+constexpr uint64_t kSmallSort = uint64_t(kSmallSortThreads) * kSmallSortIPT;
+
+__global__ void __launch_bounds__(kSmallSortThreads) k_small_sort_segment(const uint32_t* __restrict__ sets,
+                                                                          uint64_t* counts, int bits,
+                                                                          uint32_t* __restrict__ sets_out,
+                                                                          uint32_t* __restrict__ idx_out,
+                                                                          uint32_t* __restrict__ seg_start) {
+  using Sort = cub::BlockRadixSort<uint32_t, kSmallSortThreads, kSmallSortIPT, uint32_t>;
+  using Scan = cub::BlockScan<uint32_t, kSmallSortThreads>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t s_key[kSmallSort];
+  const uint32_t n = static_cast<uint32_t>(counts[0]);
+  const uint32_t pad = bits >= 32 ? 0xffffffffu : ((1u << bits) - 1u);  // pads sort after equal keys (stable)
+  uint32_t k[kSmallSortIPT], v[kSmallSortIPT];
+#pragma unroll
+  for (int q = 0; q < kSmallSortIPT; ++q) {  // blocked arrangement: item i = t * IPT + q
+    const uint32_t i = threadIdx.x * kSmallSortIPT + q;
+    k[q] = i < n ? sets[i] : pad;
+    v[q] = i;
+  }
+  Sort(tmp.sort).Sort(k, v, 0, bits <= 0 ? 1 : bits);
+#pragma unroll
+  for (int q = 0; q < kSmallSortIPT; ++q) {
+    const uint32_t i = threadIdx.x * kSmallSortIPT + q;
+    s_key[i] = k[q];
+    if (i < n) {
+      sets_out[i] = k[q];
+      idx_out[i] = v[q];
+    }
+  }
+  __syncthreads();
+  uint32_t head[kSmallSortIPT], excl[kSmallSortIPT], total = 0;
+#pragma unroll
+  for (int q = 0; q < kSmallSortIPT; ++q) {
+    const uint32_t i = threadIdx.x * kSmallSortIPT + q;
+    head[q] = (i < n && (i == 0 || s_key[i] != s_key[i - 1])) ? 1u : 0u;
+  }
+  Scan(tmp.scan).ExclusiveSum(head, excl, total);
+#pragma unroll
+  for (int q = 0; q < kSmallSortIPT; ++q)
+    if (head[q]) seg_start[excl[q]] = threadIdx.x * kSmallSortIPT + q;
+  if (threadIdx.x == 0) {
+    counts[1] = total;
+    seg_start[total] = n;
+  }
+}
+
 // Stable sort of (set id, input index) + set segments. Sizes come from c->ws_counts[0].
 int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** sets_sorted,
                      const uint32_t** idx_sorted) {
   cudaStream_t st = c->ctx->stream;
+  if (n <= kSmallSort && !c->no_small_sort) {
+    k_small_sort_segment<<<1, kSmallSortThreads, 0, st>>>(c->ws_set, c->ws_counts, bits, c->ws_keys_b, c->ws_vals_b,
+                                                          c->ws_seg);
+    HPSG_CHECK_LAUNCH("small sort + segments");
+    *sets_sorted = c->ws_keys_b;
+    *idx_sorted = c->ws_vals_b;
+    return HPS_GPU_OK;
+  }
   cudaError_t err;
   const bool in_b = radix_sort_pairs(st, c->ws_set, nullptr, c->ws_vals_a, c->ws_keys_b, c->ws_vals_b, c->ws_counts,
                                      n, bits, c->ws_sort, &err);
@@ -730,6 +797,7 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   c->ways = ways;
   c->dim = cfg->dim;
   c->f16 = cfg->dtype == HPS_DTYPE_F16;
+  if (const char* e = std::getenv("HPS_GPU_NO_SMALL_SORT")) c->no_small_sort = e[0] == '1';
   c->num_sets = cfg->capacity / ways;
   const uint64_t interval = cfg->aging_interval ? cfg->aging_interval : 10 * cfg->capacity;
   c->aging_period = std::max<uint64_t>(1, interval / c->num_sets);

@@ -96,9 +96,14 @@ def test_non_finite_entry_skipped(ctx):
     assert g.stats() == o.stats()
 
 
+@pytest.mark.parametrize("small_sort", [True, False])
 @pytest.mark.parametrize("cap,ways,aging", [(256, 8, 0), (96, 4, 40), (512, 8, 700), (32, 1, 0), (1024, 32, 0)])
-def test_randomized_sequences_match_oracle(ctx, cap, ways, aging):
+def test_randomized_sequences_match_oracle(ctx, cap, ways, aging, small_sort, monkeypatch):
+    """small_sort=False: batches <= 2048 keys also take the multi-kernel set sort (histogram +
+    onesweep passes + segment scan) instead of the single-CTA sort + segment kernel."""
     dim = 8
+    if not small_sort:
+        monkeypatch.setenv("HPS_GPU_NO_SMALL_SORT", "1")  # read when the cache is created
     g, o = pair(ctx, cap, dim, ways, aging)
     rs = np.random.default_rng(cap + ways + aging)
     zipf = W.Zipf(3 * cap, 1.05)
