@@ -72,10 +72,13 @@ __global__ void k_probe(const uint64_t* __restrict__ keys, uint64_t n, hps::Fast
                         const uint64_t* __restrict__ ckeys, const uint8_t* __restrict__ cfreq,
                         uint32_t* __restrict__ set_out, uint8_t* __restrict__ hit_out, uint64_t* state,
                         uint64_t* counts) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     state[kSnap] = state[kClock];
     state[kClock] += n;
     counts[0] = n;
+    counts[4] = 0;  // huge-set list count of this query's metadata replay (k_query_meta_lanes)
   }
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t k = keys[i];
@@ -141,6 +144,8 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ fou
                                                 const uint32_t* __restrict__ set_of, const uint8_t* __restrict__ hit,
                                                 uint32_t ways, const void* __restrict__ vec, uint32_t dim,
                                                 float* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
   const uint64_t nf = counts[2];
@@ -232,6 +237,8 @@ __global__ void __launch_bounds__(256) k_query_meta(const uint32_t* __restrict__
                                                     uint64_t aging_period, uint8_t* __restrict__ cfreq,
                                                     uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
                                                     const uint64_t* state) {
+  pdl_wait();
+  pdl_launch_dependents();
   const uint64_t U = counts[1];
   const uint64_t clock0 = state[kSnap];
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -256,6 +263,8 @@ __global__ void __launch_bounds__(256) k_query_meta_lanes(const uint32_t* __rest
                                                           uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
                                                           const uint64_t* state, uint32_t* huge_list,
                                                           unsigned long long* n_huge) {
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t lane = lane_id();
   const uint64_t U = counts[1];
   const uint64_t clock0 = state[kSnap];
@@ -345,6 +354,8 @@ __global__ void __launch_bounds__(256) k_query_meta_huge(const uint32_t* __restr
                                                          uint64_t aging_period, uint8_t* __restrict__ cfreq,
                                                          uint64_t* __restrict__ ctouch, uint64_t* __restrict__ set_acc,
                                                          const uint64_t* state) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ uint32_t s_idx[kHugeStage];
   __shared__ uint8_t s_hw[kHugeStage];
   __shared__ uint16_t s_cnt[kHugeSegs][8];  // hits per (aging segment, way)
@@ -453,6 +464,8 @@ __global__ void __launch_bounds__(256) k_entry_prep(const uint64_t* __restrict__
                                                     uint32_t* __restrict__ set_out, uint8_t* __restrict__ valid_out,
                                                     uint32_t* status, uint64_t* counts, const uint64_t* d_n,
                                                     const uint8_t* __restrict__ skip, int f16) {
+  pdl_wait();
+  pdl_launch_dependents();
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
   const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
@@ -528,6 +541,8 @@ __global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict_
                                                      uint64_t aging_period, uint32_t invalid_set, uint64_t* ckeys,
                                                      uint64_t* cver, uint8_t* cfreq, uint64_t* ctouch, uint64_t* set_acc,
                                                      void* cvec, uint64_t* state, uint64_t* admitted_out) {
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t lane = lane_id();
   const uint64_t U = counts[1];
   const uint64_t clock0 = state[kSnap];
@@ -619,6 +634,8 @@ __global__ void __launch_bounds__(256) k_refresh_sets(const uint32_t* __restrict
                                                       uint32_t dim, uint32_t invalid_set, const uint64_t* ckeys,
                                                       uint64_t* cver, const uint8_t* cfreq, void* cvec,
                                                       uint64_t* state, uint64_t* replaced_out) {
+  pdl_wait();
+  pdl_launch_dependents();
   const uint32_t lane = lane_id();
   const uint64_t U = counts[1];
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -700,6 +717,8 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_small_sort_segment(const 
                                                                           uint32_t* __restrict__ sets_out,
                                                                           uint32_t* __restrict__ idx_out,
                                                                           uint32_t* __restrict__ seg_start) {
+  pdl_wait();
+  pdl_launch_dependents();
   using Sort = cub::BlockRadixSort<uint32_t, kSmallSortThreads, kSmallSortIPT, uint32_t>;
   using Scan = cub::BlockScan<uint32_t, kSmallSortThreads>;
   __shared__ union {
@@ -748,7 +767,7 @@ int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** set
                      const uint32_t** idx_sorted) {
   cudaStream_t st = c->ctx->stream;
   if (n <= kSmallSort && !c->no_small_sort) {
-    k_small_sort_segment<<<1, kSmallSortThreads, 0, st>>>(c->ws_set, c->ws_counts, bits, c->ws_keys_b, c->ws_vals_b,
+    launch_k(true, k_small_sort_segment, 1, kSmallSortThreads, 0, st, c->ws_set, c->ws_counts, bits, c->ws_keys_b, c->ws_vals_b,
                                                           c->ws_seg);
     HPSG_CHECK_LAUNCH("small sort + segments");
     *sets_sorted = c->ws_keys_b;
@@ -761,11 +780,8 @@ int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** set
   if (err != cudaSuccess) return cuda_status(err, "cache radix sort");
   *sets_sorted = in_b ? c->ws_keys_b : c->ws_set;
   *idx_sorted = in_b ? c->ws_vals_b : c->ws_vals_a;
-  const uint64_t tiles = scan_tiles(n);
-  HPSG_CUDA(cudaMemsetAsync(c->ws_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
   SetSegOp op{*sets_sorted, c->ws_seg, c->ws_counts};
-  k_scan<SetSegOp><<<static_cast<unsigned>(std::max<uint64_t>(1, tiles)), kScanBlock, 0, st>>>(
-      op, c->ws_scan, reinterpret_cast<uint32_t*>(c->ws_scan + tiles));
+  HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
   HPSG_CHECK_LAUNCH("set segments");
   return HPS_GPU_OK;
 }
@@ -898,22 +914,19 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
   if (!keys) return HPS_GPU_E_INVALID_ARGUMENT;
   QueryPhases ph(st);
   ph.mark();
-  k_probe<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(keys, n, c->set_mod, c->ways, c->d_keys, c->d_freq,
+  launch_k(true, k_probe, grid_for(n, 256, kNumSMs * 16), 256, 0, st, keys, n, c->set_mod, c->ways, c->d_keys, c->d_freq,
                                                           c->ws_set, c->ws_hit, c->d_state, c->ws_counts);
-  const uint64_t tiles = scan_tiles(n);
-  HPSG_CUDA(cudaMemsetAsync(c->ws_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
   SplitOp op{c->ws_hit, found_idx, missing_idx, counts, c->ws_counts, c->d_state + kStats};
-  k_scan<SplitOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(op, c->ws_scan,
-                                                                       reinterpret_cast<uint32_t*>(c->ws_scan + tiles));
+  HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
   HPSG_CHECK_LAUNCH("cache probe/split");
   ph.mark();
   if (found_vecs) {
     const int lpr = lpr_for(c->dim);
     const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
 #define HPSG_G(L)                                                                                                   \
-  (c->f16 ? k_gather<L, true><<<grid, 256, 0, st>>>(found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec, \
+  (c->f16 ? launch_k(true, k_gather<L, true>, grid, 256, 0, st, found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec, \
                                                      c->dim, found_vecs)                                              \
-          : k_gather<L, false><<<grid, 256, 0, st>>>(found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec,\
+          : launch_k(true, k_gather<L, false>, grid, 256, 0, st, found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec,\
                                                       c->dim, found_vecs))
     switch (lpr) {
       case 32: HPSG_G(32); break;
@@ -933,15 +946,14 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
   ph.mark();
   if (c->ways <= 8) {
     auto* n_huge = reinterpret_cast<unsigned long long*>(c->ws_counts + 4);
-    HPSG_CUDA(cudaMemsetAsync(n_huge, 0, sizeof(unsigned long long), st));
-    k_query_meta_lanes<<<grid_for((n + 31) / 32 * 32, 256, kNumSMs * 16), 256, 0, st>>>(
+    launch_k(true, k_query_meta_lanes, grid_for((n + 31) / 32 * 32, 256, kNumSMs * 16), 256, 0, st, 
         sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, c->ws_hit, c->ways, c->aging_period, c->d_freq, c->d_touch,
         c->d_set_acc, c->d_state, c->ws_rank, n_huge);
-    k_query_meta_huge<<<kNumSMs, 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_rank,
+    launch_k(true, k_query_meta_huge, kNumSMs, 256, 0, st, sets_sorted, idx_sorted, c->ws_seg, c->ws_rank,
                                                reinterpret_cast<const uint64_t*>(n_huge), c->ws_hit, c->ways,
                                                c->aging_period, c->d_freq, c->d_touch, c->d_set_acc, c->d_state);
   } else
-    k_query_meta<<<set_warps_grid(n), 256, 0, st>>>(sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, c->ws_hit,
+    launch_k(true, k_query_meta, set_warps_grid(n), 256, 0, st, sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, c->ws_hit,
                                                     c->ways, c->aging_period, c->d_freq, c->d_touch, c->d_set_acc,
                                                     c->d_state);
   HPSG_CHECK_LAUNCH("cache meta");
@@ -955,7 +967,7 @@ static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, 
   const int lpr = lpr_for(c->dim);
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
   const uint32_t invalid = static_cast<uint32_t>(c->num_sets);
-#define HPSG_P(L) k_entry_prep<L><<<grid, 256, 0, st>>>(keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts, d_n, skip, c->f16 ? 1 : 0)
+#define HPSG_P(L) launch_k(true, k_entry_prep<L>, grid, 256, 0, st, keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts, d_n, skip, c->f16 ? 1 : 0)
   switch (lpr) {
     case 32: HPSG_P(32); break;
     case 16: HPSG_P(16); break;
@@ -978,15 +990,12 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
   if (n == 0) return HPS_GPU_OK;
   if (!keys || !vecs) return HPS_GPU_E_INVALID_ARGUMENT;
   if (int s = entry_prep(c, keys, vecs, n, d_n, skip)) return s;
-  const uint64_t tiles = scan_tiles(n);
-  HPSG_CUDA(cudaMemsetAsync(c->ws_scan, 0, (tiles + 1) * sizeof(uint64_t), st));
   RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
-  k_scan<RankOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(rop, c->ws_scan,
-                                                                      reinterpret_cast<uint32_t*>(c->ws_scan + tiles));
+  HPSG_CUDA(launch_scan(rop, n, c->ws_scan, st));
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
-  (c->f16 ? k_insert_sets<true> : k_insert_sets<false>)<<<set_warps_grid(n), 256, 0, st>>>(
+  launch_k(true, (c->f16 ? k_insert_sets<true> : k_insert_sets<false>), set_warps_grid(n), 256, 0, st, 
       sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ws_rank, c->ways, c->dim,
       c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch, c->d_set_acc,
       c->d_vec, c->d_state, admitted_out);
@@ -1018,7 +1027,7 @@ int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* ve
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
-  (c->f16 ? k_refresh_sets<true> : k_refresh_sets<false>)<<<set_warps_grid(n), 256, 0, st>>>(
+  launch_k(true, (c->f16 ? k_refresh_sets<true> : k_refresh_sets<false>), set_warps_grid(n), 256, 0, st, 
       sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ways, c->dim,
       static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_vec, c->d_state, replaced_out);
   HPSG_CHECK_LAUNCH("cache refresh");

@@ -151,6 +151,47 @@ __global__ void __launch_bounds__(kScanBlock) k_scan(Op op, uint64_t* status, ui
 
 inline uint64_t scan_tiles(uint64_t n_max) { return (n_max + kScanTile - 1) / kScanTile; }
 
+// The same scan when the input fits ONE tile (n_max <= kScanTile, known on the host): no
+// tile ticket and no look-back status, so no zeroing memset before it (small batches are
+// bound by the nodes of their chain, not by bytes).
+template <class Op>
+__global__ void __launch_bounds__(kScanBlock) k_scan_one(Op op) {
+  __shared__ uint64_t s_scratch[33];
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t n = op.size();
+  const uint64_t base = uint64_t(threadIdx.x) * kScanIPT;
+  uint64_t c[kScanIPT];
+  uint64_t sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanIPT; ++k) {
+    c[k] = (base + k < n) ? static_cast<uint64_t>(op.count(base + k)) : 0ull;
+    sum += c[k];
+  }
+  uint64_t agg;
+  uint64_t run = block_excl_scan<kScanBlock>(sum, s_scratch, &agg);
+#pragma unroll
+  for (int k = 0; k < kScanIPT; ++k) {
+    if (base + k < n) op.emit(base + k, run, c[k]);
+    run += c[k];
+  }
+  if (threadIdx.x == kScanBlock - 1) op.total(agg);
+}
+
+// k_scan over up to n_max items (device size op.size()): one tile -> k_scan_one, else the
+// decoupled look-back scan with its status words zeroed first.
+template <class Op>
+inline cudaError_t launch_scan(const Op& op, uint64_t n_max, uint64_t* status, cudaStream_t st) {
+  const uint64_t tiles = scan_tiles(n_max);
+  if (tiles <= 1) {
+    return launch_k(true, k_scan_one<Op>, 1, kScanBlock, 0, st, op);
+  }
+  cudaError_t e = cudaMemsetAsync(status, 0, (tiles + 1) * sizeof(uint64_t), st);
+  if (e != cudaSuccess) return e;
+  k_scan<Op><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(op, status, reinterpret_cast<uint32_t*>(status + tiles));
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------------
 // Stable LSD radix sort of (u32 key, u32 value) pairs, 8-bit digits.
 // ---------------------------------------------------------------------------------

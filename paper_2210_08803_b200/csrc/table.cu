@@ -493,6 +493,8 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
                                                       uint32_t dim, float* __restrict__ out, uint64_t* miss_keys,
                                                       float* miss_vecs, uint8_t* miss_absent,
                                                       const uint16_t* __restrict__ Wh) {
+  pdl_wait();
+  pdl_launch_dependents();
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
   const uint64_t nf = counts[0], nm = counts[1];
@@ -1207,12 +1209,12 @@ int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* 
   const TableDev td = t->h_tables[table];
   const float* def = t->d_defaults + uint64_t(table) * t->dim;
   switch (lpr) {
-    case 32: k_read_through<32><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 16: k_read_through<16><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 8: k_read_through<8><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 4: k_read_through<4><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 2: k_read_through<2><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    default: k_read_through<1><<<grid, 256, 0, st>>>(keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 32: launch_k(true, k_read_through<32>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 16: launch_k(true, k_read_through<16>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 8: launch_k(true, k_read_through<8>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 4: launch_k(true, k_read_through<4>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 2: launch_k(true, k_read_through<2>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    default: launch_k(true, k_read_through<1>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
   }
   HPSG_CHECK_LAUNCH("k_read_through");
   return HPS_GPU_OK;
