@@ -959,7 +959,7 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
 // ---- kernels ------------------------------------------------------------------------------
 // Short segments reduced + updated.
 template <int OPT, int LPR, int VPL, bool TMA>
-__global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : 2)
+__global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : (OPT == HPS_OPT_ADAM ? 2 : 3))
     k_reduce_short(BwdArgs a) {
   extern __shared__ __align__(128) float s_dyn[];  // TMA: [kRedWarps][cap][dim] rows, scales, bags
   __shared__ __align__(8) uint64_t s_bar[kRedWarps];
@@ -1191,7 +1191,9 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   const uint32_t nvec = t->dim / 4;
   // K4e + K5: short segments (reduce fused with the optimizer), then the long segments'
   // chunk partials + tree + optimizer.
-  const bool tma = t->dim >= 128 && t->dim <= 256 && !t->no_tma;  // narrower rows: the register path wins
+  uint32_t tma_min_dim = 128;
+  if (const char* e = std::getenv("HPS_GPU_TMA_MIN_DIM")) tma_min_dim = std::max(16, std::atoi(e));  // A/B knob
+  const bool tma = t->dim >= tma_min_dim && t->dim <= 256 && !t->no_tma;  // narrower rows: the register path wins
   size_t smem = 0;
   int grid = 0;
   if (tma) {

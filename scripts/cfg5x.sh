@@ -1,2 +1,2 @@
-timeout 600 python -m pytest tests/test_gpu_cache.py tests/test_gpu_table.py -x -q -p no:cacheprovider 2>&1 | tail -3
-timeout 900 python bench_cache.py --reps 30 --no-cpu > gpurun_out/cache_graph4.jsonl 2>&1; head -13 gpurun_out/cache_graph4.jsonl | cut -c40-150; tail -2 gpurun_out/cache_graph4.jsonl | cut -c1-250
+timeout 900 python -m pytest tests/test_gpu_table.py -x -q -p no:cacheprovider 2>&1 | tail -2
+for c in cfg3 cfg1; do timeout 400 python bench.py --config $c --no-cpu-baseline --steps 10 --e2e-steps 2 --trace 4 2>&1 | grep "reduce_short\|reduce_long\|^{" | cut -c1-170; done
