@@ -532,6 +532,11 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
 
 // Multi-hot path: a group of LPR lanes owns one bag at a time; the group resolves LPR
 // keys of the bag in parallel, then accumulates the rows in bag order (4 in flight).
+// Rows of a bag's chunk gathered before any is summed (bytes in flight per lane group).
+#ifndef HPS_MULTI_ROWS
+#define HPS_MULTI_ROWS 4
+#endif
+constexpr int kMultiRows = HPS_MULTI_ROWS;
 template <int LPR, int VPL, bool ROWS, bool F16 = false>
 __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
   constexpr int G = 32 / LPR;
@@ -552,10 +557,10 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
       const uint32_t i = c + gl;
       const uint32_t row = i < hi ? occurrence_row<ROWS>(a, i, table) : kRowEmpty;
       const uint32_t cnt = min(uint32_t(LPR), hi - c);
-      for (uint32_t m0 = 0; m0 < cnt; m0 += 4) {
-        float4 x[4][VPL];
+      for (uint32_t m0 = 0; m0 < cnt; m0 += kMultiRows) {
+        float4 x[kMultiRows][VPL];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kMultiRows; ++j) {
           const uint32_t m = m0 + j;
           const uint32_t r = __shfl_sync(gmask, row, grp * LPR + (m < LPR ? m : 0));
           const float4* p = reinterpret_cast<const float4*>(
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(256) k_lookup_multi(LookupArgs a) {
           }
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kMultiRows; ++j) {
           if (m0 + j < cnt) {
 #pragma unroll
             for (int k = 0; k < VPL; ++k) acc[k] = f4_add(acc[k], x[j][k]);
