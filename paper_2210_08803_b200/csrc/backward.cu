@@ -154,7 +154,7 @@ __device__ __forceinline__ uint32_t smem_hash_slot(uint32_t* s_key, uint32_t row
 // issued before any is consumed (these phases are latency-bound, not bandwidth-bound).
 constexpr int kDedupIPT = 8;
 
-__global__ void __launch_bounds__(kDedupBlock, 1) k_dedup(BwdArgs a, uint32_t* coop) {
+__global__ void __launch_bounds__(kDedupBlock, 2) k_dedup(BwdArgs a, uint32_t* coop) {
   extern __shared__ uint32_t s_dd[];
   uint32_t* s_key = s_dd;               // row, then its batch-table entry
   uint32_t* s_val = s_dd + kDedupHash;  // chunk count, then the CTA's base rank
