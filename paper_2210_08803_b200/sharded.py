@@ -295,7 +295,8 @@ class TrainStep:
         stream; read_host_result(slot) waits for it. Every step moves its inputs H2D and its
         result D2H inside the timed region; the copies overlap the previous step's kernels."""
         h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
-        if self.exchange is not None or not self.graph_mode or b["offs"] is not None:
+        multi = b["offs"] is not None
+        if self.exchange is not None or not self.graph_mode or (multi and self.insert_missing):
             self.run_host(b, dout, step)
             self._cnt_slots[slot].copy_(self._cnt_host)
             self._slot_ev[slot].record()
@@ -303,16 +304,20 @@ class TrainStep:
         self._prep_step(step)
         if not hasattr(self, "_copy_stream"):
             self._copy_stream = torch.cuda.Stream()
-            n = self.n_bags
-            self._dev_keys = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(2)]
+            nk = max(self.n_bags, table_max_keys(self.cfg, 1))
+            self._dev_keys = [torch.empty(nk, dtype=torch.int64, device="cuda") for _ in range(2)]
+            # multi-hot: the bag offsets travel too; the graph's kernels read sizes from them
+            self._dev_offs = [torch.empty(self.n_bags + 1, dtype=torch.int32, device="cuda") for _ in range(2)]
             self._copy_ev = [torch.cuda.Event() for _ in range(2)]
         main = torch.cuda.current_stream()
         with torch.cuda.stream(self._copy_stream):
             self._copy_stream.wait_event(self._slot_ev[slot])  # the slot's previous step is done with it
-            self._dev_keys[slot].copy_(b["keys"], non_blocking=True)
+            self._dev_keys[slot][:b["keys"].numel()].copy_(b["keys"], non_blocking=True)
+            if multi:
+                self._dev_offs[slot].copy_(b["offs"], non_blocking=True)
             self._copy_ev[slot].record()
         main.wait_event(self._copy_ev[slot])
-        dk = {"keys": self._dev_keys[slot], "offs": None, "n_keys": b["n_keys"]}
+        dk = {"keys": self._dev_keys[slot], "offs": self._dev_offs[slot] if multi else None, "n_keys": b["n_keys"]}
         out = self._cnt_slots[slot]
 
         def dev_step():

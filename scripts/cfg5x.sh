@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -2
-for c in cfg3 cfg2 cfg5 cfg1; do echo "== $c"; timeout 400 python bench.py --config $c --no-cpu-baseline --steps 20 --e2e-steps 2 --trace 4 2>&1 | grep "pool \|count \|place\|reduce_short\|^{" | cut -c1-150; done
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+for c in cfg3 cfg2; do timeout 400 python bench.py --config $c --no-cpu-baseline --steps 20 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$c', d['value'], d['e2e'])"; done

@@ -467,3 +467,35 @@ def test_adam_graph_step_matches_eager(ctx):
     for other in res[1:]:
         for a, b in zip(res[0], other):
             np.testing.assert_array_equal(a, b)
+
+
+def test_multi_hot_pipelined_host_steps_match_eager(ctx):
+    """Multi-hot (config-3 shape, small tables): the pipelined end-to-end path (keys AND bag
+    offsets H2D on a copy stream into device slots, then one graph per slot) produces
+    bitwise the table of eager device steps."""
+    from paper_2210_08803_b200 import workload as W
+    from paper_2210_08803_b200.sharded import TrainStep, build_tables
+    cfg = W.config3(batch_per_gpu=128)
+    cfg.cards = [4000 + 37 * t for t in range(26)]
+    gen = W.BatchGen(cfg)
+    rs = np.random.default_rng(9)
+    batches = [gen.batch(s)[:2] for s in range(1, 4)]
+    douts = [torch.from_numpy((rs.standard_normal((cfg.batch * cfg.n_slots, cfg.dim)) * 0.1).astype(np.float32)).cuda()
+             for _ in range(2)]
+    res = []
+    for mode in ("eager", "host"):
+        tab = build_tables(ctx, cfg)
+        ts = TrainStep(ctx, tab, cfg, use_graph=mode != "eager")
+        staged = [ts.stage_host(k, o) if mode == "host" else ts.stage_batch(k, o) for k, o in batches]
+        for step in range(1, 8):
+            b, d = staged[step % 3], douts[step % 2]
+            if mode == "host":
+                ts.run_host_async(b, d, step, step % 2)
+                ts.read_host_result(step % 2)
+            else:
+                ts.run(b, d, step=step)
+        ctx.sync()
+        res.append([np.concatenate([x.cpu().numpy().ravel() for x in tab.export(t, 0, c) if x is not None])
+                    for t, c in enumerate(cfg.cards)])
+    for a, b in zip(res[0], res[1]):
+        np.testing.assert_array_equal(a, b)
