@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_table.py -x -q -p no:cacheprovider 2>&1 | tail -2
-for k in 8 3 6; do for c in cfg2 cfg5; do HPS_GPU_LOOKUP_CTAS=$k timeout 400 python bench.py --config $c --no-cpu-baseline --steps 20 --e2e-steps 2 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('ctas $k $c frac',round(d['roofline']['frac'],3),'kernel_us',round(d['roofline']['kernel_ms']*1000,1),'step',round(d['ms_per_step'],4))"; done; done
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -2
+for c in cfg2 cfg1 cfg3 cfg5; do echo "== $c"; timeout 400 python bench.py --config $c --no-cpu-baseline --steps 20 --e2e-steps 2 --trace 8 2>&1 | grep "count\|seg_alloc\|reduce_short\|^{" | cut -c1-150; done
