@@ -408,6 +408,23 @@ def main():
     _ = step_fn.read_host_result((e2e_steps - 1) % 2)
     e1.record(stream)
     torch.cuda.synchronize()
+    if os.environ.get("HPS_BENCH_E2E_CPU"):  # debug: host time per e2e step
+        c0 = time.perf_counter()
+        for i in range(e2e_steps):
+            step_fn.run_host_async(host_batches[i % len(host_batches)], douts[i % len(douts)], step=30_000 + i,
+                                   slot=i % 2)
+            if i:
+                _ = step_fn.read_host_result((i - 1) % 2)
+        _ = step_fn.read_host_result((e2e_steps - 1) % 2)
+        print(f"# e2e host loop {1e6 * (time.perf_counter() - c0) / e2e_steps:.1f} us/step", file=sys.stderr)
+        c0 = time.perf_counter()
+        for i in range(e2e_steps):
+            step_fn.run_host_async(host_batches[i % len(host_batches)], douts[i % len(douts)], step=40_000 + i,
+                                   slot=i % 2)
+        print(f"# e2e enqueue (host, before sync) {1e6 * (time.perf_counter() - c0) / e2e_steps:.1f} us/step",
+              file=sys.stderr)
+        torch.cuda.synchronize()
+        print(f"# e2e enqueue-only {1e6 * (time.perf_counter() - c0) / e2e_steps:.1f} us/step", file=sys.stderr)
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     t = torch.tensor([e2e_ms], device="cuda")
     if world > 1:
