@@ -645,7 +645,8 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        if (!s_len[r]) continue;
+        // (LPR 16: both half-warps stay converged through the lockstep walk below)
+        if (LPR != 16 && !s_len[r]) continue;
         if (s_len[r] >= 2) {
           scale_grad<VPL>(s_f1[r], mean, x[r]);
           add_into<VPL>(g[r], x[r]);
@@ -678,6 +679,38 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
               }
             }
           }
+        } else if constexpr (LPR == 16) {
+          // two segment streams per warp: both half-warps walk occurrences 3..32 in lockstep
+          // (to the longer of their two segments, so the warp never diverges), 4 rows in
+          // flight per half; lane gl holds occurrences 2+gl and 18+gl of its half's segment
+          const uint32_t rest = s_len[r] > 2 ? s_len[r] - 2 : 0;
+          const uint32_t rest_max = max(rest, __shfl_xor_sync(0xffffffffu, rest, 16));
+          if (rest_max) {
+            const uint32_t bl0 = gl < rest ? sbag[s_off[r] + 2 + gl] : 0u;
+            const uint32_t bl1 = gl + 16 < rest ? sbag[s_off[r] + 18 + gl] : 0u;
+            const float fl0 = (mean && gl < rest) ? static_cast<float>(a.bag_len[bl0]) : 1.f;
+            const float fl1 = (mean && gl + 16 < rest) ? static_cast<float>(a.bag_len[bl1]) : 1.f;
+            constexpr int KF = VPL >= 4 ? 1 : 4 / VPL;  // rows in flight per half (register budget)
+            for (uint32_t q0 = 0; q0 < rest_max; q0 += KF) {
+              float4 y[KF][VPL];
+              float fq[KF];
+#pragma unroll
+              for (int k = 0; k < KF; ++k) {
+                const uint32_t q = q0 + k;  // warp-uniform
+                const int src = static_cast<int>(grp * 16 + (q % 16));
+                const uint32_t vl = __shfl_sync(0xffffffffu, q < 16 ? bl0 : bl1, src);
+                fq[k] = __shfl_sync(0xffffffffu, q < 16 ? fl0 : fl1, src);
+                load_grad<VPL>(a, q < rest ? vl : 0u, gl, LPR, y[k]);
+              }
+#pragma unroll
+              for (int k = 0; k < KF; ++k) {
+                if (q0 + k < rest) {
+                  scale_grad<VPL>(fq[k], mean, y[k]);
+                  add_into<VPL>(g[r], y[k]);
+                }
+              }
+            }
+          }
         } else {
           for (uint32_t q = 2; q < s_len[r]; q += 2) {  // narrow rows: two rows in flight
             const uint32_t bq = sbag[s_off[r] + q];
@@ -694,7 +727,7 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
             }
           }
         }
-        update_store<OPT, VPL>(a, s_row[r], gl, LPR, rs[r], g[r]);
+        if (s_len[r]) update_store<OPT, VPL>(a, s_row[r], gl, LPR, rs[r], g[r]);
       }
     }
     __syncwarp();  // sbag is rewritten by the next iteration
@@ -959,7 +992,7 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
 // ---- kernels ------------------------------------------------------------------------------
 // Short segments reduced + updated.
 template <int OPT, int LPR, int VPL, bool TMA>
-__global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : (OPT == HPS_OPT_ADAM ? 2 : 3))
+__global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : (OPT == HPS_OPT_ADAM || LPR == 16 ? 2 : 3))
     k_reduce_short(BwdArgs a) {
   extern __shared__ __align__(128) float s_dyn[];  // TMA: [kRedWarps][cap][dim] rows, scales, bags
   __shared__ __align__(8) uint64_t s_bar[kRedWarps];

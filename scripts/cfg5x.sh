@@ -1,8 +1,2 @@
-HPS_BENCH_E2E_CPU=1 timeout 400 python bench.py --config cfg2 --no-cpu-baseline --steps 20 2>&1 | grep "^#\|^{" | cut -c1-120
-python - <<'PY'
-import time, torch
-x=torch.zeros(1).cuda(); torch.cuda.synchronize()
-t=time.perf_counter()
-for _ in range(1000): pass
-print("noop", (time.perf_counter()-t)*1e3)
-PY
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
