@@ -1031,6 +1031,12 @@ __global__ void k_bt_used(const uint2* bt, uint64_t n, unsigned long long* out) 
   if (lane_id() == 0 && c) atomicAdd(out, c);
 }
 
+__global__ void k_unique_count(const unsigned long long* short_alloc, const uint32_t* n_long, uint64_t* count_out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) *count_out = (*short_alloc >> 32) + *n_long;
+}
+
 // Rows updated by the last backward (short + long segments), unsorted; count -> *count_out.
 __global__ void k_unique_rows(const uint4* short_rec, const unsigned long long* short_alloc, const uint32_t* long_row,
                               const uint32_t* n_long, uint32_t* out, uint64_t* count_out) {
@@ -1392,6 +1398,11 @@ int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* un
   cudaStream_t st = t->ctx->stream;
   const uint64_t nk = t->last_n_keys_host;
   const BwdArgs a = base_args(t);
+  if (!unique_rows_out) {  // the count alone (the end-to-end step's result): one thread
+    HPSG_CUDA(launch_k(true, k_unique_count, 1, 32, 0, st, static_cast<const unsigned long long*>(a.short_alloc),
+                       static_cast<const uint32_t*>(a.n_long), count_out));
+    return HPS_GPU_OK;
+  }
   // unsorted rows into the (now free) long-list buffers, then an ascending radix sort
   k_unique_rows<<<grid_for(nk, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_short_rec, a.short_alloc, t->ws_long_row,
                                                                a.n_long, t->ws_lkey_a, count_out);
