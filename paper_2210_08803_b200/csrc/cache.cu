@@ -463,9 +463,10 @@ __global__ void __launch_bounds__(256) k_entry_prep(const uint64_t* __restrict__
                                                     uint64_t n, uint32_t dim, hps::FastMod64 fm, uint32_t invalid_set,
                                                     uint32_t* __restrict__ set_out, uint8_t* __restrict__ valid_out,
                                                     uint32_t* status, uint64_t* counts, const uint64_t* d_n,
-                                                    const uint8_t* __restrict__ skip, int f16) {
+                                                    const uint8_t* __restrict__ skip, int f16, uint64_t* zero_out) {
   pdl_wait();
   pdl_launch_dependents();
+  if (zero_out && blockIdx.x == 0 && threadIdx.x == 0) *zero_out = 0;  // the call's admitted count
   constexpr int G = 32 / LPR;
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
   const uint32_t gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1u) << (grp * LPR));
@@ -962,12 +963,12 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
 }
 
 static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n,
-                      const uint64_t* d_n = nullptr, const uint8_t* skip = nullptr) {
+                      const uint64_t* d_n = nullptr, const uint8_t* skip = nullptr, uint64_t* zero_out = nullptr) {
   cudaStream_t st = c->ctx->stream;
   const int lpr = lpr_for(c->dim);
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
   const uint32_t invalid = static_cast<uint32_t>(c->num_sets);
-#define HPSG_P(L) launch_k(true, k_entry_prep<L>, grid, 256, 0, st, keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts, d_n, skip, c->f16 ? 1 : 0)
+#define HPSG_P(L) launch_k(true, k_entry_prep<L>, grid, 256, 0, st, keys, vecs, n, c->dim, c->set_mod, invalid, c->ws_set, c->ws_hit, c->ctx->d_status, c->ws_counts, d_n, skip, c->f16 ? 1 : 0, zero_out)
   switch (lpr) {
     case 32: HPSG_P(32); break;
     case 16: HPSG_P(16); break;
@@ -986,10 +987,12 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
   if (int s = check_cache(c)) return s;
   if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = c->ctx->stream;
-  if (admitted_out) HPSG_CUDA(cudaMemsetAsync(admitted_out, 0, sizeof(uint64_t), st));
-  if (n == 0) return HPS_GPU_OK;
+  if (n == 0) {
+    if (admitted_out) HPSG_CUDA(cudaMemsetAsync(admitted_out, 0, sizeof(uint64_t), st));
+    return HPS_GPU_OK;
+  }
   if (!keys || !vecs) return HPS_GPU_E_INVALID_ARGUMENT;
-  if (int s = entry_prep(c, keys, vecs, n, d_n, skip)) return s;
+  if (int s = entry_prep(c, keys, vecs, n, d_n, skip, admitted_out)) return s;  // zeroes *admitted_out
   RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
   HPSG_CUDA(launch_scan(rop, n, c->ws_scan, st));
   const uint32_t* sets_sorted;
@@ -1020,10 +1023,12 @@ int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* ve
   if (int s = check_cache(c)) return s;
   if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = c->ctx->stream;
-  if (replaced_out) HPSG_CUDA(cudaMemsetAsync(replaced_out, 0, sizeof(uint64_t), st));
-  if (n == 0) return HPS_GPU_OK;
+  if (n == 0) {
+    if (replaced_out) HPSG_CUDA(cudaMemsetAsync(replaced_out, 0, sizeof(uint64_t), st));
+    return HPS_GPU_OK;
+  }
   if (!keys || !vecs || !versions) return HPS_GPU_E_INVALID_ARGUMENT;
-  if (int s = entry_prep(c, keys, vecs, n)) return s;
+  if (int s = entry_prep(c, keys, vecs, n, nullptr, nullptr, replaced_out)) return s;  // zeroes *replaced_out
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
