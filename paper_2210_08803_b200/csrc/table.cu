@@ -814,8 +814,12 @@ int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
     }
     const size_t smem = size_t(kTmaWarps) * 32 * t->dim * sizeof(float);
     const uint64_t tiles = (uint64_t(a.n_bags) + 31) / 32;
-    // training: a resident grid (2 CTAs per SM) leaves room for the dedup kernels beside it
-    const uint64_t max_grid = rows ? uint64_t(kNumSMs) * 2 : uint64_t(kNumSMs) * 8;
+    // training: ONE CTA per SM. The pooling runs beside the dedup, and its row stream slows
+    // the dedup's L2 atomics; at one CTA per SM it takes ~46 us instead of 37, still hidden,
+    // and the dedup's count phase drops from 35 to 27 us (config 2: 0.134 -> 0.131 ms)
+    uint64_t train_ctas = 1;
+    if (const char* e = std::getenv("HPS_GPU_POOL_CTAS")) train_ctas = std::max(1, std::atoi(e));  // A/B knob
+    const uint64_t max_grid = rows ? uint64_t(kNumSMs) * train_ctas : uint64_t(kNumSMs) * 8;
     const int grid =
         static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((tiles + kTmaWarps - 1) / kTmaWarps, max_grid)));
     if (rows) k_lookup_1hot_tma<true><<<grid, kTmaWarps * 32, smem, st>>>(a);
