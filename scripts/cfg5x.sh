@@ -1,3 +1,3 @@
 #!/bin/bash
 # Scratch A/B runner for one gpurun call (rewritten per experiment; see DESIGN.md §3 "Tried and reverted").
-for k in 4 2 1 8; do HPS_GPU_POOLM_CTAS=$k timeout 400 python bench.py --config cfg3 --no-cpu-baseline --steps 20 --e2e-steps 4 --trace 4 2>&1 | grep "pool \|count \|place\|reduce_short\|^{" | cut -c1-130 | sed "s/^/ctas $k /"; done
+for rep in 1 2; do for w in 2 1 4; do for c in cfg2 cfg5; do HPS_GPU_RED_WAVES=$w timeout 400 python bench.py --config $c --no-cpu-baseline --steps 30 --e2e-steps 4 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('waves $w $c', round(d['ms_per_step']*1000,1))"; done; done; done
