@@ -1147,7 +1147,9 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
       HPSG_CUDA(prefer_max_smem(k_long_tasks));
       attr = true;
     }
-    const int g = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kNumSMs, (nk + 511) / 512)));
+    uint64_t per_cta = 256;  // occurrences per CTA below a full grid (more CTAs: shorter chains; cfg1 64.9 -> 63.4 us)
+    if (const char* e = std::getenv("HPS_GPU_DEDUP_PER_CTA")) per_cta = std::max(64, std::atoi(e));  // A/B knob
+    const int g = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kNumSMs, (nk + per_cta - 1) / per_cta)));
     // A plain launch (a cooperative one would not start beside the pooling): co-residency of
     // the grid barriers holds by construction — at most one CTA per SM, and every kernel it
     // can share the SMs with (the pooling) runs to completion without waiting on it.
