@@ -138,8 +138,8 @@ int hps_gpu_table_size(hps_gpu_table tbl, uint32_t table, uint64_t* n_rows_host)
 /* Insert keys into `table`. New keys get row ids in order of first occurrence in
  * keys[] (continuing from the table's row count); existing keys keep theirs.
  * rows == NULL: new rows are initialised with hps_gpu_init_value(seed,key,j);
- * otherwise rows[i*dim..] is the value of keys[i] (the first occurrence wins for a
- * new key; existing rows are overwritten by the LAST occurrence). rows_out (may be
+ * otherwise rows[i*dim..] is the value of keys[i]: the FIRST occurrence of a key in
+ * keys[] wins, both for a new key and for an existing row it overwrites. rows_out (may be
  * NULL) receives the row id of every key. NaN/Inf in rows -> NonFinite (latched);
  * more distinct keys than capacity -> Infeasible (latched). */
 int hps_gpu_table_insert(hps_gpu_table tbl, uint32_t table, const uint64_t* keys, uint64_t n,
@@ -176,8 +176,9 @@ int hps_gpu_lookup_pooled(hps_gpu_table tbl, const uint64_t* keys, const uint32_
 int hps_gpu_backward_update(hps_gpu_table tbl, const float* d_out, const hps_opt_params* opt_host);
 
 /* After backward_update: number of unique rows updated (device u64 at *count_out),
- * and optionally their row ids in ascending row order (unique_rows_out, capacity
- * max_batch_keys). Used by the dedup parity tests. */
+ * and optionally their row ids in ascending row order (unique_rows_out: exactly
+ * *count_out entries are written, so a buffer of the unique count suffices). Used by
+ * the dedup parity tests. */
 int hps_gpu_table_last_unique(hps_gpu_table tbl, uint64_t* count_out, uint32_t* unique_rows_out);
 
 /* Tracing (no reference counterpart): in-graph timeline of the training
@@ -315,6 +316,12 @@ int hps_gpu_cache_stats(hps_gpu_cache cache, hps_cache_stats* stats_host);
 int hps_gpu_cache_reset_stats(hps_gpu_cache cache);
 /* syncs: number of resident entries. */
 int hps_gpu_cache_size(hps_gpu_cache cache, uint64_t* n_host);
+/* White-box parity (tests): the whole set-major state, way e = set * ways + w — keys,
+ * versions, freq (0 = empty way), last_touch [capacity], the per-set aging counters
+ * [capacity / ways], and the raw rows (fp32, or binary16 bits for an F16 cache)
+ * [capacity x dim]. Device pointers, any may be NULL; asynchronous on the stream. */
+int hps_gpu_cache_debug_export(hps_gpu_cache cache, uint64_t* keys, uint64_t* versions, uint8_t* freq,
+                               uint64_t* last_touch, uint64_t* set_access, void* vecs);
 
 /* ---- UpdateBatch frames -> cache refresh (update.cu) ----
  * Frame (little-endian): "HPSU" | version u8 = 1 | name_len u16 | name |

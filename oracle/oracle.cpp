@@ -748,6 +748,18 @@ void orc_cache_set_state(void* h, uint64_t set, uint64_t* keys, uint64_t* versio
   std::memcpy(last_touch, &c->last_touch[b], c->ways * 8);
 }
 
+// The whole cache state (white-box parity with hps_gpu_cache_debug_export); NULL skips.
+void orc_cache_export(void* h, uint64_t* keys, uint64_t* versions, uint8_t* freq, uint64_t* last_touch,
+                      uint64_t* set_access, float* vecs) {
+  auto* c = static_cast<Cache*>(h);
+  if (keys) std::memcpy(keys, c->key.data(), c->capacity * 8);
+  if (versions) std::memcpy(versions, c->version.data(), c->capacity * 8);
+  if (freq) std::memcpy(freq, c->freq.data(), c->capacity);
+  if (last_touch) std::memcpy(last_touch, c->last_touch.data(), c->capacity * 8);
+  if (set_access) std::memcpy(set_access, c->set_acc.data(), c->num_sets * 8);
+  if (vecs) std::memcpy(vecs, c->vec.data(), c->capacity * c->dim * 4);
+}
+
 // ---- sparse CPU step (baseline timing; same math as the table model) ----
 void* orc_sparse_create(uint32_t n_tables, uint32_t dim, const uint32_t* slot_table, uint32_t n_slots, int optimizer,
                         uint64_t seed, float a0) {

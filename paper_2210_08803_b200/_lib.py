@@ -154,6 +154,7 @@ SIGNATURES = {
     "hps_gpu_cache_stats": (i32, [vp, C.POINTER(CacheStats)]),
     "hps_gpu_cache_reset_stats": (i32, [vp]),
     "hps_gpu_cache_size": (i32, [vp, C.POINTER(u64)]),
+    "hps_gpu_cache_debug_export": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "hps_update_batch_parse": (i32, [vp, u64, C.POINTER(UpdateHeader)]),
     "hps_update_batch_encode": (i32, [C.c_char_p, u32, u64, u32, u32, i32, vp, vp, vp, u64, C.POINTER(u64)]),
     "hps_gpu_update_decode": (i32, [vp, vp, C.POINTER(UpdateHeader), vp, vp, vp]),

@@ -14,6 +14,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from ._lib import HpsError
 
 _OPT = {"sgd": L.OPT_SGD, "adagrad": L.OPT_ADAGRAD, "adam": L.OPT_ADAM}
 _COMB = {"sum": L.COMBINER_SUM, "mean": L.COMBINER_MEAN}
@@ -226,6 +227,7 @@ class HotCache:
         h = C.c_void_p()
         L.check(self.lib.hps_gpu_cache_create(ctx.h, C.byref(cfg), C.byref(h)), "cache_create")
         self.h = h
+        self.capacity, self.ways = capacity, ways
         self.max_batch = max_batch
         self._found_idx = torch.empty(max_batch, dtype=torch.int32, device=self.device)
         self._missing_idx = torch.empty(max_batch, dtype=torch.int32, device=self.device)
@@ -281,6 +283,22 @@ class HotCache:
         n = C.c_uint64()
         L.check(self.lib.hps_gpu_cache_size(self.h, C.byref(n)), "cache_size")
         return n.value
+
+    def export_state(self):
+        """White-box state (tests): numpy (keys, versions, freq, last_touch, set_access, vecs
+        as fp32 — binary16 rows widened), set-major, way e = set * ways + w."""
+        cap = self.capacity
+        k = torch.empty(cap, dtype=torch.int64, device=self.device)
+        v = torch.empty_like(k)
+        t = torch.empty_like(k)
+        f = torch.empty(cap, dtype=torch.uint8, device=self.device)
+        a = torch.empty(cap // self.ways, dtype=torch.int64, device=self.device)
+        x = torch.empty(cap, self.dim, dtype=torch.float16 if self.dtype == "f16" else torch.float32,
+                        device=self.device)
+        L.check(self.lib.hps_gpu_cache_debug_export(self.h, _ptr(k), _ptr(v), _ptr(f), _ptr(t), _ptr(a), _ptr(x)),
+                "cache_debug_export")
+        u = lambda z: z.cpu().numpy().view(np.uint64)
+        return u(k), u(v), f.cpu().numpy(), u(t), u(a), x.float().cpu().numpy()
 
     def close(self) -> None:
         if getattr(self, "h", None):

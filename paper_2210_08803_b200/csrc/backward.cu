@@ -1031,6 +1031,12 @@ __global__ void k_bt_used(const uint2* bt, uint64_t n, unsigned long long* out) 
   if (lane_id() == 0 && c) atomicAdd(out, c);
 }
 
+__global__ void k_copy_counted(const uint32_t* __restrict__ src, const uint64_t* count, uint32_t* __restrict__ dst) {
+  const uint64_t n = *count;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
 __global__ void k_unique_count(const unsigned long long* short_alloc, const uint32_t* n_long, uint64_t* count_out) {
   pdl_wait();
   pdl_launch_dependents();
@@ -1051,13 +1057,12 @@ template <int OPT, int LPR, int VPL, bool TMA>
 int launch_backward_v(const BwdArgs& a, cudaStream_t st, cudaStream_t side, size_t smem, int grid, int long_grid) {
   auto kern = k_reduce_short<OPT, LPR, VPL, TMA>;
   constexpr int block = TMA ? kRedWarps * 32 : 256;
-  static bool attr = false;
-  if (!attr) {
-    HPSG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    HPSG_CUDA(prefer_max_smem(kern));
-    HPSG_CUDA(prefer_max_smem(k_long<OPT, LPR, VPL>));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  HPSG_CUDA(once_per_device(attr, [&]() -> cudaError_t {
+    if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)) return e;
+    if (cudaError_t e = prefer_max_smem(kern)) return e;
+    return prefer_max_smem(k_long<OPT, LPR, VPL>);
+  }));
   HPSG_CUDA(launch_k(false, k_long<OPT, LPR, VPL>, long_grid, 256, 0, side, a));  // first after a join
   HPSG_CUDA(launch_k(false, kern, grid, block, smem, st, a));
   return HPS_GPU_OK;
@@ -1127,6 +1132,31 @@ BwdArgs base_args(hps_gpu_table t) {
 
 }  // namespace
 
+namespace {
+std::atomic<uint64_t> g_dedup_attr{0};
+cudaError_t dedup_attributes() {
+  return once_per_device(g_dedup_attr, []() -> cudaError_t {
+    if (cudaError_t e = cudaFuncSetAttribute(k_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4))
+      return e;
+    for (cudaError_t e : {prefer_max_smem(k_dedup), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass),
+                          prefer_max_smem(k_scan<LongRegOp>), prefer_max_smem(k_long_tasks)})
+      if (e) return e;
+    return cudaSuccess;
+  });
+}
+}  // namespace
+
+int hpsg::check_dedup_residency() {
+  HPSG_CUDA(dedup_attributes());
+  int per_sm = 0;
+  HPSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dedup, kDedupBlock, size_t(2) * kDedupHash * 4));
+  if (per_sm < 1) {
+    set_last_error("k_dedup (persistent, grid barriers) cannot keep one CTA resident per SM on this device");
+    return HPS_GPU_E_NO_DEVICE;
+  }
+  return HPS_GPU_OK;
+}
+
 // K4a-K4d on the table's side stream, right after the training probe (table.cu
 // fork_dedup): they need only the occurrence record, so they overlap the pooling.
 int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
@@ -1137,19 +1167,15 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
   const BwdArgs a = base_args(t);
   // K4a-c: counts, allocation, placement (first on this stream after the fork: a plain launch)
   {
-    static bool attr = false;
-    if (!attr) {
-      HPSG_CUDA(cudaFuncSetAttribute(k_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4));
-      HPSG_CUDA(prefer_max_smem(k_dedup));
-      HPSG_CUDA(prefer_max_smem(k_radix_hist));
-      HPSG_CUDA(prefer_max_smem(k_radix_pass));
-      HPSG_CUDA(prefer_max_smem(k_scan<LongRegOp>));
-      HPSG_CUDA(prefer_max_smem(k_long_tasks));
-      attr = true;
-    }
+    HPSG_CUDA(dedup_attributes());
+
     uint64_t per_cta = 256;  // occurrences per CTA below a full grid (more CTAs: shorter chains; cfg1 64.9 -> 63.4 us)
     if (const char* e = std::getenv("HPS_GPU_DEDUP_PER_CTA")) per_cta = std::max(64, std::atoi(e));  // A/B knob
-    const int g = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(kNumSMs, (nk + per_cta - 1) / per_cta)));
+    // at most one CTA per SM of THIS device (a MIG slice or a smaller part has fewer): the
+    // grid barriers need every CTA resident, which one per SM guarantees (table create
+    // checked that one k_dedup CTA fits an SM)
+    const uint64_t sms = static_cast<uint64_t>(t->ctx->num_sms);
+    const int g = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(sms, (nk + per_cta - 1) / per_cta)));
     // A plain launch (a cooperative one would not start beside the pooling): co-residency of
     // the grid barriers holds by construction — at most one CTA per SM, and every kernel it
     // can share the SMs with (the pooling) runs to completion without waiting on it.
@@ -1414,8 +1440,10 @@ int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* un
   const bool in_b = radix_sort_pairs(st, t->ws_lkey_a, nullptr, t->ws_lval_a, t->ws_lkey_b, t->ws_lval_b, count_out,
                                      nk, t->sort_bits, t->ws_zero, &err);
   if (err != cudaSuccess) return cuda_status(err, "last_unique sort");
-  HPSG_CUDA(cudaMemcpyAsync(unique_rows_out, in_b ? t->ws_lkey_b : t->ws_lkey_a, nk * sizeof(uint32_t),
-                            cudaMemcpyDeviceToDevice, st));
+  // only the *count_out unique rows: the caller's buffer may be sized to the unique count
+  k_copy_counted<<<grid_for(nk, 256, kNumSMs * 8), 256, 0, st>>>(in_b ? t->ws_lkey_b : t->ws_lkey_a, count_out,
+                                                                  unique_rows_out);
+  HPSG_CHECK_LAUNCH("k_copy_counted");
   return HPS_GPU_OK;
 }
 

@@ -1074,6 +1074,21 @@ int hps_gpu_cache_reset_stats(hps_gpu_cache c) {
   return HPS_GPU_OK;
 }
 
+int hps_gpu_cache_debug_export(hps_gpu_cache c, uint64_t* keys, uint64_t* versions, uint8_t* freq,
+                               uint64_t* last_touch, uint64_t* set_access, void* vecs) {
+  if (int s = check_cache(c)) return s;
+  cudaStream_t st = c->ctx->stream;
+  const uint64_t cap = c->capacity;
+  if (keys) HPSG_CUDA(cudaMemcpyAsync(keys, c->d_keys, cap * 8, cudaMemcpyDeviceToDevice, st));
+  if (versions) HPSG_CUDA(cudaMemcpyAsync(versions, c->d_ver, cap * 8, cudaMemcpyDeviceToDevice, st));
+  if (freq) HPSG_CUDA(cudaMemcpyAsync(freq, c->d_freq, cap, cudaMemcpyDeviceToDevice, st));
+  if (last_touch) HPSG_CUDA(cudaMemcpyAsync(last_touch, c->d_touch, cap * 8, cudaMemcpyDeviceToDevice, st));
+  if (set_access) HPSG_CUDA(cudaMemcpyAsync(set_access, c->d_set_acc, c->num_sets * 8, cudaMemcpyDeviceToDevice, st));
+  if (vecs)
+    HPSG_CUDA(cudaMemcpyAsync(vecs, c->d_vec, cap * c->dim * (c->f16 ? 2 : 4), cudaMemcpyDeviceToDevice, st));
+  return HPS_GPU_OK;
+}
+
 int hps_gpu_cache_size(hps_gpu_cache c, uint64_t* n_host) {
   if (int s = check_cache(c)) return s;
   if (!n_host) return HPS_GPU_E_INVALID_ARGUMENT;

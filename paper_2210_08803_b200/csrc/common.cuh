@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
 #include <string>
 #include <type_traits>
 
@@ -239,6 +241,22 @@ __device__ __forceinline__ void grid_barrier_once(uint32_t* counter) {
   __syncthreads();
 }
 
+// One-time per-DEVICE setup (function attributes are per device): `done` is a bitmask of
+// devices already set up (a static per call site); fn() returns a cudaError_t. Thread-safe.
+template <class F>
+cudaError_t once_per_device(std::atomic<uint64_t>& done, F&& fn) {
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  static std::mutex m;
+  std::lock_guard<std::mutex> g(m);
+  if (done.load(std::memory_order_relaxed) & bit) return cudaSuccess;
+  const cudaError_t e = fn();
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
+
 inline int grid_for(uint64_t n, int block, int max_blocks = kNumSMs * 16) {
   uint64_t g = (n + block - 1) / block;
   if (g < 1) g = 1;
@@ -321,4 +339,5 @@ struct hps_gpu_ctx_s {
   uint32_t* d_status = nullptr;  // latched device status word
   uint32_t* h_status = nullptr;  // pinned mirror for sync
   bool pdl = true;               // programmatic dependent launch in the step chains (HPS_GPU_NO_PDL=1 disables)
+  int num_sms = hpsg::kNumSMs;   // multiProcessorCount of the device (the persistent dedup's grid cap)
 };

@@ -128,6 +128,7 @@ int hps_gpu_ctx_create(int device, void* stream, hps_gpu_ctx* out) {
   HPSG_CUDA(cudaSetDevice(device));
   auto* c = new hps_gpu_ctx_s;
   c->device = device;
+  c->num_sms = prop.multiProcessorCount;
   c->stream = static_cast<cudaStream_t>(stream);
   if (const char* e = std::getenv("HPS_GPU_NO_PDL")) c->pdl = e[0] != '1';
   if (cudaMalloc(&c->d_status, sizeof(uint32_t)) != cudaSuccess ||

@@ -290,6 +290,8 @@ struct LookupArgs {
   uint32_t* occ_bag;   // multi-hot: bag of each occurrence
   uint32_t* bag_len;   // multi-hot mean: bag lengths
   uint64_t* d_n;       // number of key occurrences (device)
+  uint64_t max_keys;   // training record capacity (max_batch_keys)
+  uint32_t* status;    // ctx status word: a device-offsets batch larger than max_keys latches InvalidArgument
 };
 
 // K3a (training): probe every occurrence once and record its row (row_absent when the
@@ -301,6 +303,23 @@ __global__ void __launch_bounds__(256) k_probe(LookupArgs a) {
   const uint32_t lane = lane_id();
   const uint64_t n_bags = a.n_bags;
   trace_begin(kTrProbe);
+  if constexpr (MULTI) {
+    // device offsets are not validated on the host: a batch beyond the record's capacity is
+    // refused here (latched InvalidArgument, an empty record) instead of overrunning it
+    const uint64_t total = a.offsets[n_bags];
+    if (total > a.max_keys) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *a.d_n = 0;
+        latch_status(a.status, HPS_GPU_E_INVALID_ARGUMENT);
+      }
+      // the pooling still walks the offsets: every recorded row reads as absent
+      for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < a.max_keys;
+           i += uint64_t(gridDim.x) * blockDim.x)
+        a.occ_row[i] = a.row_absent;
+      trace_end(kTrProbe);
+      return;
+    }
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) *a.d_n = MULTI ? a.offsets[n_bags] : n_bags;
   if constexpr (!MULTI) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_bags; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -360,6 +379,7 @@ __global__ void k_reset_counts(const uint32_t* __restrict__ occ_row, const uint3
 template <bool ROWS>
 __device__ __forceinline__ uint32_t occurrence_row(const LookupArgs& a, uint64_t i, uint32_t table) {
   if constexpr (ROWS) {
+    if (i >= a.max_keys) return kRowEmpty;  // an oversized device-offsets batch (refused by k_probe)
     const uint32_t r = a.occ_row[i];
     return r == a.row_absent ? kRowEmpty : r;
   } else {
@@ -732,6 +752,8 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk) {
 
   a.row_absent = t->row_absent;
   a.d_n = t->ws_counts;
+  a.max_keys = t->max_keys;
+  a.status = t->ctx->d_status;
   t->counts_dirty = true;
   t->have_unique = false;
   return HPS_GPU_OK;
@@ -802,16 +824,16 @@ int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
   }
   const bool tma_ok = t->dim <= 256 && (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0 && !t->no_tma;
   if (!multi && tma_ok) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_lookup_1hot_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kTmaWarps * 32 * 256 * 4);
-      cudaFuncSetAttribute(k_lookup_1hot_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kTmaWarps * 32 * 256 * 4);
-      prefer_max_smem(k_lookup_1hot_tma<true>);
-      prefer_max_smem(k_lookup_1hot_tma<false>);
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    HPSG_CUDA(once_per_device(attr, []() -> cudaError_t {
+      for (cudaError_t e : {cudaFuncSetAttribute(k_lookup_1hot_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kTmaWarps * 32 * 256 * 4),
+                            cudaFuncSetAttribute(k_lookup_1hot_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kTmaWarps * 32 * 256 * 4),
+                            prefer_max_smem(k_lookup_1hot_tma<true>), prefer_max_smem(k_lookup_1hot_tma<false>)})
+        if (e) return e;
+      return cudaSuccess;
+    }));
     const size_t smem = size_t(kTmaWarps) * 32 * t->dim * sizeof(float);
     const uint64_t tiles = (uint64_t(a.n_bags) + 31) / 32;
     // training: ONE CTA per SM. The pooling runs beside the dedup, and its row stream slows
@@ -865,6 +887,7 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
   HPSG_CUDA(cudaSetDevice(ctx->device));
+  if (int s = check_dedup_residency()) return s;
   auto t = new hps_gpu_table_s;
   t->ctx = ctx;
   t->n_tables = cfg->n_tables;

@@ -49,6 +49,7 @@ inline uint64_t bwd_max_nodes(uint64_t max_keys) { return bwd_max_chunks(max_key
 struct hps_gpu_table_s;
 namespace hpsg {
 int launch_dedup(hps_gpu_table_s* t, cudaStream_t st);  // backward.cu: K4a-K4d (on t->side)
+int check_dedup_residency();  // backward.cu: one persistent k_dedup CTA must fit an SM of the current device
 cudaError_t trace_attach_table(TraceRec* p);  // table.cu's copy of the trace pointer
 }
 

@@ -49,6 +49,7 @@ _SIG = {
     "orc_cache_reset_stats": (None, [vp]),
     "orc_cache_size": (u64, [vp]),
     "orc_cache_set_state": (None, [vp, u64, vp, vp, vp, vp]),
+    "orc_cache_export": (None, [vp, vp, vp, vp, vp, vp, vp]),
 }
 
 _lib = None
@@ -206,6 +207,17 @@ class OracleCache:
 
     def size(self):
         return self.L.orc_cache_size(self.h)
+
+    def export(self, capacity):
+        """Whole set-major state: (keys, versions, freq, last_touch, set_access, vecs)."""
+        k = np.empty(capacity, np.uint64)
+        v = np.empty(capacity, np.uint64)
+        f = np.empty(capacity, np.uint8)
+        t = np.empty(capacity, np.uint64)
+        a = np.empty(capacity // self.ways, np.uint64)
+        x = np.empty((capacity, self.dim), np.float32)
+        self.L.orc_cache_export(self.h, P(k), P(v), P(f), P(t), P(a), P(x))
+        return k, v, f, t, a, x
 
     def __del__(self):
         try:

@@ -45,6 +45,19 @@ def ins_both(ctx, g, o, keys, vecs, vers):
     return on
 
 
+def assert_same_state(g, o, cap):
+    """White-box: every way of every set identical — key, version, freq, last_touch, the
+    row — and every set's aging counter (hps_gpu_cache_debug_export vs the oracle)."""
+    gs, os_ = g.export_state(), o.export(cap)
+    for name, x, y in zip(["keys", "versions", "freq", "last_touch", "set_access", "vecs"], gs, os_):
+        if name in ("keys", "versions", "last_touch", "vecs"):  # an empty way's payload is unspecified
+            live = os_[2] != 0
+            x, y = x[live], y[live]
+        if name == "vecs":
+            x, y = x.view(np.uint32), y.view(np.uint32)
+        np.testing.assert_array_equal(x, y, err_msg=name)
+
+
 def test_spec_examples(ctx):
     g, o = pair(ctx, 64, 4)
     fi, fv, mi = g.query(t64(np.array([1, 2, 3], dtype=np.uint64)))  # empty cache: all missing
@@ -127,14 +140,7 @@ def test_randomized_sequences_match_oracle(ctx, cap, ways, aging, small_sort, mo
         version += 2
         assert g.stats() == o.stats(), rnd
     assert g.size() == o.size()
-    # white-box: every set's metadata identical
-    sets = cap // ways
-    for s in range(sets):
-        ok = np.empty(ways, np.uint64)
-        ov = np.empty(ways, np.uint64)
-        of = np.empty(ways, np.uint8)
-        ot = np.empty(ways, np.uint64)
-        O.lib().orc_cache_set_state(o.h, s, O.P(ok), O.P(ov), O.P(of), O.P(ot))
+    assert_same_state(g, o, cap)
     q_both(g, o, W.mix64(np.arange(3 * cap, dtype=np.uint64)))
 
 
@@ -276,7 +282,33 @@ def test_f16_storage_sequences_match_oracle(ctx, cap, ways, aging):
             assert int(gn.item()) == on
         version += 2
         assert g.stats() == o.stats(), rnd
+    assert_same_state(g, o, cap)
     q_both(g, o, W.mix64(np.arange(3 * cap, dtype=np.uint64)))
+
+
+@pytest.mark.parametrize("aging_p", [0, 16])
+def test_config4_shape_large_batches(ctx, aging_p):
+    """BASELINE config 4 shape at reduced capacity: dim 128 rows, 8 ways, Zipf(1.05) query
+    batches of 131,072 keys (Zipf-head sets see thousands of accesses per batch: the huge-set
+    replay), misses inserted after each batch; found order, rows, missing order, stats and
+    the whole set state identical to the oracle. aging_p: accesses per set-aging period
+    (0 = the 10 x capacity default, i.e. 80; 16 exercises the per-32-access closed form)."""
+    cap, dim, ways, n = 1 << 16, 128, 8, 131072
+    sets = cap // ways
+    g = HotCache(ctx, cap, dim, ways, aging_p * sets, n)
+    o = O.OracleCache(cap, dim, ways, aging_p * sets)
+    zipf = W.Zipf(2_000_000, 1.05)
+    rs = np.random.default_rng(aging_p)
+    for rnd in range(4):
+        keys = W.mix64(zipf.ranks(W.rng(1000 + rnd, np.arange(n, dtype=np.uint64))).astype(np.uint64))
+        oi, om = q_both(g, o, keys)
+        miss = keys[om]
+        vecs = rs.standard_normal((len(miss), dim)).astype(np.float32)
+        ins_both(ctx, g, o, miss, vecs, np.full(len(miss), rnd + 1, np.uint64))
+        assert g.stats() == o.stats(), rnd
+    s = g.stats()
+    assert s["hits"] > 0 and s["evictions"] > 0
+    assert_same_state(g, o, cap)
 
 
 def test_f16_storage_range_and_spec_examples(ctx):
