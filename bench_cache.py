@@ -90,31 +90,20 @@ def main():
     ctx.sync()
     warm_s = time.perf_counter() - t1
 
-    if args.phases:  # per-call device times at the max batch (events between the three C-ABI calls)
-        import ctypes as C
-        from paper_2210_08803_b200 import _lib as LL
-        ph = {"query": [], "read_through": [], "insert": []}
-        for _ in range(10):
-            kb = zipf_keys(args.max_batch)
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-            nq = kb.numel()
-            ev[0].record()
-            fv, fi, mi, cnt = cache.query_async(kb, found_vecs=rt.found)
-            ev[1].record()
-            LL.check(rt.lib.hps_gpu_table_read_through(rt.table.h, rt.table_id, kb.data_ptr(), fv.data_ptr(),
-                                                       fi.data_ptr(), mi.data_ptr(), cnt.data_ptr(), nq,
-                                                       rt.out.data_ptr(), rt.miss_keys.data_ptr(),
-                                                       rt.miss_vecs.data_ptr(), rt.miss_absent.data_ptr()), "rt")
-            ev[2].record()
-            LL.check(rt.lib.hps_gpu_cache_insert_count(cache.h, rt.miss_keys.data_ptr(), rt.miss_vecs.data_ptr(), None,
-                                                       nq, C.c_void_p(cnt.data_ptr() + 8), rt.miss_absent.data_ptr(),
-                                                       rt.admitted.data_ptr()), "ins")
-            ev[3].record()
-            ev[3].synchronize()
-            for k, (a, b2) in zip(ph, [(0, 1), (1, 2), (2, 3)]):
-                ph[k].append(ev[a].elapsed_time(ev[b2]) * 1000.0)
-        print("# phases at batch", args.max_batch, {k: round(float(np.median(v)), 1) for k, v in ph.items()},
-              file=sys.stderr, flush=True)
+    if args.phases:  # per-stage device times of the cache query inside each lookup (stderr)
+        os.environ["HPS_GPU_CACHE_PHASES"] = "1"
+        for _ in range(3):
+            rt.lookup(zipf_keys(args.max_batch))
+        ctx.sync()
+        del os.environ["HPS_GPU_CACHE_PHASES"]
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6541.8))
 
     results = []
     b = 1
@@ -138,9 +127,17 @@ def main():
             lat.append(e0.elapsed_time(e1) * 1000.0)
         s = cache.stats()
         lat = np.array(lat)
-        line = {"config": "cfg4-hps-cache", "dtype": args.dtype, "graph": not args.eager, "batch": b, "p50_us": float(np.median(lat)),
-                "p95_us": float(np.percentile(lat, 95)), "keys_per_s": b / (np.median(lat) / 1e6),
-                "hit_rate": s["hits"] / max(1, s["queries"])}
+        src = rt.sources()  # the last batch's per-key sources
+        n_hit, n_miss = src["L1"], src["L2"] + src["Default"]
+        # SURVEY §8(d) cache-query bytes over the INPUT keys: Q(k + 8 ways) + H(2 D e + 18) + M 12
+        row = args.dim * (2 if args.dtype == "f16" else 4)
+        alg = b * (8 + 8 * 8) + n_hit * (2 * row + 18) + n_miss * 12
+        p50 = float(np.median(lat))
+        line = {"config": "cfg4-hps-cache", "dtype": args.dtype, "graph": not args.eager, "batch": b, "p50_us": p50,
+                "p95_us": float(np.percentile(lat, 95)), "keys_per_s": b / (p50 / 1e6),
+                "hit_rate": s["hits"] / max(1, s["queries"]),  # over the distinct keys the cache saw
+                "key_hit_rate": n_hit / b, "unique_frac": int(rt.n_unique.item()) / b,
+                "alg_bytes": alg, "achieved_gbs": alg / (p50 * 1e3), "frac_hbm": alg / (p50 * 1e3) / hbm_peak}
         results.append(line)
         print(json.dumps(line), flush=True)
         b *= 2
@@ -162,7 +159,8 @@ def main():
                "sample": "200k cold keys, 4096-key batches, query + insert of misses, 1M-row cache"}
     summary = {"config": "cfg4-hps-cache", "dtype": args.dtype, "summary": True, "keys": args.keys, "capacity": args.capacity,
                "dim": args.dim, "zipf": args.zipf, "ideal_static_hit_rate": ideal,
-               "hit_rate_at_max_batch": results[-1]["hit_rate"], "p50_us_batch1": results[0]["p50_us"],
+               "hit_rate_at_max_batch": results[-1]["hit_rate"],
+               "key_hit_rate_at_max_batch": results[-1]["key_hit_rate"], "frac_hbm_max_batch": results[-1]["frac_hbm"], "p50_us_batch1": results[0]["p50_us"],
                "p50_us_max_batch": results[-1]["p50_us"], "keys_per_s_max_batch": results[-1]["keys_per_s"],
                "setup_s": setup_s, "warmup_s": warm_s, "warmup_accesses": n_warm, "cpu_baseline": cpu}
     print(json.dumps(summary), flush=True)

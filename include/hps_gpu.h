@@ -311,6 +311,26 @@ int hps_gpu_cache_insert_count(hps_gpu_cache cache, const uint64_t* keys, const 
 int hps_gpu_table_read_through(hps_gpu_table tbl, uint32_t table, const uint64_t* keys, const float* found_vecs,
                                const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
                                uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent);
+/* ---- orchestrator batch lookup (orchestrator.cu) --------------
+ * The orchestrator's red data flow on one GPU: the cache (L1) in front of table `table`
+ * of a table group (the lower tier; the VDB/PDB tiers are not on the GPU path).
+ * lookup: out[i] (input order, [n x dim] fp32) = the row of keys[i] from the first tier
+ * holding it — the cache, else the table, else the table's default vector. Duplicate keys
+ * are served from ONE probe per distinct key: the distinct keys, in order of first
+ * occurrence, are what the cache sees (one access each: stats count distinct keys). The
+ * distinct misses present in the table are migrated into the cache once each (version
+ * kBulkLoadVersion); keys absent everywhere are never cached. source_counts_out (device
+ * u64[4], may be NULL) = per INPUT key {L1 cache, L2 table, L3 = 0, Default}
+ * (LookupResult.source_counts); n_unique_out (device u64, may be NULL).
+ * Asynchronous, no allocation, capturable. The cache, the table and the read-through
+ * share one context; max_batch <= the cache's max_batch. */
+typedef struct hps_gpu_readthrough_s* hps_gpu_readthrough;
+int hps_gpu_readthrough_create(hps_gpu_cache cache, hps_gpu_table tbl, uint32_t table, uint64_t max_batch,
+                               hps_gpu_readthrough* out_host);
+int hps_gpu_readthrough_destroy(hps_gpu_readthrough rt);
+int hps_gpu_readthrough_lookup(hps_gpu_readthrough rt, const uint64_t* keys, uint64_t n, float* out,
+                               uint64_t* source_counts_out, uint64_t* n_unique_out);
+
 /* syncs. */
 int hps_gpu_cache_stats(hps_gpu_cache cache, hps_cache_stats* stats_host);
 int hps_gpu_cache_reset_stats(hps_gpu_cache cache);

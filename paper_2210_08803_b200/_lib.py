@@ -151,6 +151,9 @@ SIGNATURES = {
     "hps_gpu_cache_refresh": (i32, [vp, vp, vp, vp, u64, vp]),
     "hps_gpu_cache_insert_count": (i32, [vp, vp, vp, vp, u64, vp, vp, vp]),
     "hps_gpu_table_read_through": (i32, [vp, u32, vp, vp, vp, vp, vp, u64, vp, vp, vp, vp]),
+    "hps_gpu_readthrough_create": (i32, [vp, vp, u32, u64, C.POINTER(vp)]),
+    "hps_gpu_readthrough_destroy": (i32, [vp]),
+    "hps_gpu_readthrough_lookup": (i32, [vp, vp, u64, vp, vp, vp]),
     "hps_gpu_cache_stats": (i32, [vp, C.POINTER(CacheStats)]),
     "hps_gpu_cache_reset_stats": (i32, [vp]),
     "hps_gpu_cache_size": (i32, [vp, C.POINTER(u64)]),

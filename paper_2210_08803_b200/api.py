@@ -313,42 +313,57 @@ class HotCache:
 
 
 class CachedLookup:
-    """Orchestrator read-through for one table: the HPS GPU cache (L1) in
-    front of a GPU-resident backing table. lookup() = cache query -> misses read from the
-    table (default vector when absent) -> misses migrated into the cache (absent keys are
-    never cached) -> rows in input order. Three C-ABI calls, no host round trip."""
+    """The orchestrator's batch lookup for one table through
+    hps_gpu_readthrough_*: the HPS GPU cache (L1) in front of a GPU-resident backing table.
+    lookup() = distinct keys (first-occurrence order) -> cache query -> misses read from the
+    table (default vector when absent) -> distinct misses migrated into the cache (absent
+    keys never cached) -> rows in input order. One C-ABI call, no host round trip."""
 
-    def __init__(self, cache: HotCache, table: EmbeddingTableGroup, table_id: int = 0):
+    def __init__(self, cache: HotCache, table: EmbeddingTableGroup, table_id: int = 0,
+                 max_batch: Optional[int] = None):
         self.cache, self.table, self.table_id = cache, table, table_id
         self.lib, self.dim, self.device = cache.lib, cache.dim, cache.device
-        n = cache.max_batch
-        self.found = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
+        n = max_batch or cache.max_batch
+        self.max_batch = n
+        h = C.c_void_p()
+        L.check(self.lib.hps_gpu_readthrough_create(cache.h, table.h, table_id, n, C.byref(h)), "readthrough_create")
+        self.h = h
         self.out = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
-        self.miss_keys = torch.empty(n, dtype=torch.int64, device=self.device)
-        self.miss_vecs = torch.empty(n, self.dim, dtype=torch.float32, device=self.device)
-        self.miss_absent = torch.empty(n, dtype=torch.uint8, device=self.device)
-        self.admitted = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.source_counts = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self.n_unique = torch.zeros(1, dtype=torch.int64, device=self.device)
 
     def lookup(self, keys: torch.Tensor) -> torch.Tensor:
+        """Rows of keys in input order; self.source_counts = per-key {L1, L2, L3, Default}."""
+        _need_cuda(keys, "keys")
         n = keys.numel()
-        fv, fi, mi, cnt = self.cache.query_async(keys, found_vecs=self.found)
-        L.check(self.lib.hps_gpu_table_read_through(self.table.h, self.table_id, _ptr(keys), _ptr(fv), _ptr(fi),
-                                                    _ptr(mi), _ptr(cnt), n, _ptr(self.out), _ptr(self.miss_keys),
-                                                    _ptr(self.miss_vecs), _ptr(self.miss_absent)), "read_through")
-        L.check(self.lib.hps_gpu_cache_insert_count(self.cache.h, _ptr(self.miss_keys), _ptr(self.miss_vecs), None, n,
-                                                    C.c_void_p(cnt.data_ptr() + 8), _ptr(self.miss_absent),
-                                                    _ptr(self.admitted)), "cache_insert_count")
+        L.check(self.lib.hps_gpu_readthrough_lookup(self.h, _ptr(keys), n, _ptr(self.out), _ptr(self.source_counts),
+                                                    _ptr(self.n_unique)), "readthrough_lookup")
         return self.out[:n]
 
+    def sources(self) -> dict:
+        c = self.source_counts.tolist()
+        return {"L1": c[0], "L2": c[1], "L3": c[2], "Default": c[3]}
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.hps_gpu_readthrough_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
     def lookup_graphed(self, keys: torch.Tensor) -> torch.Tensor:
-        """lookup() with the three calls replayed as one CUDA graph per batch size (the keys
-        are copied into a device staging buffer first): small batches are launch-bound, and a
-        replay enqueues the ~20 kernels of a read-through as one launch. Same results and
+        """lookup() replayed as one CUDA graph per batch size (the keys are copied into a
+        device staging buffer first): small batches are launch-bound, and a replay enqueues
+        the ~15 nodes of a read-through as one launch. Same results and
         cache state as lookup(); the first call of a size runs eagerly and captures."""
         n = keys.numel()
         if not hasattr(self, "_graphs"):
             self._graphs = {}
-            self._stage = torch.empty(self.cache.max_batch, dtype=torch.int64, device=self.device)
+            self._stage = torch.empty(self.max_batch, dtype=torch.int64, device=self.device)
         self._stage[:n].copy_(keys, non_blocking=True)
         g = self._graphs.get(n)
         if g is not None:

@@ -31,6 +31,11 @@
 
 using namespace hpsg;
 
+namespace hpsg {
+int cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_t* d_n, float* found_vecs,
+                uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts);
+}
+
 struct hps_gpu_cache_s {
   hps_gpu_ctx ctx = nullptr;
   uint64_t capacity = 0, num_sets = 0, aging_period = 0, max_batch = 0;
@@ -71,9 +76,10 @@ int bits_for(uint64_t v) {
 __global__ void k_probe(const uint64_t* __restrict__ keys, uint64_t n, hps::FastMod64 fm, uint32_t ways,
                         const uint64_t* __restrict__ ckeys, const uint8_t* __restrict__ cfreq,
                         uint32_t* __restrict__ set_out, uint8_t* __restrict__ hit_out, uint64_t* state,
-                        uint64_t* counts) {
+                        uint64_t* counts, const uint64_t* d_n) {
   pdl_wait();
   pdl_launch_dependents();
+  if (d_n) n = *d_n;  // key count produced on the device (the orchestrator's distinct keys); n was the bound
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     state[kSnap] = state[kClock];
     state[kClock] += n;
@@ -902,8 +908,11 @@ struct QueryPhases {
   cudaStream_t st_;
 };
 
-int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float* found_vecs, uint32_t* found_idx,
-                        uint32_t* missing_idx, uint64_t* counts) {
+}  // extern "C"
+
+// n: the key count, or (d_n != nullptr) its bound with the count on the device.
+int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_t* d_n, float* found_vecs,
+                      uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts) {
   if (int s = check_cache(c)) return s;
   if (!found_idx || !missing_idx || !counts) return HPS_GPU_E_INVALID_ARGUMENT;
   if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
@@ -916,7 +925,7 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
   QueryPhases ph(st);
   ph.mark();
   launch_k(true, k_probe, grid_for(n, 256, kNumSMs * 16), 256, 0, st, keys, n, c->set_mod, c->ways, c->d_keys, c->d_freq,
-                                                          c->ws_set, c->ws_hit, c->d_state, c->ws_counts);
+                                                          c->ws_set, c->ws_hit, c->d_state, c->ws_counts, d_n);
   SplitOp op{c->ws_hit, found_idx, missing_idx, counts, c->ws_counts, c->d_state + kStats};
   HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
   HPSG_CHECK_LAUNCH("cache probe/split");
@@ -960,6 +969,13 @@ int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float
   HPSG_CHECK_LAUNCH("cache meta");
   ph.mark();
   return HPS_GPU_OK;
+}
+
+extern "C" {
+
+int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float* found_vecs, uint32_t* found_idx,
+                        uint32_t* missing_idx, uint64_t* counts) {
+  return cache_query(c, keys, n, nullptr, found_vecs, found_idx, missing_idx, counts);
 }
 
 static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n,
@@ -1048,6 +1064,7 @@ int cache_info(hps_gpu_cache c, hps_gpu_ctx* ctx, uint32_t* dim) {
   *dim = c->dim;
   return HPS_GPU_OK;
 }
+uint64_t cache_max_batch(hps_gpu_cache c) { return c ? c->max_batch : 0; }
 }  // namespace hpsg
 
 extern "C" {

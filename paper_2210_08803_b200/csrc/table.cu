@@ -500,6 +500,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a
   trace_end(ROWS ? kTrPool : -1);
 }
 
+// Source tier of a read-through key (SPEC.md:326 LookupResult.source_counts order).
+constexpr uint8_t kSrcCache = 0, kSrcTable = 1, kSrcDefault = 3;
+
 // Orchestrator read-through (one table): hits come from the cache's
 // compacted rows, misses from this table (or its default vector when absent); the misses
 // are listed in input order for migration into the cache (absent keys flagged: never cached).
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
                                                       const float* __restrict__ W, const float* __restrict__ def,
                                                       uint32_t dim, float* __restrict__ out, uint64_t* miss_keys,
                                                       float* miss_vecs, uint8_t* miss_absent,
-                                                      const uint16_t* __restrict__ Wh) {
+                                                      const uint16_t* __restrict__ Wh, uint8_t* src_out) {
   pdl_wait();
   pdl_launch_dependents();
   constexpr int G = 32 / LPR;
@@ -528,6 +531,7 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
     if (j < nf) {
       i = found_idx[j];
       src = reinterpret_cast<const float4*>(found_vecs + j * dim);
+      if (src_out && gl == 0) src_out[i] = kSrcCache;
     } else {
       const uint64_t m = j - nf;
       i = missing_idx[m];
@@ -539,6 +543,7 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
       if (gl == 0) {
         miss_keys[m] = k;
         miss_absent[m] = local == kRowEmpty ? 1 : 0;
+        if (src_out) src_out[i] = local == kRowEmpty ? kSrcDefault : kSrcTable;
       }
     }
     float4* dst = reinterpret_cast<float4*>(out + uint64_t(i) * dim);
@@ -1226,9 +1231,12 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   return HPS_GPU_OK;
 }
 
-int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* keys, const float* found_vecs,
-                               const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
-                               uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent) {
+}  // extern "C"
+
+int hpsg::table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* keys, const float* found_vecs,
+                             const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
+                             uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent,
+                             uint8_t* src_out) {
   if (int s = check_tbl(t)) return s;
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (n == 0) return HPS_GPU_OK;
@@ -1241,15 +1249,24 @@ int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* 
   const TableDev td = t->h_tables[table];
   const float* def = t->d_defaults + uint64_t(table) * t->dim;
   switch (lpr) {
-    case 32: launch_k(true, k_read_through<32>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 16: launch_k(true, k_read_through<16>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 8: launch_k(true, k_read_through<8>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 4: launch_k(true, k_read_through<4>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    case 2: launch_k(true, k_read_through<2>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
-    default: launch_k(true, k_read_through<1>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh); break;
+    case 32: launch_k(true, k_read_through<32>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh, src_out); break;
+    case 16: launch_k(true, k_read_through<16>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh, src_out); break;
+    case 8: launch_k(true, k_read_through<8>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh, src_out); break;
+    case 4: launch_k(true, k_read_through<4>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh, src_out); break;
+    case 2: launch_k(true, k_read_through<2>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh, src_out); break;
+    default: launch_k(true, k_read_through<1>, grid, 256, 0, st, keys, found_vecs, found_idx, missing_idx, counts, t->d_slots, td, t->d_w, def, t->dim, out, miss_keys, miss_vecs, miss_absent, t->d_wh, src_out); break;
   }
   HPSG_CHECK_LAUNCH("k_read_through");
   return HPS_GPU_OK;
+}
+
+extern "C" {
+
+int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* keys, const float* found_vecs,
+                               const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
+                               uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent) {
+  return table_read_through(t, table, keys, found_vecs, found_idx, missing_idx, counts, n, out, miss_keys, miss_vecs,
+                            miss_absent, nullptr);
 }
 
 int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,

@@ -167,44 +167,69 @@ def test_zipf_hit_rate_bound(ctx):
     assert s["hits"] / s["queries"] >= 0.9 * M, (s, M)
 
 
+def first_occurrence_unique(q):
+    """Distinct keys in order of first occurrence and the inverse map."""
+    _, first, inv_sorted = np.unique(q, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")
+    rank = np.empty_like(order)
+    rank[order] = np.arange(len(order))
+    return q[first[order]], rank[inv_sorted]
+
+
+def oracle_read_through(ocache, truth, default, q, dim):
+    """The orchestrator lookup restated on the oracle cache + a dict table: one probe per
+    distinct key (first-occurrence order), distinct present misses inserted once (version 0
+    = bulk load), rows expanded to input order, per-key source counts {L1, L2, L3, Default}."""
+    u, inv = first_occurrence_unique(q)
+    fi, fv, mi = ocache.query(u)
+    rows = np.empty((len(u), dim), np.float32)
+    src = np.empty(len(u), np.int64)
+    rows[fi] = fv
+    src[fi] = 0
+    miss = u[mi]
+    present = np.array([int(k) in truth for k in miss], dtype=bool)
+    mrows = np.stack([truth.get(int(k), default) for k in miss]) if len(mi) else np.zeros((0, dim), np.float32)
+    rows[mi] = mrows
+    src[mi] = np.where(present, 1, 3)
+    if present.any():
+        ocache.insert(miss[present], mrows[present], np.zeros(int(present.sum()), np.uint64))
+    return rows[inv], np.bincount(src[inv], minlength=4), len(u)
+
+
 @pytest.mark.parametrize("graphed", [False, True])
 def test_read_through_matches_oracle(ctx, graphed):
-    """Cache + backing table read-through: outputs in input order, hits/misses, migration
-    of misses (absent keys never cached), bit-exact with the oracle cache + a dict table.
-    graphed: lookup_graphed (one CUDA graph per batch size; sizes repeat so most rounds
-    are replays)."""
+    """Orchestrator lookup (cache + backing table): rows in input order, duplicate keys served
+    from one probe per distinct key (so cache stats count distinct keys), distinct misses
+    migrated once (absent keys never cached), source counts per input key — bit-exact with
+    the oracle cache + a dict table. Batches span the one-CTA dedup (<= 2,048 keys) and the
+    claim-table dedup. graphed: lookup_graphed (one CUDA graph per batch size)."""
     from paper_2210_08803_b200 import EmbeddingTableGroup
     from paper_2210_08803_b200.api import CachedLookup
     dim, n_keys, cap = 8, 5000, 512
     rs = np.random.default_rng(17)
     keys_all = W.mix64(np.arange(n_keys, dtype=np.uint64))
-    table = EmbeddingTableGroup(ctx, [n_keys], dim, [0], "sgd", 4096, 4096, 3)
+    table = EmbeddingTableGroup(ctx, [n_keys], dim, [0], "sgd", 8192, 8192, 3)
     table.insert(0, t64(keys_all))
     default = np.full(dim, 0.5, np.float32)
     table.set_default_vector(0, default)
     rows = table.export(0, 0, n_keys)[0].cpu().numpy()
     truth = {int(k): rows[i] for i, k in enumerate(keys_all)}
-    cache = HotCache(ctx, cap, dim, 8, 0, 4096)
+    cache = HotCache(ctx, cap, dim, 8, 0, 8192)
     rt = CachedLookup(cache, table)
     ocache = O.OracleCache(cap, dim, 8, 0)
     z = W.Zipf(n_keys + 200, 1.1)
-    for rnd in range(20):
-        m = int(rs.integers(1, 3000)) if not graphed else [1, 37, 2048][rnd % 3]
+    for rnd in range(24):
+        m = int(rs.integers(1, 7000)) if not graphed else [1, 37, 2048, 5000][rnd % 4]
         ranks = z.ranks(W.rng(rnd, np.arange(m, dtype=np.uint64)))
         q = W.mix64(ranks.astype(np.uint64))  # ranks >= n_keys are absent from the table
         got = (rt.lookup_graphed(t64(q)) if graphed else rt.lookup(t64(q))).cpu().numpy()
-        fi, fv, mi = ocache.query(q)
-        want = np.empty((len(q), dim), np.float32)
-        want[fi] = fv
-        miss = q[mi]
-        mrows = np.stack([truth.get(int(k), default) for k in miss]) if len(mi) else np.zeros((0, dim), np.float32)
-        want[mi] = mrows
-        present = np.array([int(k) in truth for k in miss], dtype=bool)
-        if present.any():
-            ocache.insert(miss[present], mrows[present], np.zeros(int(present.sum()), np.uint64))
+        want, want_src, n_u = oracle_read_through(ocache, truth, default, q, dim)
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+        assert rt.source_counts.tolist() == want_src.tolist(), rnd
+        assert int(rt.n_unique.item()) == n_u
         assert cache.stats() == ocache.stats(), rnd
     assert cache.size() == ocache.size()
+    assert_same_state(cache, ocache, cap)
 
 
 @pytest.mark.parametrize("f16", [False, True])
