@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--table-scale", type=float, default=1.0, help="debug only: shrink cardinalities")
+    ap.add_argument("--sustain-s", type=float, default=2.0,
+                    help="untimed steps run under the clock sampler right before the timed steps")
+    ap.add_argument("--full-batch", type=int, default=55296,
+                    help="N=1 cfg2: also time steps at BASELINE's literal global batch (0 = off)")
     ap.add_argument("--trace", type=int, default=0,
                     help="debug: after timing, replay N steps with the in-graph kernel timeline on (stderr)")
     return ap.parse_args()
@@ -86,6 +90,16 @@ def get_config(args):
     if args.table_scale != 1.0:
         cfg.cards = [max(1, int(c * args.table_scale)) for c in cfg.cards]
     return cfg
+
+
+def workload_config(cfg, world, args):
+    """The workload the line is quoted on — identical in the GPU arm and the reference arm."""
+    xchg = world > 1 or args.force_exchange
+    placement = args.placement if args.placement != "auto" else ("localized" if args.config == "cfg3" else "distributed")
+    return {"workload": cfg.name, "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * world,
+            "tables": len(cfg.cards), "rows": int(sum(cfg.cards)), "dim": cfg.dim, "hot": cfg.hot,
+            "combiner": cfg.combiner, "optimizer": cfg.optimizer, "keyspace": cfg.keyspace,
+            "parallelism": f"{placement}-slot x{world}" if xchg else "single"}
 
 
 def hbm_peak():
@@ -118,7 +132,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -223,8 +237,7 @@ def reference_arm(args, cfg, rank, world):
         "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * cfg.batch / val, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "tables": len(cfg.cards),
-                   "rows": int(sum(cfg.cards)), "dim": cfg.dim, "combiner": cfg.combiner, "optimizer": cfg.optimizer},
+        "config": workload_config(cfg, world, args),
         "cpu_baseline": {"value": val, "unit": "samples/s", "cores": threads, "kind": "port", "sample": sample,
                          "host": host_info()},
         "e2e": {"value": val, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -287,6 +300,7 @@ def main():
 
     torch.cuda.set_device(local)
     xchg = world > 1 or args.force_exchange
+    full_batch = 0
     if xchg:
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -302,7 +316,8 @@ def main():
     if xchg and placement == "hybrid":
         hot, tables = build_tables_hybrid(ctx, cfg, rank, world, hybrid_hot_set(cfg, int(args.hot_budget_gb * 1e9)))
     elif owned is None:
-        tables = build_tables(ctx, cfg, rank, world)
+        full_batch = args.full_batch if (world == 1 and not xchg and args.config == "cfg2") else 0
+        tables = build_tables(ctx, cfg, rank, world, batch_cap=full_batch)
     else:
         tables = build_tables_localized(ctx, cfg, owned, rank, world)
     gen = W.BatchGen(cfg)
@@ -333,12 +348,21 @@ def main():
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
+    # the clocks are sampled over a sustained run of the same step (>= args.sustain_s of
+    # untimed steps: the timed K steps alone last a few ms, shorter than nvidia-smi's
+    # sampling period) that runs straight into the timed steps
+    t_sus, n_sus = time.perf_counter(), 0
+    while time.perf_counter() - t_sus < args.sustain_s:
+        for _ in range(50):
+            one(args.warmup + n_sus)
+            n_sus += 1
+        torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.fill_(i & 0xff)  # evict L2 between timed iterations (not inside the step events)
         starts[i].record(stream)
-        step_fn.run(pool[i % len(pool)], douts[i % len(douts)], step=args.warmup + i + 1)
+        step_fn.run(pool[i % len(pool)], douts[i % len(douts)], step=args.warmup + n_sus + i + 1)
         ends[i].record(stream)
     torch.cuda.synchronize()
     clocks = sampler.stop()
@@ -367,6 +391,34 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * cfg.batch / (ms_max / 1000.0)
+
+    # BASELINE's literal global batch (55,296 samples) as ONE GPU's step: the same tables,
+    # a TrainStep at that batch, K timed steps (L2 flushed between them)
+    full = None
+    if full_batch > cfg.batch:
+        cfg_f = W.Config(**{**cfg.__dict__, "batch": full_batch})
+        step_f = TrainStep(ctx, tables, cfg_f, rank, world, use_graph=not args.no_graph)
+        gen_f = W.BatchGen(cfg_f)
+        pool_f = [step_f.stage_batch(*gen_f.batch(5000 + s)[:2]) for s in range(2)]
+        dout_f = torch.from_numpy((rs.standard_normal((full_batch * cfg.n_slots, cfg.dim)) * 0.01)
+                                  .astype(np.float32)).cuda()
+        for i in range(max(3, args.warmup)):
+            step_f.run(pool_f[i % 2], dout_f, step=i + 1)
+        torch.cuda.synchronize()
+        ev_f = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)
+            ev_f[i][0].record(stream)
+            step_f.run(pool_f[i % 2], dout_f, step=100 + i)
+            ev_f[i][1].record(stream)
+        torch.cuda.synchronize()
+        ms_f = float(np.mean([a.elapsed_time(b) for a, b in ev_f]))
+        Nf, Uf = step_f.last_counts()
+        ff, fb = algorithmic_bytes(Nf, Uf, full_batch * cfg.n_slots, cfg.dim, 0, False)
+        full = {"batch_per_gpu": full_batch, "ms_per_step": ms_f, "value": full_batch / (ms_f / 1000.0),
+                "unit": "samples/s", "unique_keys": Uf, "key_occurrences": Nf,
+                "step_algorithmic_bytes": ff + fb, "step_frac": (ff + fb) / (ms_f / 1000.0) / 1e9 / hbm_peak()[0]}
+        del step_f, pool_f, dout_f
 
     # algorithmic bytes of the last step's batch on this rank
     fwd_b, bwd_b = algorithmic_bytes(N, U, n_bags, cfg.dim, {"sgd": 0, "adagrad": 1, "adam": 2}[cfg.optimizer],
@@ -444,12 +496,9 @@ def main():
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * world,
-                       "tables": len(cfg.cards), "rows": int(sum(cfg.cards)), "dim": cfg.dim,
-                       "hot": cfg.hot, "combiner": cfg.combiner, "optimizer": cfg.optimizer,
-                       "parallelism": f"{step_fn.placement}-slot x{world}" if xchg else "single",
-                       "l2": "flushed between timed steps (256 MB write)", "graph": step_fn.graph_mode,
-                       "keyspace": cfg.keyspace, "insert_on_miss": step_fn.insert_missing},
+            "config": workload_config(cfg, world, args),
+            "run": {"l2": "flushed between timed steps (256 MB write)", "graph": step_fn.graph_mode,
+                    "insert_on_miss": step_fn.insert_missing},
             "roofline": {"bound": "hbm", "kernel": "k_lookup_1hot (fused hash+probe+gather+pool)" if cfg.hot == 1
                          else "k_lookup_multi (fused hash+probe+gather+pool)",
                          "achieved": fwd_gbs, "peak": peak, "unit": "GB/s", "frac": fwd_gbs / peak,
@@ -464,6 +513,8 @@ def main():
             "cpu_baseline": cpu,
             "unique_keys": U, "key_occurrences": N, "setup_s": setup_s,
         }
+        if full is not None:
+            line["full_batch_n1"] = full
         if xchg:
             xb = step_fn.exchange.exchanged_bytes(cfg.dim)
             line["nvlink"] = {"bytes_per_step_rank0": xb, "achieved_gbs": xb / (ms_max / 1000.0) / 1e9,

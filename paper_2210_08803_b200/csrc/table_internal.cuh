@@ -49,12 +49,12 @@ inline uint64_t bwd_max_nodes(uint64_t max_keys) { return bwd_max_chunks(max_key
 struct hps_gpu_table_s;
 namespace hpsg {
 int launch_dedup(hps_gpu_table_s* t, cudaStream_t st);  // backward.cu: K4a-K4d (on t->side)
-int check_dedup_residency();
+int check_dedup_residency();  // backward.cu: one persistent k_dedup CTA must fit an SM of the current device
 // table.cu: hps_gpu_table_read_through + the source tier of every key (src_out[i]: 0 cache,
 // 1 table, 3 default vector; may be NULL)
 int table_read_through(hps_gpu_table_s* t, uint32_t table, const uint64_t* keys, const float* found_vecs,
                        const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts, uint64_t n,
-                       float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent, uint8_t* src_out);  // backward.cu: one persistent k_dedup CTA must fit an SM of the current device
+                       float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent, uint8_t* src_out);
 cudaError_t trace_attach_table(TraceRec* p);  // table.cu's copy of the trace pointer
 }
 

@@ -39,9 +39,12 @@ def table_max_keys(cfg: W.Config, world: int) -> int:
 
 
 def build_tables(ctx: Context, cfg: W.Config, rank: int = 0, world: int = 1,
-                 chunk: int = 1 << 24) -> EmbeddingTableGroup:
+                 chunk: int = 1 << 24, batch_cap: int = 0) -> EmbeddingTableGroup:
     """Create the (shard of the) table group and bulk-insert every key of every table,
-    in index order, so that on one GPU row i of table t holds table_key(t, i)."""
+    in index order, so that on one GPU row i of table t holds table_key(t, i). batch_cap:
+    size the per-batch workspaces for up to that many samples (default cfg.batch)."""
+    if batch_cap > cfg.batch:
+        cfg = W.Config(**{**cfg.__dict__, "batch": batch_cap})
     n_bags = cfg.batch * cfg.n_slots
     max_keys = table_max_keys(cfg, world)
     n_bags_cap = n_bags if world == 1 else max(n_bags * world, max_keys)
