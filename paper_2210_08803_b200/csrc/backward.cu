@@ -847,6 +847,150 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
   }
 }
 
+// ---- short segments, register row stream -------------------------------------------------
+// A warp takes 32 segments (lane j = segment j) and flattens their rows into ONE stream:
+// segment j contributes [weight row, state rows, gradient rows in canonical order]. The
+// stream is cut into sub-lists of <= kPipeList entries (whole segments), each built in a
+// small shared-memory list (the gradient rows' bags are read from the segment CSR and
+// sorted into canonical order on the way in). The warp then walks its sub-list U rows at a
+// time: U 128-bit row loads in flight (lane l owns float4s l, l+32, ...: fully coalesced),
+// then the ordered sums, the fused optimizer at each segment's last row, 128-bit stores.
+// Latency is hidden by occupancy (small register and shared-memory footprint), not by a
+// deep per-warp pipeline: a fully unrolled ring overflows the instruction cache.
+constexpr uint32_t kPipeList = 128;  // entries per sub-list (>= 3 + kChunk: one whole segment)
+static_assert(kPipeList >= 3 + kChunk, "a sub-list holds at least one whole short segment");
+
+__device__ __forceinline__ float4 ld_row4(const float* p, uint32_t v) {
+  return __ldg(reinterpret_cast<const float4*>(p) + v);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// U rows per chunk, two chunk buffers per warp: chunk c+1's rows land (per-lane cp.async,
+// 16 B each, 128-bit coalesced) while chunk c is summed from shared memory.
+template <int OPT, int VPL, int U>
+__device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint64_t n_warps, uint2* list,
+                                           float4* buf) {
+  constexpr uint32_t NS = state_rows<OPT>();
+  constexpr uint32_t HDR = 1u + NS;  // weight (gradient-only: the row id, nothing loaded) + state rows
+  const uint32_t lane = lane_id();
+  const uint32_t D = a.dim, nvec = D / 4;
+  const bool mean = a.bag_len != nullptr;
+  const uint64_t S = *a.short_alloc >> 32;
+  for (uint64_t u0 = warp * 32; u0 < S; u0 += n_warps * 32) {
+    uint4 rec = make_uint4(0, 0, 0, 0);
+    if (u0 + lane < S) rec = a.short_rec[u0 + lane];
+    const uint32_t row = rec.x, first = rec.y, len = rec.z, slot = rec.w;
+    if (len) a.bt[slot] = make_uint2(kBtEmpty, 0xffffffffu);  // placement (previous kernels) is done with it
+    uint32_t bag0 = len ? a.short_bag[first] : 0u;
+    const uint32_t c = len ? HDR + len : 0u;
+    const uint32_t incl = warp_incl_scan(c), excl = incl - c;
+    uint32_t done = 0;  // lanes (segments) already streamed
+    while (done < 32) {
+      const uint32_t base = __shfl_sync(0xffffffffu, excl, done);
+      const bool in = lane >= done && incl - base <= kPipeList;
+      const uint32_t m = __ballot_sync(0xffffffffu, in);
+      const uint32_t j1 = 31 - __clz(m);
+      const uint32_t T = __shfl_sync(0xffffffffu, incl, j1) - base;
+      // build the sub-list: header rows + single gradients by their own lane ...
+      if (in && len) {
+        const uint32_t o = excl - base;
+        for (uint32_t q = 0; q < HDR; ++q) list[o + q] = make_uint2(row, q);
+        if (len == 1) list[o + HDR] = make_uint2(bag0, 3u | 4u | ((mean ? a.bag_len[bag0] : 1u) << 3));
+      }
+      // ... longer segments' bags sorted into canonical order by the whole warp
+      uint32_t multi = __ballot_sync(0xffffffffu, in && len >= 2);
+      while (multi) {
+        const int j = __ffs(multi) - 1;
+        multi &= multi - 1;
+        const uint32_t jl = __shfl_sync(0xffffffffu, len, j);
+        const uint32_t jf = __shfl_sync(0xffffffffu, first, j);
+        const uint32_t jo = __shfl_sync(0xffffffffu, excl, j) - base + HDR;
+        const uint32_t b = lane < jl ? a.short_bag[jf + lane] : 0xffffffffu;
+        uint32_t rank = 0;
+        for (uint32_t q = 0; q < jl; ++q) {
+          const uint32_t x = __shfl_sync(0xffffffffu, b, q);
+          rank += (x < b || (x == b && q < lane)) ? 1u : 0u;
+        }
+        if (lane < jl)
+          list[jo + rank] = make_uint2(b, 3u | (rank + 1 == jl ? 4u : 0u) | ((mean ? a.bag_len[b] : 1u) << 3));
+      }
+      __syncwarp();
+      auto issue_chunk = [&](uint32_t ch) {
+        float4* dst = buf + (ch & 1u) * U * nvec;
+        const uint32_t t0 = ch * U, n = min(uint32_t(U), T - t0);
+        for (uint32_t k = 0; k < n; ++k) {
+          const uint2 e = list[t0 + k];
+          const uint32_t kind = e.y & 3u;
+          if (OPT == kOptGrad && kind == 0) continue;  // gradient-only: the row is written, never read
+          const float4* src = reinterpret_cast<const float4*>(
+              (kind == 0 ? a.W : kind == 1 ? a.S0 : kind == 2 ? a.S1 : a.dout) + uint64_t(e.x) * D);
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            const uint32_t vv = lane + 32u * v;
+            if (vv < nvec) cp_async16(dst + k * nvec + vv, src + vv);
+          }
+        }
+        cp_async_commit();
+      };
+      const uint32_t nch = (T + U - 1) / U;
+      issue_chunk(0);
+      RowState<OPT, VPL> rs;
+      float4 g[VPL];
+      bool g0 = true;  // the next gradient row starts its segment's sum
+      uint32_t cur_row = 0;
+      for (uint32_t ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) {
+          issue_chunk(ch + 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncwarp();
+        const float4* xb = buf + (ch & 1u) * U * nvec;
+        const uint32_t t0 = ch * U, n = min(uint32_t(U), T - t0);
+        for (uint32_t k = 0; k < n; ++k) {
+          const uint2 e = list[t0 + k];
+          const uint32_t kind = e.y & 3u;
+          float4 x[VPL];
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) x[v] = xb[k * nvec + min(lane + 32u * v, nvec - 1)];
+          if (kind == 0) {
+            cur_row = e.x;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) rs.w[v] = x[v];
+          } else if (kind == 1) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) rs.s[state_rows<OPT>() >= 1 ? v : 0] = x[v];
+          } else if (kind == 2) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) rs.q[state_rows<OPT>() >= 2 ? v : 0] = x[v];
+          } else {
+            const float f = static_cast<float>(e.y >> 3);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              const float4 gx = mean ? f4_div(x[v], f) : x[v];
+              g[v] = g0 ? gx : f4_add(g[v], gx);
+            }
+            g0 = false;
+            if (e.y & 4u) {
+              update_store<OPT, VPL>(a, cur_row, lane, 32, rs, g);
+              g0 = true;
+            }
+          }
+        }
+        __syncwarp();  // this buffer is refilled two chunks from now
+      }
+      done = j1 + 1;
+    }
+  }
+}
+
 // ---- long segments: the tree above level 1 ----------------------------------------------
 // Level-1 chunk c of segment j is complete in partial[base_j + c]. The warp counts itself
 // into its parent node; the last of the parent's (<= 32) children sums them in order into
@@ -1010,6 +1154,23 @@ __global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : (OPT == 
   trace_end(kTrReduce);
 }
 
+// Short segments reduced + updated through the register-pipelined row stream (dim 128..256).
+constexpr int kPipeBlock = 256;
+template <int OPT, int VPL, int U>
+__global__ void __launch_bounds__(kPipeBlock, 3) k_reduce_pipe(BwdArgs a) {
+  extern __shared__ __align__(16) float4 s_rows[];  // per warp: 2 chunk buffers of U rows
+  __shared__ uint2 s_list[kPipeBlock / 32][kPipeList];
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t wpb = blockDim.x >> 5;
+  const uint64_t warp = uint64_t(blockIdx.x) * wpb + (threadIdx.x >> 5);
+  const uint64_t n_warps = uint64_t(gridDim.x) * wpb;
+  const uint32_t w = threadIdx.x >> 5;
+  trace_begin(kTrReduce);
+  short_pipe<OPT, VPL, U>(a, warp, n_warps, s_list[w], s_rows + size_t(w) * 2 * U * (a.dim / 4));
+  trace_end(kTrReduce);
+}
+
 // Long segments: chunk partials + the last-arriver tree + optimizer, at full occupancy
 // (this part is a latency-bound gather stream).
 template <int OPT, int LPR, int VPL>
@@ -1065,6 +1226,26 @@ int launch_backward_v(const BwdArgs& a, cudaStream_t st, cudaStream_t side, size
   }));
   HPSG_CUDA(launch_k(false, k_long<OPT, LPR, VPL>, long_grid, 256, 0, side, a));  // first after a join
   HPSG_CUDA(launch_k(false, kern, grid, block, smem, st, a));
+  return HPS_GPU_OK;
+}
+
+template <int OPT, int VPL, int U>
+int launch_backward_pipe(const BwdArgs& a, cudaStream_t st, cudaStream_t side, int long_grid, uint64_t nk) {
+  auto kern = k_reduce_pipe<OPT, VPL, U>;
+  static std::atomic<uint64_t> attr{0};
+  const size_t smem = size_t(kPipeBlock / 32) * 2 * U * a.dim * sizeof(float);
+  HPSG_CUDA(once_per_device(attr, [&]() -> cudaError_t {
+    if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024)) return e;
+    if (cudaError_t e = prefer_max_smem(kern)) return e;
+    return prefer_max_smem(k_long<OPT, 32, VPL>);
+  }));
+  int per_sm = 0;
+  HPSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kPipeBlock, smem));
+  if (const char* e = std::getenv("HPS_GPU_PIPE_CTAS")) per_sm = std::max(1, std::atoi(e));  // A/B knob
+  const int grid = static_cast<int>(std::max<uint64_t>(
+      1, std::min<uint64_t>((nk + kPipeBlock - 1) / kPipeBlock, uint64_t(kNumSMs) * std::max(1, per_sm))));
+  HPSG_CUDA(launch_k(false, k_long<OPT, 32, VPL>, long_grid, 256, 0, side, a));  // first after a join
+  HPSG_CUDA(launch_k(false, kern, grid, kPipeBlock, smem, st, a));
   return HPS_GPU_OK;
 }
 
@@ -1277,6 +1458,32 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   }
   const int long_grid = grid_for((nk / kChunk + 2) * 32, 256, kNumSMs * 16);
   int s = HPS_GPU_OK;
+  int red_mode = 2;  // 0 register path, 1 bulk-copy waves, 2 register-pipelined row stream
+  if (const char* e = std::getenv("HPS_GPU_RED_MODE")) red_mode = std::atoi(e);  // A/B knob
+  if (tma && red_mode == 2) {
+    const bool two = nvec > 32;
+    auto pipe = [&](auto opt_tag) -> int {
+      constexpr int O = decltype(opt_tag)::value;
+      static const int uu = std::getenv("HPS_GPU_PIPE_U") ? std::atoi(std::getenv("HPS_GPU_PIPE_U")) : 4;  // A/B knob
+      if (two) return uu == 16 ? launch_backward_pipe<O, 2, 8>(a, st, t->side, long_grid, nk)
+                                : launch_backward_pipe<O, 2, 4>(a, st, t->side, long_grid, nk);
+      if (uu == 16) return launch_backward_pipe<O, 1, 16>(a, st, t->side, long_grid, nk);
+      if (uu == 4) return launch_backward_pipe<O, 1, 4>(a, st, t->side, long_grid, nk);
+      return launch_backward_pipe<O, 1, 8>(a, st, t->side, long_grid, nk);
+    };
+    if (grad_only) s = pipe(std::integral_constant<int, kOptGrad>{});
+    else if (t->optimizer == HPS_OPT_SGD) s = pipe(std::integral_constant<int, HPS_OPT_SGD>{});
+    else if (t->optimizer == HPS_OPT_ADAGRAD) s = pipe(std::integral_constant<int, HPS_OPT_ADAGRAD>{});
+    else s = pipe(std::integral_constant<int, HPS_OPT_ADAM>{});
+    if (s) return s;
+    HPSG_CHECK_LAUNCH("backward");
+    HPSG_CUDA(cudaEventRecord(t->ev_join2, t->side));
+    HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join2, 0));
+    t->have_train = false;
+    t->counts_dirty = false;
+    t->have_unique = true;
+    return HPS_GPU_OK;
+  }
   if (grad_only) s = launch_backward<kOptGrad>(a, st, t->side, tma, smem, grid, long_grid, nvec);
   else if (t->optimizer == HPS_OPT_SGD) s = launch_backward<HPS_OPT_SGD>(a, st, t->side, tma, smem, grid, long_grid, nvec);
   else if (t->optimizer == HPS_OPT_ADAGRAD)
