@@ -158,9 +158,15 @@ int hps_gpu_table_row_keys(hps_gpu_table tbl, uint32_t table, uint64_t row_begin
 enum {
   HPS_LOOKUP_KEYS_HOST = 1u << 0,  /* keys/offsets are pinned HOST memory: staged H2D inside the call */
   HPS_LOOKUP_TRAIN = 1u << 1,      /* remember per-key rows/bags for the following backward_update */
-  HPS_LOOKUP_INSERT = 1u << 2      /* dynamic table: insert absent keys first (single-table groups,
+  HPS_LOOKUP_INSERT = 1u << 2,     /* dynamic table: insert absent keys first (single-table groups,
                                       host-known key count); rows materialise on first touch */
+  HPS_LOOKUP_PREFETCHED = 1u << 3  /* training lookup of the batch hps_gpu_table_prefetch recorded in
+                                      slot HPS_LOOKUP_SLOT_OF(flags): pooling only (implies TRAIN;
+                                      keys are not read; offsets must be the prefetch's, or are
+                                      taken from its host staging) */
 };
+#define HPS_LOOKUP_SLOT(k) ((uint32_t)(k) << 16)            /* batch slot of a PREFETCHED lookup */
+#define HPS_LOOKUP_SLOT_OF(flags) (((uint32_t)(flags) >> 16) & 0xffu)
 
 /* K1+K2+K3 fused: out[bag*dim + j] = combiner over the bag's rows, fp32, keys in bag
  * order, from +0.0f; mean divides by the bag length (IEEE); an empty bag gives
@@ -174,6 +180,25 @@ int hps_gpu_lookup_pooled(hps_gpu_table tbl, const uint64_t* keys, const uint32_
  * blocked rule of DESIGN.md §4.3; the optimizer then updates each unique row in place.
  * Absent keys (default-vector occurrences) receive no update. */
 int hps_gpu_backward_update(hps_gpu_table tbl, const float* d_out, const hps_opt_params* opt_host);
+
+/* Batch pipelining (DESIGN.md §3 "Prefetch"). A table keeps `depth` batch slots (default 1):
+ * a slot holds one training record (probe), its dedup (segments) and the backward's scratch.
+ * hps_gpu_table_set_pipeline allocates the slots (setup call, not hot; depth 1..4).
+ * hps_gpu_table_prefetch records batch i+1 into `slot` — [insert-on-miss] + probe + dedup —
+ * on the slot's own stream: ordered after everything enqueued on the table's stream before
+ * the call, and concurrent with what is enqueued after it (the pooling and backward of batch
+ * i in another slot). The dedup reads no weights, so only the pooling and the update remain
+ * on the step's critical path. hps_gpu_lookup_pooled(... HPS_LOOKUP_PREFETCHED |
+ * HPS_LOOKUP_SLOT(slot) ...) then pools from that record and backward_update consumes it.
+ * Results are bit-identical to the unpipelined lookup/backward sequence (HPS_LOOKUP_INSERT:
+ * rows are created in prefetch order, which must then be the batch order). Refused
+ * (InvalidArgument): a slot >= depth, or the slot of a training lookup still awaiting its
+ * backward. hps_gpu_table_join_prefetch makes the table's stream wait for every outstanding
+ * prefetch; a stream capture that contains a prefetch must call it before the capture ends. */
+int hps_gpu_table_set_pipeline(hps_gpu_table tbl, uint32_t depth);
+int hps_gpu_table_prefetch(hps_gpu_table tbl, uint32_t slot, const uint64_t* keys, const uint32_t* offsets,
+                           uint32_t n_samples, int combiner, uint32_t flags);
+int hps_gpu_table_join_prefetch(hps_gpu_table tbl);
 
 /* After backward_update: number of unique rows updated (device u64 at *count_out),
  * and optionally their row ids in ascending row order (unique_rows_out: exactly

@@ -30,7 +30,11 @@ E_NO_DEVICE = 258
 
 OPT_SGD, OPT_ADAGRAD, OPT_ADAM = 0, 1, 2
 COMBINER_SUM, COMBINER_MEAN = 0, 1
-LOOKUP_KEYS_HOST, LOOKUP_TRAIN, LOOKUP_INSERT = 1, 2, 4
+LOOKUP_KEYS_HOST, LOOKUP_TRAIN, LOOKUP_INSERT, LOOKUP_PREFETCHED = 1, 2, 4, 8
+
+
+def LOOKUP_SLOT(k: int) -> int:
+    return (k & 0xFF) << 16
 PLAN_LOCALIZED, PLAN_DISTRIBUTED, PLAN_HYBRID = 0, 1, 2
 
 
@@ -125,6 +129,9 @@ SIGNATURES = {
     "hps_gpu_table_row_keys": (i32, [vp, u32, u64, u64, vp]),
     "hps_gpu_lookup_pooled": (i32, [vp, vp, vp, u32, i32, vp, u32]),
     "hps_gpu_backward_update": (i32, [vp, vp, C.POINTER(OptParams)]),
+    "hps_gpu_table_set_pipeline": (i32, [vp, u32]),
+    "hps_gpu_table_prefetch": (i32, [vp, u32, vp, vp, u32, i32, u32]),
+    "hps_gpu_table_join_prefetch": (i32, [vp]),
     "hps_gpu_table_last_unique": (i32, [vp, vp, vp]),
     "hps_gpu_debug_trace": (i32, [i32, vp]),
     "hps_gpu_debug_batch_table_used": (i32, [vp, vp]),

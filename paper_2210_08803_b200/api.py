@@ -186,6 +186,42 @@ class EmbeddingTableGroup:
                                                _ptr(out), flags), "lookup_pooled")
         return out
 
+    # -- batch pipelining (hps_gpu_table_set_pipeline / _prefetch / _join_prefetch) --------------
+    def set_pipeline(self, depth: int) -> None:
+        L.check(self.lib.hps_gpu_table_set_pipeline(self.h, depth), "set_pipeline")
+
+    def prefetch(self, slot: int, keys: torch.Tensor, n_samples: int, offsets: Optional[torch.Tensor] = None,
+                 combiner: str = "sum", keys_on_host: bool = False, insert_missing: bool = False) -> None:
+        """Record + dedup a future training batch into `slot` on the slot's stream (concurrent
+        with whatever is enqueued after this call); lookup_prefetched(slot) consumes it."""
+        flags = (L.LOOKUP_KEYS_HOST if keys_on_host else 0) | (L.LOOKUP_INSERT if insert_missing else 0)
+        if not keys_on_host:
+            _need_cuda(keys, "keys")
+            if offsets is not None:
+                _need_cuda(offsets, "offsets")
+        L.check(self.lib.hps_gpu_table_prefetch(self.h, slot, _ptr(keys), _ptr(offsets), n_samples, _COMB[combiner],
+                                                flags), "prefetch")
+
+    def lookup_prefetched(self, slot: int, n_samples: int, offsets: Optional[torch.Tensor] = None,
+                          combiner: str = "sum", out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The training lookup of the batch prefetched into `slot` (pooling only)."""
+        n_bags = n_samples * self.n_slots
+        if out is None:
+            out = torch.empty(n_bags, self.dim, dtype=torch.float32, device=self.device)
+        flags = L.LOOKUP_TRAIN | L.LOOKUP_PREFETCHED | L.LOOKUP_SLOT(slot)
+        L.check(self.lib.hps_gpu_lookup_pooled(self.h, None, _ptr(offsets), n_samples, _COMB[combiner], _ptr(out),
+                                               flags), "lookup_pooled(prefetched)")
+        return out
+
+    def join_prefetch(self) -> None:
+        L.check(self.lib.hps_gpu_table_join_prefetch(self.h), "join_prefetch")
+
+    def batch_table_used(self) -> int:
+        """Invariant probe (tests): batch-table entries in use over every slot (0 at rest)."""
+        v = C.c_uint64(0)
+        L.check(self.lib.hps_gpu_debug_batch_table_used(self.h, C.byref(v)), "debug_batch_table_used")
+        return int(v.value)
+
     def backward_update(self, d_out: torch.Tensor, lr: float, eps: float = 1e-8, beta1: float = 0.9,
                         beta2: float = 0.999, step: int = 1, params: Optional[L.OptParams] = None) -> None:
         _need_cuda(d_out, "d_out")

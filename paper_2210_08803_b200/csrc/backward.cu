@@ -1423,7 +1423,7 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   HPSG_CUDA(cudaEventRecord(t->ev_bwd, st));
   HPSG_CUDA(cudaStreamWaitEvent(t->side, t->ev_bwd, 0));
   if (t->dedup_pending) {
-    HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join, 0));
+    HPSG_CUDA(wait_recorded(st, t->ev_join, t->pre_capture));
     t->dedup_pending = false;
   }
   BwdArgs a = base_args(t);
@@ -1613,10 +1613,13 @@ int hps_gpu_debug_batch_table_used(hps_gpu_table t, uint64_t* used_host) {
   unsigned long long* d = nullptr;
   HPSG_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
   HPSG_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), t->ctx->stream));
-  k_bt_used<<<grid_for(t->bt_mask + 1, 256, kNumSMs * 8), 256, 0, t->ctx->stream>>>(t->ws_bt, t->bt_mask + 1, d);
-  HPSG_CHECK_LAUNCH("k_bt_used");
+  for (uint32_t k = 0; k < t->parked.size(); ++k) {  // every batch slot's table
+    const BatchSlot& b = k == t->cur ? static_cast<const BatchSlot&>(*t) : t->parked[k];
+    HPSG_CUDA(cudaStreamSynchronize(b.side));
+    k_bt_used<<<grid_for(t->bt_mask + 1, 256, kNumSMs * 8), 256, 0, t->ctx->stream>>>(b.ws_bt, t->bt_mask + 1, d);
+    HPSG_CHECK_LAUNCH("k_bt_used");
+  }
   HPSG_CUDA(cudaStreamSynchronize(t->ctx->stream));
-  HPSG_CUDA(cudaStreamSynchronize(t->side));
   unsigned long long v = 0;
   HPSG_CUDA(cudaMemcpy(&v, d, sizeof(v), cudaMemcpyDeviceToHost));
   cudaFree(d);

@@ -738,13 +738,17 @@ __global__ void __launch_bounds__(256) k_hybrid_pool(const uint32_t* __restrict_
   }
 }
 
+}  // namespace
+int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
+                   uint64_t* rows_out, cudaStream_t st);
+namespace {
+
 // A training record is about to overwrite ws_rows_a: counters of a previous record that no
 // backward consumed go back to zero first (they are still described by ws_rows_a, once
 // that record's dedup on the side stream is done).
-int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk) {
-  cudaStream_t st = t->ctx->stream;
+int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk, cudaStream_t st) {
   if (t->dedup_pending) {  // the whole previous dedup, long-segment part included
-    HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_done, 0));
+    HPSG_CUDA(wait_recorded(st, t->ev_done, t->pre_capture));
     t->dedup_pending = false;
   }
   if (t->counts_dirty) {
@@ -761,35 +765,153 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk) {
   a.status = t->ctx->d_status;
   t->counts_dirty = true;
   t->have_unique = false;
+  t->prefetched = false;
+  t->pre_keys_host = false;
   return HPS_GPU_OK;
 }
 
-// Training record: probe + record every occurrence (main stream). fork_dedup then puts the
-// backward's dedup on the table's side stream (it needs only the record), after the
-// pooling was launched on the main stream: the two run concurrently; backward_update joins.
-int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk) {
-  cudaStream_t st = t->ctx->stream;
+// Training record: probe + record every occurrence (on `st`). fork_dedup then puts the
+// backward's dedup on the slot's side stream (it needs only the record), after the pooling
+// was launched on the main stream: the two run concurrently; backward_update joins.
+int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk, cudaStream_t st) {
   if (multi) k_probe<true><<<grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * 16), 256, 0, st>>>(a);
   else k_probe<false><<<grid_for(a.n_bags, 256, kNumSMs * 16), 256, 0, st>>>(a);
   HPSG_CHECK_LAUNCH("probe");
   t->last_multi = multi;
   t->last_combiner = mean ? HPS_COMBINER_MEAN : HPS_COMBINER_SUM;
   t->last_n_keys_host = nk;
+  t->pre_n_bags = a.n_bags;
+  t->pre_capture = capture_id(st);
   // the fork point: right after the record (the pooling launched next does not gate the dedup)
-  if (!t->no_fork) HPSG_CUDA(cudaEventRecord(t->ev_fork, st));
+  if (!t->no_fork && st != t->side) HPSG_CUDA(cudaEventRecord(t->ev_fork, st));
+  return HPS_GPU_OK;
+}
+
+// The dedup of the current slot on its side stream. A table's dedups run one at a time
+// (each is a persistent kernel whose grid barriers need all its CTAs resident).
+int dedup_on_side(hps_gpu_table t) {
+  if (t->last_dedup_valid && t->ev_last_dedup != t->ev_done)
+    HPSG_CUDA(wait_recorded(t->side, t->ev_last_dedup, t->last_dedup_capture));
+  if (int s = launch_dedup(t, t->side)) return s;  // records ev_join after the short placement
+  HPSG_CUDA(cudaEventRecord(t->ev_done, t->side));
+  t->ev_last_dedup = t->ev_done;
+  t->last_dedup_valid = true;
+  t->last_dedup_capture = capture_id(t->side);
+  t->dedup_pending = true;
   return HPS_GPU_OK;
 }
 
 int fork_dedup(hps_gpu_table t) {
-  cudaStream_t st = t->ctx->stream;
   if (t->no_fork) {  // A/B measurement: dedup deferred to backward_update, all on the main stream
     t->dedup_deferred = true;
     return HPS_GPU_OK;
   }
   HPSG_CUDA(cudaStreamWaitEvent(t->side, t->ev_fork, 0));
-  if (int s = launch_dedup(t, t->side)) return s;  // records ev_join after the short placement
-  HPSG_CUDA(cudaEventRecord(t->ev_done, t->side));
-  t->dedup_pending = true;
+  return dedup_on_side(t);
+}
+
+int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows);
+
+// Host-pointer keys/offsets staged H2D into the current slot (HPS_LOOKUP_KEYS_HOST); sets
+// *n_keys_host exactly when it is known on the host.
+int stage_keys(hps_gpu_table t, const uint64_t*& keys, const uint32_t*& offsets, uint64_t n_bags, uint32_t flags,
+               cudaStream_t st, uint64_t* n_keys_host) {
+  const bool multi = offsets != nullptr;
+  if (flags & HPS_LOOKUP_KEYS_HOST) {
+    // Host buffers: stage H2D on the stream (pinned memory -> async copy).
+    *n_keys_host = multi ? offsets[n_bags] : n_bags;
+    if (*n_keys_host > t->max_keys) return HPS_GPU_E_INVALID_ARGUMENT;
+    HPSG_CUDA(cudaMemcpyAsync(t->ws_keys_stage, keys, *n_keys_host * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+    if (multi)
+      HPSG_CUDA(cudaMemcpyAsync(t->ws_offsets_stage, offsets, (n_bags + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+    keys = t->ws_keys_stage;
+    if (multi) offsets = t->ws_offsets_stage;
+  } else if (!multi && n_bags > t->max_keys) {
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (flags & HPS_LOOKUP_INSERT) {
+    // Dynamic table (keys materialise on first touch): insert the batch's keys first, in
+    // batch order, so new rows get deterministic ids; then the lookup finds all of them.
+    if (t->n_tables != 1 || (multi && !(flags & HPS_LOOKUP_KEYS_HOST))) {
+      set_last_error("HPS_LOOKUP_INSERT needs a single-table group and a host-known key count");
+      return HPS_GPU_E_INVALID_ARGUMENT;
+    }
+    if (int s = hpsg_insert_on(t, 0, keys, *n_keys_host, nullptr, nullptr, st)) return s;
+  }
+  return HPS_GPU_OK;
+}
+
+void fill_lookup_args(hps_gpu_table t, LookupArgs& a, const uint64_t* keys, const uint32_t* offsets, uint64_t n_bags,
+                      int combiner, float* out) {
+  a.keys = keys;
+  a.offsets = offsets;
+  a.n_bags = static_cast<uint32_t>(n_bags);
+  a.n_slots = t->n_slots;
+  a.slot_table = t->d_slot_table;
+  a.tables = t->d_tables;
+  a.slots = t->d_slots;
+  a.W = t->d_w;
+  a.Wh = t->d_wh;
+  a.defaults = t->d_defaults;
+  a.dim = t->dim;
+  a.mean = combiner == HPS_COMBINER_MEAN;
+  a.out = out;
+}
+
+// hps_gpu_table_prefetch with the target slot current: everything on the slot's side stream,
+// after the table stream's position at the call.
+int prefetch_into_current(hps_gpu_table t, const uint64_t* keys, const uint32_t* offsets, uint64_t n_bags,
+                          int combiner, uint32_t flags) {
+  cudaStream_t st = t->side;
+  HPSG_CUDA(cudaEventRecord(t->ev_pre, t->ctx->stream));
+  HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_pre, 0));
+  const bool multi = offsets != nullptr;
+  uint64_t n_keys_host = multi ? t->max_keys : n_bags;
+  if (int s = stage_keys(t, keys, offsets, n_bags, flags, st, &n_keys_host)) return s;
+  LookupArgs a{};
+  fill_lookup_args(t, a, keys, offsets, n_bags, combiner, nullptr);
+  if (int s = begin_training_record(t, a, n_keys_host, st)) return s;
+  a.occ_bag = multi ? t->ws_occ_bag : nullptr;
+  a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
+  if (int s = record(t, a, multi, a.mean, n_keys_host, st)) return s;
+  HPSG_CUDA(cudaEventRecord(t->ev_probe, st));
+  if (int s = dedup_on_side(t)) return s;
+  t->prefetched = true;
+  t->pre_keys_host = multi && (flags & HPS_LOOKUP_KEYS_HOST);
+  t->have_train = false;
+  return HPS_GPU_OK;
+}
+
+// HPS_LOOKUP_PREFETCHED: make the prefetched slot current and pool from its record.
+int lookup_prefetched(hps_gpu_table t, const uint32_t* offsets, uint64_t n_bags, int combiner, float* out,
+                      uint32_t flags) {
+  const uint32_t slot = HPS_LOOKUP_SLOT_OF(flags);
+  if (slot >= t->parked.size() || !out) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (slot != t->cur && t->have_train) {
+    set_last_error("lookup(PREFETCHED): the previous training lookup's backward has not run");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  use_slot(t, slot);
+  const bool multi = offsets != nullptr || t->pre_keys_host;
+  if (!t->prefetched || t->have_train || t->pre_n_bags != n_bags || t->last_multi != multi ||
+      t->last_combiner != combiner) {
+    set_last_error("lookup(PREFETCHED): no matching prefetch in this slot (bags, offsets, combiner)");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  cudaStream_t st = t->ctx->stream;
+  HPSG_CUDA(wait_recorded(st, t->ev_probe, t->pre_capture));
+  LookupArgs a{};
+  fill_lookup_args(t, a, nullptr, t->pre_keys_host ? t->ws_offsets_stage : offsets, n_bags, combiner, out);
+  a.occ_row = t->ws_rows_a;
+  a.row_absent = t->row_absent;
+  a.d_n = t->ws_counts;
+  a.max_keys = t->max_keys;
+  a.status = t->ctx->d_status;
+  a.occ_bag = multi ? t->ws_occ_bag : nullptr;
+  a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
+  if (int s = launch_lookup(t, a, multi, true)) return s;
+  t->prefetched = false;
+  t->have_train = true;
   return HPS_GPU_OK;
 }
 
@@ -866,6 +988,79 @@ int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
   }
   HPSG_CHECK_LAUNCH("lookup");
   return HPS_GPU_OK;
+}
+
+// One batch slot's workspaces, side stream and events (sizes from the table's max_keys /
+// max_bags); the caller keeps it in the table (current or parked).
+int alloc_batch_slot(hps_gpu_table t, BatchSlot& b) {
+  const uint64_t D = t->dim, N = t->max_keys, B = t->max_bags;
+  int st = HPS_GPU_OK;
+  auto A = [&](int s) {
+    if (s && !st) st = s;
+  };
+  A(dalloc(&b.ws_rows_a, N));
+  A(dalloc(&b.ws_rank, N));
+  A(dalloc(&b.ws_bt, t->bt_mask + 1));
+  A(dalloc(&b.ws_occ_ent, N));
+  A(dalloc(&b.ws_lead, N));
+  A(dalloc(&b.ws_long_ent, t->max_long));
+  A(dalloc(&b.ws_occ_bag, N));
+  A(dalloc(&b.ws_bag_len, B));
+  A(dalloc(&b.ws_short_rec, N));
+  A(dalloc(&b.ws_short_bag, N));
+  A(dalloc(&b.ws_long_row, t->max_long));
+  A(dalloc(&b.ws_long_len, t->max_long));
+  A(dalloc(&b.ws_long_start, t->max_long));
+  A(dalloc(&b.ws_lkey_a, N));
+  A(dalloc(&b.ws_lval_a, N));
+  A(dalloc(&b.ws_lkey_b, N));
+  A(dalloc(&b.ws_lval_b, N));
+  A(dalloc(&b.ws_long_base, t->max_long));
+  A(dalloc(&b.ws_task_long, t->max_chunks));
+  A(dalloc(&b.ws_partial2, bwd_max_nodes(N) * D));
+  A(dalloc(&b.ws_long_hbase, t->max_long));
+  A(dalloc(&b.ws_node_cnt, bwd_max_nodes(N)));
+  A(dalloc(&b.ws_partial, t->max_chunks * D));
+  A(dalloc(&b.ws_counts, 8));
+  A(dalloc(&b.ws_zero, t->zero_words));
+  A(dalloc(&b.ws_abort, 4));
+  A(dalloc(&b.ws_keys_stage, N));
+  A(dalloc(&b.ws_offsets_stage, B + 1));
+  A(dalloc(&b.ws_ins_slot, N));
+  A(dalloc(&b.ws_ins_pos, N));
+  A(dalloc(&b.ws_ins_flag, N));
+  A(dalloc(&b.ws_ins_scan, scan_tiles(N) + 1));
+  if (st) return st;
+  cudaStream_t s = t->ctx->stream;
+  HPSG_CUDA(cudaMemsetAsync(b.ws_counts, 0, 8 * sizeof(uint64_t), s));
+  HPSG_CUDA(cudaMemsetAsync(b.ws_bt, 0xff, (t->bt_mask + 1) * sizeof(uint2), s));  // {kBtEmpty, UINT32_MAX}
+  HPSG_CUDA(cudaMemsetAsync(b.ws_node_cnt, 0, bwd_max_nodes(N) * sizeof(uint32_t), s));
+  {  // the dedup / long-segment side stream gets the higher priority: its short, latency-bound
+     // kernels are dispatched ahead of the bandwidth-bound main-stream CTAs they overlap
+    int lo = 0, hi = 0;
+    HPSG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    HPSG_CUDA(cudaStreamCreateWithPriority(&b.side, cudaStreamNonBlocking, hi));
+  }
+  for (cudaEvent_t* e : {&b.ev_bwd, &b.ev_done, &b.ev_join2, &b.ev_fork, &b.ev_join, &b.ev_pre, &b.ev_probe})
+    HPSG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  (void)D;
+  (void)B;
+  return HPS_GPU_OK;
+}
+
+void free_batch_slot(BatchSlot& b) {
+  void* ptrs[] = {b.ws_rows_a,   b.ws_bt,        b.ws_occ_ent,    b.ws_lead,       b.ws_long_ent,   b.ws_rank,
+                  b.ws_short_rec, b.ws_short_bag, b.ws_occ_bag,   b.ws_bag_len,    b.ws_long_row,   b.ws_long_len,
+                  b.ws_long_start, b.ws_lkey_a,   b.ws_lval_a,    b.ws_lkey_b,     b.ws_lval_b,     b.ws_long_base,
+                  b.ws_task_long, b.ws_partial2,  b.ws_long_hbase, b.ws_node_cnt,  b.ws_partial,    b.ws_counts,
+                  b.ws_zero,      b.ws_abort,     b.ws_keys_stage, b.ws_offsets_stage, b.ws_ins_slot, b.ws_ins_pos,
+                  b.ws_ins_flag,  b.ws_ins_scan};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (cudaEvent_t e : {b.ev_fork, b.ev_join, b.ev_bwd, b.ev_done, b.ev_join2, b.ev_pre, b.ev_probe})
+    if (e) cudaEventDestroy(e);
+  if (b.side) cudaStreamDestroy(b.side);
+  b = BatchSlot{};
 }
 
 }  // namespace
@@ -957,42 +1152,14 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   A(dalloc(&t->d_nrows, t->n_tables));
   A(dalloc(&t->d_defaults, uint64_t(t->n_tables) * D));
   A(dalloc(&t->d_slot_table, t->n_slots));
-  A(dalloc(&t->ws_rows_a, N));
-  A(dalloc(&t->ws_rank, N));
   // load <= 1/8 (<= 2^25 entries): a home-slot CAS almost always settles an insert
   uint64_t bt_mult = 8;
   if (const char* e = std::getenv("HPS_GPU_BT_MULT")) bt_mult = std::max(2, std::atoi(e));  // A/B knob
   t->bt_mask = std::min<uint64_t>(next_pow2(bt_mult * N), 1ull << 25) - 1;
-  A(dalloc(&t->ws_bt, t->bt_mask + 1));
-  A(dalloc(&t->ws_occ_ent, N));
-  A(dalloc(&t->ws_lead, N));
-  A(dalloc(&t->ws_long_ent, t->max_long));
-  A(dalloc(&t->ws_occ_bag, N));
-  A(dalloc(&t->ws_bag_len, B));
-  A(dalloc(&t->ws_short_rec, N));
-  A(dalloc(&t->ws_short_bag, N));
-  A(dalloc(&t->ws_long_row, t->max_long));
-  A(dalloc(&t->ws_long_len, t->max_long));
-  A(dalloc(&t->ws_long_start, t->max_long));
-  A(dalloc(&t->ws_lkey_a, N));
-  A(dalloc(&t->ws_lval_a, N));
-  A(dalloc(&t->ws_lkey_b, N));
-  A(dalloc(&t->ws_lval_b, N));
-  A(dalloc(&t->ws_long_base, t->max_long));
-  A(dalloc(&t->ws_task_long, t->max_chunks));
-  A(dalloc(&t->ws_partial2, bwd_max_nodes(N) * D));
-  A(dalloc(&t->ws_long_hbase, t->max_long));
-  A(dalloc(&t->ws_node_cnt, bwd_max_nodes(N)));
-  A(dalloc(&t->ws_partial, t->max_chunks * D));
-  A(dalloc(&t->ws_counts, 8));
-  A(dalloc(&t->ws_zero, t->zero_words));
-  A(dalloc(&t->ws_abort, 4));
-  A(dalloc(&t->ws_keys_stage, N));
-  A(dalloc(&t->ws_offsets_stage, B + 1));
-  A(dalloc(&t->ws_ins_slot, N));
-  A(dalloc(&t->ws_ins_pos, N));
-  A(dalloc(&t->ws_ins_flag, N));
-  A(dalloc(&t->ws_ins_scan, scan_tiles(N) + 1));
+  (void)B;
+  if (!st) st = alloc_batch_slot(t, *t);
+  t->parked.resize(1);
+  t->cur = 0;
   if (st) {
     hps_gpu_table_destroy(t);
     return st;
@@ -1003,20 +1170,6 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
                             cudaMemcpyHostToDevice, s));
   HPSG_CUDA(cudaMemsetAsync(t->d_nrows, 0, t->n_tables * sizeof(uint64_t), s));
   HPSG_CUDA(cudaMemsetAsync(t->d_defaults, 0, uint64_t(t->n_tables) * D * sizeof(float), s));
-  HPSG_CUDA(cudaMemsetAsync(t->ws_counts, 0, 8 * sizeof(uint64_t), s));
-  HPSG_CUDA(cudaMemsetAsync(t->ws_bt, 0xff, (t->bt_mask + 1) * sizeof(uint2), s));  // {kBtEmpty, UINT32_MAX}
-  {  // the dedup / long-segment side stream gets the higher priority: its short, latency-bound
-     // kernels are dispatched ahead of the bandwidth-bound main-stream CTAs they overlap
-    int lo = 0, hi = 0;
-    HPSG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    HPSG_CUDA(cudaStreamCreateWithPriority(&t->side, cudaStreamNonBlocking, hi));
-  }
-  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_bwd, cudaEventDisableTiming));
-  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_done, cudaEventDisableTiming));
-  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_join2, cudaEventDisableTiming));
-  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_fork, cudaEventDisableTiming));
-  HPSG_CUDA(cudaEventCreateWithFlags(&t->ev_join, cudaEventDisableTiming));
-  HPSG_CUDA(cudaMemsetAsync(t->ws_node_cnt, 0, bwd_max_nodes(N) * sizeof(uint32_t), s));
   k_fill_slots_empty<<<grid_for(slots, 256, kNumSMs * 32), 256, 0, s>>>(t->d_slots, slots);
   HPSG_CHECK_LAUNCH("k_fill_slots_empty");
   HPSG_CUDA(cudaStreamSynchronize(s));  // the host arrays above are caller-owned
@@ -1026,24 +1179,34 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
 
 int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
+  if (t->parked.empty()) t->parked.resize(1);
+  t->parked[t->cur] = static_cast<BatchSlot&>(*t);
+  for (BatchSlot& b : t->parked)
+    if (b.side) cudaStreamSynchronize(b.side);
   void* ptrs[] = {t->d_wh,        t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
-                  t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_rows_a,
-                  t->ws_bt,       t->ws_occ_ent,   t->ws_lead,   t->ws_long_ent,  t->ws_rank,      t->ws_short_rec, t->ws_short_bag,  t->ws_occ_bag,
-                  t->ws_bag_len,  t->ws_long_row,  t->ws_long_len,  t->ws_long_start, t->ws_lkey_a,
-                  t->ws_lval_a,   t->ws_lkey_b,    t->ws_lval_b,    t->ws_long_base,  t->ws_task_long,
-                  t->ws_partial2, t->ws_long_hbase, t->ws_node_cnt,
-                  t->ws_partial,  t->ws_counts,    t->ws_zero,      t->ws_abort,      t->ws_keys_stage,
-                  t->ws_offsets_stage, t->ws_ins_slot, t->ws_ins_pos, t->ws_ins_flag, t->ws_ins_scan};
-  if (t->side) cudaStreamSynchronize(t->side);
+                  t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  if (t->ev_fork) cudaEventDestroy(t->ev_fork);
-  if (t->ev_join) cudaEventDestroy(t->ev_join);
-  if (t->ev_bwd) cudaEventDestroy(t->ev_bwd);
-  if (t->ev_done) cudaEventDestroy(t->ev_done);
-  if (t->ev_join2) cudaEventDestroy(t->ev_join2);
-  if (t->side) cudaStreamDestroy(t->side);
+  for (BatchSlot& b : t->parked) free_batch_slot(b);
   delete t;
+  return HPS_GPU_OK;
+}
+
+// Pipeline depth (batch slots): depth 2 lets hps_gpu_table_prefetch record + dedup the next
+// batch while the current one pools and updates. Allocates the extra slots (not a hot call).
+int hps_gpu_table_set_pipeline(hps_gpu_table t, uint32_t depth) {
+  if (int s = check_tbl(t)) return s;
+  if (depth < 1 || depth > 4) return HPS_GPU_E_INVALID_ARGUMENT;
+  HPSG_CUDA(cudaSetDevice(t->ctx->device));
+  while (t->parked.size() < depth) {
+    BatchSlot b;
+    if (int s = alloc_batch_slot(t, b)) {
+      free_batch_slot(b);
+      return s;
+    }
+    t->parked.push_back(b);
+  }
+  HPSG_CUDA(cudaStreamSynchronize(t->ctx->stream));
   return HPS_GPU_OK;
 }
 
@@ -1074,10 +1237,18 @@ int hps_gpu_table_size(hps_gpu_table t, uint32_t table, uint64_t* n_rows_host) {
 int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
                          uint64_t* rows_out) {
   if (int s = check_tbl(t)) return s;
+  return hpsg_insert_on(t, table, keys, n, rows, rows_out, t->ctx->stream);
+}
+
+}  // extern "C"
+
+// Insert on stream `st` with the current batch slot's scratch (hps_gpu_table_insert; the
+// insert-on-miss of a prefetch runs it on the slot's side stream).
+int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
+                   uint64_t* rows_out, cudaStream_t st) {
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (n == 0) return HPS_GPU_OK;
   if (!keys || n >= (1ull << 32) - 1) return HPS_GPU_E_INVALID_ARGUMENT;
-  cudaStream_t st = t->ctx->stream;
   const TableDev td = t->h_tables[table];
   uint64_t* ws_slot = nullptr;
   uint32_t* ws_pos = nullptr;
@@ -1123,6 +1294,8 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
   }
   return HPS_GPU_OK;
 }
+
+extern "C" {
 
 int hps_gpu_table_find(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, uint64_t* rows_out) {
   if (int s = check_tbl(t)) return s;
@@ -1170,6 +1343,7 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
     set_last_error("lookup: n_samples * n_slots exceeds max_batch_bags");
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
+  if (flags & HPS_LOOKUP_PREFETCHED) return lookup_prefetched(t, offsets, n_bags, combiner, out, flags);
   if (n_bags == 0) {
     t->have_train = false;
     return HPS_GPU_OK;
@@ -1178,56 +1352,63 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   cudaStream_t st = t->ctx->stream;
   const bool multi = offsets != nullptr;
   uint64_t n_keys_host = multi ? t->max_keys : n_bags;
-  if (flags & HPS_LOOKUP_KEYS_HOST) {
-    // Host buffers: stage H2D on the table's stream (pinned memory -> async copy).
-    n_keys_host = multi ? offsets[n_bags] : n_bags;
-    if (n_keys_host > t->max_keys) return HPS_GPU_E_INVALID_ARGUMENT;
-    HPSG_CUDA(cudaMemcpyAsync(t->ws_keys_stage, keys, n_keys_host * sizeof(uint64_t), cudaMemcpyHostToDevice, st));
-    if (multi)
-      HPSG_CUDA(cudaMemcpyAsync(t->ws_offsets_stage, offsets, (n_bags + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
-    keys = t->ws_keys_stage;
-    if (multi) offsets = t->ws_offsets_stage;
-  } else if (!multi && n_bags > t->max_keys) {
-    return HPS_GPU_E_INVALID_ARGUMENT;
-  }
-  if (flags & HPS_LOOKUP_INSERT) {
-    // Dynamic table (keys materialise on first touch): insert the batch's keys first, in
-    // batch order, so new rows get deterministic ids; then the lookup finds all of them.
-    if (t->n_tables != 1 || (multi && !(flags & HPS_LOOKUP_KEYS_HOST))) {
-      set_last_error("HPS_LOOKUP_INSERT needs a single-table group and a host-known key count");
-      return HPS_GPU_E_INVALID_ARGUMENT;
-    }
-    if (int s = hps_gpu_table_insert(t, 0, keys, n_keys_host, nullptr, nullptr)) return s;
-  }
   const bool train = (flags & HPS_LOOKUP_TRAIN) != 0;
   if (train && t->f16) {
     set_last_error("lookup: an F16 table is an inference table (no training lookups)");
     return HPS_GPU_E_DTYPE_MISMATCH;
   }
+  if (int s = stage_keys(t, keys, offsets, n_bags, flags, st, &n_keys_host)) return s;
   LookupArgs a{};
-  a.keys = keys;
-  a.offsets = offsets;
-  a.n_bags = static_cast<uint32_t>(n_bags);
-  a.n_slots = t->n_slots;
-  a.slot_table = t->d_slot_table;
-  a.tables = t->d_tables;
-  a.slots = t->d_slots;
-  a.W = t->d_w;
-  a.Wh = t->d_wh;
-  a.defaults = t->d_defaults;
-  a.dim = t->dim;
-  a.mean = combiner == HPS_COMBINER_MEAN;
-  a.out = out;
+  fill_lookup_args(t, a, keys, offsets, n_bags, combiner, out);
   if (train) {
-    if (int s = begin_training_record(t, a, n_keys_host)) return s;
+    if (int s = begin_training_record(t, a, n_keys_host, st)) return s;
     a.occ_bag = multi ? t->ws_occ_bag : nullptr;
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
-    if (int s = record(t, a, multi, a.mean, n_keys_host)) return s;
+    if (int s = record(t, a, multi, a.mean, n_keys_host, st)) return s;
   }
   if (int s = launch_lookup(t, a, multi, train)) return s;
   if (train)
     if (int s = fork_dedup(t)) return s;
   t->have_train = train;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_table_prefetch(hps_gpu_table t, uint32_t slot, const uint64_t* keys, const uint32_t* offsets,
+                           uint32_t n_samples, int combiner, uint32_t flags) {
+  if (int s = check_tbl(t)) return s;
+  if (slot >= t->parked.size()) {
+    set_last_error("prefetch: slot >= pipeline depth (hps_gpu_table_set_pipeline)");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (combiner != HPS_COMBINER_SUM && combiner != HPS_COMBINER_MEAN) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (t->f16) return HPS_GPU_E_DTYPE_MISMATCH;
+  if (t->no_fork) {
+    set_last_error("prefetch: needs the side streams (HPS_GPU_NO_FORK is set)");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  const uint64_t n_bags = uint64_t(n_samples) * t->n_slots;
+  if (n_bags == 0 || n_bags > t->max_bags || !keys) {
+    set_last_error("prefetch: empty batch, missing keys, or n_samples * n_slots exceeds max_batch_bags");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (slot == t->cur && t->have_train) {
+    set_last_error("prefetch: the slot holds a training lookup whose backward has not run");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  const uint32_t prev = t->cur;
+  use_slot(t, slot);
+  int s = prefetch_into_current(t, keys, offsets, n_bags, combiner, flags);
+  use_slot(t, prev);
+  return s;
+}
+
+int hps_gpu_table_join_prefetch(hps_gpu_table t) {
+  if (int s = check_tbl(t)) return s;
+  cudaStream_t st = t->ctx->stream;
+  for (uint32_t k = 0; k < t->parked.size(); ++k) {
+    const BatchSlot& b = k == t->cur ? static_cast<const BatchSlot&>(*t) : t->parked[k];
+    if (b.dedup_pending) HPSG_CUDA(wait_recorded(st, b.ev_done, b.pre_capture));
+  }
   return HPS_GPU_OK;
 }
 
@@ -1285,7 +1466,7 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
   if (combiner != HPS_COMBINER_SUM && combiner != HPS_COMBINER_MEAN) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = t->ctx->stream;
   LookupArgs a{};
-  if (int s = begin_training_record(t, a, n_keys_host)) return s;
+  if (int s = begin_training_record(t, a, n_keys_host, st)) return s;
   a.keys = keys;
   a.offsets = offsets;
   a.n_bags = static_cast<uint32_t>(n_bags);
@@ -1295,7 +1476,7 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
   a.slots = t->d_slots;
   a.occ_bag = multi ? t->ws_occ_bag : nullptr;
   a.bag_len = (multi && combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
-  if (int s = record(t, a, multi, combiner == HPS_COMBINER_MEAN, n_keys_host)) return s;
+  if (int s = record(t, a, multi, combiner == HPS_COMBINER_MEAN, n_keys_host, st)) return s;
   if (int s = fork_dedup(t)) return s;
   // compaction scan: its look-back words live past the backward's zeroed region
   const uint64_t tiles = scan_tiles(std::max<uint64_t>(n_keys_host, 1));
@@ -1371,8 +1552,8 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
   a.dim = t->dim;
   a.out = rows_out;
   if (train) {
-    if (int s = begin_training_record(t, a, n)) return s;
-    if (int s = record(t, a, false, false, n)) return s;
+    if (int s = begin_training_record(t, a, n, t->ctx->stream)) return s;
+    if (int s = record(t, a, false, false, n, t->ctx->stream)) return s;
   }
   if (int s = launch_lookup(t, a, false, train)) return s;
   if (train)
