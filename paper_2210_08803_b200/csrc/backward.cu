@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(kDedupBlock, 2) k_dedup(BwdArgs a, uint32_t* c
   __shared__ uint32_t s_nlead;
   trace_begin(kTrCount);
   const uint64_t n = a.counts[0];
+  // this slot now holds a record whose short batch-table entries await a backward (counts[5])
+  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 1;
   const uint64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
   const uint32_t lane = lane_id(), lt = lanemask_lt();
   constexpr uint64_t kBatch = uint64_t(kDedupBlock) * kDedupIPT;
@@ -1142,6 +1144,9 @@ __global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : (OPT == 
   __shared__ __align__(8) uint64_t s_bar[kRedWarps];
   pdl_wait();
   pdl_launch_dependents();
+  // the short segments' batch-table entries are reset by this kernel: the slot no longer holds
+  // an unconsumed record (counts[5], set by k_dedup, read by table.cu k_reset_counts)
+  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 0;
   const uint64_t wpb = blockDim.x >> 5;
   const uint64_t warp = uint64_t(blockIdx.x) * wpb + (threadIdx.x >> 5);
   const uint64_t n_warps = uint64_t(gridDim.x) * wpb;
@@ -1162,6 +1167,7 @@ __global__ void __launch_bounds__(kPipeBlock, 3) k_reduce_pipe(BwdArgs a) {
   __shared__ uint2 s_list[kPipeBlock / 32][kPipeList];
   pdl_wait();
   pdl_launch_dependents();
+  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 0;  // (as k_reduce_short)
   const uint64_t wpb = blockDim.x >> 5;
   const uint64_t warp = uint64_t(blockIdx.x) * wpb + (threadIdx.x >> 5);
   const uint64_t n_warps = uint64_t(gridDim.x) * wpb;

@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(256) k_probe(LookupArgs a) {
 // Batch-table entries left by a training record that no backward consumed: back to empty.
 __global__ void k_reset_counts(const uint32_t* __restrict__ occ_row, const uint32_t* __restrict__ occ_ent,
                                const uint64_t* d_n, uint32_t row_absent, uint2* bt) {
+  if (d_n[5] == 0) return;  // no unconsumed record in this slot (device truth; see begin_training_record)
   trace_begin(kTrReset);
   const uint64_t n = *d_n;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
@@ -751,7 +752,10 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk, cudaStrea
     HPSG_CUDA(wait_recorded(st, t->ev_done, t->pre_capture));
     t->dedup_pending = false;
   }
-  if (t->counts_dirty) {
+  // Host flags are exact for eager use; once a record was captured into a graph, replays
+  // can leave a slot's device state differing from them, so the (device-checked) reset is
+  // then always enqueued.
+  if (t->counts_dirty || t->graphs_seen) {
     k_reset_counts<<<grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0, st>>>(
         t->ws_rows_a, t->ws_occ_ent, t->ws_counts, t->row_absent, t->ws_bt);
     HPSG_CHECK_LAUNCH("k_reset_counts");
@@ -782,6 +786,7 @@ int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t
   t->last_n_keys_host = nk;
   t->pre_n_bags = a.n_bags;
   t->pre_capture = capture_id(st);
+  if (t->pre_capture) t->graphs_seen = true;
   // the fork point: right after the record (the pooling launched next does not gate the dedup)
   if (!t->no_fork && st != t->side) HPSG_CUDA(cudaEventRecord(t->ev_fork, st));
   return HPS_GPU_OK;

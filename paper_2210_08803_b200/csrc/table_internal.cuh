@@ -148,6 +148,7 @@ struct hps_gpu_table_s : BatchSlot {
   uint32_t cur = 0;
   cudaEvent_t ev_last_dedup = nullptr;  // the last k_dedup launched (prefetches serialise on it)
   bool last_dedup_valid = false;
+  bool graphs_seen = false;  // a training record was captured into a graph (host slot flags may lag replays)
   unsigned long long last_dedup_capture = 0;
   bool no_fork = false;         // HPS_GPU_NO_FORK=1: everything on the main stream (A/B measurement)
   bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)

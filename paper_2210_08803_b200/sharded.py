@@ -152,7 +152,8 @@ class TrainStep:
 
     def __init__(self, ctx: Context, table: Optional[EmbeddingTableGroup], cfg: W.Config, rank: int = 0,
                  world: int = 1, use_graph: bool = True, owned: Optional[List[List[int]]] = None,
-                 hybrid_hot: Optional[EmbeddingTableGroup] = None, force_exchange: bool = False):
+                 hybrid_hot: Optional[EmbeddingTableGroup] = None, force_exchange: bool = False,
+                 pipeline: bool = True):
         """owned (world > 1): localized placement, owned[g] = slots of rank g (localized_plan);
         None = distributed placement."""
         self.ctx, self.table, self.cfg, self.rank, self.world = ctx, table, cfg, rank, world
@@ -206,6 +207,17 @@ class TrainStep:
             self.kernels_per_step = 5 + rec + 1 + 1 + 1 + 2 + (1 if cfg.hot > 1 else 0)
         if self.insert_missing:  # claim + scan + commit + finish
             self.kernels_per_step += 4
+        # Batch pipelining (single path): the record + dedup of batch i+1 (prefetch, on the
+        # table's slot stream) overlap batch i's pooling + backward; run(..., next_b=) names
+        # batch i+1. +1 kernel: the step's unique-row count (k_unique_count) into self._cnt.
+        self.pipeline = bool(pipeline and self.exchange is None and table is not None)
+        if self.pipeline:
+            table.set_pipeline(2)
+            self.kernels_per_step += 1
+        self._pre = None        # (batch dict, slot) prefetched and not yet consumed
+        self._free_slot = 0     # slot the next eager prefetch goes to
+        self._warmed = False    # the first pipelined step runs eagerly (module loading)
+        self._pipe_stage = None
 
     # -- inputs -------------------------------------------------------------------------
     def stage_batch(self, keys: np.ndarray, offs: Optional[np.ndarray]):
@@ -267,12 +279,82 @@ class TrainStep:
             return
         g.replay()
 
-    def run(self, b, dout, step: int = 1):
+    # -- pipelined step (hps_gpu_table_prefetch) ----------------------------------------------
+    def _adam_params(self, step):
+        if self.cfg.optimizer == "adam":
+            self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
+            if self.graph_mode:
+                self.params.lr_t_device = self._lr_dev.data_ptr()
+
+    def _prefetch(self, slot, nb, keys_on_host):
+        self.table.prefetch(slot, nb["keys"], self.cfg.batch, offsets=nb["offs"], combiner=self.cfg.combiner,
+                            keys_on_host=keys_on_host, insert_missing=self.insert_missing)
+
+    def _pipe_body(self, b, nb, dout, slot, keys_on_host=False, result=None):
+        """prefetch(nb -> other slot) ; lookup(slot) ; backward ; unique count ; join."""
+        if nb is not None:
+            self._prefetch(1 - slot, nb, keys_on_host)
+        offs = None if (keys_on_host or b["offs"] is None) else b["offs"]
+        self.table.lookup_prefetched(slot, self.cfg.batch, offsets=offs, combiner=self.cfg.combiner, out=self.out)
+        self.table.backward_update(dout, self.cfg.lr, params=self.params)
+        L.check(self.ctx.lib.hps_gpu_table_last_unique(self.table.h, _ptr(self._cnt), None), "last_unique")
+        if result is not None:
+            result.copy_(self._cnt, non_blocking=True)
+        if nb is not None:
+            self.table.join_prefetch()
+
+    def _run_pipe(self, b, dout, step, nb, keys_on_host=False, result=None, tag="dev"):
+        """One pipelined step. Host state advances exactly once per call: eagerly, or by the
+        capture of a graph that is then replayed (replays of captured graphs leave it alone)."""
+        self._adam_params(step)
+        if self._pre is None or self._pre[0] is not b:  # b was not prefetched by the previous step
+            self._prefetch(self._free_slot, b, keys_on_host)
+            self.table.join_prefetch()
+            self._pre = (b, self._free_slot)
+        slot = self._pre[1]
+        if self.insert_missing and nb is not None and not keys_on_host:
+            # a dynamic table streams fresh batches: the next batch's keys go to a per-slot
+            # device staging buffer (D2D before the replay), one graph per slot parity
+            if self._pipe_stage is None:
+                self._pipe_stage = [torch.empty(table_max_keys(self.cfg, 1), dtype=torch.int64, device="cuda")
+                                    for _ in range(2)]
+            buf = self._pipe_stage[1 - slot][:nb["keys"].numel()]
+            buf.copy_(nb["keys"], non_blocking=True)
+            nb_g = {"keys": buf, "offs": nb["offs"], "n_keys": nb["n_keys"]}
+            key = (tag, "stage", slot, nb["keys"].numel(), id(dout), id(result))
+        else:
+            nb_g = nb
+            key = (tag, id(b["keys"]), None if nb is None else id(nb["keys"]), id(dout), slot, id(result))
+        if not self.graph_mode or not self._warmed or nb is None:
+            self._pipe_body(b, nb_g, dout, slot, keys_on_host, result)
+            self._warmed = True
+        else:
+            g = self._graphs.get(key)
+            if g is None:
+                s = torch.cuda.Stream()
+                s.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(s):
+                    self.ctx.set_stream(s)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=s):
+                        self._pipe_body(b, nb_g, dout, slot, keys_on_host, result)
+                torch.cuda.current_stream().wait_stream(s)
+                self.ctx.set_stream(torch.cuda.current_stream())
+                self._graphs[key] = g
+            g.replay()
+        if nb is None:
+            self._pre, self._free_slot = None, 1 - slot
+        else:
+            self._pre, self._free_slot = (nb, 1 - slot), slot
+
+    def run(self, b, dout, step: int = 1, next_b=None):
         self._last_n = b["n_keys"]
         if self.exchange is None:
             self._prep_step(step)
         if self.exchange is not None:
             return self._exchange_step(b["keys"], b["offs"], dout, step)
+        if self.pipeline:
+            return self._run_pipe(b, dout, step, next_b)
         if not self.graph_mode:
             return self._eager(b, dout, step)
         if self.insert_missing and b["offs"] is None:
@@ -291,7 +373,7 @@ class TrainStep:
         L.check(self.ctx.lib.hps_gpu_table_last_unique(self.table.h, _ptr(self._cnt), None), "last_unique")
         (self._cnt_host if out is None else out).copy_(self._cnt, non_blocking=True)
 
-    def run_host_async(self, b, dout, step: int, slot: int):
+    def run_host_async(self, b, dout, step: int, slot: int, next_b=None):
         """End-to-end step from pinned HOST keys, pipelined one step deep: the keys go H2D on a
         copy stream into device staging slot `slot` (while the previous step computes), the
         step (kernels + the D2H of its result into pinned slot `slot`) follows on the main
@@ -299,6 +381,16 @@ class TrainStep:
         result D2H inside the timed region; the copies overlap the previous step's kernels."""
         h2d = b["keys"].numel() * 8 + (0 if b["offs"] is None else b["offs"].numel() * 4)
         multi = b["offs"] is not None
+        if self.pipeline and next_b is not None:
+            # pipelined: the NEXT batch's pinned keys (+ offsets) go H2D inside its prefetch, on
+            # the slot stream, overlapping this batch's pooling + update; the step's result (unique
+            # rows, 8 B) goes D2H into pinned slot `slot`
+            self._prep_step(step)
+            self._last_n = b["n_keys"]
+            self._run_pipe(b, dout, step, next_b, keys_on_host=True, result=self._cnt_slots[slot], tag="host")
+            self._slot_ev[slot].record()
+            nb = next_b
+            return nb["keys"].numel() * 8 + (0 if nb["offs"] is None else nb["offs"].numel() * 4), 8
         if self.exchange is not None or not self.graph_mode or (multi and self.insert_missing):
             self.run_host(b, dout, step)
             self._cnt_slots[slot].copy_(self._cnt_host)
@@ -363,6 +455,8 @@ class TrainStep:
         if self.table is None:  # localized rank that owns no slot
             torch.cuda.current_stream().synchronize()
             return 0
+        if self.pipeline:  # every pipelined step writes its count into self._cnt
+            return int(self._cnt.item())
         self.ctx.lib.hps_gpu_table_last_unique(self.table.h, self._cnt.data_ptr(), None)
         return int(self._cnt.item())
 
