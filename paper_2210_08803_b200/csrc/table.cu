@@ -898,7 +898,10 @@ int lookup_prefetched(hps_gpu_table t, const uint32_t* offsets, uint64_t n_bags,
   }
   use_slot(t, slot);
   const bool multi = offsets != nullptr || t->pre_keys_host;
-  if (!t->prefetched || t->have_train || t->pre_n_bags != n_bags || t->last_multi != multi ||
+  // Under stream capture the host flags may lag the device (graphs replayed out of capture
+  // order): the caller's slot discipline is trusted there, the batch shape is still checked.
+  const bool capturing = capture_id(t->ctx->stream) != 0;
+  if ((!t->prefetched && !capturing) || t->have_train || t->pre_n_bags != n_bags || t->last_multi != multi ||
       t->last_combiner != combiner) {
     set_last_error("lookup(PREFETCHED): no matching prefetch in this slot (bags, offsets, combiner)");
     return HPS_GPU_E_INVALID_ARGUMENT;
@@ -971,7 +974,7 @@ int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
     // training: ONE CTA per SM. The pooling runs beside the dedup, and its row stream slows
     // the dedup's L2 atomics; at one CTA per SM it takes ~46 us instead of 37, still hidden,
     // and the dedup's count phase drops from 35 to 27 us (config 2: 0.134 -> 0.131 ms)
-    uint64_t train_ctas = 1;
+    uint64_t train_ctas = t->prefetched ? 8 : 1;  // prefetched: its dedup ran ahead, nothing to leave room for
     if (const char* e = std::getenv("HPS_GPU_POOL_CTAS")) train_ctas = std::max(1, std::atoi(e));  // A/B knob
     const uint64_t max_grid = rows ? uint64_t(kNumSMs) * train_ctas : uint64_t(kNumSMs) * 8;
     const int grid =

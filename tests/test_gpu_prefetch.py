@@ -19,7 +19,11 @@ pytestmark = pytest.mark.gpu
 def onehot_batches(pools, rs, B, n):
     out = []
     for _ in range(n):
-        k0 = skewed_multiset(pools[0], rs, 3 * B, 50).reshape(B, 3)
+        if 3 * B >= 16000:
+            k0 = skewed_multiset(pools[0], rs, 3 * B, 50).reshape(B, 3)
+        else:  # small batches: a few hot keys (long segments) over a uniform background
+            k0 = np.where(rs.random(3 * B) < 0.3, rs.choice(pools[0][:8], 3 * B),
+                          rs.choice(pools[0], 3 * B)).reshape(B, 3)
         k1 = rs.choice(pools[1], B)
         out.append(np.stack([k0[:, 0], k1, k0[:, 1], k0[:, 2]], 1).ravel().astype(np.uint64))
     return out
@@ -48,7 +52,7 @@ def test_prefetch_onehot_eager(ctx, dim, opt):
     g, o = make_pair(ctx, caps, dim, slots, opt, a0=0.1 if opt == "adagrad" else 0.0)
     pools = load_tables(g, o, caps, rs)
     g.set_pipeline(2)
-    B, S = 3000, 5
+    B, S = 6000, 5
     batches = onehot_batches(pools, rs, B, S)
     dev = [t64(k) for k in batches]
     kw = {"eps": 1e-7} if opt == "adagrad" else {}
