@@ -395,6 +395,116 @@ __global__ void __launch_bounds__(kDedupBlock, 2) k_dedup(BwdArgs a, uint32_t* c
   trace_end(kTrPlace);
 }
 
+// ---- K4a-c flat: the same products from three full-occupancy kernels (no grid barriers) ---
+// k_count_flat : one occurrence per thread; the lanes of a warp holding the same row are
+//                merged (match_any) and their leader reserves the row's batch-table entry
+//                with ONE CAS + ONE add: every occurrence gets its arrival rank and entry
+// k_alloc_flat : the rank-0 occurrence of each row (its count is final now) takes a short
+//                CSR range (block scan + one packed atomic per block) or a long id
+// k_scan<PlaceOp>: short occurrences drop their bag at first + rank; long ones are compacted
+//                in canonical order (decoupled look-back scan)
+// Latency-bound phases at full occupancy: every load and atomic of a phase is in flight at
+// once, instead of one persistent CTA per SM walking its chunk.
+__global__ void __launch_bounds__(256) k_count_flat(BwdArgs a) {
+  pdl_wait();
+  pdl_launch_dependents();
+  trace_begin(kTrCount);
+  const uint64_t n = a.counts[0];
+  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 1;  // (as k_dedup)
+  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  if (blockIdx.x * uint64_t(blockDim.x) >= n) return;  // whole warps past the end leave together
+  const uint32_t row = i < n ? a.occ_row[i] : a.row_absent;
+  const bool active = row != a.row_absent;
+  const uint32_t peers = __match_any_sync(0xffffffffu, row);
+  const int leader = __ffs(peers) - 1;
+  uint32_t e = 0, base = 0;
+  if (active && static_cast<int>(lane_id()) == leader) {
+    e = bt_insert(a.bt, a.bt_mask, row);
+    base = atomicAdd(&a.bt[e].y, static_cast<uint32_t>(__popc(peers))) + 1u;
+  }
+  e = __shfl_sync(0xffffffffu, e, leader);
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (active) {
+    a.occ_ent[i] = e;
+    a.occ_rank[i] = base + __popc(peers & lanemask_lt());
+  }
+  trace_end(kTrCount);
+}
+
+constexpr int kAllocIPT = 4;
+__global__ void __launch_bounds__(256) k_alloc_flat(BwdArgs a) {
+  __shared__ unsigned long long s_scr[33];
+  __shared__ unsigned long long s_cursor;
+  pdl_wait();
+  pdl_launch_dependents();
+  trace_begin(kTrAlloc);
+  const uint64_t n = a.counts[0];
+  const uint64_t b0 = blockIdx.x * uint64_t(256 * kAllocIPT);
+  if (b0 >= n) return;
+  uint32_t ent[kAllocIPT], len[kAllocIPT];
+  unsigned long long mine = 0;
+#pragma unroll
+  for (int k = 0; k < kAllocIPT; ++k) {
+    const uint64_t i = b0 + threadIdx.x * kAllocIPT + k;
+    const bool lead = i < n && a.occ_row[i] != a.row_absent && a.occ_rank[i] == 0u;
+    ent[k] = lead ? a.occ_ent[i] : kNoEnt;
+    len[k] = lead ? __ldcg(&a.bt[ent[k]].y) + 1u : 0u;
+    if (len[k] && len[k] <= kChunk) mine += (1ull << 32) | len[k];
+  }
+  unsigned long long total;
+  unsigned long long pos = block_excl_scan<256>(mine, s_scr, &total);
+  if (threadIdx.x == 0) s_cursor = total ? atomicAdd(a.short_alloc, total) : 0ull;
+  __syncthreads();
+  pos += s_cursor;
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int k = 0; k < kAllocIPT; ++k) {
+    const uint64_t i = b0 + threadIdx.x * kAllocIPT + k;
+    const bool sh = len[k] && len[k] <= kChunk, lg = len[k] > kChunk;
+    if (sh) {
+      const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
+      a.short_rec[seg] = make_uint4(a.occ_row[i], first, len[k], ent[k]);
+      a.bt[ent[k]].y = first;
+      pos += (1ull << 32) | len[k];
+    }
+    const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
+    if (lg_mask) {
+      const int src = __ffs(lg_mask) - 1;
+      uint32_t j0 = 0;
+      if (static_cast<int>(lane_id()) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
+      j0 = __shfl_sync(0xffffffffu, j0, src);
+      if (lg) {
+        const uint32_t j = j0 + __popc(lg_mask & lt);
+        a.long_row[j] = a.occ_row[i];
+        a.long_ent[j] = ent[k];
+        a.long_len[j] = len[k];
+        a.bt[ent[k]].y = kLongFlag | j;
+      }
+    }
+  }
+  trace_end(kTrAlloc);
+}
+
+struct PlaceOp {
+  static constexpr int kTrace = kTrPlace;
+  BwdArgs a;
+  __device__ uint64_t size() const { return a.counts[0]; }
+  __device__ uint32_t bag(uint64_t i) const { return a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i); }
+  __device__ uint64_t count(uint64_t i) const {
+    if (a.occ_row[i] == a.row_absent) return 0;
+    const uint32_t loc = __ldcg(&a.bt[a.occ_ent[i]].y);
+    if (loc & kLongFlag) return 1;
+    a.short_bag[loc + a.occ_rank[i]] = bag(i);
+    return 0;
+  }
+  __device__ void emit(uint64_t i, uint64_t excl, uint64_t c) const {
+    if (!c) return;
+    a.lkey[excl] = __ldcg(&a.bt[a.occ_ent[i]].y) & ~kLongFlag;
+    a.lval[excl] = bag(i);
+  }
+  __device__ void total(uint64_t t) const { *a.long_occ = t; }
+};
+
 // ---- long segments: registration ---------------------------------------------------------
 // Nodes above level 1 of a long segment's 32-ary tree (m level-1 chunks).
 __device__ __forceinline__ uint32_t higher_nodes(uint32_t m) {
@@ -1353,7 +1463,18 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
   uint32_t* z = t->ws_zero;
   const BwdArgs a = base_args(t);
   // K4a-c: counts, allocation, placement (first on this stream after the fork: a plain launch)
-  {
+  static const bool flat = [] {
+    const char* e = std::getenv("HPS_GPU_DEDUP");  // A/B knob: "flat" (default) or "persistent"
+    return !(e && std::strcmp(e, "persistent") == 0);
+  }();
+  if (flat) {
+    const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(nk));
+    HPSG_CUDA(launch_k(false, k_count_flat, grid_for(nk, 256, 1 << 30), 256, 0, st, a));
+    HPSG_CUDA(launch_k(pdl, k_alloc_flat, grid_for((nk + kAllocIPT - 1) / kAllocIPT, 256, 1 << 30), 256, 0, st, a));
+    uint64_t* status = reinterpret_cast<uint64_t*>(z + zl.place);
+    HPSG_CUDA(launch_k(pdl, k_scan<PlaceOp>, static_cast<unsigned>(tiles), kScanBlock, 0, st, PlaceOp{a}, status,
+                       reinterpret_cast<uint32_t*>(status + tiles)));
+  } else {
     HPSG_CUDA(dedup_attributes());
 
     uint64_t per_cta = 256;  // occurrences per CTA below a full grid (more CTAs: shorter chains; cfg1 64.9 -> 63.4 us)
