@@ -77,6 +77,7 @@ struct BwdArgs {
   uint32_t* higher_total;           // allocator of partial2 nodes (zeroed per call)
   uint32_t* touched;                // kOptGrad: row -> 1 when its gradient was written
   uint32_t tma_rows;                // rows per warp buffer in short_tma
+  uint32_t n_slots;                 // one-hot: occurrence i = sample * n_slots + slot
   float* W;
   float* S0;
   float* S1;
@@ -411,9 +412,17 @@ __global__ void __launch_bounds__(256) k_count_flat(BwdArgs a) {
   trace_begin(kTrCount);
   const uint64_t n = a.counts[0];
   if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 1;  // (as k_dedup)
-  const uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (blockIdx.x * uint64_t(blockDim.x) >= n) return;  // whole warps past the end leave together
-  const uint32_t row = i < n ? a.occ_row[i] : a.row_absent;
+  // One-hot batches are walked slot-major (a warp holds 32 samples of one slot), so the rows of
+  // small tables — hundreds of occurrences each — merge within warps (config 2's 3-row table:
+  // 3 atomics per warp instead of 32 on the same three entries)
+  uint64_t i = j;
+  if (!a.occ_bag && a.n_slots > 1 && n % a.n_slots == 0) {
+    const uint64_t ns = n / a.n_slots;
+    i = (j % ns) * a.n_slots + j / ns;
+  }
+  const uint32_t row = j < n ? a.occ_row[i] : a.row_absent;
   const bool active = row != a.row_absent;
   const uint32_t peers = __match_any_sync(0xffffffffu, row);
   const int leader = __ffs(peers) - 1;
@@ -1417,6 +1426,7 @@ BwdArgs base_args(hps_gpu_table t) {
   a.lbag = (bwd_long_passes(t->last_n_keys_host) & 1) ? t->ws_lval_b : t->ws_lval_a;
   a.bag_len = (t->last_multi && t->last_combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
   a.dim = t->dim;
+  a.n_slots = t->n_slots;
   a.long_base = t->ws_long_base;
   a.task_long = t->ws_task_long;
   a.partial = t->ws_partial;
@@ -1435,7 +1445,8 @@ cudaError_t dedup_attributes() {
   return once_per_device(g_dedup_attr, []() -> cudaError_t {
     if (cudaError_t e = cudaFuncSetAttribute(k_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4))
       return e;
-    for (cudaError_t e : {prefer_max_smem(k_dedup), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass),
+    for (cudaError_t e : {prefer_max_smem(k_dedup), prefer_max_smem(k_count_flat), prefer_max_smem(k_alloc_flat),
+                          prefer_max_smem(k_scan<PlaceOp>), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass),
                           prefer_max_smem(k_scan<LongRegOp>), prefer_max_smem(k_long_tasks)})
       if (e) return e;
     return cudaSuccess;
@@ -1468,6 +1479,7 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
     return !(e && std::strcmp(e, "persistent") == 0);
   }();
   if (flat) {
+    HPSG_CUDA(dedup_attributes());
     const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(nk));
     HPSG_CUDA(launch_k(false, k_count_flat, grid_for(nk, 256, 1 << 30), 256, 0, st, a));
     HPSG_CUDA(launch_k(pdl, k_alloc_flat, grid_for((nk + kAllocIPT - 1) / kAllocIPT, 256, 1 << 30), 256, 0, st, a));

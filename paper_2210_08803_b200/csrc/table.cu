@@ -896,16 +896,17 @@ int lookup_prefetched(hps_gpu_table t, const uint32_t* offsets, uint64_t n_bags,
     set_last_error("lookup(PREFETCHED): the previous training lookup's backward has not run");
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
-  use_slot(t, slot);
-  const bool multi = offsets != nullptr || t->pre_keys_host;
+  const BatchSlot& b = slot == t->cur ? static_cast<const BatchSlot&>(*t) : t->parked[slot];
+  const bool multi = offsets != nullptr || b.pre_keys_host;
   // Under stream capture the host flags may lag the device (graphs replayed out of capture
   // order): the caller's slot discipline is trusted there, the batch shape is still checked.
   const bool capturing = capture_id(t->ctx->stream) != 0;
-  if ((!t->prefetched && !capturing) || t->have_train || t->pre_n_bags != n_bags || t->last_multi != multi ||
-      t->last_combiner != combiner) {
+  if ((!b.prefetched && !capturing) || b.have_train || b.pre_n_bags != n_bags || b.last_multi != multi ||
+      b.last_combiner != combiner) {
     set_last_error("lookup(PREFETCHED): no matching prefetch in this slot (bags, offsets, combiner)");
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
+  use_slot(t, slot);
   cudaStream_t st = t->ctx->stream;
   HPSG_CUDA(wait_recorded(st, t->ev_probe, t->pre_capture));
   LookupArgs a{};
