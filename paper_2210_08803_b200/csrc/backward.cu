@@ -83,6 +83,7 @@ struct BwdArgs {
   // the short reduce reads {row, entry * 32, count, entry} from the list + the batch table.
   uint32_t* lead_ent;               // leader list: batch-table entry (nullptr: CSR records)
   uint32_t* lead_row;               // leader list: the row
+  uint32_t* lead_bag;               // leader list: the leader's own bag (a singleton needs no other)
   float* W;
   float* S0;
   float* S1;
@@ -574,6 +575,7 @@ __global__ void __launch_bounds__(256) k_count_lead(BwdArgs a) {
     const uint32_t u = s_base + s_wn[w] + __popc(lm & lanemask_lt());
     a.lead_ent[u] = e;
     a.lead_row[u] = row;
+    a.lead_bag[u] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
   }
   trace_end(kTrCount);
 }
@@ -1138,7 +1140,7 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
     if (u0 + lane < S) rec = short_rec_at(a, u0 + lane);
     const uint32_t row = rec.x, first = rec.y, len = rec.z, slot = rec.w;
     if (len) a.bt[slot] = make_uint2(kBtEmpty, 0xffffffffu);  // placement (previous kernels) is done with it
-    uint32_t bag0 = len ? a.short_bag[first] : 0u;
+    uint32_t bag0 = len ? (a.lead_bag ? a.lead_bag[u0 + lane] : a.short_bag[first]) : 0u;
     const uint32_t c = len ? HDR + len : 0u;
     const uint32_t incl = warp_incl_scan(c), excl = incl - c;
     uint32_t done = 0;  // lanes (segments) already streamed
@@ -1562,6 +1564,7 @@ BwdArgs base_args(hps_gpu_table t) {
   if (t->lead_mode) {  // flat dedup: entry-indexed short segments
     a.lead_ent = t->ws_lead_ent;
     a.lead_row = t->ws_lead_row;
+    a.lead_bag = t->ws_lead_bag;
     a.short_bag = t->ws_bagarr;
   }
   a.long_base = t->ws_long_base;

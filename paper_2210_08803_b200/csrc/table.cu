@@ -1043,6 +1043,7 @@ int alloc_batch_slot(hps_gpu_table t, BatchSlot& b) {
     A(dalloc(&b.ws_bagarr, (t->bt_mask + 1) * kChunk));
     A(dalloc(&b.ws_lead_ent, N));
     A(dalloc(&b.ws_lead_row, N));
+    A(dalloc(&b.ws_lead_bag, N));
   }
   if (st) return st;
   cudaStream_t s = t->ctx->stream;
@@ -1068,7 +1069,8 @@ void free_batch_slot(BatchSlot& b) {
                   b.ws_long_start, b.ws_lkey_a,   b.ws_lval_a,    b.ws_lkey_b,     b.ws_lval_b,     b.ws_long_base,
                   b.ws_task_long, b.ws_partial2,  b.ws_long_hbase, b.ws_node_cnt,  b.ws_partial,    b.ws_counts,
                   b.ws_zero,      b.ws_abort,     b.ws_keys_stage, b.ws_offsets_stage, b.ws_ins_slot, b.ws_ins_pos,
-                  b.ws_ins_flag,  b.ws_ins_scan,  b.ws_bagarr,    b.ws_lead_ent,   b.ws_lead_row};
+                  b.ws_ins_flag,  b.ws_ins_scan,  b.ws_bagarr,    b.ws_lead_ent,   b.ws_lead_row,
+                  b.ws_lead_bag};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : {b.ev_fork, b.ev_join, b.ev_bwd, b.ev_done, b.ev_join2, b.ev_pre, b.ev_probe})

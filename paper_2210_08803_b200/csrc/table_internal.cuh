@@ -100,6 +100,7 @@ struct BatchSlot {
   uint32_t* ws_bagarr = nullptr;
   uint32_t* ws_lead_ent = nullptr;
   uint32_t* ws_lead_row = nullptr;
+  uint32_t* ws_lead_bag = nullptr;
   // last training lookup recorded in this slot
   bool have_train = false, last_multi = false;
   bool counts_dirty = false;  // batch-table counters hold a training record no backward has consumed

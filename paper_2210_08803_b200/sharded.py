@@ -210,6 +210,9 @@ class TrainStep:
         # Batch pipelining (single path): the record + dedup of batch i+1 (prefetch, on the
         # table's slot stream) overlap batch i's pooling + backward; run(..., next_b=) names
         # batch i+1. +1 kernel: the step's unique-row count (k_unique_count) into self._cnt.
+        import os
+        if os.environ.get("HPS_PIPELINE") == "0":  # A/B knob
+            pipeline = False
         self.pipeline = bool(pipeline and self.exchange is None and table is not None)
         if self.pipeline:
             table.set_pipeline(2)

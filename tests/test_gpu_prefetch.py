@@ -166,7 +166,8 @@ def test_prefetch_graph_replay(ctx, multi):
         return kbuf[slot][:len(batches[s][0])]
 
     stream = torch.cuda.Stream()
-    stream.wait_stream(torch.cuda.current_stream())
+    main = torch.cuda.current_stream()
+    stream.wait_stream(main)
     graphs = {}
     with torch.cuda.stream(stream):
         ctx.set_stream(stream)
@@ -195,8 +196,8 @@ def test_prefetch_graph_replay(ctx, multi):
                 stream.synchronize()
                 close(outbuf.cpu().numpy(), ref, f"graph step {s}")
         finally:
-            torch.cuda.current_stream().wait_stream(stream)
-            ctx.set_stream(torch.cuda.current_stream())
+            main.wait_stream(stream)
+            ctx.set_stream(main)  # (torch's current stream inside this block is `stream`)
     ctx.sync()
     compare_tables(g, o, caps)
 

@@ -464,9 +464,9 @@ def test_adam_graph_step_matches_eager(ctx):
         ctx.sync()
         n = tab.size(0)
         res.append([x.cpu().numpy() for x in tab.export(0, 0, n)])
-    for other in res[1:]:
-        for a, b in zip(res[0], other):
-            np.testing.assert_array_equal(a, b)
+    for mode, other in zip(("graph", "host"), res[1:]):
+        for k, (a, b) in enumerate(zip(res[0], other)):
+            np.testing.assert_array_equal(a, b, err_msg=f"{mode} vs eager, state {k}")
 
 
 def test_multi_hot_pipelined_host_steps_match_eager(ctx):
