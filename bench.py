@@ -64,7 +64,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pool", type=int, default=4, help="distinct synthetic batches rotated through")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--no-pipeline", action="store_true", help="no batch pipelining (prefetch of the next batch)")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="batch pipelining: each step prefetches (records + dedups) the next batch on a slot stream")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--table-scale", type=float, default=1.0, help="debug only: shrink cardinalities")
@@ -323,7 +324,7 @@ def main():
         tables = build_tables_localized(ctx, cfg, owned, rank, world)
     gen = W.BatchGen(cfg)
     step_fn = TrainStep(ctx, tables, cfg, rank, world, use_graph=not args.no_graph, owned=owned, hybrid_hot=hot,
-                        force_exchange=xchg, pipeline=not args.no_pipeline)
+                        force_exchange=xchg, pipeline=args.pipeline)
     pool = []
     rs = np.random.default_rng(rank)
     n_bags = cfg.batch * cfg.n_slots
@@ -418,7 +419,7 @@ def main():
     full = None
     if full_batch > cfg.batch:
         cfg_f = W.Config(**{**cfg.__dict__, "batch": full_batch})
-        step_f = TrainStep(ctx, tables, cfg_f, rank, world, use_graph=not args.no_graph, pipeline=not args.no_pipeline)
+        step_f = TrainStep(ctx, tables, cfg_f, rank, world, use_graph=not args.no_graph, pipeline=args.pipeline)
         gen_f = W.BatchGen(cfg_f)
         pool_f = [step_f.stage_batch(*gen_f.batch(5000 + s)[:2]) for s in range(2)]
         dout_f = torch.from_numpy((rs.standard_normal((full_batch * cfg.n_slots, cfg.dim)) * 0.01)

@@ -78,12 +78,6 @@ struct BwdArgs {
   uint32_t* touched;                // kOptGrad: row -> 1 when its gradient was written
   uint32_t tma_rows;                // rows per warp buffer in short_tma
   uint32_t n_slots;                 // one-hot: occurrence i = sample * n_slots + slot
-  // Entry-indexed short segments (flat dedup): the count kernel drops an occurrence of rank r
-  // < 32 straight into short_bag[entry * 32 + r] and lists every row's leader (rank 0) here;
-  // the short reduce reads {row, entry * 32, count, entry} from the list + the batch table.
-  uint32_t* lead_ent;               // leader list: batch-table entry (nullptr: CSR records)
-  uint32_t* lead_row;               // leader list: the row
-  uint32_t* lead_bag;               // leader list: the leader's own bag (a singleton needs no other)
   float* W;
   float* S0;
   float* S1;
@@ -520,115 +514,6 @@ struct PlaceOp {
   __device__ void total(uint64_t t) const { *a.long_occ = t; }
 };
 
-// ---- flat dedup, entry-indexed short segments ------------------------------------------------
-// k_count_lead: k_count_flat + an occurrence of rank r < 32 drops its bag at
-// short_bag[entry * 32 + r], and each row's leader (rank 0) joins the leader list (one atomic
-// per block on the packed short allocator). The short reduce can start right after it: the
-// allocation and placement below serve only the long segments (> 32 occurrences).
-__global__ void __launch_bounds__(256) k_count_lead(BwdArgs a) {
-  __shared__ uint32_t s_wn[8];
-  __shared__ uint32_t s_base;
-  pdl_wait();
-  pdl_launch_dependents();
-  trace_begin(kTrCount);
-  const uint64_t n = a.counts[0];
-  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 1;  // (as k_dedup)
-  if (blockIdx.x * uint64_t(blockDim.x) >= n) return;
-  const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  uint64_t i = j;  // one-hot: slot-major walk (see k_count_flat)
-  if (!a.occ_bag && a.n_slots > 1 && n % a.n_slots == 0) {
-    const uint64_t ns = n / a.n_slots;
-    i = (j % ns) * a.n_slots + j / ns;
-  }
-  const uint32_t row = j < n ? a.occ_row[i] : a.row_absent;
-  const bool active = row != a.row_absent;
-  const uint32_t peers = __match_any_sync(0xffffffffu, row);
-  const int leader = __ffs(peers) - 1;
-  uint32_t e = 0, base = 0;
-  if (active && static_cast<int>(lane_id()) == leader) {
-    e = bt_insert(a.bt, a.bt_mask, row);
-    base = atomicAdd(&a.bt[e].y, static_cast<uint32_t>(__popc(peers))) + 1u;
-  }
-  e = __shfl_sync(0xffffffffu, e, leader);
-  base = __shfl_sync(0xffffffffu, base, leader);
-  const uint32_t rank = base + __popc(peers & lanemask_lt());
-  if (active) {
-    a.occ_ent[i] = e;
-    if (rank < kChunk) a.short_bag[e * kChunk + rank] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
-  }
-  const bool lead = active && rank == 0u;
-  const uint32_t lm = __ballot_sync(0xffffffffu, lead);
-  const uint32_t w = threadIdx.x >> 5;
-  if (lane_id() == 0) s_wn[w] = __popc(lm);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t tot = 0;
-    for (int q = 0; q < 8; ++q) {
-      const uint32_t c = s_wn[q];
-      s_wn[q] = tot;
-      tot += c;
-    }
-    s_base = tot ? static_cast<uint32_t>(atomicAdd(a.short_alloc, static_cast<unsigned long long>(tot) << 32) >> 32) : 0u;
-  }
-  __syncthreads();
-  if (lead) {
-    const uint32_t u = s_base + s_wn[w] + __popc(lm & lanemask_lt());
-    a.lead_ent[u] = e;
-    a.lead_row[u] = row;
-    a.lead_bag[u] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
-  }
-  trace_end(kTrCount);
-}
-
-// Long ids for the leaders whose rows have > 32 occurrences (the count is final now).
-__global__ void __launch_bounds__(256) k_alloc_long(BwdArgs a) {
-  pdl_wait();
-  pdl_launch_dependents();
-  trace_begin(kTrAlloc);
-  const uint64_t S = *a.short_alloc >> 32;
-  const uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
-  if (blockIdx.x * uint64_t(blockDim.x) >= S) return;
-  uint32_t e = 0, len = 0;
-  if (u < S) {
-    e = a.lead_ent[u];
-    len = __ldcg(&a.bt[e].y) + 1u;  // a short entry may already be reset by the short reduce: 0
-  }
-  const bool lg = u < S && len > kChunk && len != 0u;
-  const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
-  if (lg_mask) {
-    const int src = __ffs(lg_mask) - 1;
-    uint32_t j0 = 0;
-    if (static_cast<int>(lane_id()) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
-    j0 = __shfl_sync(0xffffffffu, j0, src);
-    if (lg) {
-      const uint32_t jj = j0 + __popc(lg_mask & lanemask_lt());
-      a.long_row[jj] = a.lead_row[u];
-      a.long_ent[jj] = e;
-      a.long_len[jj] = len;
-      a.bt[e].y = kLongFlag | jj;
-    }
-  }
-  trace_end(kTrAlloc);
-}
-
-// Canonical compaction of the long segments' occurrences (the short ones are placed already).
-struct PlaceLongOp {
-  static constexpr int kTrace = kTrPlace;
-  BwdArgs a;
-  __device__ uint64_t size() const { return a.counts[0]; }
-  __device__ uint64_t count(uint64_t i) const {
-    if (a.occ_row[i] == a.row_absent) return 0;
-    const uint32_t y = __ldcg(&a.bt[a.occ_ent[i]].y);
-    return (y != 0xffffffffu && (y & kLongFlag)) ? 1 : 0;  // (a short entry the reduce reset: all ones)
-  }
-  __device__ void emit(uint64_t i, uint64_t excl, uint64_t c) const {
-    if (!c) return;
-    a.lkey[excl] = __ldcg(&a.bt[a.occ_ent[i]].y) & ~kLongFlag;
-    a.lval[excl] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
-  }
-  __device__ void total(uint64_t t) const { *a.long_occ = t; }
-};
-
 // ---- long segments: registration ---------------------------------------------------------
 // Nodes above level 1 of a long segment's 32-ary tree (m level-1 chunks).
 __device__ __forceinline__ uint32_t higher_nodes(uint32_t m) {
@@ -659,8 +544,7 @@ struct LongRegOp {
   }
   __device__ void total(uint64_t t) const {
     *a.long_chunks = t >> 32;
-    // (leader-list mode: the leaders already include the long rows)
-    const_cast<uint64_t*>(a.counts)[1] = (*a.short_alloc >> 32) + (a.lead_ent ? 0u : *a.n_long);
+    const_cast<uint64_t*>(a.counts)[1] = (*a.short_alloc >> 32) + *a.n_long;
   }
 };
 
@@ -717,27 +601,11 @@ __device__ __forceinline__ void prefetch_short_bags(const BwdArgs& a, uint64_t S
 
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// Short segment u: {row, first bag position in short_bag, length, batch-table entry}; a long
-// row's leader (or an entry already reset) reads as an empty segment.
-__device__ __forceinline__ uint4 short_rec_at(const BwdArgs& a, uint64_t u) {
-  if (!a.lead_ent) return a.short_rec[u];
-  const uint32_t e = a.lead_ent[u];
-  const uint32_t len = __ldcg(&a.bt[e].y) + 1u;  // count; kLongFlag | id or empty -> not short
-  return (len >= 1u && len <= kChunk) ? make_uint4(a.lead_row[u], e * kChunk, len, e) : make_uint4(0, 0, 0, 0);
-}
-
-// sbag receives the 32 segments' bags (<= 32 * kChunk entries), each segment sorted; returns
-// this lane's segment offset in sbag.
+// Returns this lane's segment offset in sbag; sbag receives the 32 segments' contiguous bag
+// range (<= 32 * kChunk entries), each segment sorted.
 __device__ __forceinline__ uint32_t stage_short_bags(const BwdArgs& a, uint64_t S, uint64_t u0, uint32_t first,
                                                      uint32_t len, uint32_t* sbag) {
   const uint32_t lane = lane_id();
-  if (a.lead_ent) {  // entry-indexed: every lane copies its own segment (one 128-B line)
-    const uint32_t off = warp_incl_scan(len) - len;
-    for (uint32_t q = 0; q < len; ++q) sbag[off + q] = a.short_bag[first + q];
-    __syncwarp();
-    sort_short_bags(off, len, 0, sbag);
-    return off;
-  }
   const uint32_t last = static_cast<uint32_t>(min(uint64_t(31), S - 1 - u0));
   const uint32_t r0 = __shfl_sync(0xffffffffu, first, 0);
   const uint32_t r1 = __shfl_sync(0xffffffffu, first + len, last);
@@ -858,7 +726,7 @@ __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint6
     uint32_t first = 0, len = 0, row = 0, b0 = 0, b1 = 0, slot = 0;
     float f0 = 1.f, f1 = 1.f;
     if (u < S) {
-      const uint4 rec = short_rec_at(a, u);
+      const uint4 rec = a.short_rec[u];
       row = rec.x;
       first = rec.y;
       len = rec.z;
@@ -1137,10 +1005,10 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
   const uint64_t S = *a.short_alloc >> 32;
   for (uint64_t u0 = warp * 32; u0 < S; u0 += n_warps * 32) {
     uint4 rec = make_uint4(0, 0, 0, 0);
-    if (u0 + lane < S) rec = short_rec_at(a, u0 + lane);
+    if (u0 + lane < S) rec = a.short_rec[u0 + lane];
     const uint32_t row = rec.x, first = rec.y, len = rec.z, slot = rec.w;
     if (len) a.bt[slot] = make_uint2(kBtEmpty, 0xffffffffu);  // placement (previous kernels) is done with it
-    uint32_t bag0 = len ? (a.lead_bag ? a.lead_bag[u0 + lane] : a.short_bag[first]) : 0u;
+    uint32_t bag0 = len ? a.short_bag[first] : 0u;
     const uint32_t c = len ? HDR + len : 0u;
     const uint32_t incl = warp_incl_scan(c), excl = incl - c;
     uint32_t done = 0;  // lanes (segments) already streamed
@@ -1458,18 +1326,16 @@ __global__ void k_copy_counted(const uint32_t* __restrict__ src, const uint64_t*
 __global__ void k_unique_count(const unsigned long long* short_alloc, const uint32_t* n_long, uint64_t* count_out) {
   pdl_wait();
   pdl_launch_dependents();
-  // (n_long == nullptr: leader-list mode, the leaders already include the long rows)
-  if (threadIdx.x == 0) *count_out = (*short_alloc >> 32) + (n_long ? *n_long : 0u);
+  if (threadIdx.x == 0) *count_out = (*short_alloc >> 32) + *n_long;
 }
 
 // Rows updated by the last backward (short + long segments), unsorted; count -> *count_out.
-// lead_row != nullptr: leader-list mode (every row's leader, long rows included).
-__global__ void k_unique_rows(const uint4* short_rec, const uint32_t* lead_row, const unsigned long long* short_alloc,
-                              const uint32_t* long_row, const uint32_t* n_long, uint32_t* out, uint64_t* count_out) {
-  const uint64_t S = *short_alloc >> 32, L = lead_row ? 0u : *n_long;
+__global__ void k_unique_rows(const uint4* short_rec, const unsigned long long* short_alloc, const uint32_t* long_row,
+                              const uint32_t* n_long, uint32_t* out, uint64_t* count_out) {
+  const uint64_t S = *short_alloc >> 32, L = *n_long;
   if (blockIdx.x == 0 && threadIdx.x == 0) *count_out = S + L;
   for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < S + L; u += uint64_t(gridDim.x) * blockDim.x)
-    out[u] = lead_row ? lead_row[u] : (u < S ? short_rec[u].x : long_row[u - S]);
+    out[u] = u < S ? short_rec[u].x : long_row[u - S];
 }
 
 // Short segments on `st` (main), long segments on `side` — disjoint rows, run side by side.
@@ -1561,12 +1427,6 @@ BwdArgs base_args(hps_gpu_table t) {
   a.bag_len = (t->last_multi && t->last_combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
   a.dim = t->dim;
   a.n_slots = t->n_slots;
-  if (t->lead_mode) {  // flat dedup: entry-indexed short segments
-    a.lead_ent = t->ws_lead_ent;
-    a.lead_row = t->ws_lead_row;
-    a.lead_bag = t->ws_lead_bag;
-    a.short_bag = t->ws_bagarr;
-  }
   a.long_base = t->ws_long_base;
   a.task_long = t->ws_task_long;
   a.partial = t->ws_partial;
@@ -1586,7 +1446,6 @@ cudaError_t dedup_attributes() {
     if (cudaError_t e = cudaFuncSetAttribute(k_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4))
       return e;
     for (cudaError_t e : {prefer_max_smem(k_dedup), prefer_max_smem(k_count_flat), prefer_max_smem(k_alloc_flat),
-                          prefer_max_smem(k_count_lead), prefer_max_smem(k_alloc_long), prefer_max_smem(k_scan<PlaceLongOp>),
                           prefer_max_smem(k_scan<PlaceOp>), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass),
                           prefer_max_smem(k_scan<LongRegOp>), prefer_max_smem(k_long_tasks)})
       if (e) return e;
@@ -1619,17 +1478,7 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
     const char* e = std::getenv("HPS_GPU_DEDUP");  // A/B knob: "flat" (default) or "persistent"
     return !(e && std::strcmp(e, "persistent") == 0);
   }();
-  if (t->lead_mode) {
-    // count + entry-indexed short placement + leader list: the short reduce may start after it
-    HPSG_CUDA(dedup_attributes());
-    const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(nk));
-    HPSG_CUDA(launch_k(false, k_count_lead, grid_for(nk, 256, 1 << 30), 256, 0, st, a));
-    if (st == t->side) HPSG_CUDA(cudaEventRecord(t->ev_join, st));
-    HPSG_CUDA(launch_k(pdl, k_alloc_long, grid_for(nk, 256, 1 << 30), 256, 0, st, a));
-    uint64_t* status = reinterpret_cast<uint64_t*>(z + zl.place);
-    HPSG_CUDA(launch_k(pdl, k_scan<PlaceLongOp>, static_cast<unsigned>(tiles), kScanBlock, 0, st, PlaceLongOp{a},
-                       status, reinterpret_cast<uint32_t*>(status + tiles)));
-  } else if (flat) {
+  if (flat) {
     HPSG_CUDA(dedup_attributes());
     const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(nk));
     HPSG_CUDA(launch_k(false, k_count_flat, grid_for(nk, 256, 1 << 30), 256, 0, st, a));
@@ -1654,7 +1503,7 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
   }
   // the short segments are complete: the short reduce may start (backward_update joins here);
   // the long segments' sort and registration continue on this stream
-  if (st == t->side && !t->lead_mode) HPSG_CUDA(cudaEventRecord(t->ev_join, st));
+  if (st == t->side) HPSG_CUDA(cudaEventRecord(t->ev_join, st));
   // K4c: stable sort of the long list by segment id (canonical order within each segment)
   {
     const int passes = bwd_long_passes(nk);
@@ -1750,7 +1599,6 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   int s = HPS_GPU_OK;
   int red_mode = 2;  // 0 register path, 1 bulk-copy waves, 2 register-pipelined row stream
   if (const char* e = std::getenv("HPS_GPU_RED_MODE")) red_mode = std::atoi(e);  // A/B knob
-  if (t->lead_mode) red_mode = 2;  // (the bulk-copy waves assume CSR-contiguous bags)
   if (tma && red_mode == 2) {
     const bool two = nvec > 32;
     auto pipe = [&](auto opt_tag) -> int {
@@ -1929,11 +1777,11 @@ int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* un
   const BwdArgs a = base_args(t);
   if (!unique_rows_out) {  // the count alone (the end-to-end step's result): one thread
     HPSG_CUDA(launch_k(true, k_unique_count, 1, 32, 0, st, static_cast<const unsigned long long*>(a.short_alloc),
-                       static_cast<const uint32_t*>(a.lead_ent ? nullptr : a.n_long), count_out));
+                       static_cast<const uint32_t*>(a.n_long), count_out));
     return HPS_GPU_OK;
   }
   // unsorted rows into the (now free) long-list buffers, then an ascending radix sort
-  k_unique_rows<<<grid_for(nk, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_short_rec, a.lead_row, a.short_alloc, t->ws_long_row,
+  k_unique_rows<<<grid_for(nk, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_short_rec, a.short_alloc, t->ws_long_row,
                                                                a.n_long, t->ws_lkey_a, count_out);
   HPSG_CHECK_LAUNCH("k_unique_rows");
   if (!unique_rows_out) return HPS_GPU_OK;

@@ -1039,12 +1039,6 @@ int alloc_batch_slot(hps_gpu_table t, BatchSlot& b) {
   A(dalloc(&b.ws_ins_pos, N));
   A(dalloc(&b.ws_ins_flag, N));
   A(dalloc(&b.ws_ins_scan, scan_tiles(N) + 1));
-  if (t->lead_mode) {
-    A(dalloc(&b.ws_bagarr, (t->bt_mask + 1) * kChunk));
-    A(dalloc(&b.ws_lead_ent, N));
-    A(dalloc(&b.ws_lead_row, N));
-    A(dalloc(&b.ws_lead_bag, N));
-  }
   if (st) return st;
   cudaStream_t s = t->ctx->stream;
   HPSG_CUDA(cudaMemsetAsync(b.ws_counts, 0, 8 * sizeof(uint64_t), s));
@@ -1069,8 +1063,7 @@ void free_batch_slot(BatchSlot& b) {
                   b.ws_long_start, b.ws_lkey_a,   b.ws_lval_a,    b.ws_lkey_b,     b.ws_lval_b,     b.ws_long_base,
                   b.ws_task_long, b.ws_partial2,  b.ws_long_hbase, b.ws_node_cnt,  b.ws_partial,    b.ws_counts,
                   b.ws_zero,      b.ws_abort,     b.ws_keys_stage, b.ws_offsets_stage, b.ws_ins_slot, b.ws_ins_pos,
-                  b.ws_ins_flag,  b.ws_ins_scan,  b.ws_bagarr,    b.ws_lead_ent,   b.ws_lead_row,
-                  b.ws_lead_bag};
+                  b.ws_ins_flag,  b.ws_ins_scan};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : {b.ev_fork, b.ev_join, b.ev_bwd, b.ev_done, b.ev_join2, b.ev_pre, b.ev_probe})
@@ -1124,7 +1117,6 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->max_bags = cfg->max_batch_bags;
   if (const char* e = std::getenv("HPS_GPU_NO_TMA")) t->no_tma = e[0] == '1';
   if (const char* e = std::getenv("HPS_GPU_NO_FORK")) t->no_fork = e[0] == '1';
-  if (const char* e = std::getenv("HPS_GPU_DEDUP")) t->lead_mode = std::strcmp(e, "lead") == 0;  // A/B knob
   uint64_t rows = 0, slots = 0;
   for (uint32_t i = 0; i < t->n_tables; ++i) {
     const uint64_t cap = cfg->row_capacity_host[i];

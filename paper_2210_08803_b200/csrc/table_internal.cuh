@@ -96,11 +96,6 @@ struct BatchSlot {
   uint32_t* ws_ins_pos = nullptr;
   uint8_t* ws_ins_flag = nullptr;
   uint64_t* ws_ins_scan = nullptr;
-  // flat dedup (lead_mode): entry-indexed short-segment bags [bt entries x 32] + leader list
-  uint32_t* ws_bagarr = nullptr;
-  uint32_t* ws_lead_ent = nullptr;
-  uint32_t* ws_lead_row = nullptr;
-  uint32_t* ws_lead_bag = nullptr;
   // last training lookup recorded in this slot
   bool have_train = false, last_multi = false;
   bool counts_dirty = false;  // batch-table counters hold a training record no backward has consumed
@@ -153,7 +148,6 @@ struct hps_gpu_table_s : BatchSlot {
   uint32_t cur = 0;
   cudaEvent_t ev_last_dedup = nullptr;  // the last k_dedup launched (prefetches serialise on it)
   bool last_dedup_valid = false;
-  bool lead_mode = true;     // flat dedup with entry-indexed short segments (HPS_GPU_DEDUP=lead, default)
   bool graphs_seen = false;  // a training record was captured into a graph (host slot flags may lag replays)
   unsigned long long last_dedup_capture = 0;
   bool no_fork = false;         // HPS_GPU_NO_FORK=1: everything on the main stream (A/B measurement)

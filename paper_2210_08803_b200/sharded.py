@@ -153,7 +153,7 @@ class TrainStep:
     def __init__(self, ctx: Context, table: Optional[EmbeddingTableGroup], cfg: W.Config, rank: int = 0,
                  world: int = 1, use_graph: bool = True, owned: Optional[List[List[int]]] = None,
                  hybrid_hot: Optional[EmbeddingTableGroup] = None, force_exchange: bool = False,
-                 pipeline: bool = True):
+                 pipeline: bool = False):
         """owned (world > 1): localized placement, owned[g] = slots of rank g (localized_plan);
         None = distributed placement."""
         self.ctx, self.table, self.cfg, self.rank, self.world = ctx, table, cfg, rank, world
