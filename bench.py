@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg5"])
     ap.add_argument("--batch-per-gpu", type=int, default=None)
-    ap.add_argument("--placement", default="auto", choices=["auto", "distributed", "localized", "hybrid"],
+    ap.add_argument("--placement", default="auto",
+                    choices=["auto", "distributed", "distributed-py", "localized", "hybrid"],
                     help="multi-GPU slot placement (auto: localized for cfg3, distributed otherwise)")
     ap.add_argument("--hot-budget-gb", type=float, default=0.0625, help="hybrid: replicated hot rows per GPU")
     ap.add_argument("--force-exchange", action="store_true",
@@ -324,7 +325,7 @@ def main():
         tables = build_tables_localized(ctx, cfg, owned, rank, world)
     gen = W.BatchGen(cfg)
     step_fn = TrainStep(ctx, tables, cfg, rank, world, use_graph=not args.no_graph, owned=owned, hybrid_hot=hot,
-                        force_exchange=xchg, pipeline=args.pipeline)
+                        force_exchange=xchg, pipeline=args.pipeline, cabi=placement != "distributed-py")
     pool = []
     rs = np.random.default_rng(rank)
     n_bags = cfg.batch * cfg.n_slots

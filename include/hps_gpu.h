@@ -58,7 +58,8 @@ enum {
   HPS_GPU_E_CUDA = 256,
   HPS_GPU_E_OUT_OF_MEMORY = 257,
   HPS_GPU_E_NO_DEVICE = 258,
-  HPS_GPU_E_NOT_CAPTURABLE = 259
+  HPS_GPU_E_NOT_CAPTURABLE = 259,
+  HPS_GPU_E_NCCL = 260             /* an NCCL call of the sharded path failed */
 };
 
 /* Human readable name of a status ("OK", "InvalidArgument", ..., "CudaError"). */
@@ -290,6 +291,51 @@ int hps_gpu_sum_partials(hps_gpu_ctx ctx, const float* parts, const uint32_t* to
 int hps_gpu_backward_reduce(hps_gpu_table tbl, const float* d_out, float* grads_out, uint32_t* touched_out);
 /* Optimizer step for every global row r with touched[r], gradient grads[r x dim]. */
 int hps_gpu_apply_grads(hps_gpu_table tbl, const float* grads, const uint32_t* touched, const hps_opt_params* opt);
+
+/* ---- sharded step over NCCL (sharded.cu): distributed slot placement ---------------
+ * SPEC.md:470, 487-491 (partition_of placement), PAPER.md:173-177, 188 (model-parallel
+ * embedding, all-to-all over NVLink). The context joins an NCCL communicator (rank 0 makes
+ * the id with hps_gpu_nccl_unique_id and ships it out of band — MPI, torch.distributed, a
+ * file); a hps_gpu_dist is this rank's half of every step: the requester's bucketize +
+ * pack into fixed-capacity per-peer regions, one grouped all-to-all of keys + table ids,
+ * the owner's gather of its shard (`shard`, a table group holding the keys with
+ * partition_of(key, world) == rank of every table), rows back, pooling; the backward sends
+ * per-occurrence gradients to the owners, whose ordinary backward_update applies them. No
+ * host synchronisation: a whole step is capturable into one CUDA graph. Results are
+ * bit-identical to one table over the concatenated global batch (rank-major order).
+ * Region capacity C = min(max_keys, ceil(f * max_keys / world) + 1024) occurrences per peer
+ * (hps_gpu_dist_capacity); the shard must be created with max_batch_keys and
+ * max_batch_bags >= world * C. A step whose occurrences for one owner exceed C latches
+ * Infeasible (its results are then unspecified). */
+#define HPS_NCCL_ID_BYTES 128
+int hps_gpu_nccl_unique_id(void* id_out /* HPS_NCCL_ID_BYTES */);
+int hps_gpu_ctx_comm_init(hps_gpu_ctx ctx, const void* id /* HPS_NCCL_ID_BYTES */, int rank, int world);
+
+typedef struct hps_gpu_dist_s* hps_gpu_dist;
+typedef struct {
+  uint32_t n_slots;
+  const uint32_t* slot_table_host;  /* [n_slots] table id of each slot (table ids of the shard group) */
+  uint32_t dim;
+  uint64_t max_keys;                /* key occurrences per rank per step (requester side) */
+  uint64_t max_bags;                /* bags per rank per step */
+  float capacity_factor;            /* f above; 0 -> 1.25 */
+} hps_dist_config;
+int hps_gpu_dist_create(hps_gpu_ctx ctx, hps_gpu_table shard, const hps_dist_config* cfg_host, hps_gpu_dist* out_host);
+int hps_gpu_dist_destroy(hps_gpu_dist dist);
+int hps_gpu_dist_capacity(hps_gpu_dist dist, uint64_t* per_peer_host);
+/* Forward of this rank's batch: keys in bag order, offsets == NULL for one key per bag
+ * (else device CSR offsets and n_keys = offsets[n_bags], known to the caller); flags:
+ * HPS_LOOKUP_TRAIN, HPS_LOOKUP_INSERT (dynamic single-table shards). out: [n_bags x dim]. */
+int hps_gpu_dist_forward(hps_gpu_dist dist, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,
+                         uint64_t n_keys, int combiner, float* out, uint32_t flags);
+/* Backward of the last training forward: d_out [n_bags x dim]; every owner updates its rows. */
+int hps_gpu_dist_backward(hps_gpu_dist dist, const float* d_out, const hps_opt_params* opt_host);
+/* Loopback transport (tests, single-GPU bring-up): n ranks of ONE process on one device,
+ * the all-to-alls done as device copies between their buffers. Rank r's calls must run on
+ * their own host thread (every all-to-all is a rendezvous of the n ranks); ctxs[r] should
+ * have distinct streams. Same kernels, regions and ordering as the NCCL path. */
+int hps_gpu_dist_create_loopback(const hps_gpu_ctx* ctxs, const hps_gpu_table* shards, const hps_dist_config* cfg_host,
+                                 uint32_t n, hps_gpu_dist* outs_host);
 
 /* ---- HPS inference cache (K6..K8), SPEC.md:112-190 ---------------------------- */
 typedef struct hps_gpu_cache_s* hps_gpu_cache;

@@ -6,6 +6,6 @@ include/hps_gpu.h). This package is its Python host mirror: ctypes binding
 orchestration (sharded) and the synthetic workload generators (workload).
 """
 from ._lib import HpsError, load  # noqa: F401
-from .api import Context, EmbeddingTableGroup, HotCache, opt_params  # noqa: F401
+from .api import Context, DistTable, EmbeddingTableGroup, HotCache, opt_params  # noqa: F401
 
-__all__ = ["Context", "EmbeddingTableGroup", "HotCache", "HpsError", "load", "opt_params"]
+__all__ = ["Context", "DistTable", "EmbeddingTableGroup", "HotCache", "HpsError", "load", "opt_params"]

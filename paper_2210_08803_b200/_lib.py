@@ -107,6 +107,14 @@ class SlotSpec(C.Structure):
     _fields_ = [("vocab_size", u64), ("dim", u32), ("hotness", u32)]
 
 
+class DistConfig(C.Structure):
+    _fields_ = [("n_slots", u32), ("slot_table_host", C.POINTER(u32)), ("dim", u32), ("max_keys", u64),
+                ("max_bags", u64), ("capacity_factor", f32)]
+
+
+NCCL_ID_BYTES = 128
+
+
 # name -> (restype, argtypes): every symbol include/hps_gpu.h declares.
 SIGNATURES = {
     "hps_gpu_status_string": (C.c_char_p, [i32]),
@@ -130,6 +138,13 @@ SIGNATURES = {
     "hps_gpu_lookup_pooled": (i32, [vp, vp, vp, u32, i32, vp, u32]),
     "hps_gpu_backward_update": (i32, [vp, vp, C.POINTER(OptParams)]),
     "hps_gpu_table_set_pipeline": (i32, [vp, u32]),
+    "hps_gpu_nccl_unique_id": (i32, [vp]),
+    "hps_gpu_ctx_comm_init": (i32, [vp, vp, i32, i32]),
+    "hps_gpu_dist_create": (i32, [vp, vp, C.POINTER(DistConfig), C.POINTER(vp)]),
+    "hps_gpu_dist_destroy": (i32, [vp]),
+    "hps_gpu_dist_capacity": (i32, [vp, C.POINTER(u64)]),
+    "hps_gpu_dist_forward": (i32, [vp, vp, vp, u32, u64, i32, vp, u32]),
+    "hps_gpu_dist_backward": (i32, [vp, vp, C.POINTER(OptParams)]),
     "hps_gpu_table_prefetch": (i32, [vp, u32, vp, vp, u32, i32, u32]),
     "hps_gpu_table_join_prefetch": (i32, [vp]),
     "hps_gpu_table_last_unique": (i32, [vp, vp, vp]),

@@ -71,6 +71,17 @@ class Context:
         L.check(self.lib.hps_gpu_has_non_finite_f32(self.h, _ptr(x), x.numel(), _ptr(flag)), "has_non_finite")
         return bool(flag.item())
 
+    # -- NCCL communicator of the sharded C-ABI path (sharded.cu) --------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(L.NCCL_ID_BYTES)
+        L.check(L.load().hps_gpu_nccl_unique_id(buf), "nccl_unique_id")
+        return buf.raw
+
+    def comm_init(self, unique_id: bytes, rank: int, world: int) -> None:
+        buf = C.create_string_buffer(bytes(unique_id), L.NCCL_ID_BYTES)
+        L.check(self.lib.hps_gpu_ctx_comm_init(self.h, buf, rank, world), "ctx_comm_init")
+
     def gen_keys(self, seed: int, first: int, n: int) -> torch.Tensor:
         out = torch.empty(n, dtype=torch.int64, device=f"cuda:{self.device}")
         L.check(self.lib.hps_gpu_gen_keys(self.h, seed, first, n, _ptr(out)), "gen_keys")
@@ -420,3 +431,49 @@ class CachedLookup:
                 ctx.set_stream(cur)
         self._graphs[n] = g
         return self.out[:n]
+
+
+class DistTable:
+    """hps_gpu_dist: this rank's half of a distributed-slot step over the context's NCCL
+    communicator: fixed-capacity per-peer all-to-alls, no host sync."""
+
+    def __init__(self, ctx: Context, shard: EmbeddingTableGroup, slot_table: Sequence[int], max_keys: int,
+                 max_bags: int, capacity_factor: float = 0.0):
+        self.ctx, self.shard, self.lib = ctx, shard, ctx.lib
+        self.n_slots, self.dim = len(slot_table), shard.dim
+        self._st = (C.c_uint32 * self.n_slots)(*slot_table)
+        cfg = L.DistConfig(self.n_slots, C.cast(self._st, C.POINTER(C.c_uint32)), shard.dim, max_keys, max_bags,
+                           capacity_factor)
+        h = C.c_void_p()
+        L.check(self.lib.hps_gpu_dist_create(ctx.h, shard.h, C.byref(cfg), C.byref(h)), "dist_create")
+        self.h = h
+        cap = C.c_uint64(0)
+        L.check(self.lib.hps_gpu_dist_capacity(self.h, C.byref(cap)), "dist_capacity")
+        self.capacity = int(cap.value)
+
+    def forward(self, keys: torch.Tensor, n_samples: int, offsets: Optional[torch.Tensor] = None,
+                combiner: str = "sum", train: bool = True, insert_missing: bool = False,
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        _need_cuda(keys, "keys")
+        n_bags = n_samples * self.n_slots
+        if out is None:
+            out = torch.empty(n_bags, self.dim, dtype=torch.float32, device=keys.device)
+        flags = (L.LOOKUP_TRAIN if train else 0) | (L.LOOKUP_INSERT if insert_missing else 0)
+        L.check(self.lib.hps_gpu_dist_forward(self.h, _ptr(keys), _ptr(offsets), n_samples, keys.numel(),
+                                              _COMB[combiner], _ptr(out), flags), "dist_forward")
+        return out
+
+    def backward(self, d_out: torch.Tensor, params: L.OptParams) -> None:
+        _need_cuda(d_out, "d_out")
+        L.check(self.lib.hps_gpu_dist_backward(self.h, _ptr(d_out), C.byref(params)), "dist_backward")
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.hps_gpu_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -340,4 +340,9 @@ struct hps_gpu_ctx_s {
   uint32_t* h_status = nullptr;  // pinned mirror for sync
   bool pdl = true;               // programmatic dependent launch in the step chains (HPS_GPU_NO_PDL=1 disables)
   int num_sms = hpsg::kNumSMs;   // multiProcessorCount of the device (the persistent dedup's grid cap)
+  void* nccl = nullptr;          // ncclComm_t of the sharded path (hps_gpu_ctx_comm_init; sharded.cu)
+  int rank = 0, world = 1;
 };
+namespace hpsg {
+void comm_destroy(hps_gpu_ctx_s* ctx);  // sharded.cu
+}

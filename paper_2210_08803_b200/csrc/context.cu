@@ -105,6 +105,7 @@ const char* hps_gpu_status_string(int status) {
     case HPS_GPU_E_OUT_OF_MEMORY: return "OutOfMemory";
     case HPS_GPU_E_NO_DEVICE: return "NoDevice";
     case HPS_GPU_E_NOT_CAPTURABLE: return "NotCapturable";
+    case HPS_GPU_E_NCCL: return "Nccl";
     default: return "Unknown";
   }
 }
@@ -143,6 +144,7 @@ int hps_gpu_ctx_create(int device, void* stream, hps_gpu_ctx* out) {
 
 int hps_gpu_ctx_destroy(hps_gpu_ctx ctx) {
   if (!ctx) return HPS_GPU_OK;
+  hpsg::comm_destroy(ctx);
   cudaFree(ctx->d_status);
   cudaFreeHost(ctx->h_status);
   delete ctx;

@@ -1,0 +1,378 @@
+// sharded.cu — distributed slot placement behind the C-ABI: one training step of a table
+// group sharded over the ranks of an NCCL communicator, with no host round trip.
+//
+// Placement: key k is owned by rank
+// partition_of(k, G) (proj/include/hps/hash.hpp:52-54); every rank holds that shard of every
+// table (a table group created by the caller). One step, all on the context's stream:
+//
+//   requester  bucketize the occurrences by owner, stably (exchange.cu xplan)
+//              pack them into FIXED-capacity per-peer regions [G x C] (keys, table ids);
+//              empty slots carry table id UINT32_MAX
+//   NCCL       one grouped all-to-all: keys + table ids (2 x C per peer)
+//   owner      gather the rows of all G x C received slots (training record; empty slots
+//              read as absent keys: no row, no gradient)
+//   NCCL       rows back (C x dim per peer)
+//   requester  pool bags straight from the received rows (perm: occurrence -> slot)
+//   backward   requester scatters per-occurrence gradients into the same slots; NCCL;
+//              the owner's ordinary backward (dedup + blocked reduction + optimizer)
+//
+// Fixed capacity instead of exact sizes: the per-peer counts never travel to the host, so
+// the whole step is one stream of device work — capturable into one CUDA graph with its
+// NCCL nodes. C = min(max_keys, ceil(f * max_keys / G) + 1024): hash placement puts
+// max_keys/G +- sqrt(max_keys/G) occurrences on each owner, so f = 1.25 leaves > 15 sigma
+// at config 2. A batch that overflows a region is refused on the device (latched
+// Infeasible; the step's results are then unspecified) instead of overrunning.
+// Ordering: slot p*C + r holds requester p's r-th occurrence for this owner in requester
+// order, so the owner sees every key's occurrences in global canonical order (ranks in
+// order, each rank's own order): the sharded step is bit-identical to one table over the
+// concatenated global batch. World of one: the regions alias (no copy, no NCCL call).
+#include <nccl.h>
+
+#include <algorithm>
+#include <barrier>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace hpsg;
+
+struct hps_gpu_dist_s {
+  hps_gpu_ctx ctx = nullptr;
+  hps_gpu_table shard = nullptr;
+  hps_gpu_xplan plan = nullptr;
+  uint32_t n_slots = 0, dim = 0, G = 1, rank = 0;
+  uint64_t max_keys = 0, max_bags = 0, C = 0;
+  uint32_t* d_slot_table = nullptr;
+  // requester side
+  uint64_t* dense_keys = nullptr;  // bucketize output (stable by owner)
+  uint32_t* dense_tables = nullptr;
+  uint32_t* dense_perm = nullptr;  // occurrence -> dense send position
+  uint32_t* counts = nullptr;      // per owner
+  uint32_t* occ_bag = nullptr;
+  uint32_t* perm = nullptr;        // occurrence -> slot p*C + r
+  uint64_t* send_keys = nullptr;   // [G x C]
+  uint32_t* send_tables = nullptr;
+  float* rows_back = nullptr;      // [G x C x dim] received rows
+  float* grads_send = nullptr;     // [G x C x dim]
+  // owner side
+  uint64_t* recv_keys = nullptr;
+  uint32_t* recv_tables = nullptr;
+  float* rows_own = nullptr;       // [G x C x dim]
+  float* grads_recv = nullptr;
+  // loopback transport (hps_gpu_dist_create_loopback): ranks of one process on one device
+  std::shared_ptr<struct LoopGroup> loop;
+  cudaEvent_t loop_ev = nullptr;
+  // last forward
+  const uint32_t* last_offsets = nullptr;
+  uint64_t last_bags = 0;
+  int last_combiner = 0;
+  bool have_fwd = false, train = false;
+};
+
+// A group of loopback ranks: the all-to-all is device copies between their buffers, each
+// rank's calls on its own host thread (the test harness of the multi-rank path on one GPU).
+struct LoopGroup {
+  explicit LoopGroup(uint32_t n) : bar(static_cast<std::ptrdiff_t>(n)), members(n, nullptr) {}
+  std::barrier<> bar;
+  std::vector<hps_gpu_dist_s*> members;
+};
+
+namespace {
+
+// Fixed-capacity regions from the dense bucketized order: slot p*C + r <- dense start_p + r
+// (r < count_p), empty slots get table id UINT32_MAX; perm[i] = p*C + (dense_perm[i] - start_p).
+__global__ void k_fix_regions(const uint64_t* __restrict__ dense_keys, const uint32_t* __restrict__ dense_tables,
+                              const uint32_t* __restrict__ dense_perm, const uint32_t* __restrict__ counts, uint32_t G,
+                              uint64_t C, uint64_t n, uint64_t* __restrict__ send_keys,
+                              uint32_t* __restrict__ send_tables, uint32_t* __restrict__ perm, uint32_t* status) {
+  __shared__ uint64_t s_start[257];
+  if (threadIdx.x == 0) {
+    uint64_t run = 0;
+    for (uint32_t p = 0; p < G; ++p) {
+      s_start[p] = run;
+      run += counts[p];
+    }
+    s_start[G] = run;
+  }
+  __syncthreads();
+  const uint64_t total = uint64_t(G) * C;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < total; q += stride) {
+    const uint32_t p = static_cast<uint32_t>(q / C);
+    const uint64_t r = q - uint64_t(p) * C;
+    const uint64_t cnt = s_start[p + 1] - s_start[p];
+    if (r < cnt) {
+      send_keys[q] = dense_keys[s_start[p] + r];
+      send_tables[q] = dense_tables[s_start[p] + r];
+    } else {
+      send_keys[q] = 0;
+      send_tables[q] = 0xffffffffu;
+    }
+    if (r == 0 && cnt > C) latch_status(status, HPS_GPU_E_INFEASIBLE);  // region overflow
+  }
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const uint64_t d = dense_perm[i];
+    uint32_t p = 0;
+    while (p + 1 < G && s_start[p + 1] <= d) ++p;
+    const uint64_t r = d - s_start[p];
+    // an occurrence past its region's capacity (Infeasible is latched: the step's results are
+    // unspecified) is pointed at the region's last slot, so nothing reads or writes out of bounds
+    perm[i] = static_cast<uint32_t>(uint64_t(p) * C + (r < C ? r : C - 1));
+  }
+}
+
+int nccl_status(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return HPS_GPU_OK;
+  set_last_error(std::string(what) + ": " + ncclGetErrorString(r));
+  return HPS_GPU_E_NCCL;
+}
+#define HPSG_NCCL(call)                                  \
+  do {                                                   \
+    ncclResult_t r_ = (call);                            \
+    if (r_ != ncclSuccess) return nccl_status(r_, #call); \
+  } while (0)
+
+// Which buffer pair an all-to-all moves (the loopback transport reads its peers' copies).
+enum Xfer { kXKeys = 0, kXTables = 1, kXRows = 2, kXGrads = 3 };
+const void* send_of(const hps_gpu_dist_s* d, int x) {
+  return x == kXKeys ? static_cast<const void*>(d->send_keys) : x == kXTables ? static_cast<const void*>(d->send_tables)
+         : x == kXRows ? static_cast<const void*>(d->rows_own) : static_cast<const void*>(d->grads_send);
+}
+
+int loop_a2a(hps_gpu_dist d, int x, void* recv, size_t bytes) {
+  cudaStream_t st = d->ctx->stream;
+  HPSG_CUDA(cudaEventRecord(d->loop_ev, st));  // this rank's send buffer is written
+  d->loop->bar.arrive_and_wait();
+  for (uint32_t p = 0; p < d->G; ++p) {
+    const hps_gpu_dist_s* peer = d->loop->members[p];
+    HPSG_CUDA(cudaStreamWaitEvent(st, peer->loop_ev, 0));
+    HPSG_CUDA(cudaMemcpyAsync(static_cast<char*>(recv) + p * bytes,
+                              static_cast<const char*>(send_of(peer, x)) + size_t(d->rank) * bytes, bytes,
+                              cudaMemcpyDeviceToDevice, st));
+  }
+  HPSG_CUDA(cudaStreamSynchronize(st));  // peers may reuse their send buffers after the barrier
+  d->loop->bar.arrive_and_wait();
+  return HPS_GPU_OK;
+}
+
+// All-to-all of G regions of `elems` elements each (region p of send -> rank p's region
+// `rank` of recv). World of one: the caller aliases recv to send.
+int a2a(hps_gpu_dist d, int x, const void* send, void* recv, size_t elem_bytes, uint64_t elems) {
+  if (d->G == 1) return HPS_GPU_OK;
+  if (d->loop) return loop_a2a(d, x, recv, elem_bytes * elems);
+  auto comm = static_cast<ncclComm_t>(d->ctx->nccl);
+  const size_t bytes = elem_bytes * elems;
+  HPSG_NCCL(ncclGroupStart());
+  for (uint32_t p = 0; p < d->G; ++p) {
+    HPSG_NCCL(ncclSend(static_cast<const char*>(send) + p * bytes, bytes, ncclUint8, static_cast<int>(p), comm,
+                       d->ctx->stream));
+    HPSG_NCCL(ncclRecv(static_cast<char*>(recv) + p * bytes, bytes, ncclUint8, static_cast<int>(p), comm,
+                       d->ctx->stream));
+  }
+  HPSG_NCCL(ncclGroupEnd());
+  return HPS_GPU_OK;
+}
+
+template <class T>
+int dalloc_n(T** p, uint64_t n) {
+  if (cudaMalloc(reinterpret_cast<void**>(p), std::max<uint64_t>(n, 1) * sizeof(T)) != cudaSuccess) {
+    cudaGetLastError();
+    return HPS_GPU_E_OUT_OF_MEMORY;
+  }
+  return HPS_GPU_OK;
+}
+
+}  // namespace
+
+void hpsg::comm_destroy(hps_gpu_ctx_s* ctx) {
+  if (ctx && ctx->nccl) {
+    ncclCommDestroy(static_cast<ncclComm_t>(ctx->nccl));
+    ctx->nccl = nullptr;
+  }
+}
+
+extern "C" {
+
+int hps_gpu_nccl_unique_id(void* id_out) {
+  if (!id_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  ncclUniqueId id;
+  HPSG_NCCL(ncclGetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == HPS_NCCL_ID_BYTES, "ncclUniqueId size");
+  std::memcpy(id_out, &id, sizeof(id));
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_ctx_comm_init(hps_gpu_ctx ctx, const void* id, int rank, int world) {
+  if (!ctx || !id || world < 1 || rank < 0 || rank >= world || world > 256) return HPS_GPU_E_INVALID_ARGUMENT;
+  HPSG_CUDA(cudaSetDevice(ctx->device));
+  comm_destroy(ctx);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm = nullptr;
+  HPSG_NCCL(ncclCommInitRank(&comm, world, uid, rank));
+  ctx->nccl = comm;
+  ctx->rank = rank;
+  ctx->world = world;
+  return HPS_GPU_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int dist_create(hps_gpu_ctx ctx, hps_gpu_table shard, const hps_dist_config* cfg, uint32_t G, uint32_t rank,
+                hps_gpu_dist* out) {
+  if (!ctx || !shard || !cfg || !out || cfg->n_slots == 0 || !cfg->slot_table_host || cfg->max_keys == 0 ||
+      cfg->max_keys >= (1ull << 31) || cfg->max_bags == 0 || cfg->dim == 0 || cfg->dim % 4)
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  HPSG_CUDA(cudaSetDevice(ctx->device));
+  auto d = new hps_gpu_dist_s;
+  d->ctx = ctx;
+  d->shard = shard;
+  d->n_slots = cfg->n_slots;
+  d->dim = cfg->dim;
+  d->G = G;
+  d->rank = rank;
+  d->max_keys = cfg->max_keys;
+  d->max_bags = cfg->max_bags;
+  const double f = cfg->capacity_factor > 0.f ? cfg->capacity_factor : 1.25;
+  d->C = d->G == 1 ? d->max_keys
+                   : std::min<uint64_t>(d->max_keys, uint64_t(std::ceil(f * double(d->max_keys) / d->G)) + 1024);
+  const uint64_t GC = uint64_t(d->G) * d->C, D = d->dim, N = d->max_keys;
+  int st = HPS_GPU_OK;
+  auto A = [&](int s) {
+    if (s && !st) st = s;
+  };
+  if (int s = hps_gpu_xplan_create(ctx, N, d->G, &d->plan)) A(s);
+  A(dalloc_n(&d->d_slot_table, d->n_slots));
+  A(dalloc_n(&d->dense_keys, N));
+  A(dalloc_n(&d->dense_tables, N));
+  A(dalloc_n(&d->dense_perm, N));
+  A(dalloc_n(&d->counts, d->G));
+  A(dalloc_n(&d->occ_bag, N));
+  A(dalloc_n(&d->perm, N));
+  A(dalloc_n(&d->send_keys, GC));
+  A(dalloc_n(&d->send_tables, GC));
+  A(dalloc_n(&d->rows_own, GC * D));
+  A(dalloc_n(&d->grads_send, GC * D));
+  if (d->G > 1) {
+    A(dalloc_n(&d->recv_keys, GC));
+    A(dalloc_n(&d->recv_tables, GC));
+    A(dalloc_n(&d->rows_back, GC * D));
+    A(dalloc_n(&d->grads_recv, GC * D));
+  } else {  // a world of one: every region is its own peer's — alias, no copy
+    d->recv_keys = d->send_keys;
+    d->recv_tables = d->send_tables;
+    d->rows_back = d->rows_own;
+    d->grads_recv = d->grads_send;
+  }
+  if (!st && cudaMemcpy(d->d_slot_table, cfg->slot_table_host, d->n_slots * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+    st = HPS_GPU_E_CUDA;
+  if (!st && cudaEventCreateWithFlags(&d->loop_ev, cudaEventDisableTiming) != cudaSuccess) st = HPS_GPU_E_CUDA;
+  if (st) {
+    hps_gpu_dist_destroy(d);
+    return st;
+  }
+  *out = d;
+  return HPS_GPU_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int hps_gpu_dist_create(hps_gpu_ctx ctx, hps_gpu_table shard, const hps_dist_config* cfg, hps_gpu_dist* out) {
+  if (!ctx) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (!ctx->nccl && ctx->world != 1) return HPS_GPU_E_INVALID_ARGUMENT;
+  return dist_create(ctx, shard, cfg, static_cast<uint32_t>(ctx->nccl ? ctx->world : 1),
+                     static_cast<uint32_t>(ctx->nccl ? ctx->rank : 0), out);
+}
+
+int hps_gpu_dist_create_loopback(const hps_gpu_ctx* ctxs, const hps_gpu_table* shards, const hps_dist_config* cfg,
+                                 uint32_t n, hps_gpu_dist* outs) {
+  if (!ctxs || !shards || !outs || n == 0 || n > 256) return HPS_GPU_E_INVALID_ARGUMENT;
+  auto group = std::make_shared<LoopGroup>(n);
+  for (uint32_t r = 0; r < n; ++r) {
+    if (int s = dist_create(ctxs[r], shards[r], cfg, n, r, &outs[r])) {
+      for (uint32_t q = 0; q < r; ++q) hps_gpu_dist_destroy(outs[q]);
+      return s;
+    }
+    outs[r]->loop = group;
+    group->members[r] = outs[r];
+  }
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_dist_destroy(hps_gpu_dist d) {
+  if (!d) return HPS_GPU_OK;
+  if (d->loop_ev) cudaEventDestroy(d->loop_ev);
+  if (d->plan) hps_gpu_xplan_destroy(d->plan);
+  void* own[] = {d->d_slot_table, d->dense_keys, d->dense_tables, d->dense_perm, d->counts, d->occ_bag, d->perm,
+                 d->send_keys,    d->send_tables, d->rows_own,    d->grads_send};
+  for (void* p : own)
+    if (p) cudaFree(p);
+  if (d->G > 1) {
+    void* peer[] = {d->recv_keys, d->recv_tables, d->rows_back, d->grads_recv};
+    for (void* p : peer)
+      if (p) cudaFree(p);
+  }
+  delete d;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_dist_capacity(hps_gpu_dist d, uint64_t* per_peer_out) {
+  if (!d || !per_peer_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  *per_peer_out = d->C;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_dist_forward(hps_gpu_dist d, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,
+                         uint64_t n_keys, int combiner, float* out, uint32_t flags) {
+  if (!d || !out || (combiner != HPS_COMBINER_SUM && combiner != HPS_COMBINER_MEAN)) return HPS_GPU_E_INVALID_ARGUMENT;
+  const uint64_t n_bags = uint64_t(n_samples) * d->n_slots;
+  const bool multi = offsets != nullptr;
+  const uint64_t n = multi ? n_keys : n_bags;
+  if (n_bags > d->max_bags || n > d->max_keys || (n && !keys)) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = d->ctx->stream;
+  const uint64_t GC = uint64_t(d->G) * d->C;
+  if (multi && n_bags)
+    if (int s = hps_gpu_occurrence_bags(d->ctx, offsets, n_bags, d->occ_bag)) return s;
+  if (int s = hps_gpu_xplan_bucketize(d->plan, keys, n, multi ? d->occ_bag : nullptr, d->n_slots, d->d_slot_table,
+                                      d->dense_keys, d->dense_tables, d->dense_perm, d->counts))
+    return s;
+  k_fix_regions<<<grid_for(std::max<uint64_t>(GC, n), 256, kNumSMs * 16), 256, 0, st>>>(
+      d->dense_keys, d->dense_tables, d->dense_perm, d->counts, d->G, d->C, n, d->send_keys, d->send_tables, d->perm,
+      d->ctx->d_status);
+  HPSG_CHECK_LAUNCH("k_fix_regions");
+  if (int s = a2a(d, kXKeys, d->send_keys, d->recv_keys, 8, d->C)) return s;
+  if (int s = a2a(d, kXTables, d->send_tables, d->recv_tables, 4, d->C)) return s;
+  const uint32_t gflags = (flags & HPS_LOOKUP_TRAIN) | (flags & HPS_LOOKUP_INSERT);
+  if (int s = hps_gpu_gather_rows(d->shard, d->recv_keys, d->recv_tables, GC, d->rows_own, gflags)) return s;
+  if (int s = a2a(d, kXRows, d->rows_own, d->rows_back, 4 * size_t(d->dim), d->C)) return s;
+  if (int s = hps_gpu_pool_rows(d->ctx, d->rows_back, d->perm, offsets, n_bags, d->dim, combiner, out)) return s;
+  d->last_offsets = offsets;
+  d->last_bags = n_bags;
+  d->last_combiner = combiner;
+  d->have_fwd = true;
+  d->train = (flags & HPS_LOOKUP_TRAIN) != 0;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_dist_backward(hps_gpu_dist d, const float* d_out, const hps_opt_params* opt) {
+  if (!d || !d_out || !opt) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (!d->have_fwd || !d->train) {
+    set_last_error("dist_backward: no preceding training dist_forward");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (int s = hps_gpu_scatter_grads(d->ctx, d_out, d->perm, d->last_offsets, d->last_bags, d->dim, d->last_combiner,
+                                    d->grads_send))
+    return s;
+  if (int s = a2a(d, kXGrads, d->grads_send, d->grads_recv, 4 * size_t(d->dim), d->C)) return s;
+  if (int s = hps_gpu_backward_update(d->shard, d->grads_recv, opt)) return s;
+  d->have_fwd = false;
+  return HPS_GPU_OK;
+}
+
+}  // extern "C"

@@ -56,11 +56,15 @@ __global__ void k_find(const Slot* __restrict__ slots, TableDev td, const uint64
 // read-only probe settles it (rows committed before the call cannot change during it).
 __global__ void k_insert_claim(Slot* __restrict__ slots, TableDev td, const uint64_t* __restrict__ keys, uint64_t n,
                                uint64_t* __restrict__ ws_slot, uint32_t* __restrict__ abort_flag, uint32_t* status,
-                               bool keys_only) {
+                               bool keys_only, const uint32_t* __restrict__ key_tables, uint32_t table) {
   if (*reinterpret_cast<volatile uint32_t*>(abort_flag)) return;
   Slot* base = slots + td.slot_base;
   const Slot empty{0, kRowEmpty, kAuxNone};
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    if (key_tables && key_tables[i] != table) {  // keys-only insert: entries of other tables / empty slots
+      ws_slot[i] = kPresent;
+      continue;
+    }
     const uint64_t key = keys[i];
     const uint64_t home = hps::key_hash(key) & td.slot_mask;
     if (keys_only) {
@@ -274,7 +278,9 @@ struct LookupArgs {
   uint32_t n_bags;
   uint32_t n_slots;
   const uint32_t* slot_table;
-  const uint32_t* key_tables;  // one-key bags only: table of each key (overrides slot_table)
+  const uint32_t* key_tables;  // one-key bags only: table of each key (overrides slot_table);
+                               // an id >= n_tables marks an empty slot (absent, no gradient)
+  uint32_t n_tables;
   const TableDev* tables;
   const Slot* slots;
   const float* W;
@@ -324,6 +330,10 @@ __global__ void __launch_bounds__(256) k_probe(LookupArgs a) {
   if constexpr (!MULTI) {
     for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n_bags; i += uint64_t(gridDim.x) * blockDim.x) {
       const uint32_t table = a.key_tables ? a.key_tables[i] : a.slot_table[static_cast<uint32_t>(i) % a.n_slots];
+      if (table >= a.n_tables) {  // an empty slot of a fixed-capacity exchange buffer
+        a.occ_row[i] = a.row_absent;
+        continue;
+      }
       const TableDev td = a.tables[table];
       const uint32_t local = probe_find(a.slots, td, a.keys[i]);
       a.occ_row[i] = local == kRowEmpty ? a.row_absent : static_cast<uint32_t>(td.row_base + local);
@@ -408,7 +418,8 @@ __global__ void __launch_bounds__(256, 4) k_lookup_1hot(LookupArgs a) {
     uint32_t row = kRowEmpty, table = 0;
     if (bag < a.n_bags) {
       table = a.key_tables ? a.key_tables[bag] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
-      row = occurrence_row<ROWS>(a, bag, table);
+      if (table >= a.n_tables) table = 0;  // empty exchange slot: reads as absent
+      else row = occurrence_row<ROWS>(a, bag, table);
     }
     for (int m0 = 0; m0 < LPR; m0 += kBatch) {
       float4 x[kBatch][VPL];
@@ -474,8 +485,10 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_lookup_1hot_tma(LookupArgs a
     const uint32_t nb = static_cast<uint32_t>(min(uint64_t(32), a.n_bags - t0));
     const float* src = nullptr;
     if (bag < a.n_bags) {
-      const uint32_t table = a.key_tables ? a.key_tables[bag] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
-      const uint32_t row = occurrence_row<ROWS>(a, bag, table);
+      uint32_t table = a.key_tables ? a.key_tables[bag] : a.slot_table[static_cast<uint32_t>(bag) % a.n_slots];
+      uint32_t row = kRowEmpty;
+      if (table >= a.n_tables) table = 0;  // empty exchange slot: reads as absent
+      else row = occurrence_row<ROWS>(a, bag, table);
       src = row == kRowEmpty ? a.defaults + uint64_t(table) * D : a.W + uint64_t(row) * D;
     }
     if (lane == 0) bulk_wait_read_all();  // the previous tile's store has finished reading smem
@@ -741,7 +754,7 @@ __global__ void __launch_bounds__(256) k_hybrid_pool(const uint32_t* __restrict_
 
 }  // namespace
 int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
-                   uint64_t* rows_out, cudaStream_t st);
+                   uint64_t* rows_out, cudaStream_t st, const uint32_t* key_tables = nullptr);
 namespace {
 
 // A training record is about to overwrite ws_rows_a: counters of a previous record that no
@@ -854,6 +867,7 @@ void fill_lookup_args(hps_gpu_table t, LookupArgs& a, const uint64_t* keys, cons
   a.n_slots = t->n_slots;
   a.slot_table = t->d_slot_table;
   a.tables = t->d_tables;
+  a.n_tables = t->n_tables;
   a.slots = t->d_slots;
   a.W = t->d_w;
   a.Wh = t->d_wh;
@@ -1254,7 +1268,7 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
 // Insert on stream `st` with the current batch slot's scratch (hps_gpu_table_insert; the
 // insert-on-miss of a prefetch runs it on the slot's side stream).
 int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
-                   uint64_t* rows_out, cudaStream_t st) {
+                   uint64_t* rows_out, cudaStream_t st, const uint32_t* key_tables) {
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (n == 0) return HPS_GPU_OK;
   if (!keys || n >= (1ull << 32) - 1) return HPS_GPU_E_INVALID_ARGUMENT;
@@ -1285,7 +1299,7 @@ int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64
   if (rows) k_rows_non_finite<<<grid_for(n * t->dim, 256, kNumSMs * 32), 256, 0, st>>>(rows, n * t->dim, t->ws_abort,
                                                                                       t->ctx->d_status, t->f16 ? 1 : 0);
   k_insert_claim<<<grid, 256, 0, st>>>(t->d_slots, td, keys, n, ws_slot, t->ws_abort, t->ctx->d_status,
-                                       rows == nullptr && rows_out == nullptr);
+                                       rows == nullptr && rows_out == nullptr, key_tables, table);
   InsertScanOp op{t->d_slots, td.slot_base, ws_slot, ws_pos, ws_flag, n, t->ws_counts + 3, t->ws_abort};
   k_scan<InsertScanOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(
       op, scan_status, reinterpret_cast<uint32_t*>(scan_status + tiles));
@@ -1482,6 +1496,7 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
   a.n_slots = t->n_slots;
   a.slot_table = t->d_slot_table;
   a.tables = t->d_tables;
+  a.n_tables = t->n_tables;
   a.slots = t->d_slots;
   a.occ_bag = multi ? t->ws_occ_bag : nullptr;
   a.bag_len = (multi && combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
@@ -1545,7 +1560,8 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
   if (!keys || !tables || !rows_out) return HPS_GPU_E_INVALID_ARGUMENT;
   if (flags & HPS_LOOKUP_INSERT) {  // dynamic single-table shard: materialise absent keys first
     if (t->n_tables != 1) return HPS_GPU_E_INVALID_ARGUMENT;
-    if (int s = hps_gpu_table_insert(t, 0, keys, n, nullptr, nullptr)) return s;
+    // (entries of an empty exchange slot carry a table id >= n_tables: not inserted)
+    if (int s = hpsg_insert_on(t, 0, keys, n, nullptr, nullptr, t->ctx->stream, tables)) return s;
   }
   LookupArgs a{};
   a.keys = keys;
@@ -1554,6 +1570,7 @@ int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* t
   a.slot_table = t->d_slot_table;
   a.key_tables = tables;
   a.tables = t->d_tables;
+  a.n_tables = t->n_tables;
   a.slots = t->d_slots;
   a.W = t->d_w;
   a.Wh = t->d_wh;

@@ -145,6 +145,39 @@ def build_tables_hybrid(ctx: Context, cfg: W.Config, rank: int, world: int, hot_
     return hot, cold
 
 
+class CabiDistExchange:
+    """Distributed-slot exchange through the C-ABI (hps_gpu_dist_*, sharded.cu): the
+    NCCL communicator lives in the context (rank 0's id broadcast over torch.distributed)."""
+
+    def __init__(self, ctx: Context, table: EmbeddingTableGroup, cfg: W.Config, rank: int, world: int,
+                 insert_missing: bool = False):
+        from .api import DistTable
+        if world > 1:
+            import torch.distributed as dist
+            obj = [Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctx.comm_init(obj[0], rank, world)
+        self.world, self.cfg, self.insert_missing = world, cfg, insert_missing
+        self.combiner = cfg.combiner
+        self.dt = DistTable(ctx, table, cfg.slots(), table_max_keys(cfg, 1), cfg.batch * cfg.n_slots)
+        self.out = torch.empty(cfg.batch * cfg.n_slots, cfg.dim, dtype=torch.float32, device="cuda")
+        self.last_recv = 0
+
+    def forward(self, keys, offs, n_bags, train=True):
+        self.dt.forward(keys, n_bags // self.dt.n_slots, offsets=offs, combiner=self.combiner, train=train,
+                        insert_missing=self.insert_missing, out=self.out)
+        return self.out
+
+    def backward(self, dout, params):
+        self.dt.backward(dout, params)
+
+    def exchanged_bytes(self, dim: int) -> int:
+        """Bytes this rank sends to its peers per step: keys + table ids, rows, gradients
+        (fixed-capacity regions, so independent of the batch)."""
+        C_ = self.dt.capacity
+        return (self.world - 1) * C_ * (8 + 4 + 2 * dim * 4)
+
+
 class TrainStep:
     """One fwd+bwd+update step over a staged batch. world == 1 runs the fused path
     (2 C-ABI calls, optionally replayed as one CUDA graph); world > 1 runs the
@@ -153,7 +186,7 @@ class TrainStep:
     def __init__(self, ctx: Context, table: Optional[EmbeddingTableGroup], cfg: W.Config, rank: int = 0,
                  world: int = 1, use_graph: bool = True, owned: Optional[List[List[int]]] = None,
                  hybrid_hot: Optional[EmbeddingTableGroup] = None, force_exchange: bool = False,
-                 pipeline: bool = False):
+                 pipeline: bool = False, cabi: bool = True):
         """owned (world > 1): localized placement, owned[g] = slots of rank g (localized_plan);
         None = distributed placement."""
         self.ctx, self.table, self.cfg, self.rank, self.world = ctx, table, cfg, rank, world
@@ -197,6 +230,13 @@ class TrainStep:
             # hot record + dedup + cold scan + bucketize(5) + cold gather (record + dedup + pooling)
             # + pool + cold grads + cold backward(2) + hot reduce(2) + sum_partials + apply
             self.kernels_per_step = rec + 1 + 5 + rec + 1 + 1 + 1 + 2 + 2 + 2
+        elif multi and cabi:
+            # distributed slot through the C-ABI (sharded.cu): NCCL inside libhps_gpu, fixed
+            # per-peer regions, no host sync, so the step is replayed as one CUDA graph
+            self.exchange = CabiDistExchange(ctx, table, cfg, rank, world, self.insert_missing)
+            self.placement = "distributed"
+            self.graph_mode = bool(use_graph)
+            self.kernels_per_step = 5 + 1 + rec + 1 + 1 + 1 + 2 + (1 if cfg.hot > 1 else 0)
         elif multi:
             from .exchange import DistributedExchange, GpuEngine
             max_keys = table_max_keys(cfg, 1)
@@ -256,7 +296,17 @@ class TrainStep:
                           out=self.out, keys_on_host=keys_on_host, insert_missing=self.insert_missing)
         self.table.backward_update(dout, self.cfg.lr, params=self.params)
 
-    def _exchange_step(self, keys, offs, dout, step):
+    def _exchange_step(self, keys, offs, dout, step, graph=True):
+        if isinstance(self.exchange, CabiDistExchange):
+            self._prep_step(step)
+            self._adam_params(step)
+
+            def body():
+                self.out = self.exchange.forward(keys, offs, self.n_bags, train=True)
+                self.exchange.backward(dout, self.params)
+            if self.graph_mode and graph:
+                return self._graph(("dist", id(keys), id(offs), id(dout)), body)
+            return body()
         if self.cfg.optimizer == "adam":
             self.params = opt_params("adam", self.cfg.lr, eps=self.cfg.eps, step=step)
         n = self.cfg.batch if self.placement in ("localized", "hybrid") else self.n_bags
@@ -442,7 +492,7 @@ class TrainStep:
         if self.exchange is not None:
             keys = b["keys"].to("cuda", non_blocking=True)
             offs = None if b["offs"] is None else b["offs"].to("cuda", non_blocking=True)
-            self._exchange_step(keys, offs, dout, step)
+            self._exchange_step(keys, offs, dout, step, graph=False)
             _ = self._unique_count()
             return h2d, 8
         if self.graph_mode and b["offs"] is None:

@@ -21,6 +21,7 @@ STRUCTS = {
     "hps_cache_stats": L.CacheStats,
     "hps_update_header": L.UpdateHeader,
     "hps_slot_spec": L.SlotSpec,
+    "hps_dist_config": L.DistConfig,
 }
 
 
