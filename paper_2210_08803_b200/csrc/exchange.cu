@@ -50,12 +50,16 @@ __global__ void k_pack(const uint64_t* __restrict__ keys, uint64_t n, const uint
                        uint64_t* __restrict__ send_keys, uint32_t* __restrict__ send_tables,
                        uint32_t* __restrict__ perm) {
   for (uint64_t p = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; p < n; p += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t i = sorted_idx[p];
+    const uint32_t i = sorted_idx ? sorted_idx[p] : static_cast<uint32_t>(p);  // (one owner: identity)
     const uint32_t bag = occ_bag ? occ_bag[i] : i;
     send_keys[p] = keys[i];
     send_tables[p] = slot_table[bag % n_slots];
     perm[i] = static_cast<uint32_t>(p);
   }
+}
+
+__global__ void k_count_all(uint32_t* counts, uint32_t n) {
+  if (threadIdx.x == 0) counts[0] = n;
 }
 
 __global__ void k_counts(const uint32_t* __restrict__ hist, uint32_t n_shards, uint32_t* __restrict__ counts) {
@@ -285,6 +289,13 @@ int hps_gpu_xplan_bucketize(hps_gpu_xplan p, const uint64_t* keys, uint64_t n, c
     return HPS_GPU_OK;
   }
   if (!keys || !slot_table || !send_keys || !send_tables || !perm || !counts) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (p->n_shards == 1) {  // one owner: the stable order is the input order (no sort)
+    k_pack<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(keys, n, nullptr, occ_bag, n_slots, slot_table, send_keys,
+                                                           send_tables, perm);
+    k_count_all<<<1, 32, 0, st>>>(counts, static_cast<uint32_t>(n));
+    HPSG_CHECK_LAUNCH("bucketize");
+    return HPS_GPU_OK;
+  }
   k_owner<<<grid_for(n, 256, kNumSMs * 16), 256, 0, st>>>(keys, n, p->n_shards, hps::FastMod64(p->n_shards), p->owners,
                                                           p->d_n);
   cudaError_t err;

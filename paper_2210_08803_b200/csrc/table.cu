@@ -1351,7 +1351,9 @@ int hps_gpu_table_export(hps_gpu_table t, uint32_t table, uint64_t row_begin, ui
 int hps_gpu_table_row_keys(hps_gpu_table t, uint32_t table, uint64_t row_begin, uint64_t n, uint64_t* keys_out) {
   if (int s = check_tbl(t)) return s;
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
-  if (row_begin + n > t->row_cap[table] || !keys_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (row_begin + n > t->row_cap[table]) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (n == 0) return HPS_GPU_OK;
+  if (!keys_out) return HPS_GPU_E_INVALID_ARGUMENT;
   HPSG_CUDA(cudaMemcpyAsync(keys_out, t->d_row_keys + t->row_base[table] + row_begin, n * sizeof(uint64_t),
                             cudaMemcpyDeviceToDevice, t->ctx->stream));
   return HPS_GPU_OK;

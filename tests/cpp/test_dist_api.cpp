@@ -46,14 +46,15 @@ std::vector<T> host(const T* d, size_t n) {
   return h;
 }
 
+// (the slot map only matters to the unsharded tables' lookup_pooled: a shard is addressed
+// through the table ids the requesters send)
 hps_gpu_table make_table(hps_gpu_ctx ctx, uint64_t max_keys) {
-  const uint32_t st[2] = {0, 1};
   hps_table_config c{};
   c.n_tables = 2;
   c.dim = kDim;
   c.row_capacity_host = kCaps;
-  c.n_slots = 2;
-  c.slot_table_host = st;
+  c.n_slots = kS;
+  c.slot_table_host = kSlots;
   c.optimizer = HPS_OPT_ADAGRAD;
   c.max_batch_keys = max_keys;
   c.max_batch_bags = max_keys;

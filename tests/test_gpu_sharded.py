@@ -47,6 +47,9 @@ def compare_owned(shards, single, pools, world):
         for t, ks in enumerate(pools):
             mine = ks[owners(ks, world) == r]
             n = sh.size(t)
+            if n == 0:
+                assert len(mine) == 0
+                continue
             rk_t, ex = sh.row_keys(t, 0, n), sh.export(t, 0, n)
             torch.cuda.synchronize()  # (the copies ran on the rank's context stream)
             rk = rk_t.cpu().numpy().view(np.uint64)
@@ -118,8 +121,6 @@ def run_world(world, multi, optimizer, steps=3, insert=False):
 
     for step in range(1, steps + 1):
         keys, offs = global_batch(rs, pools, slot_table, B * world, multi)
-        if insert:
-            pass
         ref = single.lookup(keys, B * world, offsets=offs.astype(np.uint32) if multi else None, combiner=comb,
                             train=True)
         dout = rs.standard_normal(ref.shape).astype(np.float32)
