@@ -36,12 +36,15 @@ from paper_2210_08803_b200 import workload as W  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "round1", "ncu_traffic.json")
+STEP_TRAFFIC_PATH = os.path.join(ROOT, "profiles", "round2", "ncu_step_traffic.json")
 
 
-def ncu_traffic(workload):
-    """DRAM bytes per launch of the roofline kernel from the committed ncu capture, or None."""
+def ncu_traffic(workload, path=TRAFFIC_PATH):
+    """DRAM bytes (read + write) from a committed ncu capture, or None: per launch of the fused
+    lookup (TRAFFIC_PATH), or per training step summed over its kernels (STEP_TRAFFIC_PATH,
+    profiles/step_traffic.py)."""
     try:
-        with open(TRAFFIC_PATH) as f:
+        with open(path) as f:
             d = json.load(f)[workload]
         return int(d["dram_read"]) + int(d["dram_write"])
     except Exception:
@@ -509,14 +512,22 @@ def main():
             "config": workload_config(cfg, world, args),
             "run": {"l2": "flushed between timed steps (256 MB write)", "graph": step_fn.graph_mode,
                     "insert_on_miss": step_fn.insert_missing},
-            "roofline": {"bound": "hbm", "kernel": "k_lookup_1hot (fused hash+probe+gather+pool)" if cfg.hot == 1
-                         else "k_lookup_multi (fused hash+probe+gather+pool)",
-                         "achieved": fwd_gbs, "peak": peak, "unit": "GB/s", "frac": fwd_gbs / peak,
-                         "peak_kind": peak_kind, "traffic": ncu_traffic(cfg.name) if world == 1 else None,
-                         "traffic_source": "ncu --set full dram__bytes_read+write per launch (profiles/round1/ncu_traffic.json)",
-                         "algorithmic_bytes": fwd_b,
-                         "kernel_ms": fwd_ms_mean,
-                         "step_achieved": step_gbs, "step_frac": step_gbs / peak, "step_algorithmic_bytes": fwd_b + bwd_b},
+            # the timed unit: one training step (lookup + backward + update, one CUDA graph);
+            # algorithmic bytes per SURVEY.md §8(d) over the step's N occurrences / U unique rows
+            "roofline": {"bound": "hbm",
+                         "kernel": "training step: probe, dedup, pooling, short + long reduce with the fused "
+                                   "optimizer (one CUDA graph)",
+                         "achieved": step_gbs, "peak": peak, "unit": "GB/s", "frac": step_gbs / peak,
+                         "peak_kind": peak_kind,
+                         "traffic": ncu_traffic(cfg.name, STEP_TRAFFIC_PATH) if world == 1 else None,
+                         "traffic_source": "ncu dram__bytes_read+write summed over one eager step's kernels, "
+                                           "cold caches (profiles/round2/ncu_step_traffic.json)",
+                         "algorithmic_bytes": fwd_b + bwd_b, "ms": ms,
+                         "fused_lookup": {
+                             "kernel": "k_lookup_1hot_tma<0> (inference: hash+probe+gather+pool)" if cfg.hot == 1
+                             else "k_lookup_multi (inference: hash+probe+gather+pool)",
+                             "achieved": fwd_gbs, "frac": fwd_gbs / peak, "algorithmic_bytes": fwd_b,
+                             "kernel_ms": fwd_ms_mean, "traffic": ncu_traffic(cfg.name) if world == 1 else None}},
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": step_fn.kernels_per_step * args.steps,
             "clocks": clocks,
