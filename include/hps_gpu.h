@@ -103,7 +103,11 @@ enum { HPS_DTYPE_F32 = 0, HPS_DTYPE_F16 = 1 };
 
 typedef struct {
   uint32_t n_tables;
-  uint32_t dim;                     /* 1..4096, multiple of 4 */
+  uint32_t dim;                     /* 1..1024 (hps::kMaxDim is 4096: wider rows -> InvalidArgument). Rows
+                                       are stored at round_up(dim, 4) floats; a dim that is not a
+                                       multiple of 4 is served through a staging copy on the core
+                                       entry points (insert/find/export/lookup/prefetch/backward), while
+                                       the exchange, hybrid and read-through paths refuse it */
   const uint64_t* row_capacity_host;/* [n_tables] max rows per table */
   uint32_t n_slots;
   const uint32_t* slot_table_host;  /* [n_slots] table id of each slot */
@@ -344,7 +348,7 @@ typedef struct {
   uint64_t capacity;        /* resident entries; capacity % ways == 0 */
   uint32_t ways;            /* 1..32, default 8 */
   uint64_t aging_interval;  /* accesses per set-aging epoch numerator; 0 -> 10*capacity */
-  uint32_t dim;
+  uint32_t dim;             /* 1..4096 (hps::kMaxDim); stored at round_up(dim, 4) */
   uint64_t max_batch;       /* workspace sizing: keys per call */
   uint32_t dtype;           /* HPS_DTYPE_F32 (0, default) or HPS_DTYPE_F16: rows held as IEEE binary16
                                (round-to-nearest-even on insert/refresh, exact widening on query;

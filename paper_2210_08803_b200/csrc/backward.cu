@@ -1674,15 +1674,28 @@ extern "C" {
 
 int hps_gpu_backward_update(hps_gpu_table t, const float* d_out, const hps_opt_params* opt) {
   if (!t || !opt) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (t->dim != t->dim_io && d_out && t->have_train) {  // padded rows: widen the gradients first
+    if (rows_widen(t->ws_io, t->dim, d_out, t->dim_io, t->pre_n_bags, t->ctx->stream) != cudaSuccess)
+      return HPS_GPU_E_CUDA;
+    d_out = t->ws_io;
+  }
   return backward_impl(t, d_out, opt, nullptr, nullptr);
 }
 
 int hps_gpu_backward_reduce(hps_gpu_table t, const float* d_out, float* grads_out, uint32_t* touched_out) {
+  if (t && t->dim != t->dim_io) {
+    set_last_error("hybrid gradient path: needs dim % 4 == 0 (rows of this table are padded)");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
   if (!t || !grads_out || !touched_out) return HPS_GPU_E_INVALID_ARGUMENT;
   return backward_impl(t, d_out, nullptr, grads_out, touched_out);
 }
 
 int hps_gpu_apply_grads(hps_gpu_table t, const float* grads, const uint32_t* touched, const hps_opt_params* opt) {
+  if (t && t->dim != t->dim_io) {
+    set_last_error("hybrid gradient path: needs dim % 4 == 0 (rows of this table are padded)");
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  }
   if (!t || !grads || !touched || !opt) return HPS_GPU_E_INVALID_ARGUMENT;
   if (t->f16) return HPS_GPU_E_DTYPE_MISMATCH;  // an F16 table is an inference table
   BwdArgs a{};

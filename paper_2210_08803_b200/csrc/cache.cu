@@ -40,6 +40,8 @@ struct hps_gpu_cache_s {
   hps_gpu_ctx ctx = nullptr;
   uint64_t capacity = 0, num_sets = 0, aging_period = 0, max_batch = 0;
   uint32_t ways = 0, dim = 0;
+  uint32_t dim_io = 0;     // the caller's dim; `dim` = padded_dim(dim_io) is the row stride
+  float* ws_io = nullptr;  // dim_io != dim: [max_batch x dim] staging of query / insert rows
   hps::FastMod64 set_mod;
   int set_bits = 0;
   uint64_t *d_keys = nullptr, *d_ver = nullptr, *d_touch = nullptr, *d_set_acc = nullptr;
@@ -803,9 +805,9 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   if (!ctx || !cfg || !out) return HPS_GPU_E_INVALID_ARGUMENT;
   *out = nullptr;
   const uint32_t ways = cfg->ways ? cfg->ways : 8;
-  if (ways > 32 || cfg->capacity < ways || cfg->capacity % ways != 0 || cfg->dim == 0 || cfg->dim % 4 != 0 ||
-      cfg->dim > 4096 || cfg->max_batch == 0 || cfg->max_batch >= (1ull << 31)) {
-    set_last_error("cache config: need 1<=ways<=32, capacity % ways == 0, dim % 4 == 0, 1<=max_batch<2^31");
+  if (ways > 32 || cfg->capacity < ways || cfg->capacity % ways != 0 || cfg->dim == 0 || cfg->dim > 4096 ||
+      cfg->max_batch == 0 || cfg->max_batch >= (1ull << 31)) {
+    set_last_error("cache config: need 1<=ways<=32, capacity % ways == 0, 1<=dim<=4096, 1<=max_batch<2^31");
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
   if (cfg->capacity / ways >= 0xffffffffull) return HPS_GPU_E_INVALID_ARGUMENT;
@@ -818,7 +820,8 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   c->ctx = ctx;
   c->capacity = cfg->capacity;
   c->ways = ways;
-  c->dim = cfg->dim;
+  c->dim_io = cfg->dim;
+  c->dim = padded_dim(cfg->dim);
   c->f16 = cfg->dtype == HPS_DTYPE_F16;
   if (const char* e = std::getenv("HPS_GPU_NO_SMALL_SORT")) c->no_small_sort = e[0] == '1';
   c->num_sets = cfg->capacity / ways;
@@ -850,6 +853,7 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   A(dalloc(&c->ws_sort, c->sort_words));
   A(dalloc(&c->ws_scan, scan_tiles(n) + 2));
   A(dalloc(&c->ws_counts, 8));
+  if (c->dim != c->dim_io) A(dalloc(&c->ws_io, n * c->dim));
   if (st) {
     hps_gpu_cache_destroy(c);
     return st;
@@ -872,7 +876,7 @@ int hps_gpu_cache_destroy(hps_gpu_cache c) {
   if (!c) return HPS_GPU_OK;
   void* ptrs[] = {c->d_keys,    c->d_ver,    c->d_touch,   c->d_freq, c->d_set_acc, c->d_vec,
                   c->d_state,   c->ws_set,   c->ws_keys_b, c->ws_vals_a, c->ws_vals_b, c->ws_hit,
-                  c->ws_rank,   c->ws_seg,   c->ws_sort,   c->ws_scan, c->ws_counts};
+                  c->ws_rank,   c->ws_seg,   c->ws_sort,   c->ws_scan, c->ws_counts, c->ws_io};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -975,7 +979,20 @@ extern "C" {
 
 int hps_gpu_cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, float* found_vecs, uint32_t* found_idx,
                         uint32_t* missing_idx, uint64_t* counts) {
+  if (c && c->dim != c->dim_io && found_vecs && n && n <= c->max_batch) {  // padded rows: gather, then narrow
+    int s = cache_query(c, keys, n, nullptr, c->ws_io, found_idx, missing_idx, counts);
+    if (!s && rows_narrow(found_vecs, c->dim_io, c->ws_io, c->dim, n, c->ctx->stream) != cudaSuccess) s = HPS_GPU_E_CUDA;
+    return s;
+  }
   return cache_query(c, keys, n, nullptr, found_vecs, found_idx, missing_idx, counts);
+}
+
+// Padded rows: the caller's [n x dim_io] entries widened into the staging (zero padding).
+static const float* widen_entries(hps_gpu_cache c, const float* vecs, uint64_t n, int* status) {
+  *status = HPS_GPU_OK;
+  if (!c || c->dim == c->dim_io || !vecs || n == 0 || n > c->max_batch) return vecs;
+  if (rows_widen(c->ws_io, c->dim, vecs, c->dim_io, n, c->ctx->stream) != cudaSuccess) *status = HPS_GPU_E_CUDA;
+  return c->ws_io;
 }
 
 static int entry_prep(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n,
@@ -1025,13 +1042,17 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
 int hps_gpu_cache_insert(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions, uint64_t n,
                          uint64_t* admitted_out) {
   if (n && !versions) return HPS_GPU_E_INVALID_ARGUMENT;
-  return insert_impl(c, keys, vecs, versions, n, nullptr, admitted_out);
+  int s = HPS_GPU_OK;
+  vecs = widen_entries(c, vecs, n, &s);
+  return s ? s : insert_impl(c, keys, vecs, versions, n, nullptr, admitted_out);
 }
 
 int hps_gpu_cache_insert_count(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions,
                                uint64_t n_max, const uint64_t* d_count, const uint8_t* skip, uint64_t* admitted_out) {
   if (!d_count) return HPS_GPU_E_INVALID_ARGUMENT;
-  return insert_impl(c, keys, vecs, versions, n_max, d_count, admitted_out, skip);
+  int s = HPS_GPU_OK;
+  vecs = widen_entries(c, vecs, n_max, &s);
+  return s ? s : insert_impl(c, keys, vecs, versions, n_max, d_count, admitted_out, skip);
 }
 
 int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions,
@@ -1044,6 +1065,11 @@ int hps_gpu_cache_refresh(hps_gpu_cache c, const uint64_t* keys, const float* ve
     return HPS_GPU_OK;
   }
   if (!keys || !vecs || !versions) return HPS_GPU_E_INVALID_ARGUMENT;
+  {
+    int s = HPS_GPU_OK;
+    vecs = widen_entries(c, vecs, n, &s);
+    if (s) return s;
+  }
   if (int s = entry_prep(c, keys, vecs, n, nullptr, nullptr, replaced_out)) return s;  // zeroes *replaced_out
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
@@ -1061,7 +1087,7 @@ namespace hpsg {
 int cache_info(hps_gpu_cache c, hps_gpu_ctx* ctx, uint32_t* dim) {
   if (int s = check_cache(c)) return s;
   *ctx = c->ctx;
-  *dim = c->dim;
+  *dim = c->dim_io;  // (the caller's dim; rows are stored padded when it is not a multiple of 4)
   return HPS_GPU_OK;
 }
 uint64_t cache_max_batch(hps_gpu_cache c) { return c ? c->max_batch : 0; }
@@ -1102,7 +1128,7 @@ int hps_gpu_cache_debug_export(hps_gpu_cache c, uint64_t* keys, uint64_t* versio
   if (last_touch) HPSG_CUDA(cudaMemcpyAsync(last_touch, c->d_touch, cap * 8, cudaMemcpyDeviceToDevice, st));
   if (set_access) HPSG_CUDA(cudaMemcpyAsync(set_access, c->d_set_acc, c->num_sets * 8, cudaMemcpyDeviceToDevice, st));
   if (vecs)
-    HPSG_CUDA(cudaMemcpyAsync(vecs, c->d_vec, cap * c->dim * (c->f16 ? 2 : 4), cudaMemcpyDeviceToDevice, st));
+    HPSG_CUDA(rows_narrow(vecs, c->dim_io, c->d_vec, c->dim, cap, st, c->f16 ? 2 : 4));
   return HPS_GPU_OK;
 }
 

@@ -318,6 +318,26 @@ struct TraceOf<Op, std::void_t<decltype(Op::kTrace)>> {
   static constexpr int id = Op::kTrace;
 };
 
+// ---- rows of a dim that is not a multiple of 4 ------------------------------------
+// Tables and caches store rows at a padded stride (round_up(dim, 4): every kernel moves
+// 128-bit vectors); the caller's buffers keep `dim`. These copy [rows x cols] fp32 between
+// the two strides (cudaMemcpy2DAsync: capturable, no kernel); widening zero-fills the
+// padding so no NaN/Inf check ever sees garbage.
+inline uint32_t padded_dim(uint32_t dim) { return (dim + 3u) & ~3u; }
+inline cudaError_t rows_narrow(void* dst, uint32_t dim_io, const void* src, uint32_t dim, uint64_t rows,
+                               cudaStream_t st, size_t elem = 4) {
+  if (rows == 0) return cudaSuccess;
+  return cudaMemcpy2DAsync(dst, size_t(dim_io) * elem, src, size_t(dim) * elem, size_t(dim_io) * elem, rows,
+                           cudaMemcpyDeviceToDevice, st);
+}
+inline cudaError_t rows_widen(float* dst, uint32_t dim, const float* src, uint32_t dim_io, uint64_t rows,
+                              cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  if (cudaError_t e = cudaMemset2DAsync(dst + dim_io, size_t(dim) * 4, 0, size_t(dim - dim_io) * 4, rows, st)) return e;
+  return cudaMemcpy2DAsync(dst, size_t(dim) * 4, src, size_t(dim_io) * 4, size_t(dim_io) * 4, rows,
+                           cudaMemcpyDeviceToDevice, st);
+}
+
 // ---- host-side error plumbing -------------------------------------------------
 void set_last_error(const std::string& msg);
 int cuda_status(cudaError_t e, const char* what);

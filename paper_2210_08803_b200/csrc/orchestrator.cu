@@ -265,9 +265,13 @@ int hps_gpu_readthrough_create(hps_gpu_cache cache, hps_gpu_table tbl, uint32_t 
   uint32_t cdim = 0;
   if (int s = cache_info(cache, &ctx, &cdim)) return s;
   if (table >= tbl->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
-  if (cdim != tbl->dim) {
+  if (cdim != tbl->dim_io) {
     set_last_error("readthrough: cache dim != table dim");
     return HPS_GPU_E_DIM_MISMATCH;
+  }
+  if (cdim % 4 != 0) {
+    set_last_error("readthrough: needs dim % 4 == 0 (padded rows are not served by the orchestrator)");
+    return HPS_GPU_E_INVALID_ARGUMENT;
   }
   if (ctx != tbl->ctx) {
     set_last_error("readthrough: cache and table must share one context");

@@ -664,6 +664,13 @@ cudaError_t hpsg::trace_attach_table(TraceRec* p) { return trace_attach_tu(p); }
 
 namespace {
 
+// Entry points whose caller buffers are addressed at the storage stride (the exchange, hybrid
+// and read-through paths) take only dims that are a multiple of 4.
+int refuse_padded(hps_gpu_table, const char* what) {
+  set_last_error(std::string(what) + ": needs dim % 4 == 0 (rows of this table are padded)");
+  return HPS_GPU_E_INVALID_ARGUMENT;
+}
+
 int check_tbl(hps_gpu_table t) {
   if (!t) {
     set_last_error("null table handle");
@@ -1097,8 +1104,8 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
     set_last_error("table config: n_tables, row_capacity, n_slots and slot_table are required");
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
-  if (cfg->dim == 0 || cfg->dim > 1024 || cfg->dim % 4 != 0) {
-    set_last_error("table config: dim must be a multiple of 4 in [4, 1024]");
+  if (cfg->dim == 0 || cfg->dim > 1024) {
+    set_last_error("table config: dim must be in [1, 1024] (rows up to 1024 floats per warp)");
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
   if (cfg->optimizer < HPS_OPT_SGD || cfg->optimizer > HPS_OPT_ADAM) return HPS_GPU_E_INVALID_ARGUMENT;
@@ -1114,7 +1121,8 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   auto t = new hps_gpu_table_s;
   t->ctx = ctx;
   t->n_tables = cfg->n_tables;
-  t->dim = cfg->dim;
+  t->dim_io = cfg->dim;
+  t->dim = padded_dim(cfg->dim);
   t->n_slots = cfg->n_slots;
   t->optimizer = cfg->optimizer;
   t->n_state = cfg->optimizer == HPS_OPT_SGD ? 0 : cfg->optimizer == HPS_OPT_ADAGRAD ? 1 : 2;
@@ -1180,6 +1188,7 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   if (const char* e = std::getenv("HPS_GPU_BT_MULT")) bt_mult = std::max(2, std::atoi(e));  // A/B knob
   t->bt_mask = std::min<uint64_t>(next_pow2(bt_mult * N), 1ull << 25) - 1;
   (void)B;
+  if (t->dim != t->dim_io) A(dalloc(&t->ws_io, B * D));
   if (!st) st = alloc_batch_slot(t, *t);
   t->parked.resize(1);
   t->cur = 0;
@@ -1207,7 +1216,7 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
   for (BatchSlot& b : t->parked)
     if (b.side) cudaStreamSynchronize(b.side);
   void* ptrs[] = {t->d_wh,        t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
-                  t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table};
+                  t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_io};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (BatchSlot& b : t->parked) free_batch_slot(b);
@@ -1237,12 +1246,14 @@ int hps_gpu_table_set_default_vector(hps_gpu_table t, uint32_t table, const floa
   if (int s = check_tbl(t)) return s;
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (!vec_host) return HPS_GPU_E_INVALID_ARGUMENT;
-  for (uint32_t j = 0; j < t->dim; ++j) {
+  std::vector<float> v(t->dim, 0.f);  // (padding columns: zero)
+  for (uint32_t j = 0; j < t->dim_io; ++j) {
     uint32_t b;
     std::memcpy(&b, vec_host + j, 4);
     if ((b & 0x7f800000u) == 0x7f800000u) return HPS_GPU_E_NON_FINITE;
+    v[j] = vec_host[j];
   }
-  HPSG_CUDA(cudaMemcpyAsync(t->d_defaults + uint64_t(table) * t->dim, vec_host, t->dim * sizeof(float),
+  HPSG_CUDA(cudaMemcpyAsync(t->d_defaults + uint64_t(table) * t->dim, v.data(), t->dim * sizeof(float),
                             cudaMemcpyHostToDevice, t->ctx->stream));
   HPSG_CUDA(cudaStreamSynchronize(t->ctx->stream));
   return HPS_GPU_OK;
@@ -1260,6 +1271,15 @@ int hps_gpu_table_size(hps_gpu_table t, uint32_t table, uint64_t* n_rows_host) {
 int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
                          uint64_t* rows_out) {
   if (int s = check_tbl(t)) return s;
+  if (rows && n && t->dim != t->dim_io) {  // padded rows: widen the given values first
+    cudaStream_t st = t->ctx->stream;
+    float* tmp = nullptr;
+    HPSG_CUDA(cudaMallocAsync(&tmp, n * t->dim * sizeof(float), st));
+    int s = rows_widen(tmp, t->dim, rows, t->dim_io, n, st) == cudaSuccess
+                ? hpsg_insert_on(t, table, keys, n, tmp, rows_out, st) : HPS_GPU_E_CUDA;
+    cudaFreeAsync(tmp, st);
+    return s;
+  }
   return hpsg_insert_on(t, table, keys, n, rows, rows_out, t->ctx->stream);
 }
 
@@ -1335,6 +1355,24 @@ int hps_gpu_table_export(hps_gpu_table t, uint32_t table, uint64_t row_begin, ui
   if (int s = check_tbl(t)) return s;
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (row_begin + n > t->row_cap[table]) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (t->dim != t->dim_io && n) {  // padded rows: export at the storage stride, then narrow
+    cudaStream_t st = t->ctx->stream;
+    float* tmp = nullptr;
+    HPSG_CUDA(cudaMallocAsync(&tmp, n * t->dim * sizeof(float), st));
+    const uint32_t io = t->dim_io;
+    t->dim_io = t->dim;  // (the recursive call exports unpadded)
+    int s = HPS_GPU_OK;
+    float* outs[3] = {w, s0, s1};
+    for (int k = 0; k < 3 && !s; ++k) {
+      if (!outs[k]) continue;
+      s = hps_gpu_table_export(t, table, row_begin, n, k == 0 ? tmp : nullptr, k == 1 ? tmp : nullptr,
+                               k == 2 ? tmp : nullptr);
+      if (!s && rows_narrow(outs[k], io, tmp, t->dim, n, st) != cudaSuccess) s = HPS_GPU_E_CUDA;
+    }
+    t->dim_io = io;
+    cudaFreeAsync(tmp, st);
+    return s;
+  }
   const uint64_t off = (t->row_base[table] + row_begin) * t->dim, bytes = n * t->dim * sizeof(float);
   cudaStream_t st = t->ctx->stream;
   if (w && t->f16) {  // binary16 rows widened exactly
@@ -1367,6 +1405,14 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
   if (n_bags > t->max_bags) {
     set_last_error("lookup: n_samples * n_slots exceeds max_batch_bags");
     return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (t->dim != t->dim_io && n_bags && out) {  // padded rows: pool into the staging, then narrow
+    const uint32_t io = t->dim_io;
+    t->dim_io = t->dim;  // (the recursive call sees an unpadded table)
+    int s = hps_gpu_lookup_pooled(t, keys, offsets, n_samples, combiner, t->ws_io, flags);
+    t->dim_io = io;
+    if (!s && rows_narrow(out, io, t->ws_io, t->dim, n_bags, t->ctx->stream) != cudaSuccess) s = HPS_GPU_E_CUDA;
+    return s;
   }
   if (flags & HPS_LOOKUP_PREFETCHED) return lookup_prefetched(t, offsets, n_bags, combiner, out, flags);
   if (n_bags == 0) {
@@ -1443,6 +1489,7 @@ int hpsg::table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* ke
                              const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
                              uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent,
                              uint8_t* src_out) {
+  if (t && t->dim != t->dim_io) return refuse_padded(t, "read_through");
   if (int s = check_tbl(t)) return s;
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (n == 0) return HPS_GPU_OK;
@@ -1478,6 +1525,7 @@ int hps_gpu_table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* 
 int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* offsets, uint32_t n_samples,
                          int combiner, uint64_t n_keys_host, uint32_t* cold_pos_out, uint64_t* cold_keys_out,
                          uint32_t* cold_bags_out, uint64_t* cold_count_out) {
+  if (t && t->dim != t->dim_io) return refuse_padded(t, "hybrid_probe");
   if (int s = check_tbl(t)) return s;
   if (t->f16) return HPS_GPU_E_DTYPE_MISMATCH;  // hybrid hot tables train
   const uint64_t n_bags = uint64_t(n_samples) * t->n_slots;
@@ -1518,6 +1566,7 @@ int hps_gpu_hybrid_probe(hps_gpu_table t, const uint64_t* keys, const uint32_t* 
 
 int hps_gpu_hybrid_pool(hps_gpu_table t, const uint32_t* cold_pos, const uint32_t* perm, const float* cold_rows,
                         const uint32_t* offsets, uint64_t n_bags, int combiner, float* out) {
+  if (t && t->dim != t->dim_io) return refuse_padded(t, "hybrid_pool");
   if (int s = check_tbl(t)) return s;
   if (t->f16) return HPS_GPU_E_DTYPE_MISMATCH;
   if (n_bags == 0) return HPS_GPU_OK;
@@ -1545,6 +1594,7 @@ int hps_gpu_hybrid_pool(hps_gpu_table t, const uint32_t* cold_pos, const uint32_
 
 int hps_gpu_gather_rows(hps_gpu_table t, const uint64_t* keys, const uint32_t* tables, uint64_t n, float* rows_out,
                         uint32_t flags) {
+  if (t && t->dim != t->dim_io) return refuse_padded(t, "gather_rows");
   if (int s = check_tbl(t)) return s;
   if (n > t->max_keys || n > t->max_bags) {
     set_last_error("gather_rows: n exceeds max_batch_keys / max_batch_bags");

@@ -121,6 +121,8 @@ struct BatchSlot {
 struct hps_gpu_table_s : BatchSlot {
   hps_gpu_ctx ctx = nullptr;
   uint32_t n_tables = 0, dim = 0, n_slots = 0;
+  uint32_t dim_io = 0;      // the caller's dim; `dim` = padded_dim(dim_io) is the storage stride
+  float* ws_io = nullptr;   // dim_io != dim: [max_bags x dim] staging of pooled outputs / gradients
   int optimizer = 0, n_state = 0;
   uint64_t seed = 0;
   float a0 = 0.f;

@@ -246,3 +246,75 @@ def test_oversized_device_offsets_refused(ctx):
     keys = rs.choice(pool, int(offs[-1]))
     run_steps(ctx, g, o, keys, 300, offs, "sum", "sgd", rs, steps=2)
     compare_tables(g, o, [500])
+
+
+ODD_DIMS = [1, 2, 3, 5, 7, 13, 30, 127, 129, 255, 1023]
+
+
+@pytest.mark.parametrize("dim", ODD_DIMS)
+def test_unpadded_dims_match_oracle(ctx, dim):
+    """Any dim in 1..1024 (hps::validate_dim accepts 1..4096, proj/src/core/types.cpp:57-60):
+    rows are stored at round_up(dim, 4); the caller's buffers keep `dim`. One-hot SGD with
+    given initial rows, multi-hot mean Adam with init_value rows, default vectors, export."""
+    rs = np.random.default_rng(dim + 1000)
+    caps = [800, 5]
+    for opt, multi in (("sgd", False), ("adam", True)):
+        g, o = make_pair(ctx, caps, dim, [0, 1, 0], opt, max_keys=1 << 13, max_bags=1 << 12)
+        pools = []
+        for t, c in enumerate(caps):
+            ks = rs.integers(0, 2**63, c).astype(np.uint64)
+            if opt == "sgd":  # given rows (the caller's stride is dim)
+                rows = rs.standard_normal((c, dim)).astype(np.float32)
+                g.insert(t, t64(ks), rows=torch.from_numpy(rows).cuda(), return_rows=False)
+                st, _ = o.insert(t, ks, rows)
+            else:
+                g.insert(t, t64(ks), return_rows=False)
+                st, _ = o.insert(t, ks)
+            assert st == 0
+            pools.append(ks)
+        dflt = rs.standard_normal(dim).astype(np.float32)
+        g.set_default_vector(1, dflt)
+        o.set_default(1, dflt)
+        B = 300
+        if multi:
+            lens = rs.integers(0, 6, B * 3)
+            offsets = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+            keys = np.concatenate([rs.choice(pools[[0, 1, 0][b % 3]][:200], l) for b, l in enumerate(lens)])
+            keys = keys.astype(np.uint64)
+            keys[::17] ^= np.uint64(0x5555)  # some absent keys (default vector)
+        else:
+            offsets = None
+            keys = np.stack([rs.choice(pools[0][:300], B), rs.choice(pools[1], B), rs.choice(pools[0], B)], 1).ravel()
+        run_steps(ctx, g, o, keys, B, offsets, "mean" if multi else "sum", opt, rs, steps=2)
+        compare_tables(g, o, caps)
+
+
+@pytest.mark.parametrize("dim", [1, 3, 6, 13, 4096])
+def test_cache_unpadded_dims(ctx, dim):
+    """Cache rows of any dim in 1..4096: insert / query / refresh round trip bitwise, stats as
+    the oracle's."""
+    from paper_2210_08803_b200 import HotCache
+    rs = np.random.default_rng(dim)
+    cap = 256
+    c = HotCache(ctx, cap, dim, 8, max_batch=1024)
+    oc = O.OracleCache(cap, dim, 8)
+    keys = rs.integers(0, 2**63, 300).astype(np.uint64)
+    vecs = rs.standard_normal((300, dim)).astype(np.float32)
+    vers = np.arange(1, 301, dtype=np.uint64)
+    c.insert(t64(keys), torch.from_numpy(vecs).cuda(), t64(vers))
+    oc.insert(keys, vecs, vers)
+    q = np.concatenate([keys[:150], rs.integers(0, 2**63, 50).astype(np.uint64)])
+    fi, fv, mi = c.query(t64(q))
+    ofi, ofv, omi = oc.query(q)
+    ctx.sync()
+    np.testing.assert_array_equal(fi.cpu().numpy(), ofi)
+    np.testing.assert_array_equal(mi.cpu().numpy(), omi)
+    assert np.array_equal(fv.cpu().numpy().view(np.uint32), np.asarray(ofv, np.float32).view(np.uint32))
+    new = (vecs[:100] * 2).astype(np.float32)
+    c.refresh(t64(keys[:100]), torch.from_numpy(new).cuda(), t64(vers[:100] + np.uint64(1000)))
+    oc.refresh(keys[:100], new, vers[:100] + np.uint64(1000))
+    fi, fv, mi = c.query(t64(keys[:100]))
+    ofi, ofv, omi = oc.query(keys[:100])
+    ctx.sync()
+    assert np.array_equal(fv.cpu().numpy().view(np.uint32), np.asarray(ofv, np.float32).view(np.uint32))
+    assert c.stats() == oc.stats()
