@@ -152,6 +152,11 @@ int hps_gpu_table_insert(hps_gpu_table tbl, uint32_t table, const uint64_t* keys
 /* rows_out[i] = row id of keys[i] in `table`, or UINT64_MAX when absent. */
 int hps_gpu_table_find(hps_gpu_table tbl, uint32_t table, const uint64_t* keys, uint64_t n,
                        uint64_t* rows_out);
+/* The same lookup with another probe scheme (A/B evidence): group 1 = the
+ * per-thread linear probe of hps_gpu_table_find; 2, 4, 8 = warp-cooperative probing, that
+ * many lanes reading consecutive slots of an aligned window per step. Identical results. */
+int hps_gpu_debug_find_variant(hps_gpu_table tbl, uint32_t table, const uint64_t* keys, uint64_t n,
+                               uint64_t* rows_out, uint32_t group);
 /* Copy rows [row_begin, row_begin+n) of `table` (weights, and when state != NULL the
  * optimizer state rows: state[k] for k < n_state_rows) out as fp32 [n x dim]. */
 int hps_gpu_table_export(hps_gpu_table tbl, uint32_t table, uint64_t row_begin, uint64_t n,

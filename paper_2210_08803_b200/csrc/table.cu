@@ -41,6 +41,48 @@ __device__ __forceinline__ uint32_t probe_find(const Slot* __restrict__ slots, c
   return kRowEmpty;
 }
 
+// Warp-cooperative probing (north_star (1)): G lanes examine G consecutive slots of an aligned
+// window at once (one 16*G-byte coalesced load), ballot for the first match or empty slot in
+// linear-probe order from the home slot — the same answer as probe_find. Kept as the measured
+// alternative (hps_gpu_debug_find_variant): at load <= 0.5 the per-thread probe
+// ends in ~1.5 slots, so the group's extra lanes are mostly wasted issue slots.
+template <int G>
+__device__ __forceinline__ uint32_t probe_find_coop(const Slot* __restrict__ slots, const TableDev& td, uint64_t key,
+                                                    uint32_t gl, uint32_t gmask) {
+  const uint64_t home = hps::key_hash(key) & td.slot_mask;
+  const Slot* base = slots + td.slot_base;
+  uint64_t w = home & ~uint64_t(G - 1);
+  uint32_t skip = static_cast<uint32_t>(home - w);  // lanes before the home slot (first window only)
+  for (uint64_t p = 0; p <= td.slot_mask; p += G) {
+    const Slot s = load_slot(base + ((w + gl) & td.slot_mask));
+    const bool valid = gl >= skip;
+    const uint32_t hit = __ballot_sync(gmask, valid && s.key == key && s.row != kRowEmpty);
+    const uint32_t emp = __ballot_sync(gmask, valid && s.row == kRowEmpty);
+    const uint32_t sh = __ffs(gmask) - 1;  // the group's first lane
+    const uint32_t h = hit >> sh, e = emp >> sh;
+    if (h | e) {
+      const int first = __ffs(h | e) - 1;
+      if (!((h >> first) & 1u)) return kRowEmpty;
+      return __shfl_sync(gmask, s.row, static_cast<int>(sh) + first);
+    }
+    w += G;
+    skip = 0;
+  }
+  return kRowEmpty;
+}
+
+template <int G>
+__global__ void k_find_coop(const Slot* __restrict__ slots, TableDev td, const uint64_t* __restrict__ keys, uint64_t n,
+                            uint64_t* __restrict__ rows_out) {
+  const uint32_t lane = lane_id(), gl = lane % G;
+  const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane - gl);
+  const uint64_t groups = (uint64_t(gridDim.x) * blockDim.x) / G;
+  for (uint64_t i0 = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) / G; i0 < n; i0 += groups) {
+    const uint32_t r = probe_find_coop<G>(slots, td, keys[i0], gl, gmask);
+    if (gl == 0) rows_out[i0] = r == kRowEmpty ? ~0ull : r;
+  }
+}
+
 __global__ void k_find(const Slot* __restrict__ slots, TableDev td, const uint64_t* __restrict__ keys, uint64_t n,
                        uint64_t* __restrict__ rows_out) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -1339,6 +1381,27 @@ int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64
 }
 
 extern "C" {
+
+// A/B of the probe scheme: group = 1 is hps_gpu_table_find's per-thread linear
+// probe, 2/4/8 the warp-cooperative window probe.
+int hps_gpu_debug_find_variant(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, uint64_t* rows_out,
+                               uint32_t group) {
+  if (int s = check_tbl(t)) return s;
+  if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
+  if (n == 0) return HPS_GPU_OK;
+  if (!keys || !rows_out) return HPS_GPU_E_INVALID_ARGUMENT;
+  cudaStream_t st = t->ctx->stream;
+  const TableDev td = t->h_tables[table];
+  switch (group) {
+    case 1: return hps_gpu_table_find(t, table, keys, n, rows_out);
+    case 2: k_find_coop<2><<<grid_for(n * 2, 256, kNumSMs * 32), 256, 0, st>>>(t->d_slots, td, keys, n, rows_out); break;
+    case 4: k_find_coop<4><<<grid_for(n * 4, 256, kNumSMs * 32), 256, 0, st>>>(t->d_slots, td, keys, n, rows_out); break;
+    case 8: k_find_coop<8><<<grid_for(n * 8, 256, kNumSMs * 32), 256, 0, st>>>(t->d_slots, td, keys, n, rows_out); break;
+    default: return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  HPSG_CHECK_LAUNCH("k_find_coop");
+  return HPS_GPU_OK;
+}
 
 int hps_gpu_table_find(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, uint64_t* rows_out) {
   if (int s = check_tbl(t)) return s;

@@ -69,3 +69,31 @@ def test_gen_keys_matches_workload(ctx):
     got = ctx.gen_keys(1234, 10, 1000).cpu().numpy().view(np.uint64)
     want = W.mix64(np.uint64(1234) ^ (np.arange(1000, dtype=np.uint64) + np.uint64(10)))
     np.testing.assert_array_equal(got, want)
+
+
+@pytest.mark.parametrize("group", [2, 4, 8])
+def test_warp_cooperative_probe_matches_per_thread(ctx, group):
+    """hps_gpu_debug_find_variant: the warp-cooperative window probe returns exactly the rows
+    of the per-thread linear probe (hps_gpu_table_find), present and absent keys, at the
+    index's full load (capacity rows inserted: load 0.5) and with wrap-around windows."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    from paper_2210_08803_b200 import EmbeddingTableGroup
+    from paper_2210_08803_b200 import _lib as L
+    rs = np.random.default_rng(group)
+    cap = 50_000
+    g = EmbeddingTableGroup(ctx, [cap, 64], 4, [0, 1], "sgd", 1 << 16, 1 << 16, 1)
+    ks = rs.integers(0, 2**63, cap).astype(np.uint64)
+    g.insert(0, torch.from_numpy(ks.view(np.int64)).cuda(), return_rows=False)
+    q = np.concatenate([ks, rs.integers(0, 2**63, 20_000).astype(np.uint64)])
+    rs.shuffle(q)
+    qt = torch.from_numpy(q.view(np.int64)).cuda()
+    a = torch.empty(len(q), dtype=torch.int64, device="cuda")
+    b = torch.empty_like(a)
+    L.check(ctx.lib.hps_gpu_table_find(g.h, 0, C.c_void_p(qt.data_ptr()), len(q), C.c_void_p(a.data_ptr())), "find")
+    L.check(ctx.lib.hps_gpu_debug_find_variant(g.h, 0, C.c_void_p(qt.data_ptr()), len(q), C.c_void_p(b.data_ptr()),
+                                               group), "find_variant")
+    ctx.sync()
+    assert torch.equal(a, b)
+    assert int((a >= 0).sum()) == cap
