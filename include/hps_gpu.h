@@ -86,6 +86,20 @@ int hps_gpu_partition_of(hps_gpu_ctx ctx, const uint64_t* keys, uint64_t n,
                          uint32_t num_shards, uint32_t* shard_out);
 /* flag_out[0] = 1 if any of v[0..n) is NaN/Inf else 0 (kernels.hpp:41-43 semantics). */
 int hps_gpu_has_non_finite_f32(hps_gpu_ctx ctx, const float* v, uint64_t n, uint32_t* flag_out);
+/* The rest of the reference's kernel API (proj/include/hps/kernels.hpp:33-43) over device
+ * buffers, bit-equivalent to its scalar path (kernels_scalar.cpp:25-123; golden vectors
+ * from the reference's compiled code): binary16 narrowing (round to nearest even, overflow
+ * -> the infinity pattern, NaN payload kept + quiet bit), exact widening, the binary16
+ * NaN/Inf scan (*flag_out = 1 if any), and CRC-32C (Castagnoli) — of one buffer continuing
+ * from the running value `crc` (start from 0; scratch: one device u32), or one CRC (from 0)
+ * per record [offsets[r], offsets[r+1]) of `data` (the PDB log-record checksum). */
+int hps_gpu_f32_to_f16(hps_gpu_ctx ctx, const float* src, uint16_t* dst, uint64_t n);
+int hps_gpu_f16_to_f32(hps_gpu_ctx ctx, const uint16_t* src, float* dst, uint64_t n);
+int hps_gpu_has_non_finite_f16(hps_gpu_ctx ctx, const uint16_t* v, uint64_t n, uint32_t* flag_out);
+int hps_gpu_crc32c(hps_gpu_ctx ctx, uint32_t crc, const void* data, uint64_t n, uint32_t* scratch,
+                   uint32_t* crc_out);
+int hps_gpu_crc32c_batch(hps_gpu_ctx ctx, const void* data, const uint64_t* offsets, uint64_t n_records,
+                         uint32_t* crc_out);
 
 /* ---- embedding table group (K2..K5) ------------------------------------------
  * A table group holds n_tables independent tables (key namespaces)

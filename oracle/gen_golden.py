@@ -89,6 +89,33 @@ def main():
     h16 = {"finite": [0x3C00, 0x7BFF], "inf": [0x7C00], "nan": [0x3C00, 0x7E01]}
     g["has_non_finite_f16"] = {k: {"bits": v, "non_finite": int(lib.ref_has_non_finite_f16((C.c_uint16 * len(v))(*v), len(v)))} for k, v in h16.items()}
     g["crc32c_123456789"] = lib.ref_crc32c(0, b"123456789", 9)
+    # CRC-32C of seeded buffers (bytes = low byte of a splitmix64 stream), lengths across the
+    # GPU kernel's chunk edges, plain and continuing from a running value; and per-record CRCs
+    blob = bytes(x & 0xFF for x in splitmix_stream(0xC5C, 1 << 18))
+    lens = [0, 1, 2, 3, 7, 8, 9, 63, 64, 65, 255, 256, 511, 512, 513, 1000, 4096, 4109, 65537, 1 << 18]
+    g["crc32c"] = {"blob_seed": 0xC5C, "blob_len": len(blob),
+                   "cases": [{"len": n, "crc_in": 0, "crc": lib.ref_crc32c(0, blob[:n], n)} for n in lens] +
+                            [{"len": n, "crc_in": 0xDEADBEEF, "crc": lib.ref_crc32c(0xDEADBEEF, blob[:n], n)}
+                             for n in (5, 777, 1 << 18)]}
+    offs = [0]
+    for x in splitmix_stream(0x0FF5, 300):
+        offs.append(min(len(blob), offs[-1] + int(x % 3000)))
+    g["crc32c"]["batch_offsets"] = offs
+    g["crc32c"]["batch_crc"] = [lib.ref_crc32c(0, blob[a:b], b - a) for a, b in zip(offs[:-1], offs[1:])]
+    # binary16 widening over all 65,536 patterns, narrowing over 2^20 seeded f32 patterns
+    # (NaN payloads, infinities, subnormals included): sha256 of the reference's outputs
+    import hashlib
+    allh = (C.c_uint16 * 65536)(*range(65536))
+    wide = (C.c_float * 65536)()
+    lib.ref_force_scalar(1)
+    lib.ref_f16_to_f32(allh, wide, 65536)
+    g["f16_to_f32_all_sha256"] = hashlib.sha256(bytes(wide)).hexdigest()
+    bits = [x & 0xFFFFFFFF for x in splitmix_stream(0xF16, 1 << 20)]
+    src = (C.c_uint32 * len(bits))(*bits)
+    nar = (C.c_uint16 * len(bits))()
+    lib.ref_f32_to_f16(C.cast(src, C.POINTER(C.c_float)), nar, len(bits))
+    lib.ref_force_scalar(0)
+    g["f32_to_f16_sample"] = {"seed": 0xF16, "n": len(bits), "sha256": hashlib.sha256(bytes(nar)).hexdigest()}
     g["error_code_name"] = {str(c): lib.ref_error_code_name(c).decode() for c in range(0, 19)}
     g["validate_dim"] = {str(d): lib.ref_validate_dim(d) for d in [0, 1, 16, 4096, 4097, 65535]}
     ev = {}

@@ -138,6 +138,11 @@ SIGNATURES = {
     "hps_gpu_lookup_pooled": (i32, [vp, vp, vp, u32, i32, vp, u32]),
     "hps_gpu_backward_update": (i32, [vp, vp, C.POINTER(OptParams)]),
     "hps_gpu_table_set_pipeline": (i32, [vp, u32]),
+    "hps_gpu_f32_to_f16": (i32, [vp, vp, vp, u64]),
+    "hps_gpu_f16_to_f32": (i32, [vp, vp, vp, u64]),
+    "hps_gpu_has_non_finite_f16": (i32, [vp, vp, u64, vp]),
+    "hps_gpu_crc32c": (i32, [vp, u32, vp, u64, vp, vp]),
+    "hps_gpu_crc32c_batch": (i32, [vp, vp, vp, u64, vp]),
     "hps_gpu_debug_find_variant": (i32, [vp, u32, vp, u64, vp, u32]),
     "hps_gpu_nccl_unique_id": (i32, [vp]),
     "hps_gpu_ctx_comm_init": (i32, [vp, vp, i32, i32]),

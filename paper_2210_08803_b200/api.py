@@ -82,6 +82,35 @@ class Context:
         buf = C.create_string_buffer(bytes(unique_id), L.NCCL_ID_BYTES)
         L.check(self.lib.hps_gpu_ctx_comm_init(self.h, buf, rank, world), "ctx_comm_init")
 
+    # -- the reference's kernel API on the device (proj/include/hps/kernels.hpp:33-43) ---------
+    def f32_to_f16(self, x: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(x.numel(), dtype=torch.int16, device=x.device)
+        L.check(self.lib.hps_gpu_f32_to_f16(self.h, _ptr(x), _ptr(out), x.numel()), "f32_to_f16")
+        return out
+
+    def f16_to_f32(self, bits: torch.Tensor) -> torch.Tensor:
+        out = torch.empty(bits.numel(), dtype=torch.float32, device=bits.device)
+        L.check(self.lib.hps_gpu_f16_to_f32(self.h, _ptr(bits), _ptr(out), bits.numel()), "f16_to_f32")
+        return out
+
+    def has_non_finite_f16(self, bits: torch.Tensor) -> bool:
+        flag = torch.zeros(1, dtype=torch.int32, device=bits.device)
+        L.check(self.lib.hps_gpu_has_non_finite_f16(self.h, _ptr(bits), bits.numel(), _ptr(flag)), "non_finite_f16")
+        return bool(flag.item())
+
+    def crc32c(self, data: torch.Tensor, crc: int = 0) -> int:
+        """CRC-32C of a uint8 device buffer, continuing from `crc` (kernels.hpp:38-39)."""
+        tmp = torch.zeros(2, dtype=torch.int32, device=data.device)
+        L.check(self.lib.hps_gpu_crc32c(self.h, crc, _ptr(data), data.numel(), _ptr(tmp),
+                                        C.c_void_p(tmp.data_ptr() + 4)), "crc32c")
+        return int(tmp[1].item()) & 0xFFFFFFFF
+
+    def crc32c_batch(self, data: torch.Tensor, offsets: torch.Tensor) -> torch.Tensor:
+        n = offsets.numel() - 1
+        out = torch.empty(max(n, 1), dtype=torch.int32, device=data.device)
+        L.check(self.lib.hps_gpu_crc32c_batch(self.h, _ptr(data), _ptr(offsets), n, _ptr(out)), "crc32c_batch")
+        return out[:n]
+
     def gen_keys(self, seed: int, first: int, n: int) -> torch.Tensor:
         out = torch.empty(n, dtype=torch.int64, device=f"cuda:{self.device}")
         L.check(self.lib.hps_gpu_gen_keys(self.h, seed, first, n, _ptr(out)), "gen_keys")

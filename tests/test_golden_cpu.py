@@ -145,3 +145,28 @@ def test_oracle_f16_matches_reference():
     L.orc_f32_to_f16(O.P(x), O.P(nar), len(x))
     with np.errstate(over="ignore"):
         np.testing.assert_array_equal(nar, x.astype(np.float16).view(np.uint16))
+
+
+def test_crc32c_golden_cases_restated():
+    """The golden CRC-32C cases (recorded from the reference) against a table-driven
+    restatement of kernels_scalar.cpp:89-108 — pins the fixture the GPU test reads."""
+    from paper_2210_08803_b200 import workload as W
+    tbl = []
+    for i in range(256):
+        c = i
+        for _ in range(8):
+            c = (0x82F63B78 ^ (c >> 1)) if c & 1 else c >> 1
+        tbl.append(c)
+
+    def crc(c, data):
+        c ^= 0xFFFFFFFF
+        for b in data:
+            c = tbl[(c ^ b) & 0xFF] ^ (c >> 8)
+        return c ^ 0xFFFFFFFF
+    g = G["crc32c"]
+    blob = bytes((W.rng(g["blob_seed"], np.arange(g["blob_len"], dtype=np.uint64)) & np.uint64(0xFF)).astype(np.uint8))
+    for c in g["cases"]:
+        if c["len"] <= 70000:
+            assert crc(c["crc_in"], blob[:c["len"]]) == c["crc"]
+    o = g["batch_offsets"]
+    assert [crc(0, blob[a:b]) for a, b in zip(o[:20], o[1:21])] == g["batch_crc"][:20]
