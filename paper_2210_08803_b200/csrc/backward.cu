@@ -1454,14 +1454,28 @@ cudaError_t dedup_attributes() {
 }
 }  // namespace
 
-int hpsg::check_dedup_residency() {
+// Which dedup a table runs: the persistent kernel (one CTA per SM, shared-memory
+// aggregation per CTA chunk: Zipf-hot rows take one global atomic per CTA) when one of its
+// CTAs fits every SM of this device, else the flat three-kernel dedup (no grid barrier, so
+// no co-residency requirement: MIG slices, smaller parts). HPS_GPU_DEDUP=flat|persistent
+// forces one (A/B). Measured on config 2/3/5 (profiles/round2): persistent <= flat on every
+// config; config 3 (Zipf multi-hot) 0.66 vs 0.70 ms.
+int hpsg::choose_dedup(bool* flat_out) {
   HPSG_CUDA(dedup_attributes());
   int per_sm = 0;
   HPSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dedup, kDedupBlock, size_t(2) * kDedupHash * 4));
-  if (per_sm < 1) {
-    set_last_error("k_dedup (persistent, grid barriers) cannot keep one CTA resident per SM on this device");
-    return HPS_GPU_E_NO_DEVICE;
+  bool flat = per_sm < 1;
+  if (const char* e = std::getenv("HPS_GPU_DEDUP")) {
+    if (std::strcmp(e, "flat") == 0) flat = true;
+    if (std::strcmp(e, "persistent") == 0) {
+      if (per_sm < 1) {
+        set_last_error("k_dedup (persistent, grid barriers) cannot keep one CTA resident per SM on this device");
+        return HPS_GPU_E_NO_DEVICE;
+      }
+      flat = false;
+    }
   }
+  *flat_out = flat;
   return HPS_GPU_OK;
 }
 
@@ -1474,11 +1488,7 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
   uint32_t* z = t->ws_zero;
   const BwdArgs a = base_args(t);
   // K4a-c: counts, allocation, placement (first on this stream after the fork: a plain launch)
-  static const bool flat = [] {
-    const char* e = std::getenv("HPS_GPU_DEDUP");  // A/B knob: "flat" (default) or "persistent"
-    return !(e && std::strcmp(e, "persistent") == 0);
-  }();
-  if (flat) {
+  if (t->flat_dedup) {
     HPSG_CUDA(dedup_attributes());
     const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(nk));
     HPSG_CUDA(launch_k(false, k_count_flat, grid_for(nk, 256, 1 << 30), 256, 0, st, a));

@@ -1159,8 +1159,10 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
     return HPS_GPU_E_INVALID_ARGUMENT;
   }
   HPSG_CUDA(cudaSetDevice(ctx->device));
-  if (int s = check_dedup_residency()) return s;
+  bool flat_dedup = false;
+  if (int s = choose_dedup(&flat_dedup)) return s;
   auto t = new hps_gpu_table_s;
+  t->flat_dedup = flat_dedup;
   t->ctx = ctx;
   t->n_tables = cfg->n_tables;
   t->dim_io = cfg->dim;

@@ -49,7 +49,7 @@ inline uint64_t bwd_max_nodes(uint64_t max_keys) { return bwd_max_chunks(max_key
 struct hps_gpu_table_s;
 namespace hpsg {
 int launch_dedup(hps_gpu_table_s* t, cudaStream_t st);  // backward.cu: K4a-K4d (on t->side)
-int check_dedup_residency();  // backward.cu: one persistent k_dedup CTA must fit an SM of the current device
+int choose_dedup(bool* flat_out);  // backward.cu: persistent k_dedup if one CTA fits every SM, else flat
 // table.cu: hps_gpu_table_read_through + the source tier of every key (src_out[i]: 0 cache,
 // 1 table, 3 default vector; may be NULL)
 int table_read_through(hps_gpu_table_s* t, uint32_t table, const uint64_t* keys, const float* found_vecs,
@@ -150,7 +150,8 @@ struct hps_gpu_table_s : BatchSlot {
   uint32_t cur = 0;
   cudaEvent_t ev_last_dedup = nullptr;  // the last k_dedup launched (prefetches serialise on it)
   bool last_dedup_valid = false;
-  bool graphs_seen = false;  // a training record was captured into a graph (host slot flags may lag replays)
+  bool graphs_seen = false;
+  bool flat_dedup = false;   // the three-kernel dedup (choose_dedup at create)  // a training record was captured into a graph (host slot flags may lag replays)
   unsigned long long last_dedup_capture = 0;
   bool no_fork = false;         // HPS_GPU_NO_FORK=1: everything on the main stream (A/B measurement)
   bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)
