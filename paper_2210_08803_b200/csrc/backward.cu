@@ -1135,8 +1135,7 @@ constexpr int kMidBlock = 256;
 template <int OPT, int VPL>
 __global__ void __launch_bounds__(kMidBlock) k_reduce_mid(BwdArgs a) {
   extern __shared__ __align__(16) float4 s_part[];  // [kChunk][VPL * 32] float4
-  __shared__ uint32_t s_arr[kMidMax];  // the segment's bags in arrival order
-  __shared__ uint32_t s_bag[kMidMax];  // ... in canonical order
+  __shared__ uint32_t s_bag[kMidMax];
   pdl_wait();
   pdl_launch_dependents();
   const uint64_t M = *a.mid_alloc >> 32;
@@ -1147,21 +1146,26 @@ __global__ void __launch_bounds__(kMidBlock) k_reduce_mid(BwdArgs a) {
   for (uint64_t j = blockIdx.x; j < M; j += gridDim.x) {
     const uint4 rec = a.mid_rec[j];  // {row, first, len, entry}
     const uint32_t len = rec.z;
-    // canonical order by counting: an element's rank = elements with a smaller bag (ties by
-    // arrival index); every thread reads the same s_arr word at a time (broadcast)
-    for (uint32_t i = threadIdx.x; i < len; i += kMidBlock) s_arr[i] = a.short_bag[rec.y + i];
+    uint32_t P = 64;
+    while (P < len) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += kMidBlock) s_bag[i] = i < len ? a.short_bag[rec.y + i] : 0xffffffffu;
     if (threadIdx.x == 0) a.bt[rec.w] = make_uint2(kBtEmpty, 0xffffffffu);  // placement is done with it
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < len; i += kMidBlock) {
-      const uint32_t b = s_arr[i];
-      uint32_t r = 0;
-      for (uint32_t q = 0; q < len; ++q) {
-        const uint32_t x = s_arr[q];
-        r += (x < b || (x == b && q < i)) ? 1u : 0u;
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+      for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+        for (uint32_t i = threadIdx.x; i < P; i += kMidBlock) {
+          const uint32_t ixj = i ^ jj;
+          if (ixj > i) {
+            const uint32_t x = s_bag[i], y = s_bag[ixj];
+            if ((x > y) == ((i & k) == 0)) {
+              s_bag[i] = y;
+              s_bag[ixj] = x;
+            }
+          }
+        }
+        __syncthreads();
       }
-      s_bag[r] = b;
     }
-    __syncthreads();
     const uint32_t m = (len + kChunk - 1) / kChunk;
     for (uint32_t c = w; c < m; c += kWarps) {
       const uint32_t s0 = c * kChunk, n = min(kChunk, len - s0);
@@ -1218,7 +1222,7 @@ int launch_mid(const BwdArgs& a, cudaStream_t st, bool pdl, uint32_t nvec) {
       if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) return e;
       return prefer_max_smem(kern);
     }));
-    HPSG_CUDA(launch_k(pdl, kern, kNumSMs * 6, kMidBlock, smem, st, a));
+    HPSG_CUDA(launch_k(pdl, kern, kNumSMs * 2, kMidBlock, smem, st, a));
     return HPS_GPU_OK;
   };
   if (vpl == 1) return go(k_reduce_mid<OPT, 1>);
