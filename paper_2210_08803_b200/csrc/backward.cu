@@ -54,9 +54,6 @@ struct BwdArgs {
   uint32_t row_absent;
   unsigned long long* short_alloc;  // (segments << 32) | occurrences
   uint4* short_rec;                 // {row, first, len, batch-table entry}
-  unsigned long long* mid_alloc;    // mid segments: (segments << 32) | occurrences
-  uint4* mid_rec;                   // {row, first, len, batch-table entry}
-  uint32_t mid_top;                 // mid bag ranges are carved from the top of short_bag down
   uint32_t* short_bag;
   uint32_t* n_long;
   uint32_t* long_row;
@@ -122,41 +119,6 @@ __device__ __forceinline__ uint32_t bt_insert_from(uint2* bt, uint64_t mask, uin
 }
 __device__ __forceinline__ uint32_t bt_insert(uint2* bt, uint64_t mask, uint32_t row) {
   return bt_insert_from(bt, mask, row, bt_home(row, mask));
-}
-
-// Allocation of a leader whose count exceeds kChunk (every lane of the warp calls it): mid
-// segments (<= kMidMax) take a bag range carved from the top of short_bag (one packed atomic
-// per warp) and a mid record; long ones an id of the long list.
-__device__ __forceinline__ void alloc_mid_long(const BwdArgs& a, uint32_t row, uint32_t ent, uint32_t len) {
-  const uint32_t lane = lane_id(), lt = lanemask_lt();
-  const bool md = len > kChunk && len <= kMidMax, lg = len > kMidMax;
-  if (__ballot_sync(0xffffffffu, md)) {
-    const unsigned long long mine = md ? ((1ull << 32) | len) : 0ull;
-    const unsigned long long incl = warp_incl_scan(mine);
-    unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(a.mid_alloc, incl);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    if (md) {
-      const unsigned long long pos = base + incl - mine;
-      const uint32_t j = static_cast<uint32_t>(pos >> 32), first = a.mid_top - static_cast<uint32_t>(pos) - len;
-      a.mid_rec[j] = make_uint4(row, first, len, ent);
-      a.bt[ent].y = first;
-    }
-  }
-  const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
-  if (lg_mask) {
-    const int src = __ffs(lg_mask) - 1;
-    uint32_t j0 = 0;
-    if (static_cast<int>(lane) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
-    j0 = __shfl_sync(0xffffffffu, j0, src);
-    if (lg) {
-      const uint32_t j = j0 + __popc(lg_mask & lt);
-      a.long_row[j] = row;
-      a.long_ent[j] = ent;
-      a.long_len[j] = len;
-      a.bt[ent].y = kLongFlag | j;
-    }
-  }
 }
 
 // ---- K4a-c fused: counts, allocation, placement in ONE persistent cooperative kernel ------
@@ -349,14 +311,27 @@ __global__ void __launch_bounds__(kDedupBlock, 2) k_dedup(BwdArgs a, uint32_t* c
     run += ttotal;
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      const bool sh = len[k] && len[k] <= kChunk;
+      const bool sh = len[k] && len[k] <= kChunk, lg = len[k] > kChunk;
       if (sh) {
         const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
         a.short_rec[seg] = make_uint4(a.occ_row[occ[k]], first, len[k], ent[k]);
         a.bt[ent[k]].y = first;
         pos += (1ull << 32) | len[k];
       }
-      alloc_mid_long(a, len[k] > kChunk ? a.occ_row[occ[k]] : 0u, ent[k], len[k]);
+      const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
+      if (lg_mask) {
+        const int src = __ffs(lg_mask) - 1;
+        uint32_t j0 = 0;
+        if (static_cast<int>(lane) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
+        j0 = __shfl_sync(0xffffffffu, j0, src);
+        if (lg) {
+          const uint32_t j = j0 + __popc(lg_mask & lt);
+          a.long_row[j] = a.occ_row[occ[k]];
+          a.long_ent[j] = ent[k];
+          a.long_len[j] = len[k];
+          a.bt[ent[k]].y = kLongFlag | j;
+        }
+      }
     }
   }
   trace_end(kTrAlloc);
@@ -494,14 +469,27 @@ __global__ void __launch_bounds__(256) k_alloc_flat(BwdArgs a) {
 #pragma unroll
   for (int k = 0; k < kAllocIPT; ++k) {
     const uint64_t i = b0 + threadIdx.x * kAllocIPT + k;
-    const bool sh = len[k] && len[k] <= kChunk;
+    const bool sh = len[k] && len[k] <= kChunk, lg = len[k] > kChunk;
     if (sh) {
       const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
       a.short_rec[seg] = make_uint4(a.occ_row[i], first, len[k], ent[k]);
       a.bt[ent[k]].y = first;
       pos += (1ull << 32) | len[k];
     }
-    alloc_mid_long(a, len[k] > kChunk ? a.occ_row[i] : 0u, ent[k], len[k]);
+    const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
+    if (lg_mask) {
+      const int src = __ffs(lg_mask) - 1;
+      uint32_t j0 = 0;
+      if (static_cast<int>(lane_id()) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
+      j0 = __shfl_sync(0xffffffffu, j0, src);
+      if (lg) {
+        const uint32_t j = j0 + __popc(lg_mask & lt);
+        a.long_row[j] = a.occ_row[i];
+        a.long_ent[j] = ent[k];
+        a.long_len[j] = len[k];
+        a.bt[ent[k]].y = kLongFlag | j;
+      }
+    }
   }
   trace_end(kTrAlloc);
 }
@@ -556,7 +544,7 @@ struct LongRegOp {
   }
   __device__ void total(uint64_t t) const {
     *a.long_chunks = t >> 32;
-    const_cast<uint64_t*>(a.counts)[1] = (*a.short_alloc >> 32) + (*a.mid_alloc >> 32) + *a.n_long;
+    const_cast<uint64_t*>(a.counts)[1] = (*a.short_alloc >> 32) + *a.n_long;
   }
 };
 
@@ -1124,113 +1112,6 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
   }
 }
 
-// ---- mid segments (kChunk < len <= kMidMax): one CTA per segment -----------------------------
-// The CTA stages the segment's bags (arrival order) in shared memory and sorts them back into
-// canonical order (bitonic, ascending bag = canonical: equal bags carry equal gradients); its
-// warps sum the level-1 chunks of 32 in order (rows 8 in flight), the chunk partials land in
-// shared memory, warp 0 sums them in order (the tree's second and last level: <= 32 chunks)
-// and applies the optimizer. The whole 32-ary blocked tree of DESIGN.md §4.3 in one CTA, no
-// global sort, no tree-node counters.
-constexpr int kMidBlock = 256;
-template <int OPT, int VPL>
-__global__ void __launch_bounds__(kMidBlock) k_reduce_mid(BwdArgs a) {
-  extern __shared__ __align__(16) float4 s_part[];  // [kChunk][VPL * 32] float4
-  __shared__ uint32_t s_bag[kMidMax];
-  pdl_wait();
-  pdl_launch_dependents();
-  const uint64_t M = *a.mid_alloc >> 32;
-  const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
-  constexpr uint32_t kWarps = kMidBlock / 32;
-  const bool mean = a.bag_len != nullptr;
-  trace_begin(kTrMid);
-  for (uint64_t j = blockIdx.x; j < M; j += gridDim.x) {
-    const uint4 rec = a.mid_rec[j];  // {row, first, len, entry}
-    const uint32_t len = rec.z;
-    uint32_t P = 64;
-    while (P < len) P <<= 1;
-    for (uint32_t i = threadIdx.x; i < P; i += kMidBlock) s_bag[i] = i < len ? a.short_bag[rec.y + i] : 0xffffffffu;
-    if (threadIdx.x == 0) a.bt[rec.w] = make_uint2(kBtEmpty, 0xffffffffu);  // placement is done with it
-    __syncthreads();
-    for (uint32_t k = 2; k <= P; k <<= 1) {
-      for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-        for (uint32_t i = threadIdx.x; i < P; i += kMidBlock) {
-          const uint32_t ixj = i ^ jj;
-          if (ixj > i) {
-            const uint32_t x = s_bag[i], y = s_bag[ixj];
-            if ((x > y) == ((i & k) == 0)) {
-              s_bag[i] = y;
-              s_bag[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
-      }
-    }
-    const uint32_t m = (len + kChunk - 1) / kChunk;
-    for (uint32_t c = w; c < m; c += kWarps) {
-      const uint32_t s0 = c * kChunk, n = min(kChunk, len - s0);
-      const uint32_t my_bag = lane < n ? s_bag[s0 + lane] : 0u;
-      const float my_f = (mean && lane < n) ? static_cast<float>(a.bag_len[my_bag]) : 1.f;
-      float4 acc[VPL];
-      constexpr int RB = VPL >= 4 ? 2 : 8 / VPL;  // rows in flight
-      for (uint32_t q0 = 0; q0 < n; q0 += RB) {
-        float4 x[RB][VPL];
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-          const uint32_t q = q0 + r;
-          const uint32_t b = __shfl_sync(0xffffffffu, my_bag, q & 31);
-          const float f = __shfl_sync(0xffffffffu, my_f, q & 31);
-          if (q < n) {
-            load_grad<VPL>(a, b, lane, 32, x[r]);
-            scale_grad<VPL>(f, mean, x[r]);
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < RB; ++r) {
-          if (q0 + r >= n) break;
-#pragma unroll
-          for (int k = 0; k < VPL; ++k) acc[k] = (q0 + r == 0) ? x[r][k] : f4_add(acc[k], x[r][k]);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) s_part[size_t(c) * VPL * 32 + k * 32 + lane] = acc[k];
-    }
-    __syncthreads();
-    if (w == 0) {
-      float4 g[VPL];
-#pragma unroll
-      for (int k = 0; k < VPL; ++k) g[k] = s_part[k * 32 + lane];
-      for (uint32_t c = 1; c < m; ++c)
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) g[k] = f4_add(g[k], s_part[size_t(c) * VPL * 32 + k * 32 + lane]);
-      RowState<OPT, VPL> rs;
-      load_row<OPT, VPL>(a, rec.x, lane, 32, rs);
-      update_store<OPT, VPL>(a, rec.x, lane, 32, rs, g);
-    }
-    __syncthreads();  // s_bag and s_part are reused by the next segment
-  }
-  trace_end(kTrMid);
-}
-
-template <int OPT>
-int launch_mid(const BwdArgs& a, cudaStream_t st, bool pdl, uint32_t nvec) {
-  const int vpl = nvec <= 32 ? 1 : nvec <= 64 ? 2 : nvec <= 128 ? 4 : 8;
-  const size_t smem = size_t(kChunk) * vpl * 32 * sizeof(float4);
-  auto go = [&](auto kern) -> int {
-    static std::atomic<uint64_t> attr{0};
-    HPSG_CUDA(once_per_device(attr, [&]() -> cudaError_t {
-      if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))) return e;
-      return prefer_max_smem(kern);
-    }));
-    HPSG_CUDA(launch_k(pdl, kern, kNumSMs * 2, kMidBlock, smem, st, a));
-    return HPS_GPU_OK;
-  };
-  if (vpl == 1) return go(k_reduce_mid<OPT, 1>);
-  if (vpl == 2) return go(k_reduce_mid<OPT, 2>);
-  if (vpl == 4) return go(k_reduce_mid<OPT, 4>);
-  return go(k_reduce_mid<OPT, 8>);
-}
-
 // ---- long segments: the tree above level 1 ----------------------------------------------
 // Level-1 chunk c of segment j is complete in partial[base_j + c]. The warp counts itself
 // into its parent node; the last of the parent's (<= 32) children sums them in order into
@@ -1442,22 +1323,19 @@ __global__ void k_copy_counted(const uint32_t* __restrict__ src, const uint64_t*
     dst[i] = src[i];
 }
 
-__global__ void k_unique_count(const unsigned long long* short_alloc, const unsigned long long* mid_alloc,
-                               const uint32_t* n_long, uint64_t* count_out) {
+__global__ void k_unique_count(const unsigned long long* short_alloc, const uint32_t* n_long, uint64_t* count_out) {
   pdl_wait();
   pdl_launch_dependents();
-  if (threadIdx.x == 0) *count_out = (*short_alloc >> 32) + (*mid_alloc >> 32) + *n_long;
+  if (threadIdx.x == 0) *count_out = (*short_alloc >> 32) + *n_long;
 }
 
-// Rows updated by the last backward (short + mid + long segments), unsorted; count -> *count_out.
-__global__ void k_unique_rows(const uint4* short_rec, const unsigned long long* short_alloc, const uint4* mid_rec,
-                              const unsigned long long* mid_alloc, const uint32_t* long_row, const uint32_t* n_long,
-                              uint32_t* out, uint64_t* count_out) {
-  const uint64_t S = *short_alloc >> 32, M = *mid_alloc >> 32, L = *n_long;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *count_out = S + M + L;
-  for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < S + M + L;
-       u += uint64_t(gridDim.x) * blockDim.x)
-    out[u] = u < S ? short_rec[u].x : u < S + M ? mid_rec[u - S].x : long_row[u - S - M];
+// Rows updated by the last backward (short + long segments), unsorted; count -> *count_out.
+__global__ void k_unique_rows(const uint4* short_rec, const unsigned long long* short_alloc, const uint32_t* long_row,
+                              const uint32_t* n_long, uint32_t* out, uint64_t* count_out) {
+  const uint64_t S = *short_alloc >> 32, L = *n_long;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *count_out = S + L;
+  for (uint64_t u = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; u < S + L; u += uint64_t(gridDim.x) * blockDim.x)
+    out[u] = u < S ? short_rec[u].x : long_row[u - S];
 }
 
 // Short segments on `st` (main), long segments on `side` — disjoint rows, run side by side.
@@ -1537,9 +1415,6 @@ BwdArgs base_args(hps_gpu_table t) {
   a.short_bag = t->ws_short_bag;
   a.n_long = z + 2;
   a.higher_total = z + 3;
-  a.mid_alloc = reinterpret_cast<unsigned long long*>(z + 8);
-  a.mid_rec = t->ws_mid_rec;
-  a.mid_top = static_cast<uint32_t>(t->max_keys);
   a.long_occ = reinterpret_cast<unsigned long long*>(z + 4);
   a.long_chunks = reinterpret_cast<unsigned long long*>(z + 6);
   a.long_row = t->ws_long_row;
@@ -1709,15 +1584,6 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   a.touched = touched_out;
   a.optimizer = t->optimizer;
   if (opt) a.opt = *opt;
-  {  // mid segments: a CTA each, on the side stream beside the short reduce (disjoint rows)
-    const uint32_t nv = t->dim / 4;
-    int s = HPS_GPU_OK;
-    if (grad_only) s = launch_mid<kOptGrad>(a, t->side, false, nv);
-    else if (t->optimizer == HPS_OPT_SGD) s = launch_mid<HPS_OPT_SGD>(a, t->side, false, nv);
-    else if (t->optimizer == HPS_OPT_ADAGRAD) s = launch_mid<HPS_OPT_ADAGRAD>(a, t->side, false, nv);
-    else s = launch_mid<HPS_OPT_ADAM>(a, t->side, false, nv);
-    if (s) return s;
-  }
 
   const uint32_t nvec = t->dim / 4;
   // K4e + K5: short segments (reduce fused with the optimizer), then the long segments'
@@ -1934,14 +1800,12 @@ int hps_gpu_table_last_unique(hps_gpu_table t, uint64_t* count_out, uint32_t* un
   const BwdArgs a = base_args(t);
   if (!unique_rows_out) {  // the count alone (the end-to-end step's result): one thread
     HPSG_CUDA(launch_k(true, k_unique_count, 1, 32, 0, st, static_cast<const unsigned long long*>(a.short_alloc),
-                       static_cast<const unsigned long long*>(a.mid_alloc), static_cast<const uint32_t*>(a.n_long),
-                       count_out));
+                       static_cast<const uint32_t*>(a.n_long), count_out));
     return HPS_GPU_OK;
   }
   // unsorted rows into the (now free) long-list buffers, then an ascending radix sort
-  k_unique_rows<<<grid_for(nk, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_short_rec, a.short_alloc, t->ws_mid_rec,
-                                                               a.mid_alloc, t->ws_long_row, a.n_long, t->ws_lkey_a,
-                                                               count_out);
+  k_unique_rows<<<grid_for(nk, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_short_rec, a.short_alloc, t->ws_long_row,
+                                                               a.n_long, t->ws_lkey_a, count_out);
   HPSG_CHECK_LAUNCH("k_unique_rows");
   if (!unique_rows_out) return HPS_GPU_OK;
   cudaError_t err = cudaSuccess;

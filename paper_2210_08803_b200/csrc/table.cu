@@ -1079,7 +1079,6 @@ int alloc_batch_slot(hps_gpu_table t, BatchSlot& b) {
   A(dalloc(&b.ws_occ_bag, N));
   A(dalloc(&b.ws_bag_len, B));
   A(dalloc(&b.ws_short_rec, N));
-  A(dalloc(&b.ws_mid_rec, bwd_max_mid(N)));
   A(dalloc(&b.ws_short_bag, N));
   A(dalloc(&b.ws_long_row, t->max_long));
   A(dalloc(&b.ws_long_len, t->max_long));
@@ -1127,7 +1126,7 @@ void free_batch_slot(BatchSlot& b) {
                   b.ws_long_start, b.ws_lkey_a,   b.ws_lval_a,    b.ws_lkey_b,     b.ws_lval_b,     b.ws_long_base,
                   b.ws_task_long, b.ws_partial2,  b.ws_long_hbase, b.ws_node_cnt,  b.ws_partial,    b.ws_counts,
                   b.ws_zero,      b.ws_abort,     b.ws_keys_stage, b.ws_offsets_stage, b.ws_ins_slot, b.ws_ins_pos,
-                  b.ws_ins_flag,  b.ws_ins_scan,  b.ws_mid_rec};
+                  b.ws_ins_flag,  b.ws_ins_scan};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : {b.ev_fork, b.ev_join, b.ev_bwd, b.ev_done, b.ev_join2, b.ev_pre, b.ev_probe})

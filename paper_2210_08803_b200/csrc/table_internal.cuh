@@ -10,22 +10,16 @@
 namespace hpsg {
 
 constexpr uint32_t kChunk = 32;  // blocked reduction width
-// Segment tiers by occurrence count: short (<= kChunk: a warp, k_reduce_short/_pipe), mid
-// (<= kMidMax = kChunk^2: one CTA sorts the segment's bags in shared memory and runs the whole
-// two-level tree, k_reduce_mid), long (> kMidMax: the global long-list sort + chunk tree).
-constexpr uint32_t kMidMax = kChunk * kChunk;
 
 // Zeroed-per-training-lookup region (u32 words), DESIGN.md §3 K4:
 //   [0,2)  u64 short-segment allocator: (segments << 32) | occurrences
 //   [2]    long segments   [3] tree nodes allocated above level 1
 //   [4,6)  u64 long occurrences (place-scan total)   [6,8) u64 level-1 chunks of long segments
-//   [8,10) u64 mid-segment allocator: (segments << 32) | occurrences
 //   then   place-scan look-back (u64 x tiles + ticket), long-registration scan look-back,
 //          and the radix-sort words of the long-occurrence sort.
 constexpr uint32_t kLongFlag = 0x80000000u;  // batch-table value after allocation: long segment id
 constexpr uint32_t kBtEmpty = 0xffffffffu;   // batch-table key of a free entry
-inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kMidMax + 1) + 2; }
-inline uint64_t bwd_max_mid(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
+inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
 inline int bwd_long_passes(uint64_t max_keys) {
   const uint64_t m = bwd_max_long(max_keys);
   int b = 0;
@@ -37,7 +31,7 @@ struct BwdZero {
 };
 inline BwdZero bwd_zero_layout(uint64_t nk) {
   BwdZero z;
-  z.place = 10;
+  z.place = 8;
   z.lreg = z.place + 2 * (scan_tiles(nk) + 1);
   z.sort = z.lreg + 2 * (scan_tiles(bwd_max_long(nk)) + 1);
   z.coop = z.sort + ((sort_ws_words(nk, bwd_long_passes(nk)) + 1) & ~size_t(1));  // 3 barriers + per-CTA counts
@@ -83,7 +77,6 @@ struct BatchSlot {
   uint32_t* ws_occ_bag = nullptr;   // occurrence -> bag (multi-hot)
   uint32_t* ws_bag_len = nullptr;   // bag lengths (multi-hot mean)
   uint4* ws_short_rec = nullptr;    // short segments {row, first, len, 0}, CSR over ws_short_bag
-  uint4* ws_mid_rec = nullptr;      // mid segments {row, first, len, entry}: bags at the top of ws_short_bag
   uint32_t* ws_short_bag = nullptr; // bags of the short segments' occurrences
   uint32_t *ws_long_row = nullptr, *ws_long_len = nullptr, *ws_long_start = nullptr;
   uint32_t *ws_lkey_a = nullptr, *ws_lval_a = nullptr, *ws_lkey_b = nullptr, *ws_lval_b = nullptr;

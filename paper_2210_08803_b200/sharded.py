@@ -25,9 +25,8 @@ def _owned_keys(ctx: Context, cfg: W.Config, t: int, rank: int, world: int, firs
 
 
 def long_sort_passes(max_keys: int) -> int:
-    """Radix passes of the long-segment list sort (table_internal.cuh bwd_long_passes:
-    segments of more than kMidMax = 1024 occurrences)."""
-    m = max_keys // 1025 + 2
+    """Radix passes of the long-segment list sort (table_internal.cuh bwd_long_passes)."""
+    m = max_keys // 33 + 2
     b = m.bit_length()
     return 1 if b <= 8 else (b + 7) // 8
 
@@ -208,7 +207,7 @@ class TrainStep:
         # training record + dedup (backward.cu launch_dedup): probe, dedup, long-list histogram,
         # its radix passes, long registration, long tasks; backward: short + long reduce
         rec = 5 + long_sort_passes(table_max_keys(cfg, 1))
-        self.kernels_per_step = rec + 1 + 3  # + pooling; backward: short, mid, long reduce
+        self.kernels_per_step = rec + 1 + 2  # + pooling
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self._cnt_host = torch.zeros(1, dtype=torch.int64).pin_memory()
         # pipelined e2e (run_host_async): one pinned result slot + event per step in flight
