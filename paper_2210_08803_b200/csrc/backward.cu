@@ -1481,7 +1481,7 @@ int hpsg::choose_dedup(bool* flat_out) {
 
 // K4a-K4d on the table's side stream, right after the training probe (table.cu
 // fork_dedup): they need only the occurrence record, so they overlap the pooling.
-int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st, cudaStream_t st_long) {
+int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
   const bool pdl = t->ctx->pdl;
   const uint64_t nk = t->last_n_keys_host;
   const BwdZero zl = bwd_zero_layout(nk);
@@ -1512,11 +1512,8 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st, cudaStream_t st_long) {
     HPSG_CUDA(launch_k(false, k_dedup, g, kDedupBlock, size_t(2) * kDedupHash * 4, st, a, z + zl.coop));
   }
   // the short segments are complete: the short reduce may start (backward_update joins here);
-  // the long segments' sort and registration continue on st_long (this stream, or the side
-  // stream when the dedup ran first on the main stream)
-  HPSG_CUDA(cudaEventRecord(t->ev_join, st));
-  if (st_long != st) HPSG_CUDA(cudaStreamWaitEvent(st_long, t->ev_join, 0));
-  st = st_long;
+  // the long segments' sort and registration continue on this stream
+  if (st == t->side) HPSG_CUDA(cudaEventRecord(t->ev_join, st));
   // K4c: stable sort of the long list by segment id (canonical order within each segment)
   {
     const int passes = bwd_long_passes(nk);
@@ -1569,7 +1566,7 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   // join the dedup forked by the training lookup; the long reduce runs on the side stream
   // (after this point of the main stream: the pooling has read the rows, d_out is ready)
   if (t->dedup_deferred) {
-    if (int s = launch_dedup(t, st, st)) return s;
+    if (int s = launch_dedup(t, st)) return s;
     t->dedup_deferred = false;
   }
   HPSG_CUDA(cudaEventRecord(t->ev_bwd, st));

@@ -854,29 +854,12 @@ int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t
   return HPS_GPU_OK;
 }
 
-// Dedup first: counts, allocation and placement on the main stream right after the probe
-// (full-occupancy kernels with the whole GPU to themselves), the long list's sort on the side
-// stream beside the pooling, which then runs at full grid.
-int dedup_before_pool(hps_gpu_table t) {
-  if (t->last_dedup_valid && t->ev_last_dedup != t->ev_done)
-    HPSG_CUDA(wait_recorded(t->ctx->stream, t->ev_last_dedup, t->last_dedup_capture));
-  HPSG_CUDA(cudaEventRecord(t->ev_fork, t->ctx->stream));
-  HPSG_CUDA(cudaStreamWaitEvent(t->side, t->ev_fork, 0));
-  if (int s = launch_dedup(t, t->ctx->stream, t->side)) return s;
-  HPSG_CUDA(cudaEventRecord(t->ev_done, t->side));
-  t->ev_last_dedup = t->ev_done;
-  t->last_dedup_valid = true;
-  t->last_dedup_capture = capture_id(t->side);
-  t->dedup_pending = true;
-  return HPS_GPU_OK;
-}
-
 // The dedup of the current slot on its side stream. A table's dedups run one at a time
 // (each is a persistent kernel whose grid barriers need all its CTAs resident).
 int dedup_on_side(hps_gpu_table t) {
   if (t->last_dedup_valid && t->ev_last_dedup != t->ev_done)
     HPSG_CUDA(wait_recorded(t->side, t->ev_last_dedup, t->last_dedup_capture));
-  if (int s = launch_dedup(t, t->side, t->side)) return s;  // records ev_join after the short placement
+  if (int s = launch_dedup(t, t->side)) return s;  // records ev_join after the short placement
   HPSG_CUDA(cudaEventRecord(t->ev_done, t->side));
   t->ev_last_dedup = t->ev_done;
   t->last_dedup_valid = true;
@@ -1055,8 +1038,7 @@ int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows) {
     // training: ONE CTA per SM. The pooling runs beside the dedup, and its row stream slows
     // the dedup's L2 atomics; at one CTA per SM it takes ~46 us instead of 37, still hidden,
     // and the dedup's count phase drops from 35 to 27 us (config 2: 0.134 -> 0.131 ms)
-    // prefetched / dedup first: the dedup ran ahead, nothing to leave room for
-    uint64_t train_ctas = (t->prefetched || t->dedup_first) ? 8 : 1;
+    uint64_t train_ctas = t->prefetched ? 8 : 1;  // prefetched: its dedup ran ahead, nothing to leave room for
     if (const char* e = std::getenv("HPS_GPU_POOL_CTAS")) train_ctas = std::max(1, std::atoi(e));  // A/B knob
     const uint64_t max_grid = rows ? uint64_t(kNumSMs) * train_ctas : uint64_t(kNumSMs) * 8;
     const int grid =
@@ -1201,7 +1183,6 @@ int hps_gpu_table_create(hps_gpu_ctx ctx, const hps_table_config* cfg, hps_gpu_t
   t->max_bags = cfg->max_batch_bags;
   if (const char* e = std::getenv("HPS_GPU_NO_TMA")) t->no_tma = e[0] == '1';
   if (const char* e = std::getenv("HPS_GPU_NO_FORK")) t->no_fork = e[0] == '1';
-  if (const char* e = std::getenv("HPS_GPU_DEDUP_FIRST")) t->dedup_first = e[0] == '1';  // A/B knob
   uint64_t rows = 0, slots = 0;
   for (uint32_t i = 0; i < t->n_tables; ++i) {
     const uint64_t cap = cfg->row_capacity_host[i];
@@ -1520,11 +1501,9 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
     a.occ_bag = multi ? t->ws_occ_bag : nullptr;
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
     if (int s = record(t, a, multi, a.mean, n_keys_host, st)) return s;
-    if (t->dedup_first && !t->no_fork)
-      if (int s = dedup_before_pool(t)) return s;
   }
   if (int s = launch_lookup(t, a, multi, train)) return s;
-  if (train && !(t->dedup_first && !t->no_fork))
+  if (train)
     if (int s = fork_dedup(t)) return s;
   t->have_train = train;
   return HPS_GPU_OK;

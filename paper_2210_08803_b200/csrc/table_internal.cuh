@@ -48,9 +48,7 @@ inline uint64_t bwd_max_nodes(uint64_t max_keys) { return bwd_max_chunks(max_key
 
 struct hps_gpu_table_s;
 namespace hpsg {
-// backward.cu: K4a-K4c (counts, allocation, placement) on st, then the long list's sort and
-// registration (K4d) on st_long
-int launch_dedup(hps_gpu_table_s* t, cudaStream_t st, cudaStream_t st_long);
+int launch_dedup(hps_gpu_table_s* t, cudaStream_t st);  // backward.cu: K4a-K4d (on t->side)
 int choose_dedup(bool* flat_out);  // backward.cu: persistent k_dedup if one CTA fits every SM, else flat
 // table.cu: hps_gpu_table_read_through + the source tier of every key (src_out[i]: 0 cache,
 // 1 table, 3 default vector; may be NULL)
@@ -153,8 +151,7 @@ struct hps_gpu_table_s : BatchSlot {
   cudaEvent_t ev_last_dedup = nullptr;  // the last k_dedup launched (prefetches serialise on it)
   bool last_dedup_valid = false;
   bool graphs_seen = false;
-  bool flat_dedup = false;   // the three-kernel dedup (choose_dedup at create)
-  bool dedup_first = false;  // the dedup runs on the main stream before the pooling (HPS_GPU_DEDUP_FIRST)  // a training record was captured into a graph (host slot flags may lag replays)
+  bool flat_dedup = false;   // the three-kernel dedup (choose_dedup at create)  // a training record was captured into a graph (host slot flags may lag replays)
   unsigned long long last_dedup_capture = 0;
   bool no_fork = false;         // HPS_GPU_NO_FORK=1: everything on the main stream (A/B measurement)
   bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)
