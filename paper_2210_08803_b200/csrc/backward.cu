@@ -20,8 +20,8 @@
 //                     compacted (canonical order) into the long list as (long id, bag)
 //   long sort       : stable radix sort of the long list by long id (few bits) — each long
 //                     segment contiguous, occurrences in canonical order
-//   k_scan<LongRegOp>, k_long_tasks: long segment starts, level-1 chunk bases, tree-node
-//                     blocks, the chunk -> segment map
+//   k_long_tasks    : the chunk -> segment map (each long segment registered its list start,
+//                     first level-1 chunk and tree-node block when it was allocated)
 // and at backward_update, the short and long reductions run side by side (disjoint rows):
 //   k_reduce_short  : a warp owns 32 short segments: sorts each one's bags back into canonical
 //                     order (warp rank), reduces and updates (bulk-copy or register path)
@@ -55,7 +55,8 @@ struct BwdArgs {
   unsigned long long* short_alloc;  // (segments << 32) | occurrences
   uint4* short_rec;                 // {row, first, len, batch-table entry}
   uint32_t* short_bag;
-  uint32_t* n_long;
+  uint32_t* n_long;                 // (the count half of long_alloc)
+  unsigned long long* long_alloc;   // (segments << 32) | occurrences: id, list start of each long segment
   uint32_t* long_row;
   uint32_t* long_ent;
   uint32_t* long_len;
@@ -119,6 +120,40 @@ __device__ __forceinline__ uint32_t bt_insert_from(uint2* bt, uint64_t mask, uin
 }
 __device__ __forceinline__ uint32_t bt_insert(uint2* bt, uint64_t mask, uint32_t row) {
   return bt_insert_from(bt, mask, row, bt_home(row, mask));
+}
+
+__device__ __forceinline__ uint32_t higher_nodes(uint32_t m);
+
+// A long leader (its row has more than kChunk occurrences) registers its segment right away
+// (every lane of the warp calls it): id and start in the sorted long list from one packed
+// atomic per warp — ids in allocator order, so the starts are the prefix of the lengths in id
+// order, exactly where the stable sort by id will put each segment — its first level-1 chunk
+// from a second counter (the chunk total is that counter) and its tree-node block.
+__device__ __forceinline__ void register_long(const BwdArgs& a, bool lg, uint32_t row, uint32_t ent, uint32_t len) {
+  if (!__ballot_sync(0xffffffffu, lg)) return;
+  const uint32_t lane = lane_id();
+  const uint32_t m = lg ? (len + kChunk - 1) / kChunk : 0u;
+  const unsigned long long mine = lg ? ((1ull << 32) | len) : 0ull;
+  const unsigned long long incl = warp_incl_scan(mine);
+  const unsigned long long cincl = warp_incl_scan(static_cast<unsigned long long>(m));
+  unsigned long long base = 0, cbase = 0;
+  if (lane == 31) {
+    base = atomicAdd(a.long_alloc, incl);
+    cbase = atomicAdd(a.long_chunks, cincl);
+  }
+  base = __shfl_sync(0xffffffffu, base, 31);
+  cbase = __shfl_sync(0xffffffffu, cbase, 31);
+  if (lg) {
+    const unsigned long long pos = base + incl - mine;
+    const uint32_t j = static_cast<uint32_t>(pos >> 32);
+    a.long_row[j] = row;
+    a.long_ent[j] = ent;
+    a.long_len[j] = len;
+    a.long_start[j] = static_cast<uint32_t>(pos);
+    a.long_base[j] = static_cast<uint32_t>(cbase + cincl - m);
+    a.long_hbase[j] = atomicAdd(a.higher_total, higher_nodes(m));
+    a.bt[ent].y = kLongFlag | j;
+  }
 }
 
 // ---- K4a-c fused: counts, allocation, placement in ONE persistent cooperative kernel ------
@@ -318,20 +353,7 @@ __global__ void __launch_bounds__(kDedupBlock, 2) k_dedup(BwdArgs a, uint32_t* c
         a.bt[ent[k]].y = first;
         pos += (1ull << 32) | len[k];
       }
-      const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
-      if (lg_mask) {
-        const int src = __ffs(lg_mask) - 1;
-        uint32_t j0 = 0;
-        if (static_cast<int>(lane) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
-        j0 = __shfl_sync(0xffffffffu, j0, src);
-        if (lg) {
-          const uint32_t j = j0 + __popc(lg_mask & lt);
-          a.long_row[j] = a.occ_row[occ[k]];
-          a.long_ent[j] = ent[k];
-          a.long_len[j] = len[k];
-          a.bt[ent[k]].y = kLongFlag | j;
-        }
-      }
+      register_long(a, lg, lg ? a.occ_row[occ[k]] : 0u, ent[k], len[k]);
     }
   }
   trace_end(kTrAlloc);
@@ -465,7 +487,6 @@ __global__ void __launch_bounds__(256) k_alloc_flat(BwdArgs a) {
   if (threadIdx.x == 0) s_cursor = total ? atomicAdd(a.short_alloc, total) : 0ull;
   __syncthreads();
   pos += s_cursor;
-  const uint32_t lt = lanemask_lt();
 #pragma unroll
   for (int k = 0; k < kAllocIPT; ++k) {
     const uint64_t i = b0 + threadIdx.x * kAllocIPT + k;
@@ -476,20 +497,7 @@ __global__ void __launch_bounds__(256) k_alloc_flat(BwdArgs a) {
       a.bt[ent[k]].y = first;
       pos += (1ull << 32) | len[k];
     }
-    const uint32_t lg_mask = __ballot_sync(0xffffffffu, lg);
-    if (lg_mask) {
-      const int src = __ffs(lg_mask) - 1;
-      uint32_t j0 = 0;
-      if (static_cast<int>(lane_id()) == src) j0 = atomicAdd(a.n_long, static_cast<uint32_t>(__popc(lg_mask)));
-      j0 = __shfl_sync(0xffffffffu, j0, src);
-      if (lg) {
-        const uint32_t j = j0 + __popc(lg_mask & lt);
-        a.long_row[j] = a.occ_row[i];
-        a.long_ent[j] = ent[k];
-        a.long_len[j] = len[k];
-        a.bt[ent[k]].y = kLongFlag | j;
-      }
-    }
+    register_long(a, lg, lg ? a.occ_row[i] : 0u, ent[k], len[k]);
   }
   trace_end(kTrAlloc);
 }
@@ -525,29 +533,6 @@ __device__ __forceinline__ uint32_t higher_nodes(uint32_t m) {
   return n;
 }
 
-// Scan over long segments of (len | chunks << 32): start in the sorted long list, first
-// level-1 chunk, tree-node block; the row's counter goes back to zero.
-struct LongRegOp {
-  static constexpr int kTrace = kTrLongReg;
-  BwdArgs a;
-  __device__ uint64_t size() const { return *a.n_long; }
-  __device__ uint64_t count(uint64_t j) const {
-    const uint64_t len = a.long_len[j];
-    return len | (((len + kChunk - 1) / kChunk) << 32);
-  }
-  __device__ void emit(uint64_t j, uint64_t excl, uint64_t c) const {
-    const uint32_t m = static_cast<uint32_t>(c >> 32);
-    a.long_start[j] = static_cast<uint32_t>(excl);
-    a.long_base[j] = static_cast<uint32_t>(excl >> 32);
-    a.long_hbase[j] = atomicAdd(a.higher_total, higher_nodes(m));
-    a.bt[a.long_ent[j]] = make_uint2(kBtEmpty, 0xffffffffu);
-  }
-  __device__ void total(uint64_t t) const {
-    *a.long_chunks = t >> 32;
-    const_cast<uint64_t*>(a.counts)[1] = (*a.short_alloc >> 32) + *a.n_long;
-  }
-};
-
 // Chunk -> long segment map (warp per long segment; consumed by k_long).
 __global__ void __launch_bounds__(256) k_long_tasks(BwdArgs a) {
   pdl_wait();
@@ -558,6 +543,7 @@ __global__ void __launch_bounds__(256) k_long_tasks(BwdArgs a) {
   for (uint64_t j = warp; j < nl; j += n_warps) {
     const uint32_t m = (a.long_len[j] + kChunk - 1) / kChunk, base = a.long_base[j];
     for (uint32_t c = lane_id(); c < m; c += 32) a.task_long[base + c] = static_cast<uint32_t>(j);
+    if (lane_id() == 0) a.bt[a.long_ent[j]] = make_uint2(kBtEmpty, 0xffffffffu);  // the entry's last reader
   }
 }
 
@@ -981,9 +967,6 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
 constexpr uint32_t kPipeList = 128;  // entries per sub-list (>= 3 + kChunk: one whole segment)
 static_assert(kPipeList >= 3 + kChunk, "a sub-list holds at least one whole short segment");
 
-__device__ __forceinline__ float4 ld_row4(const float* p, uint32_t v) {
-  return __ldg(reinterpret_cast<const float4*>(p) + v);
-}
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
@@ -1413,7 +1396,8 @@ BwdArgs base_args(hps_gpu_table t) {
   a.short_alloc = reinterpret_cast<unsigned long long*>(z);
   a.short_rec = t->ws_short_rec;
   a.short_bag = t->ws_short_bag;
-  a.n_long = z + 2;
+  a.long_alloc = reinterpret_cast<unsigned long long*>(z + 8);
+  a.n_long = z + 9;
   a.higher_total = z + 3;
   a.long_occ = reinterpret_cast<unsigned long long*>(z + 4);
   a.long_chunks = reinterpret_cast<unsigned long long*>(z + 6);
@@ -1447,7 +1431,7 @@ cudaError_t dedup_attributes() {
       return e;
     for (cudaError_t e : {prefer_max_smem(k_dedup), prefer_max_smem(k_count_flat), prefer_max_smem(k_alloc_flat),
                           prefer_max_smem(k_scan<PlaceOp>), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass),
-                          prefer_max_smem(k_scan<LongRegOp>), prefer_max_smem(k_long_tasks)})
+                          prefer_max_smem(k_long_tasks)})
       if (e) return e;
     return cudaSuccess;
   });
@@ -1538,13 +1522,7 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
       in_b = !in_b;
     }
   }
-  // K4d: long segment registration
-  {
-    const uint64_t tiles = std::max<uint64_t>(1, scan_tiles(bwd_max_long(nk)));
-    uint64_t* status = reinterpret_cast<uint64_t*>(z + zl.lreg);
-    HPSG_CUDA(launch_k(pdl, k_scan<LongRegOp>, static_cast<unsigned>(tiles), kScanBlock, 0, st, LongRegOp{a}, status,
-                       reinterpret_cast<uint32_t*>(status + tiles)));
-  }
+  // K4d: chunk -> segment map (the segments registered themselves at allocation)
   HPSG_CUDA(launch_k(pdl, k_long_tasks, grid_for(bwd_max_long(nk) * 32, 256, kNumSMs * 8), 256, 0, st, a));
   HPSG_CHECK_LAUNCH("backward dedup");
   return HPS_GPU_OK;
@@ -1561,7 +1539,6 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   }
   if (!d_out) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = t->ctx->stream;
-  const bool pdl = t->ctx->pdl;
   const uint64_t nk = t->last_n_keys_host;
   // join the dedup forked by the training lookup; the long reduce runs on the side stream
   // (after this point of the main stream: the pooling has read the rows, d_out is ready)

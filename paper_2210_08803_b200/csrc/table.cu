@@ -302,10 +302,6 @@ __global__ void k_widen_half(const uint16_t* __restrict__ src, uint64_t n, float
     dst[i] = __half2float(__ushort_as_half(src[i]));
 }
 
-__global__ void k_fill_u64(uint64_t* p, uint64_t n, uint64_t v) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) p[i] = v;
-}
-
 __global__ void k_fill_slots_empty(Slot* slots, uint64_t n) {
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     *reinterpret_cast<ulonglong2*>(slots + i) = make_ulonglong2(0ull, (uint64_t(kAuxNone) << 32) | kRowEmpty);

@@ -15,8 +15,9 @@ constexpr uint32_t kChunk = 32;  // blocked reduction width
 //   [0,2)  u64 short-segment allocator: (segments << 32) | occurrences
 //   [2]    long segments   [3] tree nodes allocated above level 1
 //   [4,6)  u64 long occurrences (place-scan total)   [6,8) u64 level-1 chunks of long segments
-//   then   place-scan look-back (u64 x tiles + ticket), long-registration scan look-back,
-//          and the radix-sort words of the long-occurrence sort.
+//   [8,10) u64 long-segment allocator: (segments << 32) | occurrences (word 9 = the count)
+//   then   place-scan look-back (u64 x tiles + ticket) and the radix-sort words of the
+//          long-occurrence sort.
 constexpr uint32_t kLongFlag = 0x80000000u;  // batch-table value after allocation: long segment id
 constexpr uint32_t kBtEmpty = 0xffffffffu;   // batch-table key of a free entry
 inline uint64_t bwd_max_long(uint64_t max_keys) { return max_keys / (kChunk + 1) + 2; }
@@ -27,13 +28,12 @@ inline int bwd_long_passes(uint64_t max_keys) {
   return b <= 8 ? 1 : (b + 7) / 8;
 }
 struct BwdZero {
-  size_t place, lreg, sort, coop, total;
+  size_t place, sort, coop, total;
 };
 inline BwdZero bwd_zero_layout(uint64_t nk) {
   BwdZero z;
-  z.place = 8;
-  z.lreg = z.place + 2 * (scan_tiles(nk) + 1);
-  z.sort = z.lreg + 2 * (scan_tiles(bwd_max_long(nk)) + 1);
+  z.place = 10;
+  z.sort = z.place + 2 * (scan_tiles(nk) + 1);
   z.coop = z.sort + ((sort_ws_words(nk, bwd_long_passes(nk)) + 1) & ~size_t(1));  // 3 barriers + per-CTA counts
   z.total = z.coop + 4 + 160;
   return z;
