@@ -20,8 +20,9 @@
 //                     compacted (canonical order) into the long list as (long id, bag)
 //   long sort       : stable radix sort of the long list by long id (few bits) — each long
 //                     segment contiguous, occurrences in canonical order
-//   k_long_tasks    : the chunk -> segment map (each long segment registered its list start,
-//                     first level-1 chunk and tree-node block when it was allocated)
+//   (no registration pass: each long segment registers its list start, first level-1 chunk,
+//                     tree-node block, the sort's digit histogram counts and its chunk ->
+//                     segment map entries when it is allocated: register_long)
 // and at backward_update, the short and long reductions run side by side (disjoint rows):
 //   k_reduce_short  : a warp owns 32 short segments: sorts each one's bags back into canonical
 //                     order (warp rank), reduces and updates (bulk-copy or register path)
@@ -61,6 +62,8 @@ struct BwdArgs {
   uint32_t* long_ent;
   uint32_t* long_len;
   uint32_t* long_start;     // first position of the segment in the sorted long list
+  uint32_t* long_hist;      // histograms of the long sort's digit passes [passes x 256] (occurrence counts)
+  int long_passes;
   uint32_t* lkey;           // long list: segment id (sort input)
   uint32_t* lval;           // long list: bag (sort input)
   const uint32_t* lbag;     // long list sorted by segment id: bags in canonical order
@@ -143,16 +146,29 @@ __device__ __forceinline__ void register_long(const BwdArgs& a, bool lg, uint32_
   }
   base = __shfl_sync(0xffffffffu, base, 31);
   cbase = __shfl_sync(0xffffffffu, cbase, 31);
+  uint32_t j = 0, cb = 0;
   if (lg) {
     const unsigned long long pos = base + incl - mine;
-    const uint32_t j = static_cast<uint32_t>(pos >> 32);
+    j = static_cast<uint32_t>(pos >> 32);
+    cb = static_cast<uint32_t>(cbase + cincl - m);
     a.long_row[j] = row;
     a.long_ent[j] = ent;
     a.long_len[j] = len;
     a.long_start[j] = static_cast<uint32_t>(pos);
-    a.long_base[j] = static_cast<uint32_t>(cbase + cincl - m);
+    a.long_base[j] = cb;
     a.long_hbase[j] = atomicAdd(a.higher_total, higher_nodes(m));
     a.bt[ent].y = kLongFlag | j;
+    // the long-list sort's digit histograms: segment j's len occurrences all carry key j
+    for (int p = 0; p < a.long_passes; ++p) atomicAdd(&a.long_hist[256 * p + ((j >> (8 * p)) & 255u)], len);
+  }
+  // the chunk -> segment map of the long reduce, written by the whole warp per segment
+  uint32_t todo = __ballot_sync(0xffffffffu, lg);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t sj = __shfl_sync(0xffffffffu, j, src), sb = __shfl_sync(0xffffffffu, cb, src);
+    const uint32_t sm = __shfl_sync(0xffffffffu, m, src);
+    for (uint32_t c = lane; c < sm; c += 32) a.task_long[sb + c] = sj;
   }
 }
 
@@ -533,19 +549,6 @@ __device__ __forceinline__ uint32_t higher_nodes(uint32_t m) {
   return n;
 }
 
-// Chunk -> long segment map (warp per long segment; consumed by k_long).
-__global__ void __launch_bounds__(256) k_long_tasks(BwdArgs a) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
-  const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const uint32_t nl = *a.n_long;
-  for (uint64_t j = warp; j < nl; j += n_warps) {
-    const uint32_t m = (a.long_len[j] + kChunk - 1) / kChunk, base = a.long_base[j];
-    for (uint32_t c = lane_id(); c < m; c += 32) a.task_long[base + c] = static_cast<uint32_t>(j);
-    if (lane_id() == 0) a.bt[a.long_ent[j]] = make_uint2(kBtEmpty, 0xffffffffu);  // the entry's last reader
-  }
-}
 
 // A warp's 32 short segments [u0, u0+32) occupy one contiguous range of the short list:
 // load it into shared memory and sort every segment's bags ascending (= canonical order;
@@ -1184,6 +1187,7 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
   for (uint64_t t = warp; t < T; t += n_warps) {
     const uint32_t j = a.task_long[t];
     const uint32_t c = static_cast<uint32_t>(t) - a.long_base[j];
+    if (c == 0 && lane == 0) a.bt[a.long_ent[j]] = make_uint2(kBtEmpty, 0xffffffffu);  // the entry's last reader
     const uint32_t s0 = a.long_start[j], e = s0 + a.long_len[j];
     const uint32_t s = s0 + c * kChunk;
     const uint32_t n = min(static_cast<uint32_t>(kChunk), e - s);
@@ -1405,6 +1409,8 @@ BwdArgs base_args(hps_gpu_table t) {
   a.long_ent = t->ws_long_ent;
   a.long_len = t->ws_long_len;
   a.long_start = t->ws_long_start;
+  a.long_hist = z + zl.sort;  // (radix_sort workspace layout: the histograms come first)
+  a.long_passes = bwd_long_passes(t->last_n_keys_host);
   a.lkey = t->ws_lkey_a;
   a.lval = t->ws_lval_a;
   a.lbag = (bwd_long_passes(t->last_n_keys_host) & 1) ? t->ws_lval_b : t->ws_lval_a;
@@ -1430,8 +1436,7 @@ cudaError_t dedup_attributes() {
     if (cudaError_t e = cudaFuncSetAttribute(k_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4))
       return e;
     for (cudaError_t e : {prefer_max_smem(k_dedup), prefer_max_smem(k_count_flat), prefer_max_smem(k_alloc_flat),
-                          prefer_max_smem(k_scan<PlaceOp>), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass),
-                          prefer_max_smem(k_long_tasks)})
+                          prefer_max_smem(k_scan<PlaceOp>), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass)})
       if (e) return e;
     return cudaSuccess;
   });
@@ -1506,8 +1511,7 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
     uint32_t* stick = hist + 4 * 256;
     uint32_t* status = stick + 4;
     const auto* d_n = reinterpret_cast<const uint64_t*>(a.long_occ);
-    HPSG_CUDA(launch_k(pdl, k_radix_hist, grid_for(nk, 256, kNumSMs * 2), 256, 0, st,
-                       static_cast<const uint32_t*>(t->ws_lkey_a), d_n, passes, hist));
+    // (the digit histograms were counted at allocation: register_long)
     const uint32_t* kin = t->ws_lkey_a;
     const uint32_t* vin = t->ws_lval_a;
     bool in_b = false;
@@ -1522,8 +1526,6 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
       in_b = !in_b;
     }
   }
-  // K4d: chunk -> segment map (the segments registered themselves at allocation)
-  HPSG_CUDA(launch_k(pdl, k_long_tasks, grid_for(bwd_max_long(nk) * 32, 256, kNumSMs * 8), 256, 0, st, a));
   HPSG_CHECK_LAUNCH("backward dedup");
   return HPS_GPU_OK;
 }

@@ -206,7 +206,7 @@ class TrainStep:
         self._graphs = {}
         # training record + dedup (backward.cu launch_dedup): probe, dedup, long-list histogram,
         # its radix passes, long registration, long tasks; backward: short + long reduce
-        rec = 5 + long_sort_passes(table_max_keys(cfg, 1))
+        rec = 2 + long_sort_passes(table_max_keys(cfg, 1))  # probe, dedup (persistent kernel), sort passes
         self.kernels_per_step = rec + 1 + 2  # + pooling
         self._cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
         self._cnt_host = torch.zeros(1, dtype=torch.int64).pin_memory()
