@@ -541,7 +541,7 @@ __device__ __forceinline__ void warp_store_row(void* cvec, uint64_t e, const flo
 
 // ---- K7: insert, one warp per touched set, entries in input order --------------------
 template <bool F16>
-__global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict__ sets_sorted,
+__global__ void __launch_bounds__(256, 4) k_insert_sets(const uint32_t* __restrict__ sets_sorted,
                                                      const uint32_t* __restrict__ idx_sorted,
                                                      const uint32_t* __restrict__ seg_start, const uint64_t* counts,
                                                      const uint64_t* __restrict__ keys, const float* __restrict__ vecs,

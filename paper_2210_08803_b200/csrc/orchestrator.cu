@@ -140,22 +140,33 @@ __global__ void __launch_bounds__(256) k_dedup_claim(const uint64_t* __restrict_
   pdl_wait();
   pdl_launch_dependents();
   if (source_counts && blockIdx.x == 0 && threadIdx.x < 4) source_counts[threadIdx.x] = 0;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint64_t k = keys[i];
+  // (whole warps iterate together: the match below needs every lane)
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x); i0 < n; i0 += stride) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool valid = i < n;
+    const uint64_t k = valid ? keys[i] : 0;
+    // a Zipf-hot key repeats within a warp: only its first lane (the smallest position)
+    // claims; the others take its slot
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? k : ~k) & __ballot_sync(0xffffffffu, valid);
+    const int leader = peers ? __ffs(peers) - 1 : 0;
     uint64_t h = hps::key_hash(k) & mask;
-    while (true) {
-      uint32_t o = claim[h];
-      if (o == kEmptyOwner) {
-        o = atomicCAS(&claim[h], kEmptyOwner, static_cast<uint32_t>(i));
-        if (o == kEmptyOwner) break;
+    if (valid && static_cast<int>(lane_id()) == leader) {
+      while (true) {
+        uint32_t o = claim[h];
+        if (o == kEmptyOwner) {
+          o = atomicCAS(&claim[h], kEmptyOwner, static_cast<uint32_t>(i));
+          if (o == kEmptyOwner) break;
+        }
+        if (keys[o] == k) {
+          if (o > i) atomicMin(&claim[h], static_cast<uint32_t>(i));  // (owners only decrease)
+          break;
+        }
+        h = (h + 1) & mask;
       }
-      if (keys[o] == k) {
-        atomicMin(&claim[h], static_cast<uint32_t>(i));
-        break;
-      }
-      h = (h + 1) & mask;
     }
-    slot_of[i] = static_cast<uint32_t>(h);
+    h = __shfl_sync(0xffffffffu, h, leader);
+    if (valid) slot_of[i] = static_cast<uint32_t>(h);
   }
 }
 
@@ -204,19 +215,47 @@ __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ urows,
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   uint32_t c0 = 0, c1 = 0, c3 = 0;
-  for (uint64_t i0 = warp * G; i0 < n; i0 += n_warps * G) {
-    const uint64_t i = i0 + grp;
-    if (i < n) {
-      const uint32_t u = inverse[i];
-      const float4* s4 = reinterpret_cast<const float4*>(urows + uint64_t(u) * dim);
-      float4* d4 = reinterpret_cast<float4*>(out + i * dim);
-      for (uint32_t v = gl; v < nvec; v += LPR) d4[v] = s4[v];
-      if (gl == 0 && source_counts) {
-        const uint8_t sv = src[u];
+  // a warp takes 32 * G consecutive outputs: their distinct ids in one coalesced load (lane l
+  // holds ids l, l + 32, ...), then the rows stream 4 per group in flight
+  constexpr int R = 4;
+  for (uint64_t i0 = warp * 32 * G; i0 < n; i0 += n_warps * 32 * G) {
+    uint32_t my_u[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const uint64_t i = i0 + q * 32 + lane;
+      my_u[q] = i < n ? inverse[i] : 0u;
+      if (i < n && source_counts) {
+        const uint8_t sv = src[my_u[q]];
         c0 += sv == 0;
         c1 += sv == 1;
         c3 += sv == 3;
       }
+    }
+    for (uint32_t r0 = 0; r0 < 32 * G; r0 += R * G) {  // output r0 + r * G + grp
+      float4 x[R];
+      uint64_t dst[R];
+      bool ok[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const uint32_t o = r0 + r * G + grp;
+        // (o / 32 is the same for every lane: G divides 32) — select it without local memory
+        const uint32_t q = o / 32;
+        uint32_t mine = my_u[0];
+#pragma unroll
+        for (int qq = 1; qq < G; ++qq) mine = qq == static_cast<int>(q) ? my_u[qq] : mine;
+        const uint32_t u = __shfl_sync(0xffffffffu, mine, o % 32);
+        const uint64_t i = i0 + o;
+        ok[r] = i < n;
+        dst[r] = i;
+        x[r] = (ok[r] && gl < nvec) ? reinterpret_cast<const float4*>(urows + uint64_t(u) * dim)[gl]
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (ok[r])
+          for (uint32_t v = gl + LPR; v < nvec; v += LPR)  // rows wider than one pass of the group
+            reinterpret_cast<float4*>(out + i * dim)[v] = reinterpret_cast<const float4*>(urows + uint64_t(u) * dim)[v];
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (ok[r] && gl < nvec) reinterpret_cast<float4*>(out + dst[r] * dim)[gl] = x[r];
     }
   }
   if (source_counts) {
