@@ -353,6 +353,16 @@ int hps_gpu_dist_forward(hps_gpu_dist dist, const uint64_t* keys, const uint32_t
                          uint64_t n_keys, int combiner, float* out, uint32_t flags);
 /* Backward of the last training forward: d_out [n_bags x dim]; every owner updates its rows. */
 int hps_gpu_dist_backward(hps_gpu_dist dist, const float* d_out, const hps_opt_params* opt_host);
+/* Transport of the exchanges. HPS_DIST_NCCL (default): grouped ncclSend/ncclRecv of the
+ * regions. HPS_DIST_PEER: no collective calls — the requester's region kernel stores keys and
+ * table ids straight into the owners' receive buffers, the pooling loads the owners' gathered
+ * rows straight from their memory, and the gradient scatter stores into the owners' gradient
+ * regions (NVLink peer loads/stores through CUDA-IPC mappings, exchanged once over NCCL; the
+ * loopback ranks of one device use each other's memory directly). Phases are ordered by
+ * per-step epochs the ranks write into each other's flag words (release/acquire at system
+ * scope), so a peer-transport step is graph-capturable too. Collective: every rank sets it. */
+enum { HPS_DIST_NCCL = 0, HPS_DIST_PEER = 1 };
+int hps_gpu_dist_set_transport(hps_gpu_dist dist, int transport);
 /* Loopback transport (tests, single-GPU bring-up): n ranks of ONE process on one device,
  * the all-to-alls done as device copies between their buffers. Rank r's calls must run on
  * their own host thread (every all-to-all is a rendezvous of the n ranks); ctxs[r] should

@@ -496,6 +496,10 @@ class DistTable:
         _need_cuda(d_out, "d_out")
         L.check(self.lib.hps_gpu_dist_backward(self.h, _ptr(d_out), C.byref(params)), "dist_backward")
 
+    def set_transport(self, transport: str) -> None:
+        """"nccl" (grouped send/recv) or "peer" (the kernels load/store the peers' regions directly)."""
+        L.check(self.lib.hps_gpu_dist_set_transport(self.h, {"nccl": 0, "peer": 1}[transport]), "dist_set_transport")
+
     def close(self) -> None:
         if getattr(self, "h", None):
             self.lib.hps_gpu_dist_destroy(self.h)

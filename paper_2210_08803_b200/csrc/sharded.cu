@@ -65,11 +65,30 @@ struct hps_gpu_dist_s {
   // loopback transport (hps_gpu_dist_create_loopback): ranks of one process on one device
   std::shared_ptr<struct LoopGroup> loop;
   cudaEvent_t loop_ev = nullptr;
+  // peer-memory transport (hps_gpu_dist_set_transport(HPS_DIST_PEER)): no all-to-all calls —
+  // the requester's kernels store keys/tables and gradients straight into the owners'
+  // regions and the pooling loads rows straight from the owners' gathered rows
+  int transport = HPS_DIST_NCCL;
+  struct PeerTab* peer = nullptr;       // host copy of the peer pointer table
+  uint64_t* flags = nullptr;            // [3 x G] epochs this rank's peers signal into
+  uint64_t* d_epoch = nullptr;          // step counter (device: graph replays advance it)
+  std::vector<void*> ipc_opened;        // peer buffers opened through CUDA IPC (NCCL mode)
   // last forward
   const uint32_t* last_offsets = nullptr;
   uint64_t last_bags = 0;
   int last_combiner = 0;
   bool have_fwd = false, train = false;
+};
+
+// Every peer's owner-side buffers, as device pointers of this rank (its own: plain pointers;
+// a peer's: CUDA-IPC mappings over NVLink, or, for loopback ranks, the same device's memory).
+constexpr uint32_t kMaxPeers = 64;
+struct PeerTab {
+  uint64_t* keys[kMaxPeers];
+  uint32_t* tables[kMaxPeers];
+  float* rows[kMaxPeers];
+  float* grads[kMaxPeers];
+  uint64_t* flags[kMaxPeers];
 };
 
 // A group of loopback ranks: the all-to-all is device copies between their buffers, each
@@ -123,6 +142,152 @@ __global__ void k_fix_regions(const uint64_t* __restrict__ dense_keys, const uin
     perm[i] = static_cast<uint32_t>(uint64_t(p) * C + (r < C ? r : C - 1));
   }
 }
+
+// ---- peer-memory transport --------------------------------------------------------------
+// Fixed regions stored straight into the owners: this rank's region p goes to rank p's
+// receive buffers at [rank * C, +C) (stores over NVLink), perm as in k_fix_regions.
+__global__ void k_fix_regions_peer(const uint64_t* __restrict__ dense_keys, const uint32_t* __restrict__ dense_tables,
+                                   const uint32_t* __restrict__ dense_perm, const uint32_t* __restrict__ counts,
+                                   uint32_t G, uint32_t rank, uint64_t C, uint64_t n, PeerTab pt,
+                                   uint32_t* __restrict__ perm, uint32_t* status) {
+  __shared__ uint64_t s_start[kMaxPeers + 1];
+  if (threadIdx.x == 0) {
+    uint64_t run = 0;
+    for (uint32_t p = 0; p < G; ++p) {
+      s_start[p] = run;
+      run += counts[p];
+    }
+    s_start[G] = run;
+  }
+  __syncthreads();
+  const uint64_t total = uint64_t(G) * C;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < total; q += stride) {
+    const uint32_t p = static_cast<uint32_t>(q / C);
+    const uint64_t r = q - uint64_t(p) * C;
+    const uint64_t cnt = s_start[p + 1] - s_start[p];
+    const uint64_t dst = uint64_t(rank) * C + r;
+    if (r < cnt) {
+      pt.keys[p][dst] = dense_keys[s_start[p] + r];
+      pt.tables[p][dst] = dense_tables[s_start[p] + r];
+    } else {
+      pt.keys[p][dst] = 0;
+      pt.tables[p][dst] = 0xffffffffu;
+    }
+    if (r == 0 && cnt > C) latch_status(status, HPS_GPU_E_INFEASIBLE);
+  }
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const uint64_t d = dense_perm[i];
+    uint32_t p = 0;
+    while (p + 1 < G && s_start[p + 1] <= d) ++p;
+    const uint64_t r = d - s_start[p];
+    perm[i] = static_cast<uint32_t>(uint64_t(p) * C + (r < C ? r : C - 1));
+  }
+  __threadfence_system();  // the remote stores are performed before the owner is signalled
+}
+
+__global__ void k_epoch_bump(uint64_t* e) {
+  if (threadIdx.x == 0) *e += 1;
+}
+
+// Signal every peer that phase `which` of this step is done on this rank: flags[which][rank].
+__global__ void k_signal(PeerTab pt, uint32_t which, uint32_t G, uint32_t rank, const uint64_t* d_epoch) {
+  const uint64_t e = *d_epoch;
+  __threadfence_system();
+  for (uint32_t p = threadIdx.x; p < G; p += blockDim.x) {
+    uint64_t* f = pt.flags[p] + uint64_t(which) * G + rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+  }
+}
+
+// Wait until every peer signalled phase `which` of this step (a single CTA spins).
+__global__ void k_wait(const uint64_t* flags, uint32_t which, uint32_t G, const uint64_t* d_epoch) {
+  const uint64_t e = *d_epoch;
+  for (uint32_t p = threadIdx.x; p < G; p += blockDim.x) {
+    const uint64_t* f = flags + uint64_t(which) * G + p;
+    uint64_t v;
+    while (true) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
+      if (v >= e) break;
+      __nanosleep(200);
+    }
+  }
+}
+
+// Pooling fused with the rows' all-to-all: occurrence i's row is owner p's gathered row at
+// [rank * C + r] (perm[i] = p*C + r), loaded straight from the owner's memory.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_pool_rows_peer(PeerTab pt, uint32_t rank, uint64_t C,
+                                                        const uint32_t* __restrict__ perm,
+                                                        const uint32_t* __restrict__ offsets, uint64_t n_bags,
+                                                        uint32_t dim, int mean, float* __restrict__ out) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t b = gid; b < n_bags; b += ng) {
+    const uint32_t lo = offsets ? offsets[b] : static_cast<uint32_t>(b);
+    const uint32_t hi = offsets ? offsets[b + 1] : static_cast<uint32_t>(b + 1);
+    float4* o = reinterpret_cast<float4*>(out + b * dim);
+    for (uint32_t v = gl; v < nvec; v += LPR) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t i = lo; i < hi; ++i) {
+        const uint32_t pr = perm[i], p = static_cast<uint32_t>(pr / C);
+        const float* src = pt.rows[p] + (uint64_t(rank) * C + (pr - uint64_t(p) * C)) * dim;
+        acc = f4_add(acc, reinterpret_cast<const float4*>(src)[v]);
+      }
+      if (mean && hi > lo) acc = f4_div(acc, static_cast<float>(hi - lo));
+      o[v] = acc;
+    }
+  }
+}
+
+// Gradient scatter fused with the gradients' all-to-all: stored straight into owner p's
+// receive region at [rank * C + r].
+template <int LPR>
+__global__ void __launch_bounds__(256) k_scatter_grads_peer(PeerTab pt, uint32_t rank, uint64_t C,
+                                                            const float* __restrict__ dout,
+                                                            const uint32_t* __restrict__ perm,
+                                                            const uint32_t* __restrict__ offsets, uint64_t n_bags,
+                                                            uint32_t dim, int mean) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t b = gid; b < n_bags; b += ng) {
+    const uint32_t lo = offsets ? offsets[b] : static_cast<uint32_t>(b);
+    const uint32_t hi = offsets ? offsets[b + 1] : static_cast<uint32_t>(b + 1);
+    const float fl = static_cast<float>(hi - lo);
+    const float4* d = reinterpret_cast<const float4*>(dout + b * dim);
+    for (uint32_t v = gl; v < nvec; v += LPR) {
+      float4 x = __ldg(d + v);
+      if (mean) x = f4_div(x, fl);
+      for (uint32_t i = lo; i < hi; ++i) {
+        const uint32_t pr = perm[i], p = static_cast<uint32_t>(pr / C);
+        float* dst = pt.grads[p] + (uint64_t(rank) * C + (pr - uint64_t(p) * C)) * dim;
+        reinterpret_cast<float4*>(dst)[v] = x;
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+int lpr_of(uint32_t dim) {
+  const uint32_t nvec = dim / 4;
+  return nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
+}
+
+#define HPSG_LPR_DISPATCH(KERNEL, LPR, GRID, ST, ...)                    \
+  do {                                                                  \
+    switch (LPR) {                                                      \
+      case 32: KERNEL<32><<<GRID, 256, 0, ST>>>(__VA_ARGS__); break;    \
+      case 16: KERNEL<16><<<GRID, 256, 0, ST>>>(__VA_ARGS__); break;    \
+      case 8: KERNEL<8><<<GRID, 256, 0, ST>>>(__VA_ARGS__); break;      \
+      case 4: KERNEL<4><<<GRID, 256, 0, ST>>>(__VA_ARGS__); break;      \
+      case 2: KERNEL<2><<<GRID, 256, 0, ST>>>(__VA_ARGS__); break;      \
+      default: KERNEL<1><<<GRID, 256, 0, ST>>>(__VA_ARGS__); break;     \
+    }                                                                   \
+  } while (0)
 
 int nccl_status(ncclResult_t r, const char* what) {
   if (r == ncclSuccess) return HPS_GPU_OK;
@@ -194,7 +359,95 @@ void hpsg::comm_destroy(hps_gpu_ctx_s* ctx) {
   }
 }
 
+namespace {
+// The forward with the peer-memory transport (after the bucketize):
+//   regions stored into the owners -> signal/wait -> owner gather -> signal/wait -> pooling
+//   that loads the owners' rows directly.
+int dist_forward_peer(hps_gpu_dist d, const uint32_t* offsets, uint64_t n_bags, uint64_t n, int combiner, float* out,
+                      uint32_t flags) {
+  cudaStream_t st = d->ctx->stream;
+  const uint64_t GC = uint64_t(d->G) * d->C;
+  k_epoch_bump<<<1, 32, 0, st>>>(d->d_epoch);
+  k_fix_regions_peer<<<grid_for(std::max<uint64_t>(GC, n), 256, kNumSMs * 16), 256, 0, st>>>(
+      d->dense_keys, d->dense_tables, d->dense_perm, d->counts, d->G, d->rank, d->C, n, *d->peer, d->perm,
+      d->ctx->d_status);
+  k_signal<<<1, 64, 0, st>>>(*d->peer, 0, d->G, d->rank, d->d_epoch);
+  k_wait<<<1, 64, 0, st>>>(d->flags, 0, d->G, d->d_epoch);
+  HPSG_CHECK_LAUNCH("dist regions (peer)");
+  const uint32_t gflags = (flags & HPS_LOOKUP_TRAIN) | (flags & HPS_LOOKUP_INSERT);
+  if (int s = hps_gpu_gather_rows(d->shard, d->recv_keys, d->recv_tables, GC, d->rows_own, gflags)) return s;
+  k_signal<<<1, 64, 0, st>>>(*d->peer, 1, d->G, d->rank, d->d_epoch);
+  k_wait<<<1, 64, 0, st>>>(d->flags, 1, d->G, d->d_epoch);
+  const int lpr = lpr_of(d->dim);
+  HPSG_LPR_DISPATCH(k_pool_rows_peer, lpr, grid_for(n_bags * lpr, 256, kNumSMs * 32), st, *d->peer, d->rank, d->C,
+                    d->perm, offsets, n_bags, d->dim, combiner == HPS_COMBINER_MEAN, out);
+  HPSG_CHECK_LAUNCH("dist pool (peer)");
+  d->last_offsets = offsets;
+  d->last_bags = n_bags;
+  d->last_combiner = combiner;
+  d->have_fwd = true;
+  d->train = (flags & HPS_LOOKUP_TRAIN) != 0;
+  return HPS_GPU_OK;
+}
+
+void fill_self(hps_gpu_dist d, PeerTab& t, uint32_t p) {
+  t.keys[p] = d->recv_keys;
+  t.tables[p] = d->recv_tables;
+  t.rows[p] = d->rows_own;
+  t.grads[p] = d->grads_recv;
+  t.flags[p] = d->flags;
+}
+}  // namespace
+
 extern "C" {
+
+int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
+  if (!d || (transport != HPS_DIST_NCCL && transport != HPS_DIST_PEER)) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (transport == HPS_DIST_NCCL) {
+    d->transport = transport;
+    return HPS_GPU_OK;
+  }
+  if (d->G > kMaxPeers) return HPS_GPU_E_INVALID_ARGUMENT;
+  HPSG_CUDA(cudaSetDevice(d->ctx->device));
+  if (!d->peer) d->peer = new PeerTab{};
+  PeerTab& t = *d->peer;
+  if (d->G == 1) {
+    fill_self(d, t, 0);
+  } else if (d->loop) {  // loopback ranks: the peers' buffers are this device's memory
+    for (uint32_t p = 0; p < d->G; ++p) fill_self(d->loop->members[p], t, p);
+  } else {  // NCCL ranks: CUDA-IPC handles of every owner-side buffer, all-gathered over NCCL
+    cudaIpcMemHandle_t mine[5];
+    void* bufs[5] = {d->recv_keys, d->recv_tables, d->rows_own, d->grads_recv, d->flags};
+    for (int k = 0; k < 5; ++k) HPSG_CUDA(cudaIpcGetMemHandle(&mine[k], bufs[k]));
+    cudaIpcMemHandle_t* d_all = nullptr;
+    HPSG_CUDA(cudaMalloc(&d_all, sizeof(mine) * d->G));
+    HPSG_CUDA(cudaMemcpy(d_all + 5 * d->rank, mine, sizeof(mine), cudaMemcpyHostToDevice));
+    HPSG_NCCL(ncclAllGather(d_all + 5 * d->rank, d_all, sizeof(mine), ncclUint8, static_cast<ncclComm_t>(d->ctx->nccl),
+                            d->ctx->stream));
+    HPSG_CUDA(cudaStreamSynchronize(d->ctx->stream));
+    std::vector<cudaIpcMemHandle_t> all(5 * d->G);
+    HPSG_CUDA(cudaMemcpy(all.data(), d_all, sizeof(mine) * d->G, cudaMemcpyDeviceToHost));
+    cudaFree(d_all);
+    for (uint32_t p = 0; p < d->G; ++p) {
+      if (p == d->rank) {
+        fill_self(d, t, p);
+        continue;
+      }
+      void* ptr[5];
+      for (int k = 0; k < 5; ++k) {
+        HPSG_CUDA(cudaIpcOpenMemHandle(&ptr[k], all[5 * p + k], cudaIpcMemLazyEnablePeerAccess));
+        d->ipc_opened.push_back(ptr[k]);
+      }
+      t.keys[p] = static_cast<uint64_t*>(ptr[0]);
+      t.tables[p] = static_cast<uint32_t*>(ptr[1]);
+      t.rows[p] = static_cast<float*>(ptr[2]);
+      t.grads[p] = static_cast<float*>(ptr[3]);
+      t.flags[p] = static_cast<uint64_t*>(ptr[4]);
+    }
+  }
+  d->transport = HPS_DIST_PEER;
+  return HPS_GPU_OK;
+}
 
 int hps_gpu_nccl_unique_id(void* id_out) {
   if (!id_out) return HPS_GPU_E_INVALID_ARGUMENT;
@@ -272,6 +525,11 @@ int dist_create(hps_gpu_ctx ctx, hps_gpu_table shard, const hps_dist_config* cfg
   if (!st && cudaMemcpy(d->d_slot_table, cfg->slot_table_host, d->n_slots * 4, cudaMemcpyHostToDevice) != cudaSuccess)
     st = HPS_GPU_E_CUDA;
   if (!st && cudaEventCreateWithFlags(&d->loop_ev, cudaEventDisableTiming) != cudaSuccess) st = HPS_GPU_E_CUDA;
+  A(dalloc_n(&d->flags, 3 * uint64_t(d->G)));
+  A(dalloc_n(&d->d_epoch, 1));
+  if (!st && (cudaMemset(d->flags, 0, 3 * d->G * sizeof(uint64_t)) != cudaSuccess ||
+              cudaMemset(d->d_epoch, 0, sizeof(uint64_t)) != cudaSuccess))
+    st = HPS_GPU_E_CUDA;
   if (st) {
     hps_gpu_dist_destroy(d);
     return st;
@@ -308,6 +566,10 @@ int hps_gpu_dist_create_loopback(const hps_gpu_ctx* ctxs, const hps_gpu_table* s
 int hps_gpu_dist_destroy(hps_gpu_dist d) {
   if (!d) return HPS_GPU_OK;
   if (d->loop_ev) cudaEventDestroy(d->loop_ev);
+  for (void* p : d->ipc_opened) cudaIpcCloseMemHandle(p);
+  delete d->peer;
+  if (d->flags) cudaFree(d->flags);
+  if (d->d_epoch) cudaFree(d->d_epoch);
   if (d->plan) hps_gpu_xplan_destroy(d->plan);
   void* own[] = {d->d_slot_table, d->dense_keys, d->dense_tables, d->dense_perm, d->counts, d->occ_bag, d->perm,
                  d->send_keys,    d->send_tables, d->rows_own,    d->grads_send};
@@ -342,6 +604,7 @@ int hps_gpu_dist_forward(hps_gpu_dist d, const uint64_t* keys, const uint32_t* o
   if (int s = hps_gpu_xplan_bucketize(d->plan, keys, n, multi ? d->occ_bag : nullptr, d->n_slots, d->d_slot_table,
                                       d->dense_keys, d->dense_tables, d->dense_perm, d->counts))
     return s;
+  if (d->transport == HPS_DIST_PEER) return dist_forward_peer(d, offsets, n_bags, n, combiner, out, flags);
   k_fix_regions<<<grid_for(std::max<uint64_t>(GC, n), 256, kNumSMs * 16), 256, 0, st>>>(
       d->dense_keys, d->dense_tables, d->dense_perm, d->counts, d->G, d->C, n, d->send_keys, d->send_tables, d->perm,
       d->ctx->d_status);
@@ -365,6 +628,19 @@ int hps_gpu_dist_backward(hps_gpu_dist d, const float* d_out, const hps_opt_para
   if (!d->have_fwd || !d->train) {
     set_last_error("dist_backward: no preceding training dist_forward");
     return HPS_GPU_E_INVALID_ARGUMENT;
+  }
+  if (d->transport == HPS_DIST_PEER) {  // gradients stored straight into the owners' regions
+    cudaStream_t st = d->ctx->stream;
+    const int lpr = lpr_of(d->dim);
+    HPSG_LPR_DISPATCH(k_scatter_grads_peer, lpr, grid_for(d->last_bags * lpr, 256, kNumSMs * 32), st, *d->peer,
+                      d->rank, d->C, d_out, d->perm, d->last_offsets, d->last_bags, d->dim,
+                      d->last_combiner == HPS_COMBINER_MEAN);
+    k_signal<<<1, 64, 0, st>>>(*d->peer, 2, d->G, d->rank, d->d_epoch);
+    k_wait<<<1, 64, 0, st>>>(d->flags, 2, d->G, d->d_epoch);
+    HPSG_CHECK_LAUNCH("dist backward (peer)");
+    if (int s = hps_gpu_backward_update(d->shard, d->grads_recv, opt)) return s;
+    d->have_fwd = false;
+    return HPS_GPU_OK;
   }
   if (int s = hps_gpu_scatter_grads(d->ctx, d_out, d->perm, d->last_offsets, d->last_bags, d->dim, d->last_combiner,
                                     d->grads_send))

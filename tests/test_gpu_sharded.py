@@ -62,7 +62,7 @@ def compare_owned(shards, single, pools, world):
                     close(g, o[orow], f"rank {r} table {t} state {k}")
 
 
-def run_world(world, multi, optimizer, steps=3, insert=False):
+def run_world(world, multi, optimizer, steps=3, insert=False, transport="nccl"):
     rs = np.random.default_rng(100 * world + 10 * multi + len(optimizer))
     cards, slot_table, dim = [3000, 9, 600], [0, 1, 2, 1], 32 if multi else 128
     comb = "mean" if multi else "sum"
@@ -100,6 +100,9 @@ def run_world(world, multi, optimizer, steps=3, insert=False):
             d.capacity = int(cp.value)
             dists.append(d)
     assert dists[0].capacity == cap
+    if transport != "nccl":
+        for d in dists:
+            d.set_transport(transport)
 
     def on_ranks(fn):
         errs = [None] * world
@@ -153,6 +156,16 @@ def run_world(world, multi, optimizer, steps=3, insert=False):
 @pytest.mark.parametrize("multi,optimizer", [(False, "sgd"), (True, "adagrad"), (False, "adam")])
 def test_dist_step_matches_single_table(ctx, world, multi, optimizer):
     run_world(world, multi, optimizer)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("multi,optimizer", [(False, "sgd"), (True, "adagrad")])
+def test_dist_peer_transport_matches_single_table(ctx, world, multi, optimizer):
+    """The peer-memory transport (hps_gpu_dist_set_transport(HPS_DIST_PEER)): the region
+    kernel stores into the owners' buffers, the pooling loads the owners' rows, the gradient
+    scatter stores into the owners' regions, epochs in flag words order the phases — on the
+    loopback ranks the peers' memory is this device's, the same code that runs over NVLink."""
+    run_world(world, multi, optimizer, transport="peer")
 
 
 def test_dist_graph_step_world1(ctx):
