@@ -63,6 +63,8 @@ def parse():
                     choices=["auto", "distributed", "distributed-py", "localized", "hybrid"],
                     help="multi-GPU slot placement (auto: localized for cfg3, distributed otherwise)")
     ap.add_argument("--hot-budget-gb", type=float, default=0.0625, help="hybrid: replicated hot rows per GPU")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="distributed placement through the C-ABI: NCCL all-to-alls, or peer-memory kernels")
     ap.add_argument("--force-exchange", action="store_true",
                     help="run the multi-GPU exchange path (NCCL world of one) on a single GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -328,7 +330,8 @@ def main():
         tables = build_tables_localized(ctx, cfg, owned, rank, world)
     gen = W.BatchGen(cfg)
     step_fn = TrainStep(ctx, tables, cfg, rank, world, use_graph=not args.no_graph, owned=owned, hybrid_hot=hot,
-                        force_exchange=xchg, pipeline=args.pipeline, cabi=placement != "distributed-py")
+                        force_exchange=xchg, pipeline=args.pipeline, cabi=placement != "distributed-py",
+                        transport=args.transport)
     pool = []
     rs = np.random.default_rng(rank)
     n_bags = cfg.batch * cfg.n_slots

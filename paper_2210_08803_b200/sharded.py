@@ -186,7 +186,7 @@ class TrainStep:
     def __init__(self, ctx: Context, table: Optional[EmbeddingTableGroup], cfg: W.Config, rank: int = 0,
                  world: int = 1, use_graph: bool = True, owned: Optional[List[List[int]]] = None,
                  hybrid_hot: Optional[EmbeddingTableGroup] = None, force_exchange: bool = False,
-                 pipeline: bool = False, cabi: bool = True):
+                 pipeline: bool = False, cabi: bool = True, transport: str = "nccl"):
         """owned (world > 1): localized placement, owned[g] = slots of rank g (localized_plan);
         None = distributed placement."""
         self.ctx, self.table, self.cfg, self.rank, self.world = ctx, table, cfg, rank, world
@@ -234,6 +234,7 @@ class TrainStep:
             # distributed slot through the C-ABI (sharded.cu): NCCL inside libhps_gpu, fixed
             # per-peer regions, no host sync, so the step is replayed as one CUDA graph
             self.exchange = CabiDistExchange(ctx, table, cfg, rank, world, self.insert_missing)
+            self.exchange.dt.set_transport(transport)
             self.placement = "distributed"
             self.graph_mode = bool(use_graph)
             self.kernels_per_step = 5 + 1 + rec + 1 + 1 + 1 + 2 + (1 if cfg.hot > 1 else 0)

@@ -3,9 +3,10 @@
 //  1. NCCL world of one: hps_gpu_nccl_unique_id + hps_gpu_ctx_comm_init, then dist steps
 //     against the unsharded path (lookup_pooled + backward_update) on a twin table: pooled
 //     outputs and the final rows bitwise equal.
-//  2. Loopback world of two (one thread per rank, hps_gpu_dist_create_loopback): each rank
-//     owns partition_of(key, 2) == rank (proj/include/hps/hash.hpp:52-54); outputs and every
-//     owned row bitwise equal to ONE table driven with the concatenated batch (rank-major).
+//  2. Loopback world of two (one thread per rank, hps_gpu_dist_create_loopback), with the
+//     copy transport and with the peer-memory transport (HPS_DIST_PEER): each rank owns
+//     partition_of(key, 2) == rank (proj/include/hps/hash.hpp:52-54); outputs and every owned
+//     row bitwise equal to ONE table driven with the concatenated batch (rank-major).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -166,8 +167,9 @@ int main() {
     OK(hps_gpu_ctx_destroy(ctx));
   }
 
-  // ---- 2. loopback world of two, one thread per rank ----
-  {
+  // ---- 2. loopback world of two, one thread per rank (all-to-alls as copies, then the
+  //         peer-memory transport: the kernels load/store each other's regions) ----
+  for (int transport : {HPS_DIST_NCCL, HPS_DIST_PEER}) {
     constexpr uint32_t G = 2;
     hps_gpu_ctx single_ctx = nullptr, ctxs[G] = {};
     OK(hps_gpu_ctx_create(0, nullptr, &single_ctx));
@@ -197,6 +199,7 @@ int main() {
     hps_dist_config dc{kS, kSlots, kDim, mk, kB * kS, 0.f};
     hps_gpu_dist ds[G];
     OK(hps_gpu_dist_create_loopback(ctxs, shards, &dc, G, ds));
+    for (uint32_t r = 0; r < G; ++r) OK(hps_gpu_dist_set_transport(ds[r], transport));
     float* os = nullptr;
     cudaMalloc(&os, G * kB * kS * kDim * 4);
     float* ol[G];
