@@ -541,7 +541,7 @@ __device__ __forceinline__ void warp_store_row(void* cvec, uint64_t e, const flo
 
 // ---- K7: insert, one warp per touched set, entries in input order --------------------
 template <bool F16>
-__global__ void __launch_bounds__(256, 4) k_insert_sets(const uint32_t* __restrict__ sets_sorted,
+__global__ void __launch_bounds__(256) k_insert_sets(const uint32_t* __restrict__ sets_sorted,
                                                      const uint32_t* __restrict__ idx_sorted,
                                                      const uint32_t* __restrict__ seg_start, const uint64_t* counts,
                                                      const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
@@ -625,6 +625,128 @@ __global__ void __launch_bounds__(256, 4) k_insert_sets(const uint32_t* __restri
     }
     if (lane == 0) set_acc[s] = acc;
   }
+  if (lane == 0 && (n_ins | n_evict | n_refresh)) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sInsertions]), n_ins);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sEvictions]), n_evict);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sRefresh]), n_refresh);
+    if (admitted_out) atomicAdd(reinterpret_cast<unsigned long long*>(admitted_out), n_ins);
+  }
+}
+
+// ---- K7, narrow sets (ways <= 8): four sets per warp, an 8-lane group each -------------
+// The same replay as k_insert_sets (entries of a set in input order; resident -> version-gated
+// refresh, else the lowest free way, else the (freq, last_touch, way) minimum is evicted),
+// with a set's ways on the 8 lanes of one group: four sets' dependent load chains in flight per
+// warp instead of one. Rows are copied by the group (lane l of 8: float4s l, l + 8, ...).
+template <bool F16>
+__device__ __forceinline__ void group_store_row(void* cvec, uint64_t e, const float* src, uint32_t dim, uint32_t gl) {
+  const uint32_t nvec = dim / 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  if constexpr (F16) {
+    uint2* d = reinterpret_cast<uint2*>(static_cast<__half*>(cvec) + e * dim);
+    for (uint32_t q = gl; q < nvec; q += 8) {
+      const float4 x = __ldg(s4 + q);
+      const __half2 lo = __floats2half2_rn(x.x, x.y), hi = __floats2half2_rn(x.z, x.w);
+      d[q] = make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
+  } else {
+    float4* d4 = reinterpret_cast<float4*>(static_cast<float*>(cvec) + e * dim);
+    for (uint32_t q = gl; q < nvec; q += 8) d4[q] = __ldg(s4 + q);
+  }
+}
+
+template <bool F16>
+__global__ void __launch_bounds__(256) k_insert_sets8(const uint32_t* __restrict__ sets_sorted,
+                                                     const uint32_t* __restrict__ idx_sorted,
+                                                     const uint32_t* __restrict__ seg_start, const uint64_t* counts,
+                                                     const uint64_t* __restrict__ keys, const float* __restrict__ vecs,
+                                                     const uint64_t* __restrict__ versions,
+                                                     const uint32_t* __restrict__ rank, uint32_t ways, uint32_t dim,
+                                                     uint64_t aging_period, uint32_t invalid_set, uint64_t* ckeys,
+                                                     uint64_t* cver, uint8_t* cfreq, uint64_t* ctouch, uint64_t* set_acc,
+                                                     void* cvec, uint64_t* state, uint64_t* admitted_out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint32_t lane = lane_id(), g = lane >> 3, gl = lane & 7u;
+  const uint32_t gmask = 0xffu << (8 * g);
+  const uint64_t U = counts[1];
+  const uint64_t clock0 = state[kSnap];
+  const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t n_groups = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * 4;
+  uint64_t n_ins = 0, n_evict = 0, n_refresh = 0;
+  for (uint64_t u = warp * 4 + g; u < U; u += n_groups) {
+    const uint32_t lo = seg_start[u], hi = seg_start[u + 1];
+    const uint32_t s32 = sets_sorted[lo];
+    if (s32 == invalid_set) continue;
+    const uint64_t s = s32, e0 = s * ways;
+    const bool way = gl < ways;
+    // the set's metadata and its first entry are loaded together
+    uint64_t k_w = way ? ckeys[e0 + gl] : 0, v_w = way ? cver[e0 + gl] : 0, t_w = way ? ctouch[e0 + gl] : 0;
+    uint32_t f_w = way ? cfreq[e0 + gl] : 0;
+    uint64_t acc = set_acc[s];
+    for (uint32_t j = lo; j < hi; ++j) {
+      const uint32_t i = idx_sorted[j];
+      const uint64_t k = keys[i], ver = versions ? versions[i] : hps::kBulkLoadVersion;
+      const uint64_t t = clock0 + rank[i] + 1;
+      if (++acc >= aging_period) {
+        acc = 0;
+        f_w = age_freq(f_w);
+      }
+      const uint32_t res = (__ballot_sync(gmask, way && f_w != 0 && k_w == k) >> (8 * g)) & 0xffu;
+      if (res) {  // resident: refresh semantics
+        const int w = __ffs(res) - 1;
+        const uint64_t vw = __shfl_sync(gmask, v_w, 8 * g + w);
+        if (ver > vw) {
+          group_store_row<F16>(cvec, e0 + w, vecs + uint64_t(i) * dim, dim, gl);
+          if (gl == static_cast<uint32_t>(w)) v_w = ver;
+          ++n_refresh;
+        }
+        continue;
+      }
+      const uint32_t free_ways = (__ballot_sync(gmask, way && f_w == 0) >> (8 * g)) & 0xffu;
+      int w;
+      if (free_ways) {
+        w = __ffs(free_ways) - 1;
+      } else {  // victim = min (freq, last_touch, way) over the group's lanes
+        uint32_t bf = way ? f_w : 0xffffffffu;
+        uint64_t bt = way ? t_w : ~0ull;
+        uint32_t bl = gl;
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) {
+          const uint32_t of = __shfl_xor_sync(gmask, bf, o);
+          const uint64_t ot = __shfl_xor_sync(gmask, bt, o);
+          const uint32_t ol = __shfl_xor_sync(gmask, bl, o);
+          if (of < bf || (of == bf && (ot < bt || (ot == bt && ol < bl)))) {
+            bf = of;
+            bt = ot;
+            bl = ol;
+          }
+        }
+        w = static_cast<int>(bl);
+        ++n_evict;
+      }
+      if (gl == static_cast<uint32_t>(w)) {
+        k_w = k;
+        v_w = ver;
+        f_w = 1;
+        t_w = t;
+      }
+      group_store_row<F16>(cvec, e0 + w, vecs + uint64_t(i) * dim, dim, gl);
+      ++n_ins;
+    }
+    if (way) {
+      ckeys[e0 + gl] = k_w;
+      cver[e0 + gl] = v_w;
+      cfreq[e0 + gl] = static_cast<uint8_t>(f_w);
+      ctouch[e0 + gl] = t_w;
+    }
+    if (gl == 0) set_acc[s] = acc;
+  }
+  // counts are per group (every lane of a group counted the same events): lane gl == 0 adds
+  if (gl != 0) n_ins = n_evict = n_refresh = 0;
+  n_ins = warp_sum(n_ins);
+  n_evict = warp_sum(n_evict);
+  n_refresh = warp_sum(n_refresh);
   if (lane == 0 && (n_ins | n_evict | n_refresh)) {
     atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sInsertions]), n_ins);
     atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sEvictions]), n_evict);
@@ -1031,6 +1153,12 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
+  if (c->ways <= 8)  // four sets per warp
+    launch_k(true, (c->f16 ? k_insert_sets8<true> : k_insert_sets8<false>), grid_for((n + 3) / 4 * 32, 256, kNumSMs * 16),
+             256, 0, st, sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ws_rank, c->ways,
+             c->dim, c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch,
+             c->d_set_acc, c->d_vec, c->d_state, admitted_out);
+  else
   launch_k(true, (c->f16 ? k_insert_sets<true> : k_insert_sets<false>), set_warps_grid(n), 256, 0, st, 
       sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ws_rank, c->ways, c->dim,
       c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch, c->d_set_acc,
