@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhps_gpu.so")
+LIB_PATH = os.environ.get("HPS_GPU_LIB_PATH") or os.path.join(HERE, "libhps_gpu.so")  # (override: A/B builds)
 
 u8, u32, u64, i32 = C.c_uint8, C.c_uint32, C.c_uint64, C.c_int
 f32 = C.c_float
