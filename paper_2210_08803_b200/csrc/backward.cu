@@ -706,7 +706,10 @@ __device__ __forceinline__ void add_into(float4 (&acc)[VPL], const float4 (&x)[V
 template <int OPT, int LPR, int VPL>
 __device__ __forceinline__ void short_reg(const BwdArgs& a, uint64_t warp, uint64_t n_warps, uint32_t* sbag) {
   constexpr int G = 32 / LPR;  // lane groups (segment streams) per warp
-  constexpr int R = VPL >= 4 ? 1 : 4 / VPL;  // segments in flight per group (register budget)
+  // segments in flight per group (register budget). Two half-warp groups (dim 64) keep 2 each
+  // at 3 CTAs/SM: 4 each needed 128 registers and held the kernel at 2 CTAs/SM (config 3:
+  // 0.668 -> 0.602 ms per step, profiles/round2)
+  constexpr int R = LPR == 16 ? 2 : (VPL >= 4 ? 1 : 4 / VPL);
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR;
   const uint64_t S = *a.short_alloc >> 32;
   const bool mean = a.bag_len != nullptr;
@@ -1244,7 +1247,8 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
 // ---- kernels ------------------------------------------------------------------------------
 // Short segments reduced + updated.
 template <int OPT, int LPR, int VPL, bool TMA>
-__global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256, TMA ? 1 : (OPT == HPS_OPT_ADAM || LPR == 16 ? 2 : 3))
+__global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256,
+                                  TMA ? 1 : (OPT == HPS_OPT_ADAM ? 2 : 3))
     k_reduce_short(BwdArgs a) {
   extern __shared__ __align__(128) float s_dyn[];  // TMA: [kRedWarps][cap][dim] rows, scales, bags
   __shared__ __align__(8) uint64_t s_bar[kRedWarps];
