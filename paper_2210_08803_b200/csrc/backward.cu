@@ -183,7 +183,6 @@ __device__ __forceinline__ void register_long(const BwdArgs& a, bool lg, uint32_
 //   P3 placement: short occurrences drop their bag at first + rank; long occurrences are
 //      compacted in canonical order (per-CTA counts -> prefix over CTAs -> block scans)
 // Batch-table words written by other CTAs are read through L2 (__ldcg) after a barrier.
-constexpr int kDedupBlock = 512;
 constexpr int kDedupHash = 8192;
 constexpr uint32_t kNoEnt = 0xffffffffu;
 constexpr uint32_t kDirectEnt = 0x80000000u;  // occ_ent flag inside P1: counted directly
@@ -203,10 +202,12 @@ __device__ __forceinline__ uint32_t smem_hash_slot(uint32_t* s_key, uint32_t row
 }
 
 // Every pass walks the chunk in batches of kDedupIPT items per thread whose loads are all
-// issued before any is consumed (these phases are latency-bound, not bandwidth-bound).
-constexpr int kDedupIPT = 8;
-
-__global__ void __launch_bounds__(kDedupBlock, 2) k_dedup(BwdArgs a, uint32_t* coop) {
+// issued before any is consumed (these phases are latency-bound, not bandwidth-bound). Two
+// shapes (choose_dedup_shape): 512 threads x 8 items, or 1024 threads x 4 (twice the warps
+// to hide the phases' L2 round trips; config 2: 0.138 -> 0.12 ms; the Zipf configs, whose
+// large chunks favour the deeper per-thread batches, keep 512 x 8).
+template <int kDedupBlock, int kDedupIPT>
+__global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdArgs a, uint32_t* coop) {
   extern __shared__ uint32_t s_dd[];
   uint32_t* s_key = s_dd;               // row, then its batch-table entry
   uint32_t* s_val = s_dd + kDedupHash;  // chunk count, then the CTA's base rank
@@ -1437,9 +1438,11 @@ namespace {
 std::atomic<uint64_t> g_dedup_attr{0};
 cudaError_t dedup_attributes() {
   return once_per_device(g_dedup_attr, []() -> cudaError_t {
-    if (cudaError_t e = cudaFuncSetAttribute(k_dedup, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4))
-      return e;
-    for (cudaError_t e : {prefer_max_smem(k_dedup), prefer_max_smem(k_count_flat), prefer_max_smem(k_alloc_flat),
+    for (auto kern : {k_dedup<512, 8>, k_dedup<1024, 4>})
+      if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kDedupHash * 4))
+        return e;
+    for (cudaError_t e : {prefer_max_smem(k_dedup<512, 8>), prefer_max_smem(k_dedup<1024, 4>),
+                          prefer_max_smem(k_count_flat), prefer_max_smem(k_alloc_flat),
                           prefer_max_smem(k_scan<PlaceOp>), prefer_max_smem(k_radix_hist), prefer_max_smem(k_radix_pass)})
       if (e) return e;
     return cudaSuccess;
@@ -1456,7 +1459,11 @@ cudaError_t dedup_attributes() {
 int hpsg::choose_dedup(bool* flat_out) {
   HPSG_CUDA(dedup_attributes());
   int per_sm = 0;
-  HPSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dedup, kDedupBlock, size_t(2) * kDedupHash * 4));
+  int per_sm_wide = 0;
+  HPSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dedup<512, 8>, 512, size_t(2) * kDedupHash * 4));
+  HPSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_wide, k_dedup<1024, 4>, 1024,
+                                                          size_t(2) * kDedupHash * 4));
+  per_sm = std::min(per_sm, per_sm_wide);
   bool flat = per_sm < 1;
   if (const char* e = std::getenv("HPS_GPU_DEDUP")) {
     if (std::strcmp(e, "flat") == 0) flat = true;
@@ -1502,7 +1509,14 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
     // A plain launch (a cooperative one would not start beside the pooling): co-residency of
     // the grid barriers holds by construction — at most one CTA per SM, and every kernel it
     // can share the SMs with (the pooling) runs to completion without waiting on it.
-    HPSG_CUDA(launch_k(false, k_dedup, g, kDedupBlock, size_t(2) * kDedupHash * 4, st, a, z + zl.coop));
+    // shape: one-hot batches 1024 x 4 (short per-CTA chunks: more warps in flight), multi-hot
+    // 512 x 8 (long chunks); HPS_GPU_DEDUP_SHAPE=512|1024 forces one (A/B)
+    bool wide = !t->last_multi;
+    if (const char* e = std::getenv("HPS_GPU_DEDUP_SHAPE")) wide = std::atoi(e) == 1024;
+    if (wide)
+      HPSG_CUDA(launch_k(false, k_dedup<1024, 4>, g, 1024, size_t(2) * kDedupHash * 4, st, a, z + zl.coop));
+    else
+      HPSG_CUDA(launch_k(false, k_dedup<512, 8>, g, 512, size_t(2) * kDedupHash * 4, st, a, z + zl.coop));
   }
   // the short segments are complete: the short reduce may start (backward_update joins here);
   // the long segments' sort and registration continue on this stream
