@@ -361,6 +361,12 @@ struct hps_gpu_ctx_s {
   bool pdl = true;               // programmatic dependent launch in the step chains (HPS_GPU_NO_PDL=1 disables)
   int num_sms = hpsg::kNumSMs;   // multiProcessorCount of the device (the persistent dedup's grid cap)
   void* nccl = nullptr;          // ncclComm_t of the sharded path (hps_gpu_ctx_comm_init; sharded.cu)
+  // The last persistent dedup launched by any table of this context: the next one waits for it.
+  // A k_dedup grid needs all its CTAs resident at once (grid barriers); two running together
+  // (two tables, e.g. the hybrid hot + cold groups, or two batch slots) could each hold part of
+  // the SMs the other needs. (Owned by the table slot that recorded it; cleared on its destroy.)
+  cudaEvent_t ev_last_dedup = nullptr;
+  unsigned long long last_dedup_capture = 0;
   int rank = 0, world = 1;
 };
 namespace hpsg {

@@ -409,6 +409,22 @@ int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
   }
   if (d->G > kMaxPeers) return HPS_GPU_E_INVALID_ARGUMENT;
   HPSG_CUDA(cudaSetDevice(d->ctx->device));
+  {  // load every kernel of the peer path now: a lazy module load inside a step could wait for
+     // the device while a peer's wait kernel spins on this rank's signal
+    cudaFuncAttributes fa;
+    for (const void* f : {reinterpret_cast<const void*>(k_fix_regions_peer), reinterpret_cast<const void*>(k_epoch_bump),
+                          reinterpret_cast<const void*>(k_signal), reinterpret_cast<const void*>(k_wait),
+                          reinterpret_cast<const void*>(k_pool_rows_peer<32>), reinterpret_cast<const void*>(k_pool_rows_peer<16>),
+                          reinterpret_cast<const void*>(k_pool_rows_peer<8>), reinterpret_cast<const void*>(k_pool_rows_peer<4>),
+                          reinterpret_cast<const void*>(k_pool_rows_peer<2>), reinterpret_cast<const void*>(k_pool_rows_peer<1>),
+                          reinterpret_cast<const void*>(k_scatter_grads_peer<32>),
+                          reinterpret_cast<const void*>(k_scatter_grads_peer<16>),
+                          reinterpret_cast<const void*>(k_scatter_grads_peer<8>),
+                          reinterpret_cast<const void*>(k_scatter_grads_peer<4>),
+                          reinterpret_cast<const void*>(k_scatter_grads_peer<2>),
+                          reinterpret_cast<const void*>(k_scatter_grads_peer<1>)})
+      HPSG_CUDA(cudaFuncGetAttributes(&fa, f));
+  }
   if (!d->peer) d->peer = new PeerTab{};
   PeerTab& t = *d->peer;
   if (d->G == 1) {

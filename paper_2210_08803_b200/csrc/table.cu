@@ -853,13 +853,13 @@ int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t
 // The dedup of the current slot on its side stream. A table's dedups run one at a time
 // (each is a persistent kernel whose grid barriers need all its CTAs resident).
 int dedup_on_side(hps_gpu_table t) {
-  if (t->last_dedup_valid && t->ev_last_dedup != t->ev_done)
-    HPSG_CUDA(wait_recorded(t->side, t->ev_last_dedup, t->last_dedup_capture));
+  hps_gpu_ctx c = t->ctx;
+  if (c->ev_last_dedup && c->ev_last_dedup != t->ev_done)
+    HPSG_CUDA(wait_recorded(t->side, c->ev_last_dedup, c->last_dedup_capture));
   if (int s = launch_dedup(t, t->side)) return s;  // records ev_join after the short placement
   HPSG_CUDA(cudaEventRecord(t->ev_done, t->side));
-  t->ev_last_dedup = t->ev_done;
-  t->last_dedup_valid = true;
-  t->last_dedup_capture = capture_id(t->side);
+  c->ev_last_dedup = t->ev_done;
+  c->last_dedup_capture = capture_id(t->side);
   t->dedup_pending = true;
   return HPS_GPU_OK;
 }
@@ -1253,8 +1253,10 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
   if (!t) return HPS_GPU_OK;
   if (t->parked.empty()) t->parked.resize(1);
   t->parked[t->cur] = static_cast<BatchSlot&>(*t);
-  for (BatchSlot& b : t->parked)
+  for (BatchSlot& b : t->parked) {
     if (b.side) cudaStreamSynchronize(b.side);
+    if (t->ctx && t->ctx->ev_last_dedup == b.ev_done) t->ctx->ev_last_dedup = nullptr;  // (about to be destroyed)
+  }
   void* ptrs[] = {t->d_wh,        t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
                   t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_io};
   for (void* p : ptrs)

@@ -148,11 +148,9 @@ struct hps_gpu_table_s : BatchSlot {
   // batch slots: `cur` is the one held in the BatchSlot base; parked[k] holds slot k otherwise
   std::vector<BatchSlot> parked;  // size = pipeline depth (entry `cur` is stale while current)
   uint32_t cur = 0;
-  cudaEvent_t ev_last_dedup = nullptr;  // the last k_dedup launched (prefetches serialise on it)
-  bool last_dedup_valid = false;
+
   bool graphs_seen = false;
   bool flat_dedup = false;   // the three-kernel dedup (choose_dedup at create)  // a training record was captured into a graph (host slot flags may lag replays)
-  unsigned long long last_dedup_capture = 0;
   bool no_fork = false;         // HPS_GPU_NO_FORK=1: everything on the main stream (A/B measurement)
   bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)
 };

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <thread>
@@ -110,6 +111,9 @@ std::vector<uint64_t> batch(std::mt19937_64& rng, const std::vector<std::vector<
 }  // namespace
 
 int main() {
+  // the loopback ranks of the peer transport spin-wait on each other inside one process: every
+  // module is loaded up front (a lazy load could wait for the device while a peer spins)
+  setenv("CUDA_MODULE_LOADING", "EAGER", 1);
   std::mt19937_64 rng(42);
   std::vector<std::vector<uint64_t>> pools(2);
   for (int t = 0; t < 2; ++t)
