@@ -19,6 +19,7 @@ same step (the oracle port, all host threads) on a bounded sample.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -256,7 +257,7 @@ def reference_arm(args, cfg, rank, world):
 TRACE_NAMES = {0: "probe", 1: "pool", 2: "seg_alloc", 3: "place", 4: "long_hist", 5: "long_pass0",
                6: "long_pass1", 7: "long_pass2", 8: "long_pass3", 9: "long_reg", 10: "reduce_short",
                11: "reduce_long", 12: "reset_counts", 13: "count", 14: "|count_local", 15: "|count_global",
-               16: "|count_cas", 17: "|count_probe"}
+               16: "|count_cas", 17: "|count_probe", 18: "mid", 19: "<step-in", 20: ">step-out"}
 
 
 def print_trace(ctx, n, step):
@@ -413,7 +414,12 @@ def main():
     torch.cuda.synchronize()
     fwd_ms = [a.elapsed_time(b) for a, b in fwd_ev]
     if args.trace:
-        print_trace(ctx, args.trace, lambda i: (flush.fill_(i & 0xff), one(i)))
+        def traced(i):  # stamps around the step mark its start/end latency in the stream
+            flush.fill_(i & 0xff)
+            ctx.lib.hps_gpu_debug_stamp(ctypes.c_void_p(stream.cuda_stream), 19)
+            one(i)
+            ctx.lib.hps_gpu_debug_stamp(ctypes.c_void_p(stream.cuda_stream), 20)
+        print_trace(ctx, args.trace, traced)
     ms = float(np.mean(step_ms))
     t = torch.tensor([ms], device="cuda")
     if world > 1:

@@ -237,6 +237,9 @@ int hps_gpu_table_last_unique(hps_gpu_table tbl, uint64_t* count_out, uint32_t* 
  * 4 long-sort histogram, 5..8 long-sort passes, 9 long registration, 10 short reduce,
  * 11 long reduce, 12 counter reset, 13 counts (14, 15: end of its local / global phase). Synchronises the device; not for hot paths. */
 int hps_gpu_debug_trace(int mode, uint64_t* trace_host);
+/* Debug: a one-warp kernel on `stream` that stamps %globaltimer into trace slot `id` (start and
+   end), marking a point in the stream's order on the hps_gpu_debug_trace timeline. */
+int hps_gpu_debug_stamp(void* stream, int id);
 
 /* Invariant check for tests: entries of the table's per-batch dedup table still in use
  * (0 whenever no training record is pending). Synchronises. */

@@ -157,6 +157,7 @@ SIGNATURES = {
     "hps_gpu_table_join_prefetch": (i32, [vp]),
     "hps_gpu_table_last_unique": (i32, [vp, vp, vp]),
     "hps_gpu_debug_trace": (i32, [i32, vp]),
+    "hps_gpu_debug_stamp": (i32, [vp, i32]),
     "hps_gpu_debug_batch_table_used": (i32, [vp, vp]),
     "hps_gpu_gather_rows": (i32, [vp, vp, vp, u64, vp, u32]),
     "hps_gpu_xplan_create": (i32, [vp, u64, u32, C.POINTER(vp)]),

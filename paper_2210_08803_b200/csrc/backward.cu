@@ -1726,6 +1726,24 @@ int hps_gpu_apply_grads(hps_gpu_table t, const float* grads, const uint32_t* tou
 // trace buffer; 2: copy the kTraceSlots x {start_ns, end_ns} records to trace_host
 // (2 * kTraceSlots u64; start = UINT64_MAX when the kernel did not run) and re-arm;
 // 0: detach. Synchronises the device.
+}  // extern "C"
+
+namespace {
+__global__ void k_stamp(int id) {
+  trace_begin(id);
+  trace_end(id);
+}
+}  // namespace
+
+extern "C" {
+
+int hps_gpu_debug_stamp(void* stream, int id) {
+  if (id < 0 || id >= kTraceSlots) return HPS_GPU_E_INVALID_ARGUMENT;
+  k_stamp<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(id);
+  HPSG_CHECK_LAUNCH("k_stamp");
+  return HPS_GPU_OK;
+}
+
 int hps_gpu_debug_trace(int mode, uint64_t* trace_host) {
   static TraceRec* buf = nullptr;
   constexpr size_t kRecs = size_t(kTraceSlots) * kTraceSMs;

@@ -336,6 +336,8 @@ struct LookupArgs {
   uint64_t* d_n;       // number of key occurrences (device)
   uint64_t max_keys;   // training record capacity (max_batch_keys)
   uint32_t* status;    // ctx status word: a device-offsets batch larger than max_keys latches InvalidArgument
+  uint32_t* zero;      // training: the backward's zeroed words (bwd_zero_layout), cleared by the probe
+  uint32_t zero_words;
 };
 
 // K3a (training): probe every occurrence once and record its row (row_absent when the
@@ -347,6 +349,9 @@ __global__ void __launch_bounds__(256) k_probe(LookupArgs a) {
   const uint32_t lane = lane_id();
   const uint64_t n_bags = a.n_bags;
   trace_begin(kTrProbe);
+  // the backward's allocators and look-back words start from zero (the dedup, forked after
+  // this kernel, is their first user): cleared here instead of by a memset node of its own
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.zero_words; i += gridDim.x * blockDim.x) a.zero[i] = 0;
   if constexpr (MULTI) {
     // device offsets are not validated on the host: a batch beyond the record's capacity is
     // refused here (latched InvalidArgument, an empty record) instead of overrunning it
@@ -415,8 +420,11 @@ __global__ void __launch_bounds__(256) k_probe(LookupArgs a) {
 // Batch-table entries left by a training record that no backward consumed: back to empty.
 __global__ void k_reset_counts(const uint32_t* __restrict__ occ_row, const uint32_t* __restrict__ occ_ent,
                                const uint64_t* d_n, uint32_t row_absent, uint2* bt) {
-  if (d_n[5] == 0) return;  // no unconsumed record in this slot (device truth; see begin_training_record)
   trace_begin(kTrReset);
+  if (d_n[5] == 0) {  // no unconsumed record in this slot (device truth; see begin_training_record)
+    trace_end(kTrReset);
+    return;
+  }
   const uint64_t n = *d_n;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     if (occ_row[i] != row_absent) bt[occ_ent[i]] = make_uint2(kBtEmpty, 0xffffffffu);
@@ -818,7 +826,8 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk, cudaStrea
         t->ws_rows_a, t->ws_occ_ent, t->ws_counts, t->row_absent, t->ws_bt);
     HPSG_CHECK_LAUNCH("k_reset_counts");
   }
-  HPSG_CUDA(cudaMemsetAsync(t->ws_zero, 0, bwd_zero_layout(nk).total * sizeof(uint32_t), st));
+  a.zero = t->ws_zero;  // cleared by k_probe, which record() launches next
+  a.zero_words = static_cast<uint32_t>(bwd_zero_layout(nk).total);
   a.occ_row = t->ws_rows_a;
 
   a.row_absent = t->row_absent;

@@ -6,6 +6,8 @@ the exchange lives in paper_2210_08803_b200.exchange.
 """
 from __future__ import annotations
 
+import os
+
 import math
 from typing import List, Optional
 
@@ -324,9 +326,14 @@ class TrainStep:
             with torch.cuda.stream(s):
                 self.ctx.set_stream(s)
                 fn()  # this call's step (capture below records without executing)
-                g = torch.cuda.CUDAGraph()
+                dump = os.environ.get("HPS_GRAPH_DUMP")  # debug: the captured graph as DOT
+                g = torch.cuda.CUDAGraph(keep_graph=bool(dump))
+                if dump:
+                    g.enable_debug_mode()
                 with torch.cuda.graph(g, stream=s):
                     fn()
+                if dump:
+                    g.debug_dump(f"{dump}_{len(self._graphs)}.dot")
             torch.cuda.current_stream().wait_stream(s)
             self.ctx.set_stream(torch.cuda.current_stream())
             self._graphs[key] = g
