@@ -217,8 +217,18 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
   __shared__ uint32_t s_nlead;
   trace_begin(kTrCount);
   const uint64_t n = a.counts[0];
-  // this slot now holds a record whose short batch-table entries await a backward (counts[5])
-  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 1;
+  if (a.counts[5]) {
+    // the slot's previous record was never consumed by a backward (counts[5], cleared by the
+    // reduces): its batch-table entries go back to empty first — read from its occ_ent (an
+    // entry per present occurrence, kNoEnt per absent one) before P1 overwrites them. Every
+    // CTA reads the same flag: it is set again only after the first barrier below.
+    const uint64_t n_old = a.counts[6];
+    for (uint64_t i = blockIdx.x * uint64_t(kDedupBlock) + threadIdx.x; i < n_old; i += uint64_t(gridDim.x) * kDedupBlock) {
+      const uint32_t e = a.occ_ent[i];
+      if (e != kNoEnt) a.bt[e] = make_uint2(kBtEmpty, 0xffffffffu);
+    }
+    grid_barrier_once(coop + 3);
+  }
   const uint64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
   const uint32_t lane = lane_id(), lt = lanemask_lt();
   constexpr uint64_t kBatch = uint64_t(kDedupBlock) * kDedupIPT;
@@ -241,8 +251,11 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
         asm volatile("prefetch.global.L2 [%0];" ::"l"(&a.bt[bt_home(row[k], a.bt_mask)]));
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      if (row[k] == a.row_absent) continue;
       const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      if (row[k] == a.row_absent) {
+        if (i < c1) a.occ_ent[i] = kNoEnt;  // (an unconsumed record's reset skips it)
+        continue;
+      }
       const uint32_t h = smem_hash_slot(s_key, row[k]);
       if (h != kNoEnt) {
         a.occ_rank[i] = atomicAdd(&s_val[h], 1u);
@@ -320,6 +333,12 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
   }
   trace_end(kTrCount);
   grid_barrier_once(coop + 0);
+  // this slot now holds a record whose batch-table entries await a backward (counts[5]; its
+  // size in counts[6] for the reset above, should none come)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const_cast<uint64_t*>(a.counts)[6] = n;
+    const_cast<uint64_t*>(a.counts)[5] = 1;
+  }
   // ---- P2: allocation. Short leaders: the CTA reserves its CSR range with one packed
   // atomic, then hands it out in item order (block scans), so segment s+1 starts where
   // segment s ends. Long leaders: ids from a warp-aggregated counter.
@@ -450,7 +469,10 @@ __global__ void __launch_bounds__(256) k_count_flat(BwdArgs a) {
   pdl_launch_dependents();
   trace_begin(kTrCount);
   const uint64_t n = a.counts[0];
-  if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 1;  // (as k_dedup)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // (as k_dedup; the flat path's reset is table.cu k_reset_counts)
+    const_cast<uint64_t*>(a.counts)[6] = n;
+    const_cast<uint64_t*>(a.counts)[5] = 1;
+  }
   const uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   if (blockIdx.x * uint64_t(blockDim.x) >= n) return;  // whole warps past the end leave together
   // One-hot batches are walked slot-major (a warp holds 32 samples of one slot), so the rows of
@@ -475,6 +497,8 @@ __global__ void __launch_bounds__(256) k_count_flat(BwdArgs a) {
   if (active) {
     a.occ_ent[i] = e;
     a.occ_rank[i] = base + __popc(peers & lanemask_lt());
+  } else if (j < n) {
+    a.occ_ent[i] = kNoEnt;
   }
   trace_end(kTrCount);
 }
@@ -1256,7 +1280,7 @@ __global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256,
   pdl_wait();
   pdl_launch_dependents();
   // the short segments' batch-table entries are reset by this kernel: the slot no longer holds
-  // an unconsumed record (counts[5], set by k_dedup, read by table.cu k_reset_counts)
+  // an unconsumed record (counts[5], set by k_dedup / k_count_flat, read by their resets)
   if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 0;
   const uint64_t wpb = blockDim.x >> 5;
   const uint64_t warp = uint64_t(blockIdx.x) * wpb + (threadIdx.x >> 5);
@@ -1626,7 +1650,6 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
     HPSG_CUDA(cudaEventRecord(t->ev_join2, t->side));
     HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join2, 0));
     t->have_train = false;
-    t->counts_dirty = false;
     t->have_unique = true;
     return HPS_GPU_OK;
   }
@@ -1639,8 +1662,7 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
   HPSG_CHECK_LAUNCH("backward");
   HPSG_CUDA(cudaEventRecord(t->ev_join2, t->side));
   HPSG_CUDA(cudaStreamWaitEvent(st, t->ev_join2, 0));
-  t->have_train = false;    // one backward per training lookup (its zeroed workspace is now used)
-  t->counts_dirty = false;  // the backward resets every counter it found
+  t->have_train = false;  // one backward per training lookup (its zeroed workspace is now used)
   t->have_unique = true;
   return HPS_GPU_OK;
 }

@@ -417,17 +417,21 @@ __global__ void __launch_bounds__(256) k_probe(LookupArgs a) {
   trace_end(kTrProbe);
 }
 
-// Batch-table entries left by a training record that no backward consumed: back to empty.
-__global__ void k_reset_counts(const uint32_t* __restrict__ occ_row, const uint32_t* __restrict__ occ_ent,
-                               const uint64_t* d_n, uint32_t row_absent, uint2* bt) {
+// Batch-table entries left by a training record that no backward consumed: back to empty
+// (the flat dedup's reset; k_dedup does the same at its start). Entries come from occ_ent,
+// which the dedup writes for every occurrence (0xffffffff: absent key), so this may run after
+// the next record's probe.
+__global__ void k_reset_counts(const uint32_t* __restrict__ occ_ent, const uint64_t* d_n, uint2* bt) {
   trace_begin(kTrReset);
   if (d_n[5] == 0) {  // no unconsumed record in this slot (device truth; see begin_training_record)
     trace_end(kTrReset);
     return;
   }
-  const uint64_t n = *d_n;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    if (occ_row[i] != row_absent) bt[occ_ent[i]] = make_uint2(kBtEmpty, 0xffffffffu);
+  const uint64_t n = d_n[6];  // the unconsumed record's size
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = occ_ent[i];
+    if (e != 0xffffffffu) bt[e] = make_uint2(kBtEmpty, 0xffffffffu);
+  }
   trace_end(kTrReset);
 }
 
@@ -818,12 +822,12 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk, cudaStrea
     HPSG_CUDA(wait_recorded(st, t->ev_done, t->pre_capture));
     t->dedup_pending = false;
   }
-  // Host flags are exact for eager use; once a record was captured into a graph, replays
-  // can leave a slot's device state differing from them, so the (device-checked) reset is
-  // then always enqueued.
-  if (t->counts_dirty || t->graphs_seen) {
-    k_reset_counts<<<grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0, st>>>(
-        t->ws_rows_a, t->ws_occ_ent, t->ws_counts, t->row_absent, t->ws_bt);
+  // An unconsumed previous record's batch-table entries: the persistent k_dedup resets them
+  // itself (device-checked at its start); the flat dedup gets the reset kernel, always (it is
+  // device-checked: a captured graph may be replayed after eager calls left a record behind).
+  if (t->flat_dedup) {
+    k_reset_counts<<<grid_for(t->last_n_keys_host, 256, kNumSMs * 8), 256, 0, st>>>(t->ws_occ_ent, t->ws_counts,
+                                                                                   t->ws_bt);
     HPSG_CHECK_LAUNCH("k_reset_counts");
   }
   a.zero = t->ws_zero;  // cleared by k_probe, which record() launches next
@@ -834,7 +838,6 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk, cudaStrea
   a.d_n = t->ws_counts;
   a.max_keys = t->max_keys;
   a.status = t->ctx->d_status;
-  t->counts_dirty = true;
   t->have_unique = false;
   t->prefetched = false;
   t->pre_keys_host = false;
@@ -853,7 +856,6 @@ int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t
   t->last_n_keys_host = nk;
   t->pre_n_bags = a.n_bags;
   t->pre_capture = capture_id(st);
-  if (t->pre_capture) t->graphs_seen = true;
   // the fork point: right after the record (the pooling launched next does not gate the dedup)
   if (!t->no_fork && st != t->side) HPSG_CUDA(cudaEventRecord(t->ev_fork, st));
   return HPS_GPU_OK;

@@ -98,7 +98,6 @@ struct BatchSlot {
   uint64_t* ws_ins_scan = nullptr;
   // last training lookup recorded in this slot
   bool have_train = false, last_multi = false;
-  bool counts_dirty = false;  // batch-table counters hold a training record no backward has consumed
   bool have_unique = false;   // the segment lists describe the last backward (last_unique)
   // The backward's dedup runs on a side stream, forked after the training probe and joined
   // by backward_update (table.cu record_and_fork).
@@ -149,8 +148,7 @@ struct hps_gpu_table_s : BatchSlot {
   std::vector<BatchSlot> parked;  // size = pipeline depth (entry `cur` is stale while current)
   uint32_t cur = 0;
 
-  bool graphs_seen = false;
-  bool flat_dedup = false;   // the three-kernel dedup (choose_dedup at create)  // a training record was captured into a graph (host slot flags may lag replays)
+  bool flat_dedup = false;  // the three-kernel dedup (choose_dedup at create)
   bool no_fork = false;         // HPS_GPU_NO_FORK=1: everything on the main stream (A/B measurement)
   bool no_tma = false;  // HPS_GPU_NO_TMA=1: use the register-staged gather (A/B measurement)
 };

@@ -9,8 +9,8 @@ for cfg in $CFGS; do
     for v in "$@"; do
       name=${v%%:*}; envs=${v#*:}
       out=gpurun_out/ab_${cfg}_${name}_${rep}.json
-      env ${envs//,/ } timeout 300 python bench.py --config $cfg --no-cpu-baseline --e2e-steps 2 --full-batch 0 > $out 2>/dev/null
-      echo "$cfg $name rep$rep $(python -c "import json; d=json.loads(open('$out').read().strip().splitlines()[-1]); print(round(d['ms_per_step']*1000,1), 'us')" 2>&1 | tail -1)"
+      env ${envs//,/ } timeout 300 python bench.py --config $cfg --steps ${AB_STEPS:-20} --no-cpu-baseline --e2e-steps ${AB_E2E:-2} --full-batch 0 > $out 2>/dev/null
+      echo "$cfg $name rep$rep $(python -c "import json; d=json.loads(open('$out').read().strip().splitlines()[-1]); print(round(d['ms_per_step']*1000,1), 'us', 'e2e', round(d['e2e']['value']/1e6,1))" 2>&1 | tail -1)"
     done
   done
 done

@@ -381,6 +381,77 @@ def test_batch_table_self_cleaning(ctx, multi):
         assert close(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0])
 
 
+@pytest.mark.parametrize("dedup", ["persistent", "flat"])
+def test_unconsumed_record_between_graph_replays(ctx, dedup, monkeypatch):
+    """A captured [training lookup + backward] graph replayed after an EAGER training lookup
+    whose backward never came: the graph's dedup must first return that record's batch-table
+    entries to empty (k_dedup checks counts[5] itself; the flat dedup's reset kernel is in the
+    graph). Both dedup variants, against the oracle."""
+    monkeypatch.setenv("HPS_GPU_DEDUP", dedup)
+    rs = np.random.default_rng(17)
+    caps = [3, 800]
+    g, o = make_pair(ctx, caps, 32, [0, 1, 1])
+    pools = []
+    for t, c in enumerate(caps):
+        ks = rs.integers(0, 2**63, c).astype(np.uint64)
+        g.insert(t, t64(ks))
+        o.insert(t, ks)
+        pools.append(ks)
+    B = 500
+    kbuf = torch.zeros(B * 3, dtype=torch.int64, device="cuda")
+    dbuf = torch.zeros(B * 3, 32, dtype=torch.float32, device="cuda")
+    obuf = torch.zeros(B * 3, 32, dtype=torch.float32, device="cuda")
+    p = opt_params("sgd", 0.05)
+
+    def batch():
+        return np.stack([rs.choice(pools[t], B) for t in [0, 1, 1]], 1).ravel()
+
+    def step():
+        g.lookup(kbuf, B, train=True, out=obuf)
+        g.backward_update(dbuf, 0.05, params=p)
+
+    stream = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    stream.wait_stream(main)
+    gr = None
+    with torch.cuda.stream(stream):
+        ctx.set_stream(stream)
+        try:
+            for it in range(6):
+                keys = batch()
+                d = rs.standard_normal((B * 3, 32)).astype(np.float32)
+                kbuf.copy_(t64(keys))
+                dbuf.copy_(torch.from_numpy(d))
+                ref = o.lookup(keys, B, train=True)
+                o.backward_update(d, p)
+                if gr is None:
+                    step()  # warm-up, then capture
+                    gr = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gr, stream=stream):
+                        step()
+                else:
+                    gr.replay()
+                stream.synchronize()
+                if it > 0:
+                    assert close(obuf.cpu().numpy(), ref), f"replay {it}"
+                # an eager training lookup (different keys) whose backward never comes
+                junk = batch()
+                g.lookup(t64(junk), B, train=True)
+                o.lookup(junk, B, train=True)
+            gr.replay()  # (the oracle's pending record is the junk one: replay without a check)
+            stream.synchronize()
+        finally:
+            main.wait_stream(stream)
+            ctx.set_stream(main)
+    ctx.sync()
+    # the last replay used kbuf/dbuf of iteration 5 again: apply it to the oracle too
+    o.lookup(keys, B, train=True)
+    o.backward_update(d, p)
+    assert _bt_used(ctx, g) == 0
+    for t, c in enumerate(caps):
+        assert close(g.export(t, 0, c)[0].cpu().numpy(), o.export(t, 0, c)[0]), f"table {t}"
+
+
 @pytest.mark.parametrize("multi", [False, True])
 def test_f16_inference_table_matches_oracle(ctx, multi):
     """binary16 table rows: bulk load (init values and given rows,
