@@ -990,7 +990,9 @@ __device__ __forceinline__ void short_tma(const BwdArgs& a, uint64_t warp, uint6
 // segment j contributes [weight row, state rows, gradient rows in canonical order]. The
 // stream is cut into sub-lists of <= kPipeList entries (whole segments), each built in a
 // small shared-memory list (the gradient rows' bags are read from the segment CSR and
-// sorted into canonical order on the way in). The warp then walks its sub-list U rows at a
+// sorted into canonical order on the way in; every entry carries its row's address, computed
+// once by the lane that builds it — per-issue address arithmetic by the whole warp was 15% of
+// the kernel's instructions). The warp then walks its sub-list U rows at a
 // time: U 128-bit row loads in flight (lane l owns float4s l, l+32, ...: fully coalesced),
 // then the ordered sums, the fused optimizer at each segment's last row, 128-bit stores.
 // Latency is hidden by occupancy (small register and shared-memory footprint), not by a
@@ -1002,24 +1004,46 @@ static_assert(kPipeList >= 3 + kChunk, "a sub-list holds at least one whole shor
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16_s(uint32_t smem_dst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// A sub-list entry: the row's global address (computed once, by the lane that builds the
+// entry, not per issue by the whole warp), its kind and flags, and an operand: the table row
+// of a weight entry (the update's store target), the bag length of a gradient (mean).
+struct PipeEntry {
+  uint32_t lo, hi;   // source address
+  uint32_t flags;    // kind (0 weight, 1/2 optimizer state, 3 gradient) | 4: segment's last row
+  uint32_t aux;      // weight: row id; gradient: mean divisor (1 for sum)
+};
+__device__ __forceinline__ PipeEntry pipe_entry(const float* base, uint32_t row, uint32_t dim, uint32_t flags,
+                                                uint32_t aux) {
+  const uint64_t p = reinterpret_cast<uint64_t>(base + uint64_t(row) * dim);
+  return PipeEntry{static_cast<uint32_t>(p), static_cast<uint32_t>(p >> 32), flags, aux};
+}
+
 // U rows per chunk, two chunk buffers per warp: chunk c+1's rows land (per-lane cp.async,
 // 16 B each, 128-bit coalesced) while chunk c is summed from shared memory.
 template <int OPT, int VPL, int U>
-__device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint64_t n_warps, uint2* list,
+__device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint64_t n_warps, PipeEntry* list,
                                            float4* buf) {
   constexpr uint32_t NS = state_rows<OPT>();
   constexpr uint32_t HDR = 1u + NS;  // weight (gradient-only: the row id, nothing loaded) + state rows
   const uint32_t lane = lane_id();
   const uint32_t D = a.dim, nvec = D / 4;
   const bool mean = a.bag_len != nullptr;
+  const uint32_t sbuf = smem_u32(buf) + lane * 16u;  // this lane's float4 of chunk buffer 0, row 0
   const uint64_t S = *a.short_alloc >> 32;
-  for (uint64_t u0 = warp * 32; u0 < S; u0 += n_warps * 32) {
+  // segments per warp pass: the whole list spread over every warp of the grid (a fixed 32
+  // left a third of the warps idle on config 2 and the rest with 32-segment chains)
+  const uint64_t spread = (S + n_warps - 1) / n_warps;
+  const uint32_t per = spread < 1 ? 1u : spread > 32 ? 32u : static_cast<uint32_t>(spread);
+  for (uint64_t u0 = warp * per; u0 < S; u0 += n_warps * per) {
     uint4 rec = make_uint4(0, 0, 0, 0);
-    if (u0 + lane < S) rec = a.short_rec[u0 + lane];
+    if (lane < per && u0 + lane < S) rec = a.short_rec[u0 + lane];
     const uint32_t row = rec.x, first = rec.y, len = rec.z, slot = rec.w;
     if (len) a.bt[slot] = make_uint2(kBtEmpty, 0xffffffffu);  // placement (previous kernels) is done with it
     uint32_t bag0 = len ? a.short_bag[first] : 0u;
@@ -1035,8 +1059,10 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
       // build the sub-list: header rows + single gradients by their own lane ...
       if (in && len) {
         const uint32_t o = excl - base;
-        for (uint32_t q = 0; q < HDR; ++q) list[o + q] = make_uint2(row, q);
-        if (len == 1) list[o + HDR] = make_uint2(bag0, 3u | 4u | ((mean ? a.bag_len[bag0] : 1u) << 3));
+        list[o] = pipe_entry(a.W, row, D, 0u, row);
+        if constexpr (NS >= 1) list[o + 1] = pipe_entry(a.S0, row, D, 1u, row);
+        if constexpr (NS >= 2) list[o + 2] = pipe_entry(a.S1, row, D, 2u, row);
+        if (len == 1) list[o + HDR] = pipe_entry(a.dout, bag0, D, 3u | 4u, mean ? a.bag_len[bag0] : 1u);
       }
       // ... longer segments' bags sorted into canonical order by the whole warp
       uint32_t multi = __ballot_sync(0xffffffffu, in && len >= 2);
@@ -1053,23 +1079,19 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
           rank += (x < b || (x == b && q < lane)) ? 1u : 0u;
         }
         if (lane < jl)
-          list[jo + rank] = make_uint2(b, 3u | (rank + 1 == jl ? 4u : 0u) | ((mean ? a.bag_len[b] : 1u) << 3));
+          list[jo + rank] = pipe_entry(a.dout, b, D, 3u | (rank + 1 == jl ? 4u : 0u), mean ? a.bag_len[b] : 1u);
       }
       __syncwarp();
       auto issue_chunk = [&](uint32_t ch) {
-        float4* dst = buf + (ch & 1u) * U * nvec;
+        const uint32_t dst = sbuf + (ch & 1u) * (U * nvec * 16u);
         const uint32_t t0 = ch * U, n = min(uint32_t(U), T - t0);
         for (uint32_t k = 0; k < n; ++k) {
-          const uint2 e = list[t0 + k];
-          const uint32_t kind = e.y & 3u;
-          if (OPT == kOptGrad && kind == 0) continue;  // gradient-only: the row is written, never read
-          const float4* src = reinterpret_cast<const float4*>(
-              (kind == 0 ? a.W : kind == 1 ? a.S0 : kind == 2 ? a.S1 : a.dout) + uint64_t(e.x) * D);
+          const PipeEntry e = list[t0 + k];
+          if (OPT == kOptGrad && (e.flags & 3u) == 0) continue;  // gradient-only: the row is written, never read
+          const char* src = reinterpret_cast<const char*>((uint64_t(e.hi) << 32) | e.lo) + lane * 16u;
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) {
-            const uint32_t vv = lane + 32u * v;
-            if (vv < nvec) cp_async16(dst + k * nvec + vv, src + vv);
-          }
+          for (int v = 0; v < VPL; ++v)
+            if (lane + 32u * v < nvec) cp_async16_s(dst + k * nvec * 16u + v * 512u, src + v * 512);
         }
         cp_async_commit();
       };
@@ -1090,13 +1112,13 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
         const float4* xb = buf + (ch & 1u) * U * nvec;
         const uint32_t t0 = ch * U, n = min(uint32_t(U), T - t0);
         for (uint32_t k = 0; k < n; ++k) {
-          const uint2 e = list[t0 + k];
-          const uint32_t kind = e.y & 3u;
+          const uint32_t flags = list[t0 + k].flags, aux = list[t0 + k].aux;
+          const uint32_t kind = flags & 3u;
           float4 x[VPL];
 #pragma unroll
           for (int v = 0; v < VPL; ++v) x[v] = xb[k * nvec + min(lane + 32u * v, nvec - 1)];
           if (kind == 0) {
-            cur_row = e.x;
+            cur_row = aux;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) rs.w[v] = x[v];
           } else if (kind == 1) {
@@ -1106,14 +1128,14 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
 #pragma unroll
             for (int v = 0; v < VPL; ++v) rs.q[state_rows<OPT>() >= 2 ? v : 0] = x[v];
           } else {
-            const float f = static_cast<float>(e.y >> 3);
+            const float f = static_cast<float>(aux);
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
               const float4 gx = mean ? f4_div(x[v], f) : x[v];
               g[v] = g0 ? gx : f4_add(g[v], gx);
             }
             g0 = false;
-            if (e.y & 4u) {
+            if (flags & 4u) {
               update_store<OPT, VPL>(a, cur_row, lane, 32, rs, g);
               g0 = true;
             }
@@ -1297,9 +1319,9 @@ __global__ void __launch_bounds__(TMA ? kRedWarps * 32 : 256,
 // Short segments reduced + updated through the register-pipelined row stream (dim 128..256).
 constexpr int kPipeBlock = 256;
 template <int OPT, int VPL, int U>
-__global__ void __launch_bounds__(kPipeBlock, 3) k_reduce_pipe(BwdArgs a) {
+__global__ void __launch_bounds__(kPipeBlock, VPL >= 2 ? 2 : (OPT == HPS_OPT_SGD ? 4 : 3)) k_reduce_pipe(BwdArgs a) {
   extern __shared__ __align__(16) float4 s_rows[];  // per warp: 2 chunk buffers of U rows
-  __shared__ uint2 s_list[kPipeBlock / 32][kPipeList];
+  __shared__ PipeEntry s_list[kPipeBlock / 32][kPipeList];
   pdl_wait();
   pdl_launch_dependents();
   if (blockIdx.x == 0 && threadIdx.x == 0) const_cast<uint64_t*>(a.counts)[5] = 0;  // (as k_reduce_short)
