@@ -257,7 +257,7 @@ def reference_arm(args, cfg, rank, world):
 TRACE_NAMES = {0: "probe", 1: "pool", 2: "seg_alloc", 3: "place", 4: "long_hist", 5: "long_pass0",
                6: "long_pass1", 7: "long_pass2", 8: "long_pass3", 9: "long_reg", 10: "reduce_short",
                11: "reduce_long", 12: "reset_counts", 13: "count", 14: "|count_local", 15: "|count_global",
-               16: "|count_cas", 17: "|count_probe", 18: "mid", 19: "<step-in", 20: ">step-out"}
+               16: "|count_cas", 17: "|count_probe", 18: "scale_dout", 19: "<step-in", 20: ">step-out"}
 
 
 def print_trace(ctx, n, step):

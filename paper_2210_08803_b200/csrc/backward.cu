@@ -66,7 +66,8 @@ struct BwdArgs {
   int long_passes;
   uint32_t* lkey;           // long list: segment id (sort input)
   uint32_t* lval;           // long list: bag (sort input)
-  const uint32_t* lbag;     // long list sorted by segment id: bags in canonical order
+  const uint32_t* lval_b;   // the sort's second value buffer: the sorted bags are in lval or here
+                            // (radix_passes_run: the passes above the segment count's digits are skipped)
   unsigned long long* long_occ;     // long-list length
   unsigned long long* long_chunks;  // level-1 chunks over all long segments
   const uint32_t* bag_len;  // mean combiner: bag lengths (nullptr: sum)
@@ -1234,6 +1235,7 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
   const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = a.dim / 4;
   const bool mean = a.bag_len != nullptr;
   const uint64_t T = *a.long_chunks;
+  const uint32_t* lbag = (radix_passes_run(*a.n_long, a.long_passes) & 1) ? a.lval_b : a.lval;
   for (uint64_t t = warp; t < T; t += n_warps) {
     const uint32_t j = a.task_long[t];
     const uint32_t c = static_cast<uint32_t>(t) - a.long_base[j];
@@ -1241,7 +1243,7 @@ __device__ __forceinline__ void long_phase(const BwdArgs& a, uint64_t warp, uint
     const uint32_t s0 = a.long_start[j], e = s0 + a.long_len[j];
     const uint32_t s = s0 + c * kChunk;
     const uint32_t n = min(static_cast<uint32_t>(kChunk), e - s);
-    const uint32_t my_bag = lane < n ? a.lbag[s + lane] : 0u;
+    const uint32_t my_bag = lane < n ? lbag[s + lane] : 0u;
     const float my_f = (mean && lane < n) ? static_cast<float>(a.bag_len[my_bag]) : 1.f;
     float4 acc[VPL];
     for (uint32_t q0 = 0; q0 < n; q0 += G * RB) {  // n is warp-uniform
@@ -1464,7 +1466,7 @@ BwdArgs base_args(hps_gpu_table t) {
   a.long_passes = bwd_long_passes(t->last_n_keys_host);
   a.lkey = t->ws_lkey_a;
   a.lval = t->ws_lval_a;
-  a.lbag = (bwd_long_passes(t->last_n_keys_host) & 1) ? t->ws_lval_b : t->ws_lval_a;
+  a.lval_b = t->ws_lval_b;
   a.bag_len = (t->last_multi && t->last_combiner == HPS_COMBINER_MEAN) ? t->ws_bag_len : nullptr;
   a.dim = t->dim;
   a.n_slots = t->n_slots;
@@ -1584,7 +1586,7 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
       uint32_t* vout = in_b ? t->ws_lval_a : t->ws_lval_b;
       HPSG_CUDA(launch_k(pdl, k_radix_pass, static_cast<unsigned>(stiles), kSortBlock, 0, st, kin, vin, kout, vout, d_n,
                          8 * p, static_cast<const uint32_t*>(hist + 256 * p), status + size_t(p) * stiles * 256,
-                         stick + p));
+                         stick + p, static_cast<const uint32_t*>(a.n_long)));  // keys: segment ids < n_long
       kin = kout;
       vin = vout;
       in_b = !in_b;
@@ -1595,6 +1597,40 @@ int hpsg::launch_dedup(hps_gpu_table t, cudaStream_t st) {
 }
 
 namespace {
+// Mean combiner: each bag's gradient row divided by the bag's length ONCE (IEEE division,
+// the oracle's g / len), instead of once per occurrence inside the reduces — on multi-hot
+// batches every bag is read by ~hots segments, and the correctly rounded divide (reciprocal,
+// refinement, range check) was a third of the long reduce's instructions on config 3.
+__global__ void __launch_bounds__(256) k_scale_dout(const float4* __restrict__ dout, const uint32_t* __restrict__ bag_len,
+                                                    uint64_t n_bags, uint32_t nvec, float4* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  trace_begin(kTrScale);
+  // a streaming pass: four float4 loads (and their bags' lengths) in flight per thread
+  constexpr int K = 4;
+  const uint32_t sh = (nvec & (nvec - 1)) == 0 ? static_cast<uint32_t>(__ffs(nvec) - 1) : 32u;
+  const uint64_t n = n_bags * nvec;
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < n; b += K * stride) {
+    float4 x[K];
+    uint32_t len[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t i = b + k * stride;
+      if (i < n) {
+        x[k] = __ldg(dout + i);
+        len[k] = __ldg(bag_len + (sh < 32 ? (i >> sh) : i / nvec));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint64_t i = b + k * stride;
+      if (i < n) out[i] = f4_div(x[k], static_cast<float>(len[k]));
+    }
+  }
+  trace_end(kTrScale);
+}
+
 // grads_out != nullptr: gradient-only mode (kOptGrad) — per-row sums into grads_out
 // [total_rows x dim] (rows not in the batch untouched) and touched_out[row] = 1.
 int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt, float* grads_out,
@@ -1612,14 +1648,26 @@ int backward_impl(hps_gpu_table t, const float* d_out, const hps_opt_params* opt
     if (int s = launch_dedup(t, st)) return s;
     t->dedup_deferred = false;
   }
+  BwdArgs a = base_args(t);
+  a.dout = d_out;
+  if (a.bag_len) {  // mean: the scaled gradient rows, once per bag (the workspace is allocated on
+                    // the first such backward outside stream capture; inside one, the reduces divide)
+    if (!t->ws_dscale && capture_id(st) == 0) HPSG_CUDA(cudaMalloc(&t->ws_dscale, t->max_bags * t->dim * sizeof(float)));
+    if (t->ws_dscale) {
+      const uint32_t nv = t->dim / 4;
+      HPSG_CUDA(launch_k(t->ctx->pdl, k_scale_dout, grid_for(uint64_t(t->pre_n_bags) * nv / 4, 256, kNumSMs * 8), 256, 0,
+                         st, reinterpret_cast<const float4*>(d_out), static_cast<const uint32_t*>(a.bag_len),
+                         uint64_t(t->pre_n_bags), nv, reinterpret_cast<float4*>(t->ws_dscale)));
+      a.dout = t->ws_dscale;
+      a.bag_len = nullptr;  // (the reduces now sum rows as given)
+    }
+  }
   HPSG_CUDA(cudaEventRecord(t->ev_bwd, st));
   HPSG_CUDA(cudaStreamWaitEvent(t->side, t->ev_bwd, 0));
   if (t->dedup_pending) {
     HPSG_CUDA(wait_recorded(st, t->ev_join, t->pre_capture));
     t->dedup_pending = false;
   }
-  BwdArgs a = base_args(t);
-  a.dout = d_out;
   const bool grad_only = grads_out != nullptr;
   a.W = grad_only ? grads_out : t->d_w;
   a.S0 = grad_only ? nullptr : t->d_s0;

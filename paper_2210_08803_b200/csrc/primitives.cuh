@@ -225,13 +225,25 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const uint32_t* __res
   trace_end(kTrHist);
 }
 
+__host__ __device__ __forceinline__ bool radix_pass_needed(uint32_t key_bound, int shift) {
+  return shift == 0 || (key_bound > 0 && ((key_bound - 1) >> shift) != 0);
+}
+// Passes of an LSD sort over `passes` digits that run when every key is below key_bound
+// (the rest are skipped by k_radix_pass): the result is in the second buffer iff this is odd.
+__host__ __device__ __forceinline__ int radix_passes_run(uint32_t key_bound, int passes) {
+  int e = 1;
+  while (e < passes && radix_pass_needed(key_bound, 8 * e)) ++e;
+  return e;
+}
+
 // One digit pass. vals_in == nullptr: the value of item i is i (identity payload).
 static __global__ void __launch_bounds__(kSortBlock) k_radix_pass(const uint32_t* __restrict__ keys_in,
                                                            const uint32_t* __restrict__ vals_in,
                                                            uint32_t* __restrict__ keys_out,
                                                            uint32_t* __restrict__ vals_out, const uint64_t* d_n,
                                                            int shift, const uint32_t* __restrict__ hist,
-                                                           uint32_t* status, uint32_t* ticket) {
+                                                           uint32_t* status, uint32_t* ticket,
+                                                           const uint32_t* key_bound) {
   __shared__ uint32_t s_keys[kSortTile];
   __shared__ uint32_t s_vals[kSortTile];
   __shared__ uint32_t s_whist[kSortWarps][256];
@@ -242,6 +254,10 @@ static __global__ void __launch_bounds__(kSortBlock) k_radix_pass(const uint32_t
 
   pdl_wait();
   pdl_launch_dependents();
+  // key_bound (optional): every key is below *key_bound, known only on the device. A pass
+  // whose digit (and every higher one) is then zero for all keys would be an identity
+  // permutation: skipped (radix_passes_run() names the buffer that holds the result).
+  if (key_bound && shift > 0 && !radix_pass_needed(*key_bound, shift)) return;
   trace_begin(kTrPass0 + shift / 8);
   const uint64_t n = *d_n;
   const uint64_t n_tiles = (n + kSortTile - 1) / kSortTile;
@@ -372,7 +388,8 @@ inline bool radix_sort_pairs(cudaStream_t st, uint32_t* keys_a, const uint32_t* 
     uint32_t* kout = in_b ? keys_a : keys_b;
     uint32_t* vout = in_b ? vals_a : vals_b;
     k_radix_pass<<<static_cast<unsigned>(tiles), kSortBlock, 0, st>>>(
-        kin, vin, kout, vout, d_n, 8 * p, hist + 256 * p, status + static_cast<size_t>(p) * tiles * 256, tickets + p);
+        kin, vin, kout, vout, d_n, 8 * p, hist + 256 * p, status + static_cast<size_t>(p) * tiles * 256, tickets + p,
+        nullptr);
     kin = kout;
     vin = vout;
     in_b = !in_b;

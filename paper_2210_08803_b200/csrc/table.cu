@@ -1269,7 +1269,8 @@ int hps_gpu_table_destroy(hps_gpu_table t) {
     if (t->ctx && t->ctx->ev_last_dedup == b.ev_done) t->ctx->ev_last_dedup = nullptr;  // (about to be destroyed)
   }
   void* ptrs[] = {t->d_wh,        t->d_tables,    t->d_slots,      t->d_w,          t->d_s0,          t->d_s1,
-                  t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_io};
+                  t->d_row_keys,  t->d_nrows,      t->d_defaults,   t->d_slot_table,  t->ws_io,
+                  t->ws_dscale};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (BatchSlot& b : t->parked) free_batch_slot(b);

@@ -122,6 +122,7 @@ struct hps_gpu_table_s : BatchSlot {
   uint32_t n_tables = 0, dim = 0, n_slots = 0;
   uint32_t dim_io = 0;      // the caller's dim; `dim` = padded_dim(dim_io) is the storage stride
   float* ws_io = nullptr;   // dim_io != dim: [max_bags x dim] staging of pooled outputs / gradients
+  float* ws_dscale = nullptr;  // mean combiner: [max_bags x dim] gradient rows / bag length (backward_impl)
   int optimizer = 0, n_state = 0;
   uint64_t seed = 0;
   float a0 = 0.f;
