@@ -133,20 +133,29 @@ __device__ __forceinline__ uint32_t higher_nodes(uint32_t m);
 // atomic per warp — ids in allocator order, so the starts are the prefix of the lengths in id
 // order, exactly where the stable sort by id will put each segment — its first level-1 chunk
 // from a second counter (the chunk total is that counter) and its tree-node block.
-__device__ __forceinline__ void register_long(const BwdArgs& a, bool lg, uint32_t row, uint32_t ent, uint32_t len) {
+// `hist`: where the sort's digit histograms are counted — the global ones, or a CTA's shared
+// copy (k_dedup: flushed once per CTA, so the high digits' few bins, which every segment id
+// shares, do not serialise thousands of global atomics).
+__device__ __forceinline__ void register_long(const BwdArgs& a, bool lg, uint32_t row, uint32_t ent, uint32_t len,
+                                              uint32_t* hist) {
   if (!__ballot_sync(0xffffffffu, lg)) return;
   const uint32_t lane = lane_id();
   const uint32_t m = lg ? (len + kChunk - 1) / kChunk : 0u;
+  const uint32_t h = lg ? higher_nodes(m) : 0u;
   const unsigned long long mine = lg ? ((1ull << 32) | len) : 0ull;
   const unsigned long long incl = warp_incl_scan(mine);
   const unsigned long long cincl = warp_incl_scan(static_cast<unsigned long long>(m));
+  const uint32_t hincl = warp_incl_scan(h);
   unsigned long long base = 0, cbase = 0;
+  uint32_t hbase = 0;
   if (lane == 31) {
     base = atomicAdd(a.long_alloc, incl);
     cbase = atomicAdd(a.long_chunks, cincl);
+    hbase = atomicAdd(a.higher_total, hincl);
   }
   base = __shfl_sync(0xffffffffu, base, 31);
   cbase = __shfl_sync(0xffffffffu, cbase, 31);
+  hbase = __shfl_sync(0xffffffffu, hbase, 31);
   uint32_t j = 0, cb = 0;
   if (lg) {
     const unsigned long long pos = base + incl - mine;
@@ -157,10 +166,10 @@ __device__ __forceinline__ void register_long(const BwdArgs& a, bool lg, uint32_
     a.long_len[j] = len;
     a.long_start[j] = static_cast<uint32_t>(pos);
     a.long_base[j] = cb;
-    a.long_hbase[j] = atomicAdd(a.higher_total, higher_nodes(m));
+    a.long_hbase[j] = hbase + hincl - h;
     a.bt[ent].y = kLongFlag | j;
     // the long-list sort's digit histograms: segment j's len occurrences all carry key j
-    for (int p = 0; p < a.long_passes; ++p) atomicAdd(&a.long_hist[256 * p + ((j >> (8 * p)) & 255u)], len);
+    for (int p = 0; p < a.long_passes; ++p) atomicAdd(&hist[256 * p + ((j >> (8 * p)) & 255u)], len);
   }
   // the chunk -> segment map of the long reduce, written by the whole warp per segment
   uint32_t todo = __ballot_sync(0xffffffffu, lg);
@@ -216,6 +225,7 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
   __shared__ unsigned long long s_cursor;
   __shared__ uint32_t s_scr32[33];
   __shared__ uint32_t s_nlead;
+  __shared__ uint32_t s_lhist[4 * 256];  // this CTA's long-sort digit histograms (register_long)
   trace_begin(kTrCount);
   const uint64_t n = a.counts[0];
   if (a.counts[5]) {
@@ -344,33 +354,24 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
   // atomic, then hands it out in item order (block scans), so segment s+1 starts where
   // segment s ends. Long leaders: ids from a warp-aggregated counter.
   trace_begin(kTrAlloc);
+  for (int e = threadIdx.x; e < a.long_passes * 256; e += kDedupBlock) s_lhist[e] = 0u;
   __syncthreads();
   const uint32_t nlead = s_nlead;  // (the CTA's own list: written before the grid barrier)
   const uint32_t* lead = a.lead + c0;
-  unsigned long long mine = 0;
-  for (uint32_t b0 = 0; b0 < nlead; b0 += kBatch) {
-    uint32_t len[kDedupIPT];
+  if (nlead <= kBatch) {
+    // one batch (every one-hot config): each thread's leaders contiguous, loaded once; the
+    // block scan gives both the CTA's total (one atomic) and each thread's offset in it
+    uint32_t ent[kDedupIPT], len[kDedupIPT], occ[kDedupIPT], row[kDedupIPT];
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      const uint32_t q = b0 + k * kDedupBlock + threadIdx.x;
-      len[k] = q < nlead ? __ldcg(&a.bt[a.occ_ent[lead[q]]].y) + 1u : 0u;
+      const uint32_t q = threadIdx.x * kDedupIPT + k;
+      occ[k] = q < nlead ? lead[q] : 0u;
     }
 #pragma unroll
-    for (int k = 0; k < kDedupIPT; ++k)
-      if (len[k] && len[k] <= kChunk) mine += (1ull << 32) | len[k];
-  }
-  unsigned long long total;
-  (void)block_excl_scan<kDedupBlock>(mine, s_scr, &total);
-  if (threadIdx.x == 0) s_cursor = total ? atomicAdd(a.short_alloc, total) : 0ull;
-  __syncthreads();
-  unsigned long long run = s_cursor;
-  for (uint32_t b0 = 0; b0 < nlead; b0 += kBatch) {  // each thread's leaders contiguous; block scan
-    uint32_t ent[kDedupIPT], len[kDedupIPT], occ[kDedupIPT];
-#pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      const uint32_t q = b0 + threadIdx.x * kDedupIPT + k;
-      occ[k] = q < nlead ? lead[q] : 0u;
+      const uint32_t q = threadIdx.x * kDedupIPT + k;
       ent[k] = q < nlead ? a.occ_ent[occ[k]] : kNoEnt;
+      row[k] = q < nlead ? a.occ_row[occ[k]] : 0u;
     }
     unsigned long long tmine = 0;
 #pragma unroll
@@ -379,38 +380,96 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
       if (len[k] && len[k] <= kChunk) tmine += (1ull << 32) | len[k];
     }
     unsigned long long ttotal;
-    unsigned long long pos = run + block_excl_scan<kDedupBlock>(tmine, s_scr, &ttotal);
-    run += ttotal;
+    const unsigned long long excl = block_excl_scan<kDedupBlock>(tmine, s_scr, &ttotal);
+    if (threadIdx.x == 0) s_cursor = ttotal ? atomicAdd(a.short_alloc, ttotal) : 0ull;
+    __syncthreads();
+    unsigned long long pos = s_cursor + excl;
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
       const bool sh = len[k] && len[k] <= kChunk, lg = len[k] > kChunk;
       if (sh) {
         const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
-        a.short_rec[seg] = make_uint4(a.occ_row[occ[k]], first, len[k], ent[k]);
+        a.short_rec[seg] = make_uint4(row[k], first, len[k], ent[k]);
         a.bt[ent[k]].y = first;
         pos += (1ull << 32) | len[k];
       }
-      register_long(a, lg, lg ? a.occ_row[occ[k]] : 0u, ent[k], len[k]);
+      register_long(a, lg, row[k], ent[k], len[k], s_lhist);
+    }
+  } else {
+    unsigned long long mine = 0;
+    for (uint32_t b0 = 0; b0 < nlead; b0 += kBatch) {
+      uint32_t len[kDedupIPT];
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k) {
+        const uint32_t q = b0 + k * kDedupBlock + threadIdx.x;
+        len[k] = q < nlead ? __ldcg(&a.bt[a.occ_ent[lead[q]]].y) + 1u : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k)
+        if (len[k] && len[k] <= kChunk) mine += (1ull << 32) | len[k];
+    }
+    unsigned long long total;
+    (void)block_excl_scan<kDedupBlock>(mine, s_scr, &total);
+    if (threadIdx.x == 0) s_cursor = total ? atomicAdd(a.short_alloc, total) : 0ull;
+    __syncthreads();
+    unsigned long long run = s_cursor;
+    for (uint32_t b0 = 0; b0 < nlead; b0 += kBatch) {  // each thread's leaders contiguous; block scan
+      uint32_t ent[kDedupIPT], len[kDedupIPT], occ[kDedupIPT];
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k) {
+        const uint32_t q = b0 + threadIdx.x * kDedupIPT + k;
+        occ[k] = q < nlead ? lead[q] : 0u;
+        ent[k] = q < nlead ? a.occ_ent[occ[k]] : kNoEnt;
+      }
+      unsigned long long tmine = 0;
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k) {
+        len[k] = ent[k] != kNoEnt ? __ldcg(&a.bt[ent[k]].y) + 1u : 0u;
+        if (len[k] && len[k] <= kChunk) tmine += (1ull << 32) | len[k];
+      }
+      unsigned long long ttotal;
+      unsigned long long pos = run + block_excl_scan<kDedupBlock>(tmine, s_scr, &ttotal);
+      run += ttotal;
+#pragma unroll
+      for (int k = 0; k < kDedupIPT; ++k) {
+        const bool sh = len[k] && len[k] <= kChunk, lg = len[k] > kChunk;
+        if (sh) {
+          const uint32_t seg = static_cast<uint32_t>(pos >> 32), first = static_cast<uint32_t>(pos);
+          a.short_rec[seg] = make_uint4(a.occ_row[occ[k]], first, len[k], ent[k]);
+          a.bt[ent[k]].y = first;
+          pos += (1ull << 32) | len[k];
+        }
+        register_long(a, lg, lg ? a.occ_row[occ[k]] : 0u, ent[k], len[k], s_lhist);
+      }
     }
   }
+  __syncthreads();
+  for (int e = threadIdx.x; e < a.long_passes * 256; e += kDedupBlock)
+    if (const uint32_t v = s_lhist[e]) atomicAdd(&a.long_hist[e], v);
   trace_end(kTrAlloc);
   grid_barrier_once(coop + 1);
   // ---- P3: placement
   trace_begin(kTrPlace);
+  // a chunk that fits one batch (every one-hot config) walks its items thread-contiguously and
+  // keeps their locators: the long compaction after the barrier then needs no second pass
+  // over the record (its canonical order is the thread order, its offsets the scan below)
+  const bool one = c1 - c0 <= kBatch;
   uint32_t my_long = 0;
+  uint32_t keep[kDedupIPT];
   for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
     uint32_t ent[kDedupIPT], loc[kDedupIPT];
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
-      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      const uint64_t i = one ? b0 + uint64_t(threadIdx.x) * kDedupIPT + k : b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
       ent[k] = (i < c1 && a.occ_row[i] != a.row_absent) ? a.occ_ent[i] : kNoEnt;
     }
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) loc[k] = ent[k] != kNoEnt ? __ldcg(&a.bt[ent[k]].y) : 0u;
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
+      keep[k] = loc[k];
       if (ent[k] == kNoEnt) continue;
-      const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+      const uint64_t i = one ? b0 + uint64_t(threadIdx.x) * kDedupIPT + k : b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
       if (loc[k] & kLongFlag) {
         ++my_long;
       } else {
@@ -419,7 +478,7 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
     }
   }
   uint32_t cta_long;
-  (void)block_excl_scan<kDedupBlock>(my_long, s_scr32, &cta_long);
+  const uint32_t my_off = block_excl_scan<kDedupBlock>(my_long, s_scr32, &cta_long);
   if (threadIdx.x == 0) st_vol32(coop + 4 + blockIdx.x, cta_long);
   grid_barrier_once(coop + 2);
   uint32_t before = 0;
@@ -427,7 +486,17 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
   uint32_t lbase;
   (void)block_excl_scan<kDedupBlock>(before, s_scr32, &lbase);
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *a.long_occ = lbase + cta_long;
-  if (cta_long) {  // canonical order: batches in order, each thread's kDedupIPT items contiguous
+  if (cta_long && one) {
+    uint32_t pos = lbase + my_off;
+#pragma unroll
+    for (int k = 0; k < kDedupIPT; ++k) {
+      if (!(keep[k] & kLongFlag)) continue;
+      const uint64_t i = c0 + uint64_t(threadIdx.x) * kDedupIPT + k;
+      a.lkey[pos] = keep[k] & ~kLongFlag;
+      a.lval[pos] = a.occ_bag ? a.occ_bag[i] : static_cast<uint32_t>(i);
+      ++pos;
+    }
+  } else if (cta_long) {  // canonical order: batches in order, each thread's kDedupIPT items contiguous
     for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
       uint32_t loc[kDedupIPT];
       uint32_t cnt = 0;
@@ -539,7 +608,7 @@ __global__ void __launch_bounds__(256) k_alloc_flat(BwdArgs a) {
       a.bt[ent[k]].y = first;
       pos += (1ull << 32) | len[k];
     }
-    register_long(a, lg, lg ? a.occ_row[i] : 0u, ent[k], len[k]);
+    register_long(a, lg, lg ? a.occ_row[i] : 0u, ent[k], len[k], a.long_hist);
   }
   trace_end(kTrAlloc);
 }
