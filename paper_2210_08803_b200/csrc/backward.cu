@@ -88,6 +88,7 @@ struct BwdArgs {
   float* S1;
   int optimizer;
   hps_opt_params opt;
+  uint32_t l2mode;  // A/B (HPS_GPU_L2): 8 gradient rows evict_first in the row stream
 };
 
 // ---- batch table ----------------------------------------------------------------------------
@@ -1077,6 +1078,10 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_async16_s(uint32_t smem_dst, const void* gsrc) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async16_sh(uint32_t smem_dst, const void* gsrc, uint64_t policy) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_dst), "l"(gsrc), "l"(policy)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -1106,6 +1111,7 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
   const uint32_t D = a.dim, nvec = D / 4;
   const bool mean = a.bag_len != nullptr;
   const uint32_t sbuf = smem_u32(buf) + lane * 16u;  // this lane's float4 of chunk buffer 0, row 0
+  const uint64_t efp = l2_policy_evict_first();
   const uint64_t S = *a.short_alloc >> 32;
   // segments per warp pass: the whole list spread over every warp of the grid (a fixed 32
   // left a third of the warps idle on config 2 and the rest with 32-segment chains)
@@ -1159,9 +1165,13 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
           const PipeEntry e = list[t0 + k];
           if (OPT == kOptGrad && (e.flags & 3u) == 0) continue;  // gradient-only: the row is written, never read
           const char* src = reinterpret_cast<const char*>((uint64_t(e.hi) << 32) | e.lo) + lane * 16u;
+          const bool ef = (a.l2mode & 8) && (e.flags & 3u) == 3u;  // A/B: gradient rows evict_first
 #pragma unroll
           for (int v = 0; v < VPL; ++v)
-            if (lane + 32u * v < nvec) cp_async16_s(dst + k * nvec * 16u + v * 512u, src + v * 512);
+            if (lane + 32u * v < nvec) {
+              if (ef) cp_async16_sh(dst + k * nvec * 16u + v * 512u, src + v * 512, efp);
+              else cp_async16_s(dst + k * nvec * 16u + v * 512u, src + v * 512);
+            }
         }
         cp_async_commit();
       };
@@ -1545,6 +1555,8 @@ BwdArgs base_args(hps_gpu_table t) {
   a.partial2 = t->ws_partial2;
   a.long_hbase = t->ws_long_hbase;
   a.node_cnt = t->ws_node_cnt;
+  static const uint32_t l2 = std::getenv("HPS_GPU_L2") ? std::atoi(std::getenv("HPS_GPU_L2")) : 0;  // A/B knob
+  a.l2mode = l2;
   (void)zl;
   return a;
 }
