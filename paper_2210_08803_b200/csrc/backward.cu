@@ -88,7 +88,7 @@ struct BwdArgs {
   float* S1;
   int optimizer;
   hps_opt_params opt;
-  uint32_t l2mode;  // A/B (HPS_GPU_L2): 8 gradient rows evict_first in the row stream
+  bool grad_once;   // one-hot batch: every gradient row is read once (row stream: L2 evict_first)
 };
 
 // ---- batch table ----------------------------------------------------------------------------
@@ -1165,7 +1165,7 @@ __device__ __forceinline__ void short_pipe(const BwdArgs& a, uint64_t warp, uint
           const PipeEntry e = list[t0 + k];
           if (OPT == kOptGrad && (e.flags & 3u) == 0) continue;  // gradient-only: the row is written, never read
           const char* src = reinterpret_cast<const char*>((uint64_t(e.hi) << 32) | e.lo) + lane * 16u;
-          const bool ef = (a.l2mode & 8) && (e.flags & 3u) == 3u;  // A/B: gradient rows evict_first
+          const bool ef = a.grad_once && (e.flags & 3u) == 3u;
 #pragma unroll
           for (int v = 0; v < VPL; ++v)
             if (lane + 32u * v < nvec) {
@@ -1555,8 +1555,7 @@ BwdArgs base_args(hps_gpu_table t) {
   a.partial2 = t->ws_partial2;
   a.long_hbase = t->ws_long_hbase;
   a.node_cnt = t->ws_node_cnt;
-  static const uint32_t l2 = std::getenv("HPS_GPU_L2") ? std::atoi(std::getenv("HPS_GPU_L2")) : 0;  // A/B knob
-  a.l2mode = l2;
+  a.grad_once = !t->last_multi;
   (void)zl;
   return a;
 }
