@@ -257,7 +257,8 @@ def reference_arm(args, cfg, rank, world):
 TRACE_NAMES = {0: "probe", 1: "pool", 2: "seg_alloc", 3: "place", 4: "long_hist", 5: "long_pass0",
                6: "long_pass1", 7: "long_pass2", 8: "long_pass3", 9: "long_reg", 10: "reduce_short",
                11: "reduce_long", 12: "reset_counts", 13: "count", 14: "|count_local", 15: "|count_global",
-               16: "|count_cas", 17: "|count_probe", 18: "scale_dout", 19: "<step-in", 20: ">step-out"}
+               16: "|count_cas", 17: "|count_probe", 18: "scale_dout", 19: "<step-in", 20: ">step-out", 21: "ins_claim",
+               22: "ins_commit", 23: "ins_finish"}
 
 
 def print_trace(ctx, n, step):
@@ -297,7 +298,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = get_config(args)
     if cfg.keyspace:  # every step sees a fresh batch, so new keys keep materialising inside the timed steps
-        args.pool = max(args.pool, args.warmup + args.steps)
+        args.pool = max(args.pool, args.warmup + args.steps + args.trace)
     if args.impl == "reference":
         return reference_arm(args, cfg, rank, world)
 
@@ -417,7 +418,10 @@ def main():
         def traced(i):  # stamps around the step mark its start/end latency in the stream
             flush.fill_(i & 0xff)
             ctx.lib.hps_gpu_debug_stamp(ctypes.c_void_p(stream.cuda_stream), 19)
-            one(i)
+            if cfg.keyspace:  # fresh batches, as the timed steps (their keys materialise in the step)
+                one(i, idx=timed0 + args.steps + i, nxt=timed0 + args.steps + i + 1 if i + 1 < args.trace else None)
+            else:
+                one(i)
             ctx.lib.hps_gpu_debug_stamp(ctypes.c_void_p(stream.cuda_stream), 20)
         print_trace(ctx, args.trace, traced)
     ms = float(np.mean(step_ms))

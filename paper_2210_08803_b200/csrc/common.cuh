@@ -285,7 +285,7 @@ constexpr int kTraceSlots = 32;
 enum TraceId : int {
   kTrProbe = 0, kTrPool = 1, kTrAlloc = 2, kTrPlace = 3, kTrHist = 4, kTrPass0 = 5, kTrLongReg = 9,
   kTrReduce = 10, kTrLong = 11, kTrReset = 12, kTrCount = 13, kTrCountLocal = 14, kTrCountGlobal = 15,
-  kTrCountCas = 16, kTrCountProbe = 17, kTrScale = 18
+  kTrCountCas = 16, kTrCountProbe = 17, kTrScale = 18, kTrInsClaim = 21, kTrInsCommit = 22, kTrInsFinish = 23
 };
 static __device__ TraceRec* g_trace = nullptr;
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -24,6 +24,22 @@ namespace {
 
 constexpr uint64_t kNoSlot = ~0ull;
 constexpr uint64_t kPresent = ~1ull;  // key committed before this call; nothing to do (keys-only insert)
+// keys-only insert that records a training batch (InsertRecord): a committed key's slot word
+// is kPresentRow | its local row. Every value >= kPresentRow (this, kPresent, kNoSlot) names
+// no slot claimed by the call.
+constexpr uint64_t kPresentRow = 1ull << 62;
+
+// A one-hot training record produced by the insert-on-miss pass itself (no separate probe):
+// k_insert_finish writes each occurrence's global row (row_absent if the insert failed for
+// it), the record's size, and clears the backward's zeroed words, as k_probe would.
+struct InsertRecord {
+  uint32_t* occ_row = nullptr;  // nullptr: not a training record
+  uint64_t row_base = 0;
+  uint32_t row_absent = 0;
+  uint64_t* d_n = nullptr;
+  uint32_t* zero = nullptr;
+  uint32_t zero_words = 0;
+};
 
 // ---------------------------------------------------------------------------------
 // K2: index probe helpers
@@ -98,8 +114,10 @@ __global__ void k_find(const Slot* __restrict__ slots, TableDev td, const uint64
 // read-only probe settles it (rows committed before the call cannot change during it).
 __global__ void k_insert_claim(Slot* __restrict__ slots, TableDev td, const uint64_t* __restrict__ keys, uint64_t n,
                                uint64_t* __restrict__ ws_slot, uint32_t* __restrict__ abort_flag, uint32_t* status,
-                               bool keys_only, const uint32_t* __restrict__ key_tables, uint32_t table) {
+                               bool keys_only, const uint32_t* __restrict__ key_tables, uint32_t table,
+                               bool record_rows) {
   if (*reinterpret_cast<volatile uint32_t*>(abort_flag)) return;
+  trace_begin(kTrInsClaim);
   Slot* base = slots + td.slot_base;
   const Slot empty{0, kRowEmpty, kAuxNone};
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -112,17 +130,19 @@ __global__ void k_insert_claim(Slot* __restrict__ slots, TableDev td, const uint
     if (keys_only) {
       uint64_t j = home;
       bool present = false;
+      uint32_t prow = 0;
       for (uint64_t p = 0; p <= td.slot_mask; ++p) {
         const Slot s = load_slot(base + j);
         if (s.row == kRowEmpty) break;
         if (s.key == key) {
           present = s.row != kRowPending;
+          prow = s.row;
           break;
         }
         j = (j + 1) & td.slot_mask;
       }
       if (present) {
-        ws_slot[i] = kPresent;
+        ws_slot[i] = record_rows ? (kPresentRow | prow) : kPresent;
         continue;
       }
     }
@@ -148,6 +168,7 @@ __global__ void k_insert_claim(Slot* __restrict__ slots, TableDev td, const uint
     }
     ws_slot[i] = found;
   }
+  trace_end(kTrInsClaim);
 }
 
 // Insert phase B (scan op): count(i) = 1 iff occurrence i is the first occurrence of a
@@ -164,7 +185,7 @@ struct InsertScanOp {
   __device__ uint64_t size() const { return *abort_flag ? 0 : n; }
   __device__ uint32_t count(uint64_t i) const {
     const uint64_t si = ws_slot[i];
-    if (si >= kPresent) return 0;
+    if (si >= kPresentRow) return 0;
     const Slot s = load_slot(slots + slot_base + si);
     return (s.row == kRowPending && s.aux == static_cast<uint32_t>(i)) ? 1u : 0u;
   }
@@ -175,7 +196,7 @@ struct InsertScanOp {
       f = 1;
     } else {
       const uint64_t si = ws_slot[i];
-      if (si < kPresent) {
+      if (si < kPresentRow) {
         const Slot s = load_slot(slots + slot_base + si);
         if (s.row != kRowPending && s.aux == static_cast<uint32_t>(i)) f = 2;
       }
@@ -202,6 +223,7 @@ __global__ void k_insert_commit(Slot* __restrict__ slots, TableDev td, uint32_t 
     }
     return;
   }
+  trace_begin(kTrInsCommit);
   const uint32_t lane = lane_id();
   const uint64_t warp = (blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -241,40 +263,53 @@ __global__ void k_insert_commit(Slot* __restrict__ slots, TableDev td, uint32_t 
       }
     }
   }
+  trace_end(kTrInsCommit);
 }
 
 // Insert phase D: publish rows_out, reset aux scratch (or roll the call back).
 __global__ void k_insert_finish(Slot* __restrict__ slots, TableDev td, uint32_t table, uint64_t n,
                                 const uint64_t* __restrict__ ws_slot, uint64_t* __restrict__ rows_out,
                                 const uint64_t* __restrict__ d_new, uint64_t* __restrict__ d_nrows,
-                                const uint32_t* __restrict__ abort_flag) {
+                                const uint32_t* __restrict__ abort_flag, InsertRecord rec) {
   const uint32_t ab = *reinterpret_cast<const volatile uint32_t*>(abort_flag);
+  trace_begin(kTrInsFinish);
   Slot* base = slots + td.slot_base;
+  if (rec.occ_row) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < rec.zero_words; w += gridDim.x * blockDim.x) rec.zero[w] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *rec.d_n = n;
+  }
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    uint32_t occ = rec.row_absent;  // (training record: the occurrence's global row)
+    const uint64_t si = ws_slot[i];
     if (ab == 1) {  // refused before any claim (NonFinite)
       if (rows_out) rows_out[i] = ~0ull;
-      continue;
-    }
-    const uint64_t si = ws_slot[i];
-    if (si == kPresent) continue;  // keys-only call: rows_out is NULL
-    if (si == kNoSlot) {
-      if (rows_out) rows_out[i] = ~0ull;
-      continue;
-    }
-    Slot* s = base + si;
-    if (ab) {  // roll back: drop every slot claimed by this call, release aux
-      if (s->row == kRowPending) {
-        *reinterpret_cast<ulonglong2*>(s) = make_ulonglong2(0ull, (uint64_t(kAuxNone) << 32) | kRowEmpty);
-      } else {
-        s->aux = kAuxNone;
-      }
-      if (rows_out) rows_out[i] = ~0ull;
+    } else if (si >= kPresentRow) {  // no slot claimed by this call: committed before, skipped, or failed
+      if (si == kNoSlot && rows_out) rows_out[i] = ~0ull;
+      if (si < kPresent) occ = static_cast<uint32_t>(td.row_base + static_cast<uint32_t>(si));
     } else {
-      if (rows_out) rows_out[i] = s->row;
-      s->aux = kAuxNone;
+      Slot* s = base + si;
+      if (ab) {  // roll back: drop every slot claimed by this call, release aux
+        if (s->row == kRowPending) {
+          *reinterpret_cast<ulonglong2*>(s) = make_ulonglong2(0ull, (uint64_t(kAuxNone) << 32) | kRowEmpty);
+        } else {
+          s->aux = kAuxNone;
+          occ = static_cast<uint32_t>(td.row_base + s->row);  // (committed by an earlier call)
+        }
+        if (rows_out) rows_out[i] = ~0ull;
+      } else {
+        // every occurrence of the key reads its row; only the first one (the claim's minimum
+        // index, in aux) releases the scratch word — a store per occurrence would serialise the
+        // hot keys' reads behind it (config 5: 29 vs 6.5 us)
+        const uint32_t r = s->row;
+        if (rows_out) rows_out[i] = r;
+        occ = static_cast<uint32_t>(td.row_base + r);
+        if (s->aux == static_cast<uint32_t>(i)) s->aux = kAuxNone;
+      }
     }
+    if (rec.occ_row) rec.occ_row[i] = occ;
   }
   if (!ab && blockIdx.x == 0 && threadIdx.x == 0) d_nrows[table] += *d_new;
+  trace_end(kTrInsFinish);
 }
 
 // Ingest validation (the whole call is refused before any claim): NaN/Inf -> NonFinite; for
@@ -815,7 +850,8 @@ __global__ void __launch_bounds__(256) k_hybrid_pool(const uint32_t* __restrict_
 
 }  // namespace
 int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
-                   uint64_t* rows_out, cudaStream_t st, const uint32_t* key_tables = nullptr);
+                   uint64_t* rows_out, cudaStream_t st, const uint32_t* key_tables = nullptr,
+                   const InsertRecord& rec = InsertRecord{});
 namespace {
 
 // A training record is about to overwrite ws_rows_a: counters of a previous record that no
@@ -851,10 +887,31 @@ int begin_training_record(hps_gpu_table t, LookupArgs& a, uint64_t nk, cudaStrea
 // Training record: probe + record every occurrence (on `st`). fork_dedup then puts the
 // backward's dedup on the slot's side stream (it needs only the record), after the pooling
 // was launched on the main stream: the two run concurrently; backward_update joins.
+int record_done(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk, cudaStream_t st);
+
 int record(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk, cudaStream_t st) {
   if (multi) k_probe<true><<<grid_for((uint64_t(a.n_bags) + 31) / 32 * 32, 256, kNumSMs * 16), 256, 0, st>>>(a);
   else k_probe<false><<<grid_for(a.n_bags, 256, kNumSMs * 16), 256, 0, st>>>(a);
   HPSG_CHECK_LAUNCH("probe");
+  return record_done(t, a, multi, mean, nk, st);
+}
+
+// One-hot insert-on-miss training record: the insert pass resolves every key anyway, so its
+// last kernel writes the record (rows, size, zeroed words) and no probe follows — one launch
+// and one full pass over the hash table fewer on config 5's critical path.
+int record_by_insert(hps_gpu_table t, const LookupArgs& a, const uint64_t* keys, uint64_t nk, cudaStream_t st) {
+  InsertRecord rec;
+  rec.occ_row = t->ws_rows_a;
+  rec.row_base = t->h_tables[0].row_base;
+  rec.row_absent = t->row_absent;
+  rec.d_n = t->ws_counts;
+  rec.zero = a.zero;
+  rec.zero_words = a.zero_words;
+  if (int s = hpsg_insert_on(t, 0, keys, nk, nullptr, nullptr, st, nullptr, rec)) return s;
+  return record_done(t, a, false, a.mean, nk, st);
+}
+
+int record_done(hps_gpu_table t, const LookupArgs& a, bool multi, bool mean, uint64_t nk, cudaStream_t st) {
   t->last_multi = multi;
   t->last_combiner = mean ? HPS_COMBINER_MEAN : HPS_COMBINER_SUM;
   t->last_n_keys_host = nk;
@@ -893,7 +950,7 @@ int launch_lookup(hps_gpu_table t, const LookupArgs& a, bool multi, bool rows);
 // Host-pointer keys/offsets staged H2D into the current slot (HPS_LOOKUP_KEYS_HOST); sets
 // *n_keys_host exactly when it is known on the host.
 int stage_keys(hps_gpu_table t, const uint64_t*& keys, const uint32_t*& offsets, uint64_t n_bags, uint32_t flags,
-               cudaStream_t st, uint64_t* n_keys_host) {
+               cudaStream_t st, uint64_t* n_keys_host, bool defer_insert = false) {
   const bool multi = offsets != nullptr;
   if (flags & HPS_LOOKUP_KEYS_HOST) {
     // Host buffers: stage H2D on the stream (pinned memory -> async copy).
@@ -914,7 +971,8 @@ int stage_keys(hps_gpu_table t, const uint64_t*& keys, const uint32_t*& offsets,
       set_last_error("HPS_LOOKUP_INSERT needs a single-table group and a host-known key count");
       return HPS_GPU_E_INVALID_ARGUMENT;
     }
-    if (int s = hpsg_insert_on(t, 0, keys, *n_keys_host, nullptr, nullptr, st)) return s;
+    if (!defer_insert)  // (deferred: the caller's training record runs the insert, record_by_insert)
+      if (int s = hpsg_insert_on(t, 0, keys, *n_keys_host, nullptr, nullptr, st)) return s;
   }
   return HPS_GPU_OK;
 }
@@ -1106,13 +1164,12 @@ int alloc_batch_slot(hps_gpu_table t, BatchSlot& b) {
   A(dalloc(&b.ws_partial, t->max_chunks * D));
   A(dalloc(&b.ws_counts, 8));
   A(dalloc(&b.ws_zero, t->zero_words));
-  A(dalloc(&b.ws_abort, 4));
   A(dalloc(&b.ws_keys_stage, N));
   A(dalloc(&b.ws_offsets_stage, B + 1));
   A(dalloc(&b.ws_ins_slot, N));
   A(dalloc(&b.ws_ins_pos, N));
   A(dalloc(&b.ws_ins_flag, N));
-  A(dalloc(&b.ws_ins_scan, scan_tiles(N) + 1));
+  A(dalloc(&b.ws_ins_scan, scan_tiles(N) + 3));
   if (st) return st;
   cudaStream_t s = t->ctx->stream;
   HPSG_CUDA(cudaMemsetAsync(b.ws_counts, 0, 8 * sizeof(uint64_t), s));
@@ -1136,7 +1193,7 @@ void free_batch_slot(BatchSlot& b) {
                   b.ws_short_rec, b.ws_short_bag, b.ws_occ_bag,   b.ws_bag_len,    b.ws_long_row,   b.ws_long_len,
                   b.ws_long_start, b.ws_lkey_a,   b.ws_lval_a,    b.ws_lkey_b,     b.ws_lval_b,     b.ws_long_base,
                   b.ws_task_long, b.ws_partial2,  b.ws_long_hbase, b.ws_node_cnt,  b.ws_partial,    b.ws_counts,
-                  b.ws_zero,      b.ws_abort,     b.ws_keys_stage, b.ws_offsets_stage, b.ws_ins_slot, b.ws_ins_pos,
+                  b.ws_zero,      b.ws_keys_stage, b.ws_offsets_stage, b.ws_ins_slot, b.ws_ins_pos,
                   b.ws_ins_flag,  b.ws_ins_scan};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1346,7 +1403,7 @@ int hps_gpu_table_insert(hps_gpu_table t, uint32_t table, const uint64_t* keys, 
 // Insert on stream `st` with the current batch slot's scratch (hps_gpu_table_insert; the
 // insert-on-miss of a prefetch runs it on the slot's side stream).
 int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64_t n, const float* rows,
-                   uint64_t* rows_out, cudaStream_t st, const uint32_t* key_tables) {
+                   uint64_t* rows_out, cudaStream_t st, const uint32_t* key_tables, const InsertRecord& rec) {
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (n == 0) return HPS_GPU_OK;
   if (!keys || n >= (1ull << 32) - 1) return HPS_GPU_E_INVALID_ARGUMENT;
@@ -1354,7 +1411,7 @@ int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64
   uint64_t* ws_slot = nullptr;
   uint32_t* ws_pos = nullptr;
   uint8_t* ws_flag = nullptr;
-  uint64_t* scan_status = nullptr;
+  uint64_t* hdr = nullptr;  // [abort flag, new-key count, scan status x tiles, ticket]: one memset
   const uint64_t tiles = scan_tiles(n);
   // Batches up to max_keys (insert-on-miss inside a step) use the preallocated scratch;
   // larger bulk loads take stream-ordered allocations.
@@ -1363,35 +1420,37 @@ int hpsg_insert_on(hps_gpu_table t, uint32_t table, const uint64_t* keys, uint64
     HPSG_CUDA(cudaMallocAsync(&ws_slot, n * sizeof(uint64_t), st));
     HPSG_CUDA(cudaMallocAsync(&ws_pos, n * sizeof(uint32_t), st));
     HPSG_CUDA(cudaMallocAsync(&ws_flag, n, st));
-    HPSG_CUDA(cudaMallocAsync(&scan_status, (tiles + 1) * sizeof(uint64_t), st));
+    HPSG_CUDA(cudaMallocAsync(&hdr, (tiles + 3) * sizeof(uint64_t), st));
   } else {
     ws_slot = t->ws_ins_slot;
     ws_pos = t->ws_ins_pos;
     ws_flag = t->ws_ins_flag;
-    scan_status = t->ws_ins_scan;
+    hdr = t->ws_ins_scan;
   }
-  HPSG_CUDA(cudaMemsetAsync(scan_status, 0, (tiles + 1) * sizeof(uint64_t), st));
-  HPSG_CUDA(cudaMemsetAsync(t->ws_abort, 0, sizeof(uint32_t), st));
-  HPSG_CUDA(cudaMemsetAsync(t->ws_counts + 3, 0, sizeof(uint64_t), st));
+  HPSG_CUDA(cudaMemsetAsync(hdr, 0, (tiles + 3) * sizeof(uint64_t), st));
+  uint32_t* abort_flag = reinterpret_cast<uint32_t*>(hdr);
+  uint64_t* d_new = hdr + 1;
+  uint64_t* scan_status = hdr + 2;
   const int grid = grid_for(n, 256, kNumSMs * 32);
-  if (rows) k_rows_non_finite<<<grid_for(n * t->dim, 256, kNumSMs * 32), 256, 0, st>>>(rows, n * t->dim, t->ws_abort,
+  if (rows) k_rows_non_finite<<<grid_for(n * t->dim, 256, kNumSMs * 32), 256, 0, st>>>(rows, n * t->dim, abort_flag,
                                                                                       t->ctx->d_status, t->f16 ? 1 : 0);
-  k_insert_claim<<<grid, 256, 0, st>>>(t->d_slots, td, keys, n, ws_slot, t->ws_abort, t->ctx->d_status,
-                                       rows == nullptr && rows_out == nullptr, key_tables, table);
-  InsertScanOp op{t->d_slots, td.slot_base, ws_slot, ws_pos, ws_flag, n, t->ws_counts + 3, t->ws_abort};
+  k_insert_claim<<<grid, 256, 0, st>>>(t->d_slots, td, keys, n, ws_slot, abort_flag, t->ctx->d_status,
+                                       rows == nullptr && rows_out == nullptr, key_tables, table,
+                                       rec.occ_row != nullptr);
+  InsertScanOp op{t->d_slots, td.slot_base, ws_slot, ws_pos, ws_flag, n, d_new, abort_flag};
   k_scan<InsertScanOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(
       op, scan_status, reinterpret_cast<uint32_t*>(scan_status + tiles));
   k_insert_commit<<<grid, 256, 0, st>>>(t->d_slots, td, table, keys, n, rows, ws_slot, ws_pos, ws_flag,
-                                        t->ws_counts + 3, t->d_nrows, t->d_w, t->d_s0, t->d_s1, t->n_state, t->a0,
-                                        t->dim, t->seed, t->d_row_keys, t->ws_abort, t->ctx->d_status, t->d_wh);
-  k_insert_finish<<<grid, 256, 0, st>>>(t->d_slots, td, table, n, ws_slot, rows_out, t->ws_counts + 3, t->d_nrows,
-                                        t->ws_abort);
+                                        d_new, t->d_nrows, t->d_w, t->d_s0, t->d_s1, t->n_state, t->a0,
+                                        t->dim, t->seed, t->d_row_keys, abort_flag, t->ctx->d_status, t->d_wh);
+  k_insert_finish<<<grid, 256, 0, st>>>(t->d_slots, td, table, n, ws_slot, rows_out, d_new, t->d_nrows, abort_flag,
+                                        rec);
   HPSG_CHECK_LAUNCH("insert");
   if (own) {
     HPSG_CUDA(cudaFreeAsync(ws_slot, st));
     HPSG_CUDA(cudaFreeAsync(ws_pos, st));
     HPSG_CUDA(cudaFreeAsync(ws_flag, st));
-    HPSG_CUDA(cudaFreeAsync(scan_status, st));
+    HPSG_CUDA(cudaFreeAsync(hdr, st));
   }
   return HPS_GPU_OK;
 }
@@ -1507,14 +1566,16 @@ int hps_gpu_lookup_pooled(hps_gpu_table t, const uint64_t* keys, const uint32_t*
     set_last_error("lookup: an F16 table is an inference table (no training lookups)");
     return HPS_GPU_E_DTYPE_MISMATCH;
   }
-  if (int s = stage_keys(t, keys, offsets, n_bags, flags, st, &n_keys_host)) return s;
+  const bool ins_rec = train && !multi && (flags & HPS_LOOKUP_INSERT);
+  if (int s = stage_keys(t, keys, offsets, n_bags, flags, st, &n_keys_host, ins_rec)) return s;
   LookupArgs a{};
   fill_lookup_args(t, a, keys, offsets, n_bags, combiner, out);
   if (train) {
     if (int s = begin_training_record(t, a, n_keys_host, st)) return s;
     a.occ_bag = multi ? t->ws_occ_bag : nullptr;
     a.bag_len = (multi && a.mean) ? t->ws_bag_len : nullptr;
-    if (int s = record(t, a, multi, a.mean, n_keys_host, st)) return s;
+    if (int s = ins_rec ? record_by_insert(t, a, keys, n_keys_host, st) : record(t, a, multi, a.mean, n_keys_host, st))
+      return s;
   }
   if (int s = launch_lookup(t, a, multi, train)) return s;
   if (train)

@@ -86,16 +86,15 @@ struct BatchSlot {
   float* ws_partial2 = nullptr;     // tree nodes above level 1 [max_nodes x dim]
   uint32_t* ws_long_hbase = nullptr;  // long segment -> its first node in ws_partial2
   uint32_t* ws_node_cnt = nullptr;    // arrivals per node; zero at rest (reset by the completing warp)
-  uint64_t* ws_counts = nullptr;    // [0]=N occurrences [1]=U segments [3] insert row counter
+  uint64_t* ws_counts = nullptr;    // [0]=N occurrences [1]=U segments [5] unconsumed record [6] its size
   uint32_t* ws_zero = nullptr;      // bwd_zero_layout(): allocators + look-back words, zeroed per training lookup
-  uint32_t* ws_abort = nullptr;
   uint64_t* ws_keys_stage = nullptr;
   uint32_t* ws_offsets_stage = nullptr;
   // insert scratch for batches up to max_keys (insert-on-miss runs inside the step)
   uint64_t* ws_ins_slot = nullptr;
   uint32_t* ws_ins_pos = nullptr;
   uint8_t* ws_ins_flag = nullptr;
-  uint64_t* ws_ins_scan = nullptr;
+  uint64_t* ws_ins_scan = nullptr;  // insert: [abort flag, new-key count, scan status, ticket] (one memset)
   // last training lookup recorded in this slot
   bool have_train = false, last_multi = false;
   bool have_unique = false;   // the segment lists describe the last backward (last_unique)
