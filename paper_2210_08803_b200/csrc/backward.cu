@@ -455,6 +455,8 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
   // keeps their locators: the long compaction after the barrier then needs no second pass
   // over the record (its canonical order is the thread order, its offsets the scan below)
   const bool one = c1 - c0 <= kBatch;
+  // a larger chunk that fits the (now idle) shared hash keeps its locators there instead
+  const bool cached = !one && c1 - c0 <= 2 * kDedupHash;
   uint32_t my_long = 0;
   uint32_t keep[kDedupIPT];
   for (uint64_t b0 = c0; b0 < c1; b0 += kBatch) {
@@ -469,6 +471,10 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
 #pragma unroll
     for (int k = 0; k < kDedupIPT; ++k) {
       keep[k] = loc[k];
+      if (cached) {
+        const uint64_t i = b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
+        if (i < c1) s_dd[i - c0] = loc[k];
+      }
       if (ent[k] == kNoEnt) continue;
       const uint64_t i = one ? b0 + uint64_t(threadIdx.x) * kDedupIPT + k : b0 + uint64_t(k) * kDedupBlock + threadIdx.x;
       if (loc[k] & kLongFlag) {
@@ -504,8 +510,12 @@ __global__ void __launch_bounds__(kDedupBlock, 1024 / kDedupBlock) k_dedup(BwdAr
 #pragma unroll
       for (int k = 0; k < kDedupIPT; ++k) {
         const uint64_t i = b0 + uint64_t(threadIdx.x) * kDedupIPT + k;
-        const uint32_t e = (i < c1 && a.occ_row[i] != a.row_absent) ? a.occ_ent[i] : kNoEnt;
-        loc[k] = e != kNoEnt ? __ldcg(&a.bt[e].y) : 0u;
+        if (cached) {
+          loc[k] = i < c1 ? s_dd[i - c0] : 0u;
+        } else {
+          const uint32_t e = (i < c1 && a.occ_row[i] != a.row_absent) ? a.occ_ent[i] : kNoEnt;
+          loc[k] = e != kNoEnt ? __ldcg(&a.bt[e].y) : 0u;
+        }
       }
 #pragma unroll
       for (int k = 0; k < kDedupIPT; ++k) cnt += (loc[k] & kLongFlag) ? 1u : 0u;
