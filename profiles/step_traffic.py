@@ -5,7 +5,9 @@ Input: `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_durat
 --clock-control none --csv -k regex:"k_"` over `bench.py --no-graph --pool 1 ...` (eager
 steps; ncu serialises kernels and flushes caches between them, so these are COLD bytes per
 launch, an upper bound on the in-graph traffic). The kernels of one training step are the
-launches between two consecutive training probes (k_probe) that include a reduce.
+launches between two consecutive step starts that include a reduce; a step starts at the
+training probe (k_probe), or, for insert-on-miss tables (config 5), at the insert's claim
+(k_insert_claim: the insert pass writes the training record itself, no k_probe).
 Usage: python profiles/step_traffic.py CSV WORKLOAD OUT_JSON
 """
 import collections
@@ -38,16 +40,18 @@ def load(path):
 
 
 def steps(recs):
-    """Split the launch list into training steps: each starts at a k_probe and must contain a reduce."""
+    """Split the launch list into training steps: each starts at a k_probe or k_insert_claim and
+    must contain a reduce."""
+    start = ("k_probe", "k_insert_claim")
     cur, out = [], []
     for r in recs:
-        if r["name"].startswith("k_probe") and cur:
+        if r["name"].startswith(start) and cur:
             out.append(cur)
             cur = []
         cur.append(r)
     if cur:
         out.append(cur)
-    return [s for s in out if s[0]["name"].startswith("k_probe") and any("reduce" in r["name"] for r in s)]
+    return [s for s in out if s[0]["name"].startswith(start) and any("reduce" in r["name"] for r in s)]
 
 
 def main(path, workload, out_path):
