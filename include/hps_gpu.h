@@ -358,14 +358,22 @@ int hps_gpu_dist_forward(hps_gpu_dist dist, const uint64_t* keys, const uint32_t
 int hps_gpu_dist_backward(hps_gpu_dist dist, const float* d_out, const hps_opt_params* opt_host);
 /* Transport of the exchanges. HPS_DIST_NCCL (default): grouped ncclSend/ncclRecv of the
  * regions. HPS_DIST_PEER: no collective calls — the requester's region kernel stores keys and
- * table ids straight into the owners' receive buffers, the pooling loads the owners' gathered
- * rows straight from their memory, and the gradient scatter stores into the owners' gradient
- * regions (NVLink peer loads/stores through CUDA-IPC mappings, exchanged once over NCCL; the
+ * table ids straight into the owners' receive buffers; each owner maps every received slot to
+ * the first slot of the same (table, key) in that requester's region, and the requester copies
+ * only those per-destination UNIQUE rows from the owner's gathered rows (U_p rows per owner
+ * cross NVLink instead of one per occurrence) and pools them locally; the gradient scatter
+ * stores per-occurrence gradients into the owners' gradient regions (the owner's backward
+ * needs them in canonical order: bit-identical results). NVLink peer loads/stores go through
+ * CUDA-IPC mappings, exchanged once over NCCL; the
  * loopback ranks of one device use each other's memory directly). Phases are ordered by
  * per-step epochs the ranks write into each other's flag words (release/acquire at system
  * scope), so a peer-transport step is graph-capturable too. Collective: every rank sets it. */
 enum { HPS_DIST_NCCL = 0, HPS_DIST_PEER = 1 };
 int hps_gpu_dist_set_transport(hps_gpu_dist dist, int transport);
+/* Cumulative count of unique rows this owner has served to requesters over the peer transport
+ * (one per distinct (table, key) per requester region per step): the rows that crossed NVLink.
+ * Synchronises the context's stream. */
+int hps_gpu_dist_unique_rows(hps_gpu_dist dist, uint64_t* served_host);
 /* Loopback transport (tests, single-GPU bring-up): n ranks of ONE process on one device,
  * the all-to-alls done as device copies between their buffers. Rank r's calls must run on
  * their own host thread (every all-to-all is a rendezvous of the n ranks); ctxs[r] should

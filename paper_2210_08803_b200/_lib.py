@@ -153,6 +153,7 @@ SIGNATURES = {
     "hps_gpu_dist_backward": (i32, [vp, vp, C.POINTER(OptParams)]),
     "hps_gpu_dist_create_loopback": (i32, [vp, vp, C.POINTER(DistConfig), u32, vp]),
     "hps_gpu_dist_set_transport": (i32, [vp, i32]),
+    "hps_gpu_dist_unique_rows": (i32, [vp, C.POINTER(u64)]),
     "hps_gpu_table_prefetch": (i32, [vp, u32, vp, vp, u32, i32, u32]),
     "hps_gpu_table_join_prefetch": (i32, [vp]),
     "hps_gpu_table_last_unique": (i32, [vp, vp, vp]),

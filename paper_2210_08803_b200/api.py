@@ -500,6 +500,12 @@ class DistTable:
         """"nccl" (grouped send/recv) or "peer" (the kernels load/store the peers' regions directly)."""
         L.check(self.lib.hps_gpu_dist_set_transport(self.h, {"nccl": 0, "peer": 1}[transport]), "dist_set_transport")
 
+    def unique_rows_served(self) -> int:
+        """Cumulative unique rows this owner served over the peer transport (syncs the stream)."""
+        v = C.c_uint64(0)
+        L.check(self.lib.hps_gpu_dist_unique_rows(self.h, C.byref(v)), "dist_unique_rows")
+        return int(v.value)
+
     def close(self) -> None:
         if getattr(self, "h", None):
             self.lib.hps_gpu_dist_destroy(self.h)

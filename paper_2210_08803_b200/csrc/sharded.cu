@@ -73,6 +73,15 @@ struct hps_gpu_dist_s {
   uint64_t* flags = nullptr;            // [3 x G] epochs this rank's peers signal into
   uint64_t* d_epoch = nullptr;          // step counter (device: graph replays advance it)
   std::vector<void*> ipc_opened;        // peer buffers opened through CUDA IPC (NCCL mode)
+  // per-destination unique rows (peer transport): the owner maps every received slot to the
+  // first slot of the same (table, key) in its requester's region (lead); the requester copies
+  // only those leaders' rows over NVLink (into rows_back) and pools locally (perm_u)
+  uint32_t* lead = nullptr;             // [G x C] owner side: slot -> leader slot (same region)
+  uint32_t* lead_ent = nullptr;         // [G x C] slot -> its hash entry (kNoLead: empty slot)
+  uint2* lead_ht = nullptr;             // {claimer slot + 1, min slot}, zero / UINT32_MAX at rest
+  uint64_t lead_mask = 0;
+  uint32_t* perm_u = nullptr;           // requester: occurrence -> its leader's slot in rows_back
+  unsigned long long* d_served = nullptr;  // cumulative unique rows served to requesters (peer)
   // last forward
   const uint32_t* last_offsets = nullptr;
   uint64_t last_bags = 0;
@@ -89,6 +98,7 @@ struct PeerTab {
   float* rows[kMaxPeers];
   float* grads[kMaxPeers];
   uint64_t* flags[kMaxPeers];
+  uint32_t* lead[kMaxPeers];
 };
 
 // A group of loopback ranks: the all-to-all is device copies between their buffers, each
@@ -272,6 +282,93 @@ __global__ void __launch_bounds__(256) k_scatter_grads_peer(PeerTab pt, uint32_t
   __threadfence_system();
 }
 
+// ---- per-destination unique rows (peer transport) -------------------------------------
+// Owner side, after the gather: every received slot q of region p = q / C (requester p's
+// occurrences) gets lead[q] = the smallest slot of region p holding the same (table, key).
+// The hash entry is claimed by the first arriving slot (claimer + 1); later slots compare
+// their (region, table, key) with the claimer's and take atomicMin. Empty slots lead
+// themselves. Three launches: claim, resolve, reset (the table returns to empty).
+constexpr uint32_t kNoLead = 0xffffffffu;
+__device__ __forceinline__ uint64_t lead_home(uint64_t key, uint32_t table, uint32_t region, uint64_t mask) {
+  return mix64(key ^ mix64((uint64_t(region) << 32) | table)) & mask;
+}
+__global__ void __launch_bounds__(256) k_lead_claim(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ tables,
+                                                    uint64_t GC, uint64_t C, uint2* ht, uint64_t mask,
+                                                    uint32_t* __restrict__ ent, uint32_t* __restrict__ lead) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < GC; q += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t tb = tables[q];
+    if (tb == 0xffffffffu) {  // empty slot of a region
+      ent[q] = kNoLead;
+      lead[q] = static_cast<uint32_t>(q);
+      continue;
+    }
+    const uint64_t key = keys[q];
+    const uint32_t region = static_cast<uint32_t>(q / C);
+    uint64_t h = lead_home(key, tb, region, mask);
+    while (true) {
+      uint32_t cur = __ldcg(&ht[h].x);
+      if (cur == 0u) {
+        cur = atomicCAS(&ht[h].x, 0u, static_cast<uint32_t>(q) + 1u);
+        if (cur == 0u) break;  // claimed
+      }
+      const uint64_t q2 = cur - 1u;
+      if (q2 / C == region && tables[q2] == tb && keys[q2] == key) break;  // same (region, table, key)
+      h = (h + 1) & mask;
+    }
+    atomicMin(&ht[h].y, static_cast<uint32_t>(q));
+    ent[q] = static_cast<uint32_t>(h);
+  }
+}
+__global__ void __launch_bounds__(256) k_lead_resolve(const uint2* __restrict__ ht, uint64_t GC,
+                                                      const uint32_t* __restrict__ ent, uint32_t* __restrict__ lead) {
+  for (uint64_t q = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; q < GC; q += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = ent[q];
+    if (e != kNoLead) lead[q] = __ldcg(&ht[e].y);
+  }
+}
+// (+ counts the leaders of non-empty slots: the rows requesters fetch from this owner)
+__global__ void __launch_bounds__(256) k_lead_reset(uint2* ht, uint64_t GC, const uint32_t* __restrict__ ent,
+                                                    const uint32_t* __restrict__ lead, unsigned long long* served) {
+  for (uint64_t base = blockIdx.x * uint64_t(blockDim.x); base < GC; base += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t q = base + threadIdx.x;
+    const uint32_t e = q < GC ? ent[q] : kNoLead;
+    const bool leader = e != kNoLead && lead[q] == q;
+    if (leader) ht[e] = make_uint2(0u, 0xffffffffu);  // one writer per entry
+    const int c = __syncthreads_count(leader);
+    if (threadIdx.x == 0 && c) atomicAdd(served, static_cast<unsigned long long>(c));
+  }
+}
+__global__ void k_lead_init(uint2* ht, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    ht[i] = make_uint2(0u, 0xffffffffu);
+}
+
+// Requester side: occurrence i (slot p*C + r of this rank's regions; slot rank*C + r on owner
+// p) reads its leader from owner p's lead map; a leader copies its row from owner p's gathered
+// rows (over NVLink) into rows_back[p*C + r]; perm_u[i] = its leader's rows_back slot. Only
+// U_p rows per owner cross NVLink instead of one per occurrence; the pooling then reads
+// rows_back locally (duplicates hit L2).
+template <int LPR>
+__global__ void __launch_bounds__(256) k_fetch_unique_peer(PeerTab pt, uint32_t rank, uint64_t C,
+                                                           const uint32_t* __restrict__ perm, uint64_t n, uint32_t dim,
+                                                           float* __restrict__ rows_back, uint32_t* __restrict__ perm_u) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t i = gid; i < n; i += ng) {
+    const uint32_t pr = perm[i], p = static_cast<uint32_t>(pr / C);
+    const uint64_t r = pr - uint64_t(p) * C, q = uint64_t(rank) * C + r;
+    const uint64_t l = pt.lead[p][q];  // same region: l in [rank*C, rank*C + C)
+    if (gl == 0) perm_u[i] = static_cast<uint32_t>(uint64_t(p) * C + (l - uint64_t(rank) * C));
+    if (l != q) continue;
+    const float4* src = reinterpret_cast<const float4*>(pt.rows[p] + q * dim);
+    float4* dst = reinterpret_cast<float4*>(rows_back + uint64_t(pr) * dim);
+    if (static_cast<const void*>(src) == static_cast<const void*>(dst)) continue;  // world of one: aliased
+    for (uint32_t v = gl; v < nvec; v += LPR) dst[v] = src[v];
+  }
+}
+
 int lpr_of(uint32_t dim) {
   const uint32_t nvec = dim / 4;
   return nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
@@ -376,11 +473,25 @@ int dist_forward_peer(hps_gpu_dist d, const uint32_t* offsets, uint64_t n_bags, 
   HPSG_CHECK_LAUNCH("dist regions (peer)");
   const uint32_t gflags = (flags & HPS_LOOKUP_TRAIN) | (flags & HPS_LOOKUP_INSERT);
   if (int s = hps_gpu_gather_rows(d->shard, d->recv_keys, d->recv_tables, GC, d->rows_own, gflags)) return s;
+  if (d->G > 1) {  // the leader map of every requester region (per-destination unique rows;
+                   // a world of one moves nothing over NVLink: it pools from its own rows)
+    const int g = grid_for(GC, 256, kNumSMs * 8);
+    k_lead_claim<<<g, 256, 0, st>>>(d->recv_keys, d->recv_tables, GC, d->C, d->lead_ht, d->lead_mask, d->lead_ent, d->lead);
+    k_lead_resolve<<<g, 256, 0, st>>>(d->lead_ht, GC, d->lead_ent, d->lead);
+    k_lead_reset<<<g, 256, 0, st>>>(d->lead_ht, GC, d->lead_ent, d->lead, d->d_served);
+    HPSG_CHECK_LAUNCH("dist leader map (peer)");
+  }
   k_signal<<<1, 64, 0, st>>>(*d->peer, 1, d->G, d->rank, d->d_epoch);
   k_wait<<<1, 64, 0, st>>>(d->flags, 1, d->G, d->d_epoch);
   const int lpr = lpr_of(d->dim);
-  HPSG_LPR_DISPATCH(k_pool_rows_peer, lpr, grid_for(n_bags * lpr, 256, kNumSMs * 32), st, *d->peer, d->rank, d->C,
-                    d->perm, offsets, n_bags, d->dim, combiner == HPS_COMBINER_MEAN, out);
+  if (d->G > 1) {
+    HPSG_LPR_DISPATCH(k_fetch_unique_peer, lpr, grid_for(n * lpr, 256, kNumSMs * 32), st, *d->peer, d->rank, d->C,
+                      d->perm, n, d->dim, d->rows_back, d->perm_u);
+    HPSG_CHECK_LAUNCH("dist unique-row fetch (peer)");
+  }
+  if (int s = hps_gpu_pool_rows(d->ctx, d->rows_back, d->G > 1 ? d->perm_u : d->perm, offsets, n_bags, d->dim, combiner,
+                                out))
+    return s;
   HPSG_CHECK_LAUNCH("dist pool (peer)");
   d->last_offsets = offsets;
   d->last_bags = n_bags;
@@ -396,6 +507,7 @@ void fill_self(hps_gpu_dist d, PeerTab& t, uint32_t p) {
   t.rows[p] = d->rows_own;
   t.grads[p] = d->grads_recv;
   t.flags[p] = d->flags;
+  t.lead[p] = d->lead;
 }
 }  // namespace
 
@@ -422,7 +534,15 @@ int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
                           reinterpret_cast<const void*>(k_scatter_grads_peer<8>),
                           reinterpret_cast<const void*>(k_scatter_grads_peer<4>),
                           reinterpret_cast<const void*>(k_scatter_grads_peer<2>),
-                          reinterpret_cast<const void*>(k_scatter_grads_peer<1>)})
+                          reinterpret_cast<const void*>(k_scatter_grads_peer<1>),
+                          reinterpret_cast<const void*>(k_lead_claim), reinterpret_cast<const void*>(k_lead_resolve),
+                          reinterpret_cast<const void*>(k_lead_reset),
+                          reinterpret_cast<const void*>(k_fetch_unique_peer<32>),
+                          reinterpret_cast<const void*>(k_fetch_unique_peer<16>),
+                          reinterpret_cast<const void*>(k_fetch_unique_peer<8>),
+                          reinterpret_cast<const void*>(k_fetch_unique_peer<4>),
+                          reinterpret_cast<const void*>(k_fetch_unique_peer<2>),
+                          reinterpret_cast<const void*>(k_fetch_unique_peer<1>)})
       HPSG_CUDA(cudaFuncGetAttributes(&fa, f));
   }
   if (!d->peer) d->peer = new PeerTab{};
@@ -432,16 +552,17 @@ int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
   } else if (d->loop) {  // loopback ranks: the peers' buffers are this device's memory
     for (uint32_t p = 0; p < d->G; ++p) fill_self(d->loop->members[p], t, p);
   } else {  // NCCL ranks: CUDA-IPC handles of every owner-side buffer, all-gathered over NCCL
-    cudaIpcMemHandle_t mine[5];
-    void* bufs[5] = {d->recv_keys, d->recv_tables, d->rows_own, d->grads_recv, d->flags};
-    for (int k = 0; k < 5; ++k) HPSG_CUDA(cudaIpcGetMemHandle(&mine[k], bufs[k]));
+    constexpr int kB = 6;
+    cudaIpcMemHandle_t mine[kB];
+    void* bufs[kB] = {d->recv_keys, d->recv_tables, d->rows_own, d->grads_recv, d->flags, d->lead};
+    for (int k = 0; k < kB; ++k) HPSG_CUDA(cudaIpcGetMemHandle(&mine[k], bufs[k]));
     cudaIpcMemHandle_t* d_all = nullptr;
     HPSG_CUDA(cudaMalloc(&d_all, sizeof(mine) * d->G));
-    HPSG_CUDA(cudaMemcpy(d_all + 5 * d->rank, mine, sizeof(mine), cudaMemcpyHostToDevice));
-    HPSG_NCCL(ncclAllGather(d_all + 5 * d->rank, d_all, sizeof(mine), ncclUint8, static_cast<ncclComm_t>(d->ctx->nccl),
+    HPSG_CUDA(cudaMemcpy(d_all + kB * d->rank, mine, sizeof(mine), cudaMemcpyHostToDevice));
+    HPSG_NCCL(ncclAllGather(d_all + kB * d->rank, d_all, sizeof(mine), ncclUint8, static_cast<ncclComm_t>(d->ctx->nccl),
                             d->ctx->stream));
     HPSG_CUDA(cudaStreamSynchronize(d->ctx->stream));
-    std::vector<cudaIpcMemHandle_t> all(5 * d->G);
+    std::vector<cudaIpcMemHandle_t> all(kB * d->G);
     HPSG_CUDA(cudaMemcpy(all.data(), d_all, sizeof(mine) * d->G, cudaMemcpyDeviceToHost));
     cudaFree(d_all);
     for (uint32_t p = 0; p < d->G; ++p) {
@@ -449,9 +570,9 @@ int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
         fill_self(d, t, p);
         continue;
       }
-      void* ptr[5];
-      for (int k = 0; k < 5; ++k) {
-        HPSG_CUDA(cudaIpcOpenMemHandle(&ptr[k], all[5 * p + k], cudaIpcMemLazyEnablePeerAccess));
+      void* ptr[kB];
+      for (int k = 0; k < kB; ++k) {
+        HPSG_CUDA(cudaIpcOpenMemHandle(&ptr[k], all[kB * p + k], cudaIpcMemLazyEnablePeerAccess));
         d->ipc_opened.push_back(ptr[k]);
       }
       t.keys[p] = static_cast<uint64_t*>(ptr[0]);
@@ -459,6 +580,7 @@ int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
       t.rows[p] = static_cast<float*>(ptr[2]);
       t.grads[p] = static_cast<float*>(ptr[3]);
       t.flags[p] = static_cast<uint64_t*>(ptr[4]);
+      t.lead[p] = static_cast<uint32_t*>(ptr[5]);
     }
   }
   d->transport = HPS_DIST_PEER;
@@ -541,6 +663,21 @@ int dist_create(hps_gpu_ctx ctx, hps_gpu_table shard, const hps_dist_config* cfg
   if (!st && cudaMemcpy(d->d_slot_table, cfg->slot_table_host, d->n_slots * 4, cudaMemcpyHostToDevice) != cudaSuccess)
     st = HPS_GPU_E_CUDA;
   if (!st && cudaEventCreateWithFlags(&d->loop_ev, cudaEventDisableTiming) != cudaSuccess) st = HPS_GPU_E_CUDA;
+  A(dalloc_n(&d->lead, GC));
+  A(dalloc_n(&d->lead_ent, GC));
+  A(dalloc_n(&d->perm_u, N));
+  A(dalloc_n(&d->d_served, 1));
+  if (!st && cudaMemset(d->d_served, 0, sizeof(unsigned long long)) != cudaSuccess) st = HPS_GPU_E_CUDA;
+  {
+    uint64_t hs = 1;
+    while (hs < 2 * GC) hs <<= 1;
+    d->lead_mask = hs - 1;
+    A(dalloc_n(&d->lead_ht, hs));
+    if (!st) {
+      k_lead_init<<<grid_for(hs, 256, kNumSMs * 8), 256, 0, ctx->stream>>>(d->lead_ht, hs);
+      if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) st = HPS_GPU_E_CUDA;
+    }
+  }
   A(dalloc_n(&d->flags, 3 * uint64_t(d->G)));
   A(dalloc_n(&d->d_epoch, 1));
   if (!st && (cudaMemset(d->flags, 0, 3 * d->G * sizeof(uint64_t)) != cudaSuccess ||
@@ -587,8 +724,9 @@ int hps_gpu_dist_destroy(hps_gpu_dist d) {
   if (d->flags) cudaFree(d->flags);
   if (d->d_epoch) cudaFree(d->d_epoch);
   if (d->plan) hps_gpu_xplan_destroy(d->plan);
-  void* own[] = {d->d_slot_table, d->dense_keys, d->dense_tables, d->dense_perm, d->counts, d->occ_bag, d->perm,
-                 d->send_keys,    d->send_tables, d->rows_own,    d->grads_send};
+  void* own[] = {d->d_slot_table, d->dense_keys, d->dense_tables, d->dense_perm, d->counts,   d->occ_bag,
+                 d->perm,         d->send_keys,  d->send_tables, d->rows_own,   d->grads_send, d->lead,
+                 d->lead_ent,     d->lead_ht,    d->perm_u,      d->d_served};
   for (void* p : own)
     if (p) cudaFree(p);
   if (d->G > 1) {
@@ -603,6 +741,15 @@ int hps_gpu_dist_destroy(hps_gpu_dist d) {
 int hps_gpu_dist_capacity(hps_gpu_dist d, uint64_t* per_peer_out) {
   if (!d || !per_peer_out) return HPS_GPU_E_INVALID_ARGUMENT;
   *per_peer_out = d->C;
+  return HPS_GPU_OK;
+}
+
+int hps_gpu_dist_unique_rows(hps_gpu_dist d, uint64_t* served_host) {
+  if (!d || !served_host) return HPS_GPU_E_INVALID_ARGUMENT;
+  HPSG_CUDA(cudaStreamSynchronize(d->ctx->stream));
+  unsigned long long v = 0;
+  HPSG_CUDA(cudaMemcpy(&v, d->d_served, sizeof(v), cudaMemcpyDeviceToHost));
+  *served_host = v;
   return HPS_GPU_OK;
 }
 

@@ -142,7 +142,20 @@ def run_world(world, multi, optimizer, steps=3, insert=False, transport="nccl"):
             k, o, _ = loc[r]
             outs_l[r] = dists[r].forward(k, B, offsets=o, combiner=comb, train=True, insert_missing=insert)
 
+        served0 = [d.unique_rows_served() for d in dists] if transport == "peer" else None
         on_ranks(fwd)
+        if transport == "peer":
+            # per-destination unique rows: every requester fetched exactly one row per distinct
+            # (table, key) of its own batch (each key has one owner), summed over the owners
+            served = sum(d.unique_rows_served() for d in dists) - sum(served0)
+            want = 0
+            for r in range(world if world > 1 else 0):  # (a world of one pools its own rows)
+                lo, hi = offs[r * B * S], offs[(r + 1) * B * S]
+                bag = np.repeat(np.arange(B * S), np.diff(offs[r * B * S:(r + 1) * B * S + 1])) if multi \
+                    else np.arange(B * S)
+                tab = np.asarray(slot_table, dtype=np.uint64)[bag % S]
+                want += len(set(zip(tab.tolist(), keys[lo:hi].tolist())))
+            assert served == want, f"world {world} step {step}: {served} unique rows served, want {want}"
         for r in range(world):
             close(outs_l[r].cpu().numpy(), ref[r * B * S:(r + 1) * B * S], f"world {world} rank {r} step {step}")
         on_ranks(lambda r: dists[r].backward(loc[r][2], p))
