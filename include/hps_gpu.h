@@ -53,6 +53,7 @@ enum {
   HPS_GPU_E_UNKNOWN_TABLE = 11,
   HPS_GPU_E_BAD_SHARD = 13,
   HPS_GPU_E_IO = 14,
+  HPS_GPU_E_CORRUPTION = 15,
   HPS_GPU_E_INFEASIBLE = 16,
   /* device failures */
   HPS_GPU_E_CUDA = 256,
@@ -518,6 +519,68 @@ int hps_plan_hybrid(const uint64_t* keys_host, const uint64_t* counts_host, uint
  * mass, required for HPS_PLAN_HYBRID. */
 int hps_estimate_comm(int strategy, uint64_t batch, const hps_slot_spec* slots_host, uint32_t n_slots,
                       uint32_t n_devices, const double* p_cold_host, double* fwd_bytes_host, double* bwd_bytes_host);
+
+/* ---- lower tiers of the miss path: VDB (L2) and PDB (L3), host-resident (tiers.cpp) ----
+ * SPEC.md:192-250 (volatile-store) and :252-318 (persistent-store); SURVEY.md §8(f) rank 4.
+ * The VDB holds one table: shard = partition_of(key, num_shards) (hps/hash.hpp), at most
+ * per_shard_capacity entries per shard; a put stores an entry iff its version is newer than
+ * the resident one (or the key is absent); a put into a full shard drops the entry
+ * (HPS_VDB_REJECT_NEW) or first removes the shard's entry with the smallest version
+ * (HPS_VDB_EVICT_OLDEST_VERSION). get has no side effects. Shards lock single-writer /
+ * multi-reader and are worked in parallel. All pointers are HOST pointers. */
+enum { HPS_VDB_REJECT_NEW = 0, HPS_VDB_EVICT_OLDEST_VERSION = 1 };
+typedef struct hps_vdb_s* hps_vdb;
+int hps_vdb_create(uint32_t num_shards, uint64_t per_shard_capacity, int overflow_policy, uint32_t dim,
+                   hps_vdb* out_host);
+int hps_vdb_destroy(hps_vdb vdb);
+int hps_vdb_put_batch(hps_vdb vdb, const uint64_t* keys, const float* vecs, const uint64_t* versions, uint64_t n,
+                      uint64_t* stored_out);
+int hps_vdb_get_batch(hps_vdb vdb, const uint64_t* keys, uint64_t n, float* vecs_out, uint64_t* versions_out,
+                      uint8_t* found_out, uint64_t* n_found_out);
+/* Point-in-time listing of one shard, ascending key; *n_out = its size (only the count when
+ * cap < size). Bad index -> HPS_GPU_E_BAD_SHARD. */
+int hps_vdb_shard_snapshot(hps_vdb vdb, uint32_t shard, uint64_t* keys, float* vecs, uint64_t* versions, uint64_t cap,
+                           uint64_t* n_out);
+int hps_vdb_size(hps_vdb vdb, uint64_t* n_out);
+
+/* PDB: <root>/<table>/MANIFEST + append-only segments seg_NNNNNNNN.log of LogRecords
+ *   key u64 | version u64 | dim u16 | dtype u8 (0 = f32) | payload dim x f32 | crc32c u32
+ * (little-endian; CRC-32C of the preceding record bytes). open rebuilds the index (highest
+ * version per key); a torn tail of a table's newest segment is dropped and truncated
+ * (*dropped_tail_out counts them), a bad record anywhere else fails with
+ * HPS_GPU_E_CORRUPTION. put appends iff newer; segments rotate at 64 MiB
+ * (HPS_PDB_SEGMENT_BYTES overrides) with a file flush, and close flushes. */
+typedef struct hps_pdb_s* hps_pdb;
+int hps_pdb_open(const char* root, hps_pdb* out_host, uint64_t* dropped_tail_out);
+int hps_pdb_close(hps_pdb pdb);
+int hps_pdb_table_count(hps_pdb pdb, uint64_t* n_out);
+int hps_pdb_create_table(hps_pdb pdb, const char* name, uint32_t dim, const float* default_vec /* NULL: zeros */);
+int hps_pdb_table_info(hps_pdb pdb, const char* table, uint32_t* dim_out, float* default_vec_out, uint64_t* keys_out);
+int hps_pdb_put_batch(hps_pdb pdb, const char* table, const uint64_t* keys, const float* vecs, const uint64_t* versions,
+                      uint64_t n, uint64_t* stored_out);
+int hps_pdb_get_batch(hps_pdb pdb, const char* table, const uint64_t* keys, uint64_t n, float* vecs_out,
+                      uint64_t* versions_out, uint8_t* found_out, uint64_t* n_found_out);
+int hps_pdb_scan(hps_pdb pdb, const char* table, uint64_t* keys, float* vecs, uint64_t* versions, uint64_t cap,
+                 uint64_t* n_out);
+int hps_pdb_compact(hps_pdb pdb, const char* table, uint64_t* reclaimed_bytes_out);
+/* CRC-32C of host bytes continuing `crc` (0 to start): the PDB record checksum (SSE4.2). */
+uint32_t hps_crc32c_host(uint32_t crc, const void* data, size_t len);
+
+/* ---- the tiered orchestrator: L1 GPU cache -> L2 VDB -> L3 PDB (tiered.cu) -----------
+ * SPEC.md:322-345. lookup(keys) on the cache's context: distinct keys in first-occurrence
+ * order (one tier probe per distinct key), L1 = hps_gpu_cache_query, the misses from the
+ * VDB, then the PDB, else the PDB table's default vector (source Default); out[n x dim]
+ * (device) in input order; source_counts_host[4] = per input key {L1, L2, L3, Default}.
+ * Migrations are started and NOT waited for: keys found in L2 are inserted into L1 (at their
+ * VDB version), keys found only in L3 into L2 and L1 (at their PDB version); absent keys are
+ * inserted nowhere. hps_gpu_tiered_await(t) = the last lookup's migrations are visible. */
+typedef struct hps_gpu_tiered_s* hps_gpu_tiered;
+int hps_gpu_tiered_create(hps_gpu_cache l1, hps_vdb l2, hps_pdb l3, const char* table, uint64_t max_batch,
+                          hps_gpu_tiered* out_host);
+int hps_gpu_tiered_destroy(hps_gpu_tiered t);
+int hps_gpu_tiered_lookup(hps_gpu_tiered t, const uint64_t* keys, uint64_t n, float* out,
+                          uint64_t* source_counts_host);
+int hps_gpu_tiered_await(hps_gpu_tiered t);
 
 /* ---- synthetic workload helpers (device-side generators) ------- */
 /* The deterministic row initialiser of DESIGN.md §4.1 (host-callable, for checks). */

@@ -23,7 +23,11 @@ E_BAD_MAGIC, E_BAD_FORMAT_VERSION, E_TRUNCATED, E_TRAILING_BYTES, E_DUPLICATE_KE
 E_DIM_MISMATCH = 7
 E_NON_FINITE = 10
 E_UNKNOWN_TABLE = 11
+E_BAD_SHARD = 13
+E_IO = 14
+E_CORRUPTION = 15
 E_INFEASIBLE = 16
+VDB_REJECT_NEW, VDB_EVICT_OLDEST_VERSION = 0, 1
 E_CUDA = 256
 E_OUT_OF_MEMORY = 257
 E_NO_DEVICE = 258
@@ -209,6 +213,27 @@ SIGNATURES = {
     "hps_validate_dim": (i32, [C.c_uint]),
     "hps_embedding_vector_f32_status": (i32, [C.POINTER(f32), C.c_ulonglong]),
     "hps_table_meta_make_status": (i32, [C.c_char_p, C.c_uint, C.c_uint]),
+    # lower tiers of the miss path (tiers.cpp, host) + the tiered orchestrator (tiered.cu)
+    "hps_vdb_create": (i32, [u32, u64, i32, u32, C.POINTER(vp)]),
+    "hps_vdb_destroy": (i32, [vp]),
+    "hps_vdb_put_batch": (i32, [vp, vp, vp, vp, u64, C.POINTER(u64)]),
+    "hps_vdb_get_batch": (i32, [vp, vp, u64, vp, vp, vp, C.POINTER(u64)]),
+    "hps_vdb_shard_snapshot": (i32, [vp, u32, vp, vp, vp, u64, C.POINTER(u64)]),
+    "hps_vdb_size": (i32, [vp, C.POINTER(u64)]),
+    "hps_pdb_open": (i32, [C.c_char_p, C.POINTER(vp), C.POINTER(u64)]),
+    "hps_pdb_close": (i32, [vp]),
+    "hps_pdb_table_count": (i32, [vp, C.POINTER(u64)]),
+    "hps_pdb_create_table": (i32, [vp, C.c_char_p, u32, vp]),
+    "hps_pdb_table_info": (i32, [vp, C.c_char_p, C.POINTER(u32), vp, C.POINTER(u64)]),
+    "hps_pdb_put_batch": (i32, [vp, C.c_char_p, vp, vp, vp, u64, C.POINTER(u64)]),
+    "hps_pdb_get_batch": (i32, [vp, C.c_char_p, vp, u64, vp, vp, vp, C.POINTER(u64)]),
+    "hps_pdb_scan": (i32, [vp, C.c_char_p, vp, vp, vp, u64, C.POINTER(u64)]),
+    "hps_pdb_compact": (i32, [vp, C.c_char_p, C.POINTER(u64)]),
+    "hps_crc32c_host": (u32, [u32, vp, C.c_size_t]),
+    "hps_gpu_tiered_create": (i32, [vp, vp, vp, C.c_char_p, u64, C.POINTER(vp)]),
+    "hps_gpu_tiered_destroy": (i32, [vp]),
+    "hps_gpu_tiered_lookup": (i32, [vp, vp, u64, vp, C.POINTER(u64)]),
+    "hps_gpu_tiered_await": (i32, [vp]),
 }
 
 _lib = None
