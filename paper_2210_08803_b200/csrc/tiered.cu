@@ -225,13 +225,11 @@ int hps_gpu_tiered_lookup(hps_gpu_tiered t, const uint64_t* keys, uint64_t n, fl
   HPSG_CUDA(cudaMemcpyAsync(t->d_ukeys, t->h_ukeys, u * 8, cudaMemcpyHostToDevice, st));
   if (int s = hps_gpu_cache_query(t->l1, t->d_ukeys, u, t->d_urows, t->d_found_idx, t->d_missing_idx, t->d_counts))
     return s;
+  // the counts and the whole missing list (its valid prefix is counts[1] long) in one round trip
   HPSG_CUDA(cudaMemcpyAsync(t->h_counts, t->d_counts, 2 * 8, cudaMemcpyDeviceToHost, st));
+  HPSG_CUDA(cudaMemcpyAsync(t->h_missing_idx, t->d_missing_idx, u * 4, cudaMemcpyDeviceToHost, st));
   HPSG_CUDA(cudaStreamSynchronize(st));
   const uint64_t nf = t->h_counts[0], nm = t->h_counts[1];
-  if (nm) {
-    HPSG_CUDA(cudaMemcpyAsync(t->h_missing_idx, t->d_missing_idx, nm * 4, cudaMemcpyDeviceToHost, st));
-    HPSG_CUDA(cudaStreamSynchronize(st));
-  }
   // 3. the misses: L2, then L3, else the default vector
   std::vector<uint8_t> src(u, 0);  // 0 L1, 1 L2, 2 L3, 3 Default
   std::vector<uint32_t> urow(u);

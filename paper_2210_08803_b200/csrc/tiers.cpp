@@ -101,11 +101,13 @@ struct VdbShard {
   std::set<std::pair<uint64_t, uint64_t>> by_version;  // (version, key): EvictOldestVersion
 };
 
-// Workers over `n` independent items (shards): min(n, hardware threads) threads.
+// Workers over `n` independent items (shards): min(n, hardware threads) threads, or the
+// calling thread alone when the batch is small (`work` entries: thread start-up would cost
+// more than the shards' work — a lookup's few misses).
 template <class F>
-void parallel_for(size_t n, F&& f) {
+void parallel_for(size_t n, F&& f, uint64_t work) {
   const size_t hw = std::max<size_t>(1, std::thread::hardware_concurrency());
-  const size_t T = std::min(n, hw);
+  const size_t T = work < 16384 ? 1 : std::min(n, hw);
   if (T <= 1) {
     for (size_t i = 0; i < n; ++i) f(i);
     return;
@@ -202,7 +204,7 @@ int hps_vdb_put_batch(hps_vdb v, const uint64_t* keys, const float* vecs, const 
       sh.by_version.insert({ver, k});
       ++stored[s];
     }
-  });
+  }, n);
   if (stored_out) {
     uint64_t t = 0;
     for (uint64_t x : stored) t += x;
@@ -229,7 +231,7 @@ int hps_vdb_get_batch(hps_vdb v, const uint64_t* keys, uint64_t n, float* vecs_o
       if (vecs_out) std::memcpy(vecs_out + size_t(i) * D, &sh.vecs[size_t(it->second) * D], D * sizeof(float));
       if (versions_out) versions_out[i] = sh.versions[it->second];
     }
-  });
+  }, n);
   if (n_found_out) {
     uint64_t t = 0;
     for (uint64_t x : nf) t += x;
