@@ -58,6 +58,13 @@ struct hps_gpu_cache_s {
   uint64_t* ws_scan = nullptr;
   uint64_t* ws_counts = nullptr;  // [0]=n [1]=U (segments) [2]=found [3]=valid
   size_t sort_words = 0;
+  // the last query's set-sorted access list (cache_insert_after_query derives an insert's
+  // set grouping from it) and that derivation's buffers
+  const uint32_t* q_sets = nullptr;
+  const uint32_t* q_idx = nullptr;
+  uint32_t *ws_der_set = nullptr, *ws_der_idx = nullptr, *ws_der_pos = nullptr;
+  uint32_t* ws_qmiss = nullptr;    // the last query's access -> miss rank (SplitOp)
+  uint64_t* ws_dcounts = nullptr;  // [0] entries of the derived list [1] its set segments
   bool no_small_sort = false;  // HPS_GPU_NO_SMALL_SORT=1: small batches take the multi-kernel sort too (tests)
 };
 
@@ -113,13 +120,16 @@ struct SplitOp {
   uint64_t* counts_out;  // caller's [found, missing]
   uint64_t* counts;      // internal [.., .., found]
   uint64_t* stats;
+  uint32_t* miss_rank;   // access -> its position in missing_idx (UINT32_MAX: a hit)
   __device__ uint64_t size() const { return counts[0]; }
   __device__ uint32_t count(uint64_t i) const { return hit[i] != kMiss ? 1u : 0u; }
   __device__ void emit(uint64_t i, uint64_t excl, uint32_t c) const {
     if (c) {
       found_idx[excl] = static_cast<uint32_t>(i);
+      miss_rank[i] = 0xffffffffu;
     } else {
       missing_idx[i - excl] = static_cast<uint32_t>(i);
+      miss_rank[i] = static_cast<uint32_t>(i - excl);
     }
   }
   __device__ void total(uint64_t f) const {
@@ -919,6 +929,36 @@ int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** set
 
 int set_warps_grid(uint64_t n) { return grid_for(n * 32, 256, kNumSMs * 16); }
 
+// An insert of a query's misses (the read-through's migration) grouped by set WITHOUT a sort:
+// the query's access list is already sorted by (set, query position), and the misses are a
+// subsequence of it whose query positions ascend with their insert positions (the missing
+// list is ascending). Keeping, in list order, the elements that missed and are valid insert
+// entries gives exactly the stable set sort of the insert's valid entries — the segment of
+// skipped entries (absent from the lower tier, non-finite) is simply not there. Element j's
+// insert position is the query's miss rank of its access (SplitOp).
+struct DeriveOp {
+  const uint32_t* q_sets;
+  const uint32_t* q_idx;
+  const uint64_t* q_n;        // the query's access count
+  const uint32_t* miss_rank;  // query access -> insert entry (UINT32_MAX: a hit)
+  const uint8_t* valid;       // per insert entry (k_entry_prep)
+  uint32_t* out_set;
+  uint32_t* out_idx;
+  uint64_t* dcounts;
+  __device__ uint64_t size() const { return *q_n; }
+  __device__ uint32_t count(uint64_t j) const {
+    const uint32_t m = miss_rank[q_idx[j]];
+    return (m != 0xffffffffu && valid[m]) ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t j, uint64_t excl, uint32_t c) const {
+    if (c) {
+      out_set[excl] = q_sets[j];
+      out_idx[excl] = miss_rank[q_idx[j]];
+    }
+  }
+  __device__ void total(uint64_t t) const { dcounts[0] = t; }
+};
+
 }  // namespace
 
 extern "C" {
@@ -975,6 +1015,11 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   A(dalloc(&c->ws_sort, c->sort_words));
   A(dalloc(&c->ws_scan, scan_tiles(n) + 2));
   A(dalloc(&c->ws_counts, 8));
+  A(dalloc(&c->ws_der_set, n));
+  A(dalloc(&c->ws_der_idx, n));
+  A(dalloc(&c->ws_der_pos, n));
+  A(dalloc(&c->ws_qmiss, n));
+  A(dalloc(&c->ws_dcounts, 4));
   if (c->dim != c->dim_io) A(dalloc(&c->ws_io, n * c->dim));
   if (st) {
     hps_gpu_cache_destroy(c);
@@ -998,7 +1043,8 @@ int hps_gpu_cache_destroy(hps_gpu_cache c) {
   if (!c) return HPS_GPU_OK;
   void* ptrs[] = {c->d_keys,    c->d_ver,    c->d_touch,   c->d_freq, c->d_set_acc, c->d_vec,
                   c->d_state,   c->ws_set,   c->ws_keys_b, c->ws_vals_a, c->ws_vals_b, c->ws_hit,
-                  c->ws_rank,   c->ws_seg,   c->ws_sort,   c->ws_scan, c->ws_counts, c->ws_io};
+                  c->ws_rank,   c->ws_seg,   c->ws_sort,   c->ws_scan, c->ws_counts, c->ws_io,
+                  c->ws_der_set, c->ws_der_idx, c->ws_der_pos, c->ws_dcounts, c->ws_qmiss};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1052,7 +1098,7 @@ int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const u
   ph.mark();
   launch_k(true, k_probe, grid_for(n, 256, kNumSMs * 16), 256, 0, st, keys, n, c->set_mod, c->ways, c->d_keys, c->d_freq,
                                                           c->ws_set, c->ws_hit, c->d_state, c->ws_counts, d_n);
-  SplitOp op{c->ws_hit, found_idx, missing_idx, counts, c->ws_counts, c->d_state + kStats};
+  SplitOp op{c->ws_hit, found_idx, missing_idx, counts, c->ws_counts, c->d_state + kStats, c->ws_qmiss};
   HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
   HPSG_CHECK_LAUNCH("cache probe/split");
   ph.mark();
@@ -1079,6 +1125,8 @@ int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const u
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, c->set_bits, &sets_sorted, &idx_sorted)) return s;
+  c->q_sets = sets_sorted;
+  c->q_idx = idx_sorted;
   ph.mark();
   if (c->ways <= 8) {
     auto* n_huge = reinterpret_cast<unsigned long long*>(c->ws_counts + 4);
@@ -1166,6 +1214,66 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
   HPSG_CHECK_LAUNCH("cache insert");
   return HPS_GPU_OK;
 }
+
+}  // extern "C"
+
+namespace hpsg {
+// The read-through's migration: insert its distinct misses (entries [0, *d_count) of keys/vecs,
+// skip[] = absent from the lower tier) right after cache_query of the same call, reusing the
+// query's set-sorted list (DeriveOp) instead of sorting the entries again. Same results as
+// hps_gpu_cache_insert_count on those entries (bulk-load versions).
+int cache_insert_after_query(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n_max,
+                             const uint64_t* d_count, const uint8_t* skip, uint64_t* admitted_out,
+                             const uint64_t* q_n, uint64_t q_n_max) {
+  if (int s = check_cache(c)) return s;
+  if (n_max > c->max_batch || !c->q_sets || !keys || !vecs || !d_count || !q_n)
+    return HPS_GPU_E_INVALID_ARGUMENT;
+  if (n_max == 0) return HPS_GPU_OK;
+  cudaStream_t st = c->ctx->stream;
+  {  // k_entry_prep: validity + the call's admitted count; its set ids go to scratch (the
+     // query's sorted list may live in ws_set)
+    const int lpr = lpr_for(c->dim);
+    const int grid = grid_for(n_max * lpr, 256, kNumSMs * 16);
+    const uint32_t invalid = static_cast<uint32_t>(c->num_sets);
+#define HPSG_P(L) launch_k(true, k_entry_prep<L>, grid, 256, 0, st, keys, vecs, n_max, c->dim, c->set_mod, invalid, c->ws_der_pos, c->ws_hit, c->ctx->d_status, c->ws_counts, d_count, skip, c->f16 ? 1 : 0, admitted_out)
+    switch (lpr) {
+      case 32: HPSG_P(32); break;
+      case 16: HPSG_P(16); break;
+      case 8: HPSG_P(8); break;
+      case 4: HPSG_P(4); break;
+      case 2: HPSG_P(2); break;
+      default: HPSG_P(1); break;
+    }
+#undef HPSG_P
+    HPSG_CHECK_LAUNCH("cache entry prep (after query)");
+  }
+  RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
+  HPSG_CUDA(launch_scan(rop, n_max, c->ws_scan, st));
+  DeriveOp dop{c->q_sets, c->q_idx, q_n, c->ws_qmiss, c->ws_hit, c->ws_der_set, c->ws_der_idx, c->ws_dcounts};
+  HPSG_CUDA(launch_scan(dop, q_n_max, c->ws_scan, st));
+  SetSegOp sop{c->ws_der_set, c->ws_seg, c->ws_dcounts};
+  HPSG_CUDA(launch_scan(sop, n_max, c->ws_scan, st));
+  HPSG_CHECK_LAUNCH("cache derived set grouping");
+  if (c->ways <= 8)
+    launch_k(true, (c->f16 ? k_insert_sets8<true> : k_insert_sets8<false>), grid_for((n_max + 3) / 4 * 32, 256, kNumSMs * 16),
+             256, 0, st, static_cast<const uint32_t*>(c->ws_der_set), static_cast<const uint32_t*>(c->ws_der_idx),
+             static_cast<const uint32_t*>(c->ws_seg), static_cast<const uint64_t*>(c->ws_dcounts), keys, vecs,
+             static_cast<const uint64_t*>(nullptr), static_cast<const uint32_t*>(c->ws_rank), c->ways, c->dim,
+             c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch,
+             c->d_set_acc, c->d_vec, c->d_state, admitted_out);
+  else
+    launch_k(true, (c->f16 ? k_insert_sets<true> : k_insert_sets<false>), set_warps_grid(n_max), 256, 0, st,
+             static_cast<const uint32_t*>(c->ws_der_set), static_cast<const uint32_t*>(c->ws_der_idx),
+             static_cast<const uint32_t*>(c->ws_seg), static_cast<const uint64_t*>(c->ws_dcounts), keys, vecs,
+             static_cast<const uint64_t*>(nullptr), static_cast<const uint32_t*>(c->ws_rank), c->ways, c->dim,
+             c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch,
+             c->d_set_acc, c->d_vec, c->d_state, admitted_out);
+  HPSG_CHECK_LAUNCH("cache insert (after query)");
+  return HPS_GPU_OK;
+}
+}  // namespace hpsg
+
+extern "C" {
 
 int hps_gpu_cache_insert(hps_gpu_cache c, const uint64_t* keys, const float* vecs, const uint64_t* versions, uint64_t n,
                          uint64_t* admitted_out) {

@@ -13,6 +13,8 @@
 //   K14c  expand: out[i] = row of inverse[i], source counts per input key
 //
 // The whole lookup is asynchronous, never allocates and is capturable into a CUDA graph.
+#include <cstdlib>
+
 #include <cub/block/block_scan.cuh>
 
 #include "common.cuh"
@@ -26,6 +28,9 @@ int cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_
                 uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts);
 int cache_info(hps_gpu_cache c, hps_gpu_ctx* ctx, uint32_t* dim);
 uint64_t cache_max_batch(hps_gpu_cache c);
+int cache_insert_after_query(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n_max,
+                             const uint64_t* d_count, const uint8_t* skip, uint64_t* admitted_out,
+                             const uint64_t* q_n, uint64_t q_n_max);
 }  // namespace hpsg
 
 struct hps_gpu_readthrough_s {
@@ -406,10 +411,21 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
   if (int s = table_read_through(r->tbl, r->table, r->ukeys, r->found, r->found_idx, r->missing_idx, r->counts + 2, n,
                                  r->urows, r->miss_keys, r->miss_vecs, r->miss_absent, r->src))
     return s;
-  // K7: migrate the distinct misses present in the table (absent keys are never cached)
-  if (int s = hps_gpu_cache_insert_count(r->cache, r->miss_keys, r->miss_vecs, nullptr, n, r->counts + 3,
-                                         r->miss_absent, r->counts + 4))
+  // K7: migrate the distinct misses present in the table (absent keys are never cached),
+  // grouped by set from the query's own sorted access list (no second sort;
+  // HPS_GPU_RT_SORT=1 sorts them again: A/B)
+  static const bool resort = [] {
+    const char* e = std::getenv("HPS_GPU_RT_SORT");
+    return e && std::atoi(e) == 1;
+  }();
+  if (resort) {
+    if (int s = hps_gpu_cache_insert_count(r->cache, r->miss_keys, r->miss_vecs, nullptr, n, r->counts + 3,
+                                           r->miss_absent, r->counts + 4))
+      return s;
+  } else if (int s = cache_insert_after_query(r->cache, r->miss_keys, r->miss_vecs, n, r->counts + 3, r->miss_absent,
+                                              r->counts + 4, r->counts, n)) {
     return s;
+  }
   // K14c: rows back in input order
   const int lpr = lpr_for(r->dim);
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);

@@ -196,16 +196,19 @@ def oracle_read_through(ocache, truth, default, q, dim):
     return rows[inv], np.bincount(src[inv], minlength=4), len(u)
 
 
-@pytest.mark.parametrize("graphed", [False, True])
-def test_read_through_matches_oracle(ctx, graphed):
+@pytest.mark.parametrize("graphed,cap", [(False, 512), (True, 512), (False, 4096)])
+def test_read_through_matches_oracle(ctx, graphed, cap):
     """Orchestrator lookup (cache + backing table): rows in input order, duplicate keys served
     from one probe per distinct key (so cache stats count distinct keys), distinct misses
     migrated once (absent keys never cached), source counts per input key — bit-exact with
     the oracle cache + a dict table. Batches span the one-CTA dedup (<= 2,048 keys) and the
-    claim-table dedup. graphed: lookup_graphed (one CUDA graph per batch size)."""
+    claim-table dedup. graphed: lookup_graphed (one CUDA graph per batch size). The migration
+    groups its inserts by set from the query's sorted list (cache_insert_after_query): cap 512
+    (64 sets) sorts in one radix pass, cap 4096 (512 sets) in two, which leaves the query's
+    list in the buffers the insert's entry prep would otherwise overwrite."""
     from paper_2210_08803_b200 import EmbeddingTableGroup
     from paper_2210_08803_b200.api import CachedLookup
-    dim, n_keys, cap = 8, 5000, 512
+    dim, n_keys = 8, 5000
     rs = np.random.default_rng(17)
     keys_all = W.mix64(np.arange(n_keys, dtype=np.uint64))
     table = EmbeddingTableGroup(ctx, [n_keys], dim, [0], "sgd", 8192, 8192, 3)
