@@ -158,6 +158,7 @@ class HotCache {
     check(hps_gpu_cache_create(ctx.handle(), &cfg, &h_), "hps_gpu_cache_create");
   }
   ~HotCache() { hps_gpu_cache_destroy(h_); }
+  hps_gpu_cache handle() const { return h_; }  // for C-ABI entries that take the cache (e.g. hps_gpu_tiered_create)
   HotCache(const HotCache&) = delete;
   HotCache& operator=(const HotCache&) = delete;
 

@@ -60,7 +60,8 @@ enum {
   HPS_GPU_E_OUT_OF_MEMORY = 257,
   HPS_GPU_E_NO_DEVICE = 258,
   HPS_GPU_E_NOT_CAPTURABLE = 259,
-  HPS_GPU_E_NCCL = 260             /* an NCCL call of the sharded path failed */
+  HPS_GPU_E_NCCL = 260,            /* an NCCL call of the sharded path failed */
+  HPS_GPU_E_PEER_TIMEOUT = 261     /* peer transport: a peer never signalled its phase (10 s) */
 };
 
 /* Human readable name of a status ("OK", "InvalidArgument", ..., "CudaError"). */

@@ -752,16 +752,27 @@ __global__ void __launch_bounds__(256) k_insert_sets8(const uint32_t* __restrict
     }
     if (gl == 0) set_acc[s] = acc;
   }
-  // counts are per group (every lane of a group counted the same events): lane gl == 0 adds
+  // counts are per group (every lane of a group counted the same events): lane gl == 0 adds;
+  // summed per CTA in shared memory first, so a large batch's thousands of inserting warps
+  // do not serialise on the three global counters
+  __shared__ unsigned long long s_cnt[3];
+  if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0ull;
+  __syncthreads();
   if (gl != 0) n_ins = n_evict = n_refresh = 0;
   n_ins = warp_sum(n_ins);
   n_evict = warp_sum(n_evict);
   n_refresh = warp_sum(n_refresh);
   if (lane == 0 && (n_ins | n_evict | n_refresh)) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sInsertions]), n_ins);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sEvictions]), n_evict);
-    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sRefresh]), n_refresh);
-    if (admitted_out) atomicAdd(reinterpret_cast<unsigned long long*>(admitted_out), n_ins);
+    atomicAdd(&s_cnt[0], static_cast<unsigned long long>(n_ins));
+    atomicAdd(&s_cnt[1], static_cast<unsigned long long>(n_evict));
+    atomicAdd(&s_cnt[2], static_cast<unsigned long long>(n_refresh));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && (s_cnt[0] | s_cnt[1] | s_cnt[2])) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sInsertions]), s_cnt[0]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sEvictions]), s_cnt[1]);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&state[kStats + sRefresh]), s_cnt[2]);
+    if (admitted_out) atomicAdd(reinterpret_cast<unsigned long long*>(admitted_out), s_cnt[0]);
   }
 }
 

@@ -106,6 +106,7 @@ const char* hps_gpu_status_string(int status) {
     case HPS_GPU_E_NO_DEVICE: return "NoDevice";
     case HPS_GPU_E_NOT_CAPTURABLE: return "NotCapturable";
     case HPS_GPU_E_NCCL: return "Nccl";
+    case HPS_GPU_E_PEER_TIMEOUT: return "PeerTimeout";
     default: return "Unknown";
   }
 }

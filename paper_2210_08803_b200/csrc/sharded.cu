@@ -210,15 +210,28 @@ __global__ void k_signal(PeerTab pt, uint32_t which, uint32_t G, uint32_t rank, 
   }
 }
 
-// Wait until every peer signalled phase `which` of this step (a single CTA spins).
-__global__ void k_wait(const uint64_t* flags, uint32_t which, uint32_t G, const uint64_t* d_epoch) {
+// Wait until every peer signalled phase `which` of this step (a single CTA spins), for at most
+// kPeerWaitNs: a peer that never arrives (it failed, or was never launched) latches
+// HPS_GPU_E_PEER_TIMEOUT instead of hanging the device (the step's results are then unspecified).
+constexpr uint64_t kPeerWaitNs = 10ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__global__ void k_wait(const uint64_t* flags, uint32_t which, uint32_t G, const uint64_t* d_epoch, uint32_t* status) {
   const uint64_t e = *d_epoch;
+  const uint64_t t0 = global_ns();
   for (uint32_t p = threadIdx.x; p < G; p += blockDim.x) {
     const uint64_t* f = flags + uint64_t(which) * G + p;
     uint64_t v;
     while (true) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(f) : "memory");
       if (v >= e) break;
+      if (global_ns() - t0 > kPeerWaitNs) {
+        latch_status(status, HPS_GPU_E_PEER_TIMEOUT);
+        break;
+      }
       __nanosleep(200);
     }
   }
@@ -369,6 +382,31 @@ __global__ void __launch_bounds__(256) k_fetch_unique_peer(PeerTab pt, uint32_t 
   }
 }
 
+// The requester's pooling over its local rows_back (after the unique-row fetch): bags in
+// occurrence order, sequential float4 sums, then the mean's divide — the same arithmetic as
+// exchange.cu's k_pool_rows (bit-identical), in this module so the peer step never loads a
+// kernel lazily while a peer's wait kernel spins.
+template <int LPR>
+__global__ void __launch_bounds__(256) k_pool_local(const float* __restrict__ rows, const uint32_t* __restrict__ perm,
+                                                    const uint32_t* __restrict__ offsets, uint64_t n_bags, uint32_t dim,
+                                                    int mean, float* __restrict__ out) {
+  constexpr int G = 32 / LPR;
+  const uint32_t lane = lane_id(), grp = lane / LPR, gl = lane % LPR, nvec = dim / 4;
+  const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
+  const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
+  for (uint64_t b = gid; b < n_bags; b += ng) {
+    const uint32_t lo = offsets ? offsets[b] : static_cast<uint32_t>(b);
+    const uint32_t hi = offsets ? offsets[b + 1] : static_cast<uint32_t>(b + 1);
+    float4* o = reinterpret_cast<float4*>(out + b * dim);
+    for (uint32_t v = gl; v < nvec; v += LPR) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (uint32_t i = lo; i < hi; ++i) acc = f4_add(acc, reinterpret_cast<const float4*>(rows + uint64_t(perm[i]) * dim)[v]);
+      if (mean && hi > lo) acc = f4_div(acc, static_cast<float>(hi - lo));
+      o[v] = acc;
+    }
+  }
+}
+
 int lpr_of(uint32_t dim) {
   const uint32_t nvec = dim / 4;
   return nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
@@ -469,7 +507,7 @@ int dist_forward_peer(hps_gpu_dist d, const uint32_t* offsets, uint64_t n_bags, 
       d->dense_keys, d->dense_tables, d->dense_perm, d->counts, d->G, d->rank, d->C, n, *d->peer, d->perm,
       d->ctx->d_status);
   k_signal<<<1, 64, 0, st>>>(*d->peer, 0, d->G, d->rank, d->d_epoch);
-  k_wait<<<1, 64, 0, st>>>(d->flags, 0, d->G, d->d_epoch);
+  k_wait<<<1, 64, 0, st>>>(d->flags, 0, d->G, d->d_epoch, d->ctx->d_status);
   HPSG_CHECK_LAUNCH("dist regions (peer)");
   const uint32_t gflags = (flags & HPS_LOOKUP_TRAIN) | (flags & HPS_LOOKUP_INSERT);
   if (int s = hps_gpu_gather_rows(d->shard, d->recv_keys, d->recv_tables, GC, d->rows_own, gflags)) return s;
@@ -482,16 +520,15 @@ int dist_forward_peer(hps_gpu_dist d, const uint32_t* offsets, uint64_t n_bags, 
     HPSG_CHECK_LAUNCH("dist leader map (peer)");
   }
   k_signal<<<1, 64, 0, st>>>(*d->peer, 1, d->G, d->rank, d->d_epoch);
-  k_wait<<<1, 64, 0, st>>>(d->flags, 1, d->G, d->d_epoch);
+  k_wait<<<1, 64, 0, st>>>(d->flags, 1, d->G, d->d_epoch, d->ctx->d_status);
   const int lpr = lpr_of(d->dim);
   if (d->G > 1) {
     HPSG_LPR_DISPATCH(k_fetch_unique_peer, lpr, grid_for(n * lpr, 256, kNumSMs * 32), st, *d->peer, d->rank, d->C,
                       d->perm, n, d->dim, d->rows_back, d->perm_u);
     HPSG_CHECK_LAUNCH("dist unique-row fetch (peer)");
   }
-  if (int s = hps_gpu_pool_rows(d->ctx, d->rows_back, d->G > 1 ? d->perm_u : d->perm, offsets, n_bags, d->dim, combiner,
-                                out))
-    return s;
+  HPSG_LPR_DISPATCH(k_pool_local, lpr, grid_for(n_bags * lpr, 256, kNumSMs * 32), st, d->rows_back,
+                    d->G > 1 ? d->perm_u : d->perm, offsets, n_bags, d->dim, combiner == HPS_COMBINER_MEAN, out);
   HPSG_CHECK_LAUNCH("dist pool (peer)");
   d->last_offsets = offsets;
   d->last_bags = n_bags;
@@ -542,7 +579,10 @@ int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
                           reinterpret_cast<const void*>(k_fetch_unique_peer<8>),
                           reinterpret_cast<const void*>(k_fetch_unique_peer<4>),
                           reinterpret_cast<const void*>(k_fetch_unique_peer<2>),
-                          reinterpret_cast<const void*>(k_fetch_unique_peer<1>)})
+                          reinterpret_cast<const void*>(k_fetch_unique_peer<1>),
+                          reinterpret_cast<const void*>(k_pool_local<32>), reinterpret_cast<const void*>(k_pool_local<16>),
+                          reinterpret_cast<const void*>(k_pool_local<8>), reinterpret_cast<const void*>(k_pool_local<4>),
+                          reinterpret_cast<const void*>(k_pool_local<2>), reinterpret_cast<const void*>(k_pool_local<1>)})
       HPSG_CUDA(cudaFuncGetAttributes(&fa, f));
   }
   if (!d->peer) d->peer = new PeerTab{};
@@ -799,7 +839,7 @@ int hps_gpu_dist_backward(hps_gpu_dist d, const float* d_out, const hps_opt_para
                       d->rank, d->C, d_out, d->perm, d->last_offsets, d->last_bags, d->dim,
                       d->last_combiner == HPS_COMBINER_MEAN);
     k_signal<<<1, 64, 0, st>>>(*d->peer, 2, d->G, d->rank, d->d_epoch);
-    k_wait<<<1, 64, 0, st>>>(d->flags, 2, d->G, d->d_epoch);
+    k_wait<<<1, 64, 0, st>>>(d->flags, 2, d->G, d->d_epoch, d->ctx->d_status);
     HPSG_CHECK_LAUNCH("dist backward (peer)");
     if (int s = hps_gpu_backward_update(d->shard, d->grads_recv, opt)) return s;
     d->have_fwd = false;

@@ -605,23 +605,36 @@ int hps_pdb_get_batch(hps_pdb db, const char* table, const uint64_t* keys, uint6
   if (n && (!keys || !found_out)) return HPS_GPU_E_INVALID_ARGUMENT;
   std::shared_lock<std::shared_mutex> lk(t->mu);
   const uint64_t D = t->dim;
-  uint64_t nf = 0;
-  for (uint64_t i = 0; i < n; ++i) {
-    auto it = t->index.find(keys[i]);
-    found_out[i] = it != t->index.end();
-    if (!found_out[i]) continue;
-    ++nf;
-    if (versions_out) versions_out[i] = it->second.version;
-    if (vecs_out) {
-      const PdbSeg& s = t->segs[it->second.seg];
-      const ssize_t r = ::pread(s.fd, vecs_out + i * D, 4 * D, static_cast<off_t>(it->second.off + kRecHead));
-      if (r != static_cast<ssize_t>(4 * D)) {
-        set_last_error("pdb: short read in " + t->dir);
-        return HPS_GPU_E_IO;
+  // key chunks on parallel host threads for large batches (index reads + one pread per key;
+  // the segments are usually in the page cache, so the syscalls, not the device, bound it)
+  constexpr uint64_t kChunkKeys = 512;
+  const uint64_t chunks = (n + kChunkKeys - 1) / kChunkKeys;
+  std::vector<uint64_t> nf(chunks, 0);
+  std::vector<uint8_t> bad(chunks, 0);
+  parallel_for(chunks, [&](size_t c) {
+    for (uint64_t i = c * kChunkKeys; i < std::min(n, (c + 1) * kChunkKeys); ++i) {
+      auto it = t->index.find(keys[i]);
+      found_out[i] = it != t->index.end();
+      if (!found_out[i]) continue;
+      ++nf[c];
+      if (versions_out) versions_out[i] = it->second.version;
+      if (vecs_out) {
+        const PdbSeg& s = t->segs[it->second.seg];
+        const ssize_t r = ::pread(s.fd, vecs_out + i * D, 4 * D, static_cast<off_t>(it->second.off + kRecHead));
+        if (r != static_cast<ssize_t>(4 * D)) bad[c] = 1;
       }
     }
+  }, n >= 2048 ? uint64_t(1) << 20 : 0);
+  for (uint8_t b : bad)
+    if (b) {
+      set_last_error("pdb: short read in " + t->dir);
+      return HPS_GPU_E_IO;
+    }
+  if (n_found_out) {
+    uint64_t tot = 0;
+    for (uint64_t x : nf) tot += x;
+    *n_found_out = tot;
   }
-  if (n_found_out) *n_found_out = nf;
   return HPS_GPU_OK;
 }
 
