@@ -623,6 +623,33 @@ int hps_gpu_dist_set_transport(hps_gpu_dist d, int transport) {
       t.lead[p] = static_cast<uint32_t*>(ptr[5]);
     }
   }
+  // ... and launch each of them once with no work: the module code is then resident whatever
+  // the runtime's lazy-loading policy (loopback ranks share one device, where a load that
+  // waits for the device while a peer's k_wait spins would deadlock the step)
+  {
+    cudaStream_t st = d->ctx->stream;
+    uint64_t* scratch = nullptr;
+    HPSG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(uint64_t), st));
+    HPSG_CUDA(cudaMemsetAsync(scratch, 0, sizeof(uint64_t), st));
+    k_epoch_bump<<<1, 32, 0, st>>>(scratch);
+    k_fix_regions_peer<<<1, 32, 0, st>>>(d->dense_keys, d->dense_tables, d->dense_perm, d->counts, 0, d->rank, d->C, 0,
+                                         t, d->perm, d->ctx->d_status);
+    k_signal<<<1, 32, 0, st>>>(t, 0, 0, d->rank, scratch);
+    k_wait<<<1, 32, 0, st>>>(d->flags, 0, 0, scratch, d->ctx->d_status);
+    k_lead_claim<<<1, 32, 0, st>>>(d->recv_keys, d->recv_tables, 0, d->C, d->lead_ht, d->lead_mask, d->lead_ent, d->lead);
+    k_lead_resolve<<<1, 32, 0, st>>>(d->lead_ht, 0, d->lead_ent, d->lead);
+    k_lead_reset<<<1, 32, 0, st>>>(d->lead_ht, 0, d->lead_ent, d->lead, d->d_served);
+#define HPSG_WARM(L)                                                                                           \
+  k_pool_rows_peer<L><<<1, 32, 0, st>>>(t, d->rank, d->C, d->perm, nullptr, 0, d->dim, 0, d->rows_back);     \
+  k_scatter_grads_peer<L><<<1, 32, 0, st>>>(t, d->rank, d->C, d->grads_send, d->perm, nullptr, 0, d->dim, 0); \
+  k_fetch_unique_peer<L><<<1, 32, 0, st>>>(t, d->rank, d->C, d->perm, 0, d->dim, d->rows_back, d->perm_u);     \
+  k_pool_local<L><<<1, 32, 0, st>>>(d->rows_back, d->perm, nullptr, 0, d->dim, 0, d->rows_back);
+    HPSG_WARM(32) HPSG_WARM(16) HPSG_WARM(8) HPSG_WARM(4) HPSG_WARM(2) HPSG_WARM(1)
+#undef HPSG_WARM
+    HPSG_CHECK_LAUNCH("peer kernels warm-up");
+    HPSG_CUDA(cudaFreeAsync(scratch, st));
+    HPSG_CUDA(cudaStreamSynchronize(st));
+  }
   d->transport = HPS_DIST_PEER;
   return HPS_GPU_OK;
 }
