@@ -64,6 +64,10 @@ struct hps_gpu_cache_s {
   const uint32_t* q_idx = nullptr;
   uint32_t *ws_der_set = nullptr, *ws_der_idx = nullptr, *ws_der_pos = nullptr;
   uint32_t* ws_qmiss = nullptr;    // the last query's access -> miss rank (SplitOp)
+  uint32_t* ws_setcnt = nullptr;   // counting grouping: per-set counters [num_sets + 1], zero at rest
+  uint32_t* ws_ticket = nullptr;   // counting grouping: arrival rank of each access in its set
+  bool count_group = false;        // distinct-key queries group by set with counters (no radix sort)
+  bool query_distinct = false;     // the next cache_query's keys are distinct (the read-through sets it)
   uint64_t* ws_dcounts = nullptr;  // [0] entries of the derived list [1] its set segments
   bool no_small_sort = false;  // HPS_GPU_NO_SMALL_SORT=1: small batches take the multi-kernel sort too (tests)
 };
@@ -914,10 +918,95 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_small_sort_segment(const 
   }
 }
 
+// ---- counting grouping (large caches: sets >= 8 x max_batch) -----------------------------
+// The same products as the radix sort — every set's accesses contiguous, in input order —
+// from per-set counters instead of 3 digit passes: an arrival ticket per access, each set's
+// first arrival reserves the set's range (a scan over the accesses), every access lands at
+// range + ticket, and one thread per range puts it back into input order (insertion sort: a
+// range holds ~1 access when the sets outnumber the batch 8:1) and zeroes the counter.
+// Segments come out in the order of their first-arriving access, not by set id: every
+// consumer treats segments independently.
+__global__ void __launch_bounds__(256) k_group_count(const uint32_t* __restrict__ sets, const uint64_t* counts,
+                                                     uint32_t* cnt, uint32_t* __restrict__ ticket) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t n = counts[0];
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+    ticket[i] = atomicAdd(&cnt[sets[i]], 1u);
+}
+struct GroupAllocOp {
+  const uint32_t* sets;
+  const uint32_t* ticket;
+  uint32_t* cnt;  // count in, the range's start out (its first arrival is its only writer)
+  const uint64_t* counts;
+  __device__ uint64_t size() const { return counts[0]; }
+  __device__ uint32_t count(uint64_t i) const { return ticket[i] == 0 ? cnt[sets[i]] : 0u; }
+  __device__ void emit(uint64_t i, uint64_t excl, uint32_t c) const {
+    if (c) cnt[sets[i]] = static_cast<uint32_t>(excl);
+  }
+  __device__ void total(uint64_t) const {}
+};
+__global__ void __launch_bounds__(256) k_group_place(const uint32_t* __restrict__ sets, const uint32_t* __restrict__ ticket,
+                                                     const uint32_t* __restrict__ cnt, const uint64_t* counts,
+                                                     uint32_t* __restrict__ out_set, uint32_t* __restrict__ out_idx) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t n = counts[0];
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = sets[i];
+    const uint32_t pos = cnt[s] + ticket[i];
+    out_set[pos] = s;
+    out_idx[pos] = static_cast<uint32_t>(i);
+  }
+}
+__global__ void __launch_bounds__(256) k_group_fix(const uint32_t* __restrict__ out_set, uint32_t* out_idx,
+                                                   const uint64_t* counts, uint32_t* cnt) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t n = counts[0];
+  for (uint64_t j = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; j < n; j += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = out_set[j];
+    if (j > 0 && out_set[j - 1] == s) continue;  // not the range's head
+    uint64_t L = 1;
+    while (j + L < n && out_set[j + L] == s) ++L;
+    for (uint64_t a = j + 1; a < j + L; ++a) {  // input order (insertion sort)
+      const uint32_t v = out_idx[a];
+      uint64_t b = a;
+      while (b > j && out_idx[b - 1] > v) {
+        out_idx[b] = out_idx[b - 1];
+        --b;
+      }
+      out_idx[b] = v;
+    }
+    cnt[s] = 0u;  // the counter is zero at rest again
+  }
+}
+
 // Stable sort of (set id, input index) + set segments. Sizes come from c->ws_counts[0].
 int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** sets_sorted,
-                     const uint32_t** idx_sorted) {
+                     const uint32_t** idx_sorted, bool distinct = false) {
   cudaStream_t st = c->ctx->stream;
+  // only for distinct keys (the read-through's deduplicated query): a range then holds the
+  // distinct keys of one set, ~1 when the sets outnumber the batch 8:1; repeated keys (the
+  // public query/insert/refresh entries) could pile thousands into one range — radix sort there
+  if (c->count_group && distinct && n > kSmallSort) {
+    const int g = grid_for(n, 256, kNumSMs * 8);
+    HPSG_CUDA(launch_k(true, k_group_count, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_set),
+                       static_cast<const uint64_t*>(c->ws_counts), c->ws_setcnt, c->ws_ticket));
+    GroupAllocOp aop{c->ws_set, c->ws_ticket, c->ws_setcnt, c->ws_counts};
+    HPSG_CUDA(launch_scan(aop, n, c->ws_scan, st));
+    HPSG_CUDA(launch_k(true, k_group_place, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_set),
+                       static_cast<const uint32_t*>(c->ws_ticket), static_cast<const uint32_t*>(c->ws_setcnt),
+                       static_cast<const uint64_t*>(c->ws_counts), c->ws_keys_b, c->ws_vals_b));
+    HPSG_CUDA(launch_k(true, k_group_fix, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_keys_b), c->ws_vals_b,
+                       static_cast<const uint64_t*>(c->ws_counts), c->ws_setcnt));
+    *sets_sorted = c->ws_keys_b;
+    *idx_sorted = c->ws_vals_b;
+    SetSegOp op{*sets_sorted, c->ws_seg, c->ws_counts};
+    HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
+    HPSG_CHECK_LAUNCH("counting set grouping");
+    return HPS_GPU_OK;
+  }
   if (n <= kSmallSort && !c->no_small_sort) {
     launch_k(true, k_small_sort_segment, 1, kSmallSortThreads, 0, st, c->ws_set, c->ws_counts, bits, c->ws_keys_b, c->ws_vals_b,
                                                           c->ws_seg);
@@ -1030,6 +1119,15 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   A(dalloc(&c->ws_der_idx, n));
   A(dalloc(&c->ws_der_pos, n));
   A(dalloc(&c->ws_qmiss, n));
+  {  // the counting grouping pays off when sets outnumber a batch (segments of ~1 access)
+    const char* e = std::getenv("HPS_GPU_COUNT_GROUP");
+    c->count_group = e ? std::atoi(e) == 1 : c->num_sets >= 8 * n;
+    if (c->count_group) {
+      A(dalloc(&c->ws_setcnt, c->num_sets + 1));
+      A(dalloc(&c->ws_ticket, n));
+      if (!st && cudaMemset(c->ws_setcnt, 0, (c->num_sets + 1) * sizeof(uint32_t)) != cudaSuccess) st = HPS_GPU_E_CUDA;
+    }
+  }
   A(dalloc(&c->ws_dcounts, 4));
   if (c->dim != c->dim_io) A(dalloc(&c->ws_io, n * c->dim));
   if (st) {
@@ -1055,7 +1153,8 @@ int hps_gpu_cache_destroy(hps_gpu_cache c) {
   void* ptrs[] = {c->d_keys,    c->d_ver,    c->d_touch,   c->d_freq, c->d_set_acc, c->d_vec,
                   c->d_state,   c->ws_set,   c->ws_keys_b, c->ws_vals_a, c->ws_vals_b, c->ws_hit,
                   c->ws_rank,   c->ws_seg,   c->ws_sort,   c->ws_scan, c->ws_counts, c->ws_io,
-                  c->ws_der_set, c->ws_der_idx, c->ws_der_pos, c->ws_dcounts, c->ws_qmiss};
+                  c->ws_der_set, c->ws_der_idx, c->ws_der_pos, c->ws_dcounts, c->ws_qmiss, c->ws_setcnt,
+                  c->ws_ticket};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1097,6 +1196,8 @@ struct QueryPhases {
 int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_t* d_n, float* found_vecs,
                       uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts) {
   if (int s = check_cache(c)) return s;
+  const bool distinct = c->query_distinct;  // (set by the read-through for this call only)
+  c->query_distinct = false;
   if (!found_idx || !missing_idx || !counts) return HPS_GPU_E_INVALID_ARGUMENT;
   if (n > c->max_batch) return HPS_GPU_E_INVALID_ARGUMENT;
   cudaStream_t st = c->ctx->stream;
@@ -1135,7 +1236,7 @@ int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const u
   ph.mark();
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
-  if (int s = sort_and_segment(c, n, c->set_bits, &sets_sorted, &idx_sorted)) return s;
+  if (int s = sort_and_segment(c, n, c->set_bits, &sets_sorted, &idx_sorted, distinct)) return s;
   c->q_sets = sets_sorted;
   c->q_idx = idx_sorted;
   ph.mark();
@@ -1229,6 +1330,9 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
 }  // extern "C"
 
 namespace hpsg {
+void cache_mark_distinct_query(hps_gpu_cache c) {
+  if (c) c->query_distinct = true;
+}
 // The read-through's migration: insert its distinct misses (entries [0, *d_count) of keys/vecs,
 // skip[] = absent from the lower tier) right after cache_query of the same call, reusing the
 // query's set-sorted list (DeriveOp) instead of sorting the entries again. Same results as

@@ -28,6 +28,7 @@ int cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_
                 uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts);
 int cache_info(hps_gpu_cache c, hps_gpu_ctx* ctx, uint32_t* dim);
 uint64_t cache_max_batch(hps_gpu_cache c);
+void cache_mark_distinct_query(hps_gpu_cache c);
 int cache_insert_after_query(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n_max,
                              const uint64_t* d_count, const uint8_t* skip, uint64_t* admitted_out,
                              const uint64_t* q_n, uint64_t q_n_max);
@@ -405,6 +406,7 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
   HPSG_CHECK_LAUNCH("readthrough dedup");
   if (n_unique_out) HPSG_CUDA(cudaMemcpyAsync(n_unique_out, r->counts, 8, cudaMemcpyDeviceToDevice, st));
   // K6 on the distinct keys (one access per distinct key: SPEC.md:340)
+  cache_mark_distinct_query(r->cache);  // its keys are distinct: counting set grouping allowed
   if (int s = cache_query(r->cache, r->ukeys, n, r->counts, r->found, r->found_idx, r->missing_idx, r->counts + 2))
     return s;
   // K14b: hits / table rows / default vector per distinct key, distinct misses listed

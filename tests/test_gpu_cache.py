@@ -196,8 +196,9 @@ def oracle_read_through(ocache, truth, default, q, dim):
     return rows[inv], np.bincount(src[inv], minlength=4), len(u)
 
 
-@pytest.mark.parametrize("graphed,cap", [(False, 512), (True, 512), (False, 4096)])
-def test_read_through_matches_oracle(ctx, graphed, cap):
+@pytest.mark.parametrize("graphed,cap,group", [(False, 512, None), (True, 512, None), (False, 4096, None),
+                                               (False, 4096, "1"), (True, 4096, "1")])
+def test_read_through_matches_oracle(ctx, graphed, cap, group, monkeypatch):
     """Orchestrator lookup (cache + backing table): rows in input order, duplicate keys served
     from one probe per distinct key (so cache stats count distinct keys), distinct misses
     migrated once (absent keys never cached), source counts per input key — bit-exact with
@@ -205,7 +206,11 @@ def test_read_through_matches_oracle(ctx, graphed, cap):
     claim-table dedup. graphed: lookup_graphed (one CUDA graph per batch size). The migration
     groups its inserts by set from the query's sorted list (cache_insert_after_query): cap 512
     (64 sets) sorts in one radix pass, cap 4096 (512 sets) in two, which leaves the query's
-    list in the buffers the insert's entry prep would otherwise overwrite."""
+    list in the buffers the insert's entry prep would otherwise overwrite. group="1": the
+    query groups its distinct keys by set with counters instead of the radix sort (the
+    default only when sets >= 8 x max_batch; forced here, so ranges hold several keys)."""
+    if group is not None:
+        monkeypatch.setenv("HPS_GPU_COUNT_GROUP", group)
     from paper_2210_08803_b200 import EmbeddingTableGroup
     from paper_2210_08803_b200.api import CachedLookup
     dim, n_keys = 8, 5000
