@@ -4,8 +4,8 @@
 //
 //   K14a  dedup      distinct keys in order of first occurrence + the inverse map
 //                    (one CTA in shared memory up to kSmallDedup keys; above it an
-//                    open-addressing claim table of u32 owners in HBM/L2, a first-occurrence
-//                    scan and an inverse pass)
+//                    open-addressing claim table of u32 owners in HBM/L2 and a first-occurrence
+//                    scan; the inverse is resolved by the expand)
 //   K6    cache query of the distinct keys (count on the device)
 //   K14b  read-through: hits from the cache, misses from the table (default vector when
 //                    absent), the source tier of each distinct key
@@ -196,24 +196,19 @@ struct FirstOp {
   __device__ void total(uint64_t t) const { counts[0] = t; }
 };
 
-// pass 3: the inverse map (the claim table is reset by a memset node sized by the batch
-// right after: this kernel is its last reader).
-__global__ void __launch_bounds__(256) k_dedup_inverse(const uint32_t* __restrict__ claim,
-                                                       const uint32_t* __restrict__ slot_of,
-                                                       const uint32_t* __restrict__ uid_at, uint64_t n,
-                                                       uint32_t* __restrict__ inverse) {
-  pdl_wait();
-  pdl_launch_dependents();
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-    inverse[i] = uid_at[claim[slot_of[i]]];
-}
+// pass 3, the inverse map inverse[i] = uid_at[claim[slot_of[i]]], is resolved inside k_expand
+// (the claim table's last reader; a memset node after it empties the table for the next call).
 
 // K14c: out[i] = urows[inverse[i]] (LPR lanes per row, 128-bit), per-key source counts
 // (warp-aggregated atomics into source_counts[0..3]).
 template <int LPR>
+// (claim != nullptr: the large-batch dedup's inverse is resolved here — uid_at[claim[slot_of[i]]]
+// — instead of by a separate pass; the claim table is reset after this kernel)
 __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ urows, const uint32_t* __restrict__ inverse,
                                                 const uint8_t* __restrict__ src, uint64_t n, uint32_t dim,
-                                                float* __restrict__ out, unsigned long long* source_counts) {
+                                                float* __restrict__ out, unsigned long long* source_counts,
+                                                const uint32_t* __restrict__ claim, const uint32_t* __restrict__ slot_of,
+                                                const uint32_t* __restrict__ uid_at) {
   pdl_wait();
   pdl_launch_dependents();
   constexpr int G = 32 / LPR;
@@ -229,7 +224,7 @@ __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ urows,
 #pragma unroll
     for (int q = 0; q < G; ++q) {
       const uint64_t i = i0 + q * 32 + lane;
-      my_u[q] = i < n ? inverse[i] : 0u;
+      my_u[q] = i < n ? (claim ? uid_at[claim[slot_of[i]]] : inverse[i]) : 0u;
       if (i < n && source_counts) {
         const uint8_t sv = src[my_u[q]];
         c0 += sv == 0;
@@ -398,11 +393,9 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
                        r->slot_of, source_counts_out));
     FirstOp op{keys, r->claim, r->slot_of, n, r->ukeys, r->uid_at, r->counts};
     HPSG_CUDA(launch_scan(op, n, r->scan, st));
-    HPSG_CUDA(launch_k(pdl, k_dedup_inverse, grid_for(n, 256, kNumSMs * 8), 256, 0, st,
-                       static_cast<const uint32_t*>(r->claim), static_cast<const uint32_t*>(r->slot_of),
-                       static_cast<const uint32_t*>(r->uid_at), n, r->inverse));
-    HPSG_CUDA(cudaMemsetAsync(r->claim, 0xff, cap * sizeof(uint32_t), st));  // empty again for the next call
+    // (the inverse map is resolved by k_expand, the claim table's last reader)
   }
+  const bool fused_inverse = n > kSmallDedup;
   HPSG_CHECK_LAUNCH("readthrough dedup");
   if (n_unique_out) HPSG_CUDA(cudaMemcpyAsync(n_unique_out, r->counts, 8, cudaMemcpyDeviceToDevice, st));
   // K6 on the distinct keys (one access per distinct key: SPEC.md:340)
@@ -432,8 +425,10 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
   const int lpr = lpr_for(r->dim);
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
   auto* sc = reinterpret_cast<unsigned long long*>(source_counts_out);
+  const uint32_t* e_claim = fused_inverse ? r->claim : nullptr;
 #define HPSG_E(L) launch_k(pdl, k_expand<L>, grid, 256, 0, st, static_cast<const float*>(r->urows), \
-                           static_cast<const uint32_t*>(r->inverse), static_cast<const uint8_t*>(r->src), n, r->dim, out, sc)
+                           static_cast<const uint32_t*>(r->inverse), static_cast<const uint8_t*>(r->src), n, r->dim, out, sc, \
+                           e_claim, static_cast<const uint32_t*>(r->slot_of), static_cast<const uint32_t*>(r->uid_at))
   cudaError_t e;
   switch (lpr) {
     case 32: e = HPSG_E(32); break;
@@ -446,6 +441,8 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
 #undef HPSG_E
   HPSG_CUDA(e);
   HPSG_CHECK_LAUNCH("readthrough expand");
+  if (fused_inverse)  // the claim table empty again for the next call (k_expand read it last)
+    HPSG_CUDA(cudaMemsetAsync(r->claim, 0xff, claim_cap_for(n) * sizeof(uint32_t), st));
   return HPS_GPU_OK;
 }
 
