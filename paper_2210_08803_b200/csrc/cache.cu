@@ -33,7 +33,7 @@ using namespace hpsg;
 
 namespace hpsg {
 int cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_t* d_n, float* found_vecs,
-                uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts);
+                uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts, bool scatter_found = false);
 }
 
 struct hps_gpu_cache_s {
@@ -165,7 +165,7 @@ template <int LPR, bool F16>
 __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ found_idx, const uint64_t* counts,
                                                 const uint32_t* __restrict__ set_of, const uint8_t* __restrict__ hit,
                                                 uint32_t ways, const void* __restrict__ vec, uint32_t dim,
-                                                float* __restrict__ out) {
+                                                float* __restrict__ out, int scatter) {
   pdl_wait();
   pdl_launch_dependents();
   constexpr int G = 32 / LPR;
@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ fou
   for (uint64_t j = gid; j < nf; j += ng) {
     const uint32_t i = found_idx[j];
     const uint64_t e = uint64_t(set_of[i]) * ways + hit[i];
-    float4* dst = reinterpret_cast<float4*>(out + j * dim);
+    // scatter: the row lands at its access position (out[i]) instead of compacted (out[j])
+    float4* dst = reinterpret_cast<float4*>(out + uint64_t(scatter ? i : static_cast<uint32_t>(j)) * dim);
     for (uint32_t v = gl; v < nvec; v += LPR) dst[v] = load_cached4<F16>(vec, e, dim, v);
   }
 }
@@ -1194,7 +1195,7 @@ struct QueryPhases {
 
 // n: the key count, or (d_n != nullptr) its bound with the count on the device.
 int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_t* d_n, float* found_vecs,
-                      uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts) {
+                      uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts, bool scatter_found) {
   if (int s = check_cache(c)) return s;
   const bool distinct = c->query_distinct;  // (set by the read-through for this call only)
   c->query_distinct = false;
@@ -1219,9 +1220,9 @@ int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const u
     const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
 #define HPSG_G(L)                                                                                                   \
   (c->f16 ? launch_k(true, k_gather<L, true>, grid, 256, 0, st, found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec, \
-                                                     c->dim, found_vecs)                                              \
+                                                     c->dim, found_vecs, scatter_found ? 1 : 0)                                              \
           : launch_k(true, k_gather<L, false>, grid, 256, 0, st, found_idx, c->ws_counts, c->ws_set, c->ws_hit, c->ways, c->d_vec,\
-                                                      c->dim, found_vecs))
+                                                      c->dim, found_vecs, scatter_found ? 1 : 0))
     switch (lpr) {
       case 32: HPSG_G(32); break;
       case 16: HPSG_G(16); break;

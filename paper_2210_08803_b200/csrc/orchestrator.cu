@@ -25,7 +25,7 @@ using namespace hpsg;
 
 namespace hpsg {
 int cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_t* d_n, float* found_vecs,
-                uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts);
+                uint32_t* found_idx, uint32_t* missing_idx, uint64_t* counts, bool scatter_found);
 int cache_info(hps_gpu_cache c, hps_gpu_ctx* ctx, uint32_t* dim);
 uint64_t cache_max_batch(hps_gpu_cache c);
 void cache_mark_distinct_query(hps_gpu_cache c);
@@ -400,11 +400,13 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
   if (n_unique_out) HPSG_CUDA(cudaMemcpyAsync(n_unique_out, r->counts, 8, cudaMemcpyDeviceToDevice, st));
   // K6 on the distinct keys (one access per distinct key: SPEC.md:340)
   cache_mark_distinct_query(r->cache);  // its keys are distinct: counting set grouping allowed
-  if (int s = cache_query(r->cache, r->ukeys, n, r->counts, r->found, r->found_idx, r->missing_idx, r->counts + 2))
+  // (the hits' rows go straight to urows[distinct id]: no compacted copy to move again)
+  if (int s = cache_query(r->cache, r->ukeys, n, r->counts, r->urows, r->found_idx, r->missing_idx, r->counts + 2,
+                          /*scatter_found=*/true))
     return s;
-  // K14b: hits / table rows / default vector per distinct key, distinct misses listed
-  if (int s = table_read_through(r->tbl, r->table, r->ukeys, r->found, r->found_idx, r->missing_idx, r->counts + 2, n,
-                                 r->urows, r->miss_keys, r->miss_vecs, r->miss_absent, r->src))
+  // K14b: table rows / default vector per distinct miss (hits already in place), misses listed
+  if (int s = table_read_through(r->tbl, r->table, r->ukeys, nullptr, r->found_idx, r->missing_idx, r->counts + 2, n,
+                                 r->urows, r->miss_keys, r->miss_vecs, r->miss_absent, r->src, /*hits_in_place=*/true))
     return s;
   // K7: migrate the distinct misses present in the table (absent keys are never cached),
   // grouped by set from the query's own sorted access list (no second sort;

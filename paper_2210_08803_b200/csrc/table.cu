@@ -633,8 +633,9 @@ __global__ void __launch_bounds__(256) k_read_through(const uint64_t* __restrict
     uint32_t i;
     if (j < nf) {
       i = found_idx[j];
-      src = reinterpret_cast<const float4*>(found_vecs + j * dim);
       if (src_out && gl == 0) src_out[i] = kSrcCache;
+      if (!found_vecs) continue;  // the hit's row is in place already
+      src = reinterpret_cast<const float4*>(found_vecs + j * dim);
     } else {
       const uint64_t m = j - nf;
       i = missing_idx[m];
@@ -1628,13 +1629,16 @@ int hps_gpu_table_join_prefetch(hps_gpu_table t) {
 int hpsg::table_read_through(hps_gpu_table t, uint32_t table, const uint64_t* keys, const float* found_vecs,
                              const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts,
                              uint64_t n, float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent,
-                             uint8_t* src_out) {
+                             uint8_t* src_out, bool hits_in_place) {
+  // hits_in_place: the hits' rows are already at out[i] (the cache query scattered them there)
   if (t && t->dim != t->dim_io) return refuse_padded(t, "read_through");
   if (int s = check_tbl(t)) return s;
   if (table >= t->n_tables) return HPS_GPU_E_UNKNOWN_TABLE;
   if (n == 0) return HPS_GPU_OK;
-  if (!keys || !found_vecs || !found_idx || !missing_idx || !counts || !out || !miss_keys || !miss_vecs || !miss_absent)
+  if (!keys || (!found_vecs && !hits_in_place) || !found_idx || !missing_idx || !counts || !out || !miss_keys ||
+      !miss_vecs || !miss_absent)
     return HPS_GPU_E_INVALID_ARGUMENT;
+  if (hits_in_place) found_vecs = nullptr;
   const uint32_t nvec = t->dim / 4;
   const int lpr = nvec >= 32 ? 32 : nvec >= 16 ? 16 : nvec >= 8 ? 8 : nvec >= 4 ? 4 : nvec >= 2 ? 2 : 1;
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);

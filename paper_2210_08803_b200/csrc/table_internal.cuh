@@ -54,7 +54,7 @@ int choose_dedup(bool* flat_out);  // backward.cu: persistent k_dedup if one CTA
 // 1 table, 3 default vector; may be NULL)
 int table_read_through(hps_gpu_table_s* t, uint32_t table, const uint64_t* keys, const float* found_vecs,
                        const uint32_t* found_idx, const uint32_t* missing_idx, const uint64_t* counts, uint64_t n,
-                       float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent, uint8_t* src_out);
+                       float* out, uint64_t* miss_keys, float* miss_vecs, uint8_t* miss_absent, uint8_t* src_out, bool hits_in_place = false);
 cudaError_t trace_attach_table(TraceRec* p);  // table.cu's copy of the trace pointer
 }
 
