@@ -68,6 +68,10 @@ struct hps_gpu_cache_s {
   uint32_t* ws_ticket = nullptr;   // counting grouping: arrival rank of each access in its set
   bool count_group = false;        // distinct-key queries group by set with counters (no radix sort)
   bool query_distinct = false;     // the next cache_query's keys are distinct (the read-through sets it)
+  // pre-zeroed scan regions (the read-through zeroes kScanRegions look-back regions with ONE
+  // memset and each scan of the call takes the next one: no memset node per scan)
+  uint64_t* ws_scan_multi = nullptr;
+  int scan_slot = -1;              // >= 0: the next scan's region; -1: memset per scan
   uint64_t* ws_dcounts = nullptr;  // [0] entries of the derived list [1] its set segments
   bool no_small_sort = false;  // HPS_GPU_NO_SMALL_SORT=1: small batches take the multi-kernel sort too (tests)
 };
@@ -75,6 +79,7 @@ struct hps_gpu_cache_s {
 namespace {
 
 constexpr uint8_t kMiss = 0xff;
+constexpr int kScanRegions = 8;
 
 enum { kClock = 0, kSnap = 1, kStats = 2, kScratch = 9 };
 enum { sQueries = 0, sHits, sMisses, sInsertions, sRejected, sRefresh, sEvictions };
@@ -919,6 +924,18 @@ __global__ void __launch_bounds__(kSmallSortThreads) k_small_sort_segment(const 
   }
 }
 
+// One device-wide scan of the cache: its own pre-zeroed region when the caller armed them
+// (cache_arm_scans), else the shared region with a memset first.
+template <class Op>
+cudaError_t cache_scan(hps_gpu_cache c, const Op& op, uint64_t n_max) {
+  cudaStream_t st = c->ctx->stream;
+  const uint64_t tiles = scan_tiles(n_max);
+  if (c->scan_slot < 0 || c->scan_slot >= kScanRegions || tiles <= 1) return launch_scan(op, n_max, c->ws_scan, st);
+  uint64_t* status = c->ws_scan_multi + uint64_t(c->scan_slot++) * (scan_tiles(c->max_batch) + 2);
+  k_scan<Op><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(op, status, reinterpret_cast<uint32_t*>(status + tiles));
+  return cudaGetLastError();
+}
+
 // ---- counting grouping (large caches: sets >= 8 x max_batch) -----------------------------
 // The same products as the radix sort — every set's accesses contiguous, in input order —
 // from per-set counters instead of 3 digit passes: an arrival ticket per access, each set's
@@ -995,7 +1012,7 @@ int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** set
     HPSG_CUDA(launch_k(true, k_group_count, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_set),
                        static_cast<const uint64_t*>(c->ws_counts), c->ws_setcnt, c->ws_ticket));
     GroupAllocOp aop{c->ws_set, c->ws_ticket, c->ws_setcnt, c->ws_counts};
-    HPSG_CUDA(launch_scan(aop, n, c->ws_scan, st));
+    HPSG_CUDA(cache_scan(c, aop, n));
     HPSG_CUDA(launch_k(true, k_group_place, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_set),
                        static_cast<const uint32_t*>(c->ws_ticket), static_cast<const uint32_t*>(c->ws_setcnt),
                        static_cast<const uint64_t*>(c->ws_counts), c->ws_keys_b, c->ws_vals_b));
@@ -1004,7 +1021,7 @@ int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** set
     *sets_sorted = c->ws_keys_b;
     *idx_sorted = c->ws_vals_b;
     SetSegOp op{*sets_sorted, c->ws_seg, c->ws_counts};
-    HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
+    HPSG_CUDA(cache_scan(c, op, n));
     HPSG_CHECK_LAUNCH("counting set grouping");
     return HPS_GPU_OK;
   }
@@ -1023,7 +1040,7 @@ int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** set
   *sets_sorted = in_b ? c->ws_keys_b : c->ws_set;
   *idx_sorted = in_b ? c->ws_vals_b : c->ws_vals_a;
   SetSegOp op{*sets_sorted, c->ws_seg, c->ws_counts};
-  HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
+  HPSG_CUDA(cache_scan(c, op, n));
   HPSG_CHECK_LAUNCH("set segments");
   return HPS_GPU_OK;
 }
@@ -1116,6 +1133,7 @@ int hps_gpu_cache_create(hps_gpu_ctx ctx, const hps_cache_config* cfg, hps_gpu_c
   A(dalloc(&c->ws_sort, c->sort_words));
   A(dalloc(&c->ws_scan, scan_tiles(n) + 2));
   A(dalloc(&c->ws_counts, 8));
+  A(dalloc(&c->ws_scan_multi, kScanRegions * (scan_tiles(n) + 2)));
   A(dalloc(&c->ws_der_set, n));
   A(dalloc(&c->ws_der_idx, n));
   A(dalloc(&c->ws_der_pos, n));
@@ -1155,7 +1173,7 @@ int hps_gpu_cache_destroy(hps_gpu_cache c) {
                   c->d_state,   c->ws_set,   c->ws_keys_b, c->ws_vals_a, c->ws_vals_b, c->ws_hit,
                   c->ws_rank,   c->ws_seg,   c->ws_sort,   c->ws_scan, c->ws_counts, c->ws_io,
                   c->ws_der_set, c->ws_der_idx, c->ws_der_pos, c->ws_dcounts, c->ws_qmiss, c->ws_setcnt,
-                  c->ws_ticket};
+                  c->ws_ticket, c->ws_scan_multi};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete c;
@@ -1212,7 +1230,7 @@ int hpsg::cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const u
   launch_k(true, k_probe, grid_for(n, 256, kNumSMs * 16), 256, 0, st, keys, n, c->set_mod, c->ways, c->d_keys, c->d_freq,
                                                           c->ws_set, c->ws_hit, c->d_state, c->ws_counts, d_n);
   SplitOp op{c->ws_hit, found_idx, missing_idx, counts, c->ws_counts, c->d_state + kStats, c->ws_qmiss};
-  HPSG_CUDA(launch_scan(op, n, c->ws_scan, st));
+  HPSG_CUDA(cache_scan(c, op, n));
   HPSG_CHECK_LAUNCH("cache probe/split");
   ph.mark();
   if (found_vecs) {
@@ -1310,7 +1328,7 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
   if (!keys || !vecs) return HPS_GPU_E_INVALID_ARGUMENT;
   if (int s = entry_prep(c, keys, vecs, n, d_n, skip, admitted_out)) return s;  // zeroes *admitted_out
   RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
-  HPSG_CUDA(launch_scan(rop, n, c->ws_scan, st));
+  HPSG_CUDA(cache_scan(c, rop, n));
   const uint32_t* sets_sorted;
   const uint32_t* idx_sorted;
   if (int s = sort_and_segment(c, n, bits_for(c->num_sets), &sets_sorted, &idx_sorted)) return s;
@@ -1333,6 +1351,19 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
 namespace hpsg {
 void cache_mark_distinct_query(hps_gpu_cache c) {
   if (c) c->query_distinct = true;
+}
+// The read-through's scans (query split, grouping, segments, insert rank, derivation,
+// segments) each take a region zeroed here by ONE memset; disarmed at the call's end.
+int cache_arm_scans(hps_gpu_cache c, bool on, uint64_t n_max) {
+  if (!c) return HPS_GPU_E_INVALID_ARGUMENT;
+  if (!on || scan_tiles(n_max) <= 1) {  // (single-tile scans need no zeroed words)
+    c->scan_slot = -1;
+    return HPS_GPU_OK;
+  }
+  HPSG_CUDA(cudaMemsetAsync(c->ws_scan_multi, 0, kScanRegions * (scan_tiles(c->max_batch) + 2) * sizeof(uint64_t),
+                            c->ctx->stream));
+  c->scan_slot = 0;
+  return HPS_GPU_OK;
 }
 // The read-through's migration: insert its distinct misses (entries [0, *d_count) of keys/vecs,
 // skip[] = absent from the lower tier) right after cache_query of the same call, reusing the
@@ -1364,11 +1395,11 @@ int cache_insert_after_query(hps_gpu_cache c, const uint64_t* keys, const float*
     HPSG_CHECK_LAUNCH("cache entry prep (after query)");
   }
   RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
-  HPSG_CUDA(launch_scan(rop, n_max, c->ws_scan, st));
+  HPSG_CUDA(cache_scan(c, rop, n_max));
   DeriveOp dop{c->q_sets, c->q_idx, q_n, c->ws_qmiss, c->ws_hit, c->ws_der_set, c->ws_der_idx, c->ws_dcounts};
-  HPSG_CUDA(launch_scan(dop, q_n_max, c->ws_scan, st));
+  HPSG_CUDA(cache_scan(c, dop, q_n_max));
   SetSegOp sop{c->ws_der_set, c->ws_seg, c->ws_dcounts};
-  HPSG_CUDA(launch_scan(sop, n_max, c->ws_scan, st));
+  HPSG_CUDA(cache_scan(c, sop, n_max));
   HPSG_CHECK_LAUNCH("cache derived set grouping");
   if (c->ways <= 8)
     launch_k(true, (c->f16 ? k_insert_sets8<true> : k_insert_sets8<false>), grid_for((n_max + 3) / 4 * 32, 256, kNumSMs * 16),

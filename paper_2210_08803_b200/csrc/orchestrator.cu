@@ -29,6 +29,7 @@ int cache_query(hps_gpu_cache c, const uint64_t* keys, uint64_t n, const uint64_
 int cache_info(hps_gpu_cache c, hps_gpu_ctx* ctx, uint32_t* dim);
 uint64_t cache_max_batch(hps_gpu_cache c);
 void cache_mark_distinct_query(hps_gpu_cache c);
+int cache_arm_scans(hps_gpu_cache c, bool on, uint64_t n_max);
 int cache_insert_after_query(hps_gpu_cache c, const uint64_t* keys, const float* vecs, uint64_t n_max,
                              const uint64_t* d_count, const uint8_t* skip, uint64_t* admitted_out,
                              const uint64_t* q_n, uint64_t q_n_max);
@@ -400,6 +401,11 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
   if (n_unique_out) HPSG_CUDA(cudaMemcpyAsync(n_unique_out, r->counts, 8, cudaMemcpyDeviceToDevice, st));
   // K6 on the distinct keys (one access per distinct key: SPEC.md:340)
   cache_mark_distinct_query(r->cache);  // its keys are distinct: counting set grouping allowed
+  if (int s = cache_arm_scans(r->cache, true, n)) return s;
+  struct Disarm {  // every exit of this call (errors included) disarms the regions
+    hps_gpu_cache c;
+    ~Disarm() { cache_arm_scans(c, false, 0); }
+  } disarm{r->cache};
   // (the hits' rows go straight to urows[distinct id]: no compacted copy to move again)
   if (int s = cache_query(r->cache, r->ukeys, n, r->counts, r->urows, r->found_idx, r->missing_idx, r->counts + 2,
                           /*scatter_found=*/true))
@@ -423,6 +429,7 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
                                               r->counts + 4, r->counts, n)) {
     return s;
   }
+  cache_arm_scans(r->cache, false, 0);  // (the guard repeats it harmlessly)
   // K14c: rows back in input order
   const int lpr = lpr_for(r->dim);
   const int grid = grid_for(n * lpr, 256, kNumSMs * 16);
