@@ -143,10 +143,14 @@ __global__ void __launch_bounds__(kSmallDedupThreads) k_dedup_small(const uint64
 // keys[owner]).
 __global__ void __launch_bounds__(256) k_dedup_claim(const uint64_t* __restrict__ keys, uint64_t n,
                                                      uint32_t* __restrict__ claim, uint64_t mask,
-                                                     uint32_t* __restrict__ slot_of, uint64_t* source_counts) {
+                                                     uint32_t* __restrict__ slot_of, uint64_t* source_counts,
+                                                     uint64_t* scan_zero, uint32_t scan_words) {
   pdl_wait();
   pdl_launch_dependents();
   if (source_counts && blockIdx.x == 0 && threadIdx.x < 4) source_counts[threadIdx.x] = 0;
+  // the first-occurrence scan's look-back words, zeroed here (it runs next): no memset node
+  if (blockIdx.x == 0)
+    for (uint32_t w = threadIdx.x; w < scan_words; w += blockDim.x) scan_zero[w] = 0;
   // (whole warps iterate together: the match below needs every lane)
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x); i0 < n; i0 += stride) {
@@ -390,10 +394,12 @@ int hps_gpu_readthrough_lookup(hps_gpu_readthrough r, const uint64_t* keys, uint
                        r->inverse, r->counts, source_counts_out));
   } else {
     const uint64_t cap = claim_cap_for(n);
+    const uint64_t tiles = scan_tiles(n);  // (> 1: n > kSmallDedup)
     HPSG_CUDA(launch_k(pdl, k_dedup_claim, grid_for(n, 256, kNumSMs * 8), 256, 0, st, keys, n, r->claim, cap - 1,
-                       r->slot_of, source_counts_out));
+                       r->slot_of, source_counts_out, r->scan, static_cast<uint32_t>(tiles + 1)));
     FirstOp op{keys, r->claim, r->slot_of, n, r->ukeys, r->uid_at, r->counts};
-    HPSG_CUDA(launch_scan(op, n, r->scan, st));
+    k_scan<FirstOp><<<static_cast<unsigned>(tiles), kScanBlock, 0, st>>>(op, r->scan,
+                                                                       reinterpret_cast<uint32_t*>(r->scan + tiles));
     // (the inverse map is resolved by k_expand, the claim table's last reader)
   }
   const bool fused_inverse = n > kSmallDedup;
