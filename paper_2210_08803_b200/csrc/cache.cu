@@ -684,7 +684,12 @@ __global__ void __launch_bounds__(256) k_insert_sets8(const uint32_t* __restrict
                                                      const uint32_t* __restrict__ rank, uint32_t ways, uint32_t dim,
                                                      uint64_t aging_period, uint32_t invalid_set, uint64_t* ckeys,
                                                      uint64_t* cver, uint8_t* cfreq, uint64_t* ctouch, uint64_t* set_acc,
-                                                     void* cvec, uint64_t* state, uint64_t* admitted_out) {
+                                                     void* cvec, uint64_t* state, uint64_t* admitted_out,
+                                                     const uint32_t* __restrict__ entry_of,
+                                                     const uint8_t* __restrict__ entry_valid) {
+  // entry_of != nullptr: the segments are a QUERY's (cache_insert_after_query): access u is
+  // insert entry entry_of[u] (UINT32_MAX: a hit), taken only when entry_valid[] — the query's
+  // set grouping serves the insert directly, no compacted copy of it
   pdl_wait();
   pdl_launch_dependents();
   const uint32_t lane = lane_id(), g = lane >> 3, gl = lane & 7u;
@@ -698,6 +703,14 @@ __global__ void __launch_bounds__(256) k_insert_sets8(const uint32_t* __restrict
     const uint32_t lo = seg_start[u], hi = seg_start[u + 1];
     const uint32_t s32 = sets_sorted[lo];
     if (s32 == invalid_set) continue;
+    if (entry_of) {  // a set none of whose accesses is an insert entry is left alone
+      bool any = false;
+      for (uint32_t j = lo; j < hi && !any; ++j) {
+        const uint32_t m = entry_of[idx_sorted[j]];
+        any = m != 0xffffffffu && entry_valid[m];
+      }
+      if (!any) continue;
+    }
     const uint64_t s = s32, e0 = s * ways;
     const bool way = gl < ways;
     // the set's metadata and its first entry are loaded together
@@ -705,7 +718,12 @@ __global__ void __launch_bounds__(256) k_insert_sets8(const uint32_t* __restrict
     uint32_t f_w = way ? cfreq[e0 + gl] : 0;
     uint64_t acc = set_acc[s];
     for (uint32_t j = lo; j < hi; ++j) {
-      const uint32_t i = idx_sorted[j];
+      uint32_t i = idx_sorted[j];
+      if (entry_of) {
+        const uint32_t m = entry_of[i];
+        if (m == 0xffffffffu || !entry_valid[m]) continue;
+        i = m;
+      }
       const uint64_t k = keys[i], ver = versions ? versions[i] : hps::kBulkLoadVersion;
       const uint64_t t = clock0 + rank[i] + 1;
       if (++acc >= aging_period) {
@@ -1336,7 +1354,8 @@ static int insert_impl(hps_gpu_cache c, const uint64_t* keys, const float* vecs,
     launch_k(true, (c->f16 ? k_insert_sets8<true> : k_insert_sets8<false>), grid_for((n + 3) / 4 * 32, 256, kNumSMs * 16),
              256, 0, st, sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ws_rank, c->ways,
              c->dim, c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch,
-             c->d_set_acc, c->d_vec, c->d_state, admitted_out);
+             c->d_set_acc, c->d_vec, c->d_state, admitted_out, static_cast<const uint32_t*>(nullptr),
+             static_cast<const uint8_t*>(nullptr));
   else
   launch_k(true, (c->f16 ? k_insert_sets<true> : k_insert_sets<false>), set_warps_grid(n), 256, 0, st, 
       sets_sorted, idx_sorted, c->ws_seg, c->ws_counts, keys, vecs, versions, c->ws_rank, c->ways, c->dim,
@@ -1396,6 +1415,17 @@ int cache_insert_after_query(hps_gpu_cache c, const uint64_t* keys, const float*
   }
   RankOp rop{c->ws_hit, c->ws_rank, c->ws_counts, c->d_state};
   HPSG_CUDA(cache_scan(c, rop, n_max));
+  if (c->ways <= 8) {  // the query's own segments, entries mapped inside the insert kernel
+    launch_k(true, (c->f16 ? k_insert_sets8<true> : k_insert_sets8<false>),
+             grid_for((q_n_max + 3) / 4 * 32, 256, kNumSMs * 16), 256, 0, st, c->q_sets, c->q_idx,
+             static_cast<const uint32_t*>(c->ws_seg), static_cast<const uint64_t*>(c->ws_counts), keys, vecs,
+             static_cast<const uint64_t*>(nullptr), static_cast<const uint32_t*>(c->ws_rank), c->ways, c->dim,
+             c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch,
+             c->d_set_acc, c->d_vec, c->d_state, admitted_out, static_cast<const uint32_t*>(c->ws_qmiss),
+             static_cast<const uint8_t*>(c->ws_hit));
+    HPSG_CHECK_LAUNCH("cache insert (query segments)");
+    return HPS_GPU_OK;
+  }
   DeriveOp dop{c->q_sets, c->q_idx, q_n, c->ws_qmiss, c->ws_hit, c->ws_der_set, c->ws_der_idx, c->ws_dcounts};
   HPSG_CUDA(cache_scan(c, dop, q_n_max));
   SetSegOp sop{c->ws_der_set, c->ws_seg, c->ws_dcounts};
@@ -1407,7 +1437,8 @@ int cache_insert_after_query(hps_gpu_cache c, const uint64_t* keys, const float*
              static_cast<const uint32_t*>(c->ws_seg), static_cast<const uint64_t*>(c->ws_dcounts), keys, vecs,
              static_cast<const uint64_t*>(nullptr), static_cast<const uint32_t*>(c->ws_rank), c->ways, c->dim,
              c->aging_period, static_cast<uint32_t>(c->num_sets), c->d_keys, c->d_ver, c->d_freq, c->d_touch,
-             c->d_set_acc, c->d_vec, c->d_state, admitted_out);
+             c->d_set_acc, c->d_vec, c->d_state, admitted_out, static_cast<const uint32_t*>(nullptr),
+             static_cast<const uint8_t*>(nullptr));
   else
     launch_k(true, (c->f16 ? k_insert_sets<true> : k_insert_sets<false>), set_warps_grid(n_max), 256, 0, st,
              static_cast<const uint32_t*>(c->ws_der_set), static_cast<const uint32_t*>(c->ws_der_idx),
