@@ -261,17 +261,26 @@ __global__ void __launch_bounds__(256) k_expand(const float* __restrict__ urows,
       }
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (ok[r] && gl < nvec) reinterpret_cast<float4*>(out + dst[r] * dim)[gl] = x[r];
+        if (ok[r] && gl < nvec) __stcs(reinterpret_cast<float4*>(out + dst[r] * dim) + gl, x[r]);  // streamed out
     }
   }
-  if (source_counts) {
+  if (source_counts) {  // per-CTA sums first: one global atomic per counter per CTA
+    __shared__ unsigned long long s_c[3];
+    if (threadIdx.x < 3) s_c[threadIdx.x] = 0ull;
+    __syncthreads();
     c0 = warp_sum(c0);
     c1 = warp_sum(c1);
     c3 = warp_sum(c3);
     if (lane == 0) {
-      if (c0) atomicAdd(&source_counts[0], static_cast<unsigned long long>(c0));
-      if (c1) atomicAdd(&source_counts[1], static_cast<unsigned long long>(c1));
-      if (c3) atomicAdd(&source_counts[3], static_cast<unsigned long long>(c3));
+      if (c0) atomicAdd(&s_c[0], static_cast<unsigned long long>(c0));
+      if (c1) atomicAdd(&s_c[1], static_cast<unsigned long long>(c1));
+      if (c3) atomicAdd(&s_c[2], static_cast<unsigned long long>(c3));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (s_c[0]) atomicAdd(&source_counts[0], s_c[0]);
+      if (s_c[1]) atomicAdd(&source_counts[1], s_c[1]);
+      if (s_c[2]) atomicAdd(&source_counts[3], s_c[2]);
     }
   }
 }
