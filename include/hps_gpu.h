@@ -379,7 +379,12 @@ int hps_gpu_dist_unique_rows(hps_gpu_dist dist, uint64_t* served_host);
 /* Loopback transport (tests, single-GPU bring-up): n ranks of ONE process on one device,
  * the all-to-alls done as device copies between their buffers. Rank r's calls must run on
  * their own host thread (every all-to-all is a rendezvous of the n ranks); ctxs[r] should
- * have distinct streams. Same kernels, regions and ordering as the NCCL path. */
+ * have distinct streams. Same kernels, regions and ordering as the NCCL path. With the peer
+ * transport the ranks' wait kernels spin on each other on the SAME device: a rank's host
+ * thread must not call a device-synchronising API (cudaMalloc/cudaFree, a synchronous
+ * memcpy, cudaDeviceSynchronize) between its forward/backward calls of one step, or it can
+ * block before enqueuing the signal a peer spins on (the bounded wait then reports
+ * HPS_GPU_E_PEER_TIMEOUT). Separate GPUs (one rank per device) are not affected. */
 int hps_gpu_dist_create_loopback(const hps_gpu_ctx* ctxs, const hps_gpu_table* shards, const hps_dist_config* cfg_host,
                                  uint32_t n, hps_gpu_dist* outs_host);
 

@@ -138,9 +138,16 @@ def run_world(world, multi, optimizer, steps=3, insert=False, transport="nccl"):
             loc.append((k, o, d))
         torch.cuda.synchronize()
 
+        # outputs allocated here, not inside the rank threads: loopback ranks share one device,
+        # and an allocation that synchronises the device while a peer's wait kernel spins on
+        # this rank's (not yet enqueued) signal would deadlock the peer transport
+        outs_pre = [torch.empty(B * S, dim, dtype=torch.float32, device="cuda") for _ in range(world)]
+        torch.cuda.synchronize()
+
         def fwd(r):
             k, o, _ = loc[r]
-            outs_l[r] = dists[r].forward(k, B, offsets=o, combiner=comb, train=True, insert_missing=insert)
+            outs_l[r] = dists[r].forward(k, B, offsets=o, combiner=comb, train=True, insert_missing=insert,
+                                         out=outs_pre[r])
 
         served0 = [d.unique_rows_served() for d in dists] if transport == "peer" else None
         on_ranks(fwd)
