@@ -1,7 +1,8 @@
 """bench_cache.py — BASELINE config 4: HPS inference cache batch sweep on one B200.
 
-100M-key dim-128 fp32 backing table resident in HBM (51.2 GB; the VDB/PDB tiers are out of
-scope, so the "lower tier" is a GPU table), a GPU cache at 10 % capacity (10M rows, 8 ways,
+100M-key dim-128 fp32 backing table resident in HBM (51.2 GB; this sweep times the all-GPU
+read-through, so the "lower tier" is a GPU table — the host VDB/PDB miss path is timed by
+scripts/bench_tiered.py), a GPU cache at 10 % capacity (10M rows, 8 ways,
 1.25M sets, aging 10 x capacity), Zipf(1.05) query keys. After a warm-up of >= 10 x
 capacity accesses, each batch size 1, 2, 4, ... 131072 is timed as one orchestrator
 read-through (cache query -> misses read from the table -> misses migrated into the
