@@ -957,31 +957,42 @@ cudaError_t cache_scan(hps_gpu_cache c, const Op& op, uint64_t n_max) {
 // ---- counting grouping (large caches: sets >= 8 x max_batch) -----------------------------
 // The same products as the radix sort — every set's accesses contiguous, in input order —
 // from per-set counters instead of 3 digit passes: an arrival ticket per access, each set's
-// first arrival reserves the set's range (a scan over the accesses), every access lands at
+// first arrival reserves the set's range (one counter), every access lands at
 // range + ticket, and one thread per range puts it back into input order (insertion sort: a
 // range holds ~1 access when the sets outnumber the batch 8:1) and zeroes the counter.
 // Segments come out in the order of their first-arriving access, not by set id: every
 // consumer treats segments independently.
 __global__ void __launch_bounds__(256) k_group_count(const uint32_t* __restrict__ sets, const uint64_t* counts,
-                                                     uint32_t* cnt, uint32_t* __restrict__ ticket) {
+                                                     uint32_t* cnt, uint32_t* __restrict__ ticket,
+                                                     unsigned long long* range_total) {
   pdl_wait();
   pdl_launch_dependents();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *range_total = 0ull;  // k_group_alloc's allocator
   const uint64_t n = counts[0];
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
     ticket[i] = atomicAdd(&cnt[sets[i]], 1u);
 }
-struct GroupAllocOp {
-  const uint32_t* sets;
-  const uint32_t* ticket;
-  uint32_t* cnt;  // count in, the range's start out (its first arrival is its only writer)
-  const uint64_t* counts;
-  __device__ uint64_t size() const { return counts[0]; }
-  __device__ uint32_t count(uint64_t i) const { return ticket[i] == 0 ? cnt[sets[i]] : 0u; }
-  __device__ void emit(uint64_t i, uint64_t excl, uint32_t c) const {
-    if (c) cnt[sets[i]] = static_cast<uint32_t>(excl);
+// Each set's first arrival reserves its range from one counter (warp-aggregated): the ranges
+// come out in allocation order, which no consumer depends on (segments are independent).
+__global__ void __launch_bounds__(256) k_group_alloc(const uint32_t* __restrict__ sets, const uint32_t* __restrict__ ticket,
+                                                     uint32_t* cnt, const uint64_t* counts,
+                                                     unsigned long long* range_total) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint64_t n = counts[0];
+  const uint32_t lane = lane_id();
+  for (uint64_t i0 = blockIdx.x * uint64_t(blockDim.x); i0 < n; i0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool lead = i < n && ticket[i] == 0;
+    const uint32_t s = lead ? sets[i] : 0u;
+    const uint32_t len = lead ? cnt[s] : 0u;
+    const uint32_t incl = warp_incl_scan(len);
+    unsigned long long base = 0;
+    if (lane == 31 && incl) base = atomicAdd(range_total, static_cast<unsigned long long>(incl));
+    base = __shfl_sync(0xffffffffu, base, 31);
+    if (lead) cnt[s] = static_cast<uint32_t>(base + incl - len);
   }
-  __device__ void total(uint64_t) const {}
-};
+}
 __global__ void __launch_bounds__(256) k_group_place(const uint32_t* __restrict__ sets, const uint32_t* __restrict__ ticket,
                                                      const uint32_t* __restrict__ cnt, const uint64_t* counts,
                                                      uint32_t* __restrict__ out_set, uint32_t* __restrict__ out_idx) {
@@ -1027,10 +1038,12 @@ int sort_and_segment(hps_gpu_cache c, uint64_t n, int bits, const uint32_t** set
   // public query/insert/refresh entries) could pile thousands into one range — radix sort there
   if (c->count_group && distinct && n > kSmallSort) {
     const int g = grid_for(n, 256, kNumSMs * 8);
+    auto* range_total = reinterpret_cast<unsigned long long*>(c->ws_counts + 6);
     HPSG_CUDA(launch_k(true, k_group_count, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_set),
-                       static_cast<const uint64_t*>(c->ws_counts), c->ws_setcnt, c->ws_ticket));
-    GroupAllocOp aop{c->ws_set, c->ws_ticket, c->ws_setcnt, c->ws_counts};
-    HPSG_CUDA(cache_scan(c, aop, n));
+                       static_cast<const uint64_t*>(c->ws_counts), c->ws_setcnt, c->ws_ticket, range_total));
+    HPSG_CUDA(launch_k(true, k_group_alloc, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_set),
+                       static_cast<const uint32_t*>(c->ws_ticket), c->ws_setcnt,
+                       static_cast<const uint64_t*>(c->ws_counts), range_total));
     HPSG_CUDA(launch_k(true, k_group_place, g, 256, 0, st, static_cast<const uint32_t*>(c->ws_set),
                        static_cast<const uint32_t*>(c->ws_ticket), static_cast<const uint32_t*>(c->ws_setcnt),
                        static_cast<const uint64_t*>(c->ws_counts), c->ws_keys_b, c->ws_vals_b));
