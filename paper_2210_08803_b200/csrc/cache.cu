@@ -179,12 +179,38 @@ __global__ void __launch_bounds__(256) k_gather(const uint32_t* __restrict__ fou
   const uint32_t nvec = dim / 4;
   const uint64_t gid = ((blockIdx.x * uint64_t(blockDim.x) + threadIdx.x) >> 5) * G + grp;
   const uint64_t ng = ((uint64_t(gridDim.x) * blockDim.x) >> 5) * G;
-  for (uint64_t j = gid; j < nf; j += ng) {
-    const uint32_t i = found_idx[j];
-    const uint64_t e = uint64_t(set_of[i]) * ways + hit[i];
+  // R rows per group in flight: their positions, then their entries, then their rows are
+  // loaded together (a lane group otherwise walks ~2 rows one dependent chain at a time)
+  constexpr int R = 4;
+  for (uint64_t j0 = gid; j0 < nf; j0 += ng * R) {
+    uint32_t i[R];
+    uint64_t e[R];
+    bool ok[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      ok[r] = j0 + uint64_t(r) * ng < nf;
+      i[r] = ok[r] ? found_idx[j0 + uint64_t(r) * ng] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) e[r] = ok[r] ? uint64_t(set_of[i[r]]) * ways + hit[i[r]] : 0ull;
     // scatter: the row lands at its access position (out[i]) instead of compacted (out[j])
-    float4* dst = reinterpret_cast<float4*>(out + uint64_t(scatter ? i : static_cast<uint32_t>(j)) * dim);
-    for (uint32_t v = gl; v < nvec; v += LPR) dst[v] = load_cached4<F16>(vec, e, dim, v);
+    if (nvec <= LPR) {
+      float4 x[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        x[r] = (ok[r] && gl < nvec) ? load_cached4<F16>(vec, e[r], dim, gl) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (ok[r] && gl < nvec)
+          reinterpret_cast<float4*>(out + (scatter ? uint64_t(i[r]) : j0 + uint64_t(r) * ng) * dim)[gl] = x[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!ok[r]) continue;
+        float4* dst = reinterpret_cast<float4*>(out + (scatter ? uint64_t(i[r]) : j0 + uint64_t(r) * ng) * dim);
+        for (uint32_t v = gl; v < nvec; v += LPR) dst[v] = load_cached4<F16>(vec, e[r], dim, v);
+      }
+    }
   }
 }
 
