@@ -579,7 +579,9 @@ uint32_t hps_crc32c_host(uint32_t crc, const void* data, size_t len);
  * (device) in input order; source_counts_host[4] = per input key {L1, L2, L3, Default}.
  * Migrations are started and NOT waited for: keys found in L2 are inserted into L1 (at their
  * VDB version), keys found only in L3 into L2 and L1 (at their PDB version); absent keys are
- * inserted nowhere. hps_gpu_tiered_await(t) = the last lookup's migrations are visible. */
+ * inserted nowhere. hps_gpu_tiered_await(t) = the last lookup's migrations are visible.
+ * One lookup at a time per hps_gpu_tiered (its staging buffers are reused); the VDB and PDB
+ * themselves may be shared by several (their shards/tables lock). */
 typedef struct hps_gpu_tiered_s* hps_gpu_tiered;
 int hps_gpu_tiered_create(hps_gpu_cache l1, hps_vdb l2, hps_pdb l3, const char* table, uint64_t max_batch,
                           hps_gpu_tiered* out_host);
